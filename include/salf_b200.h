@@ -1,0 +1,199 @@
+/*
+ * salf_b200.h -- C ABI of the B200-native SaLF render path (libsalf_b200.so).
+ *
+ * Every entry point replaces one function of the reference's Python render
+ * API (paths relative to /root/reference/pkg/src/salf); the Python mirror in
+ * paper_2507_18713_b200/ binds them through ctypes.
+ *
+ * Conventions
+ *   - all array arguments are caller-owned DEVICE pointers (one device per
+ *     call, the current CUDA device); no hidden allocation: scratch comes from
+ *     a caller-provided workspace sized by the matching *_workspace_bytes();
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *     calls are stream-ordered and re-entrant across streams;
+ *   - return 0 on success or a SALF_E* code; salf_last_error() returns a
+ *     thread-local message.  EINVAL maps to the reference's ValueError with
+ *     the same text, ENOTERM to its RuntimeError (octree.py:251-252).
+ */
+#ifndef SALF_B200_H
+#define SALF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALF_OK 0
+#define SALF_EINVAL 1     /* contract violation -> ValueError            */
+#define SALF_ENOTERM 2    /* marcher did not terminate -> RuntimeError   */
+#define SALF_ECUDA 3      /* CUDA runtime error -> RuntimeError          */
+#define SALF_EWORKSPACE 4 /* workspace too small; see *_workspace_bytes  */
+
+#define SALF_PINHOLE 0
+#define SALF_FISHEYE 1
+#define SALF_EQUIRECT 2
+
+#define SALF_DENSITY_SDF 0
+#define SALF_DENSITY_RAW 1
+
+#define SALF_PRM_STRIDE 28 /* floats per voxel: w_s[4] w_c[9] w_sh[12] pad[3] */
+#define SALF_SAVED_STRIDE 8 /* doubles per pixel/ray kept for the backward     */
+
+/* Device view of a flat voxel list (reference render_raster.py:44-60,
+ * scene.py:82-223).  geo = (cx, cy, cz, edge) f64 with centres computed as
+ * aabb_min + (ijk + 0.5) * edge; ab = (exp(log_a), exp(log_b)) f64;
+ * prm = f32 fields (exact for salf.v1 scenes, whose params are f32 on disk). */
+typedef struct {
+  int64_t n;
+  const double *geo;
+  const double *ab;
+  const float *prm;
+  int32_t density_mode;
+  int32_t pad;
+} salf_scene_t;
+
+/* CameraModel (reference sensors.py:45-74); rot = quat_to_matrix(q), row-major. */
+typedef struct {
+  int32_t kind, width, height, pad;
+  double fx, fy, cx, cy;
+  double k[4];
+  double position[3];
+  double rot[9];
+  double readout_duration;
+  double linear_velocity[3];
+  double angular_velocity[3];
+  double t0;
+} salf_camera_t;
+
+/* LidarModel (reference sensors.py:77-98); beam elevations are a device array. */
+typedef struct {
+  int32_t n_beams, steps;
+  double azimuth_start, azimuth_end, scan_period;
+  double position[3];
+  double rot[9];
+  double linear_velocity[3];
+  double angular_velocity[3];
+  double t0;
+} salf_lidar_t;
+
+/* Linear octree (reference octree.py:34-44): node word = id_or_offset with
+ * the leaf flag folded in: word >= 0 -> internal node, children at word;
+ * word == -1 -> empty; word <= -2 -> leaf of voxel (-word - 2). */
+typedef struct {
+  int64_t n_nodes;
+  const int32_t *nodes;
+  double root_min[3];
+  double root_edge;
+  int32_t max_depth;
+  int32_t pad;
+} salf_octree_t;
+
+typedef struct {
+  double background[3];
+  double near;           /* NEAR_PLANE 0.05 (render_raster.py:30)      */
+  double stop_threshold; /* STOP_THRESHOLD 0.99 (render_ray.py:31)    */
+  int32_t tile;          /* TILE_SIZE 16 (render_raster.py:29)         */
+  int32_t exact_color;   /* 1: color in fp64 (parity mode); 0: fp32    */
+} salf_raster_opts_t;
+
+const char *salf_last_error(void);
+int salf_device_sm_count(void);
+
+/* ---- rasterizer (reference render_raster.py) ------------------------- */
+
+/* project_voxels (render_raster.py:97-129) + the per-voxel half of
+ * cull_and_bin (:143-176): rect (M x 4: umin, vmin, umax, vmax; NaN if
+ * culled), z_center, culled, the reference tile span `span_ref` and the
+ * tightened render span `span_fit` (M x 4 int32: tx0, ty0, tx1, ty1; empty
+ * when tx0 > tx1), and 64-bit orderable depth keys. */
+int salf_project_voxels(const salf_scene_t *scene, const salf_camera_t *cam, double near,
+                        int32_t tile, double *rect, double *z_center, uint8_t *culled,
+                        int32_t *span_ref, int32_t *span_fit, uint64_t *zkey, void *stream);
+
+/* Workspace for salf_raster_bin given M voxels and an instance capacity. */
+size_t salf_raster_bin_workspace_bytes(int64_t n_voxels, int64_t capacity, int32_t n_tiles);
+
+/* cull_and_bin (render_raster.py:143-182): CSR of depth-sorted per-tile voxel
+ * lists.  mode 0 = reference lists (straddlers in every tile; bit-exact
+ * export), mode 1 = render lists (tightened spans; per-tile subsequence of
+ * mode 0 that drops only voxels no pixel of the tile can hit).
+ * Writes offsets[n_tiles + 1] (int64) and entries[capacity] (int32) and the
+ * instance count to *n_instances (host).  Returns SALF_EWORKSPACE with
+ * *n_instances = required capacity when capacity is too small. */
+int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double near,
+                    int32_t tile, int32_t mode, const uint64_t *zkey, const int32_t *span,
+                    const uint8_t *visible_hint, void *workspace, size_t workspace_bytes,
+                    int64_t capacity, int64_t *offsets, int32_t *entries,
+                    int64_t *n_instances, void *stream);
+
+/* rasterize (render_raster.py:201-301) over prebuilt render bins.
+ * out_rgb (H*W*3), out_opacity, out_depth f32; saved (H*W*8 f64, nullable):
+ * acc_rgb[3], acc_w, acc_wt, log_t_final, n_used, pad -- kept for the backward. */
+int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
+                          const salf_raster_opts_t *opts, const int64_t *offsets,
+                          const int32_t *entries, float *out_rgb, float *out_opacity,
+                          float *out_depth, double *saved, void *stream);
+
+/* Raster backward (no reference function: defined as backward_records,
+ * backward.py:35-101, applied to the raster pairs -- see DESIGN.md).
+ * d_rgb (H*W*3) and d_depth (H*W) f64; grad (M x 27 f64, accumulated). */
+int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
+                         const salf_raster_opts_t *opts, const int64_t *offsets,
+                         const int32_t *entries, const double *saved, const double *d_rgb,
+                         const double *d_depth, double *grad, void *stream);
+
+/* ---- sensors (reference sensors.py) ----------------------------------- */
+
+/* gen_camera_rays + apply_rolling_shutter (sensors.py:129-190):
+ * origins/dirs (N x 3 f64), t_stamps (N f64), valid (N u8), N = W*H. */
+int salf_camera_rays(const salf_camera_t *cam, double *origins, double *dirs,
+                     double *t_stamps, uint8_t *valid, void *stream);
+
+/* gen_lidar_rays (sensors.py:193-232), beam-major. */
+int salf_lidar_rays(const salf_lidar_t *lidar, const double *beam_elevations, double *origins,
+                    double *dirs, double *t_stamps, void *stream);
+
+/* ---- octree (reference octree.py) -------------------------------------- */
+
+/* build_octree (octree.py:54-125) on the host: level (u8), ijk (int32 x3)
+ * host arrays.  Node layout identical to the reference DFS.  Call with
+ * nodes == NULL to get the node count in *n_nodes first. */
+int salf_octree_build_host(int64_t n, const uint8_t *level, const int32_t *ijk,
+                           int32_t root_depth, int32_t *nodes, int64_t capacity,
+                           int64_t *n_nodes, int32_t *max_depth);
+
+/* query_batch (octree.py:136-166): flag (i8), vid (i64), corner (x3), edge. */
+int salf_octree_query(const salf_octree_t *tree, int64_t n, const double *p, int8_t *flag,
+                      int64_t *vid, double *corner, double *edge, int32_t *out_of_root,
+                      void *stream);
+
+/* march_batch (octree.py:276-295): per-ray segment counts, then the hit
+ * list in per-ray march order.  counts[n]; if seg_vid != NULL the caller
+ * passes starts (exclusive scan of counts) and the segments are written. */
+int salf_march(const salf_octree_t *tree, int64_t n, const double *origins, const double *dirs,
+               const double *t_max, const salf_scene_t *scene, double stop_threshold,
+               int32_t early_stop, int64_t *counts, const int64_t *starts, int64_t *seg_vid,
+               double *seg_t0, double *seg_t1, int32_t *status, void *stream);
+
+/* integrate_rays (render_ray.py:161-239) for a static scene, fused march +
+ * shade + composite: out_rgb (N x 3), out_opacity, out_depth (f32);
+ * saved (N x 8 f64, nullable) as for the rasterizer; status (N int32):
+ * 0 ok, 1 round cap hit (the reference would raise RuntimeError). */
+int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                     const double *origins, const double *dirs, const uint8_t *valid,
+                     const salf_raster_opts_t *opts, float *out_rgb, float *out_opacity,
+                     float *out_depth, double *saved, int32_t *status, void *stream);
+
+/* backward_records (backward.py:35-101) for the ray path, re-marching each
+ * ray: d_rgb (N x 3), d_depth (N) f64; grad (M x 27 f64, accumulated). */
+int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                      const double *origins, const double *dirs, const uint8_t *valid,
+                      const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,
+                      const double *d_depth, double *grad, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALF_B200_H */

@@ -1,0 +1,131 @@
+"""ctypes binding of libsalf_b200.so (C ABI declared in include/salf_b200.h).
+
+The shared library is built in-tree by `__graft_entry__.build()` (or
+`make -C paper_2507_18713_b200/csrc`).  There is no CPU fallback: if the
+library or a CUDA device is missing, every render call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+import torch
+
+LIB_PATH = Path(__file__).resolve().parent / "libsalf_b200.so"
+
+SALF_OK, SALF_EINVAL, SALF_ENOTERM, SALF_ECUDA, SALF_EWORKSPACE = 0, 1, 2, 3, 4
+KINDS = {"pinhole": 0, "fisheye_equidistant": 1, "equirect": 2}
+DENSITY = {"sdf": 0, "raw": 1}
+PRM_STRIDE = 28
+SAVED_STRIDE = 8
+GRAD_STRIDE = 27
+
+c_double3 = C.c_double * 3
+c_double9 = C.c_double * 9
+c_double4 = C.c_double * 4
+vp = C.c_void_p
+
+
+class SceneT(C.Structure):
+    _fields_ = [("n", C.c_int64), ("geo", vp), ("ab", vp), ("prm", vp),
+                ("density_mode", C.c_int32), ("pad", C.c_int32)]
+
+
+class CameraT(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("width", C.c_int32), ("height", C.c_int32),
+                ("pad", C.c_int32), ("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double),
+                ("cy", C.c_double), ("k", c_double4), ("position", c_double3), ("rot", c_double9),
+                ("readout_duration", C.c_double), ("linear_velocity", c_double3),
+                ("angular_velocity", c_double3), ("t0", C.c_double)]
+
+
+class LidarT(C.Structure):
+    _fields_ = [("n_beams", C.c_int32), ("steps", C.c_int32), ("azimuth_start", C.c_double),
+                ("azimuth_end", C.c_double), ("scan_period", C.c_double),
+                ("position", c_double3), ("rot", c_double9), ("linear_velocity", c_double3),
+                ("angular_velocity", c_double3), ("t0", C.c_double)]
+
+
+class OctreeT(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("nodes", vp), ("root_min", c_double3),
+                ("root_edge", C.c_double), ("max_depth", C.c_int32), ("pad", C.c_int32)]
+
+
+class RasterOptsT(C.Structure):
+    _fields_ = [("background", c_double3), ("near", C.c_double), ("stop_threshold", C.c_double),
+                ("tile", C.c_int32), ("exact_color", C.c_int32)]
+
+
+# name -> (restype, argtypes); every symbol declared in include/salf_b200.h
+SIGNATURES = {
+    "salf_last_error": (C.c_char_p, []),
+    "salf_device_sm_count": (C.c_int, []),
+    "salf_project_voxels": (C.c_int, [vp, vp, C.c_double, C.c_int32, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_bin_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int64, C.c_int32]),
+    "salf_raster_bin": (C.c_int, [vp, vp, C.c_double, C.c_int32, C.c_int32, vp, vp, vp, vp,
+                                  C.c_size_t, C.c_int64, vp, vp, vp, vp]),
+    "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_camera_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "salf_lidar_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "salf_octree_build_host": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int64, vp, vp]),
+    "salf_octree_query": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_march": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_int32, vp, vp, vp,
+                             vp, vp, vp, vp]),
+    "salf_ray_forward": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_ray_backward": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+}
+
+_lib = None
+
+
+def load(require_cuda: bool = True):
+    """Load the shared library (fails loudly; no fallback)."""
+    global _lib
+    if require_cuda and not torch.cuda.is_available():
+        raise RuntimeError("paper_2507_18713_b200 needs a CUDA device (sm_100a); none is visible")
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(make -C paper_2507_18713_b200/csrc) first")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def check(rc: int, where: str = "") -> None:
+    if rc == SALF_OK:
+        return
+    msg = load(require_cuda=False).salf_last_error().decode("utf-8", "replace")
+    if rc == SALF_EINVAL:
+        raise ValueError(msg)
+    if rc == SALF_ENOTERM:
+        raise RuntimeError(msg)
+    raise RuntimeError(f"{where}: {msg}" if where else msg)
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ref(struct):
+    return C.byref(struct)
+
+
+def as_f64(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.float64).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float64)), device=device)

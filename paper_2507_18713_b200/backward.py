@@ -1,0 +1,73 @@
+"""Reverse mode through volume rendering -- drop-in for reference backward.py.
+
+`backward_records(records, scene, d_color, d_depth)` (backward.py:35-101)
+returns {'static': {param: grad}} like the reference.  For the ray path the
+kernel re-marches each ray (no per-segment records are kept) and scatters
+per-voxel gradients with warp-aggregated fp64 atomics into a dense
+(M, 27) buffer.  Raster frames use `render_raster.rasterize_backward`.
+Loss seeds (losses.py:22-46) are provided on the device.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from .device import grads_to_dict
+from .render_ray import RenderRecords
+
+PARAM_NAMES = ("w_s", "w_c", "w_sh", "log_a", "log_b")
+
+
+def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
+                         grad: torch.Tensor | None = None) -> torch.Tensor:
+    """Accumulate into / return the raw (M, 27) f64 gradient buffer."""
+    lib = _lib.load()
+    ds = records.scene
+    dev = ds.device
+    n = records.n_rays
+    dc = _lib.as_f64(d_color, dev).reshape(n * 3)
+    dd = _lib.as_f64(d_depth, dev).reshape(n)
+    if grad is None:
+        grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    if n:
+        sc, t = ds.c_struct(), records.octree.c_struct()
+        _lib.check(lib.salf_ray_backward(_lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(),
+                                         records.dirs.data_ptr(), _lib.ptr(records.valid),
+                                         _lib.ref(records.opts), records.saved.data_ptr(),
+                                         dc.data_ptr(), dd.data_ptr(), grad.data_ptr(),
+                                         _lib.stream_ptr()), "backward_records")
+    return grad
+
+
+def backward_records(records: RenderRecords, scene, d_color, d_depth) -> dict:
+    """Parameter gradients per owner (backward.py:35-101); static scenes only."""
+    grad = backward_grad_buffer(records, d_color, d_depth)
+    return {"static": grads_to_dict(grad[: records.scene.n])}
+
+
+def loss_color_seed(out_color: torch.Tensor, gt: torch.Tensor, mask: torch.Tensor) -> torch.Tensor:
+    """losses.py:22-31: dL/dC = sign(C - gt) / (n_selected * 3)."""
+    d = torch.zeros(out_color.shape, dtype=torch.float64, device=out_color.device)
+    idx = torch.nonzero(mask, as_tuple=True)[0]
+    if idx.numel():
+        diff = out_color[idx].double() - gt.double()
+        d[idx] = torch.sign(diff) / diff.numel()
+    return d
+
+
+def loss_depth_seed(depth: torch.Tensor, gt: torch.Tensor, mask: torch.Tensor,
+                    count: int | None = None) -> torch.Tensor:
+    """losses.py:34-46: dL/dD = sign(D - gt) / #valid (count overrides #valid, e.g. a
+    global count all-reduced across ranks)."""
+    d = torch.zeros(depth.shape[0], dtype=torch.float64, device=depth.device)
+    idx = torch.nonzero(mask, as_tuple=True)[0]
+    if idx.numel() == 0:
+        return d
+    dep = depth[idx].double()
+    g = gt.double()
+    ok = torch.isfinite(dep) & torch.isfinite(g)
+    idx = idx[ok]
+    if idx.numel():
+        d[idx] = torch.sign(dep[ok] - g[ok]) / (count if count else idx.numel())
+    return d

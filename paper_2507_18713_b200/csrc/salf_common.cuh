@@ -1,0 +1,206 @@
+// salf_common.cuh -- shared device math for the SaLF render kernels (sm_100a).
+//
+// All fp64 expressions are written in the reference's NumPy evaluation order
+// and this translation unit is compiled with --fmad=false, so a product
+// followed by a sum never contracts into an FMA unless written as fma().
+// Where NumPy itself uses FMA (matmul of (N,3)@(3,3) on x86 OpenBLAS) the
+// kernels call fma() in the same chain order; where einsum uses its
+// pairwise SIMD order ((p0 + p2) + p1 for length-3 contiguous dots,
+// (p0 + p2) + (p1 + p3) for length 4) so do we.  Exactness of the integer
+// outputs (tile CSR, hit lists) depends on this; float outputs agree with
+// the reference to ~1e-12 (transcendentals differ by <= 1-2 ulp).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+#include "../../include/salf_b200.h"
+
+namespace salf {
+
+constexpr double kAlphaMax = 1.0 - 1e-12;           // scene.py:32
+constexpr double kShC0 = 0.2820947918;              // scene.py:28
+constexpr double kShC1 = 0.4886025119;              // scene.py:29
+constexpr double kEpsAdvance = 1e-4;                 // octree.py:29
+constexpr int kMaxRounds = 200000;                   // octree.py:31
+constexpr double kDepthWeightMin = 0.5;              // render_ray.py:32
+constexpr int kGradStride = 27;                      // w_s 4, w_c 9, w_sh 12, log_a, log_b
+
+// NumPy np.maximum / np.minimum: NaN in either argument propagates.
+__device__ __forceinline__ double npmax(double a, double b) { return (a != a || a > b) ? a : b; }
+__device__ __forceinline__ double npmin(double a, double b) { return (a != a || a < b) ? a : b; }
+__device__ __forceinline__ double npsign(double s) {
+  return s > 0.0 ? 1.0 : (s < 0.0 ? -1.0 : (s == 0.0 ? 0.0 : s));
+}
+
+// ray_box_range (octree.py:175-194) for one ray against one box, NumPy
+// semantics including the zero-direction override.  Returns t_in, t_out.
+__device__ __forceinline__ void ray_box(const double o[3], const double d[3], const double bmin[3],
+                                        const double bmax[3], double &t_in, double &t_out) {
+  double ti = -INFINITY, to = INFINITY;
+  bool first = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double nk, fk;
+    if (d[k] == 0.0) {
+      bool inside = (o[k] >= bmin[k]) && (o[k] <= bmax[k]);
+      nk = inside ? -INFINITY : INFINITY;
+      fk = inside ? INFINITY : -INFINITY;
+    } else {
+      double inv = 1.0 / d[k];
+      double ta = __dmul_rn(__dsub_rn(bmin[k], o[k]), inv);
+      double tb = __dmul_rn(__dsub_rn(bmax[k], o[k]), inv);
+      nk = npmin(ta, tb);
+      fk = npmax(ta, tb);
+    }
+    if (first) { ti = nk; to = fk; first = false; }
+    else { ti = npmax(ti, nk); to = npmin(to, fk); }
+  }
+  t_in = ti;
+  t_out = to;
+}
+
+// 32-byte read-only load of a double4 (two 16-byte LDG.E.128.CONSTANT).
+__device__ __forceinline__ double4 ldg_d4(const double *p) {
+  const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// Field parameters of one voxel, fp32 as stored (SALF_PRM_STRIDE floats).
+struct VoxPrm {
+  float ws[4];
+  float wc[9];
+  float wsh[12];
+};
+
+__device__ __forceinline__ void load_prm(const float *__restrict__ prm, int64_t v, VoxPrm &p) {
+  const float4 *q = reinterpret_cast<const float4 *>(prm + v * SALF_PRM_STRIDE);
+  float4 a = __ldg(q + 0), b = __ldg(q + 1), c = __ldg(q + 2), e = __ldg(q + 3), f = __ldg(q + 4),
+         g = __ldg(q + 5), h = __ldg(q + 6);
+  p.ws[0] = a.x; p.ws[1] = a.y; p.ws[2] = a.z; p.ws[3] = a.w;
+  p.wc[0] = b.x; p.wc[1] = b.y; p.wc[2] = b.z; p.wc[3] = b.w;
+  p.wc[4] = c.x; p.wc[5] = c.y; p.wc[6] = c.z; p.wc[7] = c.w;
+  p.wc[8] = e.x; p.wsh[0] = e.y; p.wsh[1] = e.z; p.wsh[2] = e.w;
+  p.wsh[3] = f.x; p.wsh[4] = f.y; p.wsh[5] = f.z; p.wsh[6] = f.w;
+  p.wsh[7] = g.x; p.wsh[8] = g.y; p.wsh[9] = g.z; p.wsh[10] = g.w;
+  p.wsh[11] = h.x;
+}
+
+// eval_sdf (scene.py:229-232): einsum dot in (p0 + p2) + p1 order, + bias.
+__device__ __forceinline__ double eval_sdf(const VoxPrm &p, const double x[3]) {
+  double p0 = __dmul_rn((double)p.ws[0], x[0]);
+  double p1 = __dmul_rn((double)p.ws[1], x[1]);
+  double p2 = __dmul_rn((double)p.ws[2], x[2]);
+  return __dadd_rn(__dadd_rn(__dadd_rn(p0, p2), p1), (double)p.ws[3]);
+}
+
+// sdf_to_density (scene.py:235-242) / raw exp (scene.py:250-252).
+// Also returns e = exp(-|s|/b) for the backward.
+__device__ __forceinline__ double density(int mode, double s, double a, double b, double &e) {
+  if (mode == SALF_DENSITY_RAW) {
+    e = 0.0;
+    return exp(s);
+  }
+  e = exp(__ddiv_rn(-fabs(s), b));
+  double inner = __dadd_rn(1.0, __dmul_rn(npsign(s), __dsub_rn(1.0, e)));
+  return __dmul_rn(__dmul_rn(0.5, a), inner);
+}
+
+// segment_opacity (scene.py:282-284).
+__device__ __forceinline__ double seg_alpha(double sigma, double delta) {
+  return npmin(-expm1(__dmul_rn(-sigma, delta)), kAlphaMax);
+}
+
+// eval_color (scene.py:270-279), fp64: z = W_c x + W_sh gamma, sigmoid.
+__device__ __forceinline__ void eval_color64(const VoxPrm &p, const double x[3], const double om[3],
+                                             double c[3]) {
+  const double g0 = kShC0, g1 = __dmul_rn(kShC1, om[1]), g2 = __dmul_rn(kShC1, om[2]),
+               g3 = __dmul_rn(kShC1, om[0]);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    double a0 = __dmul_rn((double)p.wc[3 * i + 0], x[0]);
+    double a1 = __dmul_rn((double)p.wc[3 * i + 1], x[1]);
+    double a2 = __dmul_rn((double)p.wc[3 * i + 2], x[2]);
+    double zc = __dadd_rn(__dadd_rn(a0, a2), a1);
+    double b0 = __dmul_rn((double)p.wsh[4 * i + 0], g0);
+    double b1 = __dmul_rn((double)p.wsh[4 * i + 1], g1);
+    double b2 = __dmul_rn((double)p.wsh[4 * i + 2], g2);
+    double b3 = __dmul_rn((double)p.wsh[4 * i + 3], g3);
+    double zs = __dadd_rn(__dadd_rn(b0, b2), __dadd_rn(b1, b3));
+    double z = __dadd_rn(zc, zs);
+    c[i] = 1.0 / (1.0 + exp(-z));
+  }
+}
+
+// Same field in fp32 (values only flow into the colour accumulators; no
+// threshold decision depends on them).
+__device__ __forceinline__ void eval_color32(const VoxPrm &p, const double xd[3], const double od[3],
+                                             double c[3]) {
+  const float x0 = (float)xd[0], x1 = (float)xd[1], x2 = (float)xd[2];
+  const float g0 = (float)kShC0, g1 = (float)kShC1 * (float)od[1], g2 = (float)kShC1 * (float)od[2],
+              g3 = (float)kShC1 * (float)od[0];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float z = __fmaf_rn(p.wc[3 * i + 2], x2, __fmaf_rn(p.wc[3 * i + 1], x1, p.wc[3 * i] * x0));
+    z = __fmaf_rn(p.wsh[4 * i + 0], g0, z);
+    z = __fmaf_rn(p.wsh[4 * i + 1], g1, z);
+    z = __fmaf_rn(p.wsh[4 * i + 2], g2, z);
+    z = __fmaf_rn(p.wsh[4 * i + 3], g3, z);
+    c[i] = (double)__frcp_rn(1.0f + __expf(-z));
+  }
+}
+
+// (N,3) @ (3,3) as NumPy/OpenBLAS computes it on x86: fma(a2, b2, fma(a1, b1, a0*b0)).
+// r is row-major; `transposed` selects a @ r.T (dot with row i) vs a @ r (column i).
+__device__ __forceinline__ double mm_row(const double a[3], const double *r, int i) {
+  return fma(a[2], r[3 * i + 2], fma(a[1], r[3 * i + 1], __dmul_rn(a[0], r[3 * i + 0])));
+}
+__device__ __forceinline__ double mm_col(const double a[3], const double *r, int j) {
+  return fma(a[2], r[6 + j], fma(a[1], r[3 + j], __dmul_rn(a[0], r[j])));
+}
+
+// Orderable 64-bit key of a double (ascending), NaN last.
+__device__ __forceinline__ uint64_t order_key(double z) {
+  uint64_t u = (uint64_t)__double_as_longlong(z);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes
+// of a converged warp.  Lanes holding the same voxel id form a group
+// (__match_any_sync); groups of >= 3 lanes are summed with full-warp xor
+// butterflies (non-members contribute 0) and their leader issues one set of
+// 27 atomics; lanes in smaller groups add directly.
+__device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t vid, bool active,
+                                             const double g[kGradStride]) {
+  const unsigned full = 0xffffffffu;
+  const unsigned act = __ballot_sync(full, active);
+  if (!act) return;
+  const int lane = threadIdx.x & 31;
+  const long long key = active ? (long long)vid : -1ll - lane;
+  const unsigned grp = __match_any_sync(full, key);
+  const bool big = active && __popc(grp) >= 3;
+  if (active && !big) {
+    double *dst = grad + vid * kGradStride;
+#pragma unroll
+    for (int k = 0; k < kGradStride; ++k)
+      if (g[k] != 0.0) atomicAdd(dst + k, g[k]);
+  }
+  unsigned leaders = __ballot_sync(full, big && lane == __ffs(grp) - 1);
+  while (leaders) {
+    const int L = __ffs(leaders) - 1;
+    leaders &= leaders - 1;
+    const long long lkey = __shfl_sync(full, key, L);
+    const bool mem = big && key == lkey;
+    double *dst = grad + lkey * kGradStride;
+#pragma unroll 1
+    for (int k = 0; k < kGradStride; ++k) {
+      double v = mem ? g[k] : 0.0;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(full, v, off);
+      if (lane == L && v != 0.0) atomicAdd(dst + k, v);
+    }
+  }
+}
+
+}  // namespace salf

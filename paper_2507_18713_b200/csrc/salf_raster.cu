@@ -1,0 +1,669 @@
+// salf_raster.cu -- tile rasterizer for pinhole cameras (reference render_raster.py).
+//
+// Pipeline per frame (all on one stream):
+//   k_project      fp64 corner projection, cull, reference + tightened tile spans,
+//                  orderable depth keys                         (render_raster.py:97-176)
+//   depth rank     stable radix sort of (z_center, index) -> global rank, so
+//                  ties break by voxel index exactly like lexsort    (:177)
+//   k_emit         one 64-bit key (tile << 32 | rank) per (voxel, tile) instance
+//   radix sort     instances by key -> per-tile lists in (z, index) order
+//   k_offsets      CSR offsets per tile                              (:180-181)
+//   k_composite    one CTA per tile, one thread per pixel: staged entries in
+//                  shared memory, fp64 slab test + exact-order fp64 opacity chain,
+//                  early exit when every pixel of the tile is frozen  (:201-301)
+//   k_backward     replay of k_composite producing per-voxel gradients with
+//                  warp-aggregated atomics (definition: DESIGN.md §raster backward)
+#include <cub/cub.cuh>
+
+#include "salf_common.cuh"
+#include "salf_internal.h"
+
+namespace salf {
+
+struct PinholeDev {
+  int width, height, tile, tiles_x, tiles_y;
+  double fx, fy, cx, cy;
+  double pos[3];
+  double rot[9];
+  double near;
+};
+
+static PinholeDev make_pinhole(const salf_camera_t *cam, double near, int tile) {
+  PinholeDev p;
+  p.width = cam->width;
+  p.height = cam->height;
+  p.tile = tile;
+  p.tiles_x = (cam->width + tile - 1) / tile;
+  p.tiles_y = (cam->height + tile - 1) / tile;
+  p.fx = cam->fx; p.fy = cam->fy; p.cx = cam->cx; p.cy = cam->cy;
+  for (int k = 0; k < 3; ++k) p.pos[k] = cam->position[k];
+  for (int k = 0; k < 9; ++k) p.rot[k] = cam->rot[k];
+  p.near = near;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// projection + spans
+
+__device__ __forceinline__ void span_from_rect(double umin, double vmin, double umax, double vmax,
+                                               const PinholeDev &c, bool culled, int4 &span) {
+  // cull_and_bin pixel-centre coverage (render_raster.py:151-166)
+  double u_lo = npmax(ceil(umin - 0.5), 0.0);
+  double u_hi = npmin(floor(umax - 0.5), (double)(c.width - 1));
+  double v_lo = npmax(ceil(vmin - 0.5), 0.0);
+  double v_hi = npmin(floor(vmax - 0.5), (double)(c.height - 1));
+  bool vis = !culled && (u_lo <= u_hi) && (v_lo <= v_hi);
+  if (!vis) {
+    span = make_int4(1, 1, 0, 0);
+    return;
+  }
+  span = make_int4((int)u_lo / c.tile, (int)v_lo / c.tile, (int)u_hi / c.tile, (int)v_hi / c.tile);
+}
+
+__global__ void k_project(int64_t n, const double4 *__restrict__ geo, PinholeDev c,
+                          double4 *__restrict__ rect, double *__restrict__ zc_out,
+                          uint8_t *__restrict__ culled_out, int4 *__restrict__ span_ref,
+                          int4 *__restrict__ span_fit, uint64_t *__restrict__ zkey) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double4 g = geo[i];
+  const double ctr[3] = {g.x, g.y, g.z};
+  double pc[8][3];
+  int n_front = 0, n_back = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    // corner = centre + offset * edge; offsets x fastest (render_raster.py:32-34, :106-109)
+    const double off[3] = {(k & 1) ? 0.5 : -0.5, (k & 2) ? 0.5 : -0.5, (k & 4) ? 0.5 : -0.5};
+    double rel[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) rel[j] = __dsub_rn(__dadd_rn(ctr[j], __dmul_rn(off[j], g.w)), c.pos[j]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) pc[k][j] = mm_col(rel, c.rot, j);  // (corners - pos) @ R
+    if (pc[k][2] <= c.near) ++n_back; else ++n_front;
+  }
+  double relc[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) relc[j] = __dsub_rn(ctr[j], c.pos[j]);
+  const double zc = mm_col(relc, c.rot, 2);
+  const bool culled = (n_back == 8);
+  const bool straddle = !culled && n_back > 0;
+  double umin = INFINITY, vmin = INFINITY, umax = -INFINITY, vmax = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (pc[k][2] > c.near) {
+      // cam.fx * p_cam[..., 0] / z + cam.cx  (render_raster.py:117-118)
+      double u = __dadd_rn(__ddiv_rn(__dmul_rn(c.fx, pc[k][0]), pc[k][2]), c.cx);
+      double v = __dadd_rn(__ddiv_rn(__dmul_rn(c.fy, pc[k][1]), pc[k][2]), c.cy);
+      umin = npmin(umin, u); umax = npmax(umax, u);
+      vmin = npmin(vmin, v); vmax = npmax(vmax, v);
+    }
+  }
+  double r0 = umin, r1 = vmin, r2 = umax, r3 = vmax;
+  if (straddle) { r0 = 0.0; r1 = 0.0; r2 = (double)c.width; r3 = (double)c.height; }
+  if (culled) { r0 = r1 = r2 = r3 = NAN; }
+  if (rect) rect[i] = make_double4(r0, r1, r2, r3);
+  if (zc_out) zc_out[i] = zc;
+  if (culled_out) culled_out[i] = culled ? 1 : 0;
+  int4 sref;
+  span_from_rect(r0, r1, r2, r3, c, culled, sref);
+  if (span_ref) span_ref[i] = sref;
+  if (span_fit) {
+    int4 sfit = sref;
+    if (straddle && sref.x <= sref.z) {
+      // Tight footprint of cube ∩ {z_cam >= near}: the projection of its
+      // vertices (front corners + edge crossings of the near plane), widened
+      // by one pixel.  Pixels outside it cannot produce t1 > t0 for this
+      // voxel, so dropping it from their tiles leaves every sum unchanged.
+      double fu0 = umin, fv0 = vmin, fu1 = umax, fv1 = vmax;
+#pragma unroll
+      for (int e = 0; e < 12; ++e) {
+        // 12 cube edges: 4 along each axis
+        const int axis = e >> 2, w = e & 3;
+        int a, b;
+        if (axis == 0) { a = (w & 1) * 2 + (w >> 1) * 4; b = a + 1; }
+        else if (axis == 1) { a = (w & 1) + (w >> 1) * 4; b = a + 2; }
+        else { a = (w & 1) + (w >> 1) * 2; b = a + 4; }
+        const double za = pc[a][2], zb = pc[b][2];
+        if ((za <= c.near) != (zb <= c.near)) {
+          const double s = (c.near - za) / (zb - za);
+          const double x = pc[a][0] + s * (pc[b][0] - pc[a][0]);
+          const double y = pc[a][1] + s * (pc[b][1] - pc[a][1]);
+          const double u = c.fx * x / c.near + c.cx, v = c.fy * y / c.near + c.cy;
+          fu0 = fmin(fu0, u); fu1 = fmax(fu1, u);
+          fv0 = fmin(fv0, v); fv1 = fmax(fv1, v);
+        }
+      }
+      int4 t;
+      span_from_rect(fu0 - 1.0, fv0 - 1.0, fu1 + 1.0, fv1 + 1.0, c, false, t);
+      sfit = t;
+    }
+    span_fit[i] = sfit;
+  }
+  if (zkey) zkey[i] = order_key(zc);
+}
+
+// ---------------------------------------------------------------------------
+// binning
+
+__global__ void k_span_count(int64_t n, const int4 *__restrict__ span, int64_t *__restrict__ cnt) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int4 s = span[i];
+  cnt[i] = (s.x <= s.z && s.y <= s.w) ? (int64_t)(s.z - s.x + 1) * (s.w - s.y + 1) : 0;
+}
+
+__global__ void k_iota(int64_t n, int32_t *__restrict__ v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+
+__global__ void k_rank(int64_t n, const int32_t *__restrict__ sorted_idx, uint32_t *__restrict__ rank) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) rank[sorted_idx[r]] = (uint32_t)r;
+}
+
+// One warp per voxel: lanes stride over the voxel's tiles (spans can be the
+// full image for straddling voxels in reference mode).
+__global__ void k_emit(int64_t n, const int4 *__restrict__ span, const int64_t *__restrict__ base,
+                       const uint32_t *__restrict__ rank, int tiles_x, uint64_t *__restrict__ keys,
+                       int32_t *__restrict__ vals) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const int4 s = span[warp];
+  if (s.x > s.z || s.y > s.w) return;
+  const int nx = s.z - s.x + 1;
+  const int64_t cnt = (int64_t)nx * (s.w - s.y + 1);
+  const int64_t b = base[warp];
+  const uint64_t r = rank[warp];
+  for (int64_t k = lane; k < cnt; k += 32) {
+    const int ty = s.y + (int)(k / nx), tx = s.x + (int)(k % nx);
+    keys[b + k] = ((uint64_t)(ty * tiles_x + tx) << 32) | r;
+    vals[b + k] = (int32_t)warp;
+  }
+}
+
+__global__ void k_offsets(int n_tiles, int64_t n_inst, const uint64_t *__restrict__ keys,
+                          int64_t *__restrict__ offsets) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > n_tiles) return;
+  // lower_bound of tile t in the sorted keys
+  int64_t lo = 0, hi = n_inst;
+  const uint64_t target = (uint64_t)t << 32;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  offsets[t] = lo;
+}
+
+static inline int bits_for(uint64_t v) {
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b < 1 ? 1 : b;
+}
+
+// ---------------------------------------------------------------------------
+// composite
+
+struct Entry {
+  double o[3];   // camera position - voxel centre
+  double lo[3];  // (-half) - o
+  double hi[3];  //   half  - o
+  double half;   // 0.5 * edge
+  int64_t vid;
+};
+
+struct PixelRay {
+  double d[3], inv[3], t_near;
+  bool zero[3];
+};
+
+__device__ __forceinline__ void pixel_ray(const PinholeDev &c, int px, int py, PixelRay &r) {
+  // gen_camera_rays pinhole (sensors.py:131-151) + t_near (render_raster.py:214-215)
+  const double u = (double)px + 0.5, v = (double)py + 0.5;
+  double dc[3] = {__ddiv_rn(__dsub_rn(u, c.cx), c.fx), __ddiv_rn(__dsub_rn(v, c.cy), c.fy), 1.0};
+  const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(dc[0], dc[0]), __dmul_rn(dc[1], dc[1])),
+                                    __dmul_rn(dc[2], dc[2])));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dc[k] = __ddiv_rn(dc[k], nrm);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r.d[k] = mm_row(dc, c.rot, k);  // d_cam @ R.T
+  const double dz = mm_col(r.d, c.rot, 2);                   // (dirs @ R)[:, 2]
+  r.t_near = __ddiv_rn(c.near, dz);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.zero[k] = (r.d[k] == 0.0);
+    r.inv[k] = 1.0 / r.d[k];
+  }
+}
+
+// slab test of a pixel ray against a staged entry -> (t0, t_out, hit)
+__device__ __forceinline__ bool pair_hit(const PixelRay &r, const Entry &e, double &t0, double &t1) {
+  double ti = 0.0, to = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double nk, fk;
+    if (r.zero[k]) {
+      const bool inside = (e.o[k] >= -e.half) && (e.o[k] <= e.half);
+      nk = inside ? -INFINITY : INFINITY;
+      fk = inside ? INFINITY : -INFINITY;
+    } else {
+      const double ta = __dmul_rn(e.lo[k], r.inv[k]);
+      const double tb = __dmul_rn(e.hi[k], r.inv[k]);
+      nk = npmin(ta, tb);
+      fk = npmax(ta, tb);
+    }
+    if (k == 0) { ti = nk; to = fk; }
+    else { ti = npmax(ti, nk); to = npmin(to, fk); }
+  }
+  t0 = npmax(npmax(ti, r.t_near), 0.0);
+  t1 = to;
+  return t1 > __dadd_rn(t0, 1e-12);
+}
+
+struct SegVals {
+  double tm, delta, x[3], s, e, sigma, alpha, c[3], a, b;
+};
+
+template <bool kExactColor>
+__device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const PixelRay &r, const Entry &e,
+                                           double t0, double t1, SegVals &sv, VoxPrm &p) {
+  sv.delta = __dsub_rn(t1, t0);
+  sv.tm = __dmul_rn(0.5, __dadd_rn(t0, t1));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sv.x[k] = __ddiv_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, r.d[k])), e.half);
+  load_prm(sc.prm, e.vid, p);
+  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.ab) + e.vid);
+  sv.a = ab.x;
+  sv.b = ab.y;
+  sv.s = eval_sdf(p, sv.x);
+  sv.sigma = density(sc.density_mode, sv.s, ab.x, ab.y, sv.e);
+  sv.alpha = seg_alpha(sv.sigma, sv.delta);
+  if (kExactColor) eval_color64(p, sv.x, r.d, sv.c);
+  else eval_color32(p, sv.x, r.d, sv.c);
+}
+
+__device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const PinholeDev &c, int32_t vid,
+                                            Entry &e) {
+  const double4 g = ldg_d4(sc.geo + 4 * (int64_t)vid);
+  e.vid = vid;
+  e.half = __dmul_rn(0.5, g.w);
+  e.o[0] = __dsub_rn(c.pos[0], g.x);
+  e.o[1] = __dsub_rn(c.pos[1], g.y);
+  e.o[2] = __dsub_rn(c.pos[2], g.z);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    e.lo[k] = __dsub_rn(-e.half, e.o[k]);
+    e.hi[k] = __dsub_rn(e.half, e.o[k]);
+  }
+}
+
+constexpr int kChunk = 128;
+
+template <bool kExactColor>
+__global__ void __launch_bounds__(256) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+                                                   const int64_t *__restrict__ offsets,
+                                                   const int32_t *__restrict__ entries, float *__restrict__ out_rgb,
+                                                   float *__restrict__ out_op, float *__restrict__ out_depth,
+                                                   double *__restrict__ saved) {
+  __shared__ Entry sm[kChunk];
+  const int tile_id = blockIdx.x;
+  const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
+  const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
+  const int px = tx * c.tile + lx, py = ty * c.tile + ly;
+  const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
+  const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
+  const double keep = 1.0 - opt.stop_threshold;
+
+  PixelRay r;
+  if (inside) pixel_ray(c, px, py, r);
+  double acc_c[3] = {0.0, 0.0, 0.0}, acc_l = 0.0, acc_w = 0.0, acc_wt = 0.0, log_t = 0.0;
+  bool alive = inside;
+  int64_t n_stop = end - beg;
+  const int nthreads = blockDim.x;
+
+  for (int64_t base = beg; base < end; base += kChunk) {
+    const int cn = (int)min((int64_t)kChunk, end - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry(sc, c, entries[base + j], sm[j]);
+    __syncthreads();
+    if (alive) {
+      for (int j = 0; j < cn; ++j) {
+        double t0, t1;
+        if (!pair_hit(r, sm[j], t0, t1)) continue;
+        SegVals sv;
+        VoxPrm p;
+        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv, p);
+        const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
+        const double lg = log1p(-a);
+        const double tb = exp(log_t);
+        if (tb > keep) {
+          const double w = __dmul_rn(tb, a);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+          acc_l = __dadd_rn(acc_l, lg);
+          acc_w = __dadd_rn(acc_w, w);
+          acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
+        } else {
+          alive = false;
+          n_stop = base - beg + j;
+          break;
+        }
+        log_t = __dadd_rn(log_t, lg);
+      }
+    }
+    if (!__syncthreads_or(alive)) break;
+  }
+  if (!inside) return;
+  const int64_t pix = (int64_t)py * c.width + px;
+  const double t_fin = exp(acc_l);
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    out_rgb[pix * 3 + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(t_fin, opt.background[k]));
+  out_op[pix] = (float)__dsub_rn(1.0, t_fin);
+  out_depth[pix] = acc_w > kDepthWeightMin ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
+  if (saved) {
+    double *s = saved + pix * SALF_SAVED_STRIDE;
+    s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
+    s[3] = acc_w; s[4] = acc_wt; s[5] = acc_l; s[6] = (double)n_stop; s[7] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward
+
+// Gradient of one included segment (backward.py:52-100), written into g[27].
+__device__ __forceinline__ void segment_grad(int mode, const SegVals &sv, const double om[3], double A,
+                                             double tb, double a_cl, double w, double suffix, double tail,
+                                             const double dC[3], double g[kGradStride]) {
+  const double g_alpha = __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, a_cl)));
+  const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta), exp(__dmul_rn(-sv.sigma, sv.delta)));
+  double ds;
+  if (mode == SALF_DENSITY_SDF) {
+    const double k2 = __ddiv_rn(sv.a, __dmul_rn(2.0, sv.b));
+    ds = (sv.s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), sv.e);
+    g[25] = __dmul_rn(g_sigma, sv.sigma);
+    g[26] = __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, sv.s), sv.e));
+  } else {
+    ds = __dmul_rn(g_sigma, sv.sigma);
+    g[25] = 0.0;
+    g[26] = 0.0;
+  }
+  g[0] = __dmul_rn(ds, sv.x[0]); g[1] = __dmul_rn(ds, sv.x[1]); g[2] = __dmul_rn(ds, sv.x[2]); g[3] = ds;
+  const double gam[4] = {kShC0, __dmul_rn(kShC1, om[1]), __dmul_rn(kShC1, om[2]), __dmul_rn(kShC1, om[0])};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double gz = __dmul_rn(__dmul_rn(__dmul_rn(dC[i], w), sv.c[i]), __dsub_rn(1.0, sv.c[i]));
+#pragma unroll
+    for (int j = 0; j < 3; ++j) g[4 + 3 * i + j] = __dmul_rn(gz, sv.x[j]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[13 + 4 * i + j] = __dmul_rn(gz, gam[j]);
+  }
+}
+
+template <bool kExactColor>
+__global__ void __launch_bounds__(256) k_backward(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+                                                  const int64_t *__restrict__ offsets,
+                                                  const int32_t *__restrict__ entries,
+                                                  const double *__restrict__ saved, const double *__restrict__ d_rgb,
+                                                  const double *__restrict__ d_depth, double *__restrict__ grad) {
+  __shared__ Entry sm[kChunk];
+  const int tile_id = blockIdx.x;
+  const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
+  const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
+  const int px = tx * c.tile + lx, py = ty * c.tile + ly;
+  const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
+  const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
+  const double keep = 1.0 - opt.stop_threshold;
+  const int nthreads = blockDim.x;
+
+  PixelRay r;
+  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, log_t = 0.0;
+  int64_t n_stop = 0;
+  if (inside) {
+    pixel_ray(c, px, py, r);
+    const int64_t pix = (int64_t)py * c.width + px;
+    const double *s = saved + pix * SALF_SAVED_STRIDE;
+    for (int k = 0; k < 3; ++k) dC[k] = d_rgb[pix * 3 + k];
+    const double acc_w = s[3], acc_wt = s[4];
+    // depth_valid / depth_safe / wsum_safe (backward.py:46-49)
+    const bool ok = acc_w > kDepthWeightMin;
+    dd = ok ? d_depth[pix] : 0.0;
+    D = ok ? __ddiv_rn(acc_wt, acc_w) : 0.0;
+    ws = ok ? acc_w : 1.0;
+    // sum_j A_j w_j = dC . acc_rgb + dD (acc_wt - D acc_w) / ws  (suffix sums by subtraction)
+    total = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], s[0]), __dmul_rn(dC[2], s[2])), __dmul_rn(dC[1], s[1])),
+                      __ddiv_rn(__dmul_rn(dd, __dsub_rn(acc_wt, __dmul_rn(D, acc_w))), ws));
+    // tail = (dC . background) * T_final  (backward.py:62)
+    tail = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], opt.background[0]), __dmul_rn(dC[2], opt.background[2])),
+                               __dmul_rn(dC[1], opt.background[1])),
+                     exp(s[5]));
+    n_stop = (int64_t)s[6];
+  }
+  int64_t max_stop = n_stop;
+  // CTA-wide bound on the entries any pixel still needs
+  __shared__ long long s_max;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  atomicMax(&s_max, (long long)max_stop);
+  __syncthreads();
+  const int64_t lim = beg + (int64_t)s_max;
+
+  for (int64_t base = beg; base < lim; base += kChunk) {
+    const int cn = (int)min((int64_t)kChunk, lim - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry(sc, c, entries[base + j], sm[j]);
+    __syncthreads();
+    for (int j = 0; j < cn; ++j) {
+      const int64_t jj = base - beg + j;
+      double g[kGradStride];
+      bool act = false;
+      int64_t vid = sm[j].vid;
+      double t0, t1;
+      if (inside && jj < n_stop && pair_hit(r, sm[j], t0, t1)) {
+        SegVals sv;
+        VoxPrm p;
+        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv, p);
+        const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
+        const double lg = log1p(-a);
+        const double tb = exp(log_t);
+        if (tb > keep) {
+          const double w = __dmul_rn(tb, a);
+          // A = dC . c + dD (t_mid - D) / ws   (backward.py:52-59, einsum order (0+2)+1)
+          const double A = __dadd_rn(
+              __dadd_rn(__dadd_rn(__dmul_rn(dC[0], sv.c[0]), __dmul_rn(dC[2], sv.c[2])), __dmul_rn(dC[1], sv.c[1])),
+              __ddiv_rn(__dmul_rn(dd, __dsub_rn(sv.tm, D)), ws));
+          prefix = __dadd_rn(prefix, __dmul_rn(A, w));
+          const double suffix = __dsub_rn(total, prefix);
+          segment_grad(sc.density_mode, sv, r.d, A, tb, a, w, suffix, tail, dC, g);
+          act = true;
+        }
+        log_t = __dadd_rn(log_t, lg);
+      }
+      scatter_grad(grad, vid, act, g);
+    }
+  }
+  (void)keep;
+}
+
+}  // namespace salf
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+using namespace salf;
+
+extern "C" int salf_project_voxels(const salf_scene_t *scene, const salf_camera_t *cam, double near,
+                                   int32_t tile, double *rect, double *z_center, uint8_t *culled,
+                                   int32_t *span_ref, int32_t *span_fit, uint64_t *zkey, void *stream) {
+  SALF_TRY {
+    if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
+                                                     camera_kind_repr(cam->kind));
+    if (scene->n == 0) return SALF_OK;
+    PinholeDev c = make_pinhole(cam, near, tile);
+    const int bs = 128;
+    k_project<<<(unsigned)((scene->n + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(
+        scene->n, reinterpret_cast<const double4 *>(scene->geo), c, reinterpret_cast<double4 *>(rect), z_center,
+        culled, reinterpret_cast<int4 *>(span_ref), reinterpret_cast<int4 *>(span_fit), zkey);
+    return check_cuda("salf_project_voxels");
+  }
+  SALF_CATCH
+}
+
+// workspace layout for salf_raster_bin
+struct BinWs {
+  int64_t *cnt, *base;
+  uint64_t *zk_sorted;
+  int32_t *idx_in, *idx_out;
+  uint32_t *rank;
+  uint64_t *keys_a, *keys_b;
+  int32_t *vals_b;
+  void *cub_tmp;
+  size_t cub_bytes;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t cub_bytes_needed(int64_t n_voxels, int64_t capacity) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, a, (int64_t *)nullptr, (int64_t *)nullptr, (int)std::max<int64_t>(n_voxels, 1));
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, (int)std::max<int64_t>(n_voxels, 1));
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (uint64_t *)nullptr, (uint64_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, (int64_t)std::max<int64_t>(capacity, 1));
+  return std::max(a, std::max(b, c));
+}
+
+static BinWs carve(void *ws, int64_t n, int64_t cap, size_t *total) {
+  BinWs w;
+  size_t off = 0;
+  char *p = (char *)ws;
+  auto take = [&](size_t bytes) { char *q = p ? p + off : nullptr; off += align_up(bytes); return q; };
+  w.cnt = (int64_t *)take(sizeof(int64_t) * (n + 1));
+  w.base = (int64_t *)take(sizeof(int64_t) * (n + 1));
+  w.zk_sorted = (uint64_t *)take(sizeof(uint64_t) * n);
+  w.idx_in = (int32_t *)take(sizeof(int32_t) * n);
+  w.idx_out = (int32_t *)take(sizeof(int32_t) * n);
+  w.rank = (uint32_t *)take(sizeof(uint32_t) * n);
+  w.keys_a = (uint64_t *)take(sizeof(uint64_t) * cap);
+  w.keys_b = (uint64_t *)take(sizeof(uint64_t) * cap);
+  w.vals_b = (int32_t *)take(sizeof(int32_t) * cap);
+  w.cub_bytes = cub_bytes_needed(n, cap);
+  w.cub_tmp = take(w.cub_bytes);
+  *total = off;
+  return w;
+}
+
+extern "C" size_t salf_raster_bin_workspace_bytes(int64_t n_voxels, int64_t capacity, int32_t n_tiles) {
+  (void)n_tiles;
+  size_t total = 0;
+  carve(nullptr, std::max<int64_t>(n_voxels, 1), std::max<int64_t>(capacity, 1), &total);
+  return total;
+}
+
+extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double near, int32_t tile,
+                               int32_t mode, const uint64_t *zkey, const int32_t *span, const uint8_t *visible_hint,
+                               void *workspace, size_t workspace_bytes, int64_t capacity, int64_t *offsets,
+                               int32_t *entries, int64_t *n_instances, void *stream) {
+  SALF_TRY {
+    (void)visible_hint;
+    (void)mode;
+    cudaStream_t st = (cudaStream_t)stream;
+    PinholeDev c = make_pinhole(cam, near, tile);
+    const int n_tiles = c.tiles_x * c.tiles_y;
+    const int64_t n = scene->n;
+    if (n == 0) {
+      cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (n_tiles + 1), st);
+      *n_instances = 0;
+      return check_cuda("salf_raster_bin");
+    }
+    size_t need = 0;
+    BinWs w = carve(workspace, std::max<int64_t>(n, 1), std::max<int64_t>(capacity, 1), &need);
+    if (need > workspace_bytes) return set_error(SALF_EWORKSPACE, "raster bin workspace too small: %zu < %zu",
+                                                 workspace_bytes, need);
+    const int bs = 256;
+    const unsigned gb = (unsigned)((n + bs - 1) / bs);
+    k_span_count<<<gb, bs, 0, st>>>(n, reinterpret_cast<const int4 *>(span), w.cnt);
+    size_t tb = w.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt, w.base, (int)n, st);
+    // base[n] = total instances (cnt[n] is garbage-free: set to 0 first)
+    int64_t total = 0;
+    {
+      // recompute: total = base[n-1] + cnt[n-1]
+      int64_t hb[2];
+      cudaMemcpyAsync(&hb[0], w.base + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(&hb[1], w.cnt + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      total = hb[0] + hb[1];
+    }
+    *n_instances = total;
+    if (total > capacity) return set_error(SALF_EWORKSPACE, "instance capacity %lld < %lld", (long long)capacity,
+                                           (long long)total);
+    // global depth rank: stable sort of (zkey, index) -> ties by index (lexsort)
+    k_iota<<<gb, bs, 0, st>>>(n, w.idx_in);
+    tb = w.cub_bytes;
+    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, zkey, w.zk_sorted, w.idx_in, w.idx_out, (int)n, 0, 64, st);
+    k_rank<<<gb, bs, 0, st>>>(n, w.idx_out, w.rank);
+    if (total > 0) {
+      const int64_t warps = n;
+      k_emit<<<(unsigned)((warps * 32 + bs - 1) / bs), bs, 0, st>>>(
+          n, reinterpret_cast<const int4 *>(span), w.base, w.rank, c.tiles_x, w.keys_a, entries);
+      const int end_bit = 32 + bits_for((uint64_t)n_tiles);
+      const int begin_bit = 0;
+      tb = w.cub_bytes;
+      cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.keys_a, w.keys_b, entries, w.vals_b, (int64_t)total,
+                                      begin_bit, end_bit, st);
+      cudaMemcpyAsync(entries, w.vals_b, sizeof(int32_t) * total, cudaMemcpyDeviceToDevice, st);
+      k_offsets<<<(n_tiles + 1 + bs - 1) / bs, bs, 0, st>>>(n_tiles, total, w.keys_b, offsets);
+    } else {
+      cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (n_tiles + 1), st);
+    }
+    return check_cuda("salf_raster_bin");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
+                                     const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
+                                     float *out_rgb, float *out_opacity, float *out_depth, double *saved,
+                                     void *stream) {
+  SALF_TRY {
+    if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
+                                                     camera_kind_repr(cam->kind));
+    if (opts->tile < 1 || opts->tile > 16) return set_error(SALF_EINVAL, "tile size must be in [1, 16]");
+    PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
+    const int n_tiles = c.tiles_x * c.tiles_y;
+    const int threads = std::max(32, opts->tile * opts->tile);
+    if (opts->exact_color)
+      k_composite<true><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, out_rgb,
+                                                                        out_opacity, out_depth, saved);
+    else
+      k_composite<false><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, out_rgb,
+                                                                         out_opacity, out_depth, saved);
+    return check_cuda("salf_raster_composite");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
+                                    const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
+                                    const double *saved, const double *d_rgb, const double *d_depth, double *grad,
+                                    void *stream) {
+  SALF_TRY {
+    if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
+                                                     camera_kind_repr(cam->kind));
+    if (opts->tile < 1 || opts->tile > 16) return set_error(SALF_EINVAL, "tile size must be in [1, 16]");
+    PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
+    const int n_tiles = c.tiles_x * c.tiles_y;
+    const int threads = ((std::max(32, opts->tile * opts->tile) + 31) / 32) * 32;
+    if (opts->exact_color)
+      k_backward<true><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, saved,
+                                                                       d_rgb, d_depth, grad);
+    else
+      k_backward<false><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, saved,
+                                                                        d_rgb, d_depth, grad);
+    return check_cuda("salf_raster_backward");
+  }
+  SALF_CATCH
+}

@@ -1,0 +1,426 @@
+// salf_ray.cu -- linear-octree ray path (reference octree.py, render_ray.py).
+//
+// One thread per ray runs the reference's epsilon-marching state machine
+// (octree.py:214-273) in fp64 with the reference's operation order and no FMA
+// contraction, so the ray/voxel hit list is bit-identical to march_batch.
+// The fused forward shades each leaf segment as it is found (fp64 opacity
+// chain, fp32 or fp64 colour), applies the product-of-(1 - alpha) early stop
+// of render_ray.py:154-157 and composites front to back (render_ray.py:86-114)
+// without materialising any per-segment record.  The backward re-marches the
+// same rays warp-synchronously and scatters per-voxel gradients with
+// warp-aggregated atomics.
+#include "salf_common.cuh"
+#include "salf_internal.h"
+
+namespace salf {
+
+struct OctDev {
+  const int32_t *nodes;
+  double rmin[3], rmax[3];
+  double root_edge;
+};
+
+static OctDev make_oct(const salf_octree_t *t) {
+  OctDev o;
+  o.nodes = t->nodes;
+  for (int k = 0; k < 3; ++k) {
+    o.rmin[k] = t->root_min[k];
+    o.rmax[k] = t->root_min[k] + t->root_edge;  // buffer.root_min + buffer.root_edge (octree.py:232)
+  }
+  o.root_edge = t->root_edge;
+  return o;
+}
+
+enum : int32_t { kStatusRoundCap = 1, kStatusOutsideRoot = 2, kStatusOrder = 4 };
+
+// query_batch for one point (octree.py:136-166).  Returns node word
+// (-1 empty, <= -2 leaf), writes corner/edge of the node.
+__device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3], double corner[3], double &edge,
+                                               bool &outside) {
+  double u[3];
+  outside = false;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    u[k] = __ddiv_rn(__dsub_rn(p[k], t.rmin[k]), t.root_edge);
+    if (u[k] < -1e-9 || u[k] > 1.0 + 1e-9) outside = true;
+    u[k] = npmin(npmax(u[k], 0.0), 1.0);
+    corner[k] = t.rmin[k];
+  }
+  edge = t.root_edge;
+  int32_t w = __ldg(t.nodes);
+  while (w >= 0) {
+    const int b0 = u[0] >= 0.5, b1 = u[1] >= 0.5, b2 = u[2] >= 0.5;
+    edge = __dmul_rn(edge, 0.5);
+    corner[0] = __dadd_rn(corner[0], b0 ? edge : 0.0);
+    corner[1] = __dadd_rn(corner[1], b1 ? edge : 0.0);
+    corner[2] = __dadd_rn(corner[2], b2 ? edge : 0.0);
+    u[0] = __dsub_rn(__dmul_rn(2.0, u[0]), (double)b0);
+    u[1] = __dsub_rn(__dmul_rn(2.0, u[1]), (double)b1);
+    u[2] = __dsub_rn(__dmul_rn(2.0, u[2]), (double)b2);
+    w = __ldg(t.nodes + w + b0 + 2 * b1 + 4 * b2);
+  }
+  return w;
+}
+
+// Per-ray marcher state (BatchMarch, octree.py:222-273).
+struct Marcher {
+  double o[3], d[3], t_max, t_cur, t_end;
+  bool active;
+  int rounds;
+
+  __device__ void init(const OctDev &t, const double *orig, const double *dir, double tmax) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { o[k] = orig[k]; d[k] = dir[k]; }
+    t_max = tmax;
+    double t_in, t_out;
+    ray_box(o, d, t.rmin, t.rmax, t_in, t_out);
+    t_cur = npmax(t_in, 0.0);
+    t_end = npmin(t_out, t_max);
+    active = (t_out > t_cur) && (t_cur < t_max) && isfinite(t_cur);
+    rounds = 0;
+  }
+
+  // One round; returns true and (vid, s0, s1) when a kept leaf segment was found.
+  __device__ bool step(const OctDev &t, int64_t &vid, double &s0, double &s1, int32_t &status) {
+    if (++rounds > kMaxRounds) {
+      status |= kStatusRoundCap;
+      active = false;
+      return false;
+    }
+    double p[3], corner[3], edge, cmax[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) p[k] = __dadd_rn(o[k], __dmul_rn(t_cur, d[k]));
+    bool outside;
+    const int32_t w = query_point(t, p, corner, edge, outside);
+    if (outside) {
+      status |= kStatusOutsideRoot;
+      active = false;
+      return false;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cmax[k] = __dadd_rn(corner[k], edge);
+    double ti, far;
+    ray_box(p, d, corner, cmax, ti, far);
+    t_cur = __dadd_rn(t_cur, __dadd_rn(npmax(far, 0.0), kEpsAdvance));
+    bool got = false;
+    if (w <= -2) {
+      double a_in, a_out;
+      ray_box(o, d, corner, cmax, a_in, a_out);
+      s0 = npmax(a_in, 0.0);
+      s1 = npmin(a_out, t_max);
+      if (s1 > __dadd_rn(s0, 1e-12)) {
+        vid = (int64_t)(-w - 2);
+        got = true;
+      }
+    }
+    if (t_cur >= npmin(t_end, t_max)) active = false;
+    return got;
+  }
+};
+
+struct RaySeg {
+  double tm, delta, x[3], s, e, sigma, alpha, c[3], a, b;
+};
+
+// _evaluate_geometry (render_ray.py:117-133) + eval_color for one segment.
+template <bool kExactColor>
+__device__ __forceinline__ void shade_seg(const salf_scene_t &sc, const Marcher &m, int64_t vid, double s0,
+                                          double s1, RaySeg &sv, bool want_color) {
+  sv.tm = __dmul_rn(0.5, __dadd_rn(s0, s1));
+  sv.delta = __dsub_rn(s1, s0);
+  const double4 g = ldg_d4(sc.geo + 4 * vid);
+  const double ctr[3] = {g.x, g.y, g.z};
+  const double sc2 = __ddiv_rn(2.0, g.w);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(sv.tm, m.d[k])), ctr[k]), sc2);
+  VoxPrm p;
+  load_prm(sc.prm, vid, p);
+  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.ab) + vid);
+  sv.a = ab.x;
+  sv.b = ab.y;
+  sv.s = eval_sdf(p, sv.x);
+  sv.sigma = density(sc.density_mode, sv.s, ab.x, ab.y, sv.e);
+  sv.alpha = seg_alpha(sv.sigma, sv.delta);
+  if (want_color) {
+    if (kExactColor) eval_color64(p, sv.x, m.d, sv.c);
+    else eval_color32(p, sv.x, m.d, sv.c);
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+__global__ void k_query(OctDev t, int64_t n, const double *__restrict__ pts, int8_t *__restrict__ flag,
+                        int64_t *__restrict__ vid, double *__restrict__ corner, double *__restrict__ edge,
+                        int32_t *__restrict__ outside) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]}, c[3], e;
+  bool out;
+  int32_t w = query_point(t, p, c, e, out);
+  if (out) atomicOr(outside, 1);
+  flag[i] = w >= 0 ? 0 : (w == -1 ? -1 : 1);
+  vid[i] = w <= -2 ? (int64_t)(-w - 2) : -1;
+  corner[3 * i] = c[0]; corner[3 * i + 1] = c[1]; corner[3 * i + 2] = c[2];
+  edge[i] = e;
+}
+
+// march_batch hit list (count pass when seg_vid == nullptr, fill pass otherwise).
+__global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, const double *__restrict__ dirs,
+                        const double *__restrict__ tmax, salf_scene_t sc, double keep, int early_stop,
+                        int64_t *__restrict__ counts, const int64_t *__restrict__ starts, int64_t *__restrict__ seg_vid,
+                        double *__restrict__ seg_t0, double *__restrict__ seg_t1, int32_t *__restrict__ status) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Marcher m;
+  m.init(t, orig + 3 * i, dirs + 3 * i, tmax ? tmax[i] : INFINITY);
+  int64_t k = 0, off = starts ? starts[i] : 0;
+  int32_t st = 0;
+  double t_run = 1.0;
+  while (m.active) {
+    int64_t vid;
+    double s0, s1;
+    if (!m.step(t, vid, s0, s1, st)) continue;
+    if (seg_vid) {
+      seg_vid[off + k] = vid;
+      seg_t0[off + k] = s0;
+      seg_t1[off + k] = s1;
+    }
+    ++k;
+    if (early_stop) {
+      RaySeg sv;
+      shade_seg<true>(sc, m, vid, s0, s1, sv, false);
+      t_run = __dmul_rn(t_run, __dsub_rn(1.0, npmin(npmax(sv.alpha, 0.0), kAlphaMax)));
+      if (t_run <= keep) break;
+    }
+  }
+  if (!seg_vid) counts[i] = k;
+  if (status) status[i] = st;
+}
+
+// Fused integrate_rays: march + shade + composite for one ray per thread.
+template <bool kExactColor>
+__global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
+                                                     const double *__restrict__ orig, const double *__restrict__ dirs,
+                                                     const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
+                                                     float *__restrict__ out_rgb, float *__restrict__ out_op,
+                                                     float *__restrict__ out_depth, double *__restrict__ saved,
+                                                     int32_t *__restrict__ status) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double keep = 1.0 - opt.stop_threshold;
+  double acc_c[3] = {0.0, 0.0, 0.0}, acc_l = 0.0, acc_w = 0.0, acc_wt = 0.0, log_t = 0.0, t_run = 1.0,
+         last_t0 = -INFINITY;
+  int64_t n_seg = 0;
+  int32_t st = 0;
+  const bool ok = valid ? valid[i] != 0 : true;
+  if (ok) {
+    Marcher m;
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY);
+    bool frozen = false;
+    while (m.active) {
+      int64_t vid;
+      double s0, s1;
+      if (!m.step(t, vid, s0, s1, st)) continue;
+      if (s0 < last_t0) st |= kStatusOrder;
+      last_t0 = s0;
+      ++n_seg;
+      RaySeg sv;
+      shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen);
+      const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
+      if (!frozen) {
+        const double tb = exp(log_t);
+        if (tb > keep) {
+          const double w = __dmul_rn(tb, a);
+#pragma unroll
+          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+          acc_l = __dadd_rn(acc_l, log1p(-a));
+          acc_w = __dadd_rn(acc_w, w);
+          acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
+        } else {
+          frozen = true;
+        }
+        log_t = __dadd_rn(log_t, log1p(-a));
+      }
+      // product-based early stop on the march (render_ray.py:154-157)
+      t_run = __dmul_rn(t_run, __dsub_rn(1.0, a));
+      if (t_run <= keep) break;
+    }
+  }
+  if (ok) {
+    const double t_fin = exp(acc_l);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out_rgb[3 * i + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(t_fin, opt.background[k]));
+    out_op[i] = (float)__dsub_rn(1.0, t_fin);
+    out_depth[i] = acc_w > kDepthWeightMin ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
+  } else {  // render_rays_image: invalid pixels keep the background (render_ray.py:280-293)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out_rgb[3 * i + k] = (float)opt.background[k];
+    out_op[i] = 0.0f;
+    out_depth[i] = NAN;
+  }
+  if (saved) {
+    double *s = saved + i * SALF_SAVED_STRIDE;
+    s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
+    s[3] = acc_w; s[4] = acc_wt; s[5] = acc_l; s[6] = (double)n_seg; s[7] = 0.0;
+  }
+  if (status) status[i] = st;
+}
+
+// Ray backward: warp-synchronous re-march (every lane advances one round per
+// iteration, as BatchMarch does) so gradient scatters run with the full warp.
+template <bool kExactColor>
+__global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
+                                                      const double *__restrict__ orig, const double *__restrict__ dirs,
+                                                      const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
+                                                      const double *__restrict__ saved, const double *__restrict__ d_rgb,
+                                                      const double *__restrict__ d_depth, double *__restrict__ grad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double keep = 1.0 - opt.stop_threshold;
+  bool live = i < n && (valid ? valid[i] != 0 : true);
+  Marcher m;
+  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, log_t = 0.0,
+         t_run = 1.0;
+  if (live) {
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY);
+    const double *s = saved + i * SALF_SAVED_STRIDE;
+    for (int k = 0; k < 3; ++k) dC[k] = d_rgb[3 * i + k];
+    const double acc_w = s[3], acc_wt = s[4];
+    const bool okd = acc_w > kDepthWeightMin;
+    dd = okd ? d_depth[i] : 0.0;
+    D = okd ? __ddiv_rn(acc_wt, acc_w) : 0.0;
+    ws = okd ? acc_w : 1.0;
+    total = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], s[0]), __dmul_rn(dC[2], s[2])), __dmul_rn(dC[1], s[1])),
+                      __ddiv_rn(__dmul_rn(dd, __dsub_rn(acc_wt, __dmul_rn(D, acc_w))), ws));
+    tail = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], opt.background[0]), __dmul_rn(dC[2], opt.background[2])),
+                               __dmul_rn(dC[1], opt.background[1])),
+                     exp(s[5]));
+    live = m.active && (dC[0] != 0.0 || dC[1] != 0.0 || dC[2] != 0.0 || dd != 0.0);
+  }
+  int32_t st = 0;
+  while (__any_sync(0xffffffffu, live)) {
+    bool act = false;
+    int64_t vid = 0;
+    double g[kGradStride];
+    if (live) {
+      double s0, s1;
+      if (m.step(t, vid, s0, s1, st)) {
+        RaySeg sv;
+        shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, true);
+        const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
+        const double tb = exp(log_t);
+        if (tb > keep) {
+          const double w = __dmul_rn(tb, a);
+          const double A = __dadd_rn(
+              __dadd_rn(__dadd_rn(__dmul_rn(dC[0], sv.c[0]), __dmul_rn(dC[2], sv.c[2])), __dmul_rn(dC[1], sv.c[1])),
+              __ddiv_rn(__dmul_rn(dd, __dsub_rn(sv.tm, D)), ws));
+          prefix = __dadd_rn(prefix, __dmul_rn(A, w));
+          const double suffix = __dsub_rn(total, prefix);
+          const double g_alpha =
+              __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, a)));
+          const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta), exp(__dmul_rn(-sv.sigma, sv.delta)));
+          double ds;
+          if (sc.density_mode == SALF_DENSITY_SDF) {
+            const double k2 = __ddiv_rn(sv.a, __dmul_rn(2.0, sv.b));
+            ds = (sv.s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), sv.e);
+            g[25] = __dmul_rn(g_sigma, sv.sigma);
+            g[26] = __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, sv.s), sv.e));
+          } else {
+            ds = __dmul_rn(g_sigma, sv.sigma);
+            g[25] = 0.0;
+            g[26] = 0.0;
+          }
+          g[0] = __dmul_rn(ds, sv.x[0]); g[1] = __dmul_rn(ds, sv.x[1]); g[2] = __dmul_rn(ds, sv.x[2]); g[3] = ds;
+          const double gam[4] = {kShC0, __dmul_rn(kShC1, m.d[1]), __dmul_rn(kShC1, m.d[2]),
+                                 __dmul_rn(kShC1, m.d[0])};
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double gz = __dmul_rn(__dmul_rn(__dmul_rn(dC[c], w), sv.c[c]), __dsub_rn(1.0, sv.c[c]));
+#pragma unroll
+            for (int j = 0; j < 3; ++j) g[4 + 3 * c + j] = __dmul_rn(gz, sv.x[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[13 + 4 * c + j] = __dmul_rn(gz, gam[j]);
+          }
+          act = true;
+          log_t = __dadd_rn(log_t, log1p(-a));
+          t_run = __dmul_rn(t_run, __dsub_rn(1.0, a));
+          if (t_run <= keep) live = false;
+        } else {
+          live = false;  // every later segment is excluded
+        }
+      }
+      if (!m.active) live = false;
+    }
+    scatter_grad(grad, vid, act, g);
+  }
+}
+
+}  // namespace salf
+
+using namespace salf;
+
+extern "C" int salf_octree_query(const salf_octree_t *tree, int64_t n, const double *p, int8_t *flag, int64_t *vid,
+                                 double *corner, double *edge, int32_t *out_of_root, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    OctDev t = make_oct(tree);
+    k_query<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(t, n, p, flag, vid, corner, edge,
+                                                                             out_of_root);
+    return check_cuda("salf_octree_query");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_march(const salf_octree_t *tree, int64_t n, const double *origins, const double *dirs,
+                          const double *t_max, const salf_scene_t *scene, double stop_threshold, int32_t early_stop,
+                          int64_t *counts, const int64_t *starts, int64_t *seg_vid, double *seg_t0, double *seg_t1,
+                          int32_t *status, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    OctDev t = make_oct(tree);
+    salf_scene_t sc = scene ? *scene : salf_scene_t{};
+    if (early_stop && !scene) return set_error(SALF_EINVAL, "early stop needs the scene");
+    k_march<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        t, n, origins, dirs, t_max, sc, 1.0 - stop_threshold, early_stop, counts, starts, seg_vid, seg_t0, seg_t1,
+        status);
+    return check_cuda("salf_march");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n, const double *origins,
+                                const double *dirs, const uint8_t *valid, const salf_raster_opts_t *opts,
+                                float *out_rgb, float *out_opacity, float *out_depth, double *saved, int32_t *status,
+                                void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    if (opts->exact_color)
+      k_ray_forward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
+                                                                    out_opacity, out_depth, saved, status);
+    else
+      k_ray_forward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
+                                                                     out_opacity, out_depth, saved, status);
+    return check_cuda("salf_ray_forward");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                 const double *origins, const double *dirs, const uint8_t *valid,
+                                 const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,
+                                 const double *d_depth, double *grad, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    if (opts->exact_color)
+      k_ray_backward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
+                                                                     d_rgb, d_depth, grad);
+    else
+      k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
+                                                                      d_rgb, d_depth, grad);
+    return check_cuda("salf_ray_backward");
+  }
+  SALF_CATCH
+}

@@ -1,0 +1,77 @@
+"""Device-resident scene: the HBM layout the kernels read.
+
+Per voxel (SoA of AoS blocks, all 16-byte aligned):
+  geo  double4  (cx, cy, cz, edge)           32 B  projection, slab tests, local coords
+  ab   double2  (a = exp(log_a), b = exp(log_b)) 16 B  density transfer
+  prm  float[28] w_s[4] w_c[9] w_sh[12] pad[3] 112 B  field parameters (7 x 16-B loads)
+Centres, edges and exp(log a|b) are computed on the host with NumPy exactly as
+the reference does (scene.py:186-194, :249), so the kernels start from the
+reference's own fp64 values.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scene import FlatVoxels, Scene, flatten_scene
+
+
+class DeviceScene:
+    def __init__(self, flat: FlatVoxels, device=None):
+        if np.any(flat.rotations != np.array([1.0, 0.0, 0.0, 0.0])) and flat.n:
+            if not np.allclose(flat.rotations, np.array([1.0, 0.0, 0.0, 0.0])):
+                raise NotImplementedError("rotated voxels are not supported by the B200 path yet")
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.n = flat.n
+        self.density_mode = flat.density_mode
+        geo = np.empty((flat.n, 4), np.float64)
+        geo[:, :3] = flat.centers
+        geo[:, 3] = flat.edges
+        ab = np.stack([np.exp(flat.log_a), np.exp(flat.log_b)], axis=1) if flat.n else np.zeros((0, 2))
+        prm = np.zeros((flat.n, _lib.PRM_STRIDE), np.float32)
+        prm[:, 0:4] = flat.w_s.reshape(-1, 4)
+        prm[:, 4:13] = flat.w_c.reshape(-1, 9)
+        prm[:, 13:25] = flat.w_sh.reshape(-1, 12)
+        # keep at least one element so data pointers are valid for empty scenes
+        pad = lambda a: a if a.shape[0] else np.zeros((1,) + a.shape[1:], a.dtype)
+        self.geo = torch.as_tensor(pad(geo), device=self.device).contiguous()
+        self.ab = torch.as_tensor(pad(np.ascontiguousarray(ab)), device=self.device).contiguous()
+        self.prm = torch.as_tensor(pad(prm), device=self.device).contiguous()
+        self.flat = flat
+
+    @classmethod
+    def from_scene(cls, scene: Scene, t_stamp: float = 0.0, device=None) -> "DeviceScene":
+        return cls(flatten_scene(scene, t_stamp), device)
+
+    def c_struct(self) -> _lib.SceneT:
+        s = _lib.SceneT()
+        s.n = self.n
+        s.geo, s.ab, s.prm = self.geo.data_ptr(), self.ab.data_ptr(), self.prm.data_ptr()
+        s.density_mode = _lib.DENSITY[self.density_mode]
+        return s
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.geo.nbytes + self.ab.nbytes + self.prm.nbytes)
+
+
+def as_device_scene(obj, device=None) -> DeviceScene:
+    if isinstance(obj, DeviceScene):
+        return obj
+    if isinstance(obj, FlatVoxels):
+        return DeviceScene(obj, device)
+    if isinstance(obj, Scene):
+        return DeviceScene.from_scene(obj, device=device)
+    raise TypeError(f"expected Scene, FlatVoxels or DeviceScene, got {type(obj).__name__}")
+
+
+def grads_to_dict(grad: torch.Tensor) -> dict:
+    """(M, 27) gradient buffer -> the reference's {param: array} layout (backward.py:24)."""
+    g = grad.detach().cpu().numpy()
+    m = g.shape[0]
+    return {"w_s": g[:, 0:4].copy(), "w_c": g[:, 4:13].reshape(m, 3, 3).copy(),
+            "w_sh": g[:, 13:25].reshape(m, 3, 4).copy(), "log_a": g[:, 25].copy(),
+            "log_b": g[:, 26].copy()}

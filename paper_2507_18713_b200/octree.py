@@ -1,0 +1,188 @@
+"""Linear octree + epsilon-marching -- drop-in for reference octree.py.
+
+`build_octree` (octree.py:54-125) runs natively on the host
+(`salf_octree_build_host`) and reproduces the reference's depth-first node
+numbering exactly; the node table is uploaded once as 32-bit words
+(word >= 0: internal node, children at word..word+7; -1: empty;
+<= -2: leaf holding voxel -word-2).  `query_batch` and `march_batch` run on
+the GPU with the reference's fp64 operation order, so hit lists are
+bit-identical.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scene import SceneBounds, SparseVoxelSet
+
+EPS_ADVANCE = 1e-4
+MIN_EDGE_FACTOR = 64
+_MAX_ROUNDS = 200_000
+
+
+@dataclass
+class OctreeBuffer:
+    nodes: torch.Tensor  # (n_nodes,) int32 words on the device
+    root_min: np.ndarray
+    root_edge: float
+    max_depth: int
+
+    @property
+    def n_nodes(self) -> int:
+        return int(self.nodes.shape[0])
+
+    @property
+    def nodes_id(self) -> np.ndarray:
+        w = self.nodes.cpu().numpy().astype(np.int64)
+        return np.where(w >= 0, w, np.where(w == -1, -1, -w - 2))
+
+    @property
+    def nodes_leaf(self) -> np.ndarray:
+        w = self.nodes.cpu().numpy()
+        return np.where(w >= 0, 0, np.where(w == -1, -1, 1)).astype(np.int8)
+
+    def c_struct(self) -> _lib.OctreeT:
+        t = _lib.OctreeT()
+        t.n_nodes = self.n_nodes
+        t.nodes = self.nodes.data_ptr()
+        t.root_min[:] = [float(v) for v in self.root_min]
+        t.root_edge = float(self.root_edge)
+        t.max_depth = int(self.max_depth)
+        return t
+
+
+def compute_child_index(p_local) -> np.ndarray:
+    """octree.py:47-51."""
+    bits = (np.asarray(p_local, np.float64) >= 0.5).astype(np.int64)
+    return bits[..., 0] + 2 * (bits[..., 1] + 2 * bits[..., 2])
+
+
+def build_octree(voxels: SparseVoxelSet, bounds: SceneBounds | None = None, device=None) -> OctreeBuffer:
+    """Depth-first linear octree (octree.py:54-125); same errors and messages."""
+    lib = _lib.load(require_cuda=False)
+    if bounds is None:
+        bounds = voxels.bounds
+    extent = bounds.aabb_max - bounds.aabb_min
+    m = max(0, int(np.ceil(np.log2(max(extent.max(), 1e-300) / bounds.base_edge) - 1e-12)))
+    root_edge = bounds.base_edge * 2.0 ** m
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = voxels.n
+    if n:
+        level = voxels.level.astype(np.int64)
+        cells = voxels.ijk.astype(np.int64)
+        edges = voxels.edges()
+        if edges.min() < MIN_EDGE_FACTOR * EPS_ADVANCE:
+            raise ValueError(f"voxel edge {edges.min():.3g} m below the marching floor "
+                             f"{MIN_EDGE_FACTOR * EPS_ADVANCE:.3g} m")
+        keys = (level << 54) ^ (cells[:, 0] << 36) ^ (cells[:, 1] << 18) ^ cells[:, 2]
+        if len(np.unique(keys)) != n:
+            raise ValueError("duplicate voxel cells in the set")
+        centers = voxels.centers()
+        if np.any(centers < bounds.aabb_min) or np.any(centers > bounds.aabb_max):
+            raise ValueError("voxel outside scene bounds")
+    lv = np.ascontiguousarray(voxels.level.astype(np.uint8)) if n else np.zeros(1, np.uint8)
+    ijk = np.ascontiguousarray(voxels.ijk.astype(np.int32)) if n else np.zeros((1, 3), np.int32)
+    n_nodes = _lib.C.c_int64(0)
+    depth = _lib.C.c_int32(0)
+    _lib.check(lib.salf_octree_build_host(n, lv.ctypes.data, ijk.ctypes.data, m, None, 0,
+                                          _lib.ref(n_nodes), _lib.ref(depth)), "build_octree")
+    nodes = np.empty(n_nodes.value, np.int32)
+    _lib.check(lib.salf_octree_build_host(n, lv.ctypes.data, ijk.ctypes.data, m, nodes.ctypes.data,
+                                          nodes.shape[0], _lib.ref(n_nodes), _lib.ref(depth)),
+               "build_octree")
+    return OctreeBuffer(torch.as_tensor(nodes, device=dev), bounds.aabb_min.copy(), root_edge,
+                        int(depth.value))
+
+
+def dump_table(buffer: OctreeBuffer) -> str:
+    """octree.py:128-133."""
+    ids, leaf = buffer.nodes_id, buffer.nodes_leaf
+    lines = ["index is_leaf id_or_offset"]
+    lines += [f"{i} {int(leaf[i])} {int(ids[i])}" for i in range(buffer.n_nodes)]
+    return "\n".join(lines) + "\n"
+
+
+def query_batch(buffer: OctreeBuffer, p):
+    """octree.py:136-166 -> (is_leaf i8, voxel_id i64, node_min (n,3), node_edge), NumPy."""
+    lib = _lib.load()
+    dev = buffer.nodes.device
+    pts = _lib.as_f64(np.atleast_2d(np.asarray(p, np.float64)) if not isinstance(p, torch.Tensor) else p,
+                      dev).reshape(-1, 3)
+    n = pts.shape[0]
+    flag = torch.empty(n, dtype=torch.int8, device=dev)
+    vid = torch.empty(n, dtype=torch.int64, device=dev)
+    corner = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    edge = torch.empty(n, dtype=torch.float64, device=dev)
+    outside = torch.zeros(1, dtype=torch.int32, device=dev)
+    t = buffer.c_struct()
+    _lib.check(lib.salf_octree_query(_lib.ref(t), n, pts.data_ptr(), flag.data_ptr(), vid.data_ptr(),
+                                     corner.data_ptr(), edge.data_ptr(), outside.data_ptr(),
+                                     _lib.stream_ptr()), "query_batch")
+    if int(outside.item()):
+        raise ValueError("query point outside the octree root cube")
+    return flag.cpu().numpy(), vid.cpu().numpy(), corner.cpu().numpy(), edge.cpu().numpy()
+
+
+def query(buffer: OctreeBuffer, p) -> int:
+    return int(query_batch(buffer, np.asarray(p, np.float64)[None, :])[1][0])
+
+
+def _check_unit(dirs: torch.Tensor) -> None:
+    if dirs.shape[0] and bool((torch.linalg.norm(dirs, dim=1) - 1.0).abs().gt(1e-6).any()):
+        raise ValueError("ray directions must be unit norm")
+
+
+def march_segments(buffer: OctreeBuffer, origins, dirs, t_max=np.inf, scene=None,
+                   stop_threshold: float = 0.99, early_stop: bool = False):
+    """Hit list in per-ray march order as device tensors (ray, vid, t0, t1)."""
+    lib = _lib.load()
+    dev = buffer.nodes.device
+    o = _lib.as_f64(origins, dev).reshape(-1, 3)
+    d = _lib.as_f64(dirs, dev).reshape(-1, 3)
+    _check_unit(d)
+    n = o.shape[0]
+    tm = _lib.as_f64(np.broadcast_to(np.asarray(t_max, np.float64), (n,)) if not isinstance(t_max, torch.Tensor)
+                     else t_max, dev).reshape(n)
+    t = buffer.c_struct()
+    sc = scene.c_struct() if scene is not None else None
+    counts = torch.zeros(n, dtype=torch.int64, device=dev)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    s = _lib.stream_ptr()
+    scp = _lib.ref(sc) if sc is not None else None
+    _lib.check(lib.salf_march(_lib.ref(t), n, o.data_ptr(), d.data_ptr(), tm.data_ptr(), scp,
+                              float(stop_threshold), int(early_stop), counts.data_ptr(), None, None,
+                              None, None, status.data_ptr(), s), "march_batch")
+    if n and bool((status & 1).any()):
+        raise RuntimeError("octree marching failed to terminate")
+    if n and bool((status & 2).any()):
+        raise ValueError("query point outside the octree root cube")
+    starts = torch.cumsum(counts, 0) - counts
+    total = int(counts.sum().item()) if n else 0
+    vid = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    t0 = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    t1 = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+    if total:
+        _lib.check(lib.salf_march(_lib.ref(t), n, o.data_ptr(), d.data_ptr(), tm.data_ptr(), scp,
+                                  float(stop_threshold), int(early_stop), counts.data_ptr(),
+                                  starts.data_ptr(), vid.data_ptr(), t0.data_ptr(), t1.data_ptr(),
+                                  None, s), "march_batch")
+    ray = torch.repeat_interleave(torch.arange(n, device=dev), counts)
+    return ray, vid[:total], t0[:total], t1[:total]
+
+
+def march_batch(buffer: OctreeBuffer, origins, dirs, t_max=np.inf):
+    """octree.py:276-295: (ray, vid, t0, t1) NumPy arrays sorted by (ray, t0), stable."""
+    ray, vid, t0, t1 = (x.cpu().numpy() for x in march_segments(buffer, origins, dirs, t_max))
+    order = np.lexsort((t0, ray))
+    return ray[order], vid[order], t0[order], t1[order]
+
+
+def march(buffer: OctreeBuffer, origin, direction, t_max=np.inf):
+    """octree.py:298-302: single ray -> [(voxel_id, t_entry, t_exit)]."""
+    ray, vid, t0, t1 = march_batch(buffer, np.asarray(origin, np.float64)[None, :],
+                                   np.asarray(direction, np.float64)[None, :], t_max)
+    return list(zip(vid.tolist(), t0.tolist(), t1.tolist()))

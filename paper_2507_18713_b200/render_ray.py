@@ -1,0 +1,161 @@
+"""Ray-traced rendering -- drop-in for reference render_ray.py (static scenes).
+
+`integrate_rays` (render_ray.py:161-239) runs as one fused kernel: octree
+march + midpoint field evaluation + front-to-back compositing with the
+reference's early termination, no per-segment records in HBM.  The returned
+`RenderRecords` carries the per-ray outputs plus what the backward needs to
+replay the rays (`backward.backward_records`).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceScene, as_device_scene
+from .octree import OctreeBuffer, build_octree, march_segments
+from .scene import Scene
+
+STOP_THRESHOLD = 0.99
+DEPTH_WEIGHT_MIN = 0.5
+STATIC_OWNER = -1
+
+
+@dataclass
+class SceneOctrees:
+    static: OctreeBuffer
+    actors: list
+
+
+def build_scene_octrees(scene: Scene, device=None) -> SceneOctrees:
+    """render_ray.py:44-48 (actors: a later §8(f) row)."""
+    if any(a.voxels.n for a in scene.actors):
+        raise NotImplementedError("dynamic actors are not supported by the B200 path yet")
+    return SceneOctrees(static=build_octree(scene.static, device=device), actors=[])
+
+
+@dataclass
+class RenderRecords:
+    """Per-ray outputs (CUDA tensors) + replay state for the backward."""
+
+    n_rays: int
+    out_color: torch.Tensor  # (R, 3) f32
+    opacity: torch.Tensor  # (R,) f32
+    depth: torch.Tensor  # (R,) f32, NaN = no return
+    saved: torch.Tensor  # (R, 8) f64: acc_rgb[3], w_sum, w_t, log_T, n_seg, 0
+    status: torch.Tensor  # (R,) int32: 1 round cap, 2 outside root, 4 entry-order
+    origins: torch.Tensor
+    dirs: torch.Tensor
+    valid: torch.Tensor | None
+    scene: DeviceScene
+    octree: OctreeBuffer
+    opts: _lib.RasterOptsT
+    background: np.ndarray
+
+    @property
+    def weight_sum(self) -> torch.Tensor:
+        return self.saved[:, 3]
+
+    @property
+    def t_final(self) -> torch.Tensor:
+        return torch.exp(self.saved[:, 5])
+
+    @property
+    def n_segments(self) -> torch.Tensor:
+        return self.saved[:, 6].to(torch.int64)
+
+
+def _opts(background, stop_threshold, exact_color) -> _lib.RasterOptsT:
+    o = _lib.RasterOptsT()
+    o.background[:] = [float(v) for v in np.asarray(background, np.float64).reshape(3)]
+    o.near, o.stop_threshold, o.tile = 0.0, float(stop_threshold), 0
+    o.exact_color = 1 if exact_color else 0
+    return o
+
+
+def _octree_of(octrees) -> OctreeBuffer:
+    return octrees.static if isinstance(octrees, SceneOctrees) else octrees
+
+
+def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf,
+                   background=(0.0, 0.0, 0.0), stop_threshold: float = STOP_THRESHOLD,
+                   valid=None, exact_color: bool = False) -> RenderRecords:
+    """Render a ray batch against the static scene (render_ray.py:161-239).
+
+    `t_stamps` only matter for dynamic actors (static scenes are time
+    invariant, render_ray.py tests :128-135); finite `t_max` is supported by
+    `march_batch` but not by the fused renderer (the reference's renderers
+    always pass infinity)."""
+    del t_stamps
+    if np.any(np.isfinite(np.asarray(t_max, np.float64))):
+        raise NotImplementedError("finite t_max is only supported by march_batch")
+    lib = _lib.load()
+    ds = as_device_scene(scene)
+    tree = _octree_of(octrees)
+    dev = ds.device
+    o = _lib.as_f64(origins, dev).reshape(-1, 3)
+    d = _lib.as_f64(dirs, dev).reshape(-1, 3)
+    n = o.shape[0]
+    if n and bool((torch.linalg.norm(d, dim=1) - 1.0).abs().gt(1e-6).any()):
+        raise ValueError("ray directions must be unit norm")
+    vmask = None
+    if valid is not None:
+        vmask = (valid if isinstance(valid, torch.Tensor) else torch.as_tensor(np.asarray(valid))).to(
+            device=dev, dtype=torch.uint8).contiguous()
+    rgb = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    op = torch.empty(n, dtype=torch.float32, device=dev)
+    depth = torch.empty(n, dtype=torch.float32, device=dev)
+    saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    opts = _opts(background, stop_threshold, exact_color)
+    sc, t = ds.c_struct(), tree.c_struct()
+    _lib.check(lib.salf_ray_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
+                                    _lib.ptr(vmask), _lib.ref(opts), rgb.data_ptr(), op.data_ptr(),
+                                    depth.data_ptr(), saved.data_ptr(), status.data_ptr(),
+                                    _lib.stream_ptr()), "integrate_rays")
+    return RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
+                         np.asarray(background, np.float64))
+
+
+def check_status(rec: RenderRecords) -> None:
+    """Raise like the reference would for rays it cannot march."""
+    st = rec.status
+    if rec.n_rays and bool((st & 1).any()):
+        raise RuntimeError("octree marching failed to terminate")
+    if rec.n_rays and bool((st & 2).any()):
+        raise ValueError("query point outside the octree root cube")
+
+
+def render_depth(records: RenderRecords) -> torch.Tensor:
+    return records.depth
+
+
+def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chunk: int = 65536,
+                      stop_threshold: float = STOP_THRESHOLD, exact_color: bool = False):
+    """render_ray.py:275-294 -> (color (H,W,3), opacity (H,W), depth (H,W)) CUDA tensors.
+
+    All rays go in one launch (`chunk` kept for signature compatibility);
+    invalid rays keep the background, zero opacity and NaN depth."""
+    del chunk
+    h, w = batch.shape
+    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, background=background,
+                         stop_threshold=stop_threshold, valid=batch.valid, exact_color=exact_color)
+    check_status(rec)
+    return rec.out_color.reshape(h, w, 3), rec.opacity.reshape(h, w), rec.depth.reshape(h, w)
+
+
+def render_lidar_ranges(scene, octrees, batch, *, chunk: int = 65536) -> torch.Tensor:
+    """render_ray.py:297-306: expected range per ray, (beams, steps), NaN = no return."""
+    del chunk
+    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs)
+    check_status(rec)
+    return rec.depth.reshape(batch.shape)
+
+
+def segments(scene, octrees, origins, dirs, stop_threshold: float = STOP_THRESHOLD):
+    """The ray path's hit list with the reference's early stop (parity export)."""
+    ds = as_device_scene(scene)
+    return march_segments(_octree_of(octrees), origins, dirs, np.inf, ds, stop_threshold, True)

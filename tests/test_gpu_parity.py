@@ -1,0 +1,215 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle on identical inputs.
+
+Bars (north star): bit-exact tile CSR / sort order / hit lists / octree node
+tables; <= 1e-4 relative for rendered colour, opacity, depth and gradients
+(gradients: normwise per parameter class)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import (grads_close, load_golden_scene, oracle_camera, oracle_lidar,
+                      oracle_voxels)
+from oracle import salf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _cam(d):
+    from paper_2507_18713_b200.sensors import CameraModel
+    return CameraModel.from_dict(d)
+
+
+def _flat(name):
+    from paper_2507_18713_b200.scene import flatten_scene
+    return flatten_scene(load_golden_scene(name))
+
+
+def _np(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def assert_image_close(got, want, rel=1e-4):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    nan_g, nan_w = np.isnan(got), np.isnan(want)
+    np.testing.assert_array_equal(nan_g, nan_w)
+    m = ~nan_w
+    err = np.abs(got[m] - want[m]) / np.maximum(np.abs(want[m]), 1.0)
+    assert err.max(initial=0.0) <= rel, f"max rel err {err.max():.3e}"
+
+
+# ---- rasterizer -----------------------------------------------------------------
+
+def test_project_voxels_bit_exact(golden, golden_meta):
+    from paper_2507_18713_b200 import render_raster as RR
+    rmin, rmax, zc, culled = RR.project_voxels(_flat("rand400"), _cam(golden_meta["rand400_cam"]))
+    np.testing.assert_array_equal(culled, golden["rand400_culled"])
+    np.testing.assert_array_equal(zc, golden["rand400_zc"])
+    np.testing.assert_array_equal(rmin, golden["rand400_rmin"])
+    np.testing.assert_array_equal(rmax, golden["rand400_rmax"])
+
+
+def test_cull_and_bin_bit_exact(golden, golden_meta):
+    from paper_2507_18713_b200 import render_raster as RR
+    bins = RR.cull_and_bin(_flat("rand400"), _cam(golden_meta["rand400_cam"]))
+    np.testing.assert_array_equal(bins.offsets, golden["rand400_offsets"])
+    np.testing.assert_array_equal(bins.entries, golden["rand400_entries"])
+
+
+def test_cull_and_bin_c1_bit_exact(golden, golden_meta):
+    """C1: S20k (reference CLI bytes) at 256^2: 385,735 instances, bit for bit."""
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    from paper_2507_18713_b200.scenes import make_init_scene
+    bins = RR.cull_and_bin(flatten_scene(make_init_scene("S20k")), _cam(golden_meta["c1_cam"]))
+    np.testing.assert_array_equal(bins.offsets, golden["c1_offsets"])
+    np.testing.assert_array_equal(bins.entries, golden["c1_entries"])
+
+
+def test_render_bins_are_subsequences(golden, golden_meta):
+    """Tightened render lists keep the reference order and drop only straddlers."""
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    from paper_2507_18713_b200.scenes import make_init_scene
+    flat = flatten_scene(make_init_scene("S20k"))
+    cam = _cam(golden_meta["c1_cam"])
+    fit = RR.render_bins(flat, cam)
+    off, ent = golden["c1_offsets"], golden["c1_entries"]
+    assert fit.entries.size < ent.size
+    for t in range(len(off) - 1):
+        ref = ent[off[t]:off[t + 1]]
+        got = fit.entries[fit.offsets[t]:fit.offsets[t + 1]]
+        assert np.array_equal(ref[np.isin(ref, got)], got), f"tile {t} order differs"
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_rasterize_matches_reference(golden, golden_meta, exact):
+    from paper_2507_18713_b200 import render_raster as RR
+    fb = RR.rasterize(_flat("rand400"), _cam(golden_meta["rand400_cam"]), background=(0.1, 0.2, 0.3),
+                      exact_color=exact)
+    assert_image_close(_np(fb.color), golden["rand400_color"])
+    assert_image_close(_np(fb.opacity), golden["rand400_opacity"])
+    assert_image_close(_np(fb.depth), golden["rand400_depth"])
+
+
+def test_rasterize_c1_matches_reference(golden, golden_meta):
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    from paper_2507_18713_b200.scenes import make_init_scene
+    fb = RR.rasterize(flatten_scene(make_init_scene("S20k")), _cam(golden_meta["c1_cam"]))
+    assert_image_close(_np(fb.color), golden["c1_color"])
+    assert_image_close(_np(fb.opacity), golden["c1_opacity"])
+    assert_image_close(_np(fb.depth), golden["c1_depth"])
+
+
+def test_tile_size_is_scheduling_only(golden_meta):
+    """test_render_raster.py:140-150: tile 1 == tile 16 bit for bit."""
+    from paper_2507_18713_b200 import render_raster as RR
+    flat, cam = _flat("rand400"), _cam(golden_meta["rand400_cam"])
+    a = RR.rasterize(flat, cam, tile=16)
+    b = RR.rasterize(flat, cam, tile=1)
+    assert torch.equal(a.color, b.color) and torch.equal(a.opacity, b.opacity)
+    assert torch.equal(torch.nan_to_num(a.depth, 7.0), torch.nan_to_num(b.depth, 7.0))
+
+
+def test_raster_backward_matches_reference_composition(golden, golden_meta):
+    from paper_2507_18713_b200 import render_raster as RR
+    cam = _cam(golden_meta["rand300_cam"])
+    fb, st = RR.rasterize(_flat("rand300"), cam, background=(0.05, 0.1, 0.15), return_state=True,
+                          exact_color=True)
+    h, w = cam.height, cam.width
+    g = RR.rasterize_backward(st, golden["rand300_rbw_dcolor"].reshape(h, w, 3),
+                              golden["rand300_rbw_ddepth"].reshape(h, w))
+    want = {k: golden["rand300_rbw_g_" + k] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
+    assert grads_close(g, want) < 1e-4
+
+
+# ---- octree / ray path ----------------------------------------------------------
+
+def test_octree_and_query_bit_exact(golden):
+    from paper_2507_18713_b200.octree import build_octree, query_batch
+    tree = build_octree(load_golden_scene("rand400m").static)
+    np.testing.assert_array_equal(tree.nodes_id, golden["march_nodes_id"])
+    np.testing.assert_array_equal(tree.nodes_leaf, golden["march_nodes_leaf"])
+    fl, vid, corner, edge = query_batch(tree, golden["query_p"])
+    np.testing.assert_array_equal(fl, golden["query_flag"])
+    np.testing.assert_array_equal(vid, golden["query_vid"])
+    np.testing.assert_array_equal(corner, golden["query_corner"])
+    np.testing.assert_array_equal(edge, golden["query_edge"])
+
+
+def test_march_hit_list_bit_exact(golden):
+    from paper_2507_18713_b200.octree import build_octree, march_batch
+    tree = build_octree(load_golden_scene("rand400m").static)
+    ray, vid, t0, t1 = march_batch(tree, golden["march_o"], golden["march_d"])
+    for a, k in ((ray, "ray"), (vid, "vid"), (t0, "t0"), (t1, "t1")):
+        np.testing.assert_array_equal(a, golden["march_" + k])
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_integrate_rays_matches_reference(golden, exact):
+    from paper_2507_18713_b200 import render_ray as RY
+    sc = load_golden_scene("rand300i")
+    rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), golden["integ_o"], golden["integ_d"],
+                            background=(0.2, 0.1, 0.3), exact_color=exact)
+    assert int(rec.status.max()) == 0
+    assert_image_close(_np(rec.out_color), golden["integ_color"])
+    assert_image_close(_np(rec.opacity), 1.0 - golden["integ_tfinal"])
+    assert_image_close(_np(rec.depth), golden["integ_depth"])
+    np.testing.assert_allclose(_np(rec.weight_sum), golden["integ_wsum"], rtol=1e-12, atol=1e-13)
+    # early-stopped hit list (ray, vid, t0) bit-exact
+    ray, vid, t0, t1 = (x.cpu().numpy() for x in RY.segments(sc, RY.build_scene_octrees(sc),
+                                                                golden["integ_o"], golden["integ_d"]))
+    np.testing.assert_array_equal(ray, golden["integ_ray"])
+    np.testing.assert_array_equal(vid, golden["integ_vid"])
+    np.testing.assert_array_equal(t0, golden["integ_t0"])
+    np.testing.assert_array_equal(t1, golden["integ_t1"])
+
+
+@pytest.mark.parametrize("case", ["integ", "fd"])
+def test_ray_backward_matches_reference(golden, case):
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.backward import backward_records
+    name = {"integ": "rand300i", "fd": "fd10"}[case]
+    bg = (0.2, 0.1, 0.3) if case == "integ" else golden["fd_bg"]
+    sc = load_golden_scene(name)
+    rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), golden[case + "_o"], golden[case + "_d"],
+                            background=bg, exact_color=True)
+    g = backward_records(rec, sc, golden[case + "_dcolor"], golden[case + "_ddepth"])["static"]
+    want = {k: golden[f"{case}_g_{k}"] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
+    assert grads_close(g, want) < 1e-4
+
+
+def test_ray_image_matches_reference(golden, golden_meta):
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.sensors import camera_rays
+    sc = load_golden_scene("rand300")
+    color, op, depth = RY.render_rays_image(sc, RY.build_scene_octrees(sc),
+                                            camera_rays(_cam(golden_meta["rand300_cam"])))
+    assert_image_close(_np(color), golden["rand300_ray_color"])
+    assert_image_close(_np(op), golden["rand300_ray_opacity"])
+    assert_image_close(_np(depth), golden["rand300_ray_depth"])
+
+
+# ---- sensors --------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["pin", "fish", "eq", "lidar"])
+def test_sensor_rays_match_reference(golden, golden_meta, name):
+    from paper_2507_18713_b200 import sensors as S
+    d = golden_meta["rays_" + name]
+    if name == "lidar":
+        b = S.gen_lidar_rays(S.sensor_from_dict(d), t0=0.5)
+    else:
+        b = S.camera_rays(S.CameraModel.from_dict(d))
+    np.testing.assert_allclose(_np(b.origins), golden[f"rays_{name}_o"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(_np(b.dirs), golden[f"rays_{name}_d"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(_np(b.t_stamps), golden[f"rays_{name}_t"], rtol=0, atol=1e-12)
+    np.testing.assert_array_equal(b.valid.cpu().numpy(), golden[f"rays_{name}_valid"])
