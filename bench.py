@@ -1,0 +1,441 @@
+"""Benchmark: C2 -- 1920x1080 pinhole raster forward + backward on the 1M-voxel
+synthetic scene (S1M), one frame per rank per step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: each rank renders its own C5-rig
+camera (yaw = 45 deg x rank) forward + backward and the per-voxel gradient
+buffer is all-reduced over NCCL (the training step's one exchange).  `value`
+is whole-job frames/s; rank 0 prints one JSON line.  `--impl reference` times
+the reference's CPU algorithm (the oracle port, oracle/salf_oracle.py) on the
+host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from concurrent.futures import ProcessPoolExecutor
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "camera FPS @1920x1080 (raster fwd+bwd, S1M) and LiDAR rays/s (128-beam)"
+UNIT = "frames/s"
+WORKLOAD = "C2: S1M init-regime scene (1,023,816 voxels), 1920x1080 pinhole raster forward+backward"
+
+
+# ------------------------------------------------------------------------------
+# CPU baseline: the reference algorithm (oracle port) on a bounded tile sample
+
+_W = {}
+
+
+def _cpu_init(regime):
+    from oracle import salf_oracle as O
+    from paper_2507_18713_b200.scenes import get_scene
+    sc = get_scene("S1M", regime)
+    b, v = sc.bounds, sc.static
+    _W["vox"] = O.Voxels.from_grid(b.aabb_min, b.aabb_max, b.base_edge, v.level, v.ijk, v.w_s, v.w_c,
+                                   v.w_sh, v.log_a, v.log_b)
+
+
+def _cpu_tile(args):
+    """Reference forward (rasterize) + backward (raster records -> backward_records)
+    of ONE 16x16 tile of the C2 frame; returns seconds."""
+    from oracle import salf_oracle as O
+    from paper_2507_18713_b200 import configs
+    tx, ty = args
+    c = configs.c2_camera()
+    cam = O.Camera("pinhole", c.width, c.height, c.fx, c.fy, c.cx, c.cy, position=c.position,
+                   quaternion=c.quaternion)
+    vox = _W["vox"]
+    t0 = time.perf_counter()
+    win = (tx, ty, tx, ty)
+    fb = O.rasterize(vox, cam, window=win)
+    rec = O.raster_records(vox, cam, window=win)
+    dc = np.zeros((rec["n_rays"], 3))
+    dc[:] = 1e-6
+    O.backward_records(rec, vox, dc, np.zeros(rec["n_rays"]))
+    del fb
+    return time.perf_counter() - t0
+
+
+def _cpu_ready(_):
+    return "vox" in _W
+
+
+def _sample_tiles(k, seed):
+    rng = np.random.default_rng(seed)
+    return [(int(rng.integers(0, 120)), int(rng.integers(0, 68))) for _ in range(k)]
+
+
+class CpuBaseline:
+    def __init__(self, regime="init", workers=None):
+        n = workers or min(len(os.sched_getaffinity(0)), 64)
+        self.workers = n
+        import multiprocessing as mp
+        self.pool = ProcessPoolExecutor(n, mp_context=mp.get_context("spawn"), initializer=_cpu_init,
+                                        initargs=(regime,))
+        list(self.pool.map(_cpu_ready, range(n)))  # every worker has loaded the scene
+
+    def sample(self, seed):
+        """One bounded sample: `workers` tiles in parallel -> extrapolated frames/s."""
+        tiles = _sample_tiles(self.workers, seed)
+        t0 = time.perf_counter()
+        secs = list(self.pool.map(_cpu_tile, tiles))
+        wall = time.perf_counter() - t0
+        tiles_per_s = len(tiles) / wall
+        return tiles_per_s / (120 * 68), dict(wall_s=wall, tile_s_mean=float(np.mean(secs)))
+
+    def close(self):
+        self.pool.shutdown()
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    base = CpuBaseline("init")
+    for w in range(args.warmup):
+        base.sample(1000 + w)
+    vals, info = [], []
+    for k in range(args.steps):
+        v, i = base.sample(k)
+        vals.append(v)
+        info.append(i)
+    base.close()
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256)",
+        "config": {"workload": WORKLOAD, "resolution": [1920, 1080], "voxels": 1023816,
+                   "sample": "one 16x16 tile per worker per step, extrapolated to 8160 tiles"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": base.workers, "kind": "port",
+                         "sample": f"{base.workers} random tiles of 8160 per step (fwd+bwd), "
+                                   "extrapolated linearly to the full frame"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": {"tile_s_mean": float(np.mean([i["tile_s_mean"] for i in info]))},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------
+# GPU arm
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in Path(self.f.name).read_text().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 8]
+        mx = [float(r[2]) for r in rows if len(r) > 8]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows if len(r) > 8 for j in range(4)
+                          if r[5 + j].strip().lower() == "active"})
+        load = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": float(np.median(load)) if load else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def _dist_init(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles):
+    """Compulsory HBM bytes per launch."""
+    rec = 32 + 16 + 112  # geo + ab + prm per visible voxel
+    fwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 20 * hw + 64 * hw
+    bwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 64 * hw + 32 * hw + 216 * m_vis
+    return fwd, bwd
+
+
+def run_ours(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2507_18713_b200 import _lib, configs
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.backward import loss_color_seed
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.scenes import get_scene
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    scene = get_scene("S1M", args.regime)
+    ds = DeviceScene.from_scene(scene, device=dev)
+    cam = configs.c2_camera(yaw_deg=45.0 * (rank % 8))
+    h, w = cam.height, cam.width
+    g = torch.Generator().manual_seed(rank)
+    gt_host = (0.3 + 0.4 * torch.rand((h, w, 3), generator=g)).pin_memory()
+    gt_dev = gt_host.to(dev)
+    mask = torch.ones(h * w, dtype=torch.bool, device=dev)
+    dd = torch.zeros((h, w), dtype=torch.float64, device=dev)
+    grad = torch.zeros((ds.n, _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    out_host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
+    loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
+
+    def step(gt, events=None, e2e=False):
+        fb, st = RR.rasterize(ds, cam, return_state=True, events=events)
+        diff = fb.color.double() - gt.double()
+        dc = loss_color_seed(fb.color.reshape(-1, 3), gt.reshape(-1, 3), mask).reshape(h, w, 3)
+        grad.zero_()
+        RR.rasterize_backward(st, dc, dd, grad, as_dict=False, events=events)
+        if world > 1:
+            dist.all_reduce(grad)
+        if e2e:
+            loss_host.copy_(diff.abs().mean().reshape(1), non_blocking=True)
+            out_host.copy_(fb.color, non_blocking=True)
+        return st
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        st = step(gt_dev)
+    barrier()
+
+    # kernel launches of one step (CUPTI via torch.profiler; outside the timed region)
+    launches = None
+    ours = None
+    try:
+        if args.no_profile:
+            raise RuntimeError("--no-profile")
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step(gt_dev)
+            torch.cuda.synchronize()
+        kern = [e for e in prof.events() if e.device_type.name == "CUDA"
+                and not e.name.lower().startswith(("memcpy", "memset"))]
+        launches = len(kern)
+        ours = sum(1 for e in kern if "salf" in e.name or "k_" in e.name or "cub" in e.name.lower())
+    except Exception as ex:  # profiler unavailable: leave the count unset
+        ours = None
+        print(f"[bench] launch count unavailable: {ex}", file=sys.stderr)
+
+    # ---- device-timed steps, inputs resident, L2 flushed between steps ----
+    clocks = Clocks(local)
+    barrier()
+    times, kev = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = []
+        a.record()
+        step(gt_dev, events=ev)
+        b.record()
+        times.append((a, b))
+        kev.append(ev)
+    barrier()
+    clk = clocks.stop()
+    ms = [a.elapsed_time(b) for a, b in times]
+    kms = {}
+    for ev in kev:
+        for name, s, e in ev:
+            kms.setdefault(name, []).append(s.elapsed_time(e))
+    step_ms = float(np.sum(ms)) / args.steps
+    t_max = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    step_ms_max = float(t_max.item())
+    value = world * 1e3 / step_ms_max
+
+    # ---- end to end through the public API: pinned H2D of the target, D2H of frame + loss ----
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        gt = gt_host.to(dev, non_blocking=True)
+        step(gt, e2e=True)
+    b.record()
+    barrier()
+    e2e_ms = a.elapsed_time(b) / args.steps
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * 1e3 / float(te.item())
+
+    if rank != 0:
+        return
+
+    # ---- roofline of the dominant kernel ----
+    peaks = {}
+    pp = ROOT / "MEASURED_PEAKS.json"
+    if pp.exists():
+        peaks = json.loads(pp.read_text())
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    n_inst = st.n_instances
+    m_vis = int(torch.unique(st.entries).numel()) if n_inst else 0
+    fwd_b, bwd_b = _algorithmic_bytes(n_inst, m_vis, h * w, (st.offsets.numel() - 1))
+    k_fwd = float(np.mean(kms.get("raster_composite", [np.nan])))
+    k_bwd = float(np.mean(kms.get("raster_backward", [np.nan])))
+    dom, dom_ms, dom_b = ("raster_backward", k_bwd, bwd_b) if k_bwd >= k_fwd else \
+        ("raster_composite", k_fwd, fwd_b)
+    achieved = dom_b / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get(dom)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256; random target image)",
+        "config": {"workload": WORKLOAD, "regime": args.regime, "resolution": [w, h],
+                   "voxels": ds.n, "parallelism": f"sensor-sharded x{world}, grad all-reduce (NCCL)",
+                   "l2": "flushed (256 MB write) between timed steps", "render_instances": n_inst,
+                   "visible_voxels": m_vis},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(gt_host.nbytes),
+                "d2h_bytes_per_step": int(out_host.nbytes + loss_host.nbytes)},
+        "gpu_launches": ours if ours is not None else launches,
+        "gpu_launches_all": launches,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes": dom_b, "kernel_ms": dom_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+        "kernels_ms": {k: float(np.mean(v)) for k, v in kms.items()},
+        "clocks": clk,
+    }
+    if not args.no_extras and world == 1:
+        line["extras"] = extras(ds, args)
+    if not args.no_cpu and world == 1:
+        base = CpuBaseline(args.regime)
+        v, info = base.sample(7)
+        base.close()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": base.workers, "kind": "port",
+                                "sample": f"{base.workers} random 16x16 tiles of 8160 (fwd+bwd), "
+                                          f"{info['wall_s']:.1f} s wall, extrapolated to the frame"}
+    print(json.dumps(line), flush=True)
+
+
+def extras(ds, args):
+    """Secondary configurations on rank 0: C2 forward only, C3 LiDAR, C4 fisheye, surface regime."""
+    import torch
+    from paper_2507_18713_b200 import configs
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.scenes import get_scene
+    from paper_2507_18713_b200.sensors import camera_rays, gen_lidar_rays
+
+    def timeit(fn, n=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    out = {}
+    cam = configs.c2_camera()
+    out["c2_forward_fps"] = 1e3 / timeit(lambda: RR.rasterize(ds, cam))
+    scene = get_scene("S1M", args.regime)
+    oc = RY.build_scene_octrees(scene)
+    lidar = configs.c3_lidar()
+    lb = gen_lidar_rays(lidar)
+    ms = timeit(lambda: RY.integrate_rays(ds, oc, lb.origins, lb.dirs))
+    ms_gen = timeit(lambda: RY.integrate_rays(ds, oc, gen_lidar_rays(lidar).origins, lb.dirs))
+    rec = RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
+    out["c3_lidar"] = {"rays_per_s": lb.n / (ms * 1e-3), "sweeps_per_s": 1e3 / ms, "ms": ms,
+                       "ms_with_raygen": ms_gen, "rays": lb.n,
+                       "segments": int(rec.n_segments.sum().item()),
+                       "status_max": int(rec.status.max().item())}
+    s2 = get_scene("S2M", "init")
+    ds2 = DeviceScene.from_scene(s2)
+    oc2 = RY.build_scene_octrees(s2)
+    c4 = configs.c4_camera()
+
+    def c4_frame():
+        b = camera_rays(c4)
+        return RY.integrate_rays(ds2, oc2, b.origins, b.dirs, valid=b.valid)
+
+    out["c4_fisheye_rs_fps"] = 1e3 / timeit(c4_frame, n=5)
+    del ds2, oc2
+    sur = get_scene("S1M", "surface")
+    dss = DeviceScene.from_scene(sur)
+    ocs = RY.build_scene_octrees(sur)
+    out["surface_regime"] = {"voxels": dss.n,
+                             "c2_forward_fps": 1e3 / timeit(lambda: RR.rasterize(dss, cam)),
+                             "c3_sweeps_per_s": 1e3 / timeit(lambda: RY.integrate_rays(
+                                 dss, ocs, lb.origins, lb.dirs))}
+
+    def fb_step():
+        fb, st = RR.rasterize(dss, cam, return_state=True)
+        RR.rasterize_backward(st, torch.full((1080, 1920, 3), 1e-7, device=dss.device),
+                              torch.zeros((1080, 1920), device=dss.device), as_dict=False)
+
+    out["surface_regime"]["c2_fwd_bwd_fps"] = 1e3 / timeit(fb_step, n=5)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--regime", choices=["init", "surface"], default="init")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="skip the CUPTI launch count (under ncu)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = _dist_init(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

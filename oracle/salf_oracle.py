@@ -326,8 +326,12 @@ def project_voxels(vox: Voxels, cam: Camera, near=NEAR_PLANE):
     return rmin, rmax, zc, culled
 
 
-def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE):
-    """render_raster.py:143-182 -> (tiles_x, tiles_y, offsets int64[T+1], entries int64)."""
+def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE, window=None):
+    """render_raster.py:143-182 -> (tiles_x, tiles_y, offsets int64[T+1], entries int64).
+
+    `window=(tx0, ty0, tx1, ty1)` (inclusive tile rectangle) bins only those
+    tiles; their lists are identical to the full binning's (tiles are
+    independent), the others come out empty.  Used to time bounded samples."""
     rmin, rmax, zc, culled = project_voxels(vox, cam, near)
     tx_n = -(-cam.width // tile)
     ty_n = -(-cam.height // tile)
@@ -345,6 +349,13 @@ def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE):
     x1 = (u_hi[idx] // tile).astype(np.int64)
     y0 = (v_lo[idx] // tile).astype(np.int64)
     y1 = (v_hi[idx] // tile).astype(np.int64)
+    if window is not None:
+        x0, y0 = np.maximum(x0, window[0]), np.maximum(y0, window[1])
+        x1, y1 = np.minimum(x1, window[2]), np.minimum(y1, window[3])
+        k = (x0 <= x1) & (y0 <= y1)
+        idx, x0, x1, y0, y1 = idx[k], x0[k], x1[k], y0[k], y1[k]
+        if idx.size == 0:
+            return tx_n, ty_n, np.zeros(nt + 1, np.int64), np.zeros(0, np.int64)
     nx, ny = x1 - x0 + 1, y1 - y0 + 1
     cnt = nx * ny
     vid = np.repeat(idx, cnt)
@@ -385,22 +396,24 @@ def _pair_segments(vox: Voxels, origin, dirs, t_near, pix, vid):
 
 
 def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SIZE,
-              near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, rows=None):
+              near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, rows=None, window=None):
     """render_raster.py:201-301, tile by tile.
 
-    `rows=(r0, r1)` restricts work to tile rows r0..r1-1 (used by the CPU
-    baseline to time a bounded band; other pixels keep zero accumulators)."""
+    `rows=(r0, r1)` restricts work to tile rows r0..r1-1 and `window` to a
+    tile rectangle (bounded CPU-baseline samples; other pixels keep zero
+    accumulators)."""
     bg = np.asarray(background, np.float64)
     h, w = cam.height, cam.width
-    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near)
+    if rows is not None and window is None:
+        window = (0, rows[0], -(-w // tile) - 1, rows[1] - 1)
+    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window)
     dirs, t_near = _pixel_rays(cam, near)
     keep = 1.0 - stop_threshold
     acc_c = np.zeros((h * w, 3))
     acc_l = np.zeros(h * w)
     acc_w = np.zeros(h * w)
     acc_t = np.zeros(h * w)
-    r0, r1 = (0, ty_n) if rows is None else rows
-    for ty in range(r0, r1):
+    for ty in range(ty_n):
         for tx in range(tx_n):
             t = ty * tx_n + tx
             ent = entries[offsets[t]:offsets[t + 1]]
@@ -432,7 +445,7 @@ def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SI
 
 
 def raster_records(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SIZE,
-                   near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD):
+                   near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, window=None):
     """Raster pairs restated as ray-path records (one ray per pixel, row-major).
 
     The reference has no raster backward; its gradient is defined by
@@ -441,7 +454,7 @@ def raster_records(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TI
     (render_ray.py:86-114) and differentiated by `backward_records`
     (backward.py:35-101).  Misses carry alpha = 0 and drop out exactly."""
     h, w = cam.height, cam.width
-    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near)
+    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window)
     dirs, t_near = _pixel_rays(cam, near)
     chunks = []
     for t in range(tx_n * ty_n):

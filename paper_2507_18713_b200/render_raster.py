@@ -65,6 +65,16 @@ class RasterState:
     n_instances: int
 
 
+def _timed(events, name):
+    """Profiling hook: append (name, start, end) CUDA events around one launch."""
+    if events is None:
+        return None
+    e = (name, torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    e[1].record()
+    events.append(e)
+    return e
+
+
 def _require_pinhole(cam: CameraModel) -> None:
     if cam.kind != PINHOLE:
         raise ValueError(f"rasterizer supports pinhole cameras only, got {cam.kind!r}")
@@ -184,7 +194,7 @@ def _opts(background, near, stop_threshold, tile, exact_color) -> _lib.RasterOpt
 def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int = TILE_SIZE,
               near: float = NEAR_PLANE, stop_threshold: float = STOP_THRESHOLD,
               max_pairs: int = 4_000_000, exact_color: bool = False,
-              return_state: bool = False):
+              return_state: bool = False, events: list | None = None):
     """Per-pixel exact-intersection compositing over depth-sorted tile bins.
 
     `max_pairs` is accepted for signature compatibility (the reference's host
@@ -207,10 +217,13 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
     offsets, entries, n_inst, _ = _bin(ds, cam, near, tile, p, mode=1)
     opts = _opts(background, near, stop_threshold, tile, exact_color)
     sc, cs = ds.c_struct(), cam.c_struct(rolling=False)
+    ev = _timed(events, "raster_composite")
     _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
                                          offsets.data_ptr(), entries.data_ptr() if n_inst else offsets.data_ptr(),
                                          rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
                                          _lib.ptr(saved), _lib.stream_ptr()), "rasterize")
+    if ev is not None:
+        ev[2].record()
     fb = Framebuffer(rgb, op, depth)
     if return_state:
         return fb, RasterState(ds, cam, opts, offsets, entries, saved, n_inst)
@@ -225,7 +238,7 @@ def rasterize_scene(scene: Scene, cam: CameraModel, t_stamp: float = 0.0, *,
 
 
 def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor | None = None,
-                       as_dict: bool = True):
+                       as_dict: bool = True, events: list | None = None):
     """Per-voxel gradients of a rasterized frame.
 
     The reference has no raster backward; the gradient is the one
@@ -243,10 +256,13 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
         grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
     if state.n_instances:
         sc, cs = ds.c_struct(), state.cam.c_struct(rolling=False)
+        ev = _timed(events, "raster_backward")
         _lib.check(lib.salf_raster_backward(_lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts),
                                             state.offsets.data_ptr(), state.entries.data_ptr(),
                                             state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
                                             grad.data_ptr(), _lib.stream_ptr()), "rasterize_backward")
+        if ev is not None:
+            ev[2].record()
     if as_dict:
         return grads_to_dict(grad[: ds.n])
     return grad
