@@ -43,12 +43,13 @@ extern "C" {
 
 /* Device view of a flat voxel list (reference render_raster.py:44-60,
  * scene.py:82-223).  geo = (cx, cy, cz, edge) f64 with centres computed as
- * aabb_min + (ijk + 0.5) * edge; ab = (exp(log_a), exp(log_b)) f64;
- * prm = f32 fields (exact for salf.v1 scenes, whose params are f32 on disk). */
+ * aabb_min + (ijk + 0.5) * edge; aux = (a = exp(log_a), 1 / exp(log_b),
+ * 2 / edge, 0) f64; prm = f32 fields (exact for salf.v1 scenes, whose params
+ * are f32 on disk). */
 typedef struct {
   int64_t n;
   const double *geo;
-  const double *ab;
+  const double *aux;
   const float *prm;
   int32_t density_mode;
   int32_t pad;
@@ -130,7 +131,7 @@ int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double 
 
 /* rasterize (render_raster.py:201-301) over prebuilt render bins.
  * out_rgb (H*W*3), out_opacity, out_depth f32; saved (H*W*8 f64, nullable):
- * acc_rgb[3], acc_w, acc_wt, log_t_final, n_used, pad -- kept for the backward. */
+ * acc_rgb[3], acc_w, acc_wt, T_final, n_stop, pad -- kept for the backward. */
 int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                           const salf_raster_opts_t *opts, const int64_t *offsets,
                           const int32_t *entries, float *out_rgb, float *out_opacity,

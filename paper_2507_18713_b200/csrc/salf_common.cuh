@@ -95,21 +95,29 @@ __device__ __forceinline__ double eval_sdf(const VoxPrm &p, const double x[3]) {
   return __dadd_rn(__dadd_rn(__dadd_rn(p0, p2), p1), (double)p.ws[3]);
 }
 
-// sdf_to_density (scene.py:235-242) / raw exp (scene.py:250-252).
+// sdf_to_density (scene.py:235-242) / raw exp (scene.py:250-252), with the
+// per-voxel reciprocal 1/b precomputed (x * (1/b) vs x / b: <= 1 ulp).
 // Also returns e = exp(-|s|/b) for the backward.
-__device__ __forceinline__ double density(int mode, double s, double a, double b, double &e) {
+__device__ __forceinline__ double density(int mode, double s, double a, double inv_b, double &e) {
   if (mode == SALF_DENSITY_RAW) {
     e = 0.0;
     return exp(s);
   }
-  e = exp(__ddiv_rn(-fabs(s), b));
+  e = exp(__dmul_rn(-fabs(s), inv_b));
   double inner = __dadd_rn(1.0, __dmul_rn(npsign(s), __dsub_rn(1.0, e)));
   return __dmul_rn(__dmul_rn(0.5, a), inner);
 }
 
-// segment_opacity (scene.py:282-284).
-__device__ __forceinline__ double seg_alpha(double sigma, double delta) {
-  return npmin(-expm1(__dmul_rn(-sigma, delta)), kAlphaMax);
+// segment_opacity (scene.py:282-284) -> clamped alpha and its complement
+// 1 - alpha = exp(-sigma delta) from the same expm1 (no cancellation).
+__device__ __forceinline__ double seg_alpha(double sigma, double delta, double &one_minus) {
+  const double em = expm1(__dmul_rn(-sigma, delta));
+  const double a = -em;
+  if (a != a) { one_minus = a; return a; }
+  if (a >= kAlphaMax) { one_minus = 1.0 - kAlphaMax; return kAlphaMax; }
+  if (a <= 0.0) { one_minus = 1.0; return 0.0; }  // np.clip(alpha, 0, .) (alpha >= 0 anyway)
+  one_minus = __dadd_rn(1.0, em);
+  return a;
 }
 
 // eval_color (scene.py:270-279), fp64: z = W_c x + W_sh gamma, sigmoid.
@@ -166,40 +174,58 @@ __device__ __forceinline__ uint64_t order_key(double z) {
   return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// Transposed warp reduction of a 32-vector held by every lane: five xor
+// steps, each lane sending half of what it still holds (16 + 8 + 4 + 2 + 1 =
+// 31 shuffles instead of 32 x 5).  Afterwards lane l holds the warp sum of
+// component l in v[0].  PRECONDITION: all 32 lanes converged.
+__device__ __forceinline__ double warp_transpose_reduce(double v[32]) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const double send = upper ? v[i] : v[i + n / 2];
+      const double keep = upper ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(full, send, off);
+    }
+  }
+  return v[0];
+}
+
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes
-// of a converged warp.  Lanes holding the same voxel id form a group
-// (__match_any_sync); groups of >= 3 lanes are summed with full-warp xor
-// butterflies (non-members contribute 0) and their leader issues one set of
-// 27 atomics; lanes in smaller groups add directly.
+// of a converged warp.  Lanes holding the same voxel id form a group; a group
+// of >= 3 lanes is summed with one transposed reduction (31 fp64 shuffles)
+// after which lanes 0..26 each issue one coalesced atomic; lanes of smaller
+// groups add directly.
 __device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t vid, bool active,
                                              const double g[kGradStride]) {
   const unsigned full = 0xffffffffu;
-  const unsigned act = __ballot_sync(full, active);
-  if (!act) return;
+  unsigned pending = __ballot_sync(full, active);
+  if (!pending) return;
   const int lane = threadIdx.x & 31;
-  const long long key = active ? (long long)vid : -1ll - lane;
-  const unsigned grp = __match_any_sync(full, key);
-  const bool big = active && __popc(grp) >= 3;
-  if (active && !big) {
-    double *dst = grad + vid * kGradStride;
-#pragma unroll
-    for (int k = 0; k < kGradStride; ++k)
-      if (g[k] != 0.0) atomicAdd(dst + k, g[k]);
-  }
-  unsigned leaders = __ballot_sync(full, big && lane == __ffs(grp) - 1);
-  while (leaders) {
-    const int L = __ffs(leaders) - 1;
-    leaders &= leaders - 1;
+  const long long key = active ? (long long)vid : -1ll;
+  while (pending) {
+    const int L = __ffs(pending) - 1;
     const long long lkey = __shfl_sync(full, key, L);
-    const bool mem = big && key == lkey;
-    double *dst = grad + lkey * kGradStride;
-#pragma unroll 1
-    for (int k = 0; k < kGradStride; ++k) {
-      double v = mem ? g[k] : 0.0;
+    const bool mem = active && key == lkey;
+    const unsigned members = __ballot_sync(full, mem);
+    pending &= ~members;
+    if (__popc(members) <= 2) {
+      if (mem) {
+        double *dst = grad + lkey * kGradStride;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(full, v, off);
-      if (lane == L && v != 0.0) atomicAdd(dst + k, v);
+        for (int k = 0; k < kGradStride; ++k)
+          if (g[k] != 0.0) atomicAdd(dst + k, g[k]);
+      }
+      continue;
     }
+    double v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = (mem && k < kGradStride) ? g[k] : 0.0;
+    const double tot = warp_transpose_reduce(v);
+    if (lane < kGradStride && tot != 0.0) atomicAdd(grad + lkey * kGradStride + lane, tot);
   }
 }
 

@@ -211,6 +211,7 @@ struct Entry {
   double lo[3];  // (-half) - o
   double hi[3];  //   half  - o
   double half;   // 0.5 * edge
+  double inv_half;
   int64_t vid;
 };
 
@@ -263,23 +264,26 @@ __device__ __forceinline__ bool pair_hit(const PixelRay &r, const Entry &e, doub
 }
 
 struct SegVals {
-  double tm, delta, x[3], s, e, sigma, alpha, c[3], a, b;
+  double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
 };
 
+// Fields of one hit pair (render_raster.py:239-253).  Divisions by 0.5*edge
+// and by b are multiplications by precomputed reciprocals (<= 1 ulp).
 template <bool kExactColor>
 __device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const PixelRay &r, const Entry &e,
-                                           double t0, double t1, SegVals &sv, VoxPrm &p) {
+                                           double t0, double t1, SegVals &sv) {
   sv.delta = __dsub_rn(t1, t0);
   sv.tm = __dmul_rn(0.5, __dadd_rn(t0, t1));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) sv.x[k] = __ddiv_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, r.d[k])), e.half);
+  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, r.d[k])), e.inv_half);
+  VoxPrm p;
   load_prm(sc.prm, e.vid, p);
-  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.ab) + e.vid);
+  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.aux + 4 * e.vid));
   sv.a = ab.x;
-  sv.b = ab.y;
+  sv.inv_b = ab.y;
   sv.s = eval_sdf(p, sv.x);
   sv.sigma = density(sc.density_mode, sv.s, ab.x, ab.y, sv.e);
-  sv.alpha = seg_alpha(sv.sigma, sv.delta);
+  sv.alpha = seg_alpha(sv.sigma, sv.delta, sv.om);
   if (kExactColor) eval_color64(p, sv.x, r.d, sv.c);
   else eval_color32(p, sv.x, r.d, sv.c);
 }
@@ -289,6 +293,7 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
   const double4 g = ldg_d4(sc.geo + 4 * (int64_t)vid);
   e.vid = vid;
   e.half = __dmul_rn(0.5, g.w);
+  e.inv_half = 1.0 / e.half;
   e.o[0] = __dsub_rn(c.pos[0], g.x);
   e.o[1] = __dsub_rn(c.pos[1], g.y);
   e.o[2] = __dsub_rn(c.pos[2], g.z);
@@ -318,7 +323,9 @@ __global__ void __launch_bounds__(256) k_composite(salf_scene_t sc, PinholeDev c
 
   PixelRay r;
   if (inside) pixel_ray(c, px, py, r);
-  double acc_c[3] = {0.0, 0.0, 0.0}, acc_l = 0.0, acc_w = 0.0, acc_wt = 0.0, log_t = 0.0;
+  // transmittance kept as a running product of (1 - alpha) (the reference's
+  // exp(cumsum(log1p(-alpha))), render_raster.py:258-274, to ~1e-15)
+  double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0;
   bool alive = inside;
   int64_t n_stop = end - beg;
   const int nthreads = blockDim.x;
@@ -333,40 +340,34 @@ __global__ void __launch_bounds__(256) k_composite(salf_scene_t sc, PinholeDev c
         double t0, t1;
         if (!pair_hit(r, sm[j], t0, t1)) continue;
         SegVals sv;
-        VoxPrm p;
-        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv, p);
-        const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
-        const double lg = log1p(-a);
-        const double tb = exp(log_t);
-        if (tb > keep) {
-          const double w = __dmul_rn(tb, a);
+        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv);
+        if (T > keep) {  // included iff T_before > 1 - stop_threshold
+          const double w = __dmul_rn(T, sv.alpha);
 #pragma unroll
           for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
-          acc_l = __dadd_rn(acc_l, lg);
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
+          T = __dmul_rn(T, sv.om);
         } else {
           alive = false;
           n_stop = base - beg + j;
           break;
         }
-        log_t = __dadd_rn(log_t, lg);
       }
     }
     if (!__syncthreads_or(alive)) break;
   }
   if (!inside) return;
   const int64_t pix = (int64_t)py * c.width + px;
-  const double t_fin = exp(acc_l);
 #pragma unroll
   for (int k = 0; k < 3; ++k)
-    out_rgb[pix * 3 + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(t_fin, opt.background[k]));
-  out_op[pix] = (float)__dsub_rn(1.0, t_fin);
+    out_rgb[pix * 3 + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(T, opt.background[k]));
+  out_op[pix] = (float)__dsub_rn(1.0, T);
   out_depth[pix] = acc_w > kDepthWeightMin ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
   if (saved) {
     double *s = saved + pix * SALF_SAVED_STRIDE;
     s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
-    s[3] = acc_w; s[4] = acc_wt; s[5] = acc_l; s[6] = (double)n_stop; s[7] = 0.0;
+    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_stop; s[7] = 0.0;
   }
 }
 
@@ -378,10 +379,12 @@ __device__ __forceinline__ void segment_grad(int mode, const SegVals &sv, const 
                                              double tb, double a_cl, double w, double suffix, double tail,
                                              const double dC[3], double g[kGradStride]) {
   const double g_alpha = __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, a_cl)));
-  const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta), exp(__dmul_rn(-sv.sigma, sv.delta)));
+  // exp(-sigma delta) = 1 - alpha (unclamped) from the forward's expm1
+  const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta), sv.alpha >= kAlphaMax ?
+                                   exp(__dmul_rn(-sv.sigma, sv.delta)) : sv.om);
   double ds;
   if (mode == SALF_DENSITY_SDF) {
-    const double k2 = __ddiv_rn(sv.a, __dmul_rn(2.0, sv.b));
+    const double k2 = __dmul_rn(__dmul_rn(sv.a, 0.5), sv.inv_b);
     ds = (sv.s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), sv.e);
     g[25] = __dmul_rn(g_sigma, sv.sigma);
     g[26] = __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, sv.s), sv.e));
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(256) k_backward(salf_scene_t sc, PinholeDev c,
   const int nthreads = blockDim.x;
 
   PixelRay r;
-  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, log_t = 0.0;
+  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, T = 1.0;
   int64_t n_stop = 0;
   if (inside) {
     pixel_ray(c, px, py, r);
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(256) k_backward(salf_scene_t sc, PinholeDev c,
     // tail = (dC . background) * T_final  (backward.py:62)
     tail = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], opt.background[0]), __dmul_rn(dC[2], opt.background[2])),
                                __dmul_rn(dC[1], opt.background[1])),
-                     exp(s[5]));
+                     s[5]);
     n_stop = (int64_t)s[6];
   }
   int64_t max_stop = n_stop;
@@ -463,23 +466,19 @@ __global__ void __launch_bounds__(256) k_backward(salf_scene_t sc, PinholeDev c,
       double t0, t1;
       if (inside && jj < n_stop && pair_hit(r, sm[j], t0, t1)) {
         SegVals sv;
-        VoxPrm p;
-        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv, p);
-        const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
-        const double lg = log1p(-a);
-        const double tb = exp(log_t);
-        if (tb > keep) {
-          const double w = __dmul_rn(tb, a);
+        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv);
+        if (T > keep) {
+          const double w = __dmul_rn(T, sv.alpha);
           // A = dC . c + dD (t_mid - D) / ws   (backward.py:52-59, einsum order (0+2)+1)
           const double A = __dadd_rn(
               __dadd_rn(__dadd_rn(__dmul_rn(dC[0], sv.c[0]), __dmul_rn(dC[2], sv.c[2])), __dmul_rn(dC[1], sv.c[1])),
               __ddiv_rn(__dmul_rn(dd, __dsub_rn(sv.tm, D)), ws));
           prefix = __dadd_rn(prefix, __dmul_rn(A, w));
           const double suffix = __dsub_rn(total, prefix);
-          segment_grad(sc.density_mode, sv, r.d, A, tb, a, w, suffix, tail, dC, g);
+          segment_grad(sc.density_mode, sv, r.d, A, T, sv.alpha, w, suffix, tail, dC, g);
           act = true;
+          T = __dmul_rn(T, sv.om);
         }
-        log_t = __dadd_rn(log_t, lg);
       }
       scatter_grad(grad, vid, act, g);
     }

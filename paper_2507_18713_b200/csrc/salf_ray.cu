@@ -119,7 +119,7 @@ struct Marcher {
 };
 
 struct RaySeg {
-  double tm, delta, x[3], s, e, sigma, alpha, c[3], a, b;
+  double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
 };
 
 // _evaluate_geometry (render_ray.py:117-133) + eval_color for one segment.
@@ -129,18 +129,18 @@ __device__ __forceinline__ void shade_seg(const salf_scene_t &sc, const Marcher 
   sv.tm = __dmul_rn(0.5, __dadd_rn(s0, s1));
   sv.delta = __dsub_rn(s1, s0);
   const double4 g = ldg_d4(sc.geo + 4 * vid);
+  const double4 ax = ldg_d4(sc.aux + 4 * vid);  // (a, 1/b, 2/edge, 0)
   const double ctr[3] = {g.x, g.y, g.z};
-  const double sc2 = __ddiv_rn(2.0, g.w);
+  // world_to_local: (p - centre) * (2.0 / edge)  (scene.py:196-209)
 #pragma unroll
-  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(sv.tm, m.d[k])), ctr[k]), sc2);
+  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(sv.tm, m.d[k])), ctr[k]), ax.z);
   VoxPrm p;
   load_prm(sc.prm, vid, p);
-  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.ab) + vid);
-  sv.a = ab.x;
-  sv.b = ab.y;
+  sv.a = ax.x;
+  sv.inv_b = ax.y;
   sv.s = eval_sdf(p, sv.x);
-  sv.sigma = density(sc.density_mode, sv.s, ab.x, ab.y, sv.e);
-  sv.alpha = seg_alpha(sv.sigma, sv.delta);
+  sv.sigma = density(sc.density_mode, sv.s, ax.x, ax.y, sv.e);
+  sv.alpha = seg_alpha(sv.sigma, sv.delta, sv.om);
   if (want_color) {
     if (kExactColor) eval_color64(p, sv.x, m.d, sv.c);
     else eval_color32(p, sv.x, m.d, sv.c);
@@ -189,7 +189,7 @@ __global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, co
     if (early_stop) {
       RaySeg sv;
       shade_seg<true>(sc, m, vid, s0, s1, sv, false);
-      t_run = __dmul_rn(t_run, __dsub_rn(1.0, npmin(npmax(sv.alpha, 0.0), kAlphaMax)));
+      t_run = __dmul_rn(t_run, __dsub_rn(1.0, sv.alpha));
       if (t_run <= keep) break;
     }
   }
@@ -208,8 +208,7 @@ __global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, 
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double keep = 1.0 - opt.stop_threshold;
-  double acc_c[3] = {0.0, 0.0, 0.0}, acc_l = 0.0, acc_w = 0.0, acc_wt = 0.0, log_t = 0.0, t_run = 1.0,
-         last_t0 = -INFINITY;
+  double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0, t_run = 1.0, last_t0 = -INFINITY;
   int64_t n_seg = 0;
   int32_t st = 0;
   const bool ok = valid ? valid[i] != 0 : true;
@@ -226,28 +225,25 @@ __global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, 
       ++n_seg;
       RaySeg sv;
       shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen);
-      const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
       if (!frozen) {
-        const double tb = exp(log_t);
-        if (tb > keep) {
-          const double w = __dmul_rn(tb, a);
+        if (T > keep) {  // included iff T_before > 1 - stop_threshold (render_ray.py:97-99)
+          const double w = __dmul_rn(T, sv.alpha);
 #pragma unroll
           for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
-          acc_l = __dadd_rn(acc_l, log1p(-a));
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
+          T = __dmul_rn(T, sv.om);
         } else {
           frozen = true;
         }
-        log_t = __dadd_rn(log_t, log1p(-a));
       }
       // product-based early stop on the march (render_ray.py:154-157)
-      t_run = __dmul_rn(t_run, __dsub_rn(1.0, a));
+      t_run = __dmul_rn(t_run, __dsub_rn(1.0, sv.alpha));
       if (t_run <= keep) break;
     }
   }
   if (ok) {
-    const double t_fin = exp(acc_l);
+    const double t_fin = T;
 #pragma unroll
     for (int k = 0; k < 3; ++k) out_rgb[3 * i + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(t_fin, opt.background[k]));
     out_op[i] = (float)__dsub_rn(1.0, t_fin);
@@ -261,7 +257,7 @@ __global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, 
   if (saved) {
     double *s = saved + i * SALF_SAVED_STRIDE;
     s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
-    s[3] = acc_w; s[4] = acc_wt; s[5] = acc_l; s[6] = (double)n_seg; s[7] = 0.0;
+    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_seg; s[7] = 0.0;
   }
   if (status) status[i] = st;
 }
@@ -278,7 +274,7 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
   const double keep = 1.0 - opt.stop_threshold;
   bool live = i < n && (valid ? valid[i] != 0 : true);
   Marcher m;
-  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, log_t = 0.0,
+  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, T = 1.0,
          t_run = 1.0;
   if (live) {
     m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY);
@@ -293,7 +289,7 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
                       __ddiv_rn(__dmul_rn(dd, __dsub_rn(acc_wt, __dmul_rn(D, acc_w))), ws));
     tail = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], opt.background[0]), __dmul_rn(dC[2], opt.background[2])),
                                __dmul_rn(dC[1], opt.background[1])),
-                     exp(s[5]));
+                     s[5]);
     live = m.active && (dC[0] != 0.0 || dC[1] != 0.0 || dC[2] != 0.0 || dd != 0.0);
   }
   int32_t st = 0;
@@ -306,8 +302,8 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
       if (m.step(t, vid, s0, s1, st)) {
         RaySeg sv;
         shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, true);
-        const double a = npmin(npmax(sv.alpha, 0.0), kAlphaMax);
-        const double tb = exp(log_t);
+        const double a = sv.alpha;
+        const double tb = T;
         if (tb > keep) {
           const double w = __dmul_rn(tb, a);
           const double A = __dadd_rn(
@@ -317,10 +313,11 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
           const double suffix = __dsub_rn(total, prefix);
           const double g_alpha =
               __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, a)));
-          const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta), exp(__dmul_rn(-sv.sigma, sv.delta)));
+          const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta),
+                                           a >= kAlphaMax ? exp(__dmul_rn(-sv.sigma, sv.delta)) : sv.om);
           double ds;
           if (sc.density_mode == SALF_DENSITY_SDF) {
-            const double k2 = __ddiv_rn(sv.a, __dmul_rn(2.0, sv.b));
+            const double k2 = __dmul_rn(__dmul_rn(sv.a, 0.5), sv.inv_b);
             ds = (sv.s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), sv.e);
             g[25] = __dmul_rn(g_sigma, sv.sigma);
             g[26] = __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, sv.s), sv.e));
@@ -341,7 +338,7 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
             for (int j = 0; j < 4; ++j) g[13 + 4 * c + j] = __dmul_rn(gz, gam[j]);
           }
           act = true;
-          log_t = __dadd_rn(log_t, log1p(-a));
+          T = __dmul_rn(T, sv.om);
           t_run = __dmul_rn(t_run, __dsub_rn(1.0, a));
           if (t_run <= keep) live = false;
         } else {

@@ -2,7 +2,7 @@
 
 Per voxel (SoA of AoS blocks, all 16-byte aligned):
   geo  double4  (cx, cy, cz, edge)           32 B  projection, slab tests, local coords
-  ab   double2  (a = exp(log_a), b = exp(log_b)) 16 B  density transfer
+  aux  double4  (a = exp(log_a), 1/b, 2/edge, 0)  32 B  density transfer, local coords
   prm  float[28] w_s[4] w_c[9] w_sh[12] pad[3] 112 B  field parameters (7 x 16-B loads)
 Centres, edges and exp(log a|b) are computed on the host with NumPy exactly as
 the reference does (scene.py:186-194, :249), so the kernels start from the
@@ -30,7 +30,11 @@ class DeviceScene:
         geo = np.empty((flat.n, 4), np.float64)
         geo[:, :3] = flat.centers
         geo[:, 3] = flat.edges
-        ab = np.stack([np.exp(flat.log_a), np.exp(flat.log_b)], axis=1) if flat.n else np.zeros((0, 2))
+        aux = np.zeros((flat.n, 4), np.float64)
+        if flat.n:
+            aux[:, 0] = np.exp(flat.log_a)
+            aux[:, 1] = 1.0 / np.exp(flat.log_b)
+            aux[:, 2] = 2.0 / flat.edges  # world_to_local scale (scene.py:209)
         prm = np.zeros((flat.n, _lib.PRM_STRIDE), np.float32)
         prm[:, 0:4] = flat.w_s.reshape(-1, 4)
         prm[:, 4:13] = flat.w_c.reshape(-1, 9)
@@ -38,7 +42,7 @@ class DeviceScene:
         # keep at least one element so data pointers are valid for empty scenes
         pad = lambda a: a if a.shape[0] else np.zeros((1,) + a.shape[1:], a.dtype)
         self.geo = torch.as_tensor(pad(geo), device=self.device).contiguous()
-        self.ab = torch.as_tensor(pad(np.ascontiguousarray(ab)), device=self.device).contiguous()
+        self.aux = torch.as_tensor(pad(aux), device=self.device).contiguous()
         self.prm = torch.as_tensor(pad(prm), device=self.device).contiguous()
         self.flat = flat
 
@@ -49,13 +53,13 @@ class DeviceScene:
     def c_struct(self) -> _lib.SceneT:
         s = _lib.SceneT()
         s.n = self.n
-        s.geo, s.ab, s.prm = self.geo.data_ptr(), self.ab.data_ptr(), self.prm.data_ptr()
+        s.geo, s.aux, s.prm = self.geo.data_ptr(), self.aux.data_ptr(), self.prm.data_ptr()
         s.density_mode = _lib.DENSITY[self.density_mode]
         return s
 
     @property
     def nbytes(self) -> int:
-        return int(self.geo.nbytes + self.ab.nbytes + self.prm.nbytes)
+        return int(self.geo.nbytes + self.aux.nbytes + self.prm.nbytes)
 
 
 def as_device_scene(obj, device=None) -> DeviceScene:

@@ -45,7 +45,7 @@ class RenderRecords:
     out_color: torch.Tensor  # (R, 3) f32
     opacity: torch.Tensor  # (R,) f32
     depth: torch.Tensor  # (R,) f32, NaN = no return
-    saved: torch.Tensor  # (R, 8) f64: acc_rgb[3], w_sum, w_t, log_T, n_seg, 0
+    saved: torch.Tensor  # (R, 8) f64: acc_rgb[3], w_sum, w_t, T_final, n_seg, 0
     status: torch.Tensor  # (R,) int32: 1 round cap, 2 outside root, 4 entry-order
     origins: torch.Tensor
     dirs: torch.Tensor
@@ -61,7 +61,7 @@ class RenderRecords:
 
     @property
     def t_final(self) -> torch.Tensor:
-        return torch.exp(self.saved[:, 5])
+        return self.saved[:, 5]
 
     @property
     def n_segments(self) -> torch.Tensor:
