@@ -18,6 +18,7 @@ struct OctDev {
   const int32_t *nodes;
   double rmin[3], rmax[3];
   double root_edge;
+  int max_depth;
 };
 
 static OctDev make_oct(const salf_octree_t *t) {
@@ -28,6 +29,7 @@ static OctDev make_oct(const salf_octree_t *t) {
     o.rmax[k] = t->root_min[k] + t->root_edge;  // buffer.root_min + buffer.root_edge (octree.py:232)
   }
   o.root_edge = t->root_edge;
+  o.max_depth = t->max_depth;
   return o;
 }
 
@@ -62,22 +64,157 @@ __device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3
   return w;
 }
 
+// Slab test with precomputed reciprocals (1.0 / d is IEEE-exact, so caching
+// it per ray changes nothing).  NumPy semantics incl. the zero-direction rule.
+__device__ __forceinline__ void ray_box_inv(const double o[3], const double d[3], const double inv[3],
+                                            const double bmin[3], const double bmax[3], double &t_in,
+                                            double &t_out) {
+  double ti = 0.0, to = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double nk, fk;
+    if (d[k] == 0.0) {
+      const bool inside = (o[k] >= bmin[k]) && (o[k] <= bmax[k]);
+      nk = inside ? -INFINITY : INFINITY;
+      fk = inside ? INFINITY : -INFINITY;
+    } else {
+      const double ta = __dmul_rn(__dsub_rn(bmin[k], o[k]), inv[k]);
+      const double tb = __dmul_rn(__dsub_rn(bmax[k], o[k]), inv[k]);
+      nk = npmin(ta, tb);
+      fk = npmax(ta, tb);
+    }
+    if (k == 0) { ti = nk; to = fk; } else { ti = npmax(ti, nk); to = npmin(to, fk); }
+  }
+  t_in = ti;
+  t_out = to;
+}
+
+// Exit distance only (the `far` of ray_box_range, octree.py:209-211).
+__device__ __forceinline__ double ray_box_far(const double o[3], const double d[3], const double inv[3],
+                                              const double bmin[3], const double bmax[3]) {
+  double to = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double fk;
+    if (d[k] == 0.0) {
+      fk = ((o[k] >= bmin[k]) && (o[k] <= bmax[k])) ? INFINITY : -INFINITY;
+    } else {
+      fk = npmax(__dmul_rn(__dsub_rn(bmin[k], o[k]), inv[k]), __dmul_rn(__dsub_rn(bmax[k], o[k]), inv[k]));
+    }
+    to = (k == 0) ? fk : npmin(to, fk);
+  }
+  return to;
+}
+
+constexpr int kPathCache = 24;  // tree depths up to this use the ancestor cache
+
 // Per-ray marcher state (BatchMarch, octree.py:222-273).
+//
+// Descent: the reference's per-level octant test (u >= 0.5, u <- 2u - bit,
+// octree.py:158-163) is exact arithmetic, so the bit at level k equals bit
+// (D-1-k) of floor(u * 2^D) (u = 1 -> all ones, as the iteration gives).  A
+// round therefore derives the whole root-to-leaf path from three integers,
+// resumes from the deepest ancestor it shares with the previous round's path
+// (node words cached per level), and only loads the levels below it.  The
+// node corner is re-accumulated level by level exactly as the reference
+// does (corner += bit * edge), so corners, exits and segments are unchanged.
 struct Marcher {
-  double o[3], d[3], t_max, t_cur, t_end;
+  double o[3], d[3], inv[3], t_max, t_cur, t_end;
   bool active;
   int rounds;
+  int depth_bits;    // D
+  int cached;        // levels 0..cached valid in words[]; -1 = empty
+  uint32_t cix, ciy, ciz;
+  int32_t *words;  // kPathCache + 1 per-level node words (thread-local array)
 
-  __device__ void init(const OctDev &t, const double *orig, const double *dir, double tmax) {
+  __device__ void init(const OctDev &t, const double *orig, const double *dir, double tmax, int max_depth,
+                       int32_t *word_cache) {
+    words = word_cache;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { o[k] = orig[k]; d[k] = dir[k]; }
+    for (int k = 0; k < 3; ++k) {
+      o[k] = orig[k];
+      d[k] = dir[k];
+      inv[k] = 1.0 / d[k];
+    }
     t_max = tmax;
     double t_in, t_out;
-    ray_box(o, d, t.rmin, t.rmax, t_in, t_out);
+    ray_box_inv(o, d, inv, t.rmin, t.rmax, t_in, t_out);
     t_cur = npmax(t_in, 0.0);
     t_end = npmin(t_out, t_max);
     active = (t_out > t_cur) && (t_cur < t_max) && isfinite(t_cur);
     rounds = 0;
+    depth_bits = max_depth;
+    cached = -1;
+    cix = ciy = ciz = 0;
+  }
+
+  __device__ __forceinline__ int32_t descend(const OctDev &t, const double p[3], double corner[3], double &edge,
+                                             bool &outside) {
+    double u[3];
+    outside = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      u[k] = __ddiv_rn(__dsub_rn(p[k], t.rmin[k]), t.root_edge);
+      if (u[k] < -1e-9 || u[k] > 1.0 + 1e-9) outside = true;
+      u[k] = npmin(npmax(u[k], 0.0), 1.0);
+    }
+    const int D = depth_bits;
+    if (D > kPathCache || u[0] != u[0] || u[1] != u[1] || u[2] != u[2]) {
+      // generic path (deep trees / NaN cursor): the reference iteration verbatim
+      edge = t.root_edge;
+      corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
+      int32_t w = __ldg(t.nodes);
+      while (w >= 0) {
+        const int b0 = u[0] >= 0.5, b1 = u[1] >= 0.5, b2 = u[2] >= 0.5;
+        edge = __dmul_rn(edge, 0.5);
+        corner[0] = __dadd_rn(corner[0], b0 ? edge : 0.0);
+        corner[1] = __dadd_rn(corner[1], b1 ? edge : 0.0);
+        corner[2] = __dadd_rn(corner[2], b2 ? edge : 0.0);
+        u[0] = __dsub_rn(__dmul_rn(2.0, u[0]), (double)b0);
+        u[1] = __dsub_rn(__dmul_rn(2.0, u[1]), (double)b1);
+        u[2] = __dsub_rn(__dmul_rn(2.0, u[2]), (double)b2);
+        w = __ldg(t.nodes + w + b0 + 2 * b1 + 4 * b2);
+      }
+      cached = -1;
+      return w;
+    }
+    const uint32_t full = (D >= 32) ? 0xffffffffu : ((1u << D) - 1u);
+    const double scale = ldexp(1.0, D);
+    const uint32_t ix = u[0] >= 1.0 ? full : (uint32_t)(u[0] * scale);
+    const uint32_t iy = u[1] >= 1.0 ? full : (uint32_t)(u[1] * scale);
+    const uint32_t iz = u[2] >= 1.0 ? full : (uint32_t)(u[2] * scale);
+    // deepest shared level with the cached path
+    int L = 0;
+    int32_t w;
+    if (cached >= 0) {
+      const uint32_t diff = (ix ^ cix) | (iy ^ ciy) | (iz ^ ciz);
+      const int same = diff ? (__clz(diff) - (32 - D)) : D;  // leading equal bits = shared levels
+      L = min(same, cached);
+      w = words[L];
+    } else {
+      w = __ldg(t.nodes);
+      words[0] = w;
+    }
+    while (w >= 0) {
+      const int sh = D - 1 - L;
+      const int c = ((ix >> sh) & 1) | (((iy >> sh) & 1) << 1) | (((iz >> sh) & 1) << 2);
+      w = __ldg(t.nodes + w + c);
+      ++L;
+      words[L] = w;
+    }
+    cached = L;
+    cix = ix; ciy = iy; ciz = iz;
+    // corner accumulation in the reference's order (octree.py:161-162)
+    edge = t.root_edge;
+    corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
+    for (int k = 0; k < L; ++k) {
+      const int sh = D - 1 - k;
+      edge = __dmul_rn(edge, 0.5);
+      corner[0] = __dadd_rn(corner[0], ((ix >> sh) & 1) ? edge : 0.0);
+      corner[1] = __dadd_rn(corner[1], ((iy >> sh) & 1) ? edge : 0.0);
+      corner[2] = __dadd_rn(corner[2], ((iz >> sh) & 1) ? edge : 0.0);
+    }
+    return w;
   }
 
   // One round; returns true and (vid, s0, s1) when a kept leaf segment was found.
@@ -91,7 +228,7 @@ struct Marcher {
 #pragma unroll
     for (int k = 0; k < 3; ++k) p[k] = __dadd_rn(o[k], __dmul_rn(t_cur, d[k]));
     bool outside;
-    const int32_t w = query_point(t, p, corner, edge, outside);
+    const int32_t w = descend(t, p, corner, edge, outside);
     if (outside) {
       status |= kStatusOutsideRoot;
       active = false;
@@ -99,13 +236,12 @@ struct Marcher {
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) cmax[k] = __dadd_rn(corner[k], edge);
-    double ti, far;
-    ray_box(p, d, corner, cmax, ti, far);
+    const double far = ray_box_far(p, d, inv, corner, cmax);
     t_cur = __dadd_rn(t_cur, __dadd_rn(npmax(far, 0.0), kEpsAdvance));
     bool got = false;
     if (w <= -2) {
       double a_in, a_out;
-      ray_box(o, d, corner, cmax, a_in, a_out);
+      ray_box_inv(o, d, inv, corner, cmax, a_in, a_out);
       s0 = npmax(a_in, 0.0);
       s1 = npmin(a_out, t_max);
       if (s1 > __dadd_rn(s0, 1e-12)) {
@@ -172,7 +308,8 @@ __global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, co
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Marcher m;
-  m.init(t, orig + 3 * i, dirs + 3 * i, tmax ? tmax[i] : INFINITY);
+  int32_t wc[kPathCache + 1];
+  m.init(t, orig + 3 * i, dirs + 3 * i, tmax ? tmax[i] : INFINITY, t.max_depth, wc);
   int64_t k = 0, off = starts ? starts[i] : 0;
   int32_t st = 0;
   double t_run = 1.0;
@@ -214,7 +351,8 @@ __global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, 
   const bool ok = valid ? valid[i] != 0 : true;
   if (ok) {
     Marcher m;
-    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY);
+    int32_t wc[kPathCache + 1];
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth, wc);
     bool frozen = false;
     while (m.active) {
       int64_t vid;
@@ -274,10 +412,12 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
   const double keep = 1.0 - opt.stop_threshold;
   bool live = i < n && (valid ? valid[i] != 0 : true);
   Marcher m;
+  int32_t wc[kPathCache + 1];
+  m.active = false;
   double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, T = 1.0,
          t_run = 1.0;
   if (live) {
-    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY);
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth, wc);
     const double *s = saved + i * SALF_SAVED_STRIDE;
     for (int k = 0; k < 3; ++k) dC[k] = d_rgb[3 * i + k];
     const double acc_w = s[3], acc_wt = s[4];
