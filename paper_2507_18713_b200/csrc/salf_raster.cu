@@ -307,7 +307,7 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
 constexpr int kChunk = 128;
 
 template <bool kExactColor>
-__global__ void __launch_bounds__(256) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+__global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                    const int64_t *__restrict__ offsets,
                                                    const int32_t *__restrict__ entries, float *__restrict__ out_rgb,
                                                    float *__restrict__ out_op, float *__restrict__ out_depth,
@@ -406,7 +406,7 @@ __device__ __forceinline__ void segment_grad(int mode, const SegVals &sv, const 
 }
 
 template <bool kExactColor>
-__global__ void __launch_bounds__(256) k_backward(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+__global__ void __launch_bounds__(256, 2) k_backward(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                   const int64_t *__restrict__ offsets,
                                                   const int32_t *__restrict__ entries,
                                                   const double *__restrict__ saved, const double *__restrict__ d_rgb,
