@@ -177,8 +177,10 @@ __device__ __forceinline__ uint64_t order_key(double z) {
 // Transposed warp reduction of a 32-vector held by every lane: five xor
 // steps, each lane sending half of what it still holds (16 + 8 + 4 + 2 + 1 =
 // 31 shuffles instead of 32 x 5).  Afterwards lane l holds the warp sum of
-// component l in v[0].  PRECONDITION: all 32 lanes converged.
-__device__ __forceinline__ double warp_transpose_reduce(double v[32]) {
+// component l.  fp32 partial sums (<= 32 terms; relative error ~1e-7 of the
+// warp's contribution) -- the global accumulation is fp64.
+// PRECONDITION: all 32 lanes converged.
+__device__ __forceinline__ float warp_transpose_reduce(float v[32]) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -186,8 +188,8 @@ __device__ __forceinline__ double warp_transpose_reduce(double v[32]) {
     const bool upper = (lane & off) != 0;
 #pragma unroll
     for (int i = 0; i < n / 2; ++i) {
-      const double send = upper ? v[i] : v[i + n / 2];
-      const double keep = upper ? v[i + n / 2] : v[i];
+      const float send = upper ? v[i] : v[i + n / 2];
+      const float keep = upper ? v[i + n / 2] : v[i];
       v[i] = keep + __shfl_xor_sync(full, send, off);
     }
   }
@@ -196,9 +198,9 @@ __device__ __forceinline__ double warp_transpose_reduce(double v[32]) {
 
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes
 // of a converged warp.  Lanes holding the same voxel id form a group; a group
-// of >= 3 lanes is summed with one transposed reduction (31 fp64 shuffles)
-// after which lanes 0..26 each issue one coalesced atomic; lanes of smaller
-// groups add directly.
+// of >= 3 lanes is summed with one transposed reduction, after which lanes
+// 0..26 each issue one coalesced fp64 atomic; lanes of smaller groups add
+// their fp64 values directly.
 __device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t vid, bool active,
                                              const double g[kGradStride]) {
   const unsigned full = 0xffffffffu;
@@ -221,11 +223,11 @@ __device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t 
       }
       continue;
     }
-    double v[32];
+    float v[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = (mem && k < kGradStride) ? g[k] : 0.0;
-    const double tot = warp_transpose_reduce(v);
-    if (lane < kGradStride && tot != 0.0) atomicAdd(grad + lkey * kGradStride + lane, tot);
+    for (int k = 0; k < 32; ++k) v[k] = (k < kGradStride && mem) ? (float)g[k] : 0.0f;
+    const float tot = warp_transpose_reduce(v);
+    if (lane < kGradStride && tot != 0.0f) atomicAdd(grad + lkey * kGradStride + lane, (double)tot);
   }
 }
 

@@ -218,6 +218,8 @@ struct Entry {
 struct PixelRay {
   double d[3], inv[3], t_near;
   bool zero[3];
+  bool pos[3];  // inv > 0: the slab's near face is the low face (no per-pair min/max)
+  bool fast;    // all components non-zero with finite reciprocals (no NaN can arise)
 };
 
 __device__ __forceinline__ void pixel_ray(const PinholeDev &c, int px, int py, PixelRay &r) {
@@ -232,15 +234,35 @@ __device__ __forceinline__ void pixel_ray(const PinholeDev &c, int px, int py, P
   for (int k = 0; k < 3; ++k) r.d[k] = mm_row(dc, c.rot, k);  // d_cam @ R.T
   const double dz = mm_col(r.d, c.rot, 2);                   // (dirs @ R)[:, 2]
   r.t_near = __ddiv_rn(c.near, dz);
+  r.fast = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     r.zero[k] = (r.d[k] == 0.0);
     r.inv[k] = 1.0 / r.d[k];
+    r.pos[k] = r.inv[k] > 0.0;
+    r.fast = r.fast && !r.zero[k] && isfinite(r.inv[k]);
   }
 }
 
+__device__ __forceinline__ double fmax_sel(double a, double b) { return a > b ? a : b; }
+__device__ __forceinline__ double fmin_sel(double a, double b) { return a < b ? a : b; }
+
 // slab test of a pixel ray against a staged entry -> (t0, t_out, hit)
 __device__ __forceinline__ bool pair_hit(const PixelRay &r, const Entry &e, double &t0, double &t1) {
+  if (r.fast) {
+    // lo < hi, so for inv > 0 the reference's min(ta, tb) is ta = lo * inv
+    // exactly (rounding is monotone) and max is tb; no NaN is possible.
+    const double n0 = __dmul_rn(r.pos[0] ? e.lo[0] : e.hi[0], r.inv[0]);
+    const double f0 = __dmul_rn(r.pos[0] ? e.hi[0] : e.lo[0], r.inv[0]);
+    const double n1 = __dmul_rn(r.pos[1] ? e.lo[1] : e.hi[1], r.inv[1]);
+    const double f1 = __dmul_rn(r.pos[1] ? e.hi[1] : e.lo[1], r.inv[1]);
+    const double n2 = __dmul_rn(r.pos[2] ? e.lo[2] : e.hi[2], r.inv[2]);
+    const double f2 = __dmul_rn(r.pos[2] ? e.hi[2] : e.lo[2], r.inv[2]);
+    const double ti = fmax_sel(fmax_sel(n0, n1), n2);
+    t1 = fmin_sel(fmin_sel(f0, f1), f2);
+    t0 = fmax_sel(fmax_sel(ti, r.t_near), 0.0);
+    return t1 > __dadd_rn(t0, 1e-12);
+  }
   double ti = 0.0, to = 0.0;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {

@@ -106,46 +106,81 @@ __device__ __forceinline__ double ray_box_far(const double o[3], const double d[
   return to;
 }
 
-constexpr int kPathCache = 24;  // tree depths up to this use the ancestor cache
+constexpr int kMaxBits = 30;  // trees up to this depth use the integer descent
 
 // Per-ray marcher state (BatchMarch, octree.py:222-273).
 //
 // Descent: the reference's per-level octant test (u >= 0.5, u <- 2u - bit,
 // octree.py:158-163) is exact arithmetic, so the bit at level k equals bit
 // (D-1-k) of floor(u * 2^D) (u = 1 -> all ones, as the iteration gives).  A
-// round therefore derives the whole root-to-leaf path from three integers,
-// resumes from the deepest ancestor it shares with the previous round's path
-// (node words cached per level), and only loads the levels below it.  The
-// node corner is re-accumulated level by level exactly as the reference
+// round derives its whole root-to-leaf path from three integers and resumes
+// from the parent or grandparent of the previous round's node when the new
+// path still passes through it (their node words and corners are kept in
+// registers); corners are accumulated level by level exactly as the reference
 // does (corner += bit * edge), so corners, exits and segments are unchanged.
 struct Marcher {
   double o[3], d[3], inv[3], t_max, t_cur, t_end;
-  bool active;
+  bool active, fast;
+  bool pos[3];
   int rounds;
-  int depth_bits;    // D
-  int cached;        // levels 0..cached valid in words[]; -1 = empty
+  int depth_bits;  // D
+  int pd;          // level of the previous round's node, -1 = none
   uint32_t cix, ciy, ciz;
-  int32_t *words;  // kPathCache + 1 per-level node words (thread-local array)
+  bool a1_ok, a2_ok;  // cached ancestors at levels pd-1, pd-2
+  int32_t a1_w, a2_w;
+  double a1_c[3], a2_c[3];
 
-  __device__ void init(const OctDev &t, const double *orig, const double *dir, double tmax, int max_depth,
-                       int32_t *word_cache) {
-    words = word_cache;
+  __device__ void init(const OctDev &t, const double *orig, const double *dir, double tmax, int max_depth) {
+    fast = true;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       o[k] = orig[k];
       d[k] = dir[k];
       inv[k] = 1.0 / d[k];
+      pos[k] = inv[k] > 0.0;
+      fast = fast && d[k] != 0.0 && isfinite(inv[k]);
     }
     t_max = tmax;
     double t_in, t_out;
-    ray_box_inv(o, d, inv, t.rmin, t.rmax, t_in, t_out);
+    box(o, t.rmin, t.rmax, t_in, t_out);
     t_cur = npmax(t_in, 0.0);
     t_end = npmin(t_out, t_max);
     active = (t_out > t_cur) && (t_cur < t_max) && isfinite(t_cur);
     rounds = 0;
     depth_bits = max_depth;
-    cached = -1;
-    cix = ciy = ciz = 0;
+    pd = -1;
+    a1_ok = a2_ok = false;
+  }
+
+  // ray_box_range for this ray (fast path: near face chosen by the sign of
+  // 1/d, no min/max per axis and no NaN possible)
+  __device__ __forceinline__ void box(const double p[3], const double bmin[3], const double bmax[3], double &t_in,
+                                      double &t_out) const {
+    if (fast) {
+      double n[3], f[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        n[k] = __dmul_rn(__dsub_rn(pos[k] ? bmin[k] : bmax[k], p[k]), inv[k]);
+        f[k] = __dmul_rn(__dsub_rn(pos[k] ? bmax[k] : bmin[k], p[k]), inv[k]);
+      }
+      const double a = n[0] > n[1] ? n[0] : n[1];
+      t_in = a > n[2] ? a : n[2];
+      const double b = f[0] < f[1] ? f[0] : f[1];
+      t_out = b < f[2] ? b : f[2];
+      return;
+    }
+    ray_box_inv(p, d, inv, bmin, bmax, t_in, t_out);
+  }
+
+  __device__ __forceinline__ double box_far(const double p[3], const double bmin[3], const double bmax[3]) const {
+    if (fast) {
+      double f[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) f[k] = __dmul_rn(__dsub_rn(pos[k] ? bmax[k] : bmin[k], p[k]), inv[k]);
+      const double b = f[0] < f[1] ? f[0] : f[1];
+      return b < f[2] ? b : f[2];
+    }
+    return ray_box_far(p, d, inv, bmin, bmax);
   }
 
   __device__ __forceinline__ int32_t descend(const OctDev &t, const double p[3], double corner[3], double &edge,
@@ -159,8 +194,8 @@ struct Marcher {
       u[k] = npmin(npmax(u[k], 0.0), 1.0);
     }
     const int D = depth_bits;
-    if (D > kPathCache || u[0] != u[0] || u[1] != u[1] || u[2] != u[2]) {
-      // generic path (deep trees / NaN cursor): the reference iteration verbatim
+    if (D > kMaxBits || u[0] != u[0] || u[1] != u[1] || u[2] != u[2]) {
+      // generic path (very deep trees / NaN cursor): the reference iteration verbatim
       edge = t.root_edge;
       corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
       int32_t w = __ldg(t.nodes);
@@ -175,44 +210,66 @@ struct Marcher {
         u[2] = __dsub_rn(__dmul_rn(2.0, u[2]), (double)b2);
         w = __ldg(t.nodes + w + b0 + 2 * b1 + 4 * b2);
       }
-      cached = -1;
+      pd = -1;
+      a1_ok = a2_ok = false;
       return w;
     }
-    const uint32_t full = (D >= 32) ? 0xffffffffu : ((1u << D) - 1u);
+    const uint32_t full = (1u << D) - 1u;
     const double scale = ldexp(1.0, D);
     const uint32_t ix = u[0] >= 1.0 ? full : (uint32_t)(u[0] * scale);
     const uint32_t iy = u[1] >= 1.0 ? full : (uint32_t)(u[1] * scale);
     const uint32_t iz = u[2] >= 1.0 ? full : (uint32_t)(u[2] * scale);
-    // deepest shared level with the cached path
-    int L = 0;
-    int32_t w;
-    if (cached >= 0) {
+    // resume point: deepest cached ancestor the new path still passes through
+    int same = 0;
+    if (pd >= 0) {
       const uint32_t diff = (ix ^ cix) | (iy ^ ciy) | (iz ^ ciz);
-      const int same = diff ? (__clz(diff) - (32 - D)) : D;  // leading equal bits = shared levels
-      L = min(same, cached);
-      w = words[L];
+      same = diff ? (__clz(diff) - (32 - D)) : D;
+    }
+    int L;
+    int32_t w;
+    bool h2_ok;  // history: node one level above the current one
+    int32_t h2_w;
+    double h2_c[3];
+    if (a1_ok && same >= pd - 1) {
+      L = pd - 1; w = a1_w;
+      corner[0] = a1_c[0]; corner[1] = a1_c[1]; corner[2] = a1_c[2];
+      h2_ok = a2_ok; h2_w = a2_w; h2_c[0] = a2_c[0]; h2_c[1] = a2_c[1]; h2_c[2] = a2_c[2];
+    } else if (a2_ok && same >= pd - 2) {
+      L = pd - 2; w = a2_w;
+      corner[0] = a2_c[0]; corner[1] = a2_c[1]; corner[2] = a2_c[2];
+      h2_ok = false; h2_w = 0; h2_c[0] = h2_c[1] = h2_c[2] = 0.0;
     } else {
-      w = __ldg(t.nodes);
-      words[0] = w;
+      L = 0; w = __ldg(t.nodes);
+      corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
+      h2_ok = false; h2_w = 0; h2_c[0] = h2_c[1] = h2_c[2] = 0.0;
     }
+    edge = ldexp(t.root_edge, -L);  // == root_edge * 0.5^L exactly
+    bool h1_ok = false;
+    int32_t h1_w = 0;
+    double h1_c[3] = {0.0, 0.0, 0.0};
     while (w >= 0) {
+      // node at level L is internal: it becomes the newest ancestor
+      h2_ok = h1_ok ? true : h2_ok;
+      if (h1_ok) { h2_w = h1_w; h2_c[0] = h1_c[0]; h2_c[1] = h1_c[1]; h2_c[2] = h1_c[2]; }
+      h1_ok = true; h1_w = w; h1_c[0] = corner[0]; h1_c[1] = corner[1]; h1_c[2] = corner[2];
       const int sh = D - 1 - L;
-      const int c = ((ix >> sh) & 1) | (((iy >> sh) & 1) << 1) | (((iz >> sh) & 1) << 2);
-      w = __ldg(t.nodes + w + c);
-      ++L;
-      words[L] = w;
-    }
-    cached = L;
-    cix = ix; ciy = iy; ciz = iz;
-    // corner accumulation in the reference's order (octree.py:161-162)
-    edge = t.root_edge;
-    corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
-    for (int k = 0; k < L; ++k) {
-      const int sh = D - 1 - k;
+      const int bx = (ix >> sh) & 1, by = (iy >> sh) & 1, bz = (iz >> sh) & 1;
       edge = __dmul_rn(edge, 0.5);
-      corner[0] = __dadd_rn(corner[0], ((ix >> sh) & 1) ? edge : 0.0);
-      corner[1] = __dadd_rn(corner[1], ((iy >> sh) & 1) ? edge : 0.0);
-      corner[2] = __dadd_rn(corner[2], ((iz >> sh) & 1) ? edge : 0.0);
+      if (bx) corner[0] = __dadd_rn(corner[0], edge);
+      if (by) corner[1] = __dadd_rn(corner[1], edge);
+      if (bz) corner[2] = __dadd_rn(corner[2], edge);
+      w = __ldg(t.nodes + w + bx + 2 * by + 4 * bz);
+      ++L;
+    }
+    // the returned node sits at level L; its parent is h1 (level L-1) unless
+    // we resumed at L itself (only possible at the root: L == 0)
+    pd = L;
+    cix = ix; ciy = iy; ciz = iz;
+    if (h1_ok) {
+      a1_ok = true; a1_w = h1_w; a1_c[0] = h1_c[0]; a1_c[1] = h1_c[1]; a1_c[2] = h1_c[2];
+      a2_ok = h2_ok; a2_w = h2_w; a2_c[0] = h2_c[0]; a2_c[1] = h2_c[1]; a2_c[2] = h2_c[2];
+    } else {
+      a1_ok = a2_ok = false;
     }
     return w;
   }
@@ -236,12 +293,12 @@ struct Marcher {
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) cmax[k] = __dadd_rn(corner[k], edge);
-    const double far = ray_box_far(p, d, inv, corner, cmax);
+    const double far = box_far(p, corner, cmax);
     t_cur = __dadd_rn(t_cur, __dadd_rn(npmax(far, 0.0), kEpsAdvance));
     bool got = false;
     if (w <= -2) {
       double a_in, a_out;
-      ray_box_inv(o, d, inv, corner, cmax, a_in, a_out);
+      box(o, corner, cmax, a_in, a_out);
       s0 = npmax(a_in, 0.0);
       s1 = npmin(a_out, t_max);
       if (s1 > __dadd_rn(s0, 1e-12)) {
@@ -308,8 +365,7 @@ __global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, co
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   Marcher m;
-  int32_t wc[kPathCache + 1];
-  m.init(t, orig + 3 * i, dirs + 3 * i, tmax ? tmax[i] : INFINITY, t.max_depth, wc);
+  m.init(t, orig + 3 * i, dirs + 3 * i, tmax ? tmax[i] : INFINITY, t.max_depth);
   int64_t k = 0, off = starts ? starts[i] : 0;
   int32_t st = 0;
   double t_run = 1.0;
@@ -336,7 +392,7 @@ __global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, co
 
 // Fused integrate_rays: march + shade + composite for one ray per thread.
 template <bool kExactColor>
-__global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
+__global__ void __launch_bounds__(128, 4) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
                                                      const double *__restrict__ orig, const double *__restrict__ dirs,
                                                      const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                      float *__restrict__ out_rgb, float *__restrict__ out_op,
@@ -351,8 +407,7 @@ __global__ void __launch_bounds__(128) k_ray_forward(OctDev t, salf_scene_t sc, 
   const bool ok = valid ? valid[i] != 0 : true;
   if (ok) {
     Marcher m;
-    int32_t wc[kPathCache + 1];
-    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth, wc);
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
     bool frozen = false;
     while (m.active) {
       int64_t vid;
@@ -412,12 +467,11 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
   const double keep = 1.0 - opt.stop_threshold;
   bool live = i < n && (valid ? valid[i] != 0 : true);
   Marcher m;
-  int32_t wc[kPathCache + 1];
   m.active = false;
   double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, T = 1.0,
          t_run = 1.0;
   if (live) {
-    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth, wc);
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
     const double *s = saved + i * SALF_SAVED_STRIDE;
     for (int k = 0; k < 3; ++k) dC[k] = d_rgb[3 * i + k];
     const double acc_w = s[3], acc_wt = s[4];
