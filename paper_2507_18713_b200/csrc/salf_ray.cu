@@ -9,6 +9,8 @@
 // without materialising any per-segment record.  The backward re-marches the
 // same rays warp-synchronously and scatters per-voxel gradients with
 // warp-aggregated atomics.
+#include <stdlib.h>
+
 #include "salf_common.cuh"
 #include "salf_internal.h"
 
@@ -19,6 +21,7 @@ struct OctDev {
   double rmin[3], rmax[3];
   double root_edge;
   int max_depth;
+  int variant;
 };
 
 static OctDev make_oct(const salf_octree_t *t) {
@@ -30,6 +33,8 @@ static OctDev make_oct(const salf_octree_t *t) {
   }
   o.root_edge = t->root_edge;
   o.max_depth = t->max_depth;
+  const char *v = getenv("SALF_MARCH_VARIANT");  // A/B knob for the descent (default 2)
+  o.variant = v ? atoi(v) : 2;
   return o;
 }
 
@@ -124,6 +129,7 @@ struct Marcher {
   bool pos[3];
   int rounds;
   int depth_bits;  // D
+  int variant;     // 0: reference iteration, 1: integer path from the root, 2: + ancestor cache
   int pd;          // level of the previous round's node, -1 = none
   uint32_t cix, ciy, ciz;
   bool a1_ok, a2_ok;  // cached ancestors at levels pd-1, pd-2
@@ -148,6 +154,7 @@ struct Marcher {
     active = (t_out > t_cur) && (t_cur < t_max) && isfinite(t_cur);
     rounds = 0;
     depth_bits = max_depth;
+    variant = t.variant;
     pd = -1;
     a1_ok = a2_ok = false;
   }
@@ -194,7 +201,7 @@ struct Marcher {
       u[k] = npmin(npmax(u[k], 0.0), 1.0);
     }
     const int D = depth_bits;
-    if (D > kMaxBits || u[0] != u[0] || u[1] != u[1] || u[2] != u[2]) {
+    if (variant == 0 || D > kMaxBits || u[0] != u[0] || u[1] != u[1] || u[2] != u[2]) {
       // generic path (very deep trees / NaN cursor): the reference iteration verbatim
       edge = t.root_edge;
       corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
@@ -221,6 +228,7 @@ struct Marcher {
     const uint32_t iz = u[2] >= 1.0 ? full : (uint32_t)(u[2] * scale);
     // resume point: deepest cached ancestor the new path still passes through
     int same = 0;
+    if (variant == 1) pd = -1, a1_ok = a2_ok = false;
     if (pd >= 0) {
       const uint32_t diff = (ix ^ cix) | (iy ^ ciy) | (iz ^ ciz);
       same = diff ? (__clz(diff) - (32 - D)) : D;

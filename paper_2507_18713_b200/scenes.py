@@ -228,16 +228,72 @@ def bake_surface(scene: Scene, a=50.0, b=0.02, prune=0.005) -> Scene:
                  inner_aabb=scene.inner_aabb)
 
 
+def _bake_fields(centers, edges, a, b):
+    s, alb = _primitive_sdf(centers)
+    eps = 1e-4
+    grad = np.stack([(_primitive_sdf(centers + eps * np.eye(3)[k])[0]
+                      - _primitive_sdf(centers - eps * np.eye(3)[k])[0]) / (2 * eps) for k in range(3)],
+                    axis=1)
+    n = centers.shape[0]
+    w_s = np.concatenate([grad * (edges[:, None] / 2.0), s[:, None]], axis=1)
+    w_sh = np.zeros((n, 3, 4))
+    al = np.clip(alb, 1e-3, 1 - 1e-3)
+    w_sh[:, :, 0] = np.log(al / (1 - al)) / SH_C0
+    return w_s, np.zeros((n, 3, 3)), w_sh, np.full(n, np.log(a)), np.full(n, np.log(b))
+
+
+def make_dense_surface_scene(name: str = "S1M", level: int = 7, a: float = 400.0,
+                             b: float = 0.004, band: float = 1.15) -> Scene:
+    """'surface-dense' regime: a trained-like scene of ~1M voxels.
+
+    Starting from the inner region of the reference-pipeline scene `name` at
+    its base level, cells whose cube can touch a primitive surface
+    (|sdf(centre)| <= half-diagonal, widened to a `band` x half-diagonal shell
+    at the finest level) are subdivided down to `level` (octree aligned, like
+    the reference's densification, densify.py:53-94); the surviving cells get
+    fields baked from the analytic primitives.  S1M -> ~1.0M voxels."""
+    base = make_init_scene(name)
+    bounds = base.bounds
+    lo, hi = base.inner_aabb
+    e0 = bounds.level_edge(_INNER_LEVEL)
+    i0 = np.round((lo - bounds.aabb_min) / e0).astype(np.int64)
+    i1 = np.round((hi - bounds.aabb_min) / e0).astype(np.int64)
+    g = np.meshgrid(*[np.arange(i0[k], i1[k]) for k in range(3)], indexing="ij")
+    cells = np.stack([x.ravel() for x in g], axis=1)
+    offs = np.array([[x, y, z] for z in (0, 1) for y in (0, 1) for x in (0, 1)])
+    lev = _INNER_LEVEL
+    extra = (band - 1.0) * 0.8661 * bounds.level_edge(level)
+    while True:
+        e = bounds.level_edge(lev)
+        c = bounds.aabb_min + (cells + 0.5) * e
+        sd, _ = _primitive_sdf(c)
+        cells = cells[np.abs(sd) <= 0.8661 * e + extra]
+        if lev == level:
+            break
+        cells = (cells[:, None, :] * 2 + offs[None]).reshape(-1, 3)
+        lev += 1
+    e = bounds.level_edge(level)
+    centers = bounds.aabb_min + (cells + 0.5) * e
+    fields = _bake_fields(centers, np.full(cells.shape[0], e), a, b)
+    vset = SparseVoxelSet(bounds, max(base.static.budget, cells.shape[0]))
+    vset.set_arrays(np.full(cells.shape[0], level, np.uint8), cells.astype(np.int32), *fields)
+    return f32_roundtrip(Scene(bounds=bounds, static=vset, density_mode=DENSITY_SDF,
+                               inner_aabb=base.inner_aabb))
+
+
 def get_scene(name: str, regime: str = "init", cache: bool = True) -> Scene:
     """Load (or build and cache under data/) a benchmark scene as salf.v1."""
     d = DATA / f"{name}_{regime}"
     if cache and (d / "meta.json").exists():
         return load_scene(d)[0]
-    scene = make_init_scene(name)
-    if regime == "surface":
-        scene = bake_surface(scene)
-    elif regime != "init":
-        raise ValueError(f"unknown regime {regime!r}")
+    if regime == "surface-dense":
+        scene = make_dense_surface_scene(name)
+    else:
+        scene = make_init_scene(name)
+        if regime == "surface":
+            scene = bake_surface(scene)
+        elif regime != "init":
+            raise ValueError(f"unknown regime {regime!r}")
     if cache:
         save_scene(scene, d)
         return load_scene(d)[0]  # f32 round trip, identical to what the reference loads
