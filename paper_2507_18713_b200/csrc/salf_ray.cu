@@ -21,7 +21,6 @@ struct OctDev {
   double rmin[3], rmax[3];
   double root_edge;
   int max_depth;
-  int variant;
 };
 
 static OctDev make_oct(const salf_octree_t *t) {
@@ -33,8 +32,6 @@ static OctDev make_oct(const salf_octree_t *t) {
   }
   o.root_edge = t->root_edge;
   o.max_depth = t->max_depth;
-  const char *v = getenv("SALF_MARCH_VARIANT");  // A/B knob for the descent (default 2)
-  o.variant = v ? atoi(v) : 2;
   return o;
 }
 
@@ -111,30 +108,15 @@ __device__ __forceinline__ double ray_box_far(const double o[3], const double d[
   return to;
 }
 
-constexpr int kMaxBits = 30;  // trees up to this depth use the integer descent
-
-// Per-ray marcher state (BatchMarch, octree.py:222-273).
-//
-// Descent: the reference's per-level octant test (u >= 0.5, u <- 2u - bit,
-// octree.py:158-163) is exact arithmetic, so the bit at level k equals bit
-// (D-1-k) of floor(u * 2^D) (u = 1 -> all ones, as the iteration gives).  A
-// round derives its whole root-to-leaf path from three integers and resumes
-// from the parent or grandparent of the previous round's node when the new
-// path still passes through it (their node words and corners are kept in
-// registers); corners are accumulated level by level exactly as the reference
-// does (corner += bit * edge), so corners, exits and segments are unchanged.
+// Per-ray marcher state (BatchMarch, octree.py:222-273).  1/d is cached per
+// ray (IEEE division: identical to recomputing it), exits compute only the
+// far plane, and for rays whose components are all non-zero the slab faces
+// are chosen by the sign of 1/d (no per-axis min/max, no NaN possible).
 struct Marcher {
   double o[3], d[3], inv[3], t_max, t_cur, t_end;
   bool active, fast;
   bool pos[3];
   int rounds;
-  int depth_bits;  // D
-  int variant;     // 0: reference iteration, 1: integer path from the root, 2: + ancestor cache
-  int pd;          // level of the previous round's node, -1 = none
-  uint32_t cix, ciy, ciz;
-  bool a1_ok, a2_ok;  // cached ancestors at levels pd-1, pd-2
-  int32_t a1_w, a2_w;
-  double a1_c[3], a2_c[3];
 
   __device__ void init(const OctDev &t, const double *orig, const double *dir, double tmax, int max_depth) {
     fast = true;
@@ -153,10 +135,7 @@ struct Marcher {
     t_end = npmin(t_out, t_max);
     active = (t_out > t_cur) && (t_cur < t_max) && isfinite(t_cur);
     rounds = 0;
-    depth_bits = max_depth;
-    variant = t.variant;
-    pd = -1;
-    a1_ok = a2_ok = false;
+    (void)max_depth;
   }
 
   // ray_box_range for this ray (fast path: near face chosen by the sign of
@@ -190,96 +169,13 @@ struct Marcher {
     return ray_box_far(p, d, inv, bmin, bmax);
   }
 
+  // query_batch for the cursor (octree.py:136-166): the reference's octant
+  // iteration verbatim (u >= 0.5, corner += bit * edge, u <- 2u - bit).  An
+  // integer-path descent resuming from cached ancestors was measured slower
+  // on B200 (C3: 2.17 ms vs 1.82 ms) -- the loop is latency-, not load-bound.
   __device__ __forceinline__ int32_t descend(const OctDev &t, const double p[3], double corner[3], double &edge,
-                                             bool &outside) {
-    double u[3];
-    outside = false;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      u[k] = __ddiv_rn(__dsub_rn(p[k], t.rmin[k]), t.root_edge);
-      if (u[k] < -1e-9 || u[k] > 1.0 + 1e-9) outside = true;
-      u[k] = npmin(npmax(u[k], 0.0), 1.0);
-    }
-    const int D = depth_bits;
-    if (variant == 0 || D > kMaxBits || u[0] != u[0] || u[1] != u[1] || u[2] != u[2]) {
-      // generic path (very deep trees / NaN cursor): the reference iteration verbatim
-      edge = t.root_edge;
-      corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
-      int32_t w = __ldg(t.nodes);
-      while (w >= 0) {
-        const int b0 = u[0] >= 0.5, b1 = u[1] >= 0.5, b2 = u[2] >= 0.5;
-        edge = __dmul_rn(edge, 0.5);
-        corner[0] = __dadd_rn(corner[0], b0 ? edge : 0.0);
-        corner[1] = __dadd_rn(corner[1], b1 ? edge : 0.0);
-        corner[2] = __dadd_rn(corner[2], b2 ? edge : 0.0);
-        u[0] = __dsub_rn(__dmul_rn(2.0, u[0]), (double)b0);
-        u[1] = __dsub_rn(__dmul_rn(2.0, u[1]), (double)b1);
-        u[2] = __dsub_rn(__dmul_rn(2.0, u[2]), (double)b2);
-        w = __ldg(t.nodes + w + b0 + 2 * b1 + 4 * b2);
-      }
-      pd = -1;
-      a1_ok = a2_ok = false;
-      return w;
-    }
-    const uint32_t full = (1u << D) - 1u;
-    const double scale = ldexp(1.0, D);
-    const uint32_t ix = u[0] >= 1.0 ? full : (uint32_t)(u[0] * scale);
-    const uint32_t iy = u[1] >= 1.0 ? full : (uint32_t)(u[1] * scale);
-    const uint32_t iz = u[2] >= 1.0 ? full : (uint32_t)(u[2] * scale);
-    // resume point: deepest cached ancestor the new path still passes through
-    int same = 0;
-    if (variant == 1) pd = -1, a1_ok = a2_ok = false;
-    if (pd >= 0) {
-      const uint32_t diff = (ix ^ cix) | (iy ^ ciy) | (iz ^ ciz);
-      same = diff ? (__clz(diff) - (32 - D)) : D;
-    }
-    int L;
-    int32_t w;
-    bool h2_ok;  // history: node one level above the current one
-    int32_t h2_w;
-    double h2_c[3];
-    if (a1_ok && same >= pd - 1) {
-      L = pd - 1; w = a1_w;
-      corner[0] = a1_c[0]; corner[1] = a1_c[1]; corner[2] = a1_c[2];
-      h2_ok = a2_ok; h2_w = a2_w; h2_c[0] = a2_c[0]; h2_c[1] = a2_c[1]; h2_c[2] = a2_c[2];
-    } else if (a2_ok && same >= pd - 2) {
-      L = pd - 2; w = a2_w;
-      corner[0] = a2_c[0]; corner[1] = a2_c[1]; corner[2] = a2_c[2];
-      h2_ok = false; h2_w = 0; h2_c[0] = h2_c[1] = h2_c[2] = 0.0;
-    } else {
-      L = 0; w = __ldg(t.nodes);
-      corner[0] = t.rmin[0]; corner[1] = t.rmin[1]; corner[2] = t.rmin[2];
-      h2_ok = false; h2_w = 0; h2_c[0] = h2_c[1] = h2_c[2] = 0.0;
-    }
-    edge = ldexp(t.root_edge, -L);  // == root_edge * 0.5^L exactly
-    bool h1_ok = false;
-    int32_t h1_w = 0;
-    double h1_c[3] = {0.0, 0.0, 0.0};
-    while (w >= 0) {
-      // node at level L is internal: it becomes the newest ancestor
-      h2_ok = h1_ok ? true : h2_ok;
-      if (h1_ok) { h2_w = h1_w; h2_c[0] = h1_c[0]; h2_c[1] = h1_c[1]; h2_c[2] = h1_c[2]; }
-      h1_ok = true; h1_w = w; h1_c[0] = corner[0]; h1_c[1] = corner[1]; h1_c[2] = corner[2];
-      const int sh = D - 1 - L;
-      const int bx = (ix >> sh) & 1, by = (iy >> sh) & 1, bz = (iz >> sh) & 1;
-      edge = __dmul_rn(edge, 0.5);
-      if (bx) corner[0] = __dadd_rn(corner[0], edge);
-      if (by) corner[1] = __dadd_rn(corner[1], edge);
-      if (bz) corner[2] = __dadd_rn(corner[2], edge);
-      w = __ldg(t.nodes + w + bx + 2 * by + 4 * bz);
-      ++L;
-    }
-    // the returned node sits at level L; its parent is h1 (level L-1) unless
-    // we resumed at L itself (only possible at the root: L == 0)
-    pd = L;
-    cix = ix; ciy = iy; ciz = iz;
-    if (h1_ok) {
-      a1_ok = true; a1_w = h1_w; a1_c[0] = h1_c[0]; a1_c[1] = h1_c[1]; a1_c[2] = h1_c[2];
-      a2_ok = h2_ok; a2_w = h2_w; a2_c[0] = h2_c[0]; a2_c[1] = h2_c[1]; a2_c[2] = h2_c[2];
-    } else {
-      a1_ok = a2_ok = false;
-    }
-    return w;
+                                             bool &outside) const {
+    return query_point(t, p, corner, edge, outside);
   }
 
   // One round; returns true and (vid, s0, s1) when a kept leaf segment was found.
@@ -318,6 +214,14 @@ struct Marcher {
     return got;
   }
 };
+
+__device__ __forceinline__ void prefetch_record(const salf_scene_t &sc, int64_t vid) {
+  const float *pr = sc.prm + vid * SALF_PRM_STRIDE;
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(sc.geo + 4 * vid));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(sc.aux + 4 * vid));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + SALF_PRM_STRIDE - 1));
+}
 
 struct RaySeg {
   double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
@@ -417,30 +321,44 @@ __global__ void __launch_bounds__(128, 4) k_ray_forward(OctDev t, salf_scene_t s
     Marcher m;
     m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
     bool frozen = false;
-    while (m.active) {
-      int64_t vid;
-      double s0, s1;
-      if (!m.step(t, vid, s0, s1, st)) continue;
-      if (s0 < last_t0) st |= kStatusOrder;
-      last_t0 = s0;
-      ++n_seg;
-      RaySeg sv;
-      shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen);
-      if (!frozen) {
-        if (T > keep) {  // included iff T_before > 1 - stop_threshold (render_ray.py:97-99)
-          const double w = __dmul_rn(T, sv.alpha);
+    // Software pipeline: a segment found in round k has its voxel record
+    // prefetched and is shaded after round k+1 has been marched, so the
+    // record's L2/HBM latency overlaps the next descent.  If segment k
+    // saturates the ray, round k+1's result is simply dropped (the hit list
+    // ends at k, as in the reference).
+    bool have = false;
+    int64_t pv = 0;
+    double p0 = 0.0, p1 = 0.0;
+    while (true) {
+      int64_t vid = 0;
+      double s0 = 0.0, s1 = 0.0;
+      const bool got = m.active && m.step(t, vid, s0, s1, st);
+      if (got) prefetch_record(sc, vid);
+      if (have) {
+        if (p0 < last_t0) st |= kStatusOrder;
+        last_t0 = p0;
+        ++n_seg;
+        RaySeg sv;
+        shade_seg<kExactColor>(sc, m, pv, p0, p1, sv, !frozen);
+        if (!frozen) {
+          if (T > keep) {  // included iff T_before > 1 - stop_threshold (render_ray.py:97-99)
+            const double w = __dmul_rn(T, sv.alpha);
 #pragma unroll
-          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
-          acc_w = __dadd_rn(acc_w, w);
-          acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
-          T = __dmul_rn(T, sv.om);
-        } else {
-          frozen = true;
+            for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+            acc_w = __dadd_rn(acc_w, w);
+            acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
+            T = __dmul_rn(T, sv.om);
+          } else {
+            frozen = true;
+          }
         }
+        // product-based early stop on the march (render_ray.py:154-157)
+        t_run = __dmul_rn(t_run, __dsub_rn(1.0, sv.alpha));
+        if (t_run <= keep) break;
       }
-      // product-based early stop on the march (render_ray.py:154-157)
-      t_run = __dmul_rn(t_run, __dsub_rn(1.0, sv.alpha));
-      if (t_run <= keep) break;
+      have = got;
+      pv = vid; p0 = s0; p1 = s1;
+      if (!have && !m.active) break;
     }
   }
   if (ok) {
