@@ -13,7 +13,10 @@ from pathlib import Path
 import numpy as np
 import torch
 
-LIB_PATH = Path(__file__).resolve().parent / "libsalf_b200.so"
+import os
+
+# SALF_LIB overrides the library path (A/B builds of the same ABI)
+LIB_PATH = Path(os.environ.get("SALF_LIB") or Path(__file__).resolve().parent / "libsalf_b200.so")
 
 SALF_OK, SALF_EINVAL, SALF_ENOTERM, SALF_ECUDA, SALF_EWORKSPACE = 0, 1, 2, 3, 4
 KINDS = {"pinhole": 0, "fisheye_equidistant": 1, "equirect": 2}

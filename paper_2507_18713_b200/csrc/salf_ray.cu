@@ -215,14 +215,6 @@ struct Marcher {
   }
 };
 
-__device__ __forceinline__ void prefetch_record(const salf_scene_t &sc, int64_t vid) {
-  const float *pr = sc.prm + vid * SALF_PRM_STRIDE;
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(sc.geo + 4 * vid));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(sc.aux + 4 * vid));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(pr));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(pr + SALF_PRM_STRIDE - 1));
-}
-
 struct RaySeg {
   double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
 };
@@ -304,7 +296,10 @@ __global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, co
 
 // Fused integrate_rays: march + shade + composite for one ray per thread.
 template <bool kExactColor>
-__global__ void __launch_bounds__(128, 4) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
+#ifndef SALF_RAY_MINB
+#define SALF_RAY_MINB 4
+#endif
+__global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
                                                      const double *__restrict__ orig, const double *__restrict__ dirs,
                                                      const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                      float *__restrict__ out_rgb, float *__restrict__ out_op,
@@ -321,44 +316,30 @@ __global__ void __launch_bounds__(128, 4) k_ray_forward(OctDev t, salf_scene_t s
     Marcher m;
     m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
     bool frozen = false;
-    // Software pipeline: a segment found in round k has its voxel record
-    // prefetched and is shaded after round k+1 has been marched, so the
-    // record's L2/HBM latency overlaps the next descent.  If segment k
-    // saturates the ray, round k+1's result is simply dropped (the hit list
-    // ends at k, as in the reference).
-    bool have = false;
-    int64_t pv = 0;
-    double p0 = 0.0, p1 = 0.0;
-    while (true) {
-      int64_t vid = 0;
-      double s0 = 0.0, s1 = 0.0;
-      const bool got = m.active && m.step(t, vid, s0, s1, st);
-      if (got) prefetch_record(sc, vid);
-      if (have) {
-        if (p0 < last_t0) st |= kStatusOrder;
-        last_t0 = p0;
-        ++n_seg;
-        RaySeg sv;
-        shade_seg<kExactColor>(sc, m, pv, p0, p1, sv, !frozen);
-        if (!frozen) {
-          if (T > keep) {  // included iff T_before > 1 - stop_threshold (render_ray.py:97-99)
-            const double w = __dmul_rn(T, sv.alpha);
+    while (m.active) {
+      int64_t vid;
+      double s0, s1;
+      if (!m.step(t, vid, s0, s1, st)) continue;
+      if (s0 < last_t0) st |= kStatusOrder;
+      last_t0 = s0;
+      ++n_seg;
+      RaySeg sv;
+      shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen);
+      if (!frozen) {
+        if (T > keep) {  // included iff T_before > 1 - stop_threshold (render_ray.py:97-99)
+          const double w = __dmul_rn(T, sv.alpha);
 #pragma unroll
-            for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
-            acc_w = __dadd_rn(acc_w, w);
-            acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
-            T = __dmul_rn(T, sv.om);
-          } else {
-            frozen = true;
-          }
+          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+          acc_w = __dadd_rn(acc_w, w);
+          acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
+          T = __dmul_rn(T, sv.om);
+        } else {
+          frozen = true;
         }
-        // product-based early stop on the march (render_ray.py:154-157)
-        t_run = __dmul_rn(t_run, __dsub_rn(1.0, sv.alpha));
-        if (t_run <= keep) break;
       }
-      have = got;
-      pv = vid; p0 = s0; p1 = s1;
-      if (!have && !m.active) break;
+      // product-based early stop on the march (render_ray.py:154-157)
+      t_run = __dmul_rn(t_run, __dsub_rn(1.0, sv.alpha));
+      if (t_run <= keep) break;
     }
   }
   if (ok) {

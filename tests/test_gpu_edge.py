@@ -1,0 +1,261 @@
+"""GPU: the reference suite's edge cases and known answers, run through the
+CUDA path, plus full-size (BASELINE config) checks against the oracle on
+bounded samples and size-independent invariants."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import oracle_voxels
+from oracle import salf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _scene(lo, hi, base, levels, cells, vlevels=None, a=2.0, seed=0):
+    from paper_2507_18713_b200.scene import Scene, SceneBounds, SparseVoxelSet
+    from paper_2507_18713_b200.scenes import f32_roundtrip
+    b = SceneBounds(np.asarray(lo, float), np.asarray(hi, float), base, levels)
+    v = SparseVoxelSet(b, 1000)
+    n = len(cells)
+    rng = np.random.default_rng(seed)
+    if n:
+        v.set_arrays(np.zeros(n) if vlevels is None else vlevels, cells,
+                     rng.uniform(-1 / np.sqrt(3), 1 / np.sqrt(3), (n, 4)),
+                     rng.uniform(-1 / np.sqrt(3), 1 / np.sqrt(3), (n, 3, 3)),
+                     rng.uniform(-0.5, 0.5, (n, 3, 4)), np.log(np.broadcast_to(a, (n,))),
+                     np.log(np.full(n, 0.2)))
+    return f32_roundtrip(Scene(bounds=b, static=v))
+
+
+def _cam(pos=(0, 0, 0), w=32, h=32, f=40.0, cx=None, cy=None, target=None, kind="pinhole"):
+    from paper_2507_18713_b200.sensors import CameraModel, look_at_quaternion
+    q = look_at_quaternion(pos, target) if target is not None else np.array([1.0, 0, 0, 0])
+    return CameraModel(kind=kind, width=w, height=h, fx=f, fy=f, cx=w / 2 if cx is None else cx,
+                       cy=h / 2 if cy is None else cy, position=np.asarray(pos, float), quaternion=q)
+
+
+def _raster64(scene, cam, bg=(0.0, 0.0, 0.0)):
+    """f64 outputs from the raster saved state (colour, opacity, depth, weight sum)."""
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    fb, st = RR.rasterize(flatten_scene(scene), cam, background=bg, return_state=True, exact_color=True)
+    s = st.saved.cpu().numpy()
+    T = s[:, 5]
+    col = s[:, :3] + T[:, None] * np.asarray(bg)
+    depth = np.where(s[:, 3] > 0.5, s[:, 4] / np.where(s[:, 3] > 0, s[:, 3], 1), np.nan)
+    return col, 1 - T, depth, s[:, 3], fb
+
+
+def _ray64(scene, o, d, bg=(0.0, 0.0, 0.0)):
+    from paper_2507_18713_b200 import render_ray as RY
+    rec = RY.integrate_rays(scene, RY.build_scene_octrees(scene), o, d, background=bg, exact_color=True)
+    s = rec.saved.cpu().numpy()
+    T = s[:, 5]
+    col = s[:, :3] + T[:, None] * np.asarray(bg)
+    depth = np.where(s[:, 3] > 0.5, s[:, 4] / np.where(s[:, 3] > 0, s[:, 3], 1), np.nan)
+    return col, 1 - T, depth, s[:, 3], rec
+
+
+# ---- reference-suite known answers (test_render_raster.py / test_render_ray.py) ------
+
+def test_empty_scene_background():
+    from paper_2507_18713_b200 import render_raster as RR, render_ray as RY
+    sc = _scene([0, 0, 0], [2, 2, 2], 1.0, 2, np.zeros((0, 3), int))
+    fb = RR.rasterize_scene(sc, _cam(w=32, h=32, f=30.0), background=(0.1, 0.2, 0.3))
+    assert torch.allclose(fb.color.cpu(), torch.tensor([0.1, 0.2, 0.3]))
+    assert bool((fb.opacity == 0).all()) and bool(torch.isnan(fb.depth).all())
+    rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), [[-1, 1, 1]], [[1.0, 0, 0]],
+                            background=(0.2, 0.3, 0.4))
+    assert np.allclose(rec.out_color.cpu().numpy(), [0.2, 0.3, 0.4])
+    assert float(rec.opacity[0]) == 0.0 and bool(torch.isnan(rec.depth[0]))
+
+
+def test_non_pinhole_rejected():
+    from paper_2507_18713_b200 import render_raster as RR
+    sc = _scene([0, 0, 0], [2, 2, 2], 1.0, 2, np.zeros((0, 3), int))
+    with pytest.raises(ValueError, match="pinhole"):
+        RR.rasterize_scene(sc, _cam(kind="equirect", w=8, h=8))
+
+
+def test_non_unit_direction_rejected():
+    from paper_2507_18713_b200 import octree as OC
+    sc = _scene([0, 0, 0], [2, 2, 2], 1.0, 3, [[0, 0, 0]])
+    with pytest.raises(ValueError, match="unit norm"):
+        OC.march(OC.build_octree(sc.static), [0.5, 0.5, 0.5], [1.0, 1.0, 0.0])
+
+
+def test_query_outside_root_raises():
+    from paper_2507_18713_b200 import octree as OC
+    sc = _scene([0, 0, 0], [2, 2, 2], 1.0, 3, [[0, 0, 0]])
+    with pytest.raises(ValueError):
+        OC.query(OC.build_octree(sc.static), [5.0, 0.5, 0.5])
+
+
+def test_march_known_answers():
+    """test_octree.py:149-171, :215-219."""
+    from paper_2507_18713_b200 import octree as OC
+    sc = _scene([0, 0, 0], [4, 4, 4], 1.0, 2, [[i, 0, 0] for i in range(4)])
+    segs = OC.march(OC.build_octree(sc.static), [-1.0, 0.5, 0.5], [1.0, 0, 0])
+    assert [s[0] for s in segs] == [0, 1, 2, 3]
+    sc2 = _scene([0, 0, 0], [2, 2, 2], 1.0, 3, [[0, 0, 0]])
+    buf = OC.build_octree(sc2.static)
+    segs = OC.march(buf, [0.5, 0.5, 0.5], [1.0, 0, 0])
+    assert len(segs) == 1 and segs[0][1] == 0.0 and segs[0][2] == pytest.approx(0.5)
+    sc3 = _scene([0, 0, 0], [2, 2, 2], 1.0, 3, [[0, 0, 0], [1, 0, 0]])
+    segs = OC.march(OC.build_octree(sc3.static), [-1.0, 0.5, 0.5], [1.0, 0, 0], t_max=1.5)
+    assert len(segs) == 1 and segs[0][2] <= 1.5
+
+
+def test_single_voxel_raster_equals_ray_at_principal_pixel():
+    """test_render_raster.py:110-123: 1e-6 colour, 1e-9 depth."""
+    sc = _scene([-2, -2, -2], [2, 2, 2], 1.0, 3, [[1, 1, 1]], a=50.0, seed=3)
+    cam = _cam(pos=(-0.5, -0.5, -1.8), w=33, h=33, f=40.0, cx=16.5, cy=16.5)
+    col, _, depth, _, _ = _raster64(sc, cam)
+    rcol, _, rdepth, _, _ = _ray64(sc, [cam.position], [[0, 0, 1.0]])
+    pix = 16 * 33 + 16
+    assert np.max(np.abs(col[pix] - rcol[0])) < 1e-6
+    assert depth[pix] == pytest.approx(rdepth[0], abs=1e-9)
+
+
+def test_depth_single_opaque_segment():
+    """test_render_ray.py:121-126."""
+    sc = _scene([0, 0, 0], [2, 2, 2], 1.0, 2, [[0, 0, 0]], a=1000.0, seed=5)
+    _, _, depth, _, _ = _ray64(sc, [[-1.0, 0.5, 0.5]], [[1.0, 0, 0]])
+    assert depth[0] == pytest.approx(1.5, abs=1e-9)
+
+
+def test_weights_plus_residual_is_one():
+    """test_render_ray.py:274-285 invariants on a random scene."""
+    from conftest import load_golden_scene
+    sc = load_golden_scene("rand300i")
+    rng = np.random.default_rng(42)
+    o = rng.uniform(-1, 9, (500, 3))
+    d = rng.normal(size=(500, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    _, op, _, wsum, rec = _ray64(sc, o, d)
+    assert np.allclose(wsum + (1 - op), 1.0, atol=1e-6)
+    assert int(rec.status.max()) == 0
+
+
+def test_zero_loss_and_background_only_give_zero_grads():
+    """test_backward.py:38-60."""
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.backward import backward_records
+    from conftest import load_golden_scene
+    sc = load_golden_scene("fd10")
+    rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), np.random.default_rng(1).uniform(0, 4, (15, 3)),
+                            np.tile([[0.0, 0.0, 1.0]], (15, 1)))
+    g = backward_records(rec, sc, np.zeros((15, 3)), np.zeros(15))["static"]
+    assert all(np.all(v == 0.0) for v in g.values())
+    sc1 = _scene([0, 0, 0], [2, 2, 2], 1.0, 2, [[0, 0, 0]], seed=1)
+    rec = RY.integrate_rays(sc1, RY.build_scene_octrees(sc1), [[-1.0, 1.5, 1.5]], [[1.0, 0, 0]])
+    g = backward_records(rec, sc1, np.ones((1, 3)), np.ones(1))["static"]
+    assert all(np.all(v == 0.0) for v in g.values())
+
+
+def test_fisheye_invalid_pixels_keep_background():
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.sensors import CameraModel, camera_rays
+    from conftest import load_golden_scene
+    sc = load_golden_scene("rand300")
+    cam = CameraModel(kind="fisheye_equidistant", width=40, height=30, fx=6.0, fy=6.0, cx=20.0, cy=15.0,
+                      position=np.array([13.0, 11.0, 7.0]))
+    b = camera_rays(cam)
+    assert not bool(b.valid.all())
+    col, op, depth = RY.render_rays_image(sc, RY.build_scene_octrees(sc), b, background=(0.3, 0.2, 0.1))
+    inv = ~b.valid.reshape(30, 40)
+    assert torch.allclose(col[inv].cpu(), torch.tensor([0.3, 0.2, 0.1]))
+    assert bool((op[inv] == 0).all()) and bool(torch.isnan(depth[inv]).all())
+
+
+def test_raster_repeat_bitwise_deterministic():
+    from paper_2507_18713_b200 import render_raster as RR
+    from conftest import load_golden_scene
+    from paper_2507_18713_b200.scene import flatten_scene
+    flat = flatten_scene(load_golden_scene("rand400"))
+    cam = _cam(pos=(12.0, 12.0, 6.0), target=(4.0, 4.0, 2.0), w=40, h=40, f=45.0)
+    a, b = RR.rasterize(flat, cam), RR.rasterize(flat, cam)
+    assert torch.equal(a.color, b.color)
+
+
+# ---- full-size configurations (BASELINE configs) on bounded oracle samples ------------
+
+@pytest.fixture(scope="module")
+def s1m():
+    from paper_2507_18713_b200.scenes import get_scene
+    return get_scene("S1M", "init")
+
+
+def test_c2_reference_bins_full_size(s1m):
+    """C2 at 1920x1080 on S1M: the reference CSR has 102.1M instances;
+    a sample of tiles is bit-identical to the oracle's binning of those tiles."""
+    from paper_2507_18713_b200 import configs, render_raster as RR
+    from paper_2507_18713_b200.device import DeviceScene
+    cam = configs.c2_camera()
+    ds = DeviceScene.from_scene(s1m)
+    p = RR._project(ds, cam, 0.05, 16)
+    off, ent, n_inst, _ = RR._bin(ds, cam, 0.05, 16, p, mode=0)
+    assert 100_000_000 < n_inst < 104_000_000
+    vox = oracle_voxels(s1m)
+    ocam = O.Camera("pinhole", cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy,
+                    position=cam.position, quaternion=cam.quaternion)
+    off_h = off.cpu().numpy()
+    for (tx, ty) in [(0, 0), (60, 34), (119, 67), (17, 50)]:
+        _, _, ooff, oent = O.cull_and_bin(vox, ocam, window=(tx, ty, tx, ty))
+        t = ty * 120 + tx
+        got = ent[off_h[t]:off_h[t + 1]].cpu().numpy()
+        np.testing.assert_array_equal(got, oent[ooff[t]:ooff[t + 1]])
+
+
+def test_c2_frame_tiles_match_oracle(s1m):
+    """C2 forward at full size: sampled tiles of the 1080p frame vs the oracle."""
+    from paper_2507_18713_b200 import configs, render_raster as RR
+    from paper_2507_18713_b200.device import DeviceScene
+    cam = configs.c2_camera()
+    fb = RR.rasterize(DeviceScene.from_scene(s1m), cam)
+    col = fb.color.cpu().numpy()
+    vox = oracle_voxels(s1m)
+    ocam = O.Camera("pinhole", cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy,
+                    position=cam.position, quaternion=cam.quaternion)
+    for (tx, ty) in [(60, 34), (5, 60)]:
+        ref = O.rasterize(vox, ocam, window=(tx, ty, tx, ty))
+        sl = (slice(ty * 16, ty * 16 + 16), slice(tx * 16, tx * 16 + 16))
+        assert np.max(np.abs(col[sl] - ref["color"][sl])) < 1e-4
+
+
+def test_c3_lidar_hit_lists_full_size(s1m):
+    """C3 (128 x 1800 on S1M): early-stopped hit lists of a ray sample are
+    bit-identical to the oracle; every ray terminates; invariants hold."""
+    from paper_2507_18713_b200 import configs, render_ray as RY
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.sensors import gen_lidar_rays
+    ds = DeviceScene.from_scene(s1m)
+    oc = RY.build_scene_octrees(s1m)
+    lb = gen_lidar_rays(configs.c3_lidar())
+    rec = RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
+    assert int(rec.status.max()) == 0
+    assert 31_000_000 < int(rec.n_segments.sum()) < 34_000_000  # 32.3M
+    s = rec.saved.cpu().numpy()
+    assert np.allclose(s[:, 3] + s[:, 5], 1.0, atol=1e-6)
+    idx = np.random.default_rng(0).choice(lb.n, 400, replace=False)
+    o, d = lb.origins[idx].cpu().numpy(), lb.dirs[idx].cpu().numpy()
+    ray, vid, t0, t1 = (x.cpu().numpy() for x in RY.segments(ds, oc, o, d))
+    vox = oracle_voxels(s1m)
+    tree = O.build_octree(vox)
+    ref = O.integrate_rays(vox, tree, o, d)
+    np.testing.assert_array_equal(ray, ref["ray"])
+    np.testing.assert_array_equal(vid, ref["vid"])
+    np.testing.assert_array_equal(t0, ref["t0"])
+    np.testing.assert_array_equal(t1, ref["t1"])
+    dep = rec.depth.cpu().numpy()[idx]
+    np.testing.assert_array_equal(np.isnan(dep), np.isnan(ref["depth"]))
+    m = ~np.isnan(dep)
+    assert np.max(np.abs(dep[m] - ref["depth"][m]) / np.maximum(ref["depth"][m], 1.0)) < 1e-4
