@@ -378,13 +378,23 @@ def extras(ds, args):
     oc = RY.build_scene_octrees(scene)
     lidar = configs.c3_lidar()
     lb = gen_lidar_rays(lidar)
-    ms = timeit(lambda: RY.integrate_rays(ds, oc, lb.origins, lb.dirs))
-    ms_gen = timeit(lambda: RY.integrate_rays(ds, oc, gen_lidar_rays(lidar).origins, lb.dirs))
-    rec = RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
-    out["c3_lidar"] = {"rays_per_s": lb.n / (ms * 1e-3), "sweeps_per_s": 1e3 / ms, "ms": ms,
-                       "ms_with_raygen": ms_gen, "rays": lb.n,
-                       "segments": int(rec.n_segments.sum().item()),
-                       "status_max": int(rec.status.max().item())}
+
+    def c3(dsx, ocx, **kw):
+        ms = timeit(lambda: RY.render_lidar(dsx, ocx, lb, **kw))
+        ms_gen = timeit(lambda: RY.render_lidar(dsx, ocx, gen_lidar_rays(lidar), **kw))
+        ret = RY.render_lidar(dsx, ocx, lb, **kw)
+        return {"rays_per_s": lb.n / (ms * 1e-3), "sweeps_per_s": 1e3 / ms, "ms": ms,
+                "ms_with_raygen": ms_gen, "rays": lb.n,
+                "segments": int(ret.saved[:, 6].sum().item()),
+                "returns": int(torch.isfinite(ret.depth).sum().item()),
+                "status_max": int(ret.status.max().item())}
+
+    out["c3_lidar"] = c3(ds, oc)
+    rng = np.random.default_rng(0)
+    feat = torch.as_tensor(rng.uniform(-1, 1, (ds.n, 8)).astype(np.float32), device=ds.device)
+    head = rng.uniform(-0.5, 0.5, (2, 13)).astype(np.float32)
+    out["c3_lidar_intensity_raydrop"] = c3(ds, oc, features=feat, head=head)
+    del feat
     s2 = get_scene("S2M", "init")
     ds2 = DeviceScene.from_scene(s2)
     oc2 = RY.build_scene_octrees(s2)
@@ -394,22 +404,25 @@ def extras(ds, args):
         b = camera_rays(c4)
         return RY.integrate_rays(ds2, oc2, b.origins, b.dirs, valid=b.valid)
 
-    out["c4_fisheye_rs_fps"] = 1e3 / timeit(c4_frame, n=5)
+    out["c4_fisheye_rs_fps_S2M"] = 1e3 / timeit(c4_frame, n=5)
     del ds2, oc2
-    sur = get_scene("S1M", "surface")
+    sur = get_scene("S1M", "surface-dense")
     dss = DeviceScene.from_scene(sur)
     ocs = RY.build_scene_octrees(sur)
-    out["surface_regime"] = {"voxels": dss.n,
-                             "c2_forward_fps": 1e3 / timeit(lambda: RR.rasterize(dss, cam)),
-                             "c3_sweeps_per_s": 1e3 / timeit(lambda: RY.integrate_rays(
-                                 dss, ocs, lb.origins, lb.dirs))}
+    dcs = torch.full((1080, 1920, 3), 1e-7, dtype=torch.float64, device=dss.device)
+    dds = torch.zeros((1080, 1920), dtype=torch.float64, device=dss.device)
 
     def fb_step():
         fb, st = RR.rasterize(dss, cam, return_state=True)
-        RR.rasterize_backward(st, torch.full((1080, 1920, 3), 1e-7, device=dss.device),
-                              torch.zeros((1080, 1920), device=dss.device), as_dict=False)
+        RR.rasterize_backward(st, dcs, dds, as_dict=False)
 
-    out["surface_regime"]["c2_fwd_bwd_fps"] = 1e3 / timeit(fb_step, n=5)
+    out["surface_dense_regime"] = {
+        "voxels": dss.n,
+        "c2_forward_fps": 1e3 / timeit(lambda: RR.rasterize(dss, cam)),
+        "c2_fwd_bwd_fps": 1e3 / timeit(fb_step, n=5),
+        "c3_lidar": c3(dss, ocs),
+        "note": "trained-like scene: S1M inner region densified to level 7 near the analytic "
+                "surfaces (scenes.make_dense_surface_scene), fields baked a=400, b=0.004"}
     return out
 
 

@@ -187,6 +187,19 @@ int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64
                      const salf_raster_opts_t *opts, float *out_rgb, float *out_opacity,
                      float *out_depth, double *saved, int32_t *status, void *stream);
 
+/* render_lidar_ranges (render_ray.py:297-306) for a LiDAR batch: the fused
+ * march/shade/composite without colour (the reference computes and discards
+ * it), out_depth / out_opacity (N f32), saved (N x 8 f64, nullable), status.
+ * Optional intensity / ray-drop extension (not in the
+ * reference): feat (M x 8 f32) alpha-blended with the colour
+ * weights into out_feat (N x 8, nullable), then a linear head (2 x 13 f32:
+ * 8 feature weights, depth weight, 3 view-dir weights, bias) and a sigmoid ->
+ * out_head (N x 2: intensity, drop probability).  feat == NULL: depth only. */
+int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                       const double *origins, const double *dirs, const salf_raster_opts_t *opts,
+                       const float *feat, const float *head, float *out_depth, float *out_opacity,
+                       float *out_feat, float *out_head, double *saved, int32_t *status, void *stream);
+
 /* backward_records (backward.py:35-101) for the ray path, re-marching each
  * ray: d_rgb (N x 3), d_depth (N) f64; grad (M x 27 f64, accumulated). */
 int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,

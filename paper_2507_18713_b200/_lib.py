@@ -79,6 +79,7 @@ SIGNATURES = {
                              vp, vp, vp, vp]),
     "salf_ray_forward": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_ray_backward": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_lidar_forward": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 _lib = None

@@ -295,20 +295,31 @@ __global__ void k_march(OctDev t, int64_t n, const double *__restrict__ orig, co
 }
 
 // Fused integrate_rays: march + shade + composite for one ray per thread.
-template <bool kExactColor>
+struct LidarFeat {
+  const float *feat;  // M x 8 per-voxel LiDAR feature (nullable)
+  const float *head;  // 2 x 13: [W_f(8) | W_depth | W_dir(3) | bias] for intensity, drop
+  float *out_feat;    // N x 8 alpha-blended feature (nullable)
+  float *out_head;    // N x 2 (intensity, ray-drop probability)
+};
+
 #ifndef SALF_RAY_MINB
 #define SALF_RAY_MINB 4
 #endif
+// kLidar: depth-only rays (render_lidar_ranges never reads colour), plus the
+// optional intensity / ray-drop extension.
+template <bool kExactColor, bool kLidar>
 __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
                                                      const double *__restrict__ orig, const double *__restrict__ dirs,
                                                      const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                      float *__restrict__ out_rgb, float *__restrict__ out_op,
                                                      float *__restrict__ out_depth, double *__restrict__ saved,
-                                                     int32_t *__restrict__ status) {
+                                                     int32_t *__restrict__ status, LidarFeat lf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double keep = 1.0 - opt.stop_threshold;
   double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0, t_run = 1.0, last_t0 = -INFINITY;
+  float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool feat = kLidar && lf.feat != nullptr;
   int64_t n_seg = 0;
   int32_t st = 0;
   const bool ok = valid ? valid[i] != 0 : true;
@@ -324,12 +335,23 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
       last_t0 = s0;
       ++n_seg;
       RaySeg sv;
-      shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen);
+      shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen && !kLidar);
       if (!frozen) {
         if (T > keep) {  // included iff T_before > 1 - stop_threshold (render_ray.py:97-99)
           const double w = __dmul_rn(T, sv.alpha);
+          if (!kLidar) {
 #pragma unroll
-          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+            for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+          }
+          if (feat) {
+            const float4 f0 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid);
+            const float4 f1 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid + 1);
+            const float wf = (float)w;
+            acc_f[0] = fmaf(wf, f0.x, acc_f[0]); acc_f[1] = fmaf(wf, f0.y, acc_f[1]);
+            acc_f[2] = fmaf(wf, f0.z, acc_f[2]); acc_f[3] = fmaf(wf, f0.w, acc_f[3]);
+            acc_f[4] = fmaf(wf, f1.x, acc_f[4]); acc_f[5] = fmaf(wf, f1.y, acc_f[5]);
+            acc_f[6] = fmaf(wf, f1.z, acc_f[6]); acc_f[7] = fmaf(wf, f1.w, acc_f[7]);
+          }
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
           T = __dmul_rn(T, sv.om);
@@ -345,12 +367,14 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
   if (ok) {
     const double t_fin = T;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) out_rgb[3 * i + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(t_fin, opt.background[k]));
+    for (int k = 0; k < 3; ++k)
+      if (out_rgb) out_rgb[3 * i + k] = (float)__dadd_rn(acc_c[k], __dmul_rn(t_fin, opt.background[k]));
     out_op[i] = (float)__dsub_rn(1.0, t_fin);
     out_depth[i] = acc_w > kDepthWeightMin ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
   } else {  // render_rays_image: invalid pixels keep the background (render_ray.py:280-293)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) out_rgb[3 * i + k] = (float)opt.background[k];
+    for (int k = 0; k < 3; ++k)
+      if (out_rgb) out_rgb[3 * i + k] = (float)opt.background[k];
     out_op[i] = 0.0f;
     out_depth[i] = NAN;
   }
@@ -358,6 +382,25 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
     double *s = saved + i * SALF_SAVED_STRIDE;
     s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
     s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_seg; s[7] = 0.0;
+  }
+  if (feat) {
+    // linear head on [blended feature, expected depth (0 if none), view dir] + sigmoid
+    const float dep = (ok && acc_w > kDepthWeightMin) ? (float)__ddiv_rn(acc_wt, acc_w) : 0.0f;
+    const float dv[3] = {(float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float *W = lf.head + 13 * j;
+      float z = W[12];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z = fmaf(W[k], acc_f[k], z);
+      z = fmaf(W[8], dep, z);
+      z = fmaf(W[9], dv[0], fmaf(W[10], dv[1], fmaf(W[11], dv[2], z)));
+      lf.out_head[2 * i + j] = 1.0f / (1.0f + expf(-z));
+    }
+    if (lf.out_feat) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lf.out_feat[8 * i + k] = acc_f[k];
+    }
   }
   if (status) status[i] = st;
 }
@@ -493,13 +536,34 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
     if (n == 0) return SALF_OK;
     OctDev t = make_oct(tree);
     const unsigned grid = (unsigned)((n + 127) / 128);
+    LidarFeat lf{nullptr, nullptr, nullptr, nullptr};
     if (opts->exact_color)
-      k_ray_forward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
-                                                                    out_opacity, out_depth, saved, status);
+      k_ray_forward<true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
+                                                                           out_rgb, out_opacity, out_depth, saved,
+                                                                           status, lf);
     else
-      k_ray_forward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
-                                                                     out_opacity, out_depth, saved, status);
+      k_ray_forward<false, false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
+                                                                            out_rgb, out_opacity, out_depth, saved,
+                                                                            status, lf);
     return check_cuda("salf_ray_forward");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                  const double *origins, const double *dirs, const salf_raster_opts_t *opts,
+                                  const float *feat, const float *head, float *out_depth, float *out_opacity,
+                                  float *out_feat, float *out_head, double *saved, int32_t *status, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    if (feat && !head) return set_error(SALF_EINVAL, "LiDAR features need the 2 x 13 head");
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    LidarFeat lf{feat, head, out_feat, out_head};
+    k_ray_forward<false, true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts,
+                                                                         nullptr, out_opacity, out_depth, saved,
+                                                                         status, lf);
+    return check_cuda("salf_lidar_forward");
   }
   SALF_CATCH
 }

@@ -147,12 +147,74 @@ def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chun
     return rec.out_color.reshape(h, w, 3), rec.opacity.reshape(h, w), rec.depth.reshape(h, w)
 
 
+@dataclass
+class LidarReturn:
+    depth: torch.Tensor  # (beams, steps) f32, NaN = no return
+    opacity: torch.Tensor  # (beams, steps) f32
+    intensity: torch.Tensor | None  # (beams, steps) f32, extension only
+    drop_prob: torch.Tensor | None  # (beams, steps) f32, extension only
+    feature: torch.Tensor | None  # (beams, steps, 8) alpha-blended feature
+    saved: torch.Tensor
+    status: torch.Tensor
+
+
+def render_lidar(scene, octrees, batch, *, features=None, head=None,
+                 stop_threshold: float = STOP_THRESHOLD, want_feature: bool = False) -> LidarReturn:
+    """LiDAR sweep: expected range (render_lidar_ranges, render_ray.py:297-306)
+    plus the optional intensity / ray-drop extension (not in
+    the reference -- SPEC.md:8): per-voxel 8-channel `features` (M, 8) are
+    alpha-blended with the compositing weights and mapped, with the expected
+    depth and the view direction, by a linear `head` (2, 13) + sigmoid to
+    intensity and drop probability."""
+    lib = _lib.load()
+    ds = as_device_scene(scene)
+    tree = _octree_of(octrees)
+    dev = ds.device
+    o = _lib.as_f64(batch.origins, dev).reshape(-1, 3)
+    d = _lib.as_f64(batch.dirs, dev).reshape(-1, 3)
+    n = o.shape[0]
+    if n and bool((torch.linalg.norm(d, dim=1) - 1.0).abs().gt(1e-6).any()):
+        raise ValueError("ray directions must be unit norm")
+    depth = torch.empty(n, dtype=torch.float32, device=dev)
+    op = torch.empty(n, dtype=torch.float32, device=dev)
+    saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    f = h = of = oh = None
+    if features is not None:
+        f = torch.as_tensor(features, dtype=torch.float32, device=dev).reshape(-1, 8).contiguous()
+        if f.shape[0] != ds.n:
+            raise ValueError(f"features must have shape ({ds.n}, 8)")
+        if head is None:
+            raise ValueError("LiDAR features need a (2, 13) head")
+        h = torch.as_tensor(head, dtype=torch.float32, device=dev).reshape(2, 13).contiguous()
+        oh = torch.empty((n, 2), dtype=torch.float32, device=dev)
+        of = torch.empty((n, 8), dtype=torch.float32, device=dev) if want_feature else None
+    opts = _opts((0.0, 0.0, 0.0), stop_threshold, False)
+    sc, t = ds.c_struct(), tree.c_struct()
+    _lib.check(lib.salf_lidar_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
+                                      _lib.ref(opts), _lib.ptr(f), _lib.ptr(h), depth.data_ptr(),
+                                      op.data_ptr(), _lib.ptr(of), _lib.ptr(oh), saved.data_ptr(),
+                                      status.data_ptr(), _lib.stream_ptr()), "render_lidar")
+    shp = batch.shape
+    return LidarReturn(depth.reshape(shp), op.reshape(shp),
+                       None if oh is None else oh[:, 0].reshape(shp),
+                       None if oh is None else oh[:, 1].reshape(shp),
+                       None if of is None else of.reshape(*shp, 8), saved, status)
+
+
 def render_lidar_ranges(scene, octrees, batch, *, chunk: int = 65536) -> torch.Tensor:
-    """render_ray.py:297-306: expected range per ray, (beams, steps), NaN = no return."""
+    """render_ray.py:297-306: expected range per ray, (beams, steps), NaN = no return.
+
+    One fused launch without colour (the reference evaluates colour for every
+    segment and discards it here)."""
     del chunk
-    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs)
-    check_status(rec)
-    return rec.depth.reshape(batch.shape)
+    ret = render_lidar(scene, octrees, batch)
+    st = ret.status
+    if st.numel() and bool((st & 1).any()):
+        raise RuntimeError("octree marching failed to terminate")
+    if st.numel() and bool((st & 2).any()):
+        raise ValueError("query point outside the octree root cube")
+    return ret.depth
 
 
 def segments(scene, octrees, origins, dirs, stop_threshold: float = STOP_THRESHOLD):

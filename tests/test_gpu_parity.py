@@ -213,3 +213,36 @@ def test_sensor_rays_match_reference(golden, golden_meta, name):
     np.testing.assert_allclose(_np(b.dirs), golden[f"rays_{name}_d"], rtol=0, atol=1e-12)
     np.testing.assert_allclose(_np(b.t_stamps), golden[f"rays_{name}_t"], rtol=0, atol=1e-12)
     np.testing.assert_array_equal(b.valid.cpu().numpy(), golden[f"rays_{name}_valid"])
+
+
+def test_lidar_ranges_and_extension(golden):
+    """render_lidar_ranges equals integrate_rays' depth; the intensity / ray-drop
+    extension blends features with the reference's own weights (the blended
+    feature is pinned through the oracle's weights; the head has no reference)."""
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.sensors import RayBatch
+    sc = load_golden_scene("rand300i")
+    oc = RY.build_scene_octrees(sc)
+    o, d = golden["integ_o"], golden["integ_d"]
+    n = o.shape[0]
+    b = RayBatch(torch.as_tensor(o, device="cuda"), torch.as_tensor(d, device="cuda"),
+                 torch.zeros(n, device="cuda"), torch.zeros((n, 2), device="cuda"),
+                 torch.ones(n, dtype=torch.bool, device="cuda"), (n,))
+    dep = RY.render_lidar_ranges(sc, oc, b)
+    assert_image_close(_np(dep), golden["integ_depth"])
+    rng = np.random.default_rng(5)
+    feat = rng.uniform(-1, 1, (sc.static.n, 8)).astype(np.float32)
+    head = rng.uniform(-0.5, 0.5, (2, 13)).astype(np.float32)
+    ret = RY.render_lidar(sc, oc, b, features=feat, head=head, want_feature=True)
+    # oracle: F = sum_i w_i f_vid_i over included segments, with the reference's weights
+    vox = oracle_voxels(sc)
+    rec = O.integrate_rays(vox, O.build_octree(vox), o, d)
+    w = np.where(rec["included"], rec["t_before"] * np.clip(rec["alpha"], 0, O.ALPHA_MAX), 0.0)
+    F = np.zeros((n, 8))
+    np.add.at(F, rec["ray"], w[:, None] * feat[rec["vid"]].astype(np.float64))
+    np.testing.assert_allclose(_np(ret.feature), F, atol=1e-5)
+    D = np.nan_to_num(rec["depth"], nan=0.0)
+    z = F @ head[:, :8].T.astype(np.float64) + D[:, None] * head[:, 8] + d @ head[:, 9:12].T + head[:, 12]
+    ref = 1.0 / (1.0 + np.exp(-z))
+    np.testing.assert_allclose(_np(ret.intensity), ref[:, 0], atol=1e-5)
+    np.testing.assert_allclose(_np(ret.drop_prob), ref[:, 1], atol=1e-5)
