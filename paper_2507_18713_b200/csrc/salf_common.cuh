@@ -196,13 +196,54 @@ __device__ __forceinline__ float warp_transpose_reduce(float v[32]) {
   return v[0];
 }
 
+// Gradient of one included segment (reference backward.py:52-100): the 27
+// parameter components, written as fp32 into g[0..26] (g[27..31] = 0).  The
+// scalar chain (g_alpha, g_sigma, ds, gz) is fp64; the outer products are
+// fp32 -- they only feed fp32 warp partial sums of an fp64 accumulation.
+//   A = dL/dw, tb = T_before, w = tb * alpha, suffix = sum_{j>i} A_j w_j,
+//   tail = (dC . background) * T_final.
+__device__ __forceinline__ void segment_grad(int mode, double delta, double sigma, double alpha, double om,
+                                             double s, double e, double a, double inv_b, const double x[3],
+                                             const double c[3], const double dir[3], double A, double tb,
+                                             double w, double suffix, double tail, const double dC[3],
+                                             float g[32]) {
+  const double g_alpha = __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, alpha)));
+  // exp(-sigma delta) = 1 - alpha (unclamped) from the forward's expm1
+  const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, delta),
+                                   alpha >= kAlphaMax ? exp(__dmul_rn(-sigma, delta)) : om);
+  double ds;
+  if (mode == SALF_DENSITY_SDF) {
+    const double k2 = __dmul_rn(__dmul_rn(a, 0.5), inv_b);
+    ds = (s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), e);
+    g[25] = (float)__dmul_rn(g_sigma, sigma);
+    g[26] = (float)__dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, s), e));
+  } else {
+    ds = __dmul_rn(g_sigma, sigma);
+    g[25] = 0.0f;
+    g[26] = 0.0f;
+  }
+  const float fx[3] = {(float)x[0], (float)x[1], (float)x[2]};
+  const float fds = (float)ds;
+  g[0] = fds * fx[0]; g[1] = fds * fx[1]; g[2] = fds * fx[2]; g[3] = fds;
+  const float gam[4] = {(float)kShC0, (float)(kShC1 * dir[1]), (float)(kShC1 * dir[2]), (float)(kShC1 * dir[0])};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float gz = (float)__dmul_rn(__dmul_rn(__dmul_rn(dC[i], w), c[i]), __dsub_rn(1.0, c[i]));
+#pragma unroll
+    for (int j = 0; j < 3; ++j) g[4 + 3 * i + j] = gz * fx[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[13 + 4 * i + j] = gz * gam[j];
+  }
+#pragma unroll
+  for (int k = kGradStride; k < 32; ++k) g[k] = 0.0f;
+}
+
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes
 // of a converged warp.  Lanes holding the same voxel id form a group; a group
 // of >= 3 lanes is summed with one transposed reduction, after which lanes
 // 0..26 each issue one coalesced fp64 atomic; lanes of smaller groups add
-// their fp64 values directly.
-__device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t vid, bool active,
-                                             const double g[kGradStride]) {
+// their values directly.  g is consumed (overwritten).
+__device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t vid, bool active, float g[32]) {
   const unsigned full = 0xffffffffu;
   unsigned pending = __ballot_sync(full, active);
   if (!pending) return;
@@ -219,13 +260,13 @@ __device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t 
         double *dst = grad + lkey * kGradStride;
 #pragma unroll
         for (int k = 0; k < kGradStride; ++k)
-          if (g[k] != 0.0) atomicAdd(dst + k, g[k]);
+          if (g[k] != 0.0f) atomicAdd(dst + k, (double)g[k]);
       }
       continue;
     }
     float v[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) v[k] = (k < kGradStride && mem) ? (float)g[k] : 0.0f;
+    for (int k = 0; k < 32; ++k) v[k] = mem ? g[k] : 0.0f;
     const float tot = warp_transpose_reduce(v);
     if (lane < kGradStride && tot != 0.0f) atomicAdd(grad + lkey * kGradStride + lane, (double)tot);
   }

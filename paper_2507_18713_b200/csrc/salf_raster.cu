@@ -396,39 +396,11 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
 // ---------------------------------------------------------------------------
 // backward
 
-// Gradient of one included segment (backward.py:52-100), written into g[27].
-__device__ __forceinline__ void segment_grad(int mode, const SegVals &sv, const double om[3], double A,
-                                             double tb, double a_cl, double w, double suffix, double tail,
-                                             const double dC[3], double g[kGradStride]) {
-  const double g_alpha = __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, a_cl)));
-  // exp(-sigma delta) = 1 - alpha (unclamped) from the forward's expm1
-  const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta), sv.alpha >= kAlphaMax ?
-                                   exp(__dmul_rn(-sv.sigma, sv.delta)) : sv.om);
-  double ds;
-  if (mode == SALF_DENSITY_SDF) {
-    const double k2 = __dmul_rn(__dmul_rn(sv.a, 0.5), sv.inv_b);
-    ds = (sv.s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), sv.e);
-    g[25] = __dmul_rn(g_sigma, sv.sigma);
-    g[26] = __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, sv.s), sv.e));
-  } else {
-    ds = __dmul_rn(g_sigma, sv.sigma);
-    g[25] = 0.0;
-    g[26] = 0.0;
-  }
-  g[0] = __dmul_rn(ds, sv.x[0]); g[1] = __dmul_rn(ds, sv.x[1]); g[2] = __dmul_rn(ds, sv.x[2]); g[3] = ds;
-  const double gam[4] = {kShC0, __dmul_rn(kShC1, om[1]), __dmul_rn(kShC1, om[2]), __dmul_rn(kShC1, om[0])};
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    const double gz = __dmul_rn(__dmul_rn(__dmul_rn(dC[i], w), sv.c[i]), __dsub_rn(1.0, sv.c[i]));
-#pragma unroll
-    for (int j = 0; j < 3; ++j) g[4 + 3 * i + j] = __dmul_rn(gz, sv.x[j]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) g[13 + 4 * i + j] = __dmul_rn(gz, gam[j]);
-  }
-}
-
 template <bool kExactColor>
-__global__ void __launch_bounds__(256, 2) k_backward(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+#ifndef SALF_BWD_MINB
+#define SALF_BWD_MINB 2
+#endif
+__global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                   const int64_t *__restrict__ offsets,
                                                   const int32_t *__restrict__ entries,
                                                   const double *__restrict__ saved, const double *__restrict__ d_rgb,
@@ -482,7 +454,7 @@ __global__ void __launch_bounds__(256, 2) k_backward(salf_scene_t sc, PinholeDev
     __syncthreads();
     for (int j = 0; j < cn; ++j) {
       const int64_t jj = base - beg + j;
-      double g[kGradStride];
+      float g[32];
       bool act = false;
       int64_t vid = sm[j].vid;
       double t0, t1;
@@ -497,7 +469,8 @@ __global__ void __launch_bounds__(256, 2) k_backward(salf_scene_t sc, PinholeDev
               __ddiv_rn(__dmul_rn(dd, __dsub_rn(sv.tm, D)), ws));
           prefix = __dadd_rn(prefix, __dmul_rn(A, w));
           const double suffix = __dsub_rn(total, prefix);
-          segment_grad(sc.density_mode, sv, r.d, A, T, sv.alpha, w, suffix, tail, dC, g);
+          segment_grad(sc.density_mode, sv.delta, sv.sigma, sv.alpha, sv.om, sv.s, sv.e, sv.a, sv.inv_b, sv.x, sv.c,
+                       r.d, A, T, w, suffix, tail, dC, g);
           act = true;
           T = __dmul_rn(T, sv.om);
         }

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
   while (__any_sync(0xffffffffu, live)) {
     bool act = false;
     int64_t vid = 0;
-    double g[kGradStride];
+    float g[32];
     if (live) {
       double s0, s1;
       if (m.step(t, vid, s0, s1, st)) {
@@ -455,32 +455,8 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
               __ddiv_rn(__dmul_rn(dd, __dsub_rn(sv.tm, D)), ws));
           prefix = __dadd_rn(prefix, __dmul_rn(A, w));
           const double suffix = __dsub_rn(total, prefix);
-          const double g_alpha =
-              __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, a)));
-          const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, sv.delta),
-                                           a >= kAlphaMax ? exp(__dmul_rn(-sv.sigma, sv.delta)) : sv.om);
-          double ds;
-          if (sc.density_mode == SALF_DENSITY_SDF) {
-            const double k2 = __dmul_rn(__dmul_rn(sv.a, 0.5), sv.inv_b);
-            ds = (sv.s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), sv.e);
-            g[25] = __dmul_rn(g_sigma, sv.sigma);
-            g[26] = __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, sv.s), sv.e));
-          } else {
-            ds = __dmul_rn(g_sigma, sv.sigma);
-            g[25] = 0.0;
-            g[26] = 0.0;
-          }
-          g[0] = __dmul_rn(ds, sv.x[0]); g[1] = __dmul_rn(ds, sv.x[1]); g[2] = __dmul_rn(ds, sv.x[2]); g[3] = ds;
-          const double gam[4] = {kShC0, __dmul_rn(kShC1, m.d[1]), __dmul_rn(kShC1, m.d[2]),
-                                 __dmul_rn(kShC1, m.d[0])};
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double gz = __dmul_rn(__dmul_rn(__dmul_rn(dC[c], w), sv.c[c]), __dsub_rn(1.0, sv.c[c]));
-#pragma unroll
-            for (int j = 0; j < 3; ++j) g[4 + 3 * c + j] = __dmul_rn(gz, sv.x[j]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) g[13 + 4 * c + j] = __dmul_rn(gz, gam[j]);
-          }
+          segment_grad(sc.density_mode, sv.delta, sv.sigma, sv.alpha, sv.om, sv.s, sv.e, sv.a, sv.inv_b, sv.x, sv.c,
+                       m.d, A, tb, w, suffix, tail, dC, g);
           act = true;
           T = __dmul_rn(T, sv.om);
           t_run = __dmul_rn(t_run, __dsub_rn(1.0, a));

@@ -19,6 +19,6 @@ lb = gen_lidar_rays(configs.c3_lidar())
 for _ in range(3):
     fb, st = RR.rasterize(ds, cam, return_state=True)
     RR.rasterize_backward(st, dc, dd, as_dict=False)
-    RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
+    RY.render_lidar(ds, oc, lb)
 torch.cuda.synchronize()
 print("ok")
