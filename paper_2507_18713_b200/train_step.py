@@ -5,68 +5,84 @@ Mirrors the loss/backward part of the reference's train_loop step
 (trainer.py:156-161: integrate/rasterize, loss_color, loss_depth,
 backward_records); regularisers, Adam and densification are later §8(f) rows.
 Cameras are rasterized (pinhole) in row bands; LiDARs go through the ray path
-in ray blocks (parallel.py).
+in ray blocks (parallel.py).  The step is split in two phases so the global
+normalisation counts (reference losses.py:29-30, :44-45) can be all-reduced
+between them.
 """
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import torch
 
-from . import _lib
 from . import render_raster as RR
 from . import render_ray as RY
 from .backward import backward_grad_buffer
 from .parallel import allreduce_, band_camera
-from .sensors import CameraModel, gen_lidar_rays
+from .sensors import gen_lidar_rays
 
 
-def rig_step(ds, octree, sensors, targets, items, grad: torch.Tensor, depth_weight: float = 10.0):
-    """One rank's share of a training step.
+@dataclass
+class ForwardState:
+    items: list
+    saved: list  # per item: (state, diff)
+    counts: torch.Tensor  # [n_color_terms, n_depth_returns] of this rank
+    losses: torch.Tensor  # [sum |C - gt|, sum |D - gt|] of this rank
 
-    sensors: list of CameraModel (pinhole) / LidarModel; targets[i]: (H, W, 3)
-    gt colour for cameras, (beams*steps,) gt range for LiDARs (CUDA tensors).
-    items: this rank's WorkItems.  Accumulates into `grad` (M, 27) and
-    all-reduces it; returns (color_loss_sum, depth_loss_sum, counts)."""
+
+def rig_forward(ds, octree, sensors, targets, items) -> ForwardState:
+    """Forward of this rank's work items; targets[i]: (H, W, 3) gt colour for
+    cameras, (beams * steps,) gt range for LiDARs."""
     dev = ds.device
-    fwd = []
-    n_color = torch.zeros(1, dtype=torch.float64, device=dev)
-    n_depth = torch.zeros(1, dtype=torch.float64, device=dev)
-    l_color = torch.zeros(1, dtype=torch.float64, device=dev)
-    l_depth = torch.zeros(1, dtype=torch.float64, device=dev)
+    counts = torch.zeros(2, dtype=torch.float64, device=dev)
+    losses = torch.zeros(2, dtype=torch.float64, device=dev)
+    saved = []
     for it in items:
         s = sensors[it.sensor]
         if it.kind == "raster_band":
-            cam = band_camera(s, it.lo, it.hi)
-            fb, st = RR.rasterize(ds, cam, return_state=True)
-            gt = targets[it.sensor][it.lo:it.hi].to(dev)
+            fb, st = RR.rasterize(ds, band_camera(s, it.lo, it.hi), return_state=True)
+            gt = torch.as_tensor(targets[it.sensor], device=dev)[it.lo:it.hi]
             diff = fb.color.double() - gt.double()
-            n_color += diff.numel()
-            l_color += diff.abs().sum()
-            fwd.append((it, st, diff))
+            counts[0] += diff.numel()
+            losses[0] += diff.abs().sum()
+            saved.append((st, diff))
         else:
             rays = gen_lidar_rays(s, device=dev)
-            o, d = rays.origins[it.lo:it.hi], rays.dirs[it.lo:it.hi]
-            rec = RY.integrate_rays(ds, octree, o, d)
-            gt = targets[it.sensor][it.lo:it.hi].to(dev).double()
+            rec = RY.integrate_rays(ds, octree, rays.origins[it.lo:it.hi], rays.dirs[it.lo:it.hi])
+            gt = torch.as_tensor(targets[it.sensor], device=dev)[it.lo:it.hi].double()
             dep = rec.depth.double()
             ok = torch.isfinite(dep) & torch.isfinite(gt)
             diff = torch.where(ok, dep - gt, torch.zeros_like(dep))
-            n_depth += ok.sum()
-            l_depth += diff.abs().sum()
-            fwd.append((it, rec, diff))
-    # global normalisation: L1 means over all ranks' selected rays
-    counts = torch.cat([n_color, n_depth])
-    allreduce_(counts)
-    for it, st, diff in fwd:
+            counts[1] += ok.sum()
+            losses[1] += diff.abs().sum()
+            saved.append((rec, diff))
+    return ForwardState(items, saved, counts, losses)
+
+
+def rig_backward(fs: ForwardState, grad: torch.Tensor, global_counts: torch.Tensor,
+                 depth_weight: float = 10.0) -> torch.Tensor:
+    """L1 seeds normalised by the global counts, backward into `grad` (M, 27)."""
+    n_c = global_counts[0].clamp_min(1.0)
+    n_d = global_counts[1].clamp_min(1.0)
+    for it, (st, diff) in zip(fs.items, fs.saved):
         if it.kind == "raster_band":
-            dc = torch.sign(diff) / counts[0].clamp_min(1.0)
-            dd = torch.zeros(diff.shape[:2], dtype=torch.float64, device=dev)
+            dc = torch.sign(diff) / n_c
+            dd = torch.zeros(diff.shape[:2], dtype=torch.float64, device=diff.device)
             RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
         else:
-            dd = depth_weight * torch.sign(diff) / counts[1].clamp_min(1.0)
-            dc = torch.zeros((diff.shape[0], 3), dtype=torch.float64, device=dev)
+            dd = depth_weight * torch.sign(diff) / n_d
+            dc = torch.zeros((diff.shape[0], 3), dtype=torch.float64, device=diff.device)
             backward_grad_buffer(st, dc, dd, grad)
+    return grad
+
+
+def rig_step(ds, octree, sensors, targets, items, grad: torch.Tensor, depth_weight: float = 10.0):
+    """One rank's share of a training step; all-reduces the counts, the
+    gradient buffer and the loss sums.  Returns (loss_sums, global_counts)."""
+    fs = rig_forward(ds, octree, sensors, targets, items)
+    counts = allreduce_(fs.counts.clone())
+    rig_backward(fs, grad, counts, depth_weight)
     allreduce_(grad)
-    losses = torch.cat([l_color, l_depth])
-    allreduce_(losses)
+    losses = allreduce_(fs.losses.clone())
     return losses, counts

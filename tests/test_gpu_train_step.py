@@ -1,0 +1,98 @@
+"""GPU: the C5 multi-sensor step (cameras rasterized in row bands, LiDAR in ray
+blocks, global L1 normalisation) equals the oracle's composition of the
+reference backward over all sensors, and sharding over virtual ranks sums to
+the same gradient."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import grads_close, load_golden_scene, oracle_voxels
+from oracle import salf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _rig():
+    from paper_2507_18713_b200.sensors import CameraModel, LidarModel, look_at_quaternion
+    cams = []
+    for pos in ([13.0, 11.0, 7.0], [-4.0, 9.0, 5.0]):
+        cams.append(CameraModel(kind="pinhole", width=48, height=40, fx=45.0, fy=45.0, cx=24.0, cy=20.0,
+                                position=np.array(pos), quaternion=look_at_quaternion(pos, [4.0, 4.0, 2.0])))
+    lid = LidarModel(beam_elevations=np.linspace(-0.5, 0.3, 8), steps=60, position=np.array([4.013, 3.987, 2.5]),
+                     linear_velocity=np.array([1.0, 0.0, 0.0]))
+    return cams + [lid]
+
+
+def _targets(sensors):
+    rng = np.random.default_rng(9)
+    out = []
+    for s in sensors:
+        if hasattr(s, "width"):
+            out.append(torch.as_tensor(rng.uniform(0, 1, (s.height, s.width, 3)), device="cuda"))
+        else:
+            out.append(torch.as_tensor(rng.uniform(1, 8, s.beam_elevations.shape[0] * s.steps), device="cuda"))
+    return out
+
+
+def _oracle_grad(sc, sensors, targets, depth_weight=10.0):
+    vox = oracle_voxels(sc)
+    tree = O.build_octree(vox)
+    recs = []
+    for s, gt in zip(sensors, targets):
+        gt = gt.cpu().numpy()
+        if hasattr(s, "width"):
+            cam = O.Camera("pinhole", s.width, s.height, s.fx, s.fy, s.cx, s.cy, position=s.position,
+                           quaternion=s.quaternion)
+            recs.append(("c", O.raster_records(vox, cam), gt.reshape(-1, 3)))
+        else:
+            lid = O.Lidar(s.beam_elevations, s.azimuth_start, s.azimuth_end, s.steps, s.scan_period, s.position,
+                          s.quaternion, s.linear_velocity, s.angular_velocity)
+            rays = O.lidar_rays(lid)
+            recs.append(("l", O.integrate_rays(vox, tree, rays["origins"], rays["dirs"]), gt))
+    n_c = sum(r["out_color"].size for k, r, _ in recs if k == "c")
+    n_d = sum(int((np.isfinite(r["depth"]) & np.isfinite(gt)).sum()) for k, r, gt in recs if k == "l")
+    tot = None
+    for k, r, gt in recs:
+        if k == "c":
+            dc = np.sign(r["out_color"] - gt) / n_c
+            dd = np.zeros(r["n_rays"])
+        else:
+            ok = np.isfinite(r["depth"]) & np.isfinite(gt)
+            dd = np.where(ok, depth_weight * np.sign(np.nan_to_num(r["depth"]) - gt) / n_d, 0.0)
+            dc = np.zeros((r["n_rays"], 3))
+        g = O.backward_records(r, vox, dc, dd)
+        tot = g if tot is None else {q: tot[q] + g[q] for q in g}
+    return tot
+
+
+def test_rig_step_matches_oracle_and_sharding_is_exact():
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.device import DeviceScene, grads_to_dict
+    from paper_2507_18713_b200.parallel import assign, split_work
+    from paper_2507_18713_b200.train_step import rig_backward, rig_forward, rig_step
+    sc = load_golden_scene("rand300")
+    ds = DeviceScene.from_scene(sc)
+    oc = RY.build_scene_octrees(sc)
+    sensors = _rig()
+    targets = _targets(sensors)
+    grad = torch.zeros((ds.n, 27), dtype=torch.float64, device="cuda")
+    rig_step(ds, oc, sensors, targets, split_work(sensors, 1), grad)
+    want = _oracle_grad(sc, sensors, targets)
+    assert grads_close(grads_to_dict(grad), want) < 1e-4
+    # four virtual ranks: bands + ray blocks, counts summed between the phases
+    per = assign(split_work(sensors, 4, tile=16), 4)
+    assert sum(len(p) for p in per) > len(sensors)  # cameras really are cut into bands
+    states = [rig_forward(ds, oc, sensors, targets, items) for items in per]
+    counts = sum(fs.counts for fs in states)
+    g2 = torch.zeros_like(grad)
+    for fs in states:
+        rig_backward(fs, g2, counts)
+    assert grads_close(grads_to_dict(g2), grads_to_dict(grad)) < 1e-6
