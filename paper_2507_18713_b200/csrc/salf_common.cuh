@@ -159,6 +159,19 @@ __device__ __forceinline__ void eval_color32(const VoxPrm &p, const double xd[3]
   }
 }
 
+// fp32 colour with a precomputed per-ray SH basis gam = (C0, C1 y, C1 z, C1 x).
+__device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3], const float gam[4], float c[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float z = __fmaf_rn(p.wc[3 * i + 2], x[2], __fmaf_rn(p.wc[3 * i + 1], x[1], p.wc[3 * i] * x[0]));
+    z = __fmaf_rn(p.wsh[4 * i + 0], gam[0], z);
+    z = __fmaf_rn(p.wsh[4 * i + 1], gam[1], z);
+    z = __fmaf_rn(p.wsh[4 * i + 2], gam[2], z);
+    z = __fmaf_rn(p.wsh[4 * i + 3], gam[3], z);
+    c[i] = __frcp_rn(1.0f + __expf(-z));
+  }
+}
+
 // (N,3) @ (3,3) as NumPy/OpenBLAS computes it on x86: fma(a2, b2, fma(a1, b1, a0*b0)).
 // r is row-major; `transposed` selects a @ r.T (dot with row i) vs a @ r (column i).
 __device__ __forceinline__ double mm_row(const double a[3], const double *r, int i) {

@@ -212,11 +212,14 @@ struct Entry {
   double hi[3];  //   half  - o
   double half;   // 0.5 * edge
   double inv_half;
+  double a, inv_b;  // density transfer (aux)
   int64_t vid;
+  VoxPrm p;       // field parameters, staged once per tile chunk
 };
 
 struct PixelRay {
   double d[3], inv[3], t_near;
+  float gam[4];  // SH basis of the pixel direction (fp32 colour path)
   bool zero[3];
   bool pos[3];  // inv > 0: the slab's near face is the low face (no per-pair min/max)
   bool fast;    // all components non-zero with finite reciprocals (no NaN can arise)
@@ -234,6 +237,10 @@ __device__ __forceinline__ void pixel_ray(const PinholeDev &c, int px, int py, P
   for (int k = 0; k < 3; ++k) r.d[k] = mm_row(dc, c.rot, k);  // d_cam @ R.T
   const double dz = mm_col(r.d, c.rot, 2);                   // (dirs @ R)[:, 2]
   r.t_near = __ddiv_rn(c.near, dz);
+  r.gam[0] = (float)kShC0;
+  r.gam[1] = (float)(kShC1 * r.d[1]);
+  r.gam[2] = (float)(kShC1 * r.d[2]);
+  r.gam[3] = (float)(kShC1 * r.d[0]);
   r.fast = true;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -287,6 +294,7 @@ __device__ __forceinline__ bool pair_hit(const PixelRay &r, const Entry &e, doub
 
 struct SegVals {
   double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
+  float cf[3];  // fp32 colour (fast mode)
 };
 
 // Fields of one hit pair (render_raster.py:239-253).  Divisions by 0.5*edge
@@ -298,22 +306,28 @@ __device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const PixelRa
   sv.tm = __dmul_rn(0.5, __dadd_rn(t0, t1));
 #pragma unroll
   for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, r.d[k])), e.inv_half);
-  VoxPrm p;
-  load_prm(sc.prm, e.vid, p);
-  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.aux + 4 * e.vid));
-  sv.a = ab.x;
-  sv.inv_b = ab.y;
-  sv.s = eval_sdf(p, sv.x);
-  sv.sigma = density(sc.density_mode, sv.s, ab.x, ab.y, sv.e);
+  sv.a = e.a;
+  sv.inv_b = e.inv_b;
+  sv.s = eval_sdf(e.p, sv.x);
+  sv.sigma = density(sc.density_mode, sv.s, e.a, e.inv_b, sv.e);
   sv.alpha = seg_alpha(sv.sigma, sv.delta, sv.om);
-  if (kExactColor) eval_color64(p, sv.x, r.d, sv.c);
-  else eval_color32(p, sv.x, r.d, sv.c);
+  if (kExactColor) {
+    eval_color64(e.p, sv.x, r.d, sv.c);
+  } else {
+    const float xf[3] = {(float)sv.x[0], (float)sv.x[1], (float)sv.x[2]};
+    eval_color32g(e.p, xf, r.gam, sv.cf);
+    sv.c[0] = sv.cf[0]; sv.c[1] = sv.cf[1]; sv.c[2] = sv.cf[2];
+  }
 }
 
 __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const PinholeDev &c, int32_t vid,
                                             Entry &e) {
   const double4 g = ldg_d4(sc.geo + 4 * (int64_t)vid);
+  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.aux + 4 * (int64_t)vid));
   e.vid = vid;
+  e.a = ab.x;
+  e.inv_b = ab.y;
+  load_prm(sc.prm, vid, e.p);
   e.half = __dmul_rn(0.5, g.w);
   e.inv_half = 1.0 / e.half;
   e.o[0] = __dsub_rn(c.pos[0], g.x);
@@ -326,7 +340,7 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
   }
 }
 
-constexpr int kChunk = 128;
+constexpr int kChunk = 64;  // entries staged per step (192 B each in shared memory)
 
 template <bool kExactColor>
 __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
@@ -348,6 +362,7 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
   // transmittance kept as a running product of (1 - alpha) (the reference's
   // exp(cumsum(log1p(-alpha))), render_raster.py:258-274, to ~1e-15)
   double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0;
+  float acc_cf[3] = {0.0f, 0.0f, 0.0f};  // fast mode: fp32 colour sums (outputs are fp32)
   bool alive = inside;
   int64_t n_stop = end - beg;
   const int nthreads = blockDim.x;
@@ -365,8 +380,14 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
         shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv);
         if (T > keep) {  // included iff T_before > 1 - stop_threshold
           const double w = __dmul_rn(T, sv.alpha);
+          if (kExactColor) {
 #pragma unroll
-          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+            for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
+          } else {
+            const float wf = (float)w;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) acc_cf[k] = __fmaf_rn(wf, sv.cf[k], acc_cf[k]);
+          }
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
           T = __dmul_rn(T, sv.om);
@@ -380,6 +401,9 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
     if (!__syncthreads_or(alive)) break;
   }
   if (!inside) return;
+  if (!kExactColor) {
+    acc_c[0] = acc_cf[0]; acc_c[1] = acc_cf[1]; acc_c[2] = acc_cf[2];
+  }
   const int64_t pix = (int64_t)py * c.width + px;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
