@@ -82,6 +82,8 @@ class CpuBaseline:
     def __init__(self, regime="init", workers=None):
         n = workers or min(len(os.sched_getaffinity(0)), 64)
         self.workers = n
+        from paper_2507_18713_b200.scenes import get_scene
+        get_scene("S1M", regime)  # build the cached container once, before the workers start
         import multiprocessing as mp
         self.pool = ProcessPoolExecutor(n, mp_context=mp.get_context("spawn"), initializer=_cpu_init,
                                         initargs=(regime,))

@@ -295,6 +295,15 @@ def get_scene(name: str, regime: str = "init", cache: bool = True) -> Scene:
         elif regime != "init":
             raise ValueError(f"unknown regime {regime!r}")
     if cache:
-        save_scene(scene, d)
+        # atomic publish: concurrent builders (spawned CPU-baseline workers)
+        # never observe a half-written container
+        import os
+        import shutil
+        tmp = d.parent / f".{d.name}.tmp{os.getpid()}"
+        save_scene(scene, tmp)
+        try:
+            os.rename(tmp, d)
+        except OSError:
+            shutil.rmtree(tmp, ignore_errors=True)  # another process published first
         return load_scene(d)[0]  # f32 round trip, identical to what the reference loads
     return scene
