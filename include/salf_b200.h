@@ -207,6 +207,35 @@ int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int6
                       const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,
                       const double *d_depth, double *grad, void *stream);
 
+/* ---- rest of the training step ---------------------
+ * Parameter block `params`: (M, 27) f64 rows w_s[4] w_c[9] w_sh[12] log_a
+ * log_b, the gradient buffer's layout. */
+
+/* adam_step (optim.py:48-62): one update of n = M*27 values; step = t >= 1. */
+int salf_adam_step(int64_t n, double *params, const double *grad, double *m, double *v, double lr,
+                   double beta1, double beta2, double eps, int64_t step, void *stream);
+
+/* Refresh the device scene's prm (f32) and aux (a, 1/b) from the block. */
+int salf_scene_refresh(const double *params, int64_t n_voxels, float *prm, double *aux, void *stream);
+
+/* loss_eikonal (losses.py:49-60) over voxel indices idx; adds gradients into
+ * grad and sum |.| into *loss_sum (device). */
+int salf_loss_eikonal(const double *params, int64_t n_idx, const int64_t *idx, double *grad,
+                      double *loss_sum, void *stream);
+
+/* Centre opacity over the voxel edge (loss_empty's ranking key, losses.py:216-228). */
+int salf_center_alpha(const double *params, const double *geo, int32_t density_mode, int64_t n_idx,
+                      const int64_t *idx, double *alpha, void *stream);
+
+/* loss_empty gradient (losses.py:230-249) for the k lowest-opacity outer voxels sel. */
+int salf_loss_empty_grad(const double *params, const double *geo, int32_t density_mode, int64_t k,
+                         const int64_t *sel, double *grad, void *stream);
+
+/* loss_opacity_lidar (losses.py:188-226) for n points located in leaves vid. */
+int salf_loss_opacity_lidar(const double *params, const double *geo, int32_t density_mode, int64_t n,
+                            const double *points, const int64_t *vid, double *grad, double *loss_sum,
+                            void *stream);
+
 #ifdef __cplusplus
 }
 #endif

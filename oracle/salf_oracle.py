@@ -796,3 +796,88 @@ def loss_depth_seed(depth, gt, mask):
     if idx.size:
         d[idx] = np.sign(depth[idx] - gt[ok]) / idx.size
     return d
+
+
+# ---------------------------------------------------------------------------
+# rest of the training step (reference optim.py:43-62, losses.py:49-249)
+
+def adam_step(params, grads, m, v, step, lr=0.01, lr_decay=0.8, every=800, b1=0.9, b2=0.999,
+              eps=1e-8):
+    """optim.py:48-62 on dicts of arrays; `step` is the count before this update."""
+    rate = lr * lr_decay ** (step // every)
+    t = step + 1
+    c1, c2 = 1.0 - b1 ** t, 1.0 - b2 ** t
+    for k in params:
+        m[k] = b1 * m[k] + (1.0 - b1) * grads[k]
+        v[k] = b2 * v[k] + (1.0 - b2) * grads[k] * grads[k]
+        params[k] -= rate * (m[k] / c1) / (np.sqrt(v[k] / c2) + eps)
+    return rate
+
+
+def loss_eikonal(vox: Voxels, idx):
+    """losses.py:49-60."""
+    g = np.zeros_like(vox.w_s)
+    if idx.size == 0:
+        return 0.0, g
+    w = vox.w_s[idx, :3]
+    nrm = np.linalg.norm(w, axis=1)
+    ok = nrm > 1e-12
+    gr = np.zeros_like(w)
+    gr[ok] = (np.sign(nrm - 1.0) / idx.size)[ok, None] * (w[ok] / nrm[ok, None])
+    np.add.at(g[:, :3], idx, gr)
+    return float(np.abs(nrm - 1.0).mean()), g
+
+
+def _density_grad_parts(vox, vid, s):
+    a, b = np.exp(vox.log_a[vid]), np.exp(vox.log_b[vid])
+    return a, b, sdf_to_density(s, a, b)
+
+
+def loss_empty(vox: Voxels, outer):
+    """losses.py:210-249 (lowest 20% centre opacities of outer voxels)."""
+    g = dict(w_s=np.zeros_like(vox.w_s), log_a=np.zeros_like(vox.log_a), log_b=np.zeros_like(vox.log_b))
+    if outer.size == 0:
+        return 0.0, g
+    s = vox.w_s[outer, 3]
+    edge = vox.edges[outer]
+    a, b, sig = _density_grad_parts(vox, outer, s)
+    alpha = -np.expm1(-sig * edge)
+    k = max(1, int(np.ceil(0.2 * outer.size)))
+    order = np.argsort(alpha, kind="stable")[:k]
+    sel = outer[order]
+    g_sig = (1.0 / k) * edge[order] * np.exp(-sig[order] * edge[order])
+    e = np.exp(-np.abs(s[order]) / b[order])
+    k2 = a[order] / (2.0 * b[order])
+    ds = np.where(s[order] == 0.0, 0.0, g_sig * k2 * e)
+    np.add.at(g["w_s"], (sel, 3), ds)
+    np.add.at(g["log_a"], sel, g_sig * sig[order])
+    np.add.at(g["log_b"], sel, g_sig * (-k2 * s[order] * e))
+    return float(alpha[order].mean()), g
+
+
+def loss_opacity_lidar(vox: Voxels, tree: Octree, points, delta=0.2):
+    """losses.py:188-226."""
+    g = dict(w_s=np.zeros_like(vox.w_s), log_a=np.zeros_like(vox.log_a), log_b=np.zeros_like(vox.log_b))
+    pts = np.asarray(points, np.float64).reshape(-1, 3)
+    rmax = tree.root_min + tree.root_edge
+    pts = pts[np.all((pts >= tree.root_min) & (pts <= rmax), axis=1)]
+    if pts.shape[0] == 0:
+        return 0.0, g
+    _f, vid, _c, _e = query_batch(tree, pts)
+    keep = vid >= 0
+    vid, pts = vid[keep], pts[keep]
+    if vid.size == 0:
+        return 0.0, g
+    x = (pts - vox.centers[vid]) * (2.0 / vox.edges[vid][:, None])
+    s = eval_sdf(x, vox.w_s[vid])
+    a, b, sig = _density_grad_parts(vox, vid, s)
+    alpha = -np.expm1(-sig * delta)
+    n = vid.size
+    g_sig = (-delta * np.exp(-sig * delta)) / n
+    e = np.exp(-np.abs(s) / b)
+    k2 = a / (2.0 * b)
+    ds = np.where(s == 0.0, 0.0, g_sig * k2 * e)
+    np.add.at(g["w_s"], vid, ds[:, None] * np.concatenate([x, np.ones((n, 1))], axis=1))
+    np.add.at(g["log_a"], vid, g_sig * sig)
+    np.add.at(g["log_b"], vid, g_sig * (-k2 * s * e))
+    return float(np.mean(1.0 - alpha)), g

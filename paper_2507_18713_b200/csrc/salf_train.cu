@@ -1,0 +1,205 @@
+// salf_train.cu -- the rest of the training step on the device (SURVEY §8f
+// rank 1): Adam (reference optim.py:48-62), the scene refresh after an update,
+// and the parameter regularisers eikonal / empty-space / LiDAR opacity
+// (reference losses.py:49-60, :188-249).  All fp64, reference operation order.
+//
+// Parameter block: (M, 27) f64 rows = w_s[4] w_c[9] w_sh[12] log_a log_b
+// (the gradient buffer's layout).
+#include "salf_common.cuh"
+#include "salf_internal.h"
+
+namespace salf {
+
+// Adam with the reference's expression order:
+//   m = b1 m + (1 - b1) g ; v = b2 v + (1 - b2) g g
+//   p -= lr * (m / bias1) / (sqrt(v / bias2) + eps)
+__global__ void k_adam(int64_t n, double *__restrict__ p, const double *__restrict__ g, double *__restrict__ m,
+                       double *__restrict__ v, double lr, double b1, double b2, double eps, double bias1,
+                       double bias2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double gi = g[i];
+  const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dsub_rn(1.0, b1), gi));
+  const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, b2), gi), gi));
+  m[i] = mi;
+  v[i] = vi;
+  const double mh = __ddiv_rn(mi, bias1), vh = __ddiv_rn(vi, bias2);
+  p[i] = __dsub_rn(p[i], __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(sqrt(vh), eps)));
+}
+
+// Device scene refresh from the parameter block: prm (f32 fields), aux a, 1/b.
+__global__ void k_refresh(int64_t n, const double *__restrict__ p, float *__restrict__ prm, double *__restrict__ aux) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double *r = p + i * kGradStride;
+  float *q = prm + i * SALF_PRM_STRIDE;
+#pragma unroll
+  for (int k = 0; k < 25; ++k) q[k] = (float)r[k];
+  aux[4 * i + 0] = exp(r[25]);
+  aux[4 * i + 1] = 1.0 / exp(r[26]);
+}
+
+// loss_eikonal (losses.py:49-60): mean | ||W_s[:3]|| - 1 | over `idx`.
+__global__ void k_eikonal(int64_t n_idx, const int64_t *__restrict__ idx, const double *__restrict__ p,
+                          double *__restrict__ grad, double *__restrict__ loss_sum, double inv_n) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_idx) return;
+  const int64_t v = idx[j];
+  const double *r = p + v * kGradStride;
+  const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(r[0], r[0]), __dmul_rn(r[1], r[1])), __dmul_rn(r[2], r[2])));
+  atomicAdd(loss_sum, fabs(__dsub_rn(nrm, 1.0)));
+  if (nrm > 1e-12) {
+    const double s = __dmul_rn(npsign(__dsub_rn(nrm, 1.0)), inv_n);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) atomicAdd(grad + v * kGradStride + k, __dmul_rn(s, __ddiv_rn(r[k], nrm)));
+  }
+}
+
+// density at the voxel centre (x = 0 -> s = bias) and its opacity over the edge
+// (losses.py:216-228).
+__global__ void k_center_alpha(int64_t n_idx, const int64_t *__restrict__ idx, const double *__restrict__ p,
+                               const double *__restrict__ geo, int mode, double *__restrict__ alpha_out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n_idx) return;
+  const int64_t v = idx[j];
+  const double *r = p + v * kGradStride;
+  const double s = r[3], edge = geo[4 * v + 3];
+  double e;
+  const double sigma = density(mode, s, exp(r[25]), 1.0 / exp(r[26]), e);
+  alpha_out[j] = -expm1(__dmul_rn(-sigma, edge));
+}
+
+// loss_empty gradient (losses.py:230-249) for the k selected (lowest-alpha) outer voxels.
+__global__ void k_empty_grad(int64_t k, const int64_t *__restrict__ sel, const double *__restrict__ p,
+                             const double *__restrict__ geo, int mode, double *__restrict__ grad) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  const int64_t v = sel[j];
+  const double *r = p + v * kGradStride;
+  const double s = r[3], edge = geo[4 * v + 3];
+  const double a = exp(r[25]), b = exp(r[26]);
+  double e;
+  const double sigma = density(mode, s, a, 1.0 / b, e);
+  const double g_alpha = 1.0 / (double)k;
+  const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, edge), exp(__dmul_rn(-sigma, edge)));
+  double *gr = grad + v * kGradStride;
+  if (mode == SALF_DENSITY_SDF) {
+    const double k2 = __ddiv_rn(a, __dmul_rn(2.0, b));
+    const double ee = exp(__ddiv_rn(-fabs(s), b));
+    const double ds = (s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), ee);
+    atomicAdd(gr + 3, ds);
+    atomicAdd(gr + 25, __dmul_rn(g_sigma, sigma));
+    atomicAdd(gr + 26, __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, s), ee)));
+  } else {
+    atomicAdd(gr + 3, __dmul_rn(g_sigma, sigma));
+  }
+}
+
+// loss_opacity_lidar gradient (losses.py:188-226) for points already located
+// in leaves (vid >= 0): opacity over a 20 cm traversal driven towards 1.
+__global__ void k_opacity_lidar(int64_t n, const double *__restrict__ pts, const int64_t *__restrict__ vid,
+                                const double *__restrict__ p, const double *__restrict__ geo, int mode,
+                                double *__restrict__ grad, double *__restrict__ loss_sum) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int64_t v = vid[j];
+  const double *r = p + v * kGradStride;
+  const double4 g = make_double4(geo[4 * v], geo[4 * v + 1], geo[4 * v + 2], geo[4 * v + 3]);
+  const double sc2 = __ddiv_rn(2.0, g.w);
+  const double x[3] = {__dmul_rn(__dsub_rn(pts[3 * j], g.x), sc2), __dmul_rn(__dsub_rn(pts[3 * j + 1], g.y), sc2),
+                       __dmul_rn(__dsub_rn(pts[3 * j + 2], g.z), sc2)};
+  const double s = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], x[0]), __dmul_rn(r[2], x[2])), __dmul_rn(r[1], x[1])),
+                             r[3]);
+  const double a = exp(r[25]), b = exp(r[26]);
+  double e;
+  const double sigma = density(mode, s, a, 1.0 / b, e);
+  const double delta = 0.2;  // LIDAR_OPACITY_DELTA (losses.py:17)
+  const double alpha = -expm1(__dmul_rn(-sigma, delta));
+  atomicAdd(loss_sum, __dsub_rn(1.0, alpha));
+  const double g_sigma = __ddiv_rn(__dmul_rn(-delta, exp(__dmul_rn(-sigma, delta))), (double)n);
+  double *gr = grad + v * kGradStride;
+  double ds;
+  if (mode == SALF_DENSITY_SDF) {
+    const double k2 = __ddiv_rn(a, __dmul_rn(2.0, b));
+    const double ee = exp(__ddiv_rn(-fabs(s), b));
+    ds = (s == 0.0) ? 0.0 : __dmul_rn(__dmul_rn(g_sigma, k2), ee);
+    atomicAdd(gr + 25, __dmul_rn(g_sigma, sigma));
+    atomicAdd(gr + 26, __dmul_rn(g_sigma, __dmul_rn(__dmul_rn(-k2, s), ee)));
+  } else {
+    ds = __dmul_rn(g_sigma, sigma);
+  }
+  atomicAdd(gr + 0, __dmul_rn(ds, x[0]));
+  atomicAdd(gr + 1, __dmul_rn(ds, x[1]));
+  atomicAdd(gr + 2, __dmul_rn(ds, x[2]));
+  atomicAdd(gr + 3, ds);
+}
+
+}  // namespace salf
+
+using namespace salf;
+
+extern "C" int salf_loss_opacity_lidar(const double *params, const double *geo, int32_t density_mode, int64_t n,
+                                       const double *points, const int64_t *vid, double *grad, double *loss_sum,
+                                       void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    k_opacity_lidar<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, points, vid, params, geo,
+                                                                                   density_mode, grad, loss_sum);
+    return check_cuda("salf_loss_opacity_lidar");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_adam_step(int64_t n, double *params, const double *grad, double *m, double *v, double lr,
+                              double beta1, double beta2, double eps, int64_t step, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    const double bias1 = 1.0 - pow(beta1, (double)step), bias2 = 1.0 - pow(beta2, (double)step);
+    k_adam<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, params, grad, m, v, lr, beta1, beta2,
+                                                                          eps, bias1, bias2);
+    return check_cuda("salf_adam_step");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_scene_refresh(const double *params, int64_t n, float *prm, double *aux, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    k_refresh<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n, params, prm, aux);
+    return check_cuda("salf_scene_refresh");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_loss_eikonal(const double *params, int64_t n_idx, const int64_t *idx, double *grad,
+                                 double *loss_sum, void *stream) {
+  SALF_TRY {
+    if (n_idx == 0) return SALF_OK;
+    k_eikonal<<<(unsigned)((n_idx + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_idx, idx, params, grad, loss_sum,
+                                                                                 1.0 / (double)n_idx);
+    return check_cuda("salf_loss_eikonal");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_center_alpha(const double *params, const double *geo, int32_t density_mode, int64_t n_idx,
+                                 const int64_t *idx, double *alpha, void *stream) {
+  SALF_TRY {
+    if (n_idx == 0) return SALF_OK;
+    k_center_alpha<<<(unsigned)((n_idx + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_idx, idx, params, geo,
+                                                                                       density_mode, alpha);
+    return check_cuda("salf_center_alpha");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_loss_empty_grad(const double *params, const double *geo, int32_t density_mode, int64_t k,
+                                    const int64_t *sel, double *grad, void *stream) {
+  SALF_TRY {
+    if (k == 0) return SALF_OK;
+    k_empty_grad<<<(unsigned)((k + 255) / 256), 256, 0, (cudaStream_t)stream>>>(k, sel, params, geo, density_mode,
+                                                                                grad);
+    return check_cuda("salf_loss_empty_grad");
+  }
+  SALF_CATCH
+}

@@ -1,0 +1,153 @@
+"""Device training state: Adam (reference optim.py) and the parameter
+regularisers (reference losses.py:49-249) on the GPU.
+
+`TrainableScene` keeps the optimisable parameters as one (M, 27) f64 block
+(w_s, w_c, w_sh, log_a, log_b -- the gradient buffer's layout) with Adam
+moments beside it; after each update the render-side f32 fields and the
+density constants of the `DeviceScene` are refreshed in place by a kernel.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceScene
+from .octree import OctreeBuffer
+from .scene import Scene
+
+EMPTY_QUANTILE = 0.2
+LIDAR_OPACITY_DELTA = 0.2
+
+
+@dataclass
+class AdamConfig:
+    """optim.py:12-19."""
+
+    lr: float = 0.01
+    lr_decay: float = 0.8
+    lr_decay_every: int = 800
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+
+def learning_rate(cfg: AdamConfig, step: int) -> float:
+    """optim.py:43-45: lr * decay^(step // every)."""
+    return cfg.lr * cfg.lr_decay ** (step // cfg.lr_decay_every)
+
+
+def _block(v) -> np.ndarray:
+    m = v.n
+    b = np.empty((m, 27), np.float64)
+    b[:, 0:4] = v.w_s
+    b[:, 4:13] = v.w_c.reshape(m, 9)
+    b[:, 13:25] = v.w_sh.reshape(m, 12)
+    b[:, 25] = v.log_a
+    b[:, 26] = v.log_b
+    return b
+
+
+class TrainableScene:
+    def __init__(self, scene: Scene, device=None):
+        self.scene = scene
+        self.ds = DeviceScene.from_scene(scene, device=device)
+        dev = self.ds.device
+        self.params = torch.as_tensor(_block(scene.static), device=dev).contiguous()
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.step = 0
+
+    @property
+    def n(self) -> int:
+        return self.ds.n
+
+    def zero_grad(self) -> torch.Tensor:
+        return torch.zeros_like(self.params)
+
+    def refresh(self) -> None:
+        lib = _lib.load()
+        _lib.check(lib.salf_scene_refresh(self.params.data_ptr(), self.n, self.ds.prm.data_ptr(),
+                                          self.ds.aux.data_ptr(), _lib.stream_ptr()), "refresh")
+
+    def adam_step(self, grad: torch.Tensor, cfg: AdamConfig = AdamConfig()) -> float:
+        """optim.py:48-62: one in-place update of every parameter; returns the lr used."""
+        lib = _lib.load()
+        lr = learning_rate(cfg, self.step)
+        self.step += 1
+        _lib.check(lib.salf_adam_step(self.params.numel(), self.params.data_ptr(), grad.data_ptr(),
+                                      self.m.data_ptr(), self.v.data_ptr(), lr, cfg.beta1, cfg.beta2,
+                                      cfg.eps, self.step, _lib.stream_ptr()), "adam_step")
+        self.refresh()
+        return lr
+
+    def to_numpy(self) -> dict:
+        b = self.params.cpu().numpy()
+        m = b.shape[0]
+        return {"w_s": b[:, 0:4], "w_c": b[:, 4:13].reshape(m, 3, 3),
+                "w_sh": b[:, 13:25].reshape(m, 3, 4), "log_a": b[:, 25], "log_b": b[:, 26]}
+
+
+def _idx(idx, dev) -> torch.Tensor:
+    return torch.as_tensor(np.asarray(idx) if not isinstance(idx, torch.Tensor) else idx,
+                           dtype=torch.int64, device=dev).contiguous()
+
+
+def loss_eikonal(ts: TrainableScene, sample_idx, grad: torch.Tensor) -> float:
+    """losses.py:49-60: mean | ||W_s[:3]|| - 1 |; gradient added into grad."""
+    lib = _lib.load()
+    idx = _idx(sample_idx, grad.device)
+    if idx.numel() == 0:
+        return 0.0
+    acc = torch.zeros(1, dtype=torch.float64, device=grad.device)
+    _lib.check(lib.salf_loss_eikonal(ts.params.data_ptr(), idx.numel(), idx.data_ptr(), grad.data_ptr(),
+                                     acc.data_ptr(), _lib.stream_ptr()), "loss_eikonal")
+    return float(acc.item()) / idx.numel()
+
+
+def loss_empty(ts: TrainableScene, outer_idx, grad: torch.Tensor) -> float:
+    """losses.py:210-249: mean opacity of the lowest 20% outer voxels (stable order)."""
+    lib = _lib.load()
+    idx = _idx(outer_idx, grad.device)
+    n = idx.numel()
+    if n == 0:
+        return 0.0
+    mode = _lib.DENSITY[ts.ds.density_mode]
+    alpha = torch.empty(n, dtype=torch.float64, device=grad.device)
+    _lib.check(lib.salf_center_alpha(ts.params.data_ptr(), ts.ds.geo.data_ptr(), mode, n, idx.data_ptr(),
+                                     alpha.data_ptr(), _lib.stream_ptr()), "loss_empty")
+    k = max(1, int(np.ceil(EMPTY_QUANTILE * n)))
+    order = torch.sort(alpha, stable=True).indices[:k]
+    sel = idx[order].contiguous()
+    _lib.check(lib.salf_loss_empty_grad(ts.params.data_ptr(), ts.ds.geo.data_ptr(), mode, k, sel.data_ptr(),
+                                        grad.data_ptr(), _lib.stream_ptr()), "loss_empty")
+    return float(alpha[order].mean().item())
+
+
+def loss_opacity_lidar(ts: TrainableScene, octree: OctreeBuffer, points, grad: torch.Tensor) -> float:
+    """losses.py:188-226: drive opacity at LiDAR points towards 1 over 20 cm."""
+    from .octree import query_batch
+    lib = _lib.load()
+    pts = np.asarray(points, np.float64).reshape(-1, 3)
+    if pts.shape[0] == 0:
+        return 0.0
+    rmax = octree.root_min + octree.root_edge
+    pts = pts[np.all((pts >= octree.root_min) & (pts <= rmax), axis=1)]
+    if pts.shape[0] == 0:
+        return 0.0
+    _f, vid, _c, _e = query_batch(octree, pts)
+    sel = vid >= 0
+    if not np.any(sel):
+        return 0.0
+    dev = grad.device
+    p = torch.as_tensor(pts[sel], device=dev).contiguous()
+    v = torch.as_tensor(vid[sel], dtype=torch.int64, device=dev).contiguous()
+    acc = torch.zeros(1, dtype=torch.float64, device=dev)
+    _lib.check(lib.salf_loss_opacity_lidar(ts.params.data_ptr(), ts.ds.geo.data_ptr(),
+                                           _lib.DENSITY[ts.ds.density_mode], v.numel(), p.data_ptr(),
+                                           v.data_ptr(), grad.data_ptr(), acc.data_ptr(),
+                                           _lib.stream_ptr()), "loss_opacity_lidar")
+    return float(acc.item()) / v.numel()

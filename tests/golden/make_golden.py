@@ -199,6 +199,28 @@ def main():
                fd_depth=rec.depth, fd_dcolor=d_c, fd_ddepth=10.0 * d_d,
                **{f"fd_g_{k}": v for k, v in g.items()})
 
+    # 5b. regularisers + Adam on the FD scene (losses.py:49-249, optim.py:48-62)
+    from salf.losses import loss_eikonal, loss_empty, loss_opacity_lidar
+    from salf.optim import AdamConfig, AdamState, adam_step
+    vs = sc.static
+    all_idx = np.arange(vs.n)
+    outer = np.flatnonzero(sc.outer_voxel_mask())
+    l_e, g_e = loss_eikonal(vs, all_idx)
+    l_m, g_m = loss_empty(vs, outer)
+    l_o, g_o = loss_opacity_lidar(vs, oc.static, fx["points"])
+    out.update(reg_points=fx["points"], reg_outer=outer, reg_loss=np.array([l_e, l_m, l_o]),
+               reg_eik_w_s=g_e["w_s"], **{f"reg_emp_{k}": v for k, v in g_m.items()},
+               **{f"reg_opa_{k}": v for k, v in g_o.items()})
+    params = {k: getattr(vs, k).copy() for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
+    st = AdamState.for_params(params)
+    cfg = AdamConfig(lr_decay_every=2)
+    rng = np.random.default_rng(77)
+    gseq = [{k: rng.normal(size=v.shape) for k, v in params.items()} for _ in range(3)]
+    for gs in gseq:
+        adam_step(params, gs, st, cfg)
+    out.update(**{f"adam_g{i}_{k}": v for i, gs in enumerate(gseq) for k, v in gs.items()},
+               **{f"adam_p_{k}": v for k, v in params.items()})
+
     # 6. sensors
     pin = R_sen.CameraModel(kind="pinhole", width=32, height=24, fx=30.0, fy=31.0, cx=15.5, cy=12.25,
                             position=np.array([0.3, -0.2, 1.1]),
