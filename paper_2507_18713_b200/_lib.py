@@ -139,4 +139,4 @@ def ref(struct):
 def as_f64(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=torch.float64).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(np.asarray(x, dtype=np.float64)), device=device)
+    return torch.as_tensor(np.array(x, dtype=np.float64, order="C"), device=device)
