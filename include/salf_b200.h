@@ -236,6 +236,13 @@ int salf_loss_opacity_lidar(const double *params, const double *geo, int32_t den
                             const double *points, const int64_t *vid, double *grad, double *loss_sum,
                             void *stream);
 
+/* loss_smooth (losses.py:95-185) over deduplicated face pairs (fine voxel,
+ * same-or-coarser neighbour, axis, sign): adds gradients into grad and
+ * (sum |dSDF|, sum |dColour|) into loss_sums[2] (means use 4n and 12n). */
+int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, const int64_t *fine,
+                     const int64_t *coarse, const int32_t *axis, const double *sign, double *grad,
+                     double *loss_sums, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -134,9 +134,104 @@ __global__ void k_opacity_lidar(int64_t n, const double *__restrict__ pts, const
   atomicAdd(gr + 3, ds);
 }
 
+// loss_smooth (losses.py:95-185): one thread per (face pair, face corner).
+// Corners of the finer voxel's face in its local frame; the coarse side sees
+// the same world point in its own frame; SDF and colour (view = face normal)
+// differences, L1, gradients into both voxels.
+__global__ void k_smooth(int64_t n_pairs, const int64_t *__restrict__ fine, const int64_t *__restrict__ coarse,
+                         const int32_t *__restrict__ axis, const double *__restrict__ sgn,
+                         const double *__restrict__ p, const double *__restrict__ geo, double inv_ns, double inv_nc,
+                         double *__restrict__ grad, double *__restrict__ loss_sums) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pairs * 4) return;
+  const int64_t q = t >> 2;
+  const int corner = (int)(t & 3);
+  const int64_t f = fine[q], c = coarse[q];
+  const int ax = axis[q];
+  const double sg = sgn[q];
+  const int o0 = ax == 0 ? 1 : 0, o1 = ax == 2 ? 1 : 2;  // the two in-face axes
+  // corners [(-1,-1), (-1,1), (1,-1), (1,1)] over (o0, o1)
+  double xf[3];
+  xf[ax] = sg;
+  xf[o0] = (corner & 2) ? 1.0 : -1.0;
+  xf[o1] = (corner & 1) ? 1.0 : -1.0;
+  const double *gf = geo + 4 * f, *gc = geo + 4 * c;
+  const double hf = __ddiv_rn(gf[3], 2.0), sc2 = __ddiv_rn(2.0, gc[3]);
+  double xc[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double wpt = __dadd_rn(gf[k], __dmul_rn(xf[k], hf));  // local_to_world (scene.py:211-219)
+    xc[k] = __dmul_rn(__dsub_rn(wpt, gc[k]), sc2);            // world_to_local (scene.py:196-209)
+  }
+  const double *pf = p + f * kGradStride, *pc = p + c * kGradStride;
+  auto sdf = [](const double *r, const double x[3]) {
+    return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], x[0]), __dmul_rn(r[2], x[2])), __dmul_rn(r[1], x[1])), r[3]);
+  };
+  const double om[3] = {ax == 0 ? sg : 0.0, ax == 1 ? sg : 0.0, ax == 2 ? sg : 0.0};
+  const double gam[4] = {kShC0, __dmul_rn(kShC1, om[1]), __dmul_rn(kShC1, om[2]), __dmul_rn(kShC1, om[0])};
+  auto color = [&](const double *r, const double x[3], double out[3]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double *wc = r + 4 + 3 * i, *ws = r + 13 + 4 * i;
+      const double zc = __dadd_rn(__dadd_rn(__dmul_rn(wc[0], x[0]), __dmul_rn(wc[2], x[2])), __dmul_rn(wc[1], x[1]));
+      const double zs = __dadd_rn(__dadd_rn(__dmul_rn(ws[0], gam[0]), __dmul_rn(ws[2], gam[2])),
+                                  __dadd_rn(__dmul_rn(ws[1], gam[1]), __dmul_rn(ws[3], gam[3])));
+      out[i] = 1.0 / (1.0 + exp(-__dadd_rn(zc, zs)));
+    }
+  };
+  const double ds = __dsub_rn(sdf(pf, xf), sdf(pc, xc));
+  double cf[3], cc[3];
+  color(pf, xf, cf);
+  color(pc, xc, cc);
+  double l_c = 0.0;
+  const double gs = __dmul_rn(npsign(ds), inv_ns);
+  double *Gf = grad + f * kGradStride, *Gc = grad + c * kGradStride;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    atomicAdd(Gf + k, __dmul_rn(gs, xf[k]));
+    atomicAdd(Gc + k, -__dmul_rn(gs, xc[k]));
+  }
+  atomicAdd(Gf + 3, gs);
+  atomicAdd(Gc + 3, -gs);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const double dci = __dsub_rn(cf[i], cc[i]);
+    l_c = __dadd_rn(l_c, fabs(dci));
+    const double gci = __dmul_rn(npsign(dci), inv_nc);
+    const double gzf = __dmul_rn(__dmul_rn(gci, cf[i]), __dsub_rn(1.0, cf[i]));
+    const double gzc = __dmul_rn(__dmul_rn(-gci, cc[i]), __dsub_rn(1.0, cc[i]));
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      atomicAdd(Gf + 4 + 3 * i + j, __dmul_rn(gzf, xf[j]));
+      atomicAdd(Gc + 4 + 3 * i + j, __dmul_rn(gzc, xc[j]));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      atomicAdd(Gf + 13 + 4 * i + j, __dmul_rn(gzf, gam[j]));
+      atomicAdd(Gc + 13 + 4 * i + j, __dmul_rn(gzc, gam[j]));
+    }
+  }
+  atomicAdd(loss_sums, fabs(ds));
+  atomicAdd(loss_sums + 1, l_c);
+}
+
 }  // namespace salf
 
 using namespace salf;
+
+extern "C" int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, const int64_t *fine,
+                                const int64_t *coarse, const int32_t *axis, const double *sign, double *grad,
+                                double *loss_sums, void *stream) {
+  SALF_TRY {
+    if (n_pairs == 0) return SALF_OK;
+    const int64_t n = n_pairs * 4;
+    k_smooth<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        n_pairs, fine, coarse, axis, sign, params, geo, 1.0 / (double)(4 * n_pairs), 1.0 / (double)(12 * n_pairs), grad,
+        loss_sums);
+    return check_cuda("salf_loss_smooth");
+  }
+  SALF_CATCH
+}
 
 extern "C" int salf_loss_opacity_lidar(const double *params, const double *geo, int32_t density_mode, int64_t n,
                                        const double *points, const int64_t *vid, double *grad, double *loss_sum,

@@ -127,6 +127,25 @@ def query_batch(buffer: OctreeBuffer, p):
     return flag.cpu().numpy(), vid.cpu().numpy(), corner.cpu().numpy(), edge.cpu().numpy()
 
 
+def query_device(buffer: OctreeBuffer, pts: torch.Tensor):
+    """query_batch on device tensors -> (flag int8, vid int64) CUDA tensors (no raise)."""
+    lib = _lib.load()
+    pts = pts.to(torch.float64).contiguous().reshape(-1, 3)
+    n = pts.shape[0]
+    dev = pts.device
+    flag = torch.empty(n, dtype=torch.int8, device=dev)
+    vid = torch.empty(n, dtype=torch.int64, device=dev)
+    corner = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    edge = torch.empty(n, dtype=torch.float64, device=dev)
+    outside = torch.zeros(1, dtype=torch.int32, device=dev)
+    if n:
+        t = buffer.c_struct()
+        _lib.check(lib.salf_octree_query(_lib.ref(t), n, pts.data_ptr(), flag.data_ptr(), vid.data_ptr(),
+                                         corner.data_ptr(), edge.data_ptr(), outside.data_ptr(),
+                                         _lib.stream_ptr()), "query")
+    return flag, vid
+
+
 def query(buffer: OctreeBuffer, p) -> int:
     return int(query_batch(buffer, np.asarray(p, np.float64)[None, :])[1][0])
 

@@ -59,6 +59,7 @@ class TrainableScene:
         self.params = torch.as_tensor(_block(scene.static), device=dev).contiguous()
         self.m = torch.zeros_like(self.params)
         self.v = torch.zeros_like(self.params)
+        self.level = torch.as_tensor(scene.static.level.astype(np.int64), device=dev)
         self.step = 0
 
     @property
@@ -125,6 +126,72 @@ def loss_empty(ts: TrainableScene, outer_idx, grad: torch.Tensor) -> float:
     _lib.check(lib.salf_loss_empty_grad(ts.params.data_ptr(), ts.ds.geo.data_ptr(), mode, k, sel.data_ptr(),
                                         grad.data_ptr(), _lib.stream_ptr()), "loss_empty")
     return float(alpha[order].mean().item())
+
+
+_FACES = [(0, 1), (0, -1), (1, 1), (1, -1), (2, 1), (2, -1)]
+
+
+def face_pairs(ts: TrainableScene, octree: OctreeBuffer, sample_idx):
+    """losses.py:66-92 on the device: (fine, coarse, axis, sign) of each
+    adjacent pair with a same-or-coarser neighbour, first occurrence in the
+    reference's (face, sample) iteration order."""
+    from .octree import query_device
+    dev = ts.params.device
+    idx = _idx(sample_idx, dev)
+    if idx.numel() == 0:
+        return None
+    level = ts.level
+    centers, edges = ts.ds.geo[idx, :3], ts.ds.geo[idx, 3]
+    rmin = torch.as_tensor(octree.root_min, device=dev)
+    rmax = rmin + octree.root_edge
+    cand = []
+    n = idx.numel()
+    for f, (axis, sign) in enumerate(_FACES):
+        probe = centers.clone()
+        probe[:, axis] += sign * (0.5 * edges + 1e-6 * edges)
+        inside = torch.all((probe >= rmin) & (probe <= rmax), dim=1)
+        rows = torch.nonzero(inside, as_tuple=True)[0]
+        if rows.numel() == 0:
+            continue
+        _flag, nb = query_device(octree, probe[rows])
+        fine = idx[rows]
+        ok = (nb >= 0) & (nb != fine)
+        ok &= level[nb.clamp_min(0)] <= level[fine]
+        rows, fine, nb = rows[ok], fine[ok], nb[ok]
+        same = level[nb] == level[fine]
+        lo = torch.where(same, torch.minimum(fine, nb), fine)
+        hi = torch.where(same, torch.maximum(fine, nb), nb)
+        key = ((lo << 24) | hi) * 3 + axis
+        cand.append((f * n + rows, key, fine, nb, torch.full_like(fine, axis),
+                     torch.full(fine.shape, float(sign), dtype=torch.float64, device=dev)))
+    if not cand:
+        return None
+    order, key, fine, nb, ax, sg = (torch.cat([c[i] for c in cand]) for i in range(6))
+    pos = torch.argsort(order)  # reference iteration order
+    key, fine, nb, ax, sg = key[pos], fine[pos], nb[pos], ax[pos], sg[pos]
+    # first occurrence of each key (stable sort keeps iteration order within a key)
+    ks, perm = torch.sort(key, stable=True)
+    first = torch.ones_like(ks, dtype=torch.bool)
+    first[1:] = ks[1:] != ks[:-1]
+    keep = torch.sort(perm[first]).values
+    return fine[keep], nb[keep], ax[keep].to(torch.int32), sg[keep]
+
+
+def loss_smooth(ts: TrainableScene, octree: OctreeBuffer, sample_idx, grad: torch.Tensor) -> float:
+    """losses.py:95-185: mean |SDF difference| + mean |colour difference| at the
+    four corners of each shared face (colour viewed along the face normal)."""
+    lib = _lib.load()
+    pairs = face_pairs(ts, octree, sample_idx)
+    if pairs is None or pairs[0].numel() == 0:
+        return 0.0
+    fine, nb, ax, sg = (x.contiguous() for x in pairs)
+    n = fine.numel()
+    sums = torch.zeros(2, dtype=torch.float64, device=grad.device)
+    _lib.check(lib.salf_loss_smooth(ts.params.data_ptr(), ts.ds.geo.data_ptr(), n, fine.data_ptr(),
+                                    nb.data_ptr(), ax.data_ptr(), sg.data_ptr(), grad.data_ptr(),
+                                    sums.data_ptr(), _lib.stream_ptr()), "loss_smooth")
+    s = sums.cpu().numpy()
+    return float(s[0] / (4 * n) + s[1] / (12 * n))
 
 
 def loss_opacity_lidar(ts: TrainableScene, octree: OctreeBuffer, points, grad: torch.Tensor) -> float:

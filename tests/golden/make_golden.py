@@ -200,7 +200,7 @@ def main():
                **{f"fd_g_{k}": v for k, v in g.items()})
 
     # 5b. regularisers + Adam on the FD scene (losses.py:49-249, optim.py:48-62)
-    from salf.losses import loss_eikonal, loss_empty, loss_opacity_lidar
+    from salf.losses import loss_eikonal, loss_empty, loss_opacity_lidar, loss_smooth
     from salf.optim import AdamConfig, AdamState, adam_step
     vs = sc.static
     all_idx = np.arange(vs.n)
@@ -208,6 +208,15 @@ def main():
     l_e, g_e = loss_eikonal(vs, all_idx)
     l_m, g_m = loss_empty(vs, outer)
     l_o, g_o = loss_opacity_lidar(vs, oc.static, fx["points"])
+    l_s, g_s = loss_smooth(vs, oc.static, all_idx)
+    out.update(reg_smooth_loss=np.array([l_s]), **{f"reg_smo_{k}": v for k, v in g_s.items()})
+    sm = make_random_scene(13, 60)
+    sm = roundtrip("rand60s", sm)
+    oc_sm = R_ray.build_scene_octrees(sm)
+    sm_idx = np.unique(np.random.default_rng(3).integers(0, sm.static.n, 40))
+    l_s2, g_s2 = loss_smooth(sm.static, oc_sm.static, sm_idx)
+    out.update(reg_smooth2_idx=sm_idx, reg_smooth2_loss=np.array([l_s2]),
+               **{f"reg_smo2_{k}": v for k, v in g_s2.items()})
     out.update(reg_points=fx["points"], reg_outer=outer, reg_loss=np.array([l_e, l_m, l_o]),
                reg_eik_w_s=g_e["w_s"], **{f"reg_emp_{k}": v for k, v in g_m.items()},
                **{f"reg_opa_{k}": v for k, v in g_o.items()})

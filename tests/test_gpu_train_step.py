@@ -131,3 +131,27 @@ def test_adam_and_regularisers_match_reference(golden):
         np.testing.assert_allclose(got[k], golden["adam_p_" + k], rtol=1e-13, atol=1e-15)
     # the render-side scene was refreshed from the updated block
     assert np.allclose(ts.ds.prm[:, :4].cpu().numpy(), got["w_s"].astype(np.float32))
+
+
+@pytest.mark.parametrize("case", ["fd10", "rand60s"])
+def test_smoothness_regulariser_matches_reference(golden, case):
+    """loss_smooth (losses.py:95-185): face pairs found by device octree queries,
+    deduplicated in the reference's iteration order; value and gradients."""
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.device import grads_to_dict
+    from paper_2507_18713_b200.optim import TrainableScene, loss_smooth
+    sc = load_golden_scene(case)
+    ts = TrainableScene(sc)
+    oc = RY.build_scene_octrees(sc)
+    g = ts.zero_grad()
+    if case == "fd10":
+        idx, pre = np.arange(ts.n), "reg_smo_"
+        want_loss = golden["reg_smooth_loss"][0]
+    else:
+        idx, pre = golden["reg_smooth2_idx"], "reg_smo2_"
+        want_loss = golden["reg_smooth2_loss"][0]
+    val = loss_smooth(ts, oc.static, idx, g)
+    assert val == pytest.approx(want_loss, rel=1e-10)
+    gd = grads_to_dict(g)
+    for k in ("w_s", "w_c", "w_sh"):
+        np.testing.assert_allclose(gd[k], golden[pre + k], rtol=1e-9, atol=1e-13)
