@@ -451,6 +451,30 @@ def extras(ds, args):
         fb, st = RR.rasterize(dss, cam, return_state=True)
         RR.rasterize_backward(st, dcs, dds, as_dict=False)
 
+    # C5: the 8-camera + 2-LiDAR rig training step on one GPU (all sensors on
+    # this rank): forward, global L1 seeds, backward, then device Adam
+    from paper_2507_18713_b200.optim import TrainableScene
+    from paper_2507_18713_b200.parallel import split_work
+    from paper_2507_18713_b200.train_step import rig_step
+    ts = TrainableScene(scene)
+    cams, lidars = configs.c5_rig()
+    sensors = cams + lidars
+    g = torch.Generator().manual_seed(5)
+    targets = [torch.rand((c.height, c.width, 3), generator=g, dtype=torch.float64).to(ts.ds.device)
+               for c in cams] + [(1.0 + 20.0 * torch.rand(l.beam_elevations.shape[0] * l.steps, generator=g,
+                                                            dtype=torch.float64)).to(ts.ds.device) for l in lidars]
+    items = split_work(sensors, 1)
+    gbuf = ts.zero_grad()
+
+    def c5_step():
+        gbuf.zero_()
+        rig_step(ts.ds, oc, sensors, targets, items, gbuf)
+        ts.adam_step(gbuf)
+
+    ms5 = timeit(c5_step, n=3)
+    out["c5_train_step"] = {"ms": ms5, "steps_per_s": 1e3 / ms5, "sensors": "8 x 1920x1080 pinhole + 2 x 128x1800 LiDAR",
+                            "includes": "forward, L1 seeds, raster + ray backward, device Adam, scene refresh"}
+    del ts, gbuf, targets
     out["surface_dense_regime"] = {
         "voxels": dss.n,
         "c2_forward_fps": 1e3 / timeit(lambda: RR.rasterize(dss, cam)),

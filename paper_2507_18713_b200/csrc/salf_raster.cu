@@ -340,7 +340,8 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
   }
 }
 
-constexpr int kChunk = 64;  // entries staged per step (192 B each in shared memory)
+constexpr int kChunk = 64;   // entries staged per step (192 B each in shared memory)
+constexpr int kChunkB = 32;  // backward: + a 32 x 8 x 27 fp32 reduction buffer
 
 template <bool kExactColor>
 __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
@@ -471,8 +472,13 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
   __syncthreads();
   const int64_t lim = beg + (int64_t)s_max;
 
-  for (int64_t base = beg; base < lim; base += kChunk) {
-    const int cn = (int)min((int64_t)kChunk, lim - base);
+  // Two-level reduction: each warp reduces its lanes' 27-vectors for entry j
+  // (transposed shuffle reduction) into red[j][warp][.]; after the chunk the
+  // CTA sums its warps and issues one fp64 atomic per (entry, component).
+  __shared__ float red[kChunkB][8][kGradStride];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = nthreads >> 5;
+  for (int64_t base = beg; base < lim; base += kChunkB) {
+    const int cn = (int)min((int64_t)kChunkB, lim - base);
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry(sc, c, entries[base + j], sm[j]);
     __syncthreads();
@@ -480,7 +486,6 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
       const int64_t jj = base - beg + j;
       float g[32];
       bool act = false;
-      int64_t vid = sm[j].vid;
       double t0, t1;
       if (inside && jj < n_stop && pair_hit(r, sm[j], t0, t1)) {
         SegVals sv;
@@ -499,7 +504,21 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
           T = __dmul_rn(T, sv.om);
         }
       }
-      scatter_grad(grad, vid, act, g);
+      // every active lane of this warp holds entry j's voxel: one group
+      float tot = 0.0f;
+      if (__ballot_sync(0xffffffffu, act)) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) g[k] = act ? g[k] : 0.0f;
+        tot = warp_transpose_reduce(g);
+      }
+      if (lane < kGradStride) red[j][warp][lane] = tot;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < cn * kGradStride; q += nthreads) {
+      const int j = q / kGradStride, k = q - j * kGradStride;
+      float sum = 0.0f;
+      for (int w = 0; w < nwarps; ++w) sum += red[j][w][k];
+      if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
     }
   }
   (void)keep;
