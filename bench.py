@@ -190,6 +190,13 @@ def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles):
     return fwd, bwd
 
 
+def _ncu_metrics():
+    """Per-kernel ncu metrics of the committed capture (profiles/), if present:
+    the roofline above is HBM; these kernels are FP64-pipe / latency bound."""
+    p = ROOT / "profiles" / "ncu_metrics.json"
+    return json.loads(p.read_text()) if p.exists() else None
+
+
 def run_ours(args, world, rank, local):
     import torch
     import torch.distributed as dist
@@ -370,6 +377,7 @@ def run_ours(args, world, rank, local):
                      "algorithmic_bytes": dom_b, "kernel_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
         "kernels_ms": {k: float(np.mean(v)) for k, v in kms.items()},
+        "ncu": _ncu_metrics(),
         "clocks": clk,
     }
     if not args.no_extras and world == 1:

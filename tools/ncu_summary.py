@@ -47,6 +47,7 @@ def main(rep, out_md, traffic_json=None):
              "(tools/ncu_target.py: C2 raster fwd+bwd and C3 LiDAR on S1M init). "
              "Per-launch means over the captured launches.", ""]
     traffic = {}
+    metrics = {}
     for name, lst in per.items():
         avg = {k: sum(v[k] for v in lst if k in v) / max(1, sum(1 for v in lst if k in v)) for k in want}
         dur_ms = avg["gpu__time_duration.sum"] / 1e6
@@ -54,6 +55,13 @@ def main(rep, out_md, traffic_json=None):
         key = {"k_composite": "raster_composite", "k_backward": "raster_backward",
                "k_ray_forward": "ray_forward"}.get(name.split("<")[0].replace("salf::", ""), name)
         traffic[key] = rd + wr
+        metrics[key] = {"duration_ms": dur_ms, "dram_bytes": rd + wr,
+                        "l2_hit_pct": avg["lts__t_sector_hit_rate.pct"],
+                        "l1_hit_pct": avg["l1tex__t_sector_hit_rate.pct"],
+                        "occupancy_pct": avg["sm__warps_active.avg.pct_of_peak_sustained_active"],
+                        "registers": avg["launch__registers_per_thread"],
+                        "issue_active_pct": avg["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+                        "fp64_pipe_pct": avg["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]}
         lines += [f"## {name} ({len(lst)} launches)", "",
                   f"* duration {dur_ms:.3f} ms; DRAM read {rd / 1e6:.1f} MB + write {wr / 1e6:.1f} MB "
                   f"= {(rd + wr) / dur_ms / 1e6:.1f} GB/s ({avg['dram__throughput.avg.pct_of_peak_sustained_elapsed']:.1f}% of peak)",
@@ -81,6 +89,7 @@ def main(rep, out_md, traffic_json=None):
     open(out_md, "w").write("\n".join(lines) + "\n")
     if traffic_json:
         json.dump(traffic, open(traffic_json, "w"), indent=1, sort_keys=True)
+        json.dump(metrics, open(traffic_json.replace("traffic", "ncu_metrics"), "w"), indent=1, sort_keys=True)
     print("\n".join(lines))
 
 
