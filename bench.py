@@ -190,6 +190,25 @@ def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles):
     return fwd, bwd
 
 
+def _fp64_peak(dev) -> float:
+    """Measured FP64 FMA throughput (TFLOP/s) of this GPU: best of 3 launches."""
+    import torch
+    from paper_2507_18713_b200 import _lib
+    lib = _lib.load()
+    scratch = torch.zeros(148 * 16, dtype=torch.float64, device=dev)
+    grid, iters = 148 * 16, 4000
+    best = 0.0
+    for _ in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _lib.check(lib.salf_fp64_peak(scratch.data_ptr(), grid, iters, _lib.stream_ptr()))
+        b.record()
+        torch.cuda.synchronize()
+        flops = grid * 256 * 64 * iters * 2.0
+        best = max(best, flops / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
 def _ncu_metrics():
     """Per-kernel ncu metrics of the committed capture (profiles/), if present:
     the roofline above is HBM; these kernels are FP64-pipe / latency bound."""
@@ -359,6 +378,20 @@ def run_ours(args, world, rank, local):
     if tp.exists():
         traffic = json.loads(tp.read_text()).get(dom)
 
+    # secondary (ALU) roofline of the forward composite: SURVEY §8d's
+    # F = 24 P + 120 S_inc flop (P = pair tests, S_inc = included segments,
+    # both read from the frame's saved state) against a live FP64 peak probe
+    sv = st.saved
+    pairs = float(sv[:, 6].sum().item())
+    s_inc = float(sv[:, 7].sum().item())
+    flops = 24.0 * pairs + 120.0 * s_inc
+    fp64_peak = _fp64_peak(dev)
+    alu = {"bound": "fp64", "kernel": "raster_composite", "unit": "TFLOP/s",
+           "achieved": flops / (k_fwd * 1e-3) / 1e12, "peak": fp64_peak,
+           "frac": flops / (k_fwd * 1e-3) / 1e12 / fp64_peak, "flops": flops,
+           "pair_tests": pairs, "included_segments": s_inc,
+           "formula": "24 P + 120 S_inc (SURVEY 8d)", "peak_source": "live DFMA probe (salf_fp64_peak)"}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
@@ -376,6 +409,7 @@ def run_ours(args, world, rank, local):
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes": dom_b, "kernel_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+        "roofline_alu": alu,
         "kernels_ms": {k: float(np.mean(v)) for k, v in kms.items()},
         "ncu": _ncu_metrics(),
         "clocks": clk,

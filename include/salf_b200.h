@@ -131,7 +131,8 @@ int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double 
 
 /* rasterize (render_raster.py:201-301) over prebuilt render bins.
  * out_rgb (H*W*3), out_opacity, out_depth f32; saved (H*W*8 f64, nullable):
- * acc_rgb[3], acc_w, acc_wt, T_final, n_stop, pad -- kept for the backward. */
+ * acc_rgb[3], acc_w, acc_wt, T_final, n_stop (entries examined), n_included
+ * -- kept for the backward (and the work statistics of the ALU roofline). */
 int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                           const salf_raster_opts_t *opts, const int64_t *offsets,
                           const int32_t *entries, float *out_rgb, float *out_opacity,
@@ -242,6 +243,9 @@ int salf_loss_opacity_lidar(const double *params, const double *geo, int32_t den
 int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, const int64_t *fine,
                      const int64_t *coarse, const int32_t *axis, const double *sign, double *grad,
                      double *loss_sums, void *stream);
+
+/* FP64 peak probe (benchmark utility): grid x 256 threads x 64*iters DFMA. */
+int salf_fp64_peak(double *scratch, int32_t grid, int32_t iters, void *stream);
 
 #ifdef __cplusplus
 }

@@ -88,6 +88,7 @@ SIGNATURES = {
     "salf_loss_empty_grad": (C.c_int, [vp, vp, C.c_int32, C.c_int64, vp, vp, vp]),
     "salf_loss_opacity_lidar": (C.c_int, [vp, vp, C.c_int32, C.c_int64, vp, vp, vp, vp, vp]),
     "salf_loss_smooth": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_fp64_peak": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
 }
 
 _lib = None

@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
   float acc_cf[3] = {0.0f, 0.0f, 0.0f};  // fast mode: fp32 colour sums (outputs are fp32)
   bool alive = inside;
   int64_t n_stop = end - beg;
+  int n_inc = 0;  // included segments of this pixel (work statistics, saved[7])
   const int nthreads = blockDim.x;
 
   for (int64_t base = beg; base < end; base += kChunk) {
@@ -392,6 +393,7 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
           T = __dmul_rn(T, sv.om);
+          ++n_inc;
         } else {
           alive = false;
           n_stop = base - beg + j;
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
   if (saved) {
     double *s = saved + pix * SALF_SAVED_STRIDE;
     s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
-    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_stop; s[7] = 0.0;
+    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_stop; s[7] = (double)n_inc;
   }
 }
 
