@@ -201,6 +201,16 @@ int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t *scene, int
                        const float *feat, const float *head, float *out_depth, float *out_opacity,
                        float *out_feat, float *out_head, double *saved, int32_t *status, void *stream);
 
+/* Backward of salf_lidar_forward: depth seeds d_depth (N f64) plus, for the
+ * intensity / ray-drop extension, dF = dL/d(blended feature) (N x 8 f64)
+ * with the forward's blended feature Facc (N x 8 f64): field-parameter
+ * gradients into grad (M x 27) and feature gradients into feat_grad (M x 8).
+ * feat == NULL: depth-only backward. */
+int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                        const double *origins, const double *dirs, const salf_raster_opts_t *opts,
+                        const double *saved, const double *d_depth, const float *feat, const double *dF,
+                        const double *Facc, double *grad, double *feat_grad, void *stream);
+
 /* backward_records (backward.py:35-101) for the ray path, re-marching each
  * ray: d_rgb (N x 3), d_depth (N) f64; grad (M x 27 f64, accumulated). */
 int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,

@@ -407,12 +407,20 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
 
 // Ray backward: warp-synchronous re-march (every lane advances one round per
 // iteration, as BatchMarch does) so gradient scatters run with the full warp.
+struct FeatGrad {
+  const float *feat;    // M x 8 per-voxel LiDAR feature (nullptr: no feature terms)
+  const double *dF;     // N x 8 dL/dF of the blended feature
+  const double *Facc;   // N x 8 blended feature of the forward
+  double *feat_grad;    // M x 8 dL/dfeature (accumulated)
+};
+
 template <bool kExactColor>
 __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
                                                       const double *__restrict__ orig, const double *__restrict__ dirs,
                                                       const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                       const double *__restrict__ saved, const double *__restrict__ d_rgb,
-                                                      const double *__restrict__ d_depth, double *__restrict__ grad) {
+                                                      const double *__restrict__ d_depth, double *__restrict__ grad,
+                                                      FeatGrad fg) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const double keep = 1.0 - opt.stop_threshold;
   bool live = i < n && (valid ? valid[i] != 0 : true);
@@ -420,10 +428,11 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
   m.active = false;
   double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, T = 1.0,
          t_run = 1.0;
+  double dF[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (live) {
     m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
     const double *s = saved + i * SALF_SAVED_STRIDE;
-    for (int k = 0; k < 3; ++k) dC[k] = d_rgb[3 * i + k];
+    for (int k = 0; k < 3; ++k) dC[k] = d_rgb ? d_rgb[3 * i + k] : 0.0;
     const double acc_w = s[3], acc_wt = s[4];
     const bool okd = acc_w > kDepthWeightMin;
     dd = okd ? d_depth[i] : 0.0;
@@ -435,6 +444,15 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
                                __dmul_rn(dC[1], opt.background[1])),
                      s[5]);
     live = m.active && (dC[0] != 0.0 || dC[1] != 0.0 || dC[2] != 0.0 || dd != 0.0);
+    if (fg.feat) {
+      // the blended feature F = sum w_i f_i enters like a colour without background
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        dF[k] = fg.dF[8 * i + k];
+        total = __dadd_rn(total, __dmul_rn(dF[k], fg.Facc[8 * i + k]));
+        live = live || (m.active && dF[k] != 0.0);
+      }
+    }
   }
   int32_t st = 0;
   while (__any_sync(0xffffffffu, live)) {
@@ -450,9 +468,19 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
         const double tb = T;
         if (tb > keep) {
           const double w = __dmul_rn(tb, a);
-          const double A = __dadd_rn(
+          double A = __dadd_rn(
               __dadd_rn(__dadd_rn(__dmul_rn(dC[0], sv.c[0]), __dmul_rn(dC[2], sv.c[2])), __dmul_rn(dC[1], sv.c[1])),
               __ddiv_rn(__dmul_rn(dd, __dsub_rn(sv.tm, D)), ws));
+          if (fg.feat) {
+            const float4 f0 = __ldg(reinterpret_cast<const float4 *>(fg.feat) + 2 * vid);
+            const float4 f1 = __ldg(reinterpret_cast<const float4 *>(fg.feat) + 2 * vid + 1);
+            const double f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              A = __dadd_rn(A, __dmul_rn(dF[k], f[k]));
+              if (dF[k] != 0.0) atomicAdd(fg.feat_grad + 8 * vid + k, __dmul_rn(w, dF[k]));
+            }
+          }
           prefix = __dadd_rn(prefix, __dmul_rn(A, w));
           const double suffix = __dsub_rn(total, prefix);
           segment_grad(sc.density_mode, sv.delta, sv.sigma, sv.alpha, sv.om, sv.s, sv.e, sv.a, sv.inv_b, sv.x, sv.c,
@@ -552,13 +580,32 @@ extern "C" int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *
     if (n == 0) return SALF_OK;
     OctDev t = make_oct(tree);
     const unsigned grid = (unsigned)((n + 127) / 128);
+    FeatGrad fg{nullptr, nullptr, nullptr, nullptr};
     if (opts->exact_color)
       k_ray_backward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
-                                                                     d_rgb, d_depth, grad);
+                                                                     d_rgb, d_depth, grad, fg);
     else
       k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
-                                                                      d_rgb, d_depth, grad);
+                                                                      d_rgb, d_depth, grad, fg);
     return check_cuda("salf_ray_backward");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                   const double *origins, const double *dirs, const salf_raster_opts_t *opts,
+                                   const double *saved, const double *d_depth, const float *feat, const double *dF,
+                                   const double *Facc, double *grad, double *feat_grad, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    if (feat && (!dF || !Facc || !feat_grad)) return set_error(SALF_EINVAL, "feature backward needs dF, F and a buffer");
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    // colour is not part of the LiDAR model: no colour seeds (d_rgb = nullptr)
+    FeatGrad fg{feat, dF, Facc, feat_grad};
+    k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
+                                                                    nullptr, d_depth, grad, fg);
+    return check_cuda("salf_lidar_backward");
   }
   SALF_CATCH
 }

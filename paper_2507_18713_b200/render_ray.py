@@ -149,6 +149,8 @@ def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chun
 
 @dataclass
 class LidarReturn:
+    """Outputs of `render_lidar` (CUDA tensors) + replay state for `lidar_backward`."""
+
     depth: torch.Tensor  # (beams, steps) f32, NaN = no return
     opacity: torch.Tensor  # (beams, steps) f32
     intensity: torch.Tensor | None  # (beams, steps) f32, extension only
@@ -156,6 +158,11 @@ class LidarReturn:
     feature: torch.Tensor | None  # (beams, steps, 8) alpha-blended feature
     saved: torch.Tensor
     status: torch.Tensor
+    origins: torch.Tensor | None = None
+    dirs: torch.Tensor | None = None
+    scene: DeviceScene | None = None
+    octree: OctreeBuffer | None = None
+    opts: object = None
 
 
 def render_lidar(scene, octrees, batch, *, features=None, head=None,
@@ -199,7 +206,53 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
     return LidarReturn(depth.reshape(shp), op.reshape(shp),
                        None if oh is None else oh[:, 0].reshape(shp),
                        None if oh is None else oh[:, 1].reshape(shp),
-                       None if of is None else of.reshape(*shp, 8), saved, status)
+                       None if of is None else of.reshape(*shp, 8), saved, status, o, d, ds, tree, opts)
+
+
+def lidar_backward(ret: LidarReturn, d_depth=None, *, features=None, head=None, d_intensity=None,
+                   d_drop=None, grad: torch.Tensor | None = None):
+    """Gradients of a LiDAR sweep (depth + the intensity / ray-drop extension).
+
+    d_depth, d_intensity, d_drop: per-ray loss gradients (beams, steps) or None.
+    Returns (grad (M, 27) f64 field-parameter buffer, feature grads (M, 8) f64 or
+    None, head grads (2, 13) f64 or None).  The head is the forward's linear
+    layer + sigmoid over [feature, depth (0 if none), view dir]; its gradient
+    reaches the fields through the blended feature (like colour, no
+    background) and through the expected depth."""
+    lib = _lib.load()
+    ds, dev = ret.scene, ret.scene.device
+    n = ret.saved.shape[0]
+    dd = torch.zeros(n, dtype=torch.float64, device=dev) if d_depth is None else \
+        _lib.as_f64(d_depth, dev).reshape(n).clone()
+    if grad is None:
+        grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    fgrad = hgrad = None
+    f = dF = Facc = None
+    if features is not None:
+        if ret.feature is None:
+            raise ValueError("render_lidar(..., want_feature=True) is needed for the feature backward")
+        f = torch.as_tensor(features, dtype=torch.float32, device=dev).reshape(-1, 8).contiguous()
+        W = torch.as_tensor(head, dtype=torch.float64, device=dev).reshape(2, 13)
+        outs = torch.stack([ret.intensity.reshape(n), ret.drop_prob.reshape(n)], 1).double()
+        dout = torch.stack([torch.zeros(n, dtype=torch.float64, device=dev) if x is None
+                            else _lib.as_f64(x, dev).reshape(n) for x in (d_intensity, d_drop)], 1)
+        dz = dout * outs * (1.0 - outs)  # sigmoid'
+        Facc = ret.feature.reshape(n, 8).double().contiguous()
+        wsum, wt = ret.saved[:, 3], ret.saved[:, 4]
+        valid = wsum > 0.5
+        D = torch.where(valid, wt / torch.where(valid, wsum, torch.ones_like(wsum)), torch.zeros_like(wsum))
+        z_in = torch.cat([Facc, D[:, None], ret.dirs], 1)  # (n, 12)
+        hgrad = torch.cat([dz.T @ z_in, dz.sum(0)[:, None]], 1)  # (2, 13)
+        dF = (dz @ W[:, :8]).contiguous()
+        dd = dd + torch.where(valid, dz @ W[:, 8], torch.zeros_like(dd))
+        fgrad = torch.zeros((max(ds.n, 1), 8), dtype=torch.float64, device=dev)
+    sc, t = ds.c_struct(), ret.octree.c_struct()
+    _lib.check(lib.salf_lidar_backward(_lib.ref(t), _lib.ref(sc), n, ret.origins.data_ptr(),
+                                       ret.dirs.data_ptr(), _lib.ref(ret.opts), ret.saved.data_ptr(),
+                                       dd.contiguous().data_ptr(), _lib.ptr(f), _lib.ptr(dF),
+                                       _lib.ptr(Facc), grad.data_ptr(), _lib.ptr(fgrad),
+                                       _lib.stream_ptr()), "lidar_backward")
+    return grad, (None if fgrad is None else fgrad[: ds.n]), hgrad
 
 
 def render_lidar_ranges(scene, octrees, batch, *, chunk: int = 65536) -> torch.Tensor:
