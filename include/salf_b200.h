@@ -211,6 +211,32 @@ int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t *scene, in
                         const double *saved, const double *d_depth, const float *feat, const double *dF,
                         const double *Facc, double *grad, double *feat_grad, void *stream);
 
+/* ---- dynamic actors (reference render_ray.py:161-239, next row of SURVEY §8f) --
+ * Actor segments are marched with salf_march in each actor's canonical frame,
+ * then shaded into 24-double records (t0, t1, t_mid, delta, x[3], s, e, sigma,
+ * alpha, 1-alpha, c[3], a, 1/b, dir[3], owner, global voxel id, pad[2]). */
+int salf_shade_segments(const salf_scene_t *scene, int64_t n, const double *seg_origin,
+                        const double *seg_dir, const int64_t *seg_vid, const double *seg_t0,
+                        const double *seg_t1, int32_t owner, int64_t vid_offset, int32_t exact_color,
+                        double *records, void *stream);
+
+/* integrate_rays with live actors: the static march (no early stop) merged per
+ * ray with the actor records of CSR ex_start[n + 1] / ex_rec, sorted by
+ * (t0, owner, vid) -- the reference's lexsort order. */
+int salf_ray_forward_merge(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                           const double *origins, const double *dirs, const uint8_t *valid,
+                           const salf_raster_opts_t *opts, const int64_t *ex_start, const double *ex_rec,
+                           float *out_rgb, float *out_opacity, float *out_depth, double *saved,
+                           int32_t *status, void *stream);
+
+/* Its backward: static gradients into grad (M x 27), actor gradients into
+ * ex_grad (sum of actor voxel counts x 27, by global voxel id). */
+int salf_ray_backward_merge(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                            const double *origins, const double *dirs, const uint8_t *valid,
+                            const salf_raster_opts_t *opts, const int64_t *ex_start, const double *ex_rec,
+                            const double *saved, const double *d_rgb, const double *d_depth, double *grad,
+                            double *ex_grad, void *stream);
+
 /* backward_records (backward.py:35-101) for the ray path, re-marching each
  * ray: d_rgb (N x 3), d_depth (N) f64; grad (M x 27 f64, accumulated). */
 int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,

@@ -30,6 +30,8 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
     dd = _lib.as_f64(d_depth, dev).reshape(n)
     if grad is None:
         grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    if n and records.ex_rec is not None:
+        raise ValueError("records with actor segments: use backward_records")
     if n:
         sc, t = ds.c_struct(), records.octree.c_struct()
         _lib.check(lib.salf_ray_backward(_lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(),
@@ -41,9 +43,34 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
 
 
 def backward_records(records: RenderRecords, scene, d_color, d_depth) -> dict:
-    """Parameter gradients per owner (backward.py:35-101); static scenes only."""
-    grad = backward_grad_buffer(records, d_color, d_depth)
-    return {"static": grads_to_dict(grad[: records.scene.n])}
+    """Parameter gradients per owner, 'static' and each actor id (backward.py:35-101)."""
+    if records.ex_rec is None:
+        grad = backward_grad_buffer(records, d_color, d_depth)
+        out = {"static": grads_to_dict(grad[: records.scene.n])}
+        for a in getattr(scene, "actors", []):
+            out[a.actor_id] = grads_to_dict(torch.zeros((a.voxels.n, _lib.GRAD_STRIDE), dtype=torch.float64))
+        return out
+    lib = _lib.load()
+    ds = records.scene
+    dev = ds.device
+    n = records.n_rays
+    dc = _lib.as_f64(d_color, dev).reshape(n * 3)
+    dd = _lib.as_f64(d_depth, dev).reshape(n)
+    grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    total = sum(c for _, _, c in records.actor_offsets)
+    ex_grad = torch.zeros((max(total, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    if n:
+        sc, t = ds.c_struct(), records.octree.c_struct()
+        _lib.check(lib.salf_ray_backward_merge(_lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(),
+                                               records.dirs.data_ptr(), _lib.ptr(records.valid),
+                                               _lib.ref(records.opts), records.ex_start.data_ptr(),
+                                               records.ex_rec.data_ptr(), records.saved.data_ptr(),
+                                               dc.data_ptr(), dd.data_ptr(), grad.data_ptr(),
+                                               ex_grad.data_ptr(), _lib.stream_ptr()), "backward_records")
+    out = {"static": grads_to_dict(grad[: ds.n])}
+    for actor_id, off, cnt in records.actor_offsets:
+        out[actor_id] = grads_to_dict(ex_grad[off:off + cnt])
+    return out
 
 
 def loss_color_seed(out_color: torch.Tensor, gt: torch.Tensor, mask: torch.Tensor) -> torch.Tensor:

@@ -219,10 +219,11 @@ struct RaySeg {
   double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
 };
 
-// _evaluate_geometry (render_ray.py:117-133) + eval_color for one segment.
+// _evaluate_geometry (render_ray.py:117-133) + eval_color for one segment of
+// the ray (o, d) in the frame of the voxel set `sc`.
 template <bool kExactColor>
-__device__ __forceinline__ void shade_seg(const salf_scene_t &sc, const Marcher &m, int64_t vid, double s0,
-                                          double s1, RaySeg &sv, bool want_color) {
+__device__ __forceinline__ void shade_od(const salf_scene_t &sc, const double o[3], const double d[3], int64_t vid,
+                                         double s0, double s1, RaySeg &sv, bool want_color) {
   sv.tm = __dmul_rn(0.5, __dadd_rn(s0, s1));
   sv.delta = __dsub_rn(s1, s0);
   const double4 g = ldg_d4(sc.geo + 4 * vid);
@@ -230,7 +231,7 @@ __device__ __forceinline__ void shade_seg(const salf_scene_t &sc, const Marcher 
   const double ctr[3] = {g.x, g.y, g.z};
   // world_to_local: (p - centre) * (2.0 / edge)  (scene.py:196-209)
 #pragma unroll
-  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(sv.tm, m.d[k])), ctr[k]), ax.z);
+  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dsub_rn(__dadd_rn(o[k], __dmul_rn(sv.tm, d[k])), ctr[k]), ax.z);
   VoxPrm p;
   load_prm(sc.prm, vid, p);
   sv.a = ax.x;
@@ -239,9 +240,45 @@ __device__ __forceinline__ void shade_seg(const salf_scene_t &sc, const Marcher 
   sv.sigma = density(sc.density_mode, sv.s, ax.x, ax.y, sv.e);
   sv.alpha = seg_alpha(sv.sigma, sv.delta, sv.om);
   if (want_color) {
-    if (kExactColor) eval_color64(p, sv.x, m.d, sv.c);
-    else eval_color32(p, sv.x, m.d, sv.c);
+    if (kExactColor) eval_color64(p, sv.x, d, sv.c);
+    else eval_color32(p, sv.x, d, sv.c);
   }
+}
+
+template <bool kExactColor>
+__device__ __forceinline__ void shade_seg(const salf_scene_t &sc, const Marcher &m, int64_t vid, double s0,
+                                          double s1, RaySeg &sv, bool want_color) {
+  shade_od<kExactColor>(sc, m.o, m.d, vid, s0, s1, sv, want_color);
+}
+
+// Extra (actor) segment records: 24 doubles each.
+enum : int {
+  kRecT0 = 0, kRecT1 = 1, kRecTm = 2, kRecDelta = 3, kRecX = 4, kRecS = 7, kRecE = 8, kRecSigma = 9,
+  kRecAlpha = 10, kRecOm = 11, kRecC = 12, kRecA = 15, kRecInvB = 16, kRecDir = 17, kRecOwner = 20,
+  kRecGvid = 21, kRecStride = 24
+};
+
+// Shade segments of rays given in the voxel set's own frame (actor segments,
+// render_ray.py:178-197): one record per segment.
+template <bool kExactColor>
+__global__ void k_shade_segments(salf_scene_t sc, int64_t n, const double *__restrict__ so, const double *__restrict__ sd,
+                                 const int64_t *__restrict__ vid, const double *__restrict__ t0,
+                                 const double *__restrict__ t1, int32_t owner, int64_t vid_offset,
+                                 double *__restrict__ rec) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double o[3] = {so[3 * i], so[3 * i + 1], so[3 * i + 2]}, d[3] = {sd[3 * i], sd[3 * i + 1], sd[3 * i + 2]};
+  RaySeg sv;
+  shade_od<kExactColor>(sc, o, d, vid[i], t0[i], t1[i], sv, true);
+  double *r = rec + i * kRecStride;
+  r[kRecT0] = t0[i]; r[kRecT1] = t1[i]; r[kRecTm] = sv.tm; r[kRecDelta] = sv.delta;
+  r[kRecX] = sv.x[0]; r[kRecX + 1] = sv.x[1]; r[kRecX + 2] = sv.x[2];
+  r[kRecS] = sv.s; r[kRecE] = sv.e; r[kRecSigma] = sv.sigma; r[kRecAlpha] = sv.alpha; r[kRecOm] = sv.om;
+  r[kRecC] = sv.c[0]; r[kRecC + 1] = sv.c[1]; r[kRecC + 2] = sv.c[2];
+  r[kRecA] = sv.a; r[kRecInvB] = sv.inv_b;
+  r[kRecDir] = d[0]; r[kRecDir + 1] = d[1]; r[kRecDir + 2] = d[2];
+  r[kRecOwner] = (double)owner; r[kRecGvid] = (double)(vid[i] + vid_offset);
+  r[22] = 0.0; r[23] = 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -499,6 +536,180 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
   }
 }
 
+
+// integrate_rays with live actors (render_ray.py:161-239): the static march
+// runs without early stop (:175) and is merged, in the reference's
+// lexsort((vid, owner, t0, ray)) order, with the ray's pre-shaded actor
+// segments (CSR ex_start / ex_rec).  Static wins ties at equal t0 (owner -1).
+template <bool kExactColor>
+__global__ void __launch_bounds__(128) k_ray_forward_merge(OctDev t, salf_scene_t sc, int64_t n,
+                                                           const double *__restrict__ orig,
+                                                           const double *__restrict__ dirs,
+                                                           const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
+                                                           const int64_t *__restrict__ ex_start,
+                                                           const double *__restrict__ ex_rec,
+                                                           float *__restrict__ out_rgb, float *__restrict__ out_op,
+                                                           float *__restrict__ out_depth, double *__restrict__ saved,
+                                                           int32_t *__restrict__ status) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double keep = 1.0 - opt.stop_threshold;
+  double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0;
+  int64_t n_seg = 0;
+  int32_t st = 0;
+  const bool ok = valid ? valid[i] != 0 : true;
+  if (ok) {
+    Marcher m;
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
+    int64_t k = ex_start[i];
+    const int64_t kend = ex_start[i + 1];
+    bool have = false, frozen = false;
+    int64_t vid = 0;
+    double s0 = 0.0, s1 = 0.0;
+    while (true) {
+      while (!have && m.active) have = m.step(t, vid, s0, s1, st);
+      const bool take_static = have && (k >= kend || !(ex_rec[k * kRecStride + kRecT0] < s0));
+      if (!take_static && k >= kend) break;
+      double alpha, om, tm, c[3];
+      if (take_static) {
+        RaySeg sv;
+        shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, !frozen);
+        alpha = sv.alpha; om = sv.om; tm = sv.tm; c[0] = sv.c[0]; c[1] = sv.c[1]; c[2] = sv.c[2];
+        have = false;
+      } else {
+        const double *r = ex_rec + k * kRecStride;
+        alpha = r[kRecAlpha]; om = r[kRecOm]; tm = r[kRecTm]; c[0] = r[kRecC]; c[1] = r[kRecC + 1]; c[2] = r[kRecC + 2];
+        ++k;
+      }
+      ++n_seg;
+      if (!frozen) {
+        if (T > keep) {
+          const double w = __dmul_rn(T, alpha);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) acc_c[q] = __dadd_rn(acc_c[q], __dmul_rn(w, c[q]));
+          acc_w = __dadd_rn(acc_w, w);
+          acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, tm));
+          T = __dmul_rn(T, om);
+        } else {
+          frozen = true;  // later segments are excluded; keep marching for the status only
+          break;
+        }
+      }
+    }
+  }
+  if (ok) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) out_rgb[3 * i + q] = (float)__dadd_rn(acc_c[q], __dmul_rn(T, opt.background[q]));
+    out_op[i] = (float)__dsub_rn(1.0, T);
+    out_depth[i] = acc_w > kDepthWeightMin ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) out_rgb[3 * i + q] = (float)opt.background[q];
+    out_op[i] = 0.0f;
+    out_depth[i] = NAN;
+  }
+  if (saved) {
+    double *s = saved + i * SALF_SAVED_STRIDE;
+    s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
+    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_seg; s[7] = 0.0;
+  }
+  if (status) status[i] = st;
+}
+
+// Backward of k_ray_forward_merge: static segments re-marched (grad), actor
+// segments from their records (ex_grad, indexed by the global actor voxel id).
+// Warp-synchronous: each iteration a lane either advances its marcher or
+// consumes one segment.
+template <bool kExactColor>
+__global__ void __launch_bounds__(128) k_ray_backward_merge(OctDev t, salf_scene_t sc, int64_t n,
+                                                            const double *__restrict__ orig,
+                                                            const double *__restrict__ dirs,
+                                                            const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
+                                                            const int64_t *__restrict__ ex_start,
+                                                            const double *__restrict__ ex_rec,
+                                                            const double *__restrict__ saved,
+                                                            const double *__restrict__ d_rgb,
+                                                            const double *__restrict__ d_depth,
+                                                            double *__restrict__ grad, double *__restrict__ ex_grad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double keep = 1.0 - opt.stop_threshold;
+  bool live = i < n && (valid ? valid[i] != 0 : true);
+  Marcher m;
+  m.active = false;
+  double dC[3] = {0, 0, 0}, total = 0.0, tail = 0.0, D = 0.0, dd = 0.0, ws = 1.0, prefix = 0.0, T = 1.0;
+  int64_t k = 0, kend = 0;
+  if (live) {
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
+    k = ex_start[i];
+    kend = ex_start[i + 1];
+    const double *s = saved + i * SALF_SAVED_STRIDE;
+    for (int q = 0; q < 3; ++q) dC[q] = d_rgb[3 * i + q];
+    const double acc_w = s[3], acc_wt = s[4];
+    const bool okd = acc_w > kDepthWeightMin;
+    dd = okd ? d_depth[i] : 0.0;
+    D = okd ? __ddiv_rn(acc_wt, acc_w) : 0.0;
+    ws = okd ? acc_w : 1.0;
+    total = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], s[0]), __dmul_rn(dC[2], s[2])), __dmul_rn(dC[1], s[1])),
+                      __ddiv_rn(__dmul_rn(dd, __dsub_rn(acc_wt, __dmul_rn(D, acc_w))), ws));
+    tail = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(dC[0], opt.background[0]), __dmul_rn(dC[2], opt.background[2])),
+                               __dmul_rn(dC[1], opt.background[1])),
+                     s[5]);
+    live = (m.active || k < kend) && (dC[0] != 0.0 || dC[1] != 0.0 || dC[2] != 0.0 || dd != 0.0);
+  }
+  int32_t st = 0;
+  bool have = false;
+  int64_t svid = 0;
+  double s0 = 0.0, s1 = 0.0;
+  while (__any_sync(0xffffffffu, live)) {
+    bool act_s = false, act_x = false;
+    int64_t gv = 0;
+    float g[32];
+    if (live) {
+      if (!have && m.active) {
+        have = m.step(t, svid, s0, s1, st);  // marcher advance only this iteration
+      } else {
+        const bool take_static = have && (k >= kend || !(ex_rec[k * kRecStride + kRecT0] < s0));
+        if (!take_static && k >= kend) {
+          live = false;
+        } else {
+          double tm, delta, x[3], ss, e, sigma, a, om, c[3], aa, ib, dir[3];
+          if (take_static) {
+            RaySeg sv;
+            shade_seg<kExactColor>(sc, m, svid, s0, s1, sv, true);
+            tm = sv.tm; delta = sv.delta; ss = sv.s; e = sv.e; sigma = sv.sigma; a = sv.alpha; om = sv.om;
+            aa = sv.a; ib = sv.inv_b;
+            for (int q = 0; q < 3; ++q) { x[q] = sv.x[q]; c[q] = sv.c[q]; dir[q] = m.d[q]; }
+            gv = svid;
+            have = false;
+          } else {
+            const double *r = ex_rec + k * kRecStride;
+            tm = r[kRecTm]; delta = r[kRecDelta]; ss = r[kRecS]; e = r[kRecE]; sigma = r[kRecSigma];
+            a = r[kRecAlpha]; om = r[kRecOm]; aa = r[kRecA]; ib = r[kRecInvB];
+            for (int q = 0; q < 3; ++q) { x[q] = r[kRecX + q]; c[q] = r[kRecC + q]; dir[q] = r[kRecDir + q]; }
+            gv = (int64_t)r[kRecGvid];
+            ++k;
+          }
+          if (T > keep) {
+            const double w = __dmul_rn(T, a);
+            const double A = __dadd_rn(
+                __dadd_rn(__dadd_rn(__dmul_rn(dC[0], c[0]), __dmul_rn(dC[2], c[2])), __dmul_rn(dC[1], c[1])),
+                __ddiv_rn(__dmul_rn(dd, __dsub_rn(tm, D)), ws));
+            prefix = __dadd_rn(prefix, __dmul_rn(A, w));
+            const double suffix = __dsub_rn(total, prefix);
+            segment_grad(sc.density_mode, delta, sigma, a, om, ss, e, aa, ib, x, c, dir, A, T, w, suffix, tail, dC, g);
+            if (take_static) act_s = true; else act_x = true;
+            T = __dmul_rn(T, om);
+          } else {
+            live = false;
+          }
+        }
+      }
+    }
+    scatter_grad(grad, gv, act_s, g);
+    scatter_grad(ex_grad, gv, act_x, g);
+  }
+}
+
 }  // namespace salf
 
 using namespace salf;
@@ -606,6 +817,68 @@ extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t
     k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
                                                                     nullptr, d_depth, grad, fg);
     return check_cuda("salf_lidar_backward");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_shade_segments(const salf_scene_t *scene, int64_t n, const double *seg_origin,
+                                   const double *seg_dir, const int64_t *seg_vid, const double *seg_t0,
+                                   const double *seg_t1, int32_t owner, int64_t vid_offset, int32_t exact_color,
+                                   double *records, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    if (exact_color)
+      k_shade_segments<true><<<grid, 128, 0, (cudaStream_t)stream>>>(*scene, n, seg_origin, seg_dir, seg_vid, seg_t0,
+                                                                       seg_t1, owner, vid_offset, records);
+    else
+      k_shade_segments<false><<<grid, 128, 0, (cudaStream_t)stream>>>(*scene, n, seg_origin, seg_dir, seg_vid, seg_t0,
+                                                                        seg_t1, owner, vid_offset, records);
+    return check_cuda("salf_shade_segments");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_ray_forward_merge(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                      const double *origins, const double *dirs, const uint8_t *valid,
+                                      const salf_raster_opts_t *opts, const int64_t *ex_start, const double *ex_rec,
+                                      float *out_rgb, float *out_opacity, float *out_depth, double *saved,
+                                      int32_t *status, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    if (opts->exact_color)
+      k_ray_forward_merge<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
+                                                                          ex_start, ex_rec, out_rgb, out_opacity,
+                                                                          out_depth, saved, status);
+    else
+      k_ray_forward_merge<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
+                                                                           ex_start, ex_rec, out_rgb, out_opacity,
+                                                                           out_depth, saved, status);
+    return check_cuda("salf_ray_forward_merge");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_ray_backward_merge(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                       const double *origins, const double *dirs, const uint8_t *valid,
+                                       const salf_raster_opts_t *opts, const int64_t *ex_start, const double *ex_rec,
+                                       const double *saved, const double *d_rgb, const double *d_depth, double *grad,
+                                       double *ex_grad, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    if (opts->exact_color)
+      k_ray_backward_merge<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
+                                                                           ex_start, ex_rec, saved, d_rgb, d_depth,
+                                                                           grad, ex_grad);
+    else
+      k_ray_backward_merge<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
+                                                                            ex_start, ex_rec, saved, d_rgb, d_depth,
+                                                                            grad, ex_grad);
+    return check_cuda("salf_ray_backward_merge");
   }
   SALF_CATCH
 }

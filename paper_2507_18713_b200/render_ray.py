@@ -27,14 +27,20 @@ STATIC_OWNER = -1
 @dataclass
 class SceneOctrees:
     static: OctreeBuffer
-    actors: list
+    actors: list  # one OctreeBuffer per actor (None for an empty actor)
+    actor_scenes: list = None  # one DeviceScene per actor (canonical frame)
 
 
 def build_scene_octrees(scene: Scene, device=None) -> SceneOctrees:
-    """render_ray.py:44-48 (actors: a later §8(f) row)."""
-    if any(a.voxels.n for a in scene.actors):
-        raise NotImplementedError("dynamic actors are not supported by the B200 path yet")
-    return SceneOctrees(static=build_octree(scene.static, device=device), actors=[])
+    """render_ray.py:44-48: the static octree and one octree per actor."""
+    from .scene import FlatVoxels
+    trees, dss = [], []
+    for a in scene.actors:
+        v = a.voxels
+        trees.append(build_octree(v, device=device) if v.n else None)
+        dss.append(DeviceScene(FlatVoxels(v.centers(), v.edges(), v.rotation, v.w_s, v.w_c, v.w_sh, v.log_a,
+                                          v.log_b, scene.density_mode), device) if v.n else None)
+    return SceneOctrees(static=build_octree(scene.static, device=device), actors=trees, actor_scenes=dss)
 
 
 @dataclass
@@ -54,6 +60,9 @@ class RenderRecords:
     octree: OctreeBuffer
     opts: _lib.RasterOptsT
     background: np.ndarray
+    ex_start: torch.Tensor | None = None  # actor segments merged in (CSR by ray)
+    ex_rec: torch.Tensor | None = None
+    actor_offsets: list | None = None  # (actor_id, first global id, n voxels)
 
     @property
     def weight_sum(self) -> torch.Tensor:
@@ -80,19 +89,92 @@ def _octree_of(octrees) -> OctreeBuffer:
     return octrees.static if isinstance(octrees, SceneOctrees) else octrees
 
 
+def _np_ray_box(o, d, bmin, bmax):
+    """ray_box_range (octree.py:175-194) on host arrays (actor box tests)."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        inv = 1.0 / d
+        ta = (bmin - o) * inv
+        tb = (bmax - o) * inv
+    near = np.minimum(ta, tb)
+    far = np.maximum(ta, tb)
+    zero = d == 0.0
+    inside = (o >= bmin) & (o <= bmax)
+    near = np.where(zero, np.where(inside, -np.inf, np.inf), near)
+    far = np.where(zero, np.where(inside, np.inf, -np.inf), far)
+    return near.max(axis=-1), far.min(axis=-1)
+
+
+def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: torch.Tensor, t_stamps,
+                    dev, exact_color: bool):
+    """Actor segments of every ray (render_ray.py:178-197): rays moved into each
+    actor's canonical frame at their timestamps (poses, transforms and box tests
+    on the host with the reference's own NumPy expressions), marched on that
+    actor's octree on the device and shaded into records; returned sorted by the
+    reference's lexsort((vid, owner, t0, ray)) as a CSR over rays."""
+    from .scene import quat_to_matrix
+    lib = _lib.load()
+    n = o.shape[0]
+    o_np, d_np = o.cpu().numpy(), d.cpu().numpy()
+    ts = np.broadcast_to(np.asarray(0.0 if t_stamps is None else t_stamps, np.float64), (n,))
+    recs, rays, offsets, goff = [], [], [], 0
+    for ai, actor in enumerate(scene.actors):
+        offsets.append((actor.actor_id, goff, actor.voxels.n))
+        if actor.voxels.n == 0:
+            continue
+        pos, quat = actor.pose_at(ts)
+        rmat = quat_to_matrix(quat)
+        o_a = np.einsum("nji,nj->ni", rmat, o_np - pos)
+        d_a = np.einsum("nji,nj->ni", rmat, d_np)
+        half = actor.extents / 2.0
+        t_in, t_out = _np_ray_box(o_a, d_a, -half, half)
+        t0c = np.maximum(t_in, 0.0)
+        hit_ids = np.flatnonzero((t_out > t0c) & (t0c < np.inf))
+        if hit_ids.size:
+            sub, vid, t0, t1 = march_segments(octrees.actors[ai], o_a[hit_ids], d_a[hit_ids])
+            if sub.numel():
+                ray = torch.as_tensor(hit_ids, device=dev)[sub]
+                so = torch.as_tensor(o_a, device=dev)[ray].contiguous()
+                sd = torch.as_tensor(d_a, device=dev)[ray].contiguous()
+                rec = torch.empty((sub.numel(), 24), dtype=torch.float64, device=dev)
+                dsa = octrees.actor_scenes[ai]
+                _lib.check(lib.salf_shade_segments(_lib.ref(dsa.c_struct()), sub.numel(), so.data_ptr(),
+                                                   sd.data_ptr(), vid.contiguous().data_ptr(), t0.data_ptr(),
+                                                   t1.data_ptr(), ai, goff, int(exact_color), rec.data_ptr(),
+                                                   _lib.stream_ptr()), "actor segments")
+                recs.append(rec)
+                rays.append(ray)
+        goff += actor.voxels.n
+    if recs:
+        rec = torch.cat(recs)
+        ray = torch.cat(rays)
+        order = torch.arange(ray.numel(), device=dev)
+        for key in (rec[:, 21], rec[:, 20], rec[:, 0], ray.double()):  # vid, owner, t0, ray (lexsort)
+            order = order[torch.sort(key[order], stable=True).indices]
+        rec, ray = rec[order].contiguous(), ray[order]
+    else:
+        rec = torch.zeros((1, 24), dtype=torch.float64, device=dev)
+        ray = torch.zeros(0, dtype=torch.int64, device=dev)
+    start = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    start[1:] = torch.cumsum(torch.bincount(ray, minlength=n), 0)
+    return start, rec, offsets, goff
+
+
 def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf,
                    background=(0.0, 0.0, 0.0), stop_threshold: float = STOP_THRESHOLD,
                    valid=None, exact_color: bool = False) -> RenderRecords:
-    """Render a ray batch against the static scene (render_ray.py:161-239).
+    """Render a ray batch against the composed scene (render_ray.py:161-239).
 
-    `t_stamps` only matter for dynamic actors (static scenes are time
-    invariant, render_ray.py tests :128-135); finite `t_max` is supported by
-    `march_batch` but not by the fused renderer (the reference's renderers
-    always pass infinity)."""
-    del t_stamps
+    Static scenes use one fused march/shade/composite launch with the
+    reference's early stop.  With live actors the static march runs without
+    early stop (:175) and is merged per ray with the actors' segments (rays
+    moved into each actor frame at their timestamps).  Finite `t_max` is
+    supported by `march_batch` only (the reference renderers pass infinity)."""
     if np.any(np.isfinite(np.asarray(t_max, np.float64))):
         raise NotImplementedError("finite t_max is only supported by march_batch")
     lib = _lib.load()
+    live = isinstance(scene, Scene) and any(a.voxels.n for a in scene.actors)
+    if live and not isinstance(octrees, SceneOctrees):
+        raise ValueError("scenes with actors need build_scene_octrees(scene)")
     ds = as_device_scene(scene)
     tree = _octree_of(octrees)
     dev = ds.device
@@ -112,6 +194,15 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
     status = torch.zeros(n, dtype=torch.int32, device=dev)
     opts = _opts(background, stop_threshold, exact_color)
     sc, t = ds.c_struct(), tree.c_struct()
+    if live:
+        ex_start, ex_rec, offsets, _ = _actor_segments(scene, octrees, o, d, t_stamps, dev, exact_color)
+        _lib.check(lib.salf_ray_forward_merge(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
+                                              _lib.ptr(vmask), _lib.ref(opts), ex_start.data_ptr(),
+                                              ex_rec.data_ptr(), rgb.data_ptr(), op.data_ptr(),
+                                              depth.data_ptr(), saved.data_ptr(), status.data_ptr(),
+                                              _lib.stream_ptr()), "integrate_rays")
+        return RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
+                             np.asarray(background, np.float64), ex_start, ex_rec, offsets)
     _lib.check(lib.salf_ray_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
                                     _lib.ptr(vmask), _lib.ref(opts), rgb.data_ptr(), op.data_ptr(),
                                     depth.data_ptr(), saved.data_ptr(), status.data_ptr(),
@@ -141,8 +232,9 @@ def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chun
     invalid rays keep the background, zero opacity and NaN depth."""
     del chunk
     h, w = batch.shape
-    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, background=background,
-                         stop_threshold=stop_threshold, valid=batch.valid, exact_color=exact_color)
+    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, batch.t_stamps.cpu().numpy(),
+                         background=background, stop_threshold=stop_threshold, valid=batch.valid,
+                         exact_color=exact_color)
     check_status(rec)
     return rec.out_color.reshape(h, w, 3), rec.opacity.reshape(h, w), rec.depth.reshape(h, w)
 

@@ -110,6 +110,93 @@ class SparseVoxelSet:
                 "log_a": self.log_a, "log_b": self.log_b}
 
 
+def quat_to_matrix(q) -> np.ndarray:
+    """rotations.py:19-33."""
+    q = np.asarray(q, dtype=np.float64)
+    w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+    m = np.empty(q.shape[:-1] + (3, 3))
+    m[..., 0, 0] = 1 - 2 * (y * y + z * z)
+    m[..., 0, 1] = 2 * (x * y - w * z)
+    m[..., 0, 2] = 2 * (x * z + w * y)
+    m[..., 1, 0] = 2 * (x * y + w * z)
+    m[..., 1, 1] = 1 - 2 * (x * x + z * z)
+    m[..., 1, 2] = 2 * (y * z - w * x)
+    m[..., 2, 0] = 2 * (x * z - w * y)
+    m[..., 2, 1] = 2 * (y * z + w * x)
+    m[..., 2, 2] = 1 - 2 * (x * x + y * y)
+    return m
+
+
+def quat_slerp(q0, q1, t) -> np.ndarray:
+    """rotations.py:36-50."""
+    q0 = np.asarray(q0, dtype=np.float64)
+    q1 = np.asarray(q1, dtype=np.float64)
+    t = np.asarray(t, dtype=np.float64)[..., None]
+    dot = np.sum(q0 * q1, axis=-1, keepdims=True)
+    q1 = np.where(dot < 0.0, -q1, q1)
+    dot = np.abs(dot)
+    theta = np.arccos(np.clip(dot, -1.0, 1.0))
+    sin_theta = np.sin(theta)
+    small = sin_theta < 1e-9
+    w0 = np.where(small, 1.0 - t, np.sin((1.0 - t) * theta) / np.where(small, 1.0, sin_theta))
+    w1 = np.where(small, t, np.sin(t * theta) / np.where(small, 1.0, sin_theta))
+    q = w0 * q0 + w1 * q1
+    return q / np.linalg.norm(q, axis=-1, keepdims=True)
+
+
+def quat_multiply(q0, q1) -> np.ndarray:
+    """rotations.py:74-88 (Hamilton product, q1 applied first)."""
+    q0 = np.asarray(q0, dtype=np.float64)
+    q1 = np.asarray(q1, dtype=np.float64)
+    w0, x0, y0, z0 = q0[..., 0], q0[..., 1], q0[..., 2], q0[..., 3]
+    w1, x1, y1, z1 = q1[..., 0], q1[..., 1], q1[..., 2], q1[..., 3]
+    return np.stack([w0 * w1 - x0 * x1 - y0 * y1 - z0 * z1, w0 * x1 + x0 * w1 + y0 * z1 - z0 * y1,
+                     w0 * y1 - x0 * z1 + y0 * w1 + z0 * x1, w0 * z1 + x0 * y1 - y0 * x1 + z0 * w1], axis=-1)
+
+
+@dataclass
+class Actor:
+    """A rigid dynamic volume with its own voxel set and trajectory (scene.py:290-331)."""
+
+    actor_id: str
+    extents: np.ndarray
+    voxels: SparseVoxelSet
+    times: np.ndarray
+    positions: np.ndarray
+    quaternions: np.ndarray
+
+    def __post_init__(self):
+        self.extents = np.asarray(self.extents, dtype=np.float64)
+        self.times = np.asarray(self.times, dtype=np.float64)
+        self.positions = np.asarray(self.positions, dtype=np.float64)
+        self.quaternions = np.asarray(self.quaternions, dtype=np.float64)
+        if self.times.ndim != 1 or len(self.times) == 0:
+            raise ValueError("trajectory must contain at least one pose")
+        if np.any(np.diff(self.times) <= 0):
+            raise ValueError("trajectory timestamps must be strictly increasing")
+
+    def pose_at(self, t):
+        """(translation, quaternion) at time(s) t; lerp + slerp (scene.py:316-331)."""
+        t = np.asarray(t, dtype=np.float64)
+        if np.any(t < self.times[0] - 1e-12) or np.any(t > self.times[-1] + 1e-12):
+            raise ValueError("timestamp outside the actor trajectory")
+        if len(self.times) == 1:
+            shape = t.shape
+            return (np.broadcast_to(self.positions[0], shape + (3,)).copy(),
+                    np.broadcast_to(self.quaternions[0], shape + (4,)).copy())
+        hi = np.clip(np.searchsorted(self.times, t, side="right"), 1, len(self.times) - 1)
+        lo = hi - 1
+        span = self.times[hi] - self.times[lo]
+        frac = np.clip((t - self.times[lo]) / span, 0.0, 1.0)
+        pos = self.positions[lo] + frac[..., None] * (self.positions[hi] - self.positions[lo])
+        return pos, quat_slerp(self.quaternions[lo], self.quaternions[hi], frac)
+
+
+def make_actor_bounds(extents, base_edge: float, max_levels: int = 6) -> SceneBounds:
+    extents = np.asarray(extents, dtype=np.float64)
+    return SceneBounds(-extents / 2.0, extents / 2.0, base_edge, max_levels)
+
+
 @dataclass
 class Scene:
     bounds: SceneBounds
@@ -143,15 +230,27 @@ class FlatVoxels:
 
 
 def flatten_scene(scene: Scene, t_stamp: float = 0.0) -> FlatVoxels:
-    """Static voxels as a flat list (render_raster.py:63-89).
-
-    Dynamic actors are a later §8(f) row; a scene carrying live actors is
-    rejected rather than silently rendered without them."""
-    if any(getattr(a, "voxels", None) is not None and a.voxels.n for a in scene.actors):
-        raise NotImplementedError("dynamic actors are not supported by the B200 path yet")
+    """Static voxels plus actor voxels rigidly posed at t_stamp (render_raster.py:63-89)."""
     s = scene.static
-    return FlatVoxels(centers=s.centers(), edges=s.edges(), rotations=s.rotation,
-                      w_s=s.w_s, w_c=s.w_c, w_sh=s.w_sh, log_a=s.log_a, log_b=s.log_b,
+    centers, edges, rots = [s.centers()], [s.edges()], [s.rotation]
+    w_s, w_c, w_sh, la, lb = [s.w_s], [s.w_c], [s.w_sh], [s.log_a], [s.log_b]
+    for actor in scene.actors:
+        if actor.voxels.n == 0:
+            continue
+        pos, quat = actor.pose_at(np.asarray(t_stamp))
+        rmat = quat_to_matrix(quat)
+        centers.append(actor.voxels.centers() @ rmat.T + pos)
+        edges.append(actor.voxels.edges())
+        rots.append(quat_multiply(quat, actor.voxels.rotation))
+        w_s.append(actor.voxels.w_s)
+        w_c.append(actor.voxels.w_c)
+        w_sh.append(actor.voxels.w_sh)
+        la.append(actor.voxels.log_a)
+        lb.append(actor.voxels.log_b)
+    return FlatVoxels(centers=np.concatenate(centers), edges=np.concatenate(edges),
+                      rotations=np.concatenate(rots), w_s=np.concatenate(w_s),
+                      w_c=np.concatenate(w_c), w_sh=np.concatenate(w_sh),
+                      log_a=np.concatenate(la), log_b=np.concatenate(lb),
                       density_mode=scene.density_mode)
 
 
@@ -189,12 +288,30 @@ def load_scene(path) -> tuple[Scene, dict]:
         raise ContainerError(f"voxels.bin: size mismatch, expected "
                              f"{count * VOXEL_DTYPE.itemsize} bytes for {count} voxels, "
                              f"got {len(data)}")
-    static = set_from_records(np.frombuffer(data, VOXEL_DTYPE), bounds,
-                              int(meta.get("budget", 2_500_000)), "voxels.bin")
-    if int(meta.get("actor_count", 0)):
-        raise NotImplementedError("dynamic actors are not supported by the B200 path yet")
+    budget = int(meta.get("budget", 2_500_000))
+    static = set_from_records(np.frombuffer(data, VOXEL_DTYPE), bounds, budget, "voxels.bin")
+    actors = []
+    ap = path / "actors.json"
+    actors_meta = json.loads(ap.read_text(encoding="utf-8"))["actors"] if ap.exists() else []
+    if len(actors_meta) != int(meta.get("actor_count", 0)):
+        raise ContainerError("actor_count in meta.json disagrees with actors.json")
+    for am in actors_meta:  # container.py:161-175
+        a_bounds = make_actor_bounds(np.array(am["extents"]), float(am["base_edge"]), int(am["max_levels"]))
+        cnt = int(am["voxel_count"])
+        raw = (path / f"actor_{am['id']}.bin").read_bytes()
+        if len(raw) != cnt * VOXEL_DTYPE.itemsize:
+            raise ContainerError(f"actor_{am['id']}.bin: size mismatch, expected "
+                                 f"{cnt * VOXEL_DTYPE.itemsize} bytes for {cnt} voxels, got {len(raw)}")
+        vset = set_from_records(np.frombuffer(raw, VOXEL_DTYPE), a_bounds, budget,
+                                f"actor_{am['id']}.bin")
+        traj = am["trajectory"]
+        actors.append(Actor(actor_id=str(am["id"]), extents=np.array(am["extents"], np.float64),
+                            voxels=vset, times=np.array([q["t"] for q in traj]),
+                            positions=np.array([q["position"] for q in traj]),
+                            quaternions=np.array([q["quaternion"] for q in traj])))
     inner = meta.get("inner_aabb")
-    scene = Scene(bounds=bounds, static=static, density_mode=meta.get("density_mode", "sdf"),
+    scene = Scene(bounds=bounds, static=static, actors=actors,
+                  density_mode=meta.get("density_mode", "sdf"),
                   inner_aabb=None if inner is None else np.array(inner, np.float64))
     sensors = {}
     sp = path / "sensors.json"
@@ -218,6 +335,16 @@ def save_scene(scene: Scene, path, sensors: dict | None = None) -> None:
                                      encoding="utf-8")
     dump(path / "meta.json", meta)
     (path / "voxels.bin").write_bytes(records_from_set(scene.static).tobytes())
-    dump(path / "actors.json", {"actors": []})
+    actors_meta = []
+    for a in scene.actors:  # container.py:120-133
+        actors_meta.append({
+            "id": a.actor_id, "extents": a.extents.tolist(),
+            "base_edge": a.voxels.bounds.base_edge, "max_levels": a.voxels.bounds.max_levels,
+            "voxel_count": a.voxels.n,
+            "trajectory": [{"t": float(t), "position": p.tolist(), "quaternion": q.tolist()}
+                           for t, p, q in zip(a.times, a.positions, a.quaternions)],
+        })
+        (path / f"actor_{a.actor_id}.bin").write_bytes(records_from_set(a.voxels).tobytes())
+    dump(path / "actors.json", {"actors": actors_meta})
     if sensors is not None:
         dump(path / "sensors.json", {"sensors": sensors})

@@ -230,6 +230,42 @@ def main():
     out.update(**{f"adam_g{i}_{k}": v for i, gs in enumerate(gseq) for k, v in gs.items()},
                **{f"adam_p_{k}": v for k, v in params.items()})
 
+    # 5c. dynamic actors (render_ray.py:161-239; test_render_ray.py:323-402, test_backward.py:62-81)
+    from salf.scene import Actor, make_actor_bounds
+    bounds = SceneBounds([0, 0, 0], [4, 4, 4], base_edge=1.0, max_levels=3)
+    static = SparseVoxelSet(bounds, budget=100)
+    static.add_voxels([0, 0, 0], [[0, 1, 1], [3, 1, 1], [1, 3, 2]], rng=np.random.default_rng(8), a=5.0)
+    a_bounds = make_actor_bounds([2.0, 2.0, 2.0], 1.0, max_levels=2)
+    av = SparseVoxelSet(a_bounds, budget=20)
+    av.add_voxels([0, 0, 1, 1], [[0, 0, 0], [1, 1, 1], [0, 3, 2], [2, 1, 0]], rng=np.random.default_rng(7),
+                  a=np.array([30.0, 8.0, 20.0, 12.0]))
+    yaw = lambda deg: np.array([np.cos(np.deg2rad(deg) / 2), 0.0, 0.0, np.sin(np.deg2rad(deg) / 2)])
+    cart = Actor("cart", np.array([2.0, 2, 2]), av, times=np.array([0.0, 1.0, 2.0]),
+                 positions=np.array([[2.0, 2.0, 2.0], [2.4, 2.1, 2.0], [3.0, 2.0, 2.2]]),
+                 quaternions=np.stack([yaw(0.0), yaw(35.0), yaw(90.0)]))
+    bv = SparseVoxelSet(make_actor_bounds([1.0, 1.0, 1.0], 0.5, max_levels=2), budget=10)
+    bv.add_voxels([0], [[1, 0, 1]], rng=np.random.default_rng(17), a=15.0)
+    box = Actor("box", np.array([1.0, 1.0, 1.0]), bv, times=np.array([0.0, 2.0]),
+                positions=np.array([[1.5, 2.5, 1.0], [1.5, 2.5, 1.0]]),
+                quaternions=np.array([yaw(20.0), yaw(20.0)]))
+    sc = Scene(bounds=bounds, static=static, actors=[cart, box])
+    sc = roundtrip("actors", sc)
+    oc = R_ray.build_scene_octrees(sc)
+    rng = np.random.default_rng(9)
+    o = rng.uniform(-1.0, 5.0, (400, 3))
+    d = (2.2 + rng.uniform(-1.2, 1.2, (400, 3))) - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    ts = rng.uniform(0.0, 2.0, 400)
+    rec = R_ray.integrate_rays(sc, oc, o, d, t_stamps=ts, background=(0.1, 0.2, 0.05))
+    gt = np.random.default_rng(10).uniform(0, 1, (400, 3))
+    _, d_c = loss_color(rec, gt, np.ones(400, bool))
+    _, d_d = loss_depth(rec, np.full(400, 2.5), np.ones(400, bool))
+    g = R_bw.backward_records(rec, sc, d_c, 0.3 * d_d)
+    out.update(act_o=o, act_d=d, act_t=ts, act_color=rec.out_color, act_opacity=rec.opacity,
+               act_depth=rec.depth, act_ray=rec.ray, act_owner=rec.owner, act_vid=rec.vid, act_t0=rec.t0,
+               act_dcolor=d_c, act_ddepth=0.3 * d_d,
+               **{f"act_g_{own}_{k}": v for own, gg in g.items() for k, v in gg.items()})
+
     # 6. sensors
     pin = R_sen.CameraModel(kind="pinhole", width=32, height=24, fx=30.0, fy=31.0, cx=15.5, cy=12.25,
                             position=np.array([0.3, -0.2, 1.1]),
