@@ -51,6 +51,7 @@ typedef struct {
   const double *geo;
   const double *aux;
   const float *prm;
+  const double *rot;  /* M x 9 voxel rotation matrices (flattened actors), or NULL */
   int32_t density_mode;
   int32_t pad;
 } salf_scene_t;

@@ -32,7 +32,7 @@ vp = C.c_void_p
 
 
 class SceneT(C.Structure):
-    _fields_ = [("n", C.c_int64), ("geo", vp), ("aux", vp), ("prm", vp),
+    _fields_ = [("n", C.c_int64), ("geo", vp), ("aux", vp), ("prm", vp), ("rot", vp),
                 ("density_mode", C.c_int32), ("pad", C.c_int32)]
 
 

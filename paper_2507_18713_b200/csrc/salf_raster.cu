@@ -60,7 +60,7 @@ __device__ __forceinline__ void span_from_rect(double umin, double vmin, double 
   span = make_int4((int)u_lo / c.tile, (int)v_lo / c.tile, (int)u_hi / c.tile, (int)v_hi / c.tile);
 }
 
-__global__ void k_project(int64_t n, const double4 *__restrict__ geo, PinholeDev c,
+__global__ void k_project(int64_t n, const double4 *__restrict__ geo, const double *__restrict__ vrot, PinholeDev c,
                           double4 *__restrict__ rect, double *__restrict__ zc_out,
                           uint8_t *__restrict__ culled_out, int4 *__restrict__ span_ref,
                           int4 *__restrict__ span_fit, uint64_t *__restrict__ zkey) {
@@ -74,9 +74,18 @@ __global__ void k_project(int64_t n, const double4 *__restrict__ geo, PinholeDev
   for (int k = 0; k < 8; ++k) {
     // corner = centre + offset * edge; offsets x fastest (render_raster.py:32-34, :106-109)
     const double off[3] = {(k & 1) ? 0.5 : -0.5, (k & 2) ? 0.5 : -0.5, (k & 4) ? 0.5 : -0.5};
+    double ofs[3] = {__dmul_rn(off[0], g.w), __dmul_rn(off[1], g.w), __dmul_rn(off[2], g.w)};
+    if (vrot) {  // rotated voxels: offs = R . offs, einsum("nij,nkj->nki") order (p0 + p2) + p1
+      const double *R = vrot + 9 * i;
+      double r3[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        r3[a] = __dadd_rn(__dadd_rn(__dmul_rn(R[3 * a], ofs[0]), __dmul_rn(R[3 * a + 2], ofs[2])), __dmul_rn(R[3 * a + 1], ofs[1]));
+      ofs[0] = r3[0]; ofs[1] = r3[1]; ofs[2] = r3[2];
+    }
     double rel[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) rel[j] = __dsub_rn(__dadd_rn(ctr[j], __dmul_rn(off[j], g.w)), c.pos[j]);
+    for (int j = 0; j < 3; ++j) rel[j] = __dsub_rn(__dadd_rn(ctr[j], ofs[j]), c.pos[j]);
 #pragma unroll
     for (int j = 0; j < 3; ++j) pc[k][j] = mm_col(rel, c.rot, j);  // (corners - pos) @ R
     if (pc[k][2] <= c.near) ++n_back; else ++n_front;
@@ -215,6 +224,8 @@ struct Entry {
   double a, inv_b;  // density transfer (aux)
   int64_t vid;
   VoxPrm p;       // field parameters, staged once per tile chunk
+  double R[9];    // voxel rotation (flattened actors); used when rot != 0
+  int rot;
 };
 
 struct PixelRay {
@@ -248,6 +259,27 @@ __device__ __forceinline__ void pixel_ray(const PinholeDev &c, int px, int py, P
     r.inv[k] = 1.0 / r.d[k];
     r.pos[k] = r.inv[k] > 0.0;
     r.fast = r.fast && !r.zero[k] && isfinite(r.inv[k]);
+  }
+}
+
+// The pixel ray seen in a rotated voxel's frame: d' = R^T d in the reference's
+// einsum("nji,nj->ni") order (render_raster.py:191-196); t_near is unchanged.
+__device__ __forceinline__ void rotate_ray(const PixelRay &r, const Entry &e, PixelRay &out) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    out.d[i] = __dadd_rn(__dadd_rn(__dmul_rn(e.R[i], r.d[0]), __dmul_rn(e.R[3 + i], r.d[1])), __dmul_rn(e.R[6 + i], r.d[2]));
+  out.t_near = r.t_near;
+  out.gam[0] = (float)kShC0;
+  out.gam[1] = (float)(kShC1 * out.d[1]);
+  out.gam[2] = (float)(kShC1 * out.d[2]);
+  out.gam[3] = (float)(kShC1 * out.d[0]);
+  out.fast = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    out.zero[k] = (out.d[k] == 0.0);
+    out.inv[k] = 1.0 / out.d[k];
+    out.pos[k] = out.inv[k] > 0.0;
+    out.fast = out.fast && !out.zero[k] && isfinite(out.inv[k]);
   }
 }
 
@@ -294,7 +326,8 @@ __device__ __forceinline__ bool pair_hit(const PixelRay &r, const Entry &e, doub
 
 struct SegVals {
   double tm, delta, x[3], s, e, sigma, alpha, om, c[3], a, inv_b;
-  float cf[3];  // fp32 colour (fast mode)
+  double dir[3];  // view direction in the voxel's frame
+  float cf[3];    // fp32 colour (fast mode)
 };
 
 // Fields of one hit pair (render_raster.py:239-253).  Divisions by 0.5*edge
@@ -306,6 +339,7 @@ __device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const PixelRa
   sv.tm = __dmul_rn(0.5, __dadd_rn(t0, t1));
 #pragma unroll
   for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, r.d[k])), e.inv_half);
+  sv.dir[0] = r.d[0]; sv.dir[1] = r.d[1]; sv.dir[2] = r.d[2];
   sv.a = e.a;
   sv.inv_b = e.inv_b;
   sv.s = eval_sdf(e.p, sv.x);
@@ -318,6 +352,23 @@ __device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const PixelRa
     eval_color32g(e.p, xf, r.gam, sv.cf);
     sv.c[0] = sv.cf[0]; sv.c[1] = sv.cf[1]; sv.c[2] = sv.cf[2];
   }
+}
+
+// Pair test + fields for one staged entry; rotated entries (flattened actor
+// voxels) are tested and shaded with the ray in the voxel's frame.
+template <bool kExactColor>
+__device__ __forceinline__ bool hit_and_shade(const salf_scene_t &sc, const PixelRay &r, const Entry &e, SegVals &sv) {
+  double t0, t1;
+  if (!e.rot) {
+    if (!pair_hit(r, e, t0, t1)) return false;
+    shade_pair<kExactColor>(sc, r, e, t0, t1, sv);
+    return true;
+  }
+  PixelRay rr;
+  rotate_ray(r, e, rr);
+  if (!pair_hit(rr, e, t0, t1)) return false;
+  shade_pair<kExactColor>(sc, rr, e, t0, t1, sv);
+  return true;
 }
 
 __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const PinholeDev &c, int32_t vid,
@@ -333,6 +384,22 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
   e.o[0] = __dsub_rn(c.pos[0], g.x);
   e.o[1] = __dsub_rn(c.pos[1], g.y);
   e.o[2] = __dsub_rn(c.pos[2], g.z);
+  e.rot = 0;
+  if (sc.rot) {
+    const double *R = sc.rot + 9 * (int64_t)vid;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      e.R[k] = R[k];
+      if (R[k] != ((k % 4 == 0) ? 1.0 : 0.0)) e.rot = 1;
+    }
+    if (e.rot) {  // o' = R^T o (einsum "nji,nj->ni", render_raster.py:195)
+      double o2[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        o2[i] = __dadd_rn(__dadd_rn(__dmul_rn(R[i], e.o[0]), __dmul_rn(R[3 + i], e.o[1])), __dmul_rn(R[6 + i], e.o[2]));
+      e.o[0] = o2[0]; e.o[1] = o2[1]; e.o[2] = o2[2];
+    }
+  }
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     e.lo[k] = __dsub_rn(-e.half, e.o[k]);
@@ -376,10 +443,8 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
     __syncthreads();
     if (alive) {
       for (int j = 0; j < cn; ++j) {
-        double t0, t1;
-        if (!pair_hit(r, sm[j], t0, t1)) continue;
         SegVals sv;
-        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv);
+        if (!hit_and_shade<kExactColor>(sc, r, sm[j], sv)) continue;
         if (T > keep) {  // included iff T_before > 1 - stop_threshold
           const double w = __dmul_rn(T, sv.alpha);
           if (kExactColor) {
@@ -432,7 +497,7 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
                                                   const int32_t *__restrict__ entries,
                                                   const double *__restrict__ saved, const double *__restrict__ d_rgb,
                                                   const double *__restrict__ d_depth, double *__restrict__ grad) {
-  __shared__ Entry sm[kChunk];
+  __shared__ Entry sm[kChunkB];
   const int tile_id = blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
@@ -488,10 +553,8 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
       const int64_t jj = base - beg + j;
       float g[32];
       bool act = false;
-      double t0, t1;
-      if (inside && jj < n_stop && pair_hit(r, sm[j], t0, t1)) {
-        SegVals sv;
-        shade_pair<kExactColor>(sc, r, sm[j], t0, t1, sv);
+      SegVals sv;
+      if (inside && jj < n_stop && hit_and_shade<kExactColor>(sc, r, sm[j], sv)) {
         if (T > keep) {
           const double w = __dmul_rn(T, sv.alpha);
           // A = dC . c + dD (t_mid - D) / ws   (backward.py:52-59, einsum order (0+2)+1)
@@ -501,7 +564,7 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
           prefix = __dadd_rn(prefix, __dmul_rn(A, w));
           const double suffix = __dsub_rn(total, prefix);
           segment_grad(sc.density_mode, sv.delta, sv.sigma, sv.alpha, sv.om, sv.s, sv.e, sv.a, sv.inv_b, sv.x, sv.c,
-                       r.d, A, T, w, suffix, tail, dC, g);
+                       sv.dir, A, T, w, suffix, tail, dC, g);
           act = true;
           T = __dmul_rn(T, sv.om);
         }
@@ -543,7 +606,7 @@ extern "C" int salf_project_voxels(const salf_scene_t *scene, const salf_camera_
     PinholeDev c = make_pinhole(cam, near, tile);
     const int bs = 128;
     k_project<<<(unsigned)((scene->n + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(
-        scene->n, reinterpret_cast<const double4 *>(scene->geo), c, reinterpret_cast<double4 *>(rect), z_center,
+        scene->n, reinterpret_cast<const double4 *>(scene->geo), scene->rot, c, reinterpret_cast<double4 *>(rect), z_center,
         culled, reinterpret_cast<int4 *>(span_ref), reinterpret_cast<int4 *>(span_fit), zkey);
     return check_cuda("salf_project_voxels");
   }

@@ -20,9 +20,6 @@ from .scene import FlatVoxels, Scene, flatten_scene
 
 class DeviceScene:
     def __init__(self, flat: FlatVoxels, device=None):
-        if np.any(flat.rotations != np.array([1.0, 0.0, 0.0, 0.0])) and flat.n:
-            if not np.allclose(flat.rotations, np.array([1.0, 0.0, 0.0, 0.0])):
-                raise NotImplementedError("rotated voxels are not supported by the B200 path yet")
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.n = flat.n
@@ -44,6 +41,13 @@ class DeviceScene:
         self.geo = torch.as_tensor(pad(geo), device=self.device).contiguous()
         self.aux = torch.as_tensor(pad(aux), device=self.device).contiguous()
         self.prm = torch.as_tensor(pad(prm), device=self.device).contiguous()
+        # voxel rotations (flattened actors): the reference rotates only when
+        # not np.allclose(rotations, identity) (render_raster.py:107, :192)
+        self.rot = None
+        if flat.n and not np.allclose(flat.rotations, np.array([1.0, 0.0, 0.0, 0.0])):
+            from .scene import quat_to_matrix
+            self.rot = torch.as_tensor(np.ascontiguousarray(quat_to_matrix(flat.rotations).reshape(-1, 9)),
+                                       device=self.device)
         self.flat = flat
 
     @classmethod
@@ -54,6 +58,7 @@ class DeviceScene:
         s = _lib.SceneT()
         s.n = self.n
         s.geo, s.aux, s.prm = self.geo.data_ptr(), self.aux.data_ptr(), self.prm.data_ptr()
+        s.rot = self.rot.data_ptr() if self.rot is not None else None
         s.density_mode = _lib.DENSITY[self.density_mode]
         return s
 

@@ -85,6 +85,20 @@ def _opts(background, stop_threshold, exact_color) -> _lib.RasterOptsT:
     return o
 
 
+def _static_device_scene(scene) -> DeviceScene:
+    """The static voxel set on the device (actors are marched in their own frames)."""
+    if isinstance(scene, Scene):
+        from .scene import FlatVoxels
+        v = scene.static
+        ds = DeviceScene(FlatVoxels(v.centers(), v.edges(), v.rotation, v.w_s, v.w_c, v.w_sh, v.log_a, v.log_b,
+                                    scene.density_mode))
+    else:
+        ds = as_device_scene(scene)
+    if ds.rot is not None:
+        raise NotImplementedError("rotated static voxels are not supported by the ray path")
+    return ds
+
+
 def _octree_of(octrees) -> OctreeBuffer:
     return octrees.static if isinstance(octrees, SceneOctrees) else octrees
 
@@ -175,7 +189,7 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
     live = isinstance(scene, Scene) and any(a.voxels.n for a in scene.actors)
     if live and not isinstance(octrees, SceneOctrees):
         raise ValueError("scenes with actors need build_scene_octrees(scene)")
-    ds = as_device_scene(scene)
+    ds = _static_device_scene(scene)
     tree = _octree_of(octrees)
     dev = ds.device
     o = _lib.as_f64(origins, dev).reshape(-1, 3)
@@ -266,7 +280,7 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
     depth and the view direction, by a linear `head` (2, 13) + sigmoid to
     intensity and drop probability."""
     lib = _lib.load()
-    ds = as_device_scene(scene)
+    ds = _static_device_scene(scene)
     tree = _octree_of(octrees)
     dev = ds.device
     o = _lib.as_f64(batch.origins, dev).reshape(-1, 3)
@@ -364,5 +378,5 @@ def render_lidar_ranges(scene, octrees, batch, *, chunk: int = 65536) -> torch.T
 
 def segments(scene, octrees, origins, dirs, stop_threshold: float = STOP_THRESHOLD):
     """The ray path's hit list with the reference's early stop (parity export)."""
-    ds = as_device_scene(scene)
+    ds = _static_device_scene(scene)
     return march_segments(_octree_of(octrees), origins, dirs, np.inf, ds, stop_threshold, True)

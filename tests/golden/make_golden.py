@@ -79,7 +79,7 @@ def raster_records_reference(flat, cam, background):
     dirs = batch.dirs
     t_near = R_ras.NEAR_PLANE / (dirs @ cam.rotation_matrix())[:, 2]
     h, w, tile = cam.height, cam.width, bins.tile
-    rays, vids, t0s, t1s = [], [], [], []
+    rays, vids, t0s, t1s, os_, ds_ = [], [], [], [], [], []
     for t in range(bins.tiles_x * bins.tiles_y):
         ent = bins.entries[bins.offsets[t]:bins.offsets[t + 1]]
         if ent.size == 0:
@@ -94,14 +94,16 @@ def raster_records_reference(flat, cam, background):
         t0 = np.maximum(np.maximum(t_in, t_near[pp]), 0.0)
         hit = t_out > t0 + 1e-12
         rays.append(pp[hit]); vids.append(vv[hit]); t0s.append(t0[hit]); t1s.append(t_out[hit])
+        os_.append(o[hit]); ds_.append(d[hit])
     ray = np.concatenate(rays); vid = np.concatenate(vids)
     t0 = np.concatenate(t0s); t1 = np.concatenate(t1s)
+    o_all, d_all = np.concatenate(os_), np.concatenate(ds_)
     order = np.argsort(ray, kind="stable")
     ray, vid, t0, t1 = ray[order], vid[order], t0[order], t1[order]
     from salf.scene import eval_color, eval_sdf, sdf_to_density, segment_opacity
     tm = 0.5 * (t0 + t1)
-    o = cam.position[None, :] - flat.centers[vid]
-    d = dirs[ray]
+    o = o_all[order]  # pair-frame origin / direction (rotated for actor voxels, :191-196)
+    d = d_all[order]
     x = (o + tm[:, None] * d) / (0.5 * flat.edges[vid])[:, None]
     s = eval_sdf(x, flat.w_s[vid])
     sig = sdf_to_density(s, np.exp(flat.log_a[vid]), np.exp(flat.log_b[vid]))
@@ -116,6 +118,17 @@ def raster_records_reference(flat, cam, background):
         sigma=sig, alpha=alpha, color=color, t_before=t_before, included=included,
         out_color=out_color, opacity=opacity, depth=depth, weight_sum=weight_sum, t_final=t_final,
         background=bg, density_mode="sdf", group_start=starts)
+
+
+def _flat_set(flat, bounds):
+    """A SparseVoxelSet view of flattened voxels (only the params are used by
+    backward_records' 'static' owner)."""
+    v = SparseVoxelSet(bounds, budget=flat.n + 1)
+    v.level = np.zeros(flat.n, np.uint8)
+    v.ijk = np.zeros((flat.n, 3), np.int32)
+    v.w_s, v.w_c, v.w_sh, v.log_a, v.log_b = flat.w_s, flat.w_c, flat.w_sh, flat.log_a, flat.log_b
+    v.rotation = flat.rotations
+    return v
 
 
 def main():
@@ -261,6 +274,20 @@ def main():
     _, d_c = loss_color(rec, gt, np.ones(400, bool))
     _, d_d = loss_depth(rec, np.full(400, 2.5), np.ones(400, bool))
     g = R_bw.backward_records(rec, sc, d_c, 0.3 * d_d)
+    # raster with the actors flattened at t = 0.7 (rotated voxels, render_raster.py:63-89)
+    cam = cam_at([-3.0, -2.0, 4.5], [2.0, 2.0, 1.8], width=64, height=48, f=50.0)
+    flat = R_ras.flatten_scene(sc, 0.7)
+    bins = R_ras.cull_and_bin(flat, cam)
+    fb = R_ras.rasterize(flat, cam, background=(0.1, 0.2, 0.05))
+    rr = raster_records_reference(flat, cam, (0.1, 0.2, 0.05))
+    _, d_c2 = loss_color(rr, np.full((64 * 48, 3), 0.3), np.ones(rr.n_rays, bool))
+    sc_flat = Scene(bounds=sc.bounds, static=sc.static)  # owner layout for backward_records
+    g2 = R_bw.backward_records(rr, Scene(bounds=sc.bounds, static=_flat_set(flat, sc.bounds)), d_c2,
+                               np.zeros(rr.n_rays))["static"]
+    out.update(actr_offsets=bins.offsets, actr_entries=bins.entries, actr_color=fb.color,
+               actr_opacity=fb.opacity, actr_depth=fb.depth, actr_dcolor=d_c2,
+               **{f"actr_g_{k}": v for k, v in g2.items()})
+    meta["actr_cam"] = cam_dict(cam)
     out.update(act_o=o, act_d=d, act_t=ts, act_color=rec.out_color, act_opacity=rec.opacity,
                act_depth=rec.depth, act_ray=rec.ray, act_owner=rec.owner, act_vid=rec.vid, act_t0=rec.t0,
                act_dcolor=d_c, act_ddepth=0.3 * d_d,

@@ -324,3 +324,23 @@ def test_dynamic_actors_ray_path(golden):
     for own in ("static", "cart", "box"):
         want = {k: golden[f"act_g_{own}_{k}"] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
         assert grads_close(g[own], want) < 1e-4, own
+
+
+def test_dynamic_actors_raster_path(golden, golden_meta):
+    """rasterize with the actors flattened at t = 0.7 (rotated voxels,
+    render_raster.py:63-129, :185-198): bit-exact CSR, colours, and the raster
+    backward through rotated voxels."""
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    sc = load_golden_scene("actors")
+    flat = flatten_scene(sc, 0.7)
+    cam = _cam(golden_meta["actr_cam"])
+    bins = RR.cull_and_bin(flat, cam)
+    np.testing.assert_array_equal(bins.offsets, golden["actr_offsets"])
+    np.testing.assert_array_equal(bins.entries, golden["actr_entries"])
+    fb, st = RR.rasterize(flat, cam, background=(0.1, 0.2, 0.05), return_state=True, exact_color=True)
+    assert_image_close(_np(fb.color), golden["actr_color"])
+    assert_image_close(_np(fb.depth), golden["actr_depth"])
+    g = RR.rasterize_backward(st, golden["actr_dcolor"].reshape(48, 64, 3), np.zeros((48, 64)))
+    want = {k: golden["actr_g_" + k] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
+    assert grads_close(g, want) < 1e-4
