@@ -167,6 +167,20 @@ int salf_octree_build_host(int64_t n, const uint8_t *level, const int32_t *ijk,
                            int32_t root_depth, int32_t *nodes, int64_t capacity,
                            int64_t *n_nodes, int32_t *max_depth);
 
+/* build_octree on the device, same layout as the host
+ * build.  Step 1: every voxel v (depth D = root_depth + level) writes the
+ * packed preorder keys of its D ancestors at keys[base[v] ..] (base =
+ * exclusive scan of D) and of itself at self_key[v].  The caller sorts and
+ * uniques the ancestor keys (internal nodes in reference DFS order).
+ * Step 2: nodes (1 + 8 n_internal words, pre-filled with -1) get every
+ * internal node's child-block word and every voxel's leaf word; *contained
+ * is set when a voxel sits at an internal node's depth (reference error
+ * "stored voxel contains another stored voxel"). */
+int salf_octree_ancestor_keys(int64_t n, const uint8_t *level, const int32_t *ijk, int32_t root_depth,
+                              const int64_t *base, uint64_t *keys, uint64_t *self_key, void *stream);
+int salf_octree_fill(int64_t n, int64_t n_internal, const uint64_t *internal, const uint64_t *self_key,
+                     int32_t *nodes, int32_t *contained, void *stream);
+
 /* query_batch (octree.py:136-166): flag (i8), vid (i64), corner (x3), edge. */
 int salf_octree_query(const salf_octree_t *tree, int64_t n, const double *p, int8_t *flag,
                       int64_t *vid, double *corner, double *edge, int32_t *out_of_root,

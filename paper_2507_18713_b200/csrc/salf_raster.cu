@@ -224,8 +224,7 @@ struct Entry {
   double a, inv_b;  // density transfer (aux)
   int64_t vid;
   VoxPrm p;       // field parameters, staged once per tile chunk
-  double R[9];    // voxel rotation (flattened actors); used when rot != 0
-  int rot;
+  int rot;        // rotated voxel (flattened actor): R is read from scene.rot
 };
 
 struct PixelRay {
@@ -264,10 +263,10 @@ __device__ __forceinline__ void pixel_ray(const PinholeDev &c, int px, int py, P
 
 // The pixel ray seen in a rotated voxel's frame: d' = R^T d in the reference's
 // einsum("nji,nj->ni") order (render_raster.py:191-196); t_near is unchanged.
-__device__ __forceinline__ void rotate_ray(const PixelRay &r, const Entry &e, PixelRay &out) {
+__device__ __forceinline__ void rotate_ray(const PixelRay &r, const double *R, PixelRay &out) {
 #pragma unroll
   for (int i = 0; i < 3; ++i)
-    out.d[i] = __dadd_rn(__dadd_rn(__dmul_rn(e.R[i], r.d[0]), __dmul_rn(e.R[3 + i], r.d[1])), __dmul_rn(e.R[6 + i], r.d[2]));
+    out.d[i] = __dadd_rn(__dadd_rn(__dmul_rn(R[i], r.d[0]), __dmul_rn(R[3 + i], r.d[1])), __dmul_rn(R[6 + i], r.d[2]));
   out.t_near = r.t_near;
   out.gam[0] = (float)kShC0;
   out.gam[1] = (float)(kShC1 * out.d[1]);
@@ -330,47 +329,63 @@ struct SegVals {
   float cf[3];    // fp32 colour (fast mode)
 };
 
-// Fields of one hit pair (render_raster.py:239-253).  Divisions by 0.5*edge
-// and by b are multiplications by precomputed reciprocals (<= 1 ulp).
+// Fields of one hit pair (render_raster.py:239-253), with the ray direction
+// `dir` in the voxel's frame (the pixel ray, or R^T d for rotated voxels).
+// Divisions by 0.5*edge and by b are multiplications by precomputed
+// reciprocals (<= 1 ulp).
 template <bool kExactColor>
-__device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const PixelRay &r, const Entry &e,
-                                           double t0, double t1, SegVals &sv) {
+__device__ __forceinline__ void shade_pair(const salf_scene_t &sc, const double dir[3], const float gam[4],
+                                           const Entry &e, double t0, double t1, SegVals &sv) {
   sv.delta = __dsub_rn(t1, t0);
   sv.tm = __dmul_rn(0.5, __dadd_rn(t0, t1));
 #pragma unroll
-  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, r.d[k])), e.inv_half);
-  sv.dir[0] = r.d[0]; sv.dir[1] = r.d[1]; sv.dir[2] = r.d[2];
+  for (int k = 0; k < 3; ++k) sv.x[k] = __dmul_rn(__dadd_rn(e.o[k], __dmul_rn(sv.tm, dir[k])), e.inv_half);
+  sv.dir[0] = dir[0]; sv.dir[1] = dir[1]; sv.dir[2] = dir[2];
   sv.a = e.a;
   sv.inv_b = e.inv_b;
   sv.s = eval_sdf(e.p, sv.x);
   sv.sigma = density(sc.density_mode, sv.s, e.a, e.inv_b, sv.e);
   sv.alpha = seg_alpha(sv.sigma, sv.delta, sv.om);
   if (kExactColor) {
-    eval_color64(e.p, sv.x, r.d, sv.c);
+    eval_color64(e.p, sv.x, dir, sv.c);
   } else {
     const float xf[3] = {(float)sv.x[0], (float)sv.x[1], (float)sv.x[2]};
-    eval_color32g(e.p, xf, r.gam, sv.cf);
+    eval_color32g(e.p, xf, gam, sv.cf);
     sv.c[0] = sv.cf[0]; sv.c[1] = sv.cf[1]; sv.c[2] = sv.cf[2];
   }
 }
 
 // Pair test + fields for one staged entry; rotated entries (flattened actor
-// voxels) are tested and shaded with the ray in the voxel's frame.
-template <bool kExactColor>
+// voxels) are tested and shaded with the ray in the voxel's frame.  One
+// shading instance serves both cases (only the slab test is duplicated).
+template <bool kExactColor, bool kRot>
 __device__ __forceinline__ bool hit_and_shade(const salf_scene_t &sc, const PixelRay &r, const Entry &e, SegVals &sv) {
   double t0, t1;
-  if (!e.rot) {
+  if (!kRot) {
     if (!pair_hit(r, e, t0, t1)) return false;
-    shade_pair<kExactColor>(sc, r, e, t0, t1, sv);
+    shade_pair<kExactColor>(sc, r.d, r.gam, e, t0, t1, sv);
     return true;
   }
   PixelRay rr;
-  rotate_ray(r, e, rr);
-  if (!pair_hit(rr, e, t0, t1)) return false;
-  shade_pair<kExactColor>(sc, rr, e, t0, t1, sv);
+  bool hit;
+  if (!e.rot) {
+    hit = pair_hit(r, e, t0, t1);
+  } else {
+    rotate_ray(r, sc.rot + 9 * e.vid, rr);
+    hit = pair_hit(rr, e, t0, t1);
+  }
+  if (!hit) return false;
+  double dir[3];
+  float gam[4];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) dir[k] = e.rot ? rr.d[k] : r.d[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) gam[k] = e.rot ? rr.gam[k] : r.gam[k];
+  shade_pair<kExactColor>(sc, dir, gam, e, t0, t1, sv);
   return true;
 }
 
+template <bool kRot>
 __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const PinholeDev &c, int32_t vid,
                                             Entry &e) {
   const double4 g = ldg_d4(sc.geo + 4 * (int64_t)vid);
@@ -385,13 +400,11 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
   e.o[1] = __dsub_rn(c.pos[1], g.y);
   e.o[2] = __dsub_rn(c.pos[2], g.z);
   e.rot = 0;
-  if (sc.rot) {
+  if (kRot) {
     const double *R = sc.rot + 9 * (int64_t)vid;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      e.R[k] = R[k];
+    for (int k = 0; k < 9; ++k)
       if (R[k] != ((k % 4 == 0) ? 1.0 : 0.0)) e.rot = 1;
-    }
     if (e.rot) {  // o' = R^T o (einsum "nji,nj->ni", render_raster.py:195)
       double o2[3];
 #pragma unroll
@@ -410,7 +423,7 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
 constexpr int kChunk = 64;   // entries staged per step (192 B each in shared memory)
 constexpr int kChunkB = 32;  // backward: + a 32 x 8 x 27 fp32 reduction buffer
 
-template <bool kExactColor>
+template <bool kExactColor, bool kRot>
 __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                    const int64_t *__restrict__ offsets,
                                                    const int32_t *__restrict__ entries, float *__restrict__ out_rgb,
@@ -439,12 +452,12 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
   for (int64_t base = beg; base < end; base += kChunk) {
     const int cn = (int)min((int64_t)kChunk, end - base);
     __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry(sc, c, entries[base + j], sm[j]);
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry<kRot>(sc, c, entries[base + j], sm[j]);
     __syncthreads();
     if (alive) {
       for (int j = 0; j < cn; ++j) {
         SegVals sv;
-        if (!hit_and_shade<kExactColor>(sc, r, sm[j], sv)) continue;
+        if (!hit_and_shade<kExactColor, kRot>(sc, r, sm[j], sv)) continue;
         if (T > keep) {  // included iff T_before > 1 - stop_threshold
           const double w = __dmul_rn(T, sv.alpha);
           if (kExactColor) {
@@ -488,7 +501,7 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
 // ---------------------------------------------------------------------------
 // backward
 
-template <bool kExactColor>
+template <bool kExactColor, bool kRot>
 #ifndef SALF_BWD_MINB
 #define SALF_BWD_MINB 2
 #endif
@@ -547,14 +560,14 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
   for (int64_t base = beg; base < lim; base += kChunkB) {
     const int cn = (int)min((int64_t)kChunkB, lim - base);
     __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry(sc, c, entries[base + j], sm[j]);
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry<kRot>(sc, c, entries[base + j], sm[j]);
     __syncthreads();
     for (int j = 0; j < cn; ++j) {
       const int64_t jj = base - beg + j;
       float g[32];
       bool act = false;
       SegVals sv;
-      if (inside && jj < n_stop && hit_and_shade<kExactColor>(sc, r, sm[j], sv)) {
+      if (inside && jj < n_stop && hit_and_shade<kExactColor, kRot>(sc, r, sm[j], sv)) {
         if (T > keep) {
           const double w = __dmul_rn(T, sv.alpha);
           // A = dC . c + dD (t_mid - D) / ws   (backward.py:52-59, einsum order (0+2)+1)
@@ -737,12 +750,20 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
     PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
     const int n_tiles = c.tiles_x * c.tiles_y;
     const int threads = std::max(32, opts->tile * opts->tile);
-    if (opts->exact_color)
-      k_composite<true><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, out_rgb,
-                                                                        out_opacity, out_depth, saved);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool rot = scene->rot != nullptr;
+    if (opts->exact_color && rot)
+      k_composite<true, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                           out_depth, saved);
+    else if (opts->exact_color)
+      k_composite<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                            out_depth, saved);
+    else if (rot)
+      k_composite<false, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                            out_depth, saved);
     else
-      k_composite<false><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, out_rgb,
-                                                                         out_opacity, out_depth, saved);
+      k_composite<false, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                             out_depth, saved);
     return check_cuda("salf_raster_composite");
   }
   SALF_CATCH
@@ -759,12 +780,20 @@ extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera
     PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
     const int n_tiles = c.tiles_x * c.tiles_y;
     const int threads = ((std::max(32, opts->tile * opts->tile) + 31) / 32) * 32;
-    if (opts->exact_color)
-      k_backward<true><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, saved,
-                                                                       d_rgb, d_depth, grad);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool rot = scene->rot != nullptr;
+    if (opts->exact_color && rot)
+      k_backward<true, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                          grad);
+    else if (opts->exact_color)
+      k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                           grad);
+    else if (rot)
+      k_backward<false, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                           grad);
     else
-      k_backward<false><<<n_tiles, threads, 0, (cudaStream_t)stream>>>(*scene, c, *opts, offsets, entries, saved,
-                                                                        d_rgb, d_depth, grad);
+      k_backward<false, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                            grad);
     return check_cuda("salf_raster_backward");
   }
   SALF_CATCH

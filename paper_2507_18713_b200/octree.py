@@ -98,6 +98,57 @@ def build_octree(voxels: SparseVoxelSet, bounds: SceneBounds | None = None, devi
                         int(depth.value))
 
 
+def build_octree_device(voxels: SparseVoxelSet, bounds: SceneBounds | None = None, device=None) -> OctreeBuffer:
+    """build_octree on the GPU: the reference's DFS layout
+    from sorted preorder keys (csrc/salf_octree.cu); same validation as
+    build_octree."""
+    lib = _lib.load()
+    if bounds is None:
+        bounds = voxels.bounds
+    extent = bounds.aabb_max - bounds.aabb_min
+    m = max(0, int(np.ceil(np.log2(max(extent.max(), 1e-300) / bounds.base_edge) - 1e-12)))
+    root_edge = bounds.base_edge * 2.0 ** m
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    n = voxels.n
+    if n == 0:
+        return OctreeBuffer(torch.full((1,), -1, dtype=torch.int32, device=dev), bounds.aabb_min.copy(),
+                            root_edge, m)
+    level = voxels.level.astype(np.int64)
+    if m + int(level.max()) > 19:
+        return build_octree(voxels, bounds, device)  # deeper than the packed key: host build
+    cells = voxels.ijk.astype(np.int64)
+    edges = voxels.edges()
+    if edges.min() < MIN_EDGE_FACTOR * EPS_ADVANCE:
+        raise ValueError(f"voxel edge {edges.min():.3g} m below the marching floor "
+                         f"{MIN_EDGE_FACTOR * EPS_ADVANCE:.3g} m")
+    keys = (level << 54) ^ (cells[:, 0] << 36) ^ (cells[:, 1] << 18) ^ cells[:, 2]
+    if len(np.unique(keys)) != n:
+        raise ValueError("duplicate voxel cells in the set")
+    centers = voxels.centers()
+    if np.any(centers < bounds.aabb_min) or np.any(centers > bounds.aabb_max):
+        raise ValueError("voxel outside scene bounds")
+    lv = torch.as_tensor(voxels.level.astype(np.uint8), device=dev)
+    ijk = torch.as_tensor(np.ascontiguousarray(voxels.ijk.astype(np.int32)), device=dev)
+    depth = m + lv.to(torch.int64)
+    base = torch.cumsum(depth, 0) - depth
+    total = int(depth.sum().item())
+    akeys = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
+    skeys = torch.empty(n, dtype=torch.int64, device=dev)
+    s = _lib.stream_ptr()
+    _lib.check(lib.salf_octree_ancestor_keys(n, lv.data_ptr(), ijk.data_ptr(), m, base.data_ptr(),
+                                             akeys.data_ptr(), skeys.data_ptr(), s), "build_octree")
+    # keys < 2^62, so signed int64 order == unsigned order
+    internal = torch.unique(akeys[:total]) if total else akeys[:0]
+    n_int = int(internal.numel())
+    nodes = torch.full((1 + 8 * n_int,), -1, dtype=torch.int32, device=dev)
+    contained = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(lib.salf_octree_fill(n, n_int, internal.data_ptr(), skeys.data_ptr(), nodes.data_ptr(),
+                                    contained.data_ptr(), s), "build_octree")
+    if int(contained.item()):
+        raise ValueError("stored voxel contains another stored voxel")
+    return OctreeBuffer(nodes, bounds.aabb_min.copy(), root_edge, m + int(level.max()))
+
+
 def dump_table(buffer: OctreeBuffer) -> str:
     """octree.py:128-133."""
     ids, leaf = buffer.nodes_id, buffer.nodes_leaf
