@@ -15,6 +15,7 @@
 #include <math.h>
 
 #include "../../include/salf_b200.h"
+#include "salf_fastmath.h"
 
 namespace salf {
 
@@ -101,9 +102,9 @@ __device__ __forceinline__ double eval_sdf(const VoxPrm &p, const double x[3]) {
 __device__ __forceinline__ double density(int mode, double s, double a, double inv_b, double &e) {
   if (mode == SALF_DENSITY_RAW) {
     e = 0.0;
-    return exp(s);
+    return salf_fm::exp(s);
   }
-  e = exp(__dmul_rn(-fabs(s), inv_b));
+  e = salf_fm::exp(__dmul_rn(-fabs(s), inv_b));
   double inner = __dadd_rn(1.0, __dmul_rn(npsign(s), __dsub_rn(1.0, e)));
   return __dmul_rn(__dmul_rn(0.5, a), inner);
 }
@@ -111,13 +112,21 @@ __device__ __forceinline__ double density(int mode, double s, double a, double i
 // segment_opacity (scene.py:282-284) -> clamped alpha and its complement
 // 1 - alpha = exp(-sigma delta) from the same expm1 (no cancellation).
 __device__ __forceinline__ double seg_alpha(double sigma, double delta, double &one_minus) {
-  const double em = expm1(__dmul_rn(-sigma, delta));
+  const double em = salf_fm::expm1(__dmul_rn(-sigma, delta));
   const double a = -em;
   if (a != a) { one_minus = a; return a; }
   if (a >= kAlphaMax) { one_minus = 1.0 - kAlphaMax; return kAlphaMax; }
   if (a <= 0.0) { one_minus = 1.0; return 0.0; }  // np.clip(alpha, 0, .) (alpha >= 0 anyway)
   one_minus = __dadd_rn(1.0, em);
   return a;
+}
+
+// MUFU reciprocal (rcp.approx.ftz, ~1 ulp; rcp(inf) = 0) for the fp32
+// sigmoid -- the IEEE __frcp_rn adds a Newton step and a slow-path branch.
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // eval_color (scene.py:270-279), fp64: z = W_c x + W_sh gamma, sigmoid.
@@ -155,7 +164,7 @@ __device__ __forceinline__ void eval_color32(const VoxPrm &p, const double xd[3]
     z = __fmaf_rn(p.wsh[4 * i + 1], g1, z);
     z = __fmaf_rn(p.wsh[4 * i + 2], g2, z);
     z = __fmaf_rn(p.wsh[4 * i + 3], g3, z);
-    c[i] = (double)__frcp_rn(1.0f + __expf(-z));
+    c[i] = (double)fast_rcp(1.0f + __expf(-z));
   }
 }
 
@@ -168,7 +177,7 @@ __device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3],
     z = __fmaf_rn(p.wsh[4 * i + 1], gam[1], z);
     z = __fmaf_rn(p.wsh[4 * i + 2], gam[2], z);
     z = __fmaf_rn(p.wsh[4 * i + 3], gam[3], z);
-    c[i] = __frcp_rn(1.0f + __expf(-z));
+    c[i] = fast_rcp(1.0f + __expf(-z));
   }
 }
 
@@ -223,7 +232,7 @@ __device__ __forceinline__ void segment_grad(int mode, double delta, double sigm
   const double g_alpha = __dsub_rn(__dmul_rn(A, tb), __ddiv_rn(__dadd_rn(suffix, tail), __dsub_rn(1.0, alpha)));
   // exp(-sigma delta) = 1 - alpha (unclamped) from the forward's expm1
   const double g_sigma = __dmul_rn(__dmul_rn(g_alpha, delta),
-                                   alpha >= kAlphaMax ? exp(__dmul_rn(-sigma, delta)) : om);
+                                   alpha >= kAlphaMax ? salf_fm::exp(__dmul_rn(-sigma, delta)) : om);
   double ds;
   if (mode == SALF_DENSITY_SDF) {
     const double k2 = __dmul_rn(__dmul_rn(a, 0.5), inv_b);

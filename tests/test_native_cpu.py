@@ -90,3 +90,15 @@ def test_no_cpu_fallback_without_gpu():
     sc = load_golden_scene("rand400")
     with pytest.raises(RuntimeError, match="CUDA"):
         render_raster.rasterize_scene(sc, CameraModel("pinhole", 8, 8, 8.0, 8.0, 4.0, 4.0))
+
+
+def test_fastmath_exp_expm1_accuracy(tmp_path):
+    """csrc/salf_fastmath.h (the exp/expm1 the render kernels use), compiled
+    on the host with FMA contraction off: exp <= 1 ulp, expm1 <= 1.1 ulp on the
+    render path's range (x <= 0), specials (NaN, +-inf, 0, overflow) exact."""
+    import subprocess
+    exe = tmp_path / "fmc"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-std=c++17", str(ROOT / "tools" / "fastmath_check.cpp"),
+                    "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe), "300000"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr

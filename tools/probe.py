@@ -31,6 +31,9 @@ for regime in sys.argv[1:] or ["surface","init"]:
     dc=torch.full((1080,1920,3),1e-6,device='cuda',dtype=torch.float64); dd=torch.zeros((1080,1920),device='cuda',dtype=torch.float64)
     res[f"c2_bwd_ms_{regime}"]=timeit(lambda: RR.rasterize_backward(st, dc, dd, as_dict=False), n=3)
     t=time.time(); oc=RY.build_scene_octrees(sc); res[f"octree_build_s_{regime}"]=time.time()-t
+    from paper_2507_18713_b200.octree import build_octree_device
+    build_octree_device(sc.static); torch.cuda.synchronize()
+    t=time.time(); build_octree_device(sc.static); torch.cuda.synchronize(); res[f"octree_build_device_s_{regime}"]=time.time()-t
     lb=S.gen_lidar_rays(configs.c3_lidar())
     res[f"c3_ms_{regime}"]=timeit(lambda: RY.integrate_rays(ds, oc, lb.origins, lb.dirs))
     rec=RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
