@@ -168,6 +168,22 @@ __device__ __forceinline__ void eval_color32(const VoxPrm &p, const double xd[3]
   }
 }
 
+// MUFU exp (ex2.approx of x log2 e): relative error ~2^-22 + |x| 2^-24.
+__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+
+// expm1(x) for x <= 0 in fp32 without cancellation: degree-7 Taylor on
+// (-0.25, 0] (truncation |x|^8/8! < 4e-10 relative), exp(x) - 1 below it
+// (|expm1| >= 0.22 there, so the MUFU error stays ~1e-7 relative).  Branchless.
+__device__ __forceinline__ float expm1_neg(float x) {
+  float p = __fmaf_rn(x, 1.0f / 5040.0f, 1.0f / 720.0f);
+  p = __fmaf_rn(x, p, 1.0f / 120.0f);
+  p = __fmaf_rn(x, p, 1.0f / 24.0f);
+  p = __fmaf_rn(x, p, 1.0f / 6.0f);
+  p = __fmaf_rn(x, p, 0.5f);
+  const float small = __fmaf_rn(x * x, p, x);
+  return x > -0.25f ? small : fast_exp(x) - 1.0f;
+}
+
 // fp32 colour with a precomputed per-ray SH basis gam = (C0, C1 y, C1 z, C1 x).
 __device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3], const float gam[4], float c[3]) {
 #pragma unroll

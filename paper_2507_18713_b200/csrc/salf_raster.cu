@@ -602,6 +602,167 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
   (void)keep;
 }
 
+// Mixed-precision backward (default, fast mode).  Which entries a pixel
+// includes is fixed by the forward: the hits before its saved stop index
+// n_stop (inclusion is monotone in T), so no fp64 transmittance is needed to
+// reproduce it.  What stays fp64 is what is ill-conditioned at driving-scene
+// distances (camera-voxel distance ~1000x the voxel edge): the slab test,
+// delta, t_mid, the local coordinates x and t_mid - D.  Everything after x
+// (SDF, density, alpha, colour, the gradient chain) is fp32; the prefix sum
+// of A w stays fp64 because the suffix is recovered by subtraction.
+// Segment fields in the reference's order: backward.py:52-100.
+#ifndef SALF_BWDF_MINB
+#define SALF_BWDF_MINB 3
+#endif
+template <bool kRot>
+__global__ void __launch_bounds__(256, SALF_BWDF_MINB) k_backward_fast(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+                                                          const int64_t *__restrict__ offsets,
+                                                          const int32_t *__restrict__ entries,
+                                                          const double *__restrict__ saved,
+                                                          const double *__restrict__ d_rgb,
+                                                          const double *__restrict__ d_depth,
+                                                          double *__restrict__ grad) {
+  __shared__ Entry sm[kChunkB];
+  __shared__ float red[kChunkB][8][kGradStride];
+  __shared__ long long s_max;
+  const int tile_id = blockIdx.x;
+  const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
+  const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
+  const int px = tx * c.tile + lx, py = ty * c.tile + ly;
+  const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
+  const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
+  const int nthreads = blockDim.x;
+  const bool sdf = sc.density_mode == SALF_DENSITY_SDF;
+
+  PixelRay r;
+  float dC[3] = {0.f, 0.f, 0.f}, dws = 0.f, tail = 0.f, T = 1.f;
+  double total = 0.0, prefix = 0.0, D = 0.0;
+  int64_t n_stop = 0;
+  if (threadIdx.x == 0) s_max = 0;
+  if (inside) {
+    pixel_ray(c, px, py, r);
+    const int64_t pix = (int64_t)py * c.width + px;
+    const double *s = saved + pix * SALF_SAVED_STRIDE;
+    double dCd[3];
+    for (int k = 0; k < 3; ++k) dCd[k] = d_rgb[pix * 3 + k];
+    const double acc_w = s[3], acc_wt = s[4];
+    const bool ok = acc_w > kDepthWeightMin;  // depth_valid (backward.py:46-49)
+    const double dd = ok ? d_depth[pix] : 0.0;
+    D = ok ? acc_wt / acc_w : 0.0;
+    const double ws = ok ? acc_w : 1.0;
+    total = dCd[0] * s[0] + dCd[1] * s[1] + dCd[2] * s[2] + dd * (acc_wt - D * acc_w) / ws;
+    tail = (float)((dCd[0] * opt.background[0] + dCd[1] * opt.background[1] + dCd[2] * opt.background[2]) * s[5]);
+    dws = (float)(dd / ws);
+    for (int k = 0; k < 3; ++k) dC[k] = (float)dCd[k];
+    n_stop = (int64_t)s[6];
+  }
+  __syncthreads();
+  if (n_stop > 0) atomicMax(&s_max, (long long)n_stop);
+  __syncthreads();
+  const int64_t lim = beg + (int64_t)s_max;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = nthreads >> 5;
+  for (int64_t base = beg; base < lim; base += kChunkB) {
+    const int cn = (int)min((int64_t)kChunkB, lim - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry<kRot>(sc, c, entries[base + j], sm[j]);
+    __syncthreads();
+    for (int j = 0; j < cn; ++j) {
+      const Entry &e = sm[j];
+      float g[32];
+      bool act = false;
+      double t0, t1;
+      if (base - beg + j < n_stop) {
+        const double *dir = r.d;
+        const float *gam = r.gam;
+        PixelRay rr;
+        bool hit;
+        if (kRot && e.rot) {
+          rotate_ray(r, sc.rot + 9 * e.vid, rr);
+          hit = pair_hit(rr, e, t0, t1);
+          dir = rr.d;
+          gam = rr.gam;
+        } else {
+          hit = pair_hit(r, e, t0, t1);
+        }
+        if (hit) {
+          act = true;
+          // fp64: delta, t_mid, local coordinates (render_raster.py:242-244)
+          const double tm = 0.5 * (t0 + t1);
+          const float delta = (float)(t1 - t0);
+          const float q = (float)(tm - D);
+          float x[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) x[k] = (float)((e.o[k] + tm * dir[k]) * e.inv_half);
+          // fp32 fields (scene.py:229-284)
+          const VoxPrm &p = e.p;
+          const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
+          const float a = (float)e.a, inv_b = (float)e.inv_b;
+          float ee = 0.f, sigma;
+          if (sdf) {
+            ee = fast_exp(-fabsf(s) * inv_b);
+            const float sg = s > 0.f ? 1.f : (s < 0.f ? -1.f : 0.f);
+            sigma = 0.5f * a * __fmaf_rn(sg, 1.f - ee, 1.f);
+          } else {
+            sigma = fast_exp(s);
+          }
+          const float y = sigma * delta;
+          const float om = fast_exp(-y);                   // exp(-sigma delta), unclamped
+          const bool clamped = y > 27.631021115928547f;    // alpha >= 1 - 1e-12 (scene.py:32)
+          const float alpha = clamped ? 1.f : -expm1_neg(-y);
+          const float omc = clamped ? 1e-12f : om;         // 1 - alpha as the reference clamps it
+          float col[3];
+          eval_color32g(p, x, gam, col);
+          const float w = T * alpha;
+          // A = dC . c + dD (t_mid - D) / ws (backward.py:52-59)
+          const float A = __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], dC[0] * col[0])) + dws * q;
+          prefix += (double)(A * w);
+          const float suffix = (float)(total - prefix);
+          const float g_alpha = A * T - (suffix + tail) / omc;  // backward.py:62-64
+          const float g_sigma = g_alpha * delta * om;           // :66
+          float ds;
+          if (sdf) {
+            const float k2 = 0.5f * a * inv_b;
+            ds = (s == 0.f) ? 0.f : g_sigma * k2 * ee;         // :92
+            g[25] = g_sigma * sigma;                            // :94
+            g[26] = -g_sigma * k2 * s * ee;                     // :95
+          } else {
+            ds = g_sigma * sigma;
+            g[25] = 0.f;
+            g[26] = 0.f;
+          }
+          g[0] = ds * x[0]; g[1] = ds * x[1]; g[2] = ds * x[2]; g[3] = ds;
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const float gz = dC[i] * w * col[i] * (1.f - col[i]);  // :69-70
+#pragma unroll
+            for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = gz * x[k];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) g[13 + 4 * i + k] = gz * gam[k];
+          }
+#pragma unroll
+          for (int k = kGradStride; k < 32; ++k) g[k] = 0.f;
+          T *= omc;
+        }
+      }
+      float tot = 0.0f;
+      if (__ballot_sync(0xffffffffu, act)) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) g[k] = act ? g[k] : 0.0f;
+        tot = warp_transpose_reduce(g);
+      }
+      if (lane < kGradStride) red[j][warp][lane] = tot;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < cn * kGradStride; q += nthreads) {
+      const int j = q / kGradStride, k = q - j * kGradStride;
+      float sum = 0.0f;
+      for (int w = 0; w < nwarps; ++w) sum += red[j][w][k];
+      if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
+    }
+  }
+}
+
 }  // namespace salf
 
 // ---------------------------------------------------------------------------
@@ -789,11 +950,11 @@ extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera
       k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
                                                            grad);
     else if (rot)
-      k_backward<false, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
-                                                           grad);
+      k_backward_fast<true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                         grad);
     else
-      k_backward<false, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
-                                                            grad);
+      k_backward_fast<false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                          grad);
     return check_cuda("salf_raster_backward");
   }
   SALF_CATCH

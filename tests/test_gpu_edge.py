@@ -161,6 +161,35 @@ def test_zero_loss_and_background_only_give_zero_grads():
     assert all(np.all(v == 0.0) for v in g.values())
 
 
+@pytest.mark.parametrize("mode", ["sdf", "raw"])
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_raster_backward_density_modes(mode, exact):
+    """Raster backward in both density modes (scene.py:245-253) and both
+    precisions against the oracle composition (raster pairs -> _composite ->
+    backward_records), normwise 1e-4 per parameter class."""
+    import dataclasses
+    from conftest import grads_close
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    rng = np.random.default_rng(11)
+    cells = np.unique(rng.integers(0, 8, (120, 3)), axis=0)
+    sc = _scene([0, 0, 0], [4, 4, 4], 0.5, 2, cells, a=3.0, seed=11)
+    sc = dataclasses.replace(sc, density_mode=mode)
+    cam = _cam(pos=(5.3, 4.7, 3.9), w=40, h=36, f=36.0, target=(2.0, 2.0, 2.0))
+    bg = (0.05, 0.1, 0.15)
+    fb, st = RR.rasterize(flatten_scene(sc), cam, background=bg, return_state=True, exact_color=exact)
+    dc = rng.normal(size=(36, 40, 3)) * 1e-2
+    dd = rng.normal(size=(36, 40)) * 1e-3
+    g = RR.rasterize_backward(st, dc, dd)
+    vox = oracle_voxels(sc)
+    ocam = O.Camera("pinhole", 40, 36, 36.0, 36.0, 20.0, 18.0, position=cam.position,
+                    quaternion=cam.quaternion)
+    rec = O.raster_records(vox, ocam, background=bg)
+    want = O.backward_records(rec, vox, dc.reshape(-1, 3), dd.reshape(-1))
+    assert np.isfinite(rec["out_color"]).all() and np.abs(want["w_s"]).max() > 0
+    assert grads_close(g, want) < 1e-4
+
+
 def test_fisheye_invalid_pixels_keep_background():
     from paper_2507_18713_b200 import render_ray as RY
     from paper_2507_18713_b200.sensors import CameraModel, camera_rays

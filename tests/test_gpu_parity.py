@@ -120,11 +120,13 @@ def test_tile_size_is_scheduling_only(golden_meta):
     assert torch.equal(torch.nan_to_num(a.depth, 7.0), torch.nan_to_num(b.depth, 7.0))
 
 
-def test_raster_backward_matches_reference_composition(golden, golden_meta):
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_raster_backward_matches_reference_composition(golden, golden_meta, exact):
+    """exact: the fp64 backward; mixed: the default fp64-geometry / fp32-field backward."""
     from paper_2507_18713_b200 import render_raster as RR
     cam = _cam(golden_meta["rand300_cam"])
     fb, st = RR.rasterize(_flat("rand300"), cam, background=(0.05, 0.1, 0.15), return_state=True,
-                          exact_color=True)
+                          exact_color=exact)
     h, w = cam.height, cam.width
     g = RR.rasterize_backward(st, golden["rand300_rbw_dcolor"].reshape(h, w, 3),
                               golden["rand300_rbw_ddepth"].reshape(h, w))
@@ -326,7 +328,8 @@ def test_dynamic_actors_ray_path(golden):
         assert grads_close(g[own], want) < 1e-4, own
 
 
-def test_dynamic_actors_raster_path(golden, golden_meta):
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_dynamic_actors_raster_path(golden, golden_meta, exact):
     """rasterize with the actors flattened at t = 0.7 (rotated voxels,
     render_raster.py:63-129, :185-198): bit-exact CSR, colours, and the raster
     backward through rotated voxels."""
@@ -338,7 +341,7 @@ def test_dynamic_actors_raster_path(golden, golden_meta):
     bins = RR.cull_and_bin(flat, cam)
     np.testing.assert_array_equal(bins.offsets, golden["actr_offsets"])
     np.testing.assert_array_equal(bins.entries, golden["actr_entries"])
-    fb, st = RR.rasterize(flat, cam, background=(0.1, 0.2, 0.05), return_state=True, exact_color=True)
+    fb, st = RR.rasterize(flat, cam, background=(0.1, 0.2, 0.05), return_state=True, exact_color=exact)
     assert_image_close(_np(fb.color), golden["actr_color"])
     assert_image_close(_np(fb.depth), golden["actr_depth"])
     g = RR.rasterize_backward(st, golden["actr_dcolor"].reshape(48, 64, 3), np.zeros((48, 64)))
