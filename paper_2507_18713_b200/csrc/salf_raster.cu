@@ -611,53 +611,536 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
 // (SDF, density, alpha, colour, the gradient chain) is fp32; the prefix sum
 // of A w stays fp64 because the suffix is recovered by subtraction.
 // Segment fields in the reference's order: backward.py:52-100.
-#ifndef SALF_BWDF_MINB
-#define SALF_BWDF_MINB 3
+//
+// Each thread owns NP pixels of the tile (rows ly, ly + rows/NP, ...): their
+// 27-vectors are summed in registers before the warp's transposed
+// reduction, so the shuffle reduction, the staged-entry reads and the loop
+// overhead are paid once per NP pixels.
+
+// Pixel ray for the mixed-precision pair test: fp64 direction (for the
+// closest-approach parameter), fp32 direction / reciprocals / SH basis.
+struct RayF {
+  double d[3];
+  double tn0;  // max(t_near, 0)
+  float df[3], inv[3], gam[4];
+  bool fast;   // no zero component (else the fp64 reference slab test runs)
+};
+
+__device__ __forceinline__ void rayf_from_dir(const double d[3], double t_near, RayF &r) {
+  r.fast = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.d[k] = d[k];
+    r.df[k] = (float)d[k];
+    r.inv[k] = 1.0f / r.df[k];
+    r.fast = r.fast && d[k] != 0.0 && isfinite(r.inv[k]);
+  }
+  r.tn0 = t_near > 0.0 ? t_near : 0.0;
+  r.gam[0] = (float)kShC0;
+  r.gam[1] = (float)(kShC1 * d[1]);
+  r.gam[2] = (float)(kShC1 * d[2]);
+  r.gam[3] = (float)(kShC1 * d[0]);
+}
+
+// Staged entry of the mixed-precision backward.
+struct EntryF {
+  double o[3];      // camera position - voxel centre (fp64)
+  double half;      // 0.5 * edge (fp64, for the reference slab test fallback)
+  float hf, inv_hf; // fp32 half edge and its reciprocal
+  float a, inv_b;
+  int vid, rot;
+  VoxPrm p;
+  float wn;         // |w_s| 1-norm (error bound of the fp32 SDF)
+};
+
+template <bool kRot>
+__device__ __forceinline__ void stage_entry_f(const salf_scene_t &sc, const PinholeDev &c, int32_t vid, EntryF &e) {
+  const double4 g = ldg_d4(sc.geo + 4 * (int64_t)vid);
+  const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.aux + 4 * (int64_t)vid));
+  e.vid = vid;
+  e.a = (float)ab.x;
+  e.inv_b = (float)ab.y;
+  load_prm(sc.prm, vid, e.p);
+  e.wn = fabsf(e.p.ws[0]) + fabsf(e.p.ws[1]) + fabsf(e.p.ws[2]) + fabsf(e.p.ws[3]);
+  e.half = 0.5 * g.w;
+  e.hf = (float)e.half;
+  e.inv_hf = (float)(1.0 / e.half);
+  e.o[0] = c.pos[0] - g.x;
+  e.o[1] = c.pos[1] - g.y;
+  e.o[2] = c.pos[2] - g.z;
+  e.rot = 0;
+  if (kRot) {
+    const double *R = sc.rot + 9 * (int64_t)vid;
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (R[k] != ((k % 4 == 0) ? 1.0 : 0.0)) e.rot = 1;
+    if (e.rot) {  // o' = R^T o (render_raster.py:195)
+      double o2[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) o2[i] = R[i] * e.o[0] + R[3 + i] * e.o[1] + R[6 + i] * e.o[2];
+      e.o[0] = o2[0]; e.o[1] = o2[1]; e.o[2] = o2[2];
+    }
+  }
+}
+
+// Pair test in closest-approach coordinates.  With t* = -(o . d) the ray
+// point closest to the voxel centre, the ray is q + u d with
+// q = o + t* d (|q| ~ the voxel size for any hit) and u = t - t*, so the
+// slab test, delta, t_mid - t* and the local coordinates are all
+// well-conditioned in fp32; only t* and q take fp64 (6 DFMA per pair).
+// Returns the fp32 u-interval [u0, u1] and t* (fp64).  Rays with a zero
+// direction component use the fp64 reference slab test (octree.py:184-194).
+__device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float q[3], float &u0, float &u1,
+                                           double &ts) {
+  ts = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
+  if (r.fast) {
+    // slab k: u in [(-s h - q) / d, (s h - q) / d], s = sign(d): h |1/d| -/+ q/d
+    float un = -INFINITY, uf = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      q[k] = (float)fma(ts, r.d[k], e.o[k]);
+      const float qi = q[k] * r.inv[k];
+      un = fmaxf(un, __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi));
+      uf = fminf(uf, __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi));
+    }
+    u0 = fmaxf(un, (float)(r.tn0 - ts));
+    u1 = uf;
+    return u1 > u0;
+  }
+  double ti = 0.0, to = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    q[k] = (float)fma(ts, r.d[k], e.o[k]);
+    const double lo = -e.half - e.o[k], hi = e.half - e.o[k];
+    double nk, fk;
+    if (r.d[k] == 0.0) {
+      const bool inside = (e.o[k] >= -e.half) && (e.o[k] <= e.half);
+      nk = inside ? -INFINITY : INFINITY;
+      fk = inside ? INFINITY : -INFINITY;
+    } else {
+      const double inv = 1.0 / r.d[k];
+      const double ta = lo * inv, tb = hi * inv;
+      nk = npmin(ta, tb);
+      fk = npmax(ta, tb);
+    }
+    if (k == 0) { ti = nk; to = fk; }
+    else { ti = npmax(ti, nk); to = npmin(to, fk); }
+  }
+  const double t0 = npmax(ti, r.tn0);
+  if (!(to > t0 + 1e-12)) return false;
+  u0 = (float)(t0 - ts);
+  u1 = (float)(to - ts);
+  return true;
+}
+
+// Per-pixel backward state (fp64 only where the text above says).
+struct BwdPix {
+  RayF r;
+  float dC[3], dws, tail, T;
+  double total, prefix, D;
+  int n_stop;
+};
+
+__device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_raster_opts_t &opt, int px, int py,
+                                               const double *__restrict__ saved, const double *__restrict__ d_rgb,
+                                               const double *__restrict__ d_depth, BwdPix &q) {
+  PixelRay pr;
+  pixel_ray(c, px, py, pr);
+  rayf_from_dir(pr.d, pr.t_near, q.r);
+  const int64_t pix = (int64_t)py * c.width + px;
+  const double *s = saved + pix * SALF_SAVED_STRIDE;
+  double dCd[3];
+  for (int k = 0; k < 3; ++k) dCd[k] = d_rgb[pix * 3 + k];
+  const double acc_w = s[3], acc_wt = s[4];
+  const bool ok = acc_w > kDepthWeightMin;  // depth_valid (backward.py:46-49)
+  const double dd = ok ? d_depth[pix] : 0.0;
+  q.D = ok ? acc_wt / acc_w : 0.0;
+  const double ws = ok ? acc_w : 1.0;
+  // sum_j A_j w_j = dC . acc_rgb + dD (acc_wt - D acc_w) / ws (suffix sums by subtraction)
+  q.total = dCd[0] * s[0] + dCd[1] * s[1] + dCd[2] * s[2] + dd * (acc_wt - q.D * acc_w) / ws;
+  // tail = (dC . background) * T_final (backward.py:62)
+  q.tail = (float)((dCd[0] * opt.background[0] + dCd[1] * opt.background[1] + dCd[2] * opt.background[2]) * s[5]);
+  q.dws = (float)(dd / ws);
+  for (int k = 0; k < 3; ++k) q.dC[k] = (float)dCd[k];
+  q.n_stop = (int)s[6];
+  q.prefix = 0.0;
+  q.T = 1.f;
+}
+
+// One included segment of pixel q against staged entry e: adds its 27
+// gradient components to g.  Returns false on a miss.
+template <bool kRot>
+__device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, bool sdf, const EntryF &e, BwdPix &q,
+                                            float g[32]) {
+  float qv[3], u0, u1;
+  double ts;
+  const RayF *ray = &q.r;
+  RayF rr;
+  if (kRot && e.rot) {  // the pixel ray in the voxel's frame: d' = R^T d (render_raster.py:191-196)
+    const double *R = sc.rot + 9 * (int64_t)e.vid;
+    double d2[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) d2[i] = R[i] * q.r.d[0] + R[3 + i] * q.r.d[1] + R[6 + i] * q.r.d[2];
+    rayf_from_dir(d2, q.r.tn0, rr);
+    ray = &rr;
+  }
+  if (!pair_hit_f(*ray, e, qv, u0, u1, ts)) return false;
+  const float delta = u1 - u0;
+  const float um = 0.5f * (u0 + u1);
+  const float dq = (float)(ts - q.D) + um;  // t_mid - D
+  // (fp32 below: explicit FMAs -- this file is compiled with --fmad=false)
+  float x[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
+  const float *gam = ray->gam;
+  // fp32 fields (scene.py:229-284)
+  const VoxPrm &p = e.p;
+  const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
+  const float a = e.a, inv_b = e.inv_b;
+  const float ha = 0.5f * a;
+  float ee = 0.f, sigma;
+  if (sdf) {
+    // a/2 (1 + sign(s)(1 - e)): a - a/2 e for s > 0, a/2 e otherwise (e = 1 at s = 0)
+    ee = fast_exp(-fabsf(s) * inv_b);
+    const float he = ha * ee;
+    sigma = s > 0.f ? a - he : he;
+  } else {
+    sigma = fast_exp(s);
+  }
+  const float y = sigma * delta;
+  const float om = fast_exp(-y);                 // exp(-sigma delta), unclamped
+  const bool clamped = y > 27.631021115928547f;  // alpha >= 1 - 1e-12 (scene.py:32)
+  const float alpha = clamped ? 1.f : -expm1_neg(-y);
+  const float omc = clamped ? 1e-12f : om;       // 1 - alpha as the reference clamps it
+  float col[3];
+  eval_color32g(p, x, gam, col);
+  const float T = q.T;
+  const float w = T * alpha;
+  // A = dC . c + dD (t_mid - D) / ws (backward.py:52-59)
+  const float A = __fmaf_rn(q.dC[2], col[2], __fmaf_rn(q.dC[1], col[1], __fmaf_rn(q.dC[0], col[0], q.dws * dq)));
+  q.prefix += (double)(A * w);
+  const float suffix = (float)(q.total - q.prefix);
+  const float g_alpha = __fmaf_rn(A, T, -(suffix + q.tail) * fast_rcp(omc));  // backward.py:62-64
+  const float g_sigma = g_alpha * delta * om;                                  // :66
+  float ds, ga, gb;
+  if (sdf) {
+    const float k2e = ha * inv_b * ee;
+    ds = (s == 0.f) ? 0.f : g_sigma * k2e;  // :92
+    ga = g_sigma * sigma;                    // :94
+    gb = -g_sigma * k2e * s;                 // :95
+  } else {
+    ds = g_sigma * sigma;
+    ga = 0.f;
+    gb = 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k] = __fmaf_rn(ds, x[k], g[k]);
+  g[3] += ds;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float wc = w * col[i];
+    const float gz = q.dC[i] * __fmaf_rn(-wc, col[i], wc);  // dC w c (1 - c)  :69-70
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = __fmaf_rn(gz, x[k], g[4 + 3 * i + k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g[13 + 4 * i + k] = __fmaf_rn(gz, gam[k], g[13 + 4 * i + k]);
+  }
+  g[25] += ga;
+  g[26] += gb;
+  q.T = T * omc;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// Certified mixed-precision forward (default, fast mode).
+//
+// Same pair test and fields as the mixed-precision backward (closest-approach
+// fp32 geometry, fp32 fields).  The reference's transmittance is
+// T = exp(cumsum(log1p(-alpha))) = exp(-Y), Y = sum of y = min(sigma delta,
+// ln 1e12) (render_raster.py:258-266, scene.py:32); the kernel accumulates
+// Y in fp64 from fp32 y together with a bound EY on |Y - Y_exact|, so every
+// discrete decision of the reference is either certified or the pixel is
+// flagged:
+//   * hit / miss, t1 > t0 + 1e-12 (render_raster.py:241): a pair within its
+//     fp32 error of grazing contributes y <= sigma 4 dd either way, which is
+//     added to EY (SDF density, sigma <= a) or flags the pixel (raw density);
+//   * inclusion, T_before > 1 - stop_threshold (:267), i.e.
+//     Y < ln(1 / keep): certified outside +-(2 EY + 1e-9);
+//   * depth validity, sum w > 0.5 (:299); sum w = 1 - T_final (the weights
+//     telescope), i.e. Y_final > ln 2: certified outside the same band.
+// Flagged pixels are marked with opacity = NaN and recomputed by
+// k_composite_redo in fp64 reference order, so every pixel's hit set, stop
+// index and NaN-depth mask equal the fp64 path's; values differ by fp32
+// rounding (T = exp(-Y) to ~5e-7 relative).
+//
+// Error model (2^-24 = u): the u-parameters (+-h |1/d| - q / d) of a pair
+// carry |du| <= u (h + 2|q_k| + 3 |u_k|) |1/d_k| <= dd = 8 u h max|1/d|
+// (|q_k|, |u_k| <= sqrt(3) h wherever a hit is possible), so
+// |d delta| <= 2 dd and |dx| <= dd / h + 6 u; the SDF then carries
+// |ds| <= |w_s|_1 (|dx| + 4 u), sigma a relative error
+// rel <= |ds| / b + 3e-7 (1 + |s| / b) + 2.4e-7 (MUFU ex2 and roundings),
+// and |dy| <= y (rel + 2 u) + sigma 2 dd.
+#ifndef SALF_FLAGMASK
+#define SALF_FLAGMASK 7  // diagnostics: bit 0 hit, bit 1 inclusion, bit 2 depth certification
+#endif
+constexpr float kU24 = 5.9604645e-8f;  // 2^-24
+
+#ifndef SALF_FWDF_MINB
+#define SALF_FWDF_MINB 3
 #endif
 template <bool kRot>
-__global__ void __launch_bounds__(256, SALF_BWDF_MINB) k_backward_fast(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
-                                                          const int64_t *__restrict__ offsets,
-                                                          const int32_t *__restrict__ entries,
-                                                          const double *__restrict__ saved,
-                                                          const double *__restrict__ d_rgb,
-                                                          const double *__restrict__ d_depth,
-                                                          double *__restrict__ grad) {
-  __shared__ Entry sm[kChunkB];
-  __shared__ float red[kChunkB][8][kGradStride];
-  __shared__ long long s_max;
+__global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+                                                        const int64_t *__restrict__ offsets,
+                                                        const int32_t *__restrict__ entries,
+                                                        float *__restrict__ out_rgb, float *__restrict__ out_op,
+                                                        float *__restrict__ out_depth, double *__restrict__ saved) {
+  __shared__ EntryF sm[kChunk];
   const int tile_id = blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
   const int px = tx * c.tile + lx, py = ty * c.tile + ly;
   const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
   const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
-  const int nthreads = blockDim.x;
   const bool sdf = sc.density_mode == SALF_DENSITY_SDF;
+  const double y_stop = -log(1.0 - opt.stop_threshold);  // included iff Y_before < y_stop
+  constexpr double kLn2 = 0.6931471805599453;             // sum w > 0.5 iff Y_final > ln 2
+  constexpr float kYClamp = 27.631021115928547f;           // -ln(1 - kAlphaMax)
 
-  PixelRay r;
-  float dC[3] = {0.f, 0.f, 0.f}, dws = 0.f, tail = 0.f, T = 1.f;
-  double total = 0.0, prefix = 0.0, D = 0.0;
-  int64_t n_stop = 0;
-  if (threadIdx.x == 0) s_max = 0;
+  RayF r;
+  float pdd = 0.f;  // dd / h for this pixel
   if (inside) {
+    PixelRay pr;
+    pixel_ray(c, px, py, pr);
+    rayf_from_dir(pr.d, pr.t_near, r);
+    const float im = fmaxf(fabsf(r.inv[0]), fmaxf(fabsf(r.inv[1]), fabsf(r.inv[2])));
+    pdd = 8.f * kU24 * im;
+  }
+  float T = 1.f, acc_c[3] = {0.f, 0.f, 0.f}, acc_w = 0.f, EY = 0.f;
+  double Y = 0.0, acc_wt = 0.0;
+  bool alive = inside, flag = false;
+  int n_stop = (int)(end - beg), n_inc = 0;
+  const int nthreads = blockDim.x;
+
+  for (int64_t base = beg; base < end; base += kChunk) {
+    const int cn = (int)min((int64_t)kChunk, end - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j]);
+    __syncthreads();
+    if (alive) {
+      for (int j = 0; j < cn; ++j) {
+        const EntryF &e = sm[j];
+        const RayF *ray = &r;
+        RayF rr;
+        if (kRot && e.rot) {  // the pixel ray in the voxel's frame (render_raster.py:191-196)
+          const double *R = sc.rot + 9 * (int64_t)e.vid;
+          double d2[3];
+#pragma unroll
+          for (int i = 0; i < 3; ++i) d2[i] = R[i] * r.d[0] + R[3 + i] * r.d[1] + R[6 + i] * r.d[2];
+          rayf_from_dir(d2, r.tn0, rr);
+          ray = &rr;
+        }
+        float qv[3], u0, u1;
+        double ts;
+        const bool hit = pair_hit_f(*ray, e, qv, u0, u1, ts);
+        const float dd = pdd * e.hf;
+        if (!hit) {
+          // A near-grazing miss may be an fp64 hit with y <= sigma 4 dd <= a 4 dd (SDF: sigma <= a):
+          // widen the band instead of flagging; raw density has no such bound.  (Near-grazing hits
+          // are covered by the 2 sigma dd term of |dy|.)
+          if ((SALF_FLAGMASK & 1) && ray->fast && u1 - u0 > -2.f * dd) {
+            if (sdf) EY = __fmaf_rn(4.f * e.a, dd, EY);
+            else flag = true;
+          }
+          continue;
+        }
+        // inclusion of this hit: Y_before < y_stop (certified outside the band)
+        const double gap = y_stop - Y;
+        if ((SALF_FLAGMASK & 2) && fabs(gap) <= (double)__fmaf_rn(2.f, EY, 1e-9f)) flag = true;
+        if (!(gap > 0.0)) {  // stop: every later segment is excluded
+          alive = false;
+          n_stop = (int)(base - beg) + j;
+          break;
+        }
+        const float delta = u1 - u0;
+        const float um = 0.5f * (u0 + u1);
+        float x[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
+        const VoxPrm &p = e.p;
+        const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
+        const float ds_abs = e.wn * (pdd + 10.f * kU24);
+        float sigma, rel;
+        if (sdf) {
+          const float sb = fabsf(s) * e.inv_b;
+          const float he = 0.5f * e.a * fast_exp(-sb);
+          sigma = s > 0.f ? e.a - he : he;
+          rel = __fmaf_rn(ds_abs, e.inv_b, __fmaf_rn(3e-7f, sb, 5.4e-7f));
+        } else {
+          sigma = fast_exp(s);
+          rel = ds_abs + __fmaf_rn(3e-7f, fabsf(s), 5.4e-7f);
+        }
+        const float y = fminf(sigma * delta, kYClamp);  // -log1p(-clip(alpha))
+        const float alpha = y >= kYClamp ? 1.f : -expm1_neg(-y);
+        float col[3];
+        eval_color32g(p, x, ray->gam, col);
+        const float w = T * alpha;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
+        acc_w += w;
+        acc_wt = fma((double)w, ts + (double)um, acc_wt);
+        EY += __fmaf_rn(y, rel + 2.f * kU24, 2.f * sigma * dd);
+        Y += (double)y;
+        T = fast_exp(-(float)Y);
+        ++n_inc;
+      }
+    }
+    if (!__syncthreads_or(alive)) break;
+  }
+  if (!inside) return;
+  if ((SALF_FLAGMASK & 4) && fabs(Y - kLn2) <= (double)__fmaf_rn(2.f, EY, 1e-9f)) flag = true;
+  const bool valid = Y > kLn2;  // sum w = 1 - T_final > 0.5
+  const double wsum = -expm1(-Y);  // 1 - T_final, consistent with `valid`
+  const int64_t pix = (int64_t)py * c.width + px;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) out_rgb[pix * 3 + k] = __fmaf_rn(T, (float)opt.background[k], acc_c[k]);
+  out_op[pix] = flag ? NAN : 1.f - T;
+  out_depth[pix] = valid ? (float)(acc_wt / (double)acc_w) : NAN;
+  if (saved) {
+    double *sv = saved + pix * SALF_SAVED_STRIDE;
+    sv[0] = acc_c[0]; sv[1] = acc_c[1]; sv[2] = acc_c[2];
+    sv[3] = valid ? fmax(wsum, 0.5000000001) : fmin(wsum, 0.5);
+    sv[4] = acc_wt * (sv[3] / (double)acc_w);  // keeps D = acc_wt / acc_w
+    sv[5] = T; sv[6] = (double)n_stop; sv[7] = (double)n_inc;
+  }
+}
+
+// fp64 reference-order recomputation of the pixels k_composite_fast flagged
+// (opacity NaN).  One warp per 32 pixels of the image; for each flagged
+// pixel of its slice the whole warp cooperates: lane k stages and shades
+// entry base + k (fp64, the exact kernel's code), then the hits are
+// composited in list order from lane-broadcast values, so the arithmetic is
+// the sequential fp64 kernel's (same operations, same order).
+template <bool kRot>
+__global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
+                                                       const int64_t *__restrict__ offsets,
+                                                       const int32_t *__restrict__ entries,
+                                                       float *__restrict__ out_rgb, float *__restrict__ out_op,
+                                                       float *__restrict__ out_depth, double *__restrict__ saved) {
+  const int64_t npx = (int64_t)c.width * c.height;
+  const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
+  const int lane = threadIdx.x & 31;
+  if (p0 >= npx) return;
+  const int64_t mine = p0 + lane;
+  const float op = mine < npx ? out_op[mine] : 0.f;
+  unsigned todo = __ballot_sync(0xffffffffu, op != op);
+  const double keep = 1.0 - opt.stop_threshold;
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int64_t pix = p0 + src;
+    const int px = (int)(pix % c.width), py = (int)(pix / c.width);
+    const int tile_id = (py / c.tile) * c.tiles_x + px / c.tile;
+    const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
+    PixelRay r;
     pixel_ray(c, px, py, r);
-    const int64_t pix = (int64_t)py * c.width + px;
-    const double *s = saved + pix * SALF_SAVED_STRIDE;
-    double dCd[3];
-    for (int k = 0; k < 3; ++k) dCd[k] = d_rgb[pix * 3 + k];
-    const double acc_w = s[3], acc_wt = s[4];
-    const bool ok = acc_w > kDepthWeightMin;  // depth_valid (backward.py:46-49)
-    const double dd = ok ? d_depth[pix] : 0.0;
-    D = ok ? acc_wt / acc_w : 0.0;
-    const double ws = ok ? acc_w : 1.0;
-    total = dCd[0] * s[0] + dCd[1] * s[1] + dCd[2] * s[2] + dd * (acc_wt - D * acc_w) / ws;
-    tail = (float)((dCd[0] * opt.background[0] + dCd[1] * opt.background[1] + dCd[2] * opt.background[2]) * s[5]);
-    dws = (float)(dd / ws);
-    for (int k = 0; k < 3; ++k) dC[k] = (float)dCd[k];
-    n_stop = (int64_t)s[6];
+    double acc_w = 0.0, acc_wt = 0.0, T = 1.0;
+    float acc_c[3] = {0.f, 0.f, 0.f};
+    int64_t n_stop = end - beg;
+    int n_inc = 0;
+    bool alive = true;
+    for (int64_t base = beg; base < end && alive; base += 32) {
+      const int64_t j = base + lane;
+      SegVals sv;
+      bool hit = false;
+      if (j < end) {
+        Entry e;
+        stage_entry<kRot>(sc, c, entries[j], e);
+        hit = hit_and_shade<false, kRot>(sc, r, e, sv);
+      }
+      unsigned hits = __ballot_sync(0xffffffffu, hit);
+      while (hits) {
+        const int k = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const double alpha = __shfl_sync(0xffffffffu, sv.alpha, k);
+        const double om = __shfl_sync(0xffffffffu, sv.om, k);
+        const double tm = __shfl_sync(0xffffffffu, sv.tm, k);
+        float cf[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) cf[q] = __shfl_sync(0xffffffffu, sv.cf[q], k);
+        if (!(T > keep)) {  // included iff T_before > keep (render_raster.py:267)
+          n_stop = base - beg + k;
+          alive = false;
+          break;
+        }
+        const double w = __dmul_rn(T, alpha);
+        const float wf = (float)w;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc_c[q] = __fmaf_rn(wf, cf[q], acc_c[q]);
+        acc_w = __dadd_rn(acc_w, w);
+        acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, tm));
+        T = __dmul_rn(T, om);
+        ++n_inc;
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) out_rgb[pix * 3 + q] = (float)__dadd_rn(acc_c[q], __dmul_rn(T, opt.background[q]));
+      out_op[pix] = (float)__dsub_rn(1.0, T);
+      out_depth[pix] = acc_w > kDepthWeightMin ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
+      if (saved) {
+        double *s = saved + pix * SALF_SAVED_STRIDE;
+        s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
+        s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_stop; s[7] = (double)n_inc;
+      }
+    }
+  }
+}
+
+#ifndef SALF_BWD_SMEMRED
+#define SALF_BWD_SMEMRED 1  // warp reduction by a shared-memory transpose (0: shuffles; measured slower)
+#endif
+#ifndef SALF_BWD_NP
+#define SALF_BWD_NP 2  // pixels per thread
+#endif
+#ifndef SALF_BWDF_MINB
+#define SALF_BWDF_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
+
+template <bool kRot, int NP>
+__global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
+    salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
+    const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
+    const double *__restrict__ d_depth, double *__restrict__ grad) {
+  __shared__ EntryF sm[kChunkB];
+  __shared__ float red[kChunkB][8 / NP][kGradStride];
+#if SALF_BWD_SMEMRED
+  __shared__ __align__(16) float xp[8 / NP][32][28];
+#endif
+  __shared__ int s_max;
+  const int tile_id = blockIdx.x;
+  const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
+  const int nthreads = blockDim.x;
+  const int npix = c.tile * c.tile;
+  const bool sdf = sc.density_mode == SALF_DENSITY_SDF;
+  const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
+  (void)end;
+
+  BwdPix q[NP];
+  bool in[NP];
+  if (threadIdx.x == 0) s_max = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int li = threadIdx.x + k * nthreads;  // pixel slot in the tile
+    const int px = tx * c.tile + li % c.tile, py = ty * c.tile + li / c.tile;
+    in[k] = li < npix && px < c.width && py < c.height;
+    q[k].n_stop = 0;
+    if (in[k]) bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, q[k]);
   }
   __syncthreads();
-  if (n_stop > 0) atomicMax(&s_max, (long long)n_stop);
+  int my_max = 0;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) my_max = max(my_max, q[k].n_stop);
+  if (my_max > 0) atomicMax(&s_max, my_max);
   __syncthreads();
   const int64_t lim = beg + (int64_t)s_max;
 
@@ -665,97 +1148,40 @@ __global__ void __launch_bounds__(256, SALF_BWDF_MINB) k_backward_fast(salf_scen
   for (int64_t base = beg; base < lim; base += kChunkB) {
     const int cn = (int)min((int64_t)kChunkB, lim - base);
     __syncthreads();
-    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry<kRot>(sc, c, entries[base + j], sm[j]);
+    for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j]);
     __syncthreads();
+    const int jb = (int)(base - beg);
     for (int j = 0; j < cn; ++j) {
-      const Entry &e = sm[j];
+      const EntryF &e = sm[j];
       float g[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) g[k] = 0.f;
       bool act = false;
-      double t0, t1;
-      if (base - beg + j < n_stop) {
-        const double *dir = r.d;
-        const float *gam = r.gam;
-        PixelRay rr;
-        bool hit;
-        if (kRot && e.rot) {
-          rotate_ray(r, sc.rot + 9 * e.vid, rr);
-          hit = pair_hit(rr, e, t0, t1);
-          dir = rr.d;
-          gam = rr.gam;
-        } else {
-          hit = pair_hit(r, e, t0, t1);
-        }
-        if (hit) {
-          act = true;
-          // fp64: delta, t_mid, local coordinates (render_raster.py:242-244)
-          const double tm = 0.5 * (t0 + t1);
-          const float delta = (float)(t1 - t0);
-          const float q = (float)(tm - D);
-          float x[3];
 #pragma unroll
-          for (int k = 0; k < 3; ++k) x[k] = (float)((e.o[k] + tm * dir[k]) * e.inv_half);
-          // fp32 fields (scene.py:229-284)
-          const VoxPrm &p = e.p;
-          const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
-          const float a = (float)e.a, inv_b = (float)e.inv_b;
-          float ee = 0.f, sigma;
-          if (sdf) {
-            ee = fast_exp(-fabsf(s) * inv_b);
-            const float sg = s > 0.f ? 1.f : (s < 0.f ? -1.f : 0.f);
-            sigma = 0.5f * a * __fmaf_rn(sg, 1.f - ee, 1.f);
-          } else {
-            sigma = fast_exp(s);
-          }
-          const float y = sigma * delta;
-          const float om = fast_exp(-y);                   // exp(-sigma delta), unclamped
-          const bool clamped = y > 27.631021115928547f;    // alpha >= 1 - 1e-12 (scene.py:32)
-          const float alpha = clamped ? 1.f : -expm1_neg(-y);
-          const float omc = clamped ? 1e-12f : om;         // 1 - alpha as the reference clamps it
-          float col[3];
-          eval_color32g(p, x, gam, col);
-          const float w = T * alpha;
-          // A = dC . c + dD (t_mid - D) / ws (backward.py:52-59)
-          const float A = __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], dC[0] * col[0])) + dws * q;
-          prefix += (double)(A * w);
-          const float suffix = (float)(total - prefix);
-          const float g_alpha = A * T - (suffix + tail) / omc;  // backward.py:62-64
-          const float g_sigma = g_alpha * delta * om;           // :66
-          float ds;
-          if (sdf) {
-            const float k2 = 0.5f * a * inv_b;
-            ds = (s == 0.f) ? 0.f : g_sigma * k2 * ee;         // :92
-            g[25] = g_sigma * sigma;                            // :94
-            g[26] = -g_sigma * k2 * s * ee;                     // :95
-          } else {
-            ds = g_sigma * sigma;
-            g[25] = 0.f;
-            g[26] = 0.f;
-          }
-          g[0] = ds * x[0]; g[1] = ds * x[1]; g[2] = ds * x[2]; g[3] = ds;
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            const float gz = dC[i] * w * col[i] * (1.f - col[i]);  // :69-70
-#pragma unroll
-            for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = gz * x[k];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) g[13 + 4 * i + k] = gz * gam[k];
-          }
-#pragma unroll
-          for (int k = kGradStride; k < 32; ++k) g[k] = 0.f;
-          T *= omc;
-        }
-      }
+      for (int k = 0; k < NP; ++k)
+        if (jb + j < q[k].n_stop) act |= bwd_segment<kRot>(sc, sdf, e, q[k], g);
       float tot = 0.0f;
+#if SALF_BWD_SMEMRED
+      // transpose through shared memory: 7 x STS.128 per lane, lane k sums column k
       if (__ballot_sync(0xffffffffu, act)) {
+        float4 *row = reinterpret_cast<float4 *>(&xp[warp][lane][0]);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) g[k] = act ? g[k] : 0.0f;
-        tot = warp_transpose_reduce(g);
+        for (int m = 0; m < 7; ++m) row[m] = make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]);
+        __syncwarp();
+        if (lane < kGradStride) {
+#pragma unroll 8
+          for (int rr = 0; rr < 32; ++rr) tot += xp[warp][rr][lane];
+        }
+        __syncwarp();
       }
+#else
+      if (__ballot_sync(0xffffffffu, act)) tot = warp_transpose_reduce(g);
+#endif
       if (lane < kGradStride) red[j][warp][lane] = tot;
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < cn * kGradStride; q += nthreads) {
-      const int j = q / kGradStride, k = q - j * kGradStride;
+    for (int t = threadIdx.x; t < cn * kGradStride; t += nthreads) {
+      const int j = t / kGradStride, k = t - j * kGradStride;
       float sum = 0.0f;
       for (int w = 0; w < nwarps; ++w) sum += red[j][w][k];
       if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
@@ -919,12 +1345,26 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
     else if (opts->exact_color)
       k_composite<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
                                                             out_depth, saved);
-    else if (rot)
-      k_composite<false, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
-                                                            out_depth, saved);
-    else
-      k_composite<false, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+    else {
+      // certified mixed-precision pass, then fp64 recomputation of the flagged pixels
+      // (SALF_NO_REDO=1 skips the second pass: flagged pixels keep opacity NaN; diagnostics only)
+      static const bool no_redo = getenv("SALF_NO_REDO") && getenv("SALF_NO_REDO")[0] == '1';
+      const int64_t npx = (int64_t)c.width * c.height;
+      const unsigned rb = (unsigned)((npx + 127) / 128);
+      if (rot) {
+        k_composite_fast<true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
                                                              out_depth, saved);
+        if (!no_redo)
+          k_composite_redo<true><<<rb, 128, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                     out_depth, saved);
+      } else {
+        k_composite_fast<false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                              out_depth, saved);
+        if (!no_redo)
+          k_composite_redo<false><<<rb, 128, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+                                                      out_depth, saved);
+      }
+    }
     return check_cuda("salf_raster_composite");
   }
   SALF_CATCH
@@ -941,6 +1381,7 @@ extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera
     PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
     const int n_tiles = c.tiles_x * c.tiles_y;
     const int threads = ((std::max(32, opts->tile * opts->tile) + 31) / 32) * 32;
+    const int threads_np = ((std::max(32, (opts->tile * opts->tile + SALF_BWD_NP - 1) / SALF_BWD_NP) + 31) / 32) * 32;
     cudaStream_t st = (cudaStream_t)stream;
     const bool rot = scene->rot != nullptr;
     if (opts->exact_color && rot)
@@ -950,11 +1391,11 @@ extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera
       k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
                                                            grad);
     else if (rot)
-      k_backward_fast<true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
-                                                         grad);
+      k_backward_fast<true, SALF_BWD_NP><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved,
+                                                                          d_rgb, d_depth, grad);
     else
-      k_backward_fast<false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
-                                                          grad);
+      k_backward_fast<false, SALF_BWD_NP><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved,
+                                                                           d_rgb, d_depth, grad);
     return check_cuda("salf_raster_backward");
   }
   SALF_CATCH

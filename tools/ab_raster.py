@@ -52,6 +52,16 @@ for exact in (False, True):
     RR.rasterize_backward(st, dc, dd, grad=grad, as_dict=False)
     out[f"{key}_grad"] = grad.clone()
     out[f"{key}_rgb"] = fb.color.clone()
+# forward decisions: fast (certified + fp64 redo) vs exact, per pixel
+fa, sa = RR.rasterize(ds, cam, return_state=True, exact_color=False)
+fe, se = RR.rasterize(ds, cam, return_state=True, exact_color=True)
+na, ne = sa.saved[:, 6], se.saved[:, 6]
+out["fwd_stop_index_mismatch"] = int((na != ne).sum())
+out["fwd_depth_nan_mismatch"] = int((torch.isnan(fa.depth) != torch.isnan(fe.depth)).sum())
+m = ~torch.isnan(fe.depth)
+out["fwd_depth_max_rel"] = float(((fa.depth[m] - fe.depth[m]).abs() / fe.depth[m].abs()).max())
+out["fwd_opacity_max_abs"] = float((fa.opacity - fe.opacity).abs().max())
+out["fwd_color_max_abs_vs_exact"] = float((fa.color - fe.color).abs().max())
 ga, gb = out.pop("fast_grad"), out.pop("exact_grad")
 sl = {"w_s": slice(0, 4), "w_c": slice(4, 13), "w_sh": slice(13, 25), "log_a": slice(25, 26),
       "log_b": slice(26, 27)}
@@ -59,4 +69,7 @@ out["grad_normwise_err"] = {k: float((ga[:, s] - gb[:, s]).abs().max() / gb[:, s
                             for k, s in sl.items()}
 ra, rb = out.pop("fast_rgb"), out.pop("exact_rgb")
 out["rgb_max_abs_err"] = float((ra - rb).abs().max())
+import os
+if os.environ.get("SALF_NO_REDO") == "1":
+    out["flagged_pixels"] = int(torch.isnan(fa.opacity).sum())
 print(json.dumps(out))
