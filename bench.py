@@ -190,18 +190,19 @@ def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles):
     return fwd, bwd
 
 
-def _fp64_peak(dev) -> float:
-    """Measured FP64 FMA throughput (TFLOP/s) of this GPU: best of 3 launches."""
+def _alu_peak(dev, fp32: bool) -> float:
+    """Measured FP64 (DFMA) or FP32 (FFMA) throughput (TFLOP/s) of this GPU: best of 4 launches."""
     import torch
     from paper_2507_18713_b200 import _lib
     lib = _lib.load()
     scratch = torch.zeros(148 * 16, dtype=torch.float64, device=dev)
-    grid, iters = 148 * 16, 4000
+    grid, iters = 148 * 16, (16000 if fp32 else 4000)
+    fn = lib.salf_fp32_peak if fp32 else lib.salf_fp64_peak
     best = 0.0
     for _ in range(4):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        _lib.check(lib.salf_fp64_peak(scratch.data_ptr(), grid, iters, _lib.stream_ptr()))
+        _lib.check(fn(scratch.data_ptr(), grid, iters, _lib.stream_ptr()))
         b.record()
         torch.cuda.synchronize()
         flops = grid * 256 * 64 * iters * 2.0
@@ -380,22 +381,25 @@ def run_ours(args, world, rank, local):
 
     # secondary (ALU) roofline of the forward composite: SURVEY §8d's
     # F = 24 P + 120 S_inc flop (P = pair tests, S_inc = included segments,
-    # both read from the frame's saved state) against a live FP64 peak probe
+    # both read from the frame's saved state) against a live FP32 FFMA peak
+    # probe -- the default path shades in fp32 (fp64 only for the per-pair
+    # closest-approach parameter and the log-transmittance sum)
     sv = st.saved
     pairs = float(sv[:, 6].sum().item())
     s_inc = float(sv[:, 7].sum().item())
     flops = 24.0 * pairs + 120.0 * s_inc
-    fp64_peak = _fp64_peak(dev)
-    alu = {"bound": "fp64", "kernel": "raster_composite", "unit": "TFLOP/s",
-           "achieved": flops / (k_fwd * 1e-3) / 1e12, "peak": fp64_peak,
-           "frac": flops / (k_fwd * 1e-3) / 1e12 / fp64_peak, "flops": flops,
+    fp32_peak = _alu_peak(dev, fp32=True)
+    alu = {"bound": "fp32", "kernel": "raster_composite", "unit": "TFLOP/s",
+           "achieved": flops / (k_fwd * 1e-3) / 1e12, "peak": fp32_peak,
+           "frac": flops / (k_fwd * 1e-3) / 1e12 / fp32_peak, "flops": flops,
            "pair_tests": pairs, "included_segments": s_inc,
-           "formula": "24 P + 120 S_inc (SURVEY 8d)", "peak_source": "live DFMA probe (salf_fp64_peak)"}
+           "formula": "24 P + 120 S_inc (SURVEY 8d)", "peak_source": "live FFMA probe (salf_fp32_peak)",
+           "fp64_peak": _alu_peak(dev, fp32=False)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256; random target image)",
         "config": {"workload": WORKLOAD, "regime": args.regime, "resolution": [w, h],
                    "voxels": ds.n, "parallelism": f"sensor-sharded x{world}, grad all-reduce (NCCL)",

@@ -298,6 +298,9 @@ int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, c
 /* FP64 peak probe (benchmark utility): grid x 256 threads x 64*iters DFMA. */
 int salf_fp64_peak(double *scratch, int32_t grid, int32_t iters, void *stream);
 
+/* FP32 peak probe (benchmark utility): grid x 256 threads x 64*iters FFMA. */
+int salf_fp32_peak(float *scratch, int32_t grid, int32_t iters, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

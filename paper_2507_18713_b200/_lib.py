@@ -90,6 +90,7 @@ SIGNATURES = {
     "salf_loss_opacity_lidar": (C.c_int, [vp, vp, C.c_int32, C.c_int64, vp, vp, vp, vp, vp]),
     "salf_loss_smooth": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
     "salf_fp64_peak": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
+    "salf_fp32_peak": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
     "salf_octree_ancestor_keys": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, vp, vp, vp]),
     "salf_octree_fill": (C.c_int, [C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),
     "salf_shade_segments": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int32, C.c_int64, C.c_int32,

@@ -1,6 +1,6 @@
-// salf_bench.cu -- FP64 peak probe for the ALU roofline reported by bench.py
-// (the kernels here are FP64-pipe bound; MEASURED_PEAKS.json only holds HBM
-// and bf16 tensor peaks).  Independent DFMA chains, one launch per call.
+// salf_bench.cu -- FP64 / FP32 peak probes for the ALU rooflines reported by
+// bench.py (MEASURED_PEAKS.json only holds HBM and bf16 tensor peaks).
+// Independent FMA chains, one launch per call.
 #include "salf_common.cuh"
 #include "salf_internal.h"
 
@@ -19,6 +19,22 @@ __global__ void k_fp64_peak(double *out, int iters, double seed) {
   const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
   if (r == 12345.0) out[blockIdx.x] = r;  // keep the chains alive
 }
+__global__ void k_fp32_peak(float *out, int iters, float seed) {
+  float a[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = seed + threadIdx.x + k;
+  const float m = 0.9999f, c = 1e-4f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) a[k] = __fmaf_rn(a[k], m, c);
+  }
+  float t = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) t += a[k];
+  if (t == 12345.0f) out[blockIdx.x] = t;  // keep the chains alive
+}
 }  // namespace salf
 
 using namespace salf;
@@ -28,6 +44,15 @@ extern "C" int salf_fp64_peak(double *scratch, int32_t grid, int32_t iters, void
   SALF_TRY {
     k_fp64_peak<<<grid, 256, 0, (cudaStream_t)stream>>>(scratch, iters, 0.5);
     return check_cuda("salf_fp64_peak");
+  }
+  SALF_CATCH
+}
+
+// Launches grid x 256 threads, each 64 * iters FFMA (2 flops each).
+extern "C" int salf_fp32_peak(float *scratch, int32_t grid, int32_t iters, void *stream) {
+  SALF_TRY {
+    k_fp32_peak<<<grid, 256, 0, (cudaStream_t)stream>>>(scratch, iters, 0.5f);
+    return check_cuda("salf_fp32_peak");
   }
   SALF_CATCH
 }

@@ -260,6 +260,26 @@ def test_c2_frame_tiles_match_oracle(s1m):
         assert np.max(np.abs(col[sl] - ref["color"][sl])) < 1e-4
 
 
+@pytest.mark.parametrize("yaw", [0.0, 135.0])
+def test_c2_certified_forward_equals_fp64_decisions(s1m, yaw):
+    """The default (certified mixed-precision) forward against the fp64
+    reference-order forward on a whole 1080p frame of S1M: every pixel's stop
+    index and depth-NaN mask identical, values within fp32 rounding."""
+    from paper_2507_18713_b200 import configs, render_raster as RR
+    from paper_2507_18713_b200.device import DeviceScene
+    ds = DeviceScene.from_scene(s1m)
+    cam = configs.c2_camera(yaw)
+    fa, sa = RR.rasterize(ds, cam, return_state=True)
+    fe, se = RR.rasterize(ds, cam, return_state=True, exact_color=True)
+    assert torch.equal(sa.saved[:, 6], se.saved[:, 6])
+    assert torch.equal(torch.isnan(fa.depth), torch.isnan(fe.depth))
+    assert not torch.isnan(fa.opacity).any()
+    assert float((fa.color - fe.color).abs().max()) < 1e-5
+    assert float((fa.opacity - fe.opacity).abs().max()) < 1e-5
+    m = ~torch.isnan(fe.depth)
+    assert float(((fa.depth[m] - fe.depth[m]).abs() / fe.depth[m]).max()) < 1e-5
+
+
 def test_c3_lidar_hit_lists_full_size(s1m):
     """C3 (128 x 1800 on S1M): early-stopped hit lists of a ray sample are
     bit-identical to the oracle; every ray terminates; invariants hold."""
