@@ -295,6 +295,36 @@ int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, c
                      const int64_t *coarse, const int32_t *axis, const double *sign, double *grad,
                      double *loss_sums, void *stream);
 
+/* ---- densify / prune (reference densify.py:39-94, optim.py:35-40) ------- */
+
+/* Centre opacity and the prune / eligible flags of every voxel
+ * (densify.py:39-46, :62-70): flags bit 0 = prune (opacity < prune_opacity),
+ * bit 1 = eligible for splitting (kept and level < max_levels - 1).
+ * params: (n x 27) f64 parameter block; geo: (n x 4) f64 (edge at [3]);
+ * opacity (n f64) may be NULL. */
+int salf_densify_flags(int64_t n, const double *params, const double *geo, const uint8_t *level,
+                       int32_t density_mode, double prune_opacity, int32_t max_levels, uint8_t *flags,
+                       double *opacity, void *stream);
+
+/* grad_acc[i] += ||dL/dW_c[i]||_2 over the (n x 27) gradient block (trainer.py:193). */
+int salf_grad_norm_acc(int64_t n, const double *grad, double *acc, void *stream);
+
+/* The densified set (densify.py:72-91): rows [0, n_keep) gathered from
+ * keep_idx, then 8 children per split_idx entry (level + 1, 2 ijk + offset,
+ * offsets x fastest) inheriting the parameters; Adam moments m/v (optional,
+ * NULL to skip) carried for kept rows and zeroed for children (optim.py:35-40). */
+int salf_densify_apply(int64_t n_keep, const int64_t *keep_idx, int64_t n_split, const int64_t *split_idx,
+                       const uint8_t *level, const int32_t *ijk, const double *params, const double *m,
+                       const double *v, uint8_t *level_out, int32_t *ijk_out, double *params_out,
+                       double *m_out, double *v_out, void *stream);
+
+/* Device scene arrays from (level, ijk, params) (scene.py:186-194): geo
+ * (n x 4 f64: centre, edge), aux (n x 4 f64: exp(log_a), 1/exp(log_b),
+ * 2/edge, 0), prm (n x SALF_PRM_STRIDE f32). aabb_min: 3 host doubles. */
+int salf_voxel_geometry(int64_t n, const uint8_t *level, const int32_t *ijk, const double *aabb_min,
+                        double base_edge, const double *params, double *geo, double *aux, float *prm,
+                        void *stream);
+
 /* FP64 peak probe (benchmark utility): grid x 256 threads x 64*iters DFMA. */
 int salf_fp64_peak(double *scratch, int32_t grid, int32_t iters, void *stream);
 

@@ -923,3 +923,55 @@ def feature_backward(rec, vox: Voxels, feat, dF, d_depth):
     np.add.at(g["log_b"], vid, g_sigma * (-(ap / (2.0 * bp)) * s * e))
     np.add.at(fg, vid, w[:, None] * dF[ray])
     return g, fg
+
+
+# ---------------------------------------------------------------------------
+# densify / prune round (reference densify.py:39-94, optim.py:35-40)
+
+PRUNE_OPACITY = 0.005
+SPLIT_DENOMINATOR = 8 * 5
+CHILD_OFFSETS = np.array([[x, y, z] for z in (0, 1) for y in (0, 1) for x in (0, 1)], np.int64)
+
+
+def center_opacity(w_s, log_a, log_b, edges, mode="sdf"):
+    """densify.py:39-46: 1 - exp(-sigma(centre) edge), sigma from the bias w_s[3]."""
+    s = np.asarray(w_s)[:, 3]
+    sigma = sdf_to_density(s, np.exp(log_a), np.exp(log_b)) if mode == "sdf" else np.exp(s)
+    return -np.expm1(-sigma * edges)
+
+
+def densify_and_prune(level, ijk, params: dict, edges, grad_norms, budget, max_levels, mode="sdf",
+                      prune_opacity=PRUNE_OPACITY):
+    """densify.py:53-94.  Returns (new level, new ijk, new params, keep_idx, n_split).
+
+    Prune = centre opacity < prune_opacity; split count
+    max(0, (budget + n_prune - n) // 40); candidates ranked by gradient norm
+    descending, ties by index (lexsort), finest-level voxels skipped; kept
+    voxels first (index order), then 8 children per split voxel (split order
+    ascending, child offsets x fastest) inheriting every parameter."""
+    n = level.shape[0]
+    opa = center_opacity(params["w_s"], params["log_a"], params["log_b"], edges, mode)
+    prune = opa < prune_opacity
+    n_prune = int(prune.sum())
+    want = max(0, (budget + n_prune - n) // SPLIT_DENOMINATOR)
+    eligible = ~prune & (level.astype(np.int64) < max_levels - 1)
+    order = np.lexsort((np.arange(n), -np.asarray(grad_norms)))
+    split_idx = np.sort(order[eligible[order]][:want])
+    split = np.zeros(n, bool)
+    split[split_idx] = True
+    keep_idx = np.flatnonzero(~prune & ~split)
+    child_level = np.repeat(level[split_idx].astype(np.int64) + 1, 8).astype(np.uint8)
+    child_ijk = (ijk[split_idx].astype(np.int64)[:, None, :] * 2 + CHILD_OFFSETS[None]).reshape(-1, 3)
+    new_level = np.concatenate([level[keep_idx], child_level])
+    new_ijk = np.concatenate([ijk[keep_idx], child_ijk.astype(np.int32)])
+    new_params = {k: np.concatenate([v[keep_idx], np.repeat(v[split_idx], 8, axis=0)])
+                  for k, v in params.items()}
+    if new_level.shape[0] > budget:
+        raise RuntimeError(f"densification exceeded the budget: {new_level.shape[0]} > {budget}")
+    return new_level, new_ijk, new_params, keep_idx, int(split_idx.size)
+
+
+def adam_remap(moments: dict, keep_idx, n_split):
+    """optim.py:35-40: kept voxels' moments carried over, children zeroed."""
+    return {k: np.concatenate([v[keep_idx], np.zeros((8 * n_split,) + v.shape[1:], v.dtype)])
+            for k, v in moments.items()}

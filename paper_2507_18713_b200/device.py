@@ -51,6 +51,20 @@ class DeviceScene:
         self.flat = flat
 
     @classmethod
+    def from_arrays(cls, geo: torch.Tensor, aux: torch.Tensor, prm: torch.Tensor, n: int,
+                    density_mode: str) -> "DeviceScene":
+        """A static device scene from device arrays already in the HBM layout
+        (e.g. rebuilt on the device after densification)."""
+        self = cls.__new__(cls)
+        self.device = geo.device
+        self.n = int(n)
+        self.density_mode = density_mode
+        self.geo, self.aux, self.prm = geo, aux, prm
+        self.rot = None
+        self.flat = None
+        return self
+
+    @classmethod
     def from_scene(cls, scene: Scene, t_stamp: float = 0.0, device=None) -> "DeviceScene":
         return cls(flatten_scene(scene, t_stamp), device)
 

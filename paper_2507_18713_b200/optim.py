@@ -60,6 +60,8 @@ class TrainableScene:
         self.m = torch.zeros_like(self.params)
         self.v = torch.zeros_like(self.params)
         self.level = torch.as_tensor(scene.static.level.astype(np.int64), device=dev)
+        self.level8 = torch.as_tensor(scene.static.level.astype(np.uint8), device=dev)
+        self.ijk = torch.as_tensor(np.ascontiguousarray(scene.static.ijk.astype(np.int32)), device=dev)
         self.step = 0
 
     @property
@@ -84,6 +86,41 @@ class TrainableScene:
                                       cfg.eps, self.step, _lib.stream_ptr()), "adam_step")
         self.refresh()
         return lr
+
+    def densify(self, grad_acc: torch.Tensor, cfg=None):
+        """trainer.py:198-206 on the device: one densify/prune round
+        (densify.py:53-94) over the live parameters, Adam moments remapped
+        (optim.py:35-40), device scene arrays rebuilt from (level, ijk);
+        returns (keep_idx, n_split).  The caller rebuilds the octree
+        (`host_voxel_set()` + octree.build_octree_device) and resets grad_acc."""
+        from .densify import DensifyConfig, densify_device
+        lib = _lib.load()
+        cfg = cfg or DensifyConfig()
+        b = self.scene.bounds
+        r = densify_device(self.params, self.ds.geo, self.level8, self.ijk, grad_acc, cfg, b.max_levels,
+                           self.ds.density_mode, self.m, self.v)
+        n = int(r["level"].numel())
+        dev = self.params.device
+        self.params, self.m, self.v = r["params"].contiguous(), r["m"].contiguous(), r["v"].contiguous()
+        self.level8, self.ijk = r["level"].contiguous(), r["ijk"].contiguous()
+        self.level = self.level8.to(torch.int64)
+        geo = torch.empty((max(n, 1), 4), dtype=torch.float64, device=dev)
+        aux = torch.empty((max(n, 1), 4), dtype=torch.float64, device=dev)
+        prm = torch.zeros((max(n, 1), _lib.PRM_STRIDE), dtype=torch.float32, device=dev)
+        lo = np.ascontiguousarray(b.aabb_min, np.float64)
+        _lib.check(lib.salf_voxel_geometry(n, self.level8.data_ptr(), self.ijk.data_ptr(), lo.ctypes.data,
+                                           float(b.base_edge), self.params.data_ptr(), geo.data_ptr(),
+                                           aux.data_ptr(), prm.data_ptr(), _lib.stream_ptr()), "densify")
+        self.ds = DeviceScene.from_arrays(geo, aux, prm, n, self.ds.density_mode)
+        return r["keep_idx"], r["n_split"]
+
+    def host_voxel_set(self):
+        """The current static set on the host (for the octree rebuild / export)."""
+        from .scene import SparseVoxelSet
+        p = self.to_numpy()
+        v = SparseVoxelSet(self.scene.bounds, budget=self.scene.static.budget)
+        return v.set_arrays(self.level8.cpu().numpy(), self.ijk.cpu().numpy(), p["w_s"], p["w_c"], p["w_sh"],
+                            p["log_a"], p["log_b"])
 
     def to_numpy(self) -> dict:
         b = self.params.cpu().numpy()
