@@ -52,8 +52,10 @@ def main(rep, out_md, traffic_json=None):
         avg = {k: sum(v[k] for v in lst if k in v) / max(1, sum(1 for v in lst if k in v)) for k in want}
         dur_ms = avg["gpu__time_duration.sum"] / 1e6
         rd, wr = avg["dram__bytes_read.sum"], avg["dram__bytes_write.sum"]
-        key = {"k_composite": "raster_composite", "k_backward": "raster_backward",
-               "k_ray_forward": "ray_forward"}.get(name.split("<")[0].replace("salf::", ""), name)
+        key = {"k_composite": "raster_composite", "k_composite_fast": "raster_composite",
+               "k_composite_redo": "raster_composite_redo", "k_backward": "raster_backward",
+               "k_backward_fast": "raster_backward", "k_ray_forward": "ray_forward"}.get(
+            name.split("<")[0].replace("salf::", ""), name)
         traffic[key] = rd + wr
         metrics[key] = {"duration_ms": dur_ms, "dram_bytes": rd + wr,
                         "l2_hit_pct": avg["lts__t_sector_hit_rate.pct"],
