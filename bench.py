@@ -222,7 +222,7 @@ def run_ours(args, world, rank, local):
     import torch.distributed as dist
     from paper_2507_18713_b200 import _lib, configs
     from paper_2507_18713_b200 import render_raster as RR
-    from paper_2507_18713_b200.backward import loss_color_seed
+    from paper_2507_18713_b200.backward import l1_color_seed
     from paper_2507_18713_b200.device import DeviceScene
     from paper_2507_18713_b200.scenes import get_scene
 
@@ -235,7 +235,6 @@ def run_ours(args, world, rank, local):
     g = torch.Generator().manual_seed(rank)
     gt_host = (0.3 + 0.4 * torch.rand((h, w, 3), generator=g)).pin_memory()
     gt_dev = gt_host.to(dev)
-    mask = torch.ones(h * w, dtype=torch.bool, device=dev)
     dd = torch.zeros((h, w), dtype=torch.float64, device=dev)
     grad = torch.zeros((ds.n, _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
@@ -244,14 +243,13 @@ def run_ours(args, world, rank, local):
 
     def step(gt, events=None, e2e=False):
         fb, st = RR.rasterize(ds, cam, return_state=True, events=events)
-        diff = fb.color.double() - gt.double()
-        dc = loss_color_seed(fb.color.reshape(-1, 3), gt.reshape(-1, 3), mask).reshape(h, w, 3)
+        dc, lsum = l1_color_seed(fb.color, gt)  # losses.py:22-31, one fused kernel
         grad.zero_()
         RR.rasterize_backward(st, dc, dd, grad, as_dict=False, events=events)
         if world > 1:
             dist.all_reduce(grad)
         if e2e:
-            loss_host.copy_(diff.abs().mean().reshape(1), non_blocking=True)
+            loss_host.copy_((lsum / dc.numel()).reshape(1), non_blocking=True)
             out_host.copy_(fb.color, non_blocking=True)
         return st
 
@@ -330,8 +328,8 @@ def run_ours(args, world, rank, local):
         cur = gt_bufs[k % 2]
         cs.wait_event(up[k % 2])
         fb, st = RR.rasterize(ds, cam, return_state=True)
-        dc = loss_color_seed(fb.color.reshape(-1, 3), cur.reshape(-1, 3), mask).reshape(h, w, 3)
-        loss_dev.copy_((fb.color.double() - cur.double()).abs().mean().reshape(1))
+        dc, lsum = l1_color_seed(fb.color, cur)
+        loss_dev.copy_((lsum / dc.numel()).reshape(1))
         used[k % 2].record(cs)
         xs.wait_event(used[k % 2])
         with torch.cuda.stream(xs):

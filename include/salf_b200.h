@@ -295,6 +295,13 @@ int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, c
                      const int64_t *coarse, const int32_t *axis, const double *sign, double *grad,
                      double *loss_sums, void *stream);
 
+/* L1 loss seed and value (losses.py:22-31): d_out[i] = sign(pred[i] - gt[i]) * scale
+ * where selected (mask[i / group] != 0; mask NULL selects all), else 0;
+ * *loss_sum += sum of |pred - gt| over the selection (f64 accumulation).
+ * pred: n f32; gt: n f32 or f64 (gt_f64). */
+int salf_l1_seed(int64_t n, const float *pred, const void *gt, int32_t gt_f64, const uint8_t *mask,
+                 int32_t group, double scale, double *d_out, double *loss_sum, void *stream);
+
 /* ---- densify / prune (reference densify.py:39-94, optim.py:35-40) ------- */
 
 /* Centre opacity and the prune / eligible flags of every voxel

@@ -83,6 +83,33 @@ def loss_color_seed(out_color: torch.Tensor, gt: torch.Tensor, mask: torch.Tenso
     return d
 
 
+def l1_color_seed(out_color: torch.Tensor, gt: torch.Tensor, mask: torch.Tensor | None = None,
+                  count: int | None = None):
+    """Fused losses.py:22-31 (one kernel): returns (dL/dC (.., 3) f64, sum |C - gt|
+    over the selection as a 0-d f64 device tensor).  mask selects pixels
+    (None = all); the normaliser is count, or 3 x #selected."""
+    lib = _lib.load()
+    pred = out_color.reshape(-1).contiguous()
+    if pred.dtype != torch.float32:
+        pred = pred.float()
+    g = gt.reshape(-1).contiguous()
+    if g.dtype not in (torch.float32, torch.float64):
+        g = g.double()
+    n = pred.numel()
+    m = None
+    if mask is not None:
+        m = mask.reshape(-1).to(torch.uint8).contiguous()
+        if count is None:
+            count = 3 * int(m.sum().item())
+    elif count is None:
+        count = n
+    d = torch.empty(n, dtype=torch.float64, device=pred.device)
+    loss = torch.zeros((), dtype=torch.float64, device=pred.device)
+    _lib.check(lib.salf_l1_seed(n, pred.data_ptr(), g.data_ptr(), int(g.dtype == torch.float64), _lib.ptr(m), 3,
+                                1.0 / max(count, 1), d.data_ptr(), loss.data_ptr(), _lib.stream_ptr()), "l1_seed")
+    return d.reshape(out_color.shape), loss
+
+
 def loss_depth_seed(depth: torch.Tensor, gt: torch.Tensor, mask: torch.Tensor,
                     count: int | None = None) -> torch.Tensor:
     """losses.py:34-46: dL/dD = sign(D - gt) / #valid (count overrides #valid, e.g. a

@@ -3,10 +3,12 @@
 // Pipeline per frame (all on one stream):
 //   k_project      fp64 corner projection, cull, reference + tightened tile spans,
 //                  orderable depth keys                         (render_raster.py:97-176)
-//   depth rank     stable radix sort of (z_center, index) -> global rank, so
-//                  ties break by voxel index exactly like lexsort    (:177)
-//   k_emit         one 64-bit key (tile << 32 | rank) per (voxel, tile) instance
-//   radix sort     instances by key -> per-tile lists in (z, index) order
+//   depth rank     visible voxels only (non-empty span): stable radix sort of
+//                  (z_center key, index) -> ties break by voxel index exactly
+//                  like lexsort                                      (:177)
+//   k_emit         instances written in depth-rank order, key = tile id
+//   radix sort     stable sort by tile id (ceil(log2 T) bits, 2 passes at
+//                  C2) -> per-tile lists in (z, index) order
 //   k_offsets      CSR offsets per tile                              (:180-181)
 //   k_composite    one CTA per tile, one thread per pixel: staged entries in
 //                  shared memory, fp64 slab test + exact-order fp64 opacity chain,
@@ -154,54 +156,61 @@ __global__ void k_project(int64_t n, const double4 *__restrict__ geo, const doub
 // ---------------------------------------------------------------------------
 // binning
 
-__global__ void k_span_count(int64_t n, const int4 *__restrict__ span, int64_t *__restrict__ cnt) {
+__global__ void k_span_count(int64_t n, const int4 *__restrict__ span, int64_t *__restrict__ cnt,
+                             uint8_t *__restrict__ vis) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int4 s = span[i];
-  cnt[i] = (s.x <= s.z && s.y <= s.w) ? (int64_t)(s.z - s.x + 1) * (s.w - s.y + 1) : 0;
+  const int64_t c = (s.x <= s.z && s.y <= s.w) ? (int64_t)(s.z - s.x + 1) * (s.w - s.y + 1) : 0;
+  cnt[i] = c;
+  vis[i] = c > 0;
 }
 
-__global__ void k_iota(int64_t n, int32_t *__restrict__ v) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (int32_t)i;
-}
-
-__global__ void k_rank(int64_t n, const int32_t *__restrict__ sorted_idx, uint32_t *__restrict__ rank) {
+// depth keys and instance counts of the visible voxels (vis_idx ascending)
+__global__ void k_gather_vis(int64_t n_vis, const int32_t *__restrict__ vis_idx, const uint64_t *__restrict__ zkey,
+                             uint64_t *__restrict__ zk_vis) {
   int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n) rank[sorted_idx[r]] = (uint32_t)r;
+  if (r < n_vis) zk_vis[r] = zkey[vis_idx[r]];
 }
 
-// One warp per voxel: lanes stride over the voxel's tiles (spans can be the
-// full image for straddling voxels in reference mode).
-__global__ void k_emit(int64_t n, const int4 *__restrict__ span, const int64_t *__restrict__ base,
-                       const uint32_t *__restrict__ rank, int tiles_x, uint64_t *__restrict__ keys,
+__global__ void k_count_ranked(int64_t n_vis, const int32_t *__restrict__ sorted_vis, const int64_t *__restrict__ cnt,
+                               int64_t *__restrict__ cnt_r) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n_vis) cnt_r[r] = cnt[sorted_vis[r]];
+}
+
+// One warp per visible voxel, in global depth-rank order: its instances are
+// written at base_r[rank] with the tile id as the (only) sort key, so a
+// stable sort by tile leaves every tile's list in (z, index) order.  Lanes
+// stride over the voxel's tiles (spans can be the full image for straddling
+// voxels in reference mode).
+__global__ void k_emit(int64_t n_vis, const int32_t *__restrict__ sorted_vis, const int4 *__restrict__ span,
+                       const int64_t *__restrict__ base_r, int tiles_x, uint32_t *__restrict__ keys,
                        int32_t *__restrict__ vals) {
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= n) return;
-  const int4 s = span[warp];
-  if (s.x > s.z || s.y > s.w) return;
+  if (r >= n_vis) return;
+  const int32_t v = sorted_vis[r];
+  const int4 s = span[v];
   const int nx = s.z - s.x + 1;
   const int64_t cnt = (int64_t)nx * (s.w - s.y + 1);
-  const int64_t b = base[warp];
-  const uint64_t r = rank[warp];
+  const int64_t b = base_r[r];
   for (int64_t k = lane; k < cnt; k += 32) {
     const int ty = s.y + (int)(k / nx), tx = s.x + (int)(k % nx);
-    keys[b + k] = ((uint64_t)(ty * tiles_x + tx) << 32) | r;
-    vals[b + k] = (int32_t)warp;
+    keys[b + k] = (uint32_t)(ty * tiles_x + tx);
+    vals[b + k] = v;
   }
 }
 
-__global__ void k_offsets(int n_tiles, int64_t n_inst, const uint64_t *__restrict__ keys,
+__global__ void k_offsets(int n_tiles, int64_t n_inst, const uint32_t *__restrict__ keys,
                           int64_t *__restrict__ offsets) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > n_tiles) return;
   // lower_bound of tile t in the sorted keys
   int64_t lo = 0, hi = n_inst;
-  const uint64_t target = (uint64_t)t << 32;
   while (lo < hi) {
     int64_t mid = (lo + hi) >> 1;
-    if (keys[mid] < target) lo = mid + 1; else hi = mid;
+    if (keys[mid] < (uint32_t)t) lo = mid + 1; else hi = mid;
   }
   offsets[t] = lo;
 }
@@ -1215,12 +1224,12 @@ extern "C" int salf_project_voxels(const salf_scene_t *scene, const salf_camera_
 
 // workspace layout for salf_raster_bin
 struct BinWs {
-  int64_t *cnt, *base;
-  uint64_t *zk_sorted;
-  int32_t *idx_in, *idx_out;
-  uint32_t *rank;
-  uint64_t *keys_a, *keys_b;
-  int32_t *vals_b;
+  int64_t *cnt, *cnt_r, *base_r, *nums;  // nums[0] = visible voxels, nums[1] = instances
+  uint8_t *vis;
+  int32_t *vis_idx, *vis_sorted;
+  uint64_t *zk_vis, *zk_sorted;
+  uint32_t *keys_a, *keys_b;
+  int32_t *vals_a;
   void *cub_tmp;
   size_t cub_bytes;
 };
@@ -1228,13 +1237,17 @@ struct BinWs {
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static size_t cub_bytes_needed(int64_t n_voxels, int64_t capacity) {
-  size_t a = 0, b = 0, c = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, a, (int64_t *)nullptr, (int64_t *)nullptr, (int)std::max<int64_t>(n_voxels, 1));
+  const int n = (int)std::max<int64_t>(n_voxels, 1);
+  size_t a = 0, b = 0, c = 0, d = 0, e = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, a, (int64_t *)nullptr, (int64_t *)nullptr, n);
   cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int32_t *)nullptr,
-                                  (int32_t *)nullptr, (int)std::max<int64_t>(n_voxels, 1));
-  cub::DeviceRadixSort::SortPairs(nullptr, c, (uint64_t *)nullptr, (uint64_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, n);
+  cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
                                   (int32_t *)nullptr, (int64_t)std::max<int64_t>(capacity, 1));
-  return std::max(a, std::max(b, c));
+  cub::DeviceSelect::Flagged(nullptr, d, cub::CountingInputIterator<int32_t>(0), (const uint8_t *)nullptr,
+                             (int32_t *)nullptr, (int64_t *)nullptr, n);
+  cub::DeviceReduce::Sum(nullptr, e, (const int64_t *)nullptr, (int64_t *)nullptr, n);
+  return std::max(std::max(a, b), std::max(c, std::max(d, e)));
 }
 
 static BinWs carve(void *ws, int64_t n, int64_t cap, size_t *total) {
@@ -1243,14 +1256,17 @@ static BinWs carve(void *ws, int64_t n, int64_t cap, size_t *total) {
   char *p = (char *)ws;
   auto take = [&](size_t bytes) { char *q = p ? p + off : nullptr; off += align_up(bytes); return q; };
   w.cnt = (int64_t *)take(sizeof(int64_t) * (n + 1));
-  w.base = (int64_t *)take(sizeof(int64_t) * (n + 1));
+  w.cnt_r = (int64_t *)take(sizeof(int64_t) * (n + 1));
+  w.base_r = (int64_t *)take(sizeof(int64_t) * (n + 1));
+  w.nums = (int64_t *)take(sizeof(int64_t) * 2);
+  w.vis = (uint8_t *)take(n);
+  w.vis_idx = (int32_t *)take(sizeof(int32_t) * n);
+  w.vis_sorted = (int32_t *)take(sizeof(int32_t) * n);
+  w.zk_vis = (uint64_t *)take(sizeof(uint64_t) * n);
   w.zk_sorted = (uint64_t *)take(sizeof(uint64_t) * n);
-  w.idx_in = (int32_t *)take(sizeof(int32_t) * n);
-  w.idx_out = (int32_t *)take(sizeof(int32_t) * n);
-  w.rank = (uint32_t *)take(sizeof(uint32_t) * n);
-  w.keys_a = (uint64_t *)take(sizeof(uint64_t) * cap);
-  w.keys_b = (uint64_t *)take(sizeof(uint64_t) * cap);
-  w.vals_b = (int32_t *)take(sizeof(int32_t) * cap);
+  w.keys_a = (uint32_t *)take(sizeof(uint32_t) * cap);
+  w.keys_b = (uint32_t *)take(sizeof(uint32_t) * cap);
+  w.vals_a = (int32_t *)take(sizeof(int32_t) * cap);
   w.cub_bytes = cub_bytes_needed(n, cap);
   w.cub_tmp = take(w.cub_bytes);
   *total = off;
@@ -1286,41 +1302,42 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
                                                  workspace_bytes, need);
     const int bs = 256;
     const unsigned gb = (unsigned)((n + bs - 1) / bs);
-    k_span_count<<<gb, bs, 0, st>>>(n, reinterpret_cast<const int4 *>(span), w.cnt);
+    // instance counts, visible voxels (non-empty span, ascending index) and the total
+    k_span_count<<<gb, bs, 0, st>>>(n, reinterpret_cast<const int4 *>(span), w.cnt, w.vis);
     size_t tb = w.cub_bytes;
-    cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt, w.base, (int)n, st);
-    // base[n] = total instances (cnt[n] is garbage-free: set to 0 first)
-    int64_t total = 0;
-    {
-      // recompute: total = base[n-1] + cnt[n-1]
-      int64_t hb[2];
-      cudaMemcpyAsync(&hb[0], w.base + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(&hb[1], w.cnt + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      total = hb[0] + hb[1];
-    }
+    cub::DeviceSelect::Flagged(w.cub_tmp, tb, cub::CountingInputIterator<int32_t>(0), w.vis, w.vis_idx, w.nums,
+                               (int)n, st);
+    tb = w.cub_bytes;
+    cub::DeviceReduce::Sum(w.cub_tmp, tb, w.cnt, w.nums + 1, (int)n, st);
+    int64_t hn[2];
+    cudaMemcpyAsync(hn, w.nums, sizeof(hn), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const int64_t n_vis = hn[0], total = hn[1];
     *n_instances = total;
     if (total > capacity) return set_error(SALF_EWORKSPACE, "instance capacity %lld < %lld", (long long)capacity,
                                            (long long)total);
-    // global depth rank: stable sort of (zkey, index) -> ties by index (lexsort)
-    k_iota<<<gb, bs, 0, st>>>(n, w.idx_in);
-    tb = w.cub_bytes;
-    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, zkey, w.zk_sorted, w.idx_in, w.idx_out, (int)n, 0, 64, st);
-    k_rank<<<gb, bs, 0, st>>>(n, w.idx_out, w.rank);
-    if (total > 0) {
-      const int64_t warps = n;
-      k_emit<<<(unsigned)((warps * 32 + bs - 1) / bs), bs, 0, st>>>(
-          n, reinterpret_cast<const int4 *>(span), w.base, w.rank, c.tiles_x, w.keys_a, entries);
-      const int end_bit = 32 + bits_for((uint64_t)n_tiles);
-      const int begin_bit = 0;
-      tb = w.cub_bytes;
-      cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.keys_a, w.keys_b, entries, w.vals_b, (int64_t)total,
-                                      begin_bit, end_bit, st);
-      cudaMemcpyAsync(entries, w.vals_b, sizeof(int32_t) * total, cudaMemcpyDeviceToDevice, st);
-      k_offsets<<<(n_tiles + 1 + bs - 1) / bs, bs, 0, st>>>(n_tiles, total, w.keys_b, offsets);
-    } else {
+    if (total == 0) {
       cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (n_tiles + 1), st);
+      return check_cuda("salf_raster_bin");
     }
+    // global depth rank of the visible voxels: stable sort of (zkey, index)
+    const unsigned gv = (unsigned)((n_vis + bs - 1) / bs);
+    k_gather_vis<<<gv, bs, 0, st>>>(n_vis, w.vis_idx, zkey, w.zk_vis);
+    tb = w.cub_bytes;
+    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.zk_vis, w.zk_sorted, w.vis_idx, w.vis_sorted, (int)n_vis, 0, 64,
+                                    st);
+    // instance slots in rank order
+    k_count_ranked<<<gv, bs, 0, st>>>(n_vis, w.vis_sorted, w.cnt, w.cnt_r);
+    tb = w.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt_r, w.base_r, (int)n_vis, st);
+    k_emit<<<(unsigned)((n_vis * 32 + bs - 1) / bs), bs, 0, st>>>(n_vis, w.vis_sorted,
+                                                                 reinterpret_cast<const int4 *>(span), w.base_r,
+                                                                 c.tiles_x, w.keys_a, w.vals_a);
+    // stable sort by tile: each tile's list stays in depth-rank order
+    tb = w.cub_bytes;
+    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.keys_a, w.keys_b, w.vals_a, entries, (int64_t)total, 0,
+                                    bits_for((uint64_t)n_tiles), st);
+    k_offsets<<<(n_tiles + 1 + bs - 1) / bs, bs, 0, st>>>(n_tiles, total, w.keys_b, offsets);
     return check_cuda("salf_raster_bin");
   }
   SALF_CATCH

@@ -215,6 +215,26 @@ __global__ void k_smooth(int64_t n_pairs, const int64_t *__restrict__ fine, cons
   atomicAdd(loss_sums + 1, l_c);
 }
 
+// L1 loss seed + value (losses.py:22-31): d[i] = sign(pred - gt) * scale on
+// selected elements (mask[i / group] != 0, or all when mask is NULL), 0
+// elsewhere; loss_sum += sum |pred - gt| over the selection.
+template <typename G>
+__global__ void k_l1_seed(int64_t n, const float *__restrict__ pred, const G *__restrict__ gt,
+                          const uint8_t *__restrict__ mask, int group, double scale, double *__restrict__ d,
+                          double *__restrict__ loss_sum) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double l = 0.0;
+  if (i < n) {
+    const bool sel = mask == nullptr || mask[i / group] != 0;
+    const double diff = (double)pred[i] - (double)gt[i];
+    d[i] = sel ? __dmul_rn(npsign(diff), scale) : 0.0;
+    l = sel ? fabs(diff) : 0.0;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+  if ((threadIdx.x & 31) == 0 && l != 0.0 && loss_sum) atomicAdd(loss_sum, l);
+}
+
 }  // namespace salf
 
 using namespace salf;
@@ -295,6 +315,23 @@ extern "C" int salf_loss_empty_grad(const double *params, const double *geo, int
     k_empty_grad<<<(unsigned)((k + 255) / 256), 256, 0, (cudaStream_t)stream>>>(k, sel, params, geo, density_mode,
                                                                                 grad);
     return check_cuda("salf_loss_empty_grad");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_l1_seed(int64_t n, const float *pred, const void *gt, int32_t gt_f64, const uint8_t *mask,
+                            int32_t group, double scale, double *d_out, double *loss_sum, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    if (group < 1) return set_error(SALF_EINVAL, "group must be >= 1");
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (gt_f64)
+      k_l1_seed<double><<<g, 256, 0, (cudaStream_t)stream>>>(n, pred, (const double *)gt, mask, group, scale, d_out,
+                                                             loss_sum);
+    else
+      k_l1_seed<float><<<g, 256, 0, (cudaStream_t)stream>>>(n, pred, (const float *)gt, mask, group, scale, d_out,
+                                                            loss_sum);
+    return check_cuda("salf_l1_seed");
   }
   SALF_CATCH
 }

@@ -155,3 +155,21 @@ def test_smoothness_regulariser_matches_reference(golden, case):
     gd = grads_to_dict(g)
     for k in ("w_s", "w_c", "w_sh"):
         np.testing.assert_allclose(gd[k], golden[pre + k], rtol=1e-9, atol=1e-13)
+
+
+@pytest.mark.parametrize("gt_dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("masked", [False, True])
+def test_fused_l1_color_seed(gt_dtype, masked):
+    """backward.l1_color_seed (one kernel) == losses.py:22-31 restated with torch ops."""
+    from paper_2507_18713_b200.backward import l1_color_seed, loss_color_seed
+    g = torch.Generator(device="cuda").manual_seed(3)
+    c = torch.rand((37, 29, 3), device="cuda", generator=g)
+    gt = torch.rand((37, 29, 3), device="cuda", generator=g).to(gt_dtype)
+    gt[0, 0] = c[0, 0].to(gt_dtype)  # sign(0) = 0
+    mask = (torch.rand(37 * 29, device="cuda", generator=g) > 0.3) if masked else None
+    d, lsum = l1_color_seed(c, gt, mask)
+    mref = mask if masked else torch.ones(37 * 29, dtype=torch.bool, device="cuda")
+    want = loss_color_seed(c.reshape(-1, 3), gt.reshape(-1, 3)[mref], mref).reshape(37, 29, 3)
+    assert torch.equal(d, want)
+    diff = (c.double() - gt.double()).reshape(-1, 3)[mref]
+    torch.testing.assert_close(lsum, diff.abs().sum(), rtol=1e-12, atol=0)
