@@ -295,6 +295,32 @@ int salf_loss_smooth(const double *params, const double *geo, int64_t n_pairs, c
                      const int64_t *coarse, const int32_t *axis, const double *sign, double *grad,
                      double *loss_sums, void *stream);
 
+/* ---- secondary-ray effects (reference render_ray.py:310-489) ---------- */
+
+enum { SALF_SPHERE_MIRROR = 0, SALF_SPHERE_GLASS = 1, SALF_SPHERE_OPAQUE = 2 };
+
+/* InjectedSphere (render_ray.py:313-330). */
+typedef struct {
+  double center[3];
+  double radius;
+  double ior;
+  double albedo[3];
+  int32_t material, pad;
+} salf_sphere_t;
+
+/* One wave of trace_effects (render_ray.py:360-489) after the wave's rays
+ * were rendered through the volume (vol_rgb n x 3 f32, vol_saved n x 8 f64
+ * from salf_ray_forward): sphere hits, volume-vs-sphere decision, sun
+ * shadows, accumulation into out (n_pixels x 3 f64, atomic adds at pix),
+ * and the next wave in slots 2i / 2i+1 (next_flag marks the used slots;
+ * capacity 2n).  spheres: device array; sun_dir: 3 host doubles (unit). */
+int salf_effects_wave(int64_t n, const double *origins, const double *dirs, const double *t_stamps,
+                      const double *weight, const int32_t *budget, const int64_t *pix,
+                      const float *vol_rgb, const double *vol_saved, int32_t n_spheres,
+                      const salf_sphere_t *spheres, const double *sun_dir, double *out,
+                      double *next_origins, double *next_dirs, double *next_t_stamps, double *next_weight,
+                      int32_t *next_budget, int64_t *next_pix, uint8_t *next_flag, void *stream);
+
 /* L1 loss seed and value (losses.py:22-31): d_out[i] = sign(pred[i] - gt[i]) * scale
  * where selected (mask[i / group] != 0; mask NULL selects all), else 0;
  * *loss_sum += sum of |pred - gt| over the selection (f64 accumulation).

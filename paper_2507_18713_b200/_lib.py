@@ -56,6 +56,11 @@ class OctreeT(C.Structure):
                 ("root_edge", C.c_double), ("max_depth", C.c_int32), ("pad", C.c_int32)]
 
 
+class SphereT(C.Structure):
+    _fields_ = [("center", c_double3), ("radius", C.c_double), ("ior", C.c_double), ("albedo", c_double3),
+                ("material", C.c_int32), ("pad", C.c_int32)]
+
+
 class RasterOptsT(C.Structure):
     _fields_ = [("background", c_double3), ("near", C.c_double), ("stop_threshold", C.c_double),
                 ("tile", C.c_int32), ("exact_color", C.c_int32)]
@@ -91,6 +96,8 @@ SIGNATURES = {
     "salf_loss_smooth": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
     "salf_fp64_peak": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
     "salf_fp32_peak": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
+    "salf_effects_wave": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int32, vp, vp, vp, vp, vp,
+                                    vp, vp, vp, vp, vp, vp]),
     "salf_l1_seed": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int32, C.c_double, vp, vp, vp]),
     "salf_densify_flags": (C.c_int, [C.c_int64, vp, vp, vp, C.c_int32, C.c_double, C.c_int32, vp, vp, vp]),
     "salf_grad_norm_acc": (C.c_int, [C.c_int64, vp, vp, vp]),

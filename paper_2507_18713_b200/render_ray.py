@@ -380,3 +380,93 @@ def segments(scene, octrees, origins, dirs, stop_threshold: float = STOP_THRESHO
     """The ray path's hit list with the reference's early stop (parity export)."""
     ds = _static_device_scene(scene)
     return march_segments(_octree_of(octrees), origins, dirs, np.inf, ds, stop_threshold, True)
+
+
+# -- secondary-ray effects (injected analytic spheres) -----------------------
+
+_MATERIALS = {"mirror": 0, "glass": 1, "opaque": 2}
+
+
+@dataclass
+class InjectedSphere:
+    """render_ray.py:313-330 (same validation and messages)."""
+
+    center: np.ndarray
+    radius: float
+    material: str  # mirror | glass | opaque
+    ior: float = 1.5
+    albedo: np.ndarray = None
+
+    def __post_init__(self):
+        self.center = np.asarray(self.center, dtype=np.float64)
+        self.albedo = np.full(3, 0.5) if self.albedo is None else np.asarray(self.albedo, dtype=np.float64)
+        if self.radius <= 0:
+            raise ValueError("radius must be positive")
+        if self.material not in _MATERIALS:
+            raise ValueError(f"unknown material {self.material!r}")
+        if self.material == "glass" and self.ior < 1.0:
+            raise ValueError("index of refraction must be >= 1")
+
+
+def trace_effects(scene, octrees, origins, dirs, t_stamps, spheres: list, sun_dir, max_bounces: int = 2, *,
+                  background=(0.0, 0.0, 0.0)) -> torch.Tensor:
+    """Ray-traced composition of the volume with injected analytic spheres
+    (render_ray.py:360-489): the nearest sphere hit wins against the
+    volumetric expected depth; mirrors reflect, glass splits into
+    Schlick-weighted reflected and Snell-refracted rays, opaque spheres
+    return their albedo; recursion stops at max_bounces, after which rays
+    fall back to plain volume rendering; volume surface points a sphere
+    occludes from the sun are darkened by SHADOW_FACTOR.
+
+    Wavefront on the device: each wave is one fused volume launch
+    (integrate_rays) plus one `salf_effects_wave` launch; the next wave is a
+    stable compaction of the at-most-two children per ray.  Returns the
+    (N, 3) f64 colour (CUDA tensor)."""
+    if max_bounces < 1:
+        raise ValueError("max_bounces must be at least 1")
+    lib = _lib.load()
+    ds = _static_device_scene(scene)
+    dev = ds.device
+    o = _lib.as_f64(origins, dev).reshape(-1, 3)
+    d = _lib.as_f64(dirs, dev).reshape(-1, 3)
+    n = o.shape[0]
+    if isinstance(t_stamps, torch.Tensor):
+        ts = t_stamps.to(device=dev, dtype=torch.float64).reshape(-1).expand(n).contiguous()
+    else:
+        ts = _lib.as_f64(np.broadcast_to(np.asarray(0.0 if t_stamps is None else t_stamps, np.float64), (n,)), dev)
+    sun = np.asarray(sun_dir, dtype=np.float64).reshape(3)
+    sun = np.ascontiguousarray(sun / np.linalg.norm(sun))
+    sph = (_lib.SphereT * max(len(spheres), 1))()
+    for i, sp in enumerate(spheres):
+        sph[i].center[:] = [float(v) for v in sp.center]
+        sph[i].radius, sph[i].ior = float(sp.radius), float(sp.ior)
+        sph[i].albedo[:] = [float(v) for v in sp.albedo]
+        sph[i].material = _MATERIALS[sp.material]
+    sph_dev = torch.frombuffer(bytearray(bytes(sph)), dtype=torch.uint8).to(dev)
+    out = torch.zeros((n, 3), dtype=torch.float64, device=dev)
+    pix = torch.arange(n, dtype=torch.int64, device=dev)
+    w = torch.ones(n, dtype=torch.float64, device=dev)
+    budget = torch.full((n,), int(max_bounces), dtype=torch.int32, device=dev)
+    live = isinstance(scene, Scene) and any(a.voxels.n for a in scene.actors)
+    while n:
+        # timestamps only matter for actor poses (host-side in integrate_rays)
+        rec = integrate_rays(scene, octrees, o, d, ts.cpu().numpy() if live else None, background=background)
+        nxt = dict(o=torch.empty((2 * n, 3), dtype=torch.float64, device=dev),
+                   d=torch.empty((2 * n, 3), dtype=torch.float64, device=dev),
+                   ts=torch.empty(2 * n, dtype=torch.float64, device=dev),
+                   w=torch.empty(2 * n, dtype=torch.float64, device=dev),
+                   b=torch.empty(2 * n, dtype=torch.int32, device=dev),
+                   pix=torch.empty(2 * n, dtype=torch.int64, device=dev),
+                   flag=torch.empty(2 * n, dtype=torch.uint8, device=dev))
+        _lib.check(lib.salf_effects_wave(n, o.data_ptr(), d.data_ptr(), ts.data_ptr(), w.data_ptr(),
+                                         budget.data_ptr(), pix.data_ptr(), rec.out_color.data_ptr(),
+                                         rec.saved.data_ptr(), len(spheres), sph_dev.data_ptr(),
+                                         sun.ctypes.data, out.data_ptr(), nxt["o"].data_ptr(),
+                                         nxt["d"].data_ptr(), nxt["ts"].data_ptr(), nxt["w"].data_ptr(),
+                                         nxt["b"].data_ptr(), nxt["pix"].data_ptr(), nxt["flag"].data_ptr(),
+                                         _lib.stream_ptr()), "trace_effects")
+        keep = torch.nonzero(nxt["flag"], as_tuple=True)[0]
+        n = int(keep.numel())
+        o, d, ts, w = nxt["o"][keep], nxt["d"][keep], nxt["ts"][keep], nxt["w"][keep]
+        budget, pix = nxt["b"][keep], nxt["pix"][keep]
+    return out
