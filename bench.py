@@ -519,6 +519,47 @@ def extras(ds, args):
     out["c5_train_step"] = {"ms": ms5, "steps_per_s": 1e3 / ms5, "sensors": "8 x 1920x1080 pinhole + 2 x 128x1800 LiDAR",
                             "includes": "forward, L1 seeds, raster + ray backward, device Adam, scene refresh"}
     del ts, gbuf, targets
+    # §8f rows beyond the hot path: densify round, salf.v1 device load, secondary effects
+    import time
+    from paper_2507_18713_b200.densify import DensifyConfig
+    from paper_2507_18713_b200.device import load_device_scene
+    from paper_2507_18713_b200.octree import build_octree_from_device
+    from paper_2507_18713_b200.scenes import DATA
+    ts = TrainableScene(scene)
+    gacc = torch.rand(ts.n, dtype=torch.float64, device=ts.ds.device, generator=torch.Generator(
+        device=ts.ds.device).manual_seed(1))
+
+    def dens():
+        t2 = TrainableScene.__new__(TrainableScene)
+        t2.__dict__.update(ts.__dict__)
+        t2.densify(gacc, DensifyConfig(budget=ts.n + 40 * 20000))
+        build_octree_from_device(t2.level8, t2.ijk, scene.bounds)
+
+    out["densify_round_S1M"] = {"ms": timeit(dens, n=3), "splits": 20000,
+                                "includes": "flags, ranking, gather + 8-child expansion, moment remap, "
+                                            "device scene rebuild, device octree build"}
+    del ts, gacc
+    sp = DATA / "S1M_init"
+    if (sp / "voxels.bin").exists():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        load_device_scene(sp)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        from paper_2507_18713_b200.scene import load_scene
+        sc_h, _ = load_scene(sp)
+        DeviceScene.from_scene(sc_h)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        out["scene_load_S1M"] = {"device_decode_s": t1 - t0, "host_load_plus_upload_s": t2 - t1,
+                                 "bytes": (sp / "voxels.bin").stat().st_size}
+    sph = [RY.InjectedSphere([2.0, 0.0, 0.8], 0.6, "mirror"), RY.InjectedSphere([4.0, 1.5, 0.6], 0.5, "glass"),
+           RY.InjectedSphere([3.0, -1.5, 0.5], 0.4, "opaque", albedo=[0.8, 0.2, 0.1])]
+    cb = camera_rays(cam)
+    out["effects_c2_camera_S1M"] = {
+        "fps": 1e3 / timeit(lambda: RY.trace_effects(ds, oc, cb.origins, cb.dirs, None, sph, [0.3, -0.5, 0.8],
+                                                     max_bounces=2), n=3),
+        "rays": cb.n, "spheres": "mirror, glass, opaque; 2 bounces; sun shadows"}
     out["surface_dense_regime"] = {
         "voxels": dss.n,
         "c2_forward_fps": 1e3 / timeit(lambda: RR.rasterize(dss, cam)),

@@ -358,6 +358,15 @@ int salf_voxel_geometry(int64_t n, const uint8_t *level, const int32_t *ijk, con
                         double base_edge, const double *params, double *geo, double *aux, float *prm,
                         void *stream);
 
+/* salf.v1 voxel records (container.py:27-35; 121-byte little-endian records,
+ * device copy of voxels.bin, 16-byte aligned) decoded straight into the
+ * device layout: level (u8), ijk (i32 x3), params (n x 27 f64), geo, aux,
+ * prm as salf_voxel_geometry; *bad |= 1 << f for non-finite values in field
+ * f (0 w_s, 1 w_c, 2 w_sh, 3 log_a, 4 log_b; container.py:56-59). */
+int salf_decode_records(int64_t n, const uint8_t *records, const double *aabb_min, double base_edge,
+                        uint8_t *level, int32_t *ijk, double *params, double *geo, double *aux, float *prm,
+                        int32_t *bad, void *stream);
+
 /* FP64 peak probe (benchmark utility): grid x 256 threads x 64*iters DFMA. */
 int salf_fp64_peak(double *scratch, int32_t grid, int32_t iters, void *stream);
 

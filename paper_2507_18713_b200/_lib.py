@@ -98,6 +98,7 @@ SIGNATURES = {
     "salf_fp32_peak": (C.c_int, [vp, C.c_int32, C.c_int32, vp]),
     "salf_effects_wave": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int32, vp, vp, vp, vp, vp,
                                     vp, vp, vp, vp, vp, vp]),
+    "salf_decode_records": (C.c_int, [C.c_int64, vp, vp, C.c_double, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_l1_seed": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int32, C.c_double, vp, vp, vp]),
     "salf_densify_flags": (C.c_int, [C.c_int64, vp, vp, vp, C.c_int32, C.c_double, C.c_int32, vp, vp, vp]),
     "salf_grad_norm_acc": (C.c_int, [C.c_int64, vp, vp, vp]),

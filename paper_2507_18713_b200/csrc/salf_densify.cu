@@ -165,3 +165,95 @@ extern "C" int salf_voxel_geometry(int64_t n, const uint8_t *level, const int32_
   }
   SALF_CATCH
 }
+
+// ---------------------------------------------------------------------------
+// salf.v1 voxel records straight into the device layout (container.py:27-35,
+// :91-100).  Record (121 B, little endian, unaligned):
+// u8 level | i32 ijk[3] | f32 w_s[4] | f32 w_c[9] | f32 w_sh[12] | f32 log_a | f32 log_b.
+// A warp stages 32 records (3872 B = 242 x 16 B, 16-B aligned because
+// 32 x 121 = 3872) with vector loads into shared memory, then each lane
+// decodes its record: level / ijk, the (27) f64 parameter row, geo / aux /
+// prm (k_voxel_geometry's arithmetic), and flags non-finite fields
+// (bit f of *bad for field f = w_s, w_c, w_sh, log_a, log_b).
+namespace salf {
+constexpr int kRecBytes = 121;
+
+__device__ __forceinline__ float rec_f32(const uint8_t *r, int off) {
+  const uint32_t u = (uint32_t)r[off] | ((uint32_t)r[off + 1] << 8) | ((uint32_t)r[off + 2] << 16) |
+                     ((uint32_t)r[off + 3] << 24);
+  return __uint_as_float(u);
+}
+
+__global__ void __launch_bounds__(128) k_decode_records(int64_t n, const uint8_t *__restrict__ rec, double ax,
+                                                        double ay, double az, double base_edge,
+                                                        uint8_t *__restrict__ level, int32_t *__restrict__ ijk,
+                                                        double *__restrict__ params, double *__restrict__ geo,
+                                                        double *__restrict__ aux, float *__restrict__ prm,
+                                                        int32_t *__restrict__ bad) {
+  __shared__ __align__(16) uint8_t stage[4][32 * kRecBytes];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t first = ((int64_t)blockIdx.x * 4 + warp) * 32;
+  if (first >= n) return;
+  const int cnt = (int)min((int64_t)32, n - first);
+  const uint8_t *src = rec + first * kRecBytes;
+  uint8_t *buf = stage[warp];
+  if (cnt == 32) {
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);  // 16-B aligned (see above)
+    uint4 *d4 = reinterpret_cast<uint4 *>(buf);
+    for (int k = lane; k < 32 * kRecBytes / 16; k += 32) d4[k] = __ldg(s4 + k);
+  } else {
+    for (int k = lane; k < cnt * kRecBytes; k += 32) buf[k] = src[k];
+  }
+  __syncwarp();
+  if (lane >= cnt) return;
+  const int64_t i = first + lane;
+  const uint8_t *r = buf + lane * kRecBytes;
+  const uint8_t lv = r[0];
+  level[i] = lv;
+  int32_t c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c[k] = (int32_t)__float_as_uint(rec_f32(r, 1 + 4 * k));
+    ijk[3 * i + k] = c[k];
+  }
+  double p[27];
+  int flags = 0;
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    const float f = rec_f32(r, 13 + 4 * k);
+    p[k] = (double)f;
+    const int field = k < 4 ? 0 : (k < 13 ? 1 : (k < 25 ? 2 : k - 22));
+    if (!isfinite(f)) flags |= 1 << field;
+    params[i * kGradStride + k] = p[k];
+  }
+  if (flags) atomicOr(bad, flags);
+  const double edge = __ddiv_rn(base_edge, ldexp(1.0, (int)lv));
+  const double lo[3] = {ax, ay, az};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) geo[4 * i + k] = __dadd_rn(lo[k], __dmul_rn(__dadd_rn((double)c[k], 0.5), edge));
+  geo[4 * i + 3] = edge;
+  aux[4 * i + 0] = exp(p[25]);
+  aux[4 * i + 1] = 1.0 / exp(p[26]);
+  aux[4 * i + 2] = __ddiv_rn(2.0, edge);
+  aux[4 * i + 3] = 0.0;
+  float *q = prm + i * SALF_PRM_STRIDE;
+#pragma unroll
+  for (int k = 0; k < 25; ++k) q[k] = (float)p[k];
+#pragma unroll
+  for (int k = 25; k < SALF_PRM_STRIDE; ++k) q[k] = 0.f;
+}
+}  // namespace salf
+
+extern "C" int salf_decode_records(int64_t n, const uint8_t *records, const double *aabb_min, double base_edge,
+                                   uint8_t *level, int32_t *ijk, double *params, double *geo, double *aux,
+                                   float *prm, int32_t *bad, void *stream) {
+  SALF_TRY {
+    if (n == 0) return SALF_OK;
+    if (((uintptr_t)records & 15) != 0) return set_error(SALF_EINVAL, "record buffer must be 16-byte aligned");
+    const int64_t warps = (n + 31) / 32;
+    k_decode_records<<<(unsigned)((warps + 3) / 4), 128, 0, (cudaStream_t)stream>>>(
+        n, records, aabb_min[0], aabb_min[1], aabb_min[2], base_edge, level, ijk, params, geo, aux, prm, bad);
+    return check_cuda("salf_decode_records");
+  }
+  SALF_CATCH
+}

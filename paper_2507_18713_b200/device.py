@@ -98,3 +98,61 @@ def grads_to_dict(grad: torch.Tensor) -> dict:
     return {"w_s": g[:, 0:4].copy(), "w_c": g[:, 4:13].reshape(m, 3, 3).copy(),
             "w_sh": g[:, 13:25].reshape(m, 3, 4).copy(), "log_a": g[:, 25].copy(),
             "log_b": g[:, 26].copy()}
+
+
+_FIELDS = ("w_s", "w_c", "w_sh", "log_a", "log_b")
+
+
+def load_device_scene(path, device=None) -> DeviceScene:
+    """salf.v1 static voxel set straight into HBM (container.py:91-100,
+    :130-158): voxels.bin is read once into pinned host
+    memory, copied to the device as raw 121-byte records and decoded there
+    (`salf_decode_records`) into the render layout plus the (M, 27) f64
+    parameter block, level and ijk (attributes `params`, `level`, `ijk`,
+    `bounds`, `meta`).  Validation and messages follow the reference loader:
+    size mismatch, non-finite fields (first offending field in record
+    order), duplicate cells.  Actors, if any, are left to `scene.load_scene`."""
+    import json
+    from pathlib import Path
+
+    from .scene import FORMAT_VERSION, VOXEL_DTYPE, ContainerError, SceneBounds
+    path = Path(path)
+    meta = json.loads((path / "meta.json").read_text(encoding="utf-8"))
+    if meta.get("format") != FORMAT_VERSION:
+        raise ContainerError(f"meta.json: unsupported format {meta.get('format')!r}")
+    bounds = SceneBounds.from_dict(meta["bounds"])
+    count = int(meta["voxel_count"])
+    vb = path / "voxels.bin"
+    size = vb.stat().st_size
+    rec_size = VOXEL_DTYPE.itemsize
+    if size != count * rec_size:
+        raise ContainerError(f"voxels.bin: size mismatch, expected {count * rec_size} bytes for {count} voxels, "
+                             f"got {size}")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    lib = _lib.load()
+    m = max(count, 1)
+    host = torch.empty(((count * rec_size + 15) // 16) * 16 or 16, dtype=torch.uint8).pin_memory()
+    with open(vb, "rb") as f:
+        f.readinto(host.numpy()[: count * rec_size].data)
+    raw = host.to(dev, non_blocking=True)
+    level = torch.empty(m, dtype=torch.uint8, device=dev)
+    ijk = torch.empty((m, 3), dtype=torch.int32, device=dev)
+    params = torch.empty((m, 27), dtype=torch.float64, device=dev)
+    geo = torch.empty((m, 4), dtype=torch.float64, device=dev)
+    aux = torch.empty((m, 4), dtype=torch.float64, device=dev)
+    prm = torch.zeros((m, _lib.PRM_STRIDE), dtype=torch.float32, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    lo = np.ascontiguousarray(bounds.aabb_min, np.float64)
+    _lib.check(lib.salf_decode_records(count, raw.data_ptr(), lo.ctypes.data, float(bounds.base_edge),
+                                       level.data_ptr(), ijk.data_ptr(), params.data_ptr(), geo.data_ptr(),
+                                       aux.data_ptr(), prm.data_ptr(), bad.data_ptr(), _lib.stream_ptr()),
+               "load_device_scene")
+    flags = int(bad.item())
+    for k, name in enumerate(_FIELDS):
+        if flags >> k & 1:
+            raise ContainerError(f"voxels.bin: non-finite values in field {name!r}")
+    if count and int(torch.unique(torch.cat([level[:, None].to(torch.int32), ijk], 1), dim=0).shape[0]) != count:
+        raise ContainerError("voxels.bin: duplicate voxel cells")
+    ds = DeviceScene.from_arrays(geo, aux, prm, count, meta.get("density_mode", "sdf"))
+    ds.params, ds.level, ds.ijk, ds.bounds, ds.meta = params[:count], level[:count], ijk[:count], bounds, meta
+    return ds

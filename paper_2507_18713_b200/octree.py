@@ -102,40 +102,59 @@ def build_octree_device(voxels: SparseVoxelSet, bounds: SceneBounds | None = Non
     """build_octree on the GPU: the reference's DFS layout
     from sorted preorder keys (csrc/salf_octree.cu); same validation as
     build_octree."""
-    lib = _lib.load()
     if bounds is None:
         bounds = voxels.bounds
-    extent = bounds.aabb_max - bounds.aabb_min
-    m = max(0, int(np.ceil(np.log2(max(extent.max(), 1e-300) / bounds.base_edge) - 1e-12)))
-    root_edge = bounds.base_edge * 2.0 ** m
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    n = voxels.n
+    if voxels.n and int(voxels.level.astype(np.int64).max()) + _root_depth(bounds) > 19:
+        return build_octree(voxels, bounds, device)  # deeper than the packed key: host build
+    lv = torch.as_tensor(voxels.level.astype(np.uint8), device=dev)
+    ijk = torch.as_tensor(np.ascontiguousarray(voxels.ijk.astype(np.int32)).reshape(-1, 3), device=dev)
+    return build_octree_from_device(lv, ijk, bounds)
+
+
+def _root_depth(bounds: SceneBounds) -> int:
+    extent = bounds.aabb_max - bounds.aabb_min
+    return max(0, int(np.ceil(np.log2(max(extent.max(), 1e-300) / bounds.base_edge) - 1e-12)))
+
+
+def build_octree_from_device(level: torch.Tensor, ijk: torch.Tensor, bounds: SceneBounds) -> OctreeBuffer:
+    """build_octree (octree.py:54-125) from device-resident (level u8, ijk i32)
+    -- e.g. a scene decoded on the device or a densified set -- with the
+    reference's validation (octree.py:66-90) done on the device."""
+    lib = _lib.load()
+    dev = level.device
+    m = _root_depth(bounds)
+    root_edge = bounds.base_edge * 2.0 ** m
+    n = int(level.numel())
     if n == 0:
         return OctreeBuffer(torch.full((1,), -1, dtype=torch.int32, device=dev), bounds.aabb_min.copy(),
                             root_edge, m)
-    level = voxels.level.astype(np.int64)
-    if m + int(level.max()) > 19:
-        return build_octree(voxels, bounds, device)  # deeper than the packed key: host build
-    cells = voxels.ijk.astype(np.int64)
-    edges = voxels.edges()
-    if edges.min() < MIN_EDGE_FACTOR * EPS_ADVANCE:
-        raise ValueError(f"voxel edge {edges.min():.3g} m below the marching floor "
+    lv64 = level.to(torch.int64)
+    max_level = int(lv64.max().item())
+    if m + max_level > 19:
+        raise ValueError("octree deeper than the packed device key; use build_octree")
+    edges = bounds.base_edge / torch.exp2(lv64.to(torch.float64))
+    if float(edges.min().item()) < MIN_EDGE_FACTOR * EPS_ADVANCE:
+        raise ValueError(f"voxel edge {float(edges.min().item()):.3g} m below the marching floor "
                          f"{MIN_EDGE_FACTOR * EPS_ADVANCE:.3g} m")
-    keys = (level << 54) ^ (cells[:, 0] << 36) ^ (cells[:, 1] << 18) ^ cells[:, 2]
-    if len(np.unique(keys)) != n:
+    cells = ijk.to(torch.int64)
+    keys = (lv64 << 54) ^ (cells[:, 0] << 36) ^ (cells[:, 1] << 18) ^ cells[:, 2]
+    if int(torch.unique(keys).numel()) != n:
         raise ValueError("duplicate voxel cells in the set")
-    centers = voxels.centers()
-    if np.any(centers < bounds.aabb_min) or np.any(centers > bounds.aabb_max):
+    lo = torch.as_tensor(bounds.aabb_min, device=dev)
+    hi = torch.as_tensor(bounds.aabb_max, device=dev)
+    centers = lo + (cells.to(torch.float64) + 0.5) * edges[:, None]
+    if bool(((centers < lo) | (centers > hi)).any()):
         raise ValueError("voxel outside scene bounds")
-    lv = torch.as_tensor(voxels.level.astype(np.uint8), device=dev)
-    ijk = torch.as_tensor(np.ascontiguousarray(voxels.ijk.astype(np.int32)), device=dev)
-    depth = m + lv.to(torch.int64)
+    lv = level.to(torch.uint8).contiguous()
+    ijk32 = ijk.to(torch.int32).contiguous()
+    depth = m + lv64
     base = torch.cumsum(depth, 0) - depth
     total = int(depth.sum().item())
     akeys = torch.empty(max(total, 1), dtype=torch.int64, device=dev)
     skeys = torch.empty(n, dtype=torch.int64, device=dev)
     s = _lib.stream_ptr()
-    _lib.check(lib.salf_octree_ancestor_keys(n, lv.data_ptr(), ijk.data_ptr(), m, base.data_ptr(),
+    _lib.check(lib.salf_octree_ancestor_keys(n, lv.data_ptr(), ijk32.data_ptr(), m, base.data_ptr(),
                                              akeys.data_ptr(), skeys.data_ptr(), s), "build_octree")
     # keys < 2^62, so signed int64 order == unsigned order
     internal = torch.unique(akeys[:total]) if total else akeys[:0]
@@ -146,7 +165,7 @@ def build_octree_device(voxels: SparseVoxelSet, bounds: SceneBounds | None = Non
                                     contained.data_ptr(), s), "build_octree")
     if int(contained.item()):
         raise ValueError("stored voxel contains another stored voxel")
-    return OctreeBuffer(nodes, bounds.aabb_min.copy(), root_edge, m + int(level.max()))
+    return OctreeBuffer(nodes, bounds.aabb_min.copy(), root_edge, m + max_level)
 
 
 def dump_table(buffer: OctreeBuffer) -> str:
