@@ -277,31 +277,31 @@ __device__ __forceinline__ void segment_grad(int mode, double delta, double sigm
 }
 
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes
-// of a converged warp.  Lanes holding the same voxel id form a group; a group
-// of >= 3 lanes is summed with one transposed reduction, after which lanes
-// 0..26 each issue one coalesced fp64 atomic; lanes of smaller groups add
-// their values directly.  g is consumed (overwritten).
+// of a converged warp.  Lanes holding the same voxel id form a group
+// (__match_any_sync).  Lanes in groups of fewer than 4 add their non-zero
+// components directly -- all such lanes in the same 27 (predicated) RED
+// instructions, so distinct voxels never serialise; each group of >= 4
+// lanes is summed with one transposed reduction, after which lanes 0..26
+// issue one coalesced fp64 atomic per component.  g is consumed.
 __device__ __forceinline__ void scatter_grad(double *__restrict__ grad, int64_t vid, bool active, float g[32]) {
   const unsigned full = 0xffffffffu;
-  unsigned pending = __ballot_sync(full, active);
-  if (!pending) return;
+  if (!__ballot_sync(full, active)) return;
   const int lane = threadIdx.x & 31;
   const long long key = active ? (long long)vid : -1ll;
+  const unsigned peers = __match_any_sync(full, key);
+  const bool big = active && __popc(peers) >= 4;
+  if (active && !big) {
+    double *dst = grad + key * kGradStride;
+#pragma unroll
+    for (int k = 0; k < kGradStride; ++k)
+      if (g[k] != 0.0f) atomicAdd(dst + k, (double)g[k]);
+  }
+  unsigned pending = __ballot_sync(full, big);
   while (pending) {
     const int L = __ffs(pending) - 1;
     const long long lkey = __shfl_sync(full, key, L);
-    const bool mem = active && key == lkey;
-    const unsigned members = __ballot_sync(full, mem);
-    pending &= ~members;
-    if (__popc(members) <= 2) {
-      if (mem) {
-        double *dst = grad + lkey * kGradStride;
-#pragma unroll
-        for (int k = 0; k < kGradStride; ++k)
-          if (g[k] != 0.0f) atomicAdd(dst + k, (double)g[k]);
-      }
-      continue;
-    }
+    const bool mem = big && key == lkey;
+    pending &= ~__ballot_sync(full, mem);
     float v[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) v[k] = mem ? g[k] : 0.0f;

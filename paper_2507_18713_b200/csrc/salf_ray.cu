@@ -492,6 +492,7 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
     }
   }
   int32_t st = 0;
+  const bool want_color = dC[0] != 0.0 || dC[1] != 0.0 || dC[2] != 0.0;
   while (__any_sync(0xffffffffu, live)) {
     bool act = false;
     int64_t vid = 0;
@@ -500,7 +501,8 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
       double s0, s1;
       if (m.step(t, vid, s0, s1, st)) {
         RaySeg sv;
-        shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, true);
+        sv.c[0] = sv.c[1] = sv.c[2] = 0.0;  // depth-only rays (LiDAR): no colour term
+        shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, want_color);
         const double a = sv.alpha;
         const double tb = T;
         if (tb > keep) {
