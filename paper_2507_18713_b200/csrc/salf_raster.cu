@@ -631,7 +631,8 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
 struct RayF {
   double d[3];
   double tn0;  // max(t_near, 0)
-  float df[3], inv[3], gam[4];
+  float df[3], dl[3], inv[3], gam[4];  // d = df + dl (two-float split)
+  float tn0f;
   bool fast;   // no zero component (else the fp64 reference slab test runs)
 };
 
@@ -641,10 +642,12 @@ __device__ __forceinline__ void rayf_from_dir(const double d[3], double t_near, 
   for (int k = 0; k < 3; ++k) {
     r.d[k] = d[k];
     r.df[k] = (float)d[k];
+    r.dl[k] = (float)(d[k] - (double)r.df[k]);
     r.inv[k] = 1.0f / r.df[k];
     r.fast = r.fast && d[k] != 0.0 && isfinite(r.inv[k]);
   }
   r.tn0 = t_near > 0.0 ? t_near : 0.0;
+  r.tn0f = (float)r.tn0;
   r.gam[0] = (float)kShC0;
   r.gam[1] = (float)(kShC1 * d[1]);
   r.gam[2] = (float)(kShC1 * d[2]);
@@ -660,6 +663,7 @@ struct EntryF {
   int vid, rot;
   VoxPrm p;
   float wn;         // |w_s| 1-norm (error bound of the fp32 SDF)
+  float oh[3], ol[3];  // o = oh + ol (two-float split)
 };
 
 template <bool kRot>
@@ -690,16 +694,72 @@ __device__ __forceinline__ void stage_entry_f(const salf_scene_t &sc, const Pinh
       e.o[0] = o2[0]; e.o[1] = o2[1]; e.o[2] = o2[2];
     }
   }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    e.oh[k] = (float)e.o[k];
+    e.ol[k] = (float)(e.o[k] - (double)e.oh[k]);
+  }
 }
 
-// Pair test in closest-approach coordinates.  With t* = -(o . d) the ray
-// point closest to the voxel centre, the ray is q + u d with
-// q = o + t* d (|q| ~ the voxel size for any hit) and u = t - t*, so the
-// slab test, delta, t_mid - t* and the local coordinates are all
-// well-conditioned in fp32; only t* and q take fp64 (6 DFMA per pair).
-// Returns the fp32 u-interval [u0, u1] and t* (fp64).  Rays with a zero
-// direction component use the fp64 reference slab test (octree.py:184-194).
+// Pair test in closest-approach coordinates.  With t* ~ -(o . d) (any
+// value near the closest approach to the voxel centre) the ray is q + u d
+// with q = o + t* d (|q| ~ the voxel size for any pair that can hit) and
+// u = t - t*, so the slab test, delta, t_mid - t* and the local coordinates
+// are well-conditioned in fp32 even though |o| ~ 1000 voxel edges.  q is
+// evaluated in two-float arithmetic (o = oh + ol, d = dh + dl):
+// q = fma(t*, dh, oh) + fma(t*, dl, ol), |dq| <= 2^-23 |q| + 1e-12; t* itself
+// is fp32 (its error only moves the reference point along the ray).  No fp64
+// and no fp64<->fp32 conversion per pair.  Rays with a zero direction
+// component use the fp64 reference slab test (octree.py:184-194).
 __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float q[3], float &u0, float &u1,
+                                           float &ts) {
+  if (r.fast) {
+    ts = -__fmaf_rn(e.oh[2], r.df[2], __fmaf_rn(e.oh[1], r.df[1], e.oh[0] * r.df[0]));
+    // slab k: u in [(-s h - q) / d, (s h - q) / d], s = sign(d): h |1/d| -/+ q/d
+    float un = -INFINITY, uf = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      q[k] = __fmaf_rn(ts, r.df[k], e.oh[k]) + __fmaf_rn(ts, r.dl[k], e.ol[k]);
+      const float qi = q[k] * r.inv[k];
+      un = fmaxf(un, __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi));
+      uf = fminf(uf, __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi));
+    }
+    u0 = fmaxf(un, r.tn0f - ts);
+    u1 = uf;
+    return u1 > u0;
+  }
+  const double tsd = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
+  ts = (float)tsd;
+  const double t_ref = (double)ts;  // u relative to the fp32 reference point
+  double ti = 0.0, to = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    q[k] = (float)fma(t_ref, r.d[k], e.o[k]);
+    const double lo = -e.half - e.o[k], hi = e.half - e.o[k];
+    double nk, fk;
+    if (r.d[k] == 0.0) {
+      const bool inside = (e.o[k] >= -e.half) && (e.o[k] <= e.half);
+      nk = inside ? -INFINITY : INFINITY;
+      fk = inside ? INFINITY : -INFINITY;
+    } else {
+      const double inv = 1.0 / r.d[k];
+      const double ta = lo * inv, tb = hi * inv;
+      nk = npmin(ta, tb);
+      fk = npmax(ta, tb);
+    }
+    if (k == 0) { ti = nk; to = fk; }
+    else { ti = npmax(ti, nk); to = npmin(to, fk); }
+  }
+  const double t0 = npmax(ti, r.tn0);
+  if (!(to > t0 + 1e-12)) return false;
+  u0 = (float)(t0 - t_ref);
+  u1 = (float)(to - t_ref);
+  return true;
+}
+
+// The backward's variant: t* and q in fp64 (6 DFMA), rounded to fp32 once.
+// (The two-float form above measured slower in the issue-bound backward.)
+__device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, float q[3], float &u0, float &u1,
                                            double &ts) {
   ts = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
   if (r.fast) {
@@ -763,10 +823,11 @@ __device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_r
   const double acc_w = s[3], acc_wt = s[4];
   const bool ok = acc_w > kDepthWeightMin;  // depth_valid (backward.py:46-49)
   const double dd = ok ? d_depth[pix] : 0.0;
-  q.D = ok ? acc_wt / acc_w : 0.0;
+  const double D = ok ? acc_wt / acc_w : 0.0;
+  q.D = D;
   const double ws = ok ? acc_w : 1.0;
   // sum_j A_j w_j = dC . acc_rgb + dD (acc_wt - D acc_w) / ws (suffix sums by subtraction)
-  q.total = dCd[0] * s[0] + dCd[1] * s[1] + dCd[2] * s[2] + dd * (acc_wt - q.D * acc_w) / ws;
+  q.total = dCd[0] * s[0] + dCd[1] * s[1] + dCd[2] * s[2] + dd * (acc_wt - D * acc_w) / ws;
   // tail = (dC . background) * T_final (backward.py:62)
   q.tail = (float)((dCd[0] * opt.background[0] + dCd[1] * opt.background[1] + dCd[2] * opt.background[2]) * s[5]);
   q.dws = (float)(dd / ws);
@@ -793,7 +854,7 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, bool sdf, co
     rayf_from_dir(d2, q.r.tn0, rr);
     ray = &rr;
   }
-  if (!pair_hit_f(*ray, e, qv, u0, u1, ts)) return false;
+  if (!pair_hit_bwd(*ray, e, qv, u0, u1, ts)) return false;
   const float delta = u1 - u0;
   const float um = 0.5f * (u0 + u1);
   const float dq = (float)(ts - q.D) + um;  // t_mid - D
@@ -911,21 +972,23 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
   const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
   const bool sdf = sc.density_mode == SALF_DENSITY_SDF;
-  const double y_stop = -log(1.0 - opt.stop_threshold);  // included iff Y_before < y_stop
+  const double y_stop_d = -log(1.0 - opt.stop_threshold);  // included iff Y_before < y_stop
+  const float y_stop = (float)y_stop_d, y_stop_err = (float)fabs(y_stop_d - (double)y_stop);
   constexpr double kLn2 = 0.6931471805599453;             // sum w > 0.5 iff Y_final > ln 2
   constexpr float kYClamp = 27.631021115928547f;           // -ln(1 - kAlphaMax)
 
   RayF r;
-  float pdd = 0.f;  // dd / h for this pixel
+  float pdd = 0.f, pdd0 = 0.f;  // dd = pdd h + pdd0 for this pixel
   if (inside) {
     PixelRay pr;
     pixel_ray(c, px, py, pr);
     rayf_from_dir(pr.d, pr.t_near, r);
     const float im = fmaxf(fabsf(r.inv[0]), fmaxf(fabsf(r.inv[1]), fabsf(r.inv[2])));
-    pdd = 8.f * kU24 * im;
+    pdd = 12.f * kU24 * im;
+    pdd0 = 2e-12f * im;
   }
-  float T = 1.f, acc_c[3] = {0.f, 0.f, 0.f}, acc_w = 0.f, EY = 0.f;
-  double Y = 0.0, acc_wt = 0.0;
+  // Y = Yh + Yc: compensated (Neumaier) fp32 sum, |error| <= 2^-23 Y + n 2^-46 Y
+  float T = 1.f, acc_c[3] = {0.f, 0.f, 0.f}, acc_w = 0.f, acc_wt = 0.f, EY = 0.f, Yh = 0.f, Yc = 0.f;
   bool alive = inside, flag = false;
   int n_stop = (int)(end - beg), n_inc = 0;
   const int nthreads = blockDim.x;
@@ -948,10 +1011,9 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           rayf_from_dir(d2, r.tn0, rr);
           ray = &rr;
         }
-        float qv[3], u0, u1;
-        double ts;
+        float qv[3], u0, u1, ts;
         const bool hit = pair_hit_f(*ray, e, qv, u0, u1, ts);
-        const float dd = pdd * e.hf;
+        const float dd = __fmaf_rn(pdd, e.hf, pdd0);
         if (!hit) {
           // A near-grazing miss may be an fp64 hit with y <= sigma 4 dd <= a 4 dd (SDF: sigma <= a):
           // widen the band instead of flagging; raw density has no such bound.  (Near-grazing hits
@@ -963,9 +1025,11 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           continue;
         }
         // inclusion of this hit: Y_before < y_stop (certified outside the band)
-        const double gap = y_stop - Y;
-        if ((SALF_FLAGMASK & 2) && fabs(gap) <= (double)__fmaf_rn(2.f, EY, 1e-9f)) flag = true;
-        if (!(gap > 0.0)) {  // stop: every later segment is excluded
+        const float Ys = Yh + Yc;
+        const float gap = y_stop - Ys;
+        if ((SALF_FLAGMASK & 2) && fabsf(gap) <= __fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU24, Ys, y_stop_err + 1e-9f)))
+          flag = true;
+        if (!(gap > 0.f)) {  // stop: every later segment is excluded
           alive = false;
           n_stop = (int)(base - beg) + j;
           break;
@@ -977,7 +1041,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
         for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
         const VoxPrm &p = e.p;
         const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
-        const float ds_abs = e.wn * (pdd + 10.f * kU24);
+        const float ds_abs = e.wn * (__fmaf_rn(pdd0, e.inv_hf, pdd) + 10.f * kU24);
         float sigma, rel;
         if (sdf) {
           const float sb = fabsf(s) * e.inv_b;
@@ -996,17 +1060,21 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
         acc_w += w;
-        acc_wt = fma((double)w, ts + (double)um, acc_wt);
+        acc_wt = __fmaf_rn(w, ts + um, acc_wt);
         EY += __fmaf_rn(y, rel + 2.f * kU24, 2.f * sigma * dd);
-        Y += (double)y;
-        T = fast_exp(-(float)Y);
+        const float Yt = Yh + y;  // Neumaier: Yc collects the rounding of every addition
+        Yc += fabsf(Yh) >= y ? (Yh - Yt) + y : (y - Yt) + Yh;
+        Yh = Yt;
+        T = fast_exp(-(Yh + Yc));
         ++n_inc;
       }
     }
     if (!__syncthreads_or(alive)) break;
   }
   if (!inside) return;
-  if ((SALF_FLAGMASK & 4) && fabs(Y - kLn2) <= (double)__fmaf_rn(2.f, EY, 1e-9f)) flag = true;
+  const double Y = (double)Yh + (double)Yc;
+  if ((SALF_FLAGMASK & 4) && fabs(Y - kLn2) <= (double)__fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU24, (float)Y, 1e-9f)))
+    flag = true;
   const bool valid = Y > kLn2;  // sum w = 1 - T_final > 0.5
   const double wsum = -expm1(-Y);  // 1 - T_final, consistent with `valid`
   const int64_t pix = (int64_t)py * c.width + px;
@@ -1018,7 +1086,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
     double *sv = saved + pix * SALF_SAVED_STRIDE;
     sv[0] = acc_c[0]; sv[1] = acc_c[1]; sv[2] = acc_c[2];
     sv[3] = valid ? fmax(wsum, 0.5000000001) : fmin(wsum, 0.5);
-    sv[4] = acc_wt * (sv[3] / (double)acc_w);  // keeps D = acc_wt / acc_w
+    sv[4] = (double)acc_wt * (sv[3] / (double)acc_w);  // keeps D = acc_wt / acc_w
     sv[5] = T; sv[6] = (double)n_stop; sv[7] = (double)n_inc;
   }
 }
