@@ -37,6 +37,9 @@ static OctDev make_oct(const salf_octree_t *t) {
 
 enum : int32_t { kStatusRoundCap = 1, kStatusOutsideRoot = 2, kStatusOrder = 4 };
 
+#ifndef SALF_MARCH_INTBITS
+#define SALF_MARCH_INTBITS 1
+#endif
 // query_batch for one point (octree.py:136-166).  Returns node word
 // (-1 empty, <= -2 leaf), writes corner/edge of the node.
 __device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3], double corner[3], double &edge,
@@ -52,17 +55,39 @@ __device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3
   }
   edge = t.root_edge;
   int32_t w = __ldg(t.nodes);
+#if SALF_MARCH_INTBITS
+  // The reference's iterate u <- 2u - bit is exact, so the bit taken at
+  // level l is bit (30 - l) of floor(u 2^31) (exact scaling; u == 1
+  // iterates to 1, i.e. all ones; trees are < 31 levels deep).  Integer bit
+  // extraction replaces the per-level fp64 compare / update; the corner
+  // accumulation stays fp64 in the reference's order.
+  uint32_t U[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) U[k] = min((uint32_t)__dmul_rn(u[k], 2147483648.0), 0x7fffffffu);
+  int sh = 30;
+  while (w >= 0) {
+    const int b0 = (U[0] >> sh) & 1, b1 = (U[1] >> sh) & 1, b2 = (U[2] >> sh) & 1;
+    --sh;
+    edge = __dmul_rn(edge, 0.5);
+    corner[0] = __dadd_rn(corner[0], b0 ? edge : 0.0);
+    corner[1] = __dadd_rn(corner[1], b1 ? edge : 0.0);
+    corner[2] = __dadd_rn(corner[2], b2 ? edge : 0.0);
+    w = __ldg(t.nodes + w + b0 + 2 * b1 + 4 * b2);
+  }
+#else
   while (w >= 0) {
     const int b0 = u[0] >= 0.5, b1 = u[1] >= 0.5, b2 = u[2] >= 0.5;
     edge = __dmul_rn(edge, 0.5);
     corner[0] = __dadd_rn(corner[0], b0 ? edge : 0.0);
     corner[1] = __dadd_rn(corner[1], b1 ? edge : 0.0);
     corner[2] = __dadd_rn(corner[2], b2 ? edge : 0.0);
-    u[0] = __dsub_rn(__dmul_rn(2.0, u[0]), (double)b0);
-    u[1] = __dsub_rn(__dmul_rn(2.0, u[1]), (double)b1);
-    u[2] = __dsub_rn(__dmul_rn(2.0, u[2]), (double)b2);
+    // 2u - bit is exact, so one fma gives the reference's value
+    u[0] = fma(2.0, u[0], -(double)b0);
+    u[1] = fma(2.0, u[1], -(double)b1);
+    u[2] = fma(2.0, u[2], -(double)b2);
     w = __ldg(t.nodes + w + b0 + 2 * b1 + 4 * b2);
   }
+#endif
   return w;
 }
 
