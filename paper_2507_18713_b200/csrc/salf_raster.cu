@@ -655,14 +655,16 @@ __device__ __forceinline__ void rayf_from_dir(const double d[3], double t_near, 
 }
 
 // Staged entry of the mixed-precision backward.
-struct EntryF {
-  double o[3];      // camera position - voxel centre (fp64)
-  double half;      // 0.5 * edge (fp64, for the reference slab test fallback)
+// Layout: the 25 field parameters first (16-B aligned: LDS.128 reads), then
+// the scalars, then the fp64 geometry.
+struct __align__(16) EntryF {
+  VoxPrm p;
+  float wn;         // |w_s| 1-norm (error bound of the fp32 SDF)
   float hf, inv_hf; // fp32 half edge and its reciprocal
   float a, inv_b;
   int vid, rot;
-  VoxPrm p;
-  float wn;         // |w_s| 1-norm (error bound of the fp32 SDF)
+  double o[3];      // camera position - voxel centre (fp64)
+  double half;      // 0.5 * edge (fp64, for the reference slab test fallback)
   float oh[3], ol[3];  // o = oh + ol (two-float split)
 };
 
