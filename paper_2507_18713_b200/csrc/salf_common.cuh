@@ -169,7 +169,11 @@ __device__ __forceinline__ void eval_color32(const VoxPrm &p, const double xd[3]
 }
 
 // MUFU exp (ex2.approx of x log2 e): relative error ~2^-22 + |x| 2^-24.
-__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
+}
 
 // expm1(x) for x <= 0 in fp32 without cancellation: degree-7 Taylor on
 // (-0.25, 0] (truncation |x|^8/8! < 4e-10 relative), exp(x) - 1 below it

@@ -841,8 +841,8 @@ __device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_r
 
 // One included segment of pixel q against staged entry e: adds its 27
 // gradient components to g.  Returns false on a miss.
-template <bool kRot>
-__device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, bool sdf, const EntryF &e, BwdPix &q,
+template <bool kRot, bool sdf>
+__device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF &e, BwdPix &q,
                                             float g[32]) {
   float qv[3], u0, u1;
   double ts;
@@ -960,7 +960,7 @@ constexpr float kU24 = 5.9604645e-8f;  // 2^-24
 #ifndef SALF_FWDF_MINB
 #define SALF_FWDF_MINB 3
 #endif
-template <bool kRot>
+template <bool kRot, bool sdf>
 __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                         const int64_t *__restrict__ offsets,
                                                         const int32_t *__restrict__ entries,
@@ -973,7 +973,6 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   const int px = tx * c.tile + lx, py = ty * c.tile + ly;
   const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
   const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
-  const bool sdf = sc.density_mode == SALF_DENSITY_SDF;
   const double y_stop_d = -log(1.0 - opt.stop_threshold);  // included iff Y_before < y_stop
   const float y_stop = (float)y_stop_d, y_stop_err = (float)fabs(y_stop_d - (double)y_stop);
   constexpr double kLn2 = 0.6931471805599453;             // sum w > 0.5 iff Y_final > ln 2
@@ -1185,7 +1184,7 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
 #define SALF_BWDF_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 
-template <bool kRot, int NP>
+template <bool kRot, int NP, bool sdf>
 __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
@@ -1200,7 +1199,6 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   const int nthreads = blockDim.x;
   const int npix = c.tile * c.tile;
-  const bool sdf = sc.density_mode == SALF_DENSITY_SDF;
   const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
   (void)end;
 
@@ -1238,7 +1236,7 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
       bool act = false;
 #pragma unroll
       for (int k = 0; k < NP; ++k)
-        if (jb + j < q[k].n_stop) act |= bwd_segment<kRot>(sc, sdf, e, q[k], g);
+        if (jb + j < q[k].n_stop) act |= bwd_segment<kRot, sdf>(sc, e, q[k], g);
       float tot = 0.0f;
 #if SALF_BWD_SMEMRED
       // transpose through shared memory: 7 x STS.128 per lane, lane k sums column k
@@ -1438,19 +1436,22 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
       static const bool no_redo = getenv("SALF_NO_REDO") && getenv("SALF_NO_REDO")[0] == '1';
       const int64_t npx = (int64_t)c.width * c.height;
       const unsigned rb = (unsigned)((npx + 127) / 128);
+      const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
+#define SALF_LAUNCH_FWD(ROT, SDF)                                                                             \
+  k_composite_fast<ROT, SDF><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity, \
+                                                         out_depth, saved)
       if (rot) {
-        k_composite_fast<true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
-                                                             out_depth, saved);
+        if (sdf) SALF_LAUNCH_FWD(true, true); else SALF_LAUNCH_FWD(true, false);
         if (!no_redo)
           k_composite_redo<true><<<rb, 128, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
                                                      out_depth, saved);
       } else {
-        k_composite_fast<false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
-                                                              out_depth, saved);
+        if (sdf) SALF_LAUNCH_FWD(false, true); else SALF_LAUNCH_FWD(false, false);
         if (!no_redo)
           k_composite_redo<false><<<rb, 128, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
                                                       out_depth, saved);
       }
+#undef SALF_LAUNCH_FWD
     }
     return check_cuda("salf_raster_composite");
   }
@@ -1477,12 +1478,18 @@ extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera
     else if (opts->exact_color)
       k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
                                                            grad);
-    else if (rot)
-      k_backward_fast<true, SALF_BWD_NP><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved,
-                                                                          d_rgb, d_depth, grad);
-    else
-      k_backward_fast<false, SALF_BWD_NP><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved,
-                                                                           d_rgb, d_depth, grad);
+    else {
+      const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
+#define SALF_LAUNCH_BWD(ROT, SDF)                                                                               \
+  k_backward_fast<ROT, SALF_BWD_NP, SDF><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved, \
+                                                                        d_rgb, d_depth, grad)
+      if (rot) {
+        if (sdf) SALF_LAUNCH_BWD(true, true); else SALF_LAUNCH_BWD(true, false);
+      } else {
+        if (sdf) SALF_LAUNCH_BWD(false, true); else SALF_LAUNCH_BWD(false, false);
+      }
+#undef SALF_LAUNCH_BWD
+    }
     return check_cuda("salf_raster_backward");
   }
   SALF_CATCH
