@@ -311,43 +311,51 @@ def run_ours(args, world, rank, local):
     # Copies run on a side stream and overlap compute: step k+1's target is
     # uploaded during step k's backward, step k's frame is read back while its
     # backward runs.  Every byte still crosses PCIe inside the timed region.
-    barrier()
     cs = torch.cuda.current_stream(dev)
     xs = torch.cuda.Stream(dev)
     gt_bufs = [torch.empty_like(gt_dev), torch.empty_like(gt_dev)]
     loss_dev = torch.zeros(1, dtype=torch.float64, device=dev)
-    up = [torch.cuda.Event(), torch.cuda.Event()]
-    used = [torch.cuda.Event(), torch.cuda.Event()]
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(cs)
-    xs.wait_stream(cs)
-    with torch.cuda.stream(xs):
-        gt_bufs[0].copy_(gt_host, non_blocking=True)
-        up[0].record(xs)
-    for k in range(args.steps):
-        cur = gt_bufs[k % 2]
-        cs.wait_event(up[k % 2])
-        fb, st = RR.rasterize(ds, cam, return_state=True)
-        dc, lsum = l1_color_seed(fb.color, cur)
-        loss_dev.copy_((lsum / dc.numel()).reshape(1))
-        used[k % 2].record(cs)
-        xs.wait_event(used[k % 2])
+
+    def e2e_pass(n_steps):
+        up = [torch.cuda.Event(), torch.cuda.Event()]
+        used = [torch.cuda.Event(), torch.cuda.Event()]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        xs.wait_stream(cs)
         with torch.cuda.stream(xs):
-            fb.color.record_stream(xs)
-            loss_dev.record_stream(xs)
-            out_host.copy_(fb.color, non_blocking=True)
-            loss_host.copy_(loss_dev, non_blocking=True)
-            if k + 1 < args.steps:
-                if k >= 1:
-                    xs.wait_event(used[(k + 1) % 2])
-                gt_bufs[(k + 1) % 2].copy_(gt_host, non_blocking=True)
-                up[(k + 1) % 2].record(xs)
-        grad.zero_()
-        RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
-        if world > 1:
-            dist.all_reduce(grad)
-    cs.wait_stream(xs)
-    b.record(cs)
+            gt_bufs[0].copy_(gt_host, non_blocking=True)
+            up[0].record(xs)
+        for k in range(n_steps):
+            cur = gt_bufs[k % 2]
+            cs.wait_event(up[k % 2])
+            fb, st = RR.rasterize(ds, cam, return_state=True)
+            dc, lsum = l1_color_seed(fb.color, cur)
+            loss_dev.copy_((lsum / dc.numel()).reshape(1))
+            used[k % 2].record(cs)
+            xs.wait_event(used[k % 2])
+            with torch.cuda.stream(xs):
+                fb.color.record_stream(xs)
+                loss_dev.record_stream(xs)
+                out_host.copy_(fb.color, non_blocking=True)
+                loss_host.copy_(loss_dev, non_blocking=True)
+                if k + 1 < n_steps:
+                    if k >= 1:
+                        xs.wait_event(used[(k + 1) % 2])
+                    gt_bufs[(k + 1) % 2].copy_(gt_host, non_blocking=True)
+                    up[(k + 1) % 2].record(xs)
+            grad.zero_()
+            RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
+            if world > 1:
+                dist.all_reduce(grad)
+        cs.wait_stream(xs)
+        b.record(cs)
+        return a, b
+
+    # untimed warm-up of the end-to-end pipeline (pinned copies, side stream,
+    # allocator blocks held by record_stream), then the timed pass
+    e2e_pass(max(args.warmup, 3))
+    barrier()
+    a, b = e2e_pass(args.steps)
     barrier()
     e2e_ms = a.elapsed_time(b) / args.steps
     te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
