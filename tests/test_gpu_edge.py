@@ -260,6 +260,32 @@ def test_c2_frame_tiles_match_oracle(s1m):
         assert np.max(np.abs(col[sl] - ref["color"][sl])) < 1e-4
 
 
+@pytest.mark.parametrize("tile", [(60, 34), (5, 60)])
+def test_c2_backward_full_size_tile_matches_oracle(s1m, tile):
+    """C2 (1080p, S1M) fwd+bwd at full size with the loss seeded on one tile:
+    the default mixed-precision gradient equals the oracle composition
+    (raster pairs of that tile -> _composite -> backward_records) to 1e-4
+    normwise per parameter class."""
+    from conftest import grads_close
+    from paper_2507_18713_b200 import configs, render_raster as RR
+    from paper_2507_18713_b200.device import DeviceScene
+    cam = configs.c2_camera()
+    h, w = cam.height, cam.width
+    tx, ty = tile
+    rng = np.random.default_rng(tx * 100 + ty)
+    dc = np.zeros((h, w, 3))
+    dc[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = np.sign(rng.normal(size=(16, 16, 3))) / 1e4
+    fb, st = RR.rasterize(DeviceScene.from_scene(s1m), cam, return_state=True)
+    g = RR.rasterize_backward(st, dc, np.zeros((h, w)))
+    vox = oracle_voxels(s1m)
+    ocam = O.Camera("pinhole", w, h, cam.fx, cam.fy, cam.cx, cam.cy, position=cam.position,
+                    quaternion=cam.quaternion)
+    rec = O.raster_records(vox, ocam, window=(tx, ty, tx, ty))
+    want = O.backward_records(rec, vox, dc.reshape(-1, 3), np.zeros(h * w))
+    assert np.abs(want["w_s"]).max() > 0
+    assert grads_close(g, want) < 1e-4
+
+
 @pytest.mark.parametrize("yaw", [0.0, 135.0])
 def test_c2_certified_forward_equals_fp64_decisions(s1m, yaw):
     """The default (certified mixed-precision) forward against the fp64
