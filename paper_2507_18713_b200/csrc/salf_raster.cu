@@ -429,8 +429,14 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
   }
 }
 
-constexpr int kChunk = 64;   // entries staged per step (192 B each in shared memory)
-constexpr int kChunkB = 32;  // backward: + a 32 x 8 x 27 fp32 reduction buffer
+#ifndef SALF_CHUNK
+#define SALF_CHUNK 64
+#endif
+#ifndef SALF_CHUNKB
+#define SALF_CHUNKB 32
+#endif
+constexpr int kChunk = SALF_CHUNK;    // forward: entries staged per step in shared memory
+constexpr int kChunkB = SALF_CHUNKB;  // backward: + a kChunkB x warps x 27 fp32 reduction buffer
 
 template <bool kExactColor, bool kRot>
 __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
