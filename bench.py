@@ -363,6 +363,28 @@ def run_ours(args, world, rank, local):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * 1e3 / float(te.item())
 
+    # ---- the LiDAR half of the metric at N GPUs: each rank sweeps its own
+    # 128 x 1800 C3 LiDAR (sensor-sharded, no exchange), device-timed, max over ranks ----
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.sensors import gen_lidar_rays
+    oc = RY.build_scene_octrees(scene)
+    lid = configs.c3_lidar(position=(0.0137 + 0.5 * rank, -0.0213, 1.3))
+    lb = gen_lidar_rays(lid)
+    for _ in range(max(args.warmup, 3)):
+        RY.render_lidar(ds, oc, lb)
+    barrier()
+    la, lb_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    la.record()
+    for _ in range(args.steps):
+        RY.render_lidar(ds, oc, lb)
+    lb_ev.record()
+    barrier()
+    t_l = torch.tensor([la.elapsed_time(lb_ev) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_l, op=dist.ReduceOp.MAX)
+    lidar_ms = float(t_l.item())
+    del oc
+
     if rank != 0:
         return
 
@@ -420,6 +442,9 @@ def run_ours(args, world, rank, local):
                      "algorithmic_bytes": dom_b, "kernel_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
         "roofline_alu": alu,
+        "lidar": {"metric": "LiDAR rays/s (128-beam, 1800 steps, S1M init)", "rays_per_s": world * lb.n / (lidar_ms * 1e-3),
+                  "sweeps_per_s": world * 1e3 / lidar_ms, "ms_per_sweep": lidar_ms, "n_gpus": world,
+                  "scaling": "weak", "sharding": "one LiDAR sweep per rank, no exchange"},
         "kernels_ms": {k: float(np.mean(v)) for k, v in kms.items()},
         "ncu": _ncu_metrics(),
         "clocks": clk,
