@@ -147,6 +147,19 @@ int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                          const int32_t *entries, const double *saved, const double *d_rgb,
                          const double *d_depth, double *grad, void *stream);
 
+/* Deterministic variant of salf_raster_backward (SPEC.md:531, :541 ordered
+ * reductions; SURVEY §7 hard part 5): one fixed-order 27-row per (tile,
+ * entry) instance into the workspace, instances stable-sorted by voxel, each
+ * voxel's rows summed sequentially in fp64 and added to grad -- bitwise
+ * identical across runs.  n_instances = length of `entries`; workspace of
+ * salf_raster_backward_det_workspace_bytes(n_instances) bytes. */
+size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances);
+int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_camera_t *cam,
+                                       const salf_raster_opts_t *opts, const int64_t *offsets,
+                                       const int32_t *entries, int64_t n_instances, const double *saved,
+                                       const double *d_rgb, const double *d_depth, double *grad,
+                                       void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- sensors (reference sensors.py) ----------------------------------- */
 
 /* gen_camera_rays + apply_rolling_shutter (sensors.py:129-190):

@@ -76,6 +76,9 @@ SIGNATURES = {
                                   C.c_size_t, C.c_int64, vp, vp, vp, vp]),
     "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_backward_det_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "salf_raster_backward_deterministic": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_size_t,
+                                                     vp]),
     "salf_camera_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_lidar_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_octree_build_host": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int64, vp, vp]),

@@ -524,7 +524,8 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
                                                   const int64_t *__restrict__ offsets,
                                                   const int32_t *__restrict__ entries,
                                                   const double *__restrict__ saved, const double *__restrict__ d_rgb,
-                                                  const double *__restrict__ d_depth, double *__restrict__ grad) {
+                                                  const double *__restrict__ d_depth, double *__restrict__ grad,
+                                                  float *__restrict__ partial) {
   __shared__ Entry sm[kChunkB];
   const int tile_id = blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
@@ -611,7 +612,8 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
       const int j = q / kGradStride, k = q - j * kGradStride;
       float sum = 0.0f;
       for (int w = 0; w < nwarps; ++w) sum += red[j][w][k];
-      if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
+      if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode
+      else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
     }
   }
   (void)keep;
@@ -1194,7 +1196,7 @@ template <bool kRot, int NP, bool sdf>
 __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
-    const double *__restrict__ d_depth, double *__restrict__ grad) {
+    const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial) {
   __shared__ EntryF sm[kChunkB];
   __shared__ float red[kChunkB][8 / NP][kGradStride];
 #if SALF_BWD_SMEMRED
@@ -1267,7 +1269,8 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
       const int j = t / kGradStride, k = t - j * kGradStride;
       float sum = 0.0f;
       for (int w = 0; w < nwarps; ++w) sum += red[j][w][k];
-      if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
+      if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
+      else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
     }
   }
 }
@@ -1464,39 +1467,154 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
   SALF_CATCH
 }
 
+static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t *cam,
+                                  const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
+                                  const double *saved, const double *d_rgb, const double *d_depth, double *grad,
+                                  float *partial, cudaStream_t st) {
+  if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
+                                                   camera_kind_repr(cam->kind));
+  if (opts->tile < 1 || opts->tile > 16) return set_error(SALF_EINVAL, "tile size must be in [1, 16]");
+  PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
+  const int n_tiles = c.tiles_x * c.tiles_y;
+  const int threads = ((std::max(32, opts->tile * opts->tile) + 31) / 32) * 32;
+  const int threads_np = ((std::max(32, (opts->tile * opts->tile + SALF_BWD_NP - 1) / SALF_BWD_NP) + 31) / 32) * 32;
+  const bool rot = scene->rot != nullptr;
+  if (opts->exact_color && rot)
+    k_backward<true, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                        grad, partial);
+  else if (opts->exact_color)
+    k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+                                                         grad, partial);
+  else {
+    const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
+#define SALF_LAUNCH_BWD(ROT, SDF)                                                                               \
+  k_backward_fast<ROT, SALF_BWD_NP, SDF><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved, \
+                                                                        d_rgb, d_depth, grad, partial)
+    if (rot) {
+      if (sdf) SALF_LAUNCH_BWD(true, true); else SALF_LAUNCH_BWD(true, false);
+    } else {
+      if (sdf) SALF_LAUNCH_BWD(false, true); else SALF_LAUNCH_BWD(false, false);
+    }
+#undef SALF_LAUNCH_BWD
+  }
+  return check_cuda("salf_raster_backward");
+}
+
 extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                                     const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                     const double *saved, const double *d_rgb, const double *d_depth, double *grad,
                                     void *stream) {
   SALF_TRY {
-    if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
-                                                     camera_kind_repr(cam->kind));
-    if (opts->tile < 1 || opts->tile > 16) return set_error(SALF_EINVAL, "tile size must be in [1, 16]");
-    PinholeDev c = make_pinhole(cam, opts->near, opts->tile);
-    const int n_tiles = c.tiles_x * c.tiles_y;
-    const int threads = ((std::max(32, opts->tile * opts->tile) + 31) / 32) * 32;
-    const int threads_np = ((std::max(32, (opts->tile * opts->tile + SALF_BWD_NP - 1) / SALF_BWD_NP) + 31) / 32) * 32;
+    return raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, nullptr,
+                                  (cudaStream_t)stream);
+  }
+  SALF_CATCH
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic raster backward (SPEC-mandated ordered reduction; SURVEY §7
+// hard part 5): the kernel writes one 27-row per (tile, entry) instance --
+// the CTA's fixed-order sum -- instead of atomics; instances are then
+// stable-sorted by voxel (ties in instance, i.e. tile-major, order) and each
+// voxel's rows are summed sequentially in fp64 by one warp (lane = component)
+// and added to grad.  Bitwise identical across runs.
+
+__global__ void k_iota32(int64_t n, int32_t *__restrict__ v) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = (int32_t)i;
+}
+
+__global__ void k_run_heads(int64_t n, const uint32_t *__restrict__ key, uint8_t *__restrict__ head) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
+}
+
+__global__ void k_det_reduce(int64_t n, const int64_t *__restrict__ n_runs, const int32_t *__restrict__ heads,
+                             const uint32_t *__restrict__ vid, const int32_t *__restrict__ inst,
+                             const float *__restrict__ partial, double *__restrict__ grad) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nr = *n_runs;
+  if (r >= nr || lane >= kGradStride) return;
+  const int64_t p0 = heads[r], p1 = (r + 1 < nr) ? heads[r + 1] : n;
+  double s = 0.0;
+  for (int64_t p = p0; p < p1; ++p) s += (double)partial[(int64_t)inst[p] * kGradStride + lane];
+  double *g = grad + (int64_t)vid[p0] * kGradStride + lane;
+  *g = *g + s;
+}
+
+struct DetWs {
+  float *partial;
+  uint32_t *vid_sorted;
+  int32_t *inst, *inst_sorted, *heads;
+  uint8_t *head_flag;
+  int64_t *n_runs;
+  void *cub_tmp;
+  size_t cub_bytes;
+};
+
+static DetWs carve_det(void *ws, int64_t ni, size_t *total) {
+  DetWs w;
+  size_t off = 0;
+  char *p = (char *)ws;
+  auto take = [&](size_t bytes) { char *q = p ? p + off : nullptr; off += align_up(bytes); return q; };
+  w.partial = (float *)take(sizeof(float) * kGradStride * ni);
+  w.vid_sorted = (uint32_t *)take(sizeof(uint32_t) * ni);
+  w.inst = (int32_t *)take(sizeof(int32_t) * ni);
+  w.inst_sorted = (int32_t *)take(sizeof(int32_t) * ni);
+  w.heads = (int32_t *)take(sizeof(int32_t) * ni);
+  w.head_flag = (uint8_t *)take(ni);
+  w.n_runs = (int64_t *)take(sizeof(int64_t));
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, (int64_t)ni);
+  cub::DeviceSelect::Flagged(nullptr, b, cub::CountingInputIterator<int32_t>(0), (const uint8_t *)nullptr,
+                             (int32_t *)nullptr, (int64_t *)nullptr, (int)ni);
+  w.cub_bytes = std::max(a, b);
+  w.cub_tmp = take(w.cub_bytes);
+  *total = off;
+  return w;
+}
+
+extern "C" size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances) {
+  size_t total = 0;
+  carve_det(nullptr, std::max<int64_t>(n_instances, 1), &total);
+  return total;
+}
+
+extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_camera_t *cam,
+                                                  const salf_raster_opts_t *opts, const int64_t *offsets,
+                                                  const int32_t *entries, int64_t n_instances, const double *saved,
+                                                  const double *d_rgb, const double *d_depth, double *grad,
+                                                  void *workspace, size_t workspace_bytes, void *stream) {
+  SALF_TRY {
+    if (n_instances <= 0) return SALF_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    const bool rot = scene->rot != nullptr;
-    if (opts->exact_color && rot)
-      k_backward<true, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
-                                                          grad);
-    else if (opts->exact_color)
-      k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
-                                                           grad);
-    else {
-      const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
-#define SALF_LAUNCH_BWD(ROT, SDF)                                                                               \
-  k_backward_fast<ROT, SALF_BWD_NP, SDF><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved, \
-                                                                        d_rgb, d_depth, grad)
-      if (rot) {
-        if (sdf) SALF_LAUNCH_BWD(true, true); else SALF_LAUNCH_BWD(true, false);
-      } else {
-        if (sdf) SALF_LAUNCH_BWD(false, true); else SALF_LAUNCH_BWD(false, false);
-      }
-#undef SALF_LAUNCH_BWD
-    }
-    return check_cuda("salf_raster_backward");
+    size_t need = 0;
+    DetWs w = carve_det(workspace, n_instances, &need);
+    if (need > workspace_bytes)
+      return set_error(SALF_EWORKSPACE, "deterministic backward workspace too small: %zu < %zu", workspace_bytes,
+                       need);
+    cudaMemsetAsync(w.partial, 0, sizeof(float) * kGradStride * n_instances, st);
+    const int rc = raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, w.partial,
+                                          st);
+    if (rc != SALF_OK) return rc;
+    const int bs = 256;
+    const unsigned g = (unsigned)((n_instances + bs - 1) / bs);
+    k_iota32<<<g, bs, 0, st>>>(n_instances, w.inst);
+    size_t tb = w.cub_bytes;
+    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, reinterpret_cast<const uint32_t *>(entries), w.vid_sorted, w.inst,
+                                    w.inst_sorted, (int64_t)n_instances, 0,
+                                    bits_for((uint64_t)std::max<int64_t>(scene->n, 1)), st);
+    k_run_heads<<<g, bs, 0, st>>>(n_instances, w.vid_sorted, w.head_flag);
+    tb = w.cub_bytes;
+    cub::DeviceSelect::Flagged(w.cub_tmp, tb, cub::CountingInputIterator<int32_t>(0), w.head_flag, w.heads, w.n_runs,
+                               (int)n_instances, st);
+    const int64_t max_runs = std::min<int64_t>(n_instances, std::max<int64_t>(scene->n, 1));
+    k_det_reduce<<<(unsigned)((max_runs * 32 + bs - 1) / bs), bs, 0, st>>>(n_instances, w.n_runs, w.heads,
+                                                                          w.vid_sorted, w.inst_sorted, w.partial,
+                                                                          grad);
+    return check_cuda("salf_raster_backward_deterministic");
   }
   SALF_CATCH
 }

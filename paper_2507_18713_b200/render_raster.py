@@ -238,14 +238,16 @@ def rasterize_scene(scene: Scene, cam: CameraModel, t_stamp: float = 0.0, *,
 
 
 def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor | None = None,
-                       as_dict: bool = True, events: list | None = None):
+                       as_dict: bool = True, events: list | None = None, deterministic: bool = False):
     """Per-voxel gradients of a rasterized frame.
 
     The reference has no raster backward; the gradient is the one
     `backward_records` (reference backward.py:35-101) assigns to the frame's
     hit pairs taken in tile-list order (DESIGN.md §raster backward).
     d_color (H, W, 3) and d_depth (H, W); returns {param: array} like
-    backward_records' 'static' entry, or the raw (M, 27) f64 buffer."""
+    backward_records' 'static' entry, or the raw (M, 27) f64 buffer.
+    `deterministic=True`: ordered per-voxel reduction instead of atomics,
+    bitwise identical across runs."""
     lib = _lib.load()
     ds = state.scene
     dev = ds.device
@@ -257,10 +259,18 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
     if state.n_instances:
         sc, cs = ds.c_struct(), state.cam.c_struct(rolling=False)
         ev = _timed(events, "raster_backward")
-        _lib.check(lib.salf_raster_backward(_lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts),
-                                            state.offsets.data_ptr(), state.entries.data_ptr(),
-                                            state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
-                                            grad.data_ptr(), _lib.stream_ptr()), "rasterize_backward")
+        if deterministic:
+            wsb = lib.salf_raster_backward_det_workspace_bytes(state.n_instances)
+            ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+            _lib.check(lib.salf_raster_backward_deterministic(
+                _lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts), state.offsets.data_ptr(),
+                state.entries.data_ptr(), state.n_instances, state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
+                grad.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()), "rasterize_backward")
+        else:
+            _lib.check(lib.salf_raster_backward(_lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts),
+                                                state.offsets.data_ptr(), state.entries.data_ptr(),
+                                                state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
+                                                grad.data_ptr(), _lib.stream_ptr()), "rasterize_backward")
         if ev is not None:
             ev[2].record()
     if as_dict:

@@ -367,3 +367,22 @@ def test_c4_fisheye_rolling_shutter_full_size():
     np.testing.assert_array_equal(t0, ref["t0"])
     got = col.reshape(-1, 3).cpu().numpy()[idx]
     assert np.max(np.abs(got - ref["out_color"])) < 1e-4
+
+
+def test_c2_deterministic_backward_full_size(s1m):
+    """C2 at full size: deterministic mode bitwise stable across reruns and
+    within fp32 partial-sum rounding of the atomic mode."""
+    from paper_2507_18713_b200 import configs, render_raster as RR
+    from paper_2507_18713_b200.device import DeviceScene
+    cam = configs.c2_camera()
+    h, w = cam.height, cam.width
+    g = torch.Generator(device="cuda").manual_seed(9)
+    dc = (torch.randint(0, 2, (h, w, 3), device="cuda", generator=g).double() * 2 - 1) / (h * w * 3)
+    dd = torch.zeros((h, w), dtype=torch.float64, device="cuda")
+    fb, st = RR.rasterize(DeviceScene.from_scene(s1m), cam, return_state=True)
+    a = RR.rasterize_backward(st, dc, dd, as_dict=False, deterministic=True)
+    b = RR.rasterize_backward(st, dc, dd, as_dict=False, deterministic=True)
+    assert torch.equal(a, b)
+    c = RR.rasterize_backward(st, dc, dd, as_dict=False)
+    err = ((a - c).abs().max(dim=0).values / c.abs().max(dim=0).values.clamp_min(1e-30)).max()
+    assert float(err) < 1e-6

@@ -347,3 +347,22 @@ def test_dynamic_actors_raster_path(golden, golden_meta, exact):
     g = RR.rasterize_backward(st, golden["actr_dcolor"].reshape(48, 64, 3), np.zeros((48, 64)))
     want = {k: golden["actr_g_" + k] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
     assert grads_close(g, want) < 1e-4
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_raster_backward_deterministic_mode(golden, golden_meta, exact):
+    """Deterministic gradient mode: the
+    reference composition to 1e-4 and bitwise identical across reruns."""
+    from paper_2507_18713_b200 import render_raster as RR
+    cam = _cam(golden_meta["rand300_cam"])
+    fb, st = RR.rasterize(_flat("rand300"), cam, background=(0.05, 0.1, 0.15), return_state=True,
+                          exact_color=exact)
+    h, w = cam.height, cam.width
+    dc, dd = golden["rand300_rbw_dcolor"].reshape(h, w, 3), golden["rand300_rbw_ddepth"].reshape(h, w)
+    runs = [RR.rasterize_backward(st, dc, dd, as_dict=False, deterministic=True) for _ in range(3)]
+    assert all(torch.equal(runs[0], r) for r in runs[1:])
+    want = {k: golden["rand300_rbw_g_" + k] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
+    from paper_2507_18713_b200.device import grads_to_dict
+    assert grads_close(grads_to_dict(runs[0]), want) < 1e-4
+    atomic = RR.rasterize_backward(st, dc, dd, as_dict=False)
+    torch.testing.assert_close(runs[0], atomic, rtol=1e-6, atol=1e-12)
