@@ -160,6 +160,18 @@ int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_cam
                                        const double *d_rgb, const double *d_depth, double *grad,
                                        void *workspace, size_t workspace_bytes, void *stream);
 
+/* Deterministic variant of salf_ray_backward: each included segment's
+ * 27-row goes to slot row_start[ray] + k (row_start: (n + 1) exclusive scan
+ * of the forward's per-ray segment counts, saved[:, 6]), then the ordered
+ * per-voxel reduction of salf_raster_backward_deterministic.  Bitwise
+ * identical across runs.  Workspace: salf_ray_backward_det_workspace_bytes(n_slots). */
+size_t salf_ray_backward_det_workspace_bytes(int64_t n_slots);
+int salf_ray_backward_deterministic(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                    const double *origins, const double *dirs, const uint8_t *valid,
+                                    const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,
+                                    const double *d_depth, double *grad, const int64_t *row_start, int64_t n_slots,
+                                    void *workspace, size_t workspace_bytes, void *stream);
+
 /* ---- sensors (reference sensors.py) ----------------------------------- */
 
 /* gen_camera_rays + apply_rolling_shutter (sensors.py:129-190):

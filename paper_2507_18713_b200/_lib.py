@@ -77,6 +77,9 @@ SIGNATURES = {
     "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_raster_backward_det_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "salf_ray_backward_det_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "salf_ray_backward_deterministic": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64,
+                                                  vp, C.c_size_t, vp]),
     "salf_raster_backward_deterministic": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_size_t,
                                                      vp]),
     "salf_camera_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),

@@ -20,8 +20,10 @@ PARAM_NAMES = ("w_s", "w_c", "w_sh", "log_a", "log_b")
 
 
 def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
-                         grad: torch.Tensor | None = None) -> torch.Tensor:
-    """Accumulate into / return the raw (M, 27) f64 gradient buffer."""
+                         grad: torch.Tensor | None = None, deterministic: bool = False) -> torch.Tensor:
+    """Accumulate into / return the raw (M, 27) f64 gradient buffer.
+    `deterministic=True`: per-segment rows + ordered per-voxel reduction
+    instead of atomics (bitwise identical reruns)."""
     lib = _lib.load()
     ds = records.scene
     dev = ds.device
@@ -32,7 +34,19 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
         grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
     if n and records.ex_rec is not None:
         raise ValueError("records with actor segments: use backward_records")
-    if n:
+    if n and deterministic:
+        sc, t = ds.c_struct(), records.octree.c_struct()
+        start = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        start[1:] = torch.cumsum(records.saved[:, 6].to(torch.int64), 0)
+        slots = int(start[-1].item())
+        wsb = lib.salf_ray_backward_det_workspace_bytes(slots)
+        ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+        _lib.check(lib.salf_ray_backward_deterministic(
+            _lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(), records.dirs.data_ptr(),
+            _lib.ptr(records.valid), _lib.ref(records.opts), records.saved.data_ptr(), dc.data_ptr(),
+            dd.data_ptr(), grad.data_ptr(), start.data_ptr(), slots, ws.data_ptr(), wsb, _lib.stream_ptr()),
+            "backward_records")
+    elif n:
         sc, t = ds.c_struct(), records.octree.c_struct()
         _lib.check(lib.salf_ray_backward(_lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(),
                                          records.dirs.data_ptr(), _lib.ptr(records.valid),

@@ -1529,24 +1529,27 @@ __global__ void k_run_heads(int64_t n, const uint32_t *__restrict__ key, uint8_t
   if (p < n) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
 }
 
+// one warp per run of equal voxel ids; lane k sums component k over the
+// run's rows in order (fp64) and adds it to grad (single writer per voxel);
+// runs with vid >= n_vox (unused row slots) are skipped
 __global__ void k_det_reduce(int64_t n, const int64_t *__restrict__ n_runs, const int32_t *__restrict__ heads,
-                             const uint32_t *__restrict__ vid, const int32_t *__restrict__ inst,
-                             const float *__restrict__ partial, double *__restrict__ grad) {
+                             const uint32_t *__restrict__ vid, const int32_t *__restrict__ row,
+                             const float *__restrict__ rows, int64_t n_vox, double *__restrict__ grad) {
   const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int64_t nr = *n_runs;
   if (r >= nr || lane >= kGradStride) return;
   const int64_t p0 = heads[r], p1 = (r + 1 < nr) ? heads[r + 1] : n;
+  if ((int64_t)vid[p0] >= n_vox) return;
   double s = 0.0;
-  for (int64_t p = p0; p < p1; ++p) s += (double)partial[(int64_t)inst[p] * kGradStride + lane];
+  for (int64_t p = p0; p < p1; ++p) s += (double)rows[(int64_t)row[p] * kGradStride + lane];
   double *g = grad + (int64_t)vid[p0] * kGradStride + lane;
   *g = *g + s;
 }
 
 struct DetWs {
-  float *partial;
   uint32_t *vid_sorted;
-  int32_t *inst, *inst_sorted, *heads;
+  int32_t *row, *row_sorted, *heads;
   uint8_t *head_flag;
   int64_t *n_runs;
   void *cub_tmp;
@@ -1558,10 +1561,9 @@ static DetWs carve_det(void *ws, int64_t ni, size_t *total) {
   size_t off = 0;
   char *p = (char *)ws;
   auto take = [&](size_t bytes) { char *q = p ? p + off : nullptr; off += align_up(bytes); return q; };
-  w.partial = (float *)take(sizeof(float) * kGradStride * ni);
   w.vid_sorted = (uint32_t *)take(sizeof(uint32_t) * ni);
-  w.inst = (int32_t *)take(sizeof(int32_t) * ni);
-  w.inst_sorted = (int32_t *)take(sizeof(int32_t) * ni);
+  w.row = (int32_t *)take(sizeof(int32_t) * ni);
+  w.row_sorted = (int32_t *)take(sizeof(int32_t) * ni);
   w.heads = (int32_t *)take(sizeof(int32_t) * ni);
   w.head_flag = (uint8_t *)take(ni);
   w.n_runs = (int64_t *)take(sizeof(int64_t));
@@ -1576,10 +1578,41 @@ static DetWs carve_det(void *ws, int64_t ni, size_t *total) {
   return w;
 }
 
-extern "C" size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances) {
+size_t salf::det_reduce_workspace_bytes(int64_t n_rows) {
   size_t total = 0;
-  carve_det(nullptr, std::max<int64_t>(n_instances, 1), &total);
+  carve_det(nullptr, std::max<int64_t>(n_rows, 1), &total);
   return total;
+}
+
+// Ordered reduction of 27-rows into grad: rows stable-sorted by voxel id
+// (row order within a voxel), summed sequentially per voxel.  row_vid[i] ==
+// n_vox marks an unused row.
+int salf::det_reduce_rows(int64_t n_rows, const uint32_t *row_vid, const float *rows, int64_t n_vox, double *grad,
+                          void *workspace, size_t workspace_bytes, cudaStream_t st) {
+  if (n_rows <= 0) return SALF_OK;
+  size_t need = 0;
+  DetWs w = carve_det(workspace, n_rows, &need);
+  if (need > workspace_bytes)
+    return set_error(SALF_EWORKSPACE, "deterministic reduction workspace too small: %zu < %zu", workspace_bytes, need);
+  const int bs = 256;
+  const unsigned g = (unsigned)((n_rows + bs - 1) / bs);
+  k_iota32<<<g, bs, 0, st>>>(n_rows, w.row);
+  size_t tb = w.cub_bytes;
+  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, row_vid, w.vid_sorted, w.row, w.row_sorted, (int64_t)n_rows, 0,
+                                  bits_for((uint64_t)std::max<int64_t>(n_vox, 1)), st);
+  k_run_heads<<<g, bs, 0, st>>>(n_rows, w.vid_sorted, w.head_flag);
+  tb = w.cub_bytes;
+  cub::DeviceSelect::Flagged(w.cub_tmp, tb, cub::CountingInputIterator<int32_t>(0), w.head_flag, w.heads, w.n_runs,
+                             (int)n_rows, st);
+  const int64_t max_runs = std::min<int64_t>(n_rows, std::max<int64_t>(n_vox, 1) + 1);
+  k_det_reduce<<<(unsigned)((max_runs * 32 + bs - 1) / bs), bs, 0, st>>>(n_rows, w.n_runs, w.heads, w.vid_sorted,
+                                                                        w.row_sorted, rows, n_vox, grad);
+  return check_cuda("det_reduce_rows");
+}
+
+extern "C" size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances) {
+  const int64_t ni = std::max<int64_t>(n_instances, 1);
+  return align_up(sizeof(float) * kGradStride * ni) + det_reduce_workspace_bytes(ni);
 }
 
 extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_camera_t *cam,
@@ -1590,31 +1623,16 @@ extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, con
   SALF_TRY {
     if (n_instances <= 0) return SALF_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    size_t need = 0;
-    DetWs w = carve_det(workspace, n_instances, &need);
-    if (need > workspace_bytes)
-      return set_error(SALF_EWORKSPACE, "deterministic backward workspace too small: %zu < %zu", workspace_bytes,
-                       need);
-    cudaMemsetAsync(w.partial, 0, sizeof(float) * kGradStride * n_instances, st);
-    const int rc = raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, w.partial,
+    const size_t part = align_up(sizeof(float) * kGradStride * n_instances);
+    if (workspace_bytes < part) return set_error(SALF_EWORKSPACE, "deterministic backward workspace too small");
+    float *partial = (float *)workspace;
+    cudaMemsetAsync(partial, 0, sizeof(float) * kGradStride * n_instances, st);
+    const int rc = raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, partial,
                                           st);
     if (rc != SALF_OK) return rc;
-    const int bs = 256;
-    const unsigned g = (unsigned)((n_instances + bs - 1) / bs);
-    k_iota32<<<g, bs, 0, st>>>(n_instances, w.inst);
-    size_t tb = w.cub_bytes;
-    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, reinterpret_cast<const uint32_t *>(entries), w.vid_sorted, w.inst,
-                                    w.inst_sorted, (int64_t)n_instances, 0,
-                                    bits_for((uint64_t)std::max<int64_t>(scene->n, 1)), st);
-    k_run_heads<<<g, bs, 0, st>>>(n_instances, w.vid_sorted, w.head_flag);
-    tb = w.cub_bytes;
-    cub::DeviceSelect::Flagged(w.cub_tmp, tb, cub::CountingInputIterator<int32_t>(0), w.head_flag, w.heads, w.n_runs,
-                               (int)n_instances, st);
-    const int64_t max_runs = std::min<int64_t>(n_instances, std::max<int64_t>(scene->n, 1));
-    k_det_reduce<<<(unsigned)((max_runs * 32 + bs - 1) / bs), bs, 0, st>>>(n_instances, w.n_runs, w.heads,
-                                                                          w.vid_sorted, w.inst_sorted, w.partial,
-                                                                          grad);
-    return check_cuda("salf_raster_backward_deterministic");
+    // instance rows keyed by their voxel (entries[i])
+    return det_reduce_rows(n_instances, reinterpret_cast<const uint32_t *>(entries), partial, scene->n, grad,
+                           (char *)workspace + part, workspace_bytes - part, st);
   }
   SALF_CATCH
 }

@@ -476,13 +476,22 @@ struct FeatGrad {
   double *feat_grad;    // M x 8 dL/dfeature (accumulated)
 };
 
+// Deterministic mode: each included segment's 27-row goes to its own slot
+// (row_start[ray] + k-th included segment) instead of the atomic scatter;
+// salf::det_reduce_rows then sums the rows per voxel in a fixed order.
+struct RowSink {
+  float *rows;               // (slots, 27) or nullptr (atomic mode)
+  uint32_t *row_vid;         // (slots,) voxel of each used slot (unused: n_vox)
+  const int64_t *row_start;  // (n + 1,) exclusive scan of the forward's segment counts
+};
+
 template <bool kExactColor>
 __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
                                                       const double *__restrict__ orig, const double *__restrict__ dirs,
                                                       const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                       const double *__restrict__ saved, const double *__restrict__ d_rgb,
                                                       const double *__restrict__ d_depth, double *__restrict__ grad,
-                                                      FeatGrad fg) {
+                                                      FeatGrad fg, RowSink sink) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const double keep = 1.0 - opt.stop_threshold;
   bool live = i < n && (valid ? valid[i] != 0 : true);
@@ -517,6 +526,8 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
     }
   }
   int32_t st = 0;
+  int64_t slot = (sink.rows && i < n) ? sink.row_start[i] : 0;
+  const int64_t slot_end = (sink.rows && i < n) ? sink.row_start[i + 1] : 0;
   const bool want_color = dC[0] != 0.0 || dC[1] != 0.0 || dC[2] != 0.0;
   while (__any_sync(0xffffffffu, live)) {
     bool act = false;
@@ -559,7 +570,17 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
       }
       if (!m.active) live = false;
     }
-    scatter_grad(grad, vid, act, g);
+    if (sink.rows) {
+      if (act && slot < slot_end) {
+        float *dst = sink.rows + slot * kGradStride;
+#pragma unroll
+        for (int k = 0; k < kGradStride; ++k) dst[k] = g[k];
+        sink.row_vid[slot] = (uint32_t)vid;
+        ++slot;
+      }
+    } else {
+      scatter_grad(grad, vid, act, g);
+    }
   }
 }
 
@@ -821,11 +842,53 @@ extern "C" int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *
     FeatGrad fg{nullptr, nullptr, nullptr, nullptr};
     if (opts->exact_color)
       k_ray_backward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
-                                                                     d_rgb, d_depth, grad, fg);
+                                                                     d_rgb, d_depth, grad, fg, RowSink{});
     else
       k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
-                                                                      d_rgb, d_depth, grad, fg);
+                                                                      d_rgb, d_depth, grad, fg, RowSink{});
     return check_cuda("salf_ray_backward");
+  }
+  SALF_CATCH
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+__global__ void k_fill_u32(int64_t n, uint32_t v, uint32_t *__restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = v;
+}
+
+extern "C" size_t salf_ray_backward_det_workspace_bytes(int64_t n_slots) {
+  const int64_t ns = std::max<int64_t>(n_slots, 1);
+  return align256(sizeof(float) * kGradStride * ns) + align256(sizeof(uint32_t) * ns) + det_reduce_workspace_bytes(ns);
+}
+
+extern "C" int salf_ray_backward_deterministic(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
+                                               const double *origins, const double *dirs, const uint8_t *valid,
+                                               const salf_raster_opts_t *opts, const double *saved,
+                                               const double *d_rgb, const double *d_depth, double *grad,
+                                               const int64_t *row_start, int64_t n_slots, void *workspace,
+                                               size_t workspace_bytes, void *stream) {
+  SALF_TRY {
+    if (n == 0 || n_slots <= 0) return SALF_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t a = align256(sizeof(float) * kGradStride * n_slots), b = align256(sizeof(uint32_t) * n_slots);
+    if (workspace_bytes < a + b) return set_error(SALF_EWORKSPACE, "deterministic ray backward workspace too small");
+    RowSink sink{(float *)workspace, (uint32_t *)((char *)workspace + a), row_start};
+    k_fill_u32<<<(unsigned)((n_slots + 255) / 256), 256, 0, st>>>(n_slots, (uint32_t)scene->n, sink.row_vid);
+    OctDev t = make_oct(tree);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    FeatGrad fg{nullptr, nullptr, nullptr, nullptr};
+    if (opts->exact_color)
+      k_ray_backward<true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth,
+                                                 grad, fg, sink);
+    else
+      k_ray_backward<false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth,
+                                                  grad, fg, sink);
+    const int rc = check_cuda("salf_ray_backward_deterministic");
+    if (rc != SALF_OK) return rc;
+    return det_reduce_rows(n_slots, sink.row_vid, sink.rows, scene->n, grad, (char *)workspace + a + b,
+                           workspace_bytes - a - b, st);
   }
   SALF_CATCH
 }
@@ -842,7 +905,7 @@ extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t
     // colour is not part of the LiDAR model: no colour seeds (d_rgb = nullptr)
     FeatGrad fg{feat, dF, Facc, feat_grad};
     k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
-                                                                    nullptr, d_depth, grad, fg);
+                                                                    nullptr, d_depth, grad, fg, RowSink{});
     return check_cuda("salf_lidar_backward");
   }
   SALF_CATCH

@@ -386,3 +386,23 @@ def test_c2_deterministic_backward_full_size(s1m):
     c = RR.rasterize_backward(st, dc, dd, as_dict=False)
     err = ((a - c).abs().max(dim=0).values / c.abs().max(dim=0).values.clamp_min(1e-30)).max()
     assert float(err) < 1e-6
+
+
+def test_c3_deterministic_ray_backward_full_size(s1m):
+    """C3 LiDAR sweep at full size (32M segments): deterministic ray backward
+    bitwise stable across reruns and equal to the atomic mode up to order."""
+    from paper_2507_18713_b200 import configs, render_ray as RY
+    from paper_2507_18713_b200.backward import backward_grad_buffer
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.sensors import gen_lidar_rays
+    lb = gen_lidar_rays(configs.c3_lidar())
+    rec = RY.integrate_rays(DeviceScene.from_scene(s1m), RY.build_scene_octrees(s1m), lb.origins, lb.dirs)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    dd = (torch.randint(0, 2, (lb.n,), device="cuda", generator=g).double() * 2 - 1) / lb.n
+    dc = torch.zeros((lb.n, 3), dtype=torch.float64, device="cuda")
+    a = backward_grad_buffer(rec, dc, dd, deterministic=True)
+    b = backward_grad_buffer(rec, dc, dd, deterministic=True)
+    assert torch.equal(a, b)
+    c = backward_grad_buffer(rec, dc, dd)
+    err = ((a - c).abs().max(dim=0).values / c.abs().max(dim=0).values.clamp_min(1e-30)).max()
+    assert float(err) < 1e-6

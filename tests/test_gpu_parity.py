@@ -366,3 +366,23 @@ def test_raster_backward_deterministic_mode(golden, golden_meta, exact):
     assert grads_close(grads_to_dict(runs[0]), want) < 1e-4
     atomic = RR.rasterize_backward(st, dc, dd, as_dict=False)
     torch.testing.assert_close(runs[0], atomic, rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("case", ["integ", "fd"])
+def test_ray_backward_deterministic_mode(golden, case):
+    """Ray-path deterministic gradients: reference values to 1e-4, bitwise
+    identical across reruns, and equal to the atomic mode up to summation order."""
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.backward import backward_grad_buffer
+    from paper_2507_18713_b200.device import grads_to_dict
+    name = {"integ": "rand300i", "fd": "fd10"}[case]
+    bg = (0.2, 0.1, 0.3) if case == "integ" else golden["fd_bg"]
+    sc = load_golden_scene(name)
+    rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), golden[case + "_o"], golden[case + "_d"],
+                            background=bg, exact_color=True)
+    dc, dd = golden[case + "_dcolor"], golden[case + "_ddepth"]
+    runs = [backward_grad_buffer(rec, dc, dd, deterministic=True) for _ in range(3)]
+    assert all(torch.equal(runs[0], r) for r in runs[1:])
+    want = {k: golden[f"{case}_g_{k}"] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
+    assert grads_close(grads_to_dict(runs[0][: sc.static.n]), want) < 1e-4
+    torch.testing.assert_close(runs[0], backward_grad_buffer(rec, dc, dd), rtol=1e-6, atol=1e-12)
