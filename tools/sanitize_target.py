@@ -1,0 +1,38 @@
+"""Small workload for compute-sanitizer: raster fwd+bwd (default, deterministic,
+fp64 modes), ray fwd+bwd, LiDAR, densify, effects on the golden scenes."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tests"))
+import numpy as np
+import torch
+from conftest import load_golden_scene
+from paper_2507_18713_b200 import render_raster as RR, render_ray as RY
+from paper_2507_18713_b200.backward import backward_grad_buffer
+from paper_2507_18713_b200.densify import DensifyConfig, densify_and_prune
+from paper_2507_18713_b200.scene import flatten_scene
+from paper_2507_18713_b200.sensors import CameraModel, look_at_quaternion
+
+sc = load_golden_scene("rand300")
+pos = np.array([13.0, 11.0, 7.0])
+cam = CameraModel(kind="pinhole", width=48, height=40, fx=45.0, fy=45.0, cx=24.0, cy=20.0, position=pos,
+                  quaternion=look_at_quaternion(pos, [4.0, 4.0, 2.0]))
+flat = flatten_scene(sc)
+dc = torch.full((40, 48, 3), 1e-3, device="cuda", dtype=torch.float64)
+dd = torch.full((40, 48), 1e-4, device="cuda", dtype=torch.float64)
+for exact in (False, True):
+    fb, st = RR.rasterize(flat, cam, return_state=True, exact_color=exact)
+    RR.rasterize_backward(st, dc, dd)
+    RR.rasterize_backward(st, dc, dd, deterministic=True)
+oc = RY.build_scene_octrees(sc)
+rng = np.random.default_rng(3)
+o = rng.uniform(-1, 9, (300, 3))
+d = rng.normal(size=(300, 3))
+d /= np.linalg.norm(d, axis=1, keepdims=True)
+rec = RY.integrate_rays(sc, oc, o, d)
+backward_grad_buffer(rec, np.full((300, 3), 1e-3), np.full(300, 1e-3))
+backward_grad_buffer(rec, np.full((300, 3), 1e-3), np.full(300, 1e-3), deterministic=True)
+densify_and_prune(sc.static, rng.random(sc.static.n), DensifyConfig(budget=sc.static.n + 400))
+RY.trace_effects(sc, oc, o, d, 0.0, [RY.InjectedSphere([4, 4, 3], 1.0, "glass")], [0, 0, 1])
+torch.cuda.synchronize()
+print("sanitize target ok")
