@@ -219,20 +219,28 @@ __global__ void k_smooth(int64_t n_pairs, const int64_t *__restrict__ fine, cons
 // selected elements (mask[i / group] != 0, or all when mask is NULL), 0
 // elsewhere; loss_sum += sum |pred - gt| over the selection.
 template <typename G>
-__global__ void k_l1_seed(int64_t n, const float *__restrict__ pred, const G *__restrict__ gt,
-                          const uint8_t *__restrict__ mask, int group, double scale, double *__restrict__ d,
-                          double *__restrict__ loss_sum) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_l1_seed(int64_t n, const float *__restrict__ pred, const G *__restrict__ gt,
+                                                 const uint8_t *__restrict__ mask, int group, double scale,
+                                                 double *__restrict__ d, double *__restrict__ loss_sum) {
+  // grid-stride over elements; the loss is reduced per warp, then per block,
+  // with one fp64 atomic per block (not per warp: a single address)
+  __shared__ double part[8];
   double l = 0.0;
-  if (i < n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const bool sel = mask == nullptr || mask[i / group] != 0;
     const double diff = (double)pred[i] - (double)gt[i];
     d[i] = sel ? __dmul_rn(npsign(diff), scale) : 0.0;
-    l = sel ? fabs(diff) : 0.0;
+    l += sel ? fabs(diff) : 0.0;
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-  if ((threadIdx.x & 31) == 0 && l != 0.0 && loss_sum) atomicAdd(loss_sum, l);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = l;
+  __syncthreads();
+  if (threadIdx.x == 0 && loss_sum) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += part[w];
+    if (t != 0.0) atomicAdd(loss_sum, t);
+  }
 }
 
 }  // namespace salf
@@ -324,7 +332,7 @@ extern "C" int salf_l1_seed(int64_t n, const float *pred, const void *gt, int32_
   SALF_TRY {
     if (n == 0) return SALF_OK;
     if (group < 1) return set_error(SALF_EINVAL, "group must be >= 1");
-    const unsigned g = (unsigned)((n + 255) / 256);
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8);
     if (gt_f64)
       k_l1_seed<double><<<g, 256, 0, (cudaStream_t)stream>>>(n, pred, (const double *)gt, mask, group, scale, d_out,
                                                              loss_sum);
