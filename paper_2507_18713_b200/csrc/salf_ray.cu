@@ -35,7 +35,7 @@ static OctDev make_oct(const salf_octree_t *t) {
   return o;
 }
 
-enum : int32_t { kStatusRoundCap = 1, kStatusOutsideRoot = 2, kStatusOrder = 4 };
+enum : int32_t { kStatusRoundCap = 1, kStatusOutsideRoot = 2, kStatusOrder = 4, kStatusRedo = 8 };
 
 #ifndef SALF_MARCH_INTBITS
 #define SALF_MARCH_INTBITS 1
@@ -369,7 +369,7 @@ struct LidarFeat {
 #endif
 // kLidar: depth-only rays (render_lidar_ranges never reads colour), plus the
 // optional intensity / ray-drop extension.
-template <bool kExactColor, bool kLidar>
+template <bool kExactColor, bool kLidar, bool kRedo = false>
 __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
                                                      const double *__restrict__ orig, const double *__restrict__ dirs,
                                                      const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
                                                      int32_t *__restrict__ status, LidarFeat lf) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (kRedo && !(status[i] & kStatusRedo)) return;  // only the rays the certified pass flagged
   const double keep = 1.0 - opt.stop_threshold;
   double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0, t_run = 1.0, last_t0 = -INFINITY;
   float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -465,6 +466,126 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
     }
   }
   if (status) status[i] = st;
+}
+
+// Certified mixed-precision ray forward (default mode, no LiDAR features).
+// The march (segment list) stays fp64 and bit-exact; per segment only the
+// local coordinates x are fp64 (as shade_od), the fields and opacity are fp32
+// (MUFU exp, cancellation-free expm1), and the transmittance is
+// T = exp(-Y), Y = sum min(sigma delta, ln 1e12) as a compensated fp32 sum with
+// a running bound EY on |Y - Y_exact| (model as in salf_raster.cu: x rounded
+// to fp32, SDF |ds| <= |w_s|_1 (4e-7), MUFU / rounding terms).  The
+// reference's decisions -- inclusion T_before > keep (render_ray.py:97-99),
+// the product early stop (:154-157) and depth validity sum w > 0.5
+// (:111-112) -- are certified outside the band or the ray is flagged
+// (status bit 8) and recomputed by the fp64 kernel (k_ray_forward<.., kRedo>).
+template <bool kLidar, bool kSdf>
+__global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
+    OctDev t, salf_scene_t sc, int64_t n, const double *__restrict__ orig, const double *__restrict__ dirs,
+    const uint8_t *__restrict__ valid, salf_raster_opts_t opt, float *__restrict__ out_rgb,
+    float *__restrict__ out_op, float *__restrict__ out_depth, double *__restrict__ saved,
+    int32_t *__restrict__ status) {
+  constexpr float kU = 5.9604645e-8f;  // 2^-24
+  constexpr float kYClamp = 27.631021115928547f;
+  constexpr double kLn2 = 0.6931471805599453;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double y_stop_d = -log(1.0 - opt.stop_threshold);
+  const float y_stop = (float)y_stop_d, y_stop_err = (float)fabs(y_stop_d - (double)y_stop);
+  float T = 1.f, acc_c[3] = {0.f, 0.f, 0.f}, acc_w = 0.f, acc_wt = 0.f, EY = 0.f, Yh = 0.f, Yc = 0.f;
+  double last_t0 = -INFINITY;
+  int64_t n_seg = 0;
+  int32_t st = 0;
+  bool flag = false;
+  const bool ok = valid ? valid[i] != 0 : true;
+  if (ok) {
+    Marcher m;
+    m.init(t, orig + 3 * i, dirs + 3 * i, INFINITY, t.max_depth);
+    while (m.active) {
+      int64_t vid;
+      double s0, s1;
+      if (!m.step(t, vid, s0, s1, st)) continue;
+      if (s0 < last_t0) st |= kStatusOrder;
+      last_t0 = s0;
+      ++n_seg;
+      // inclusion: T_before > keep  <=>  Y_before < y_stop (certified outside the band)
+      const float Ys = Yh + Yc;
+      const float band = __fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU, Ys, y_stop_err + 1e-9f));
+      if (fabsf(y_stop - Ys) <= band) flag = true;
+      if (!(Ys < y_stop)) break;  // frozen: the reference's march would already have stopped
+      const double tm = __dmul_rn(0.5, __dadd_rn(s0, s1));
+      const float delta = (float)__dsub_rn(s1, s0);
+      const double4 g = ldg_d4(sc.geo + 4 * vid);
+      const double4 ax = ldg_d4(sc.aux + 4 * vid);  // (a, 1/b, 2/edge, 0)
+      const double ctr[3] = {g.x, g.y, g.z};
+      float x[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        x[k] = (float)__dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(tm, m.d[k])), ctr[k]), ax.z);
+      VoxPrm p;
+      load_prm(sc.prm, vid, p);
+      const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
+      const float wn = fabsf(p.ws[0]) + fabsf(p.ws[1]) + fabsf(p.ws[2]) + fabsf(p.ws[3]);
+      const float a = (float)ax.x, inv_b = (float)ax.y;
+      float sigma, rel;
+      if (kSdf) {
+        const float sb = fabsf(s) * inv_b;
+        const float he = 0.5f * a * fast_exp(-sb);
+        sigma = s > 0.f ? a - he : he;
+        rel = __fmaf_rn(wn * 4e-7f, inv_b, __fmaf_rn(3e-7f, sb, 5.4e-7f));
+      } else {
+        sigma = fast_exp(s);
+        rel = __fmaf_rn(wn, 4e-7f, __fmaf_rn(3e-7f, fabsf(s), 5.4e-7f));
+      }
+      const float y = fminf(sigma * delta, kYClamp);
+      const float alpha = y >= kYClamp ? 1.f : -expm1_neg(-y);
+      const float w = T * alpha;
+      if (!kLidar) {
+        float col[3];
+        const float od[3] = {(float)m.d[0], (float)m.d[1], (float)m.d[2]};
+        const float gam[4] = {(float)kShC0, (float)kShC1 * od[1], (float)kShC1 * od[2], (float)kShC1 * od[0]};
+        eval_color32g(p, x, gam, col);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
+      }
+      acc_w += w;
+      acc_wt = __fmaf_rn(w, (float)tm, acc_wt);
+      EY += y * (rel + 2.f * kU);
+      const float Yt = Yh + y;
+      Yc += fabsf(Yh) >= y ? (Yh - Yt) + y : (y - Yt) + Yh;
+      Yh = Yt;
+      T = fast_exp(-(Yh + Yc));
+      // product early stop after this segment: prod(1 - alpha) <= keep  <=>  Y >= y_stop
+      const float Ya = Yh + Yc;
+      if (fabsf(y_stop - Ya) <= __fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU, Ya, y_stop_err + 1e-9f))) flag = true;
+      if (Ya >= y_stop) break;
+    }
+  }
+  const double Y = (double)Yh + (double)Yc;
+  if (ok && fabs(Y - kLn2) <= (double)__fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU, (float)Y, 1e-9f))) flag = true;
+  const bool vdepth = ok && Y > kLn2;  // sum w = 1 - T_final > 0.5
+  if (ok) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (out_rgb) out_rgb[3 * i + k] = __fmaf_rn(T, (float)opt.background[k], acc_c[k]);
+    out_op[i] = 1.f - T;
+    out_depth[i] = vdepth ? acc_wt / acc_w : NAN;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (out_rgb) out_rgb[3 * i + k] = (float)opt.background[k];
+    out_op[i] = 0.0f;
+    out_depth[i] = NAN;
+  }
+  if (saved) {
+    double *sv = saved + i * SALF_SAVED_STRIDE;
+    const double wsum = -expm1(-Y);
+    sv[0] = acc_c[0]; sv[1] = acc_c[1]; sv[2] = acc_c[2];
+    sv[3] = !ok ? 0.0 : (vdepth ? fmax(wsum, 0.5000000001) : fmin(wsum, 0.5));
+    sv[4] = acc_w > 0.f ? (double)acc_wt * (sv[3] / (double)acc_w) : 0.0;  // keeps D = acc_wt / acc_w
+    sv[5] = T; sv[6] = (double)n_seg; sv[7] = 0.0;
+  }
+  if (status) status[i] = st | (flag ? kStatusRedo : 0);
 }
 
 // Ray backward: warp-synchronous re-march (every lane advances one round per
@@ -804,10 +925,19 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
       k_ray_forward<true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
                                                                            out_rgb, out_opacity, out_depth, saved,
                                                                            status, lf);
-    else
-      k_ray_forward<false, false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
-                                                                            out_rgb, out_opacity, out_depth, saved,
-                                                                            status, lf);
+    else {
+      // certified mixed precision, then fp64 recomputation of the flagged rays
+      if (!status) return set_error(SALF_EINVAL, "the mixed-precision ray forward needs a status buffer");
+      cudaStream_t st = (cudaStream_t)stream;
+      if (scene->density_mode == SALF_DENSITY_SDF)
+        k_ray_forward_fast<false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
+                                                              out_opacity, out_depth, saved, status);
+      else
+        k_ray_forward_fast<false, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
+                                                               out_opacity, out_depth, saved, status);
+      k_ray_forward<false, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
+                                                              out_opacity, out_depth, saved, status, lf);
+    }
     return check_cuda("salf_ray_forward");
   }
   SALF_CATCH
@@ -823,9 +953,21 @@ extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t 
     OctDev t = make_oct(tree);
     const unsigned grid = (unsigned)((n + 127) / 128);
     LidarFeat lf{feat, head, out_feat, out_head};
-    k_ray_forward<false, true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts,
-                                                                         nullptr, out_opacity, out_depth, saved,
-                                                                         status, lf);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!feat && status && !opts->exact_color) {
+      // depth-only sweep: certified mixed precision + fp64 redo of flagged rays
+      if (scene->density_mode == SALF_DENSITY_SDF)
+        k_ray_forward_fast<true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
+                                                             out_opacity, out_depth, saved, status);
+      else
+        k_ray_forward_fast<true, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
+                                                              out_opacity, out_depth, saved, status);
+      k_ray_forward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
+                                                             out_opacity, out_depth, saved, status, lf);
+    } else {
+      k_ray_forward<false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
+                                                       out_opacity, out_depth, saved, status, lf);
+    }
     return check_cuda("salf_lidar_forward");
   }
   SALF_CATCH

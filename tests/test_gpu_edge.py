@@ -406,3 +406,31 @@ def test_c3_deterministic_ray_backward_full_size(s1m):
     c = backward_grad_buffer(rec, dc, dd)
     err = ((a - c).abs().max(dim=0).values / c.abs().max(dim=0).values.clamp_min(1e-30)).max()
     assert float(err) < 1e-6
+
+
+@pytest.mark.parametrize("sensor", ["c3_lidar", "c4_fisheye"])
+def test_certified_ray_forward_equals_fp64_decisions(s1m, sensor):
+    """The default (certified mixed-precision) ray forward vs the fp64 one on
+    a full C3 sweep and a full C4-camera frame over S1M: per-ray segment
+    counts (the product early stop) and depth-NaN masks identical, values
+    within fp32 rounding."""
+    from paper_2507_18713_b200 import configs, render_ray as RY
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.sensors import camera_rays, gen_lidar_rays
+    ds = DeviceScene.from_scene(s1m)
+    oc = RY.build_scene_octrees(s1m)
+    if sensor == "c3_lidar":
+        b = gen_lidar_rays(configs.c3_lidar())
+        valid = None
+    else:
+        b = camera_rays(configs.c4_camera())
+        valid = b.valid
+    fa = RY.integrate_rays(ds, oc, b.origins, b.dirs, valid=valid)
+    fe = RY.integrate_rays(ds, oc, b.origins, b.dirs, valid=valid, exact_color=True)
+    assert int(fa.status.max()) == 0 and int(fe.status.max()) == 0
+    assert torch.equal(fa.saved[:, 6], fe.saved[:, 6])
+    assert torch.equal(torch.isnan(fa.depth), torch.isnan(fe.depth))
+    m = ~torch.isnan(fe.depth)
+    assert float(((fa.depth[m] - fe.depth[m]).abs() / fe.depth[m]).max()) < 1e-5
+    assert float((fa.opacity - fe.opacity).abs().max()) < 1e-5
+    assert float((fa.out_color - fe.out_color).abs().max()) < 1e-5

@@ -166,7 +166,11 @@ def test_integrate_rays_matches_reference(golden, exact):
     assert_image_close(_np(rec.out_color), golden["integ_color"])
     assert_image_close(_np(rec.opacity), 1.0 - golden["integ_tfinal"])
     assert_image_close(_np(rec.depth), golden["integ_depth"])
-    np.testing.assert_allclose(_np(rec.weight_sum), golden["integ_wsum"], rtol=1e-12, atol=1e-13)
+    # exact mode: the fp64 reference-order sums; default mode: 1 - exp(-Y) from the certified fp32 Y
+    tol = dict(rtol=1e-12, atol=1e-13) if exact else dict(rtol=0, atol=2e-6)
+    np.testing.assert_allclose(_np(rec.weight_sum), golden["integ_wsum"], **tol)
+    if not exact:  # every reference decision certified: depth-NaN mask and the 0.5 threshold identical
+        np.testing.assert_array_equal(_np(rec.weight_sum) > 0.5, golden["integ_wsum"] > 0.5)
     # early-stopped hit list (ray, vid, t0) bit-exact
     ray, vid, t0, t1 = (x.cpu().numpy() for x in RY.segments(sc, RY.build_scene_octrees(sc),
                                                                 golden["integ_o"], golden["integ_d"]))
