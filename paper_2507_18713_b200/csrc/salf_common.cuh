@@ -280,6 +280,66 @@ __device__ __forceinline__ void segment_grad(int mode, double delta, double sigm
   for (int k = kGradStride; k < 32; ++k) g[k] = 0.0f;
 }
 
+// Mixed-precision gradient of one included segment (backward.py:52-100)
+// from fp32 fields: x (local coordinates), delta, dq = t_mid - D; the running
+// transmittance T (fp32, advanced here) and the fp64 prefix sum of A w (the
+// suffix is total - prefix).  Writes the 27 components into g (g[27..31] = 0).
+template <bool kSdf>
+__device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv_b, const float x[3], float delta,
+                                             float dq, const float gam[4], bool want_color, const float dC[3],
+                                             float dws, double total, float tail, float &T, double &prefix,
+                                             float g[32]) {
+  const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
+  const float ha = 0.5f * a;
+  float ee = 0.f, sigma;
+  if (kSdf) {
+    ee = fast_exp(-fabsf(s) * inv_b);
+    const float he = ha * ee;
+    sigma = s > 0.f ? a - he : he;
+  } else {
+    sigma = fast_exp(s);
+  }
+  const float y = sigma * delta;
+  const float om = fast_exp(-y);
+  const bool clamped = y > 27.631021115928547f;
+  const float alpha = clamped ? 1.f : -expm1_neg(-y);
+  const float omc = clamped ? 1e-12f : om;
+  float col[3] = {0.f, 0.f, 0.f};
+  if (want_color) eval_color32g(p, x, gam, col);
+  const float w = T * alpha;
+  const float A = __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], __fmaf_rn(dC[0], col[0], dws * dq)));
+  prefix += (double)(A * w);
+  const float suffix = (float)(total - prefix);
+  const float g_alpha = __fmaf_rn(A, T, -(suffix + tail) * fast_rcp(omc));
+  const float g_sigma = g_alpha * delta * om;
+  float ds, ga, gb;
+  if (kSdf) {
+    const float k2e = ha * inv_b * ee;
+    ds = (s == 0.f) ? 0.f : g_sigma * k2e;
+    ga = g_sigma * sigma;
+    gb = -g_sigma * k2e * s;
+  } else {
+    ds = g_sigma * sigma;
+    ga = 0.f;
+    gb = 0.f;
+  }
+  g[0] = ds * x[0]; g[1] = ds * x[1]; g[2] = ds * x[2]; g[3] = ds;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float wc = w * col[i];
+    const float gz = dC[i] * __fmaf_rn(-wc, col[i], wc);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = gz * x[k];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g[13 + 4 * i + k] = gz * gam[k];
+  }
+  g[25] = ga;
+  g[26] = gb;
+#pragma unroll
+  for (int k = kGradStride; k < 32; ++k) g[k] = 0.f;
+  T = T * omc;
+}
+
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes
 // of a converged warp.  Lanes holding the same voxel id form a group
 // (__match_any_sync).  Lanes in groups of fewer than 4 add their non-zero

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
   double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0, t_run = 1.0, last_t0 = -INFINITY;
   float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   const bool feat = kLidar && lf.feat != nullptr;
-  int64_t n_seg = 0;
+  int64_t n_seg = 0, n_inc = 0;
   int32_t st = 0;
   const bool ok = valid ? valid[i] != 0 : true;
   if (ok) {
@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
           T = __dmul_rn(T, sv.om);
+          ++n_inc;
         } else {
           frozen = true;
         }
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
   if (saved) {
     double *s = saved + i * SALF_SAVED_STRIDE;
     s[0] = acc_c[0]; s[1] = acc_c[1]; s[2] = acc_c[2];
-    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_seg; s[7] = 0.0;
+    s[3] = acc_w; s[4] = acc_wt; s[5] = T; s[6] = (double)n_seg; s[7] = (double)n_inc;
   }
   if (feat) {
     // linear head on [blended feature, expected depth (0 if none), view dir] + sigmoid
@@ -494,7 +495,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
   const float y_stop = (float)y_stop_d, y_stop_err = (float)fabs(y_stop_d - (double)y_stop);
   float T = 1.f, acc_c[3] = {0.f, 0.f, 0.f}, acc_w = 0.f, acc_wt = 0.f, EY = 0.f, Yh = 0.f, Yc = 0.f;
   double last_t0 = -INFINITY;
-  int64_t n_seg = 0;
+  int64_t n_seg = 0, n_inc = 0;
   int32_t st = 0;
   bool flag = false;
   const bool ok = valid ? valid[i] != 0 : true;
@@ -555,6 +556,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
       Yc += fabsf(Yh) >= y ? (Yh - Yt) + y : (y - Yt) + Yh;
       Yh = Yt;
       T = fast_exp(-(Yh + Yc));
+      ++n_inc;
       // product early stop after this segment: prod(1 - alpha) <= keep  <=>  Y >= y_stop
       const float Ya = Yh + Yc;
       if (fabsf(y_stop - Ya) <= __fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU, Ya, y_stop_err + 1e-9f))) flag = true;
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
     sv[0] = acc_c[0]; sv[1] = acc_c[1]; sv[2] = acc_c[2];
     sv[3] = !ok ? 0.0 : (vdepth ? fmax(wsum, 0.5000000001) : fmin(wsum, 0.5));
     sv[4] = acc_w > 0.f ? (double)acc_wt * (sv[3] / (double)acc_w) : 0.0;  // keeps D = acc_wt / acc_w
-    sv[5] = T; sv[6] = (double)n_seg; sv[7] = 0.0;
+    sv[5] = T; sv[6] = (double)n_seg; sv[7] = (double)n_inc;
   }
   if (status) status[i] = st | (flag ? kStatusRedo : 0);
 }
@@ -606,7 +608,11 @@ struct RowSink {
   const int64_t *row_start;  // (n + 1,) exclusive scan of the forward's segment counts
 };
 
-template <bool kExactColor>
+// kMixed (default mode, no LiDAR features): inclusion is the forward's
+// included-segment count saved[:, 7] (the certified forward's decisions equal
+// the fp64 ones), the march stays fp64 and bit-exact, and the segment fields
+// and gradient chain are fp32 (seg_grad_f32); kSdf selects the density.
+template <bool kExactColor, bool kMixed = false, bool kSdf = true>
 __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
                                                       const double *__restrict__ orig, const double *__restrict__ dirs,
                                                       const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
@@ -646,6 +652,19 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
       }
     }
   }
+  int64_t n_inc = 0, n_done = 0;
+  float Tf = 1.f;
+  float dCf[3] = {(float)dC[0], (float)dC[1], (float)dC[2]};
+  const float dwsf = (float)(dd / ws), tailf = (float)tail;
+  float gam[4] = {0.f, 0.f, 0.f, 0.f};
+  if (kMixed && live) {
+    n_inc = (int64_t)saved[i * SALF_SAVED_STRIDE + 7];
+    if (n_inc == 0) live = false;
+    gam[0] = (float)kShC0;
+    gam[1] = (float)(kShC1 * m.d[1]);
+    gam[2] = (float)(kShC1 * m.d[2]);
+    gam[3] = (float)(kShC1 * m.d[0]);
+  }
   int32_t st = 0;
   int64_t slot = (sink.rows && i < n) ? sink.row_start[i] : 0;
   const int64_t slot_end = (sink.rows && i < n) ? sink.row_start[i + 1] : 0;
@@ -656,7 +675,25 @@ __global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc,
     float g[32];
     if (live) {
       double s0, s1;
-      if (m.step(t, vid, s0, s1, st)) {
+      if (kMixed) {
+        if (m.step(t, vid, s0, s1, st)) {
+          // fp64: t_mid, delta, local coordinates (shade_od); fp32 after
+          const double tm = __dmul_rn(0.5, __dadd_rn(s0, s1));
+          const double4 gg = ldg_d4(sc.geo + 4 * vid);
+          const double4 ax = ldg_d4(sc.aux + 4 * vid);
+          const double ctr[3] = {gg.x, gg.y, gg.z};
+          float x[3];
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            x[k] = (float)__dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(tm, m.d[k])), ctr[k]), ax.z);
+          VoxPrm p;
+          load_prm(sc.prm, vid, p);
+          seg_grad_f32<kSdf>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), (float)__dsub_rn(tm, D),
+                             gam, want_color, dCf, dwsf, total, tailf, Tf, prefix, g);
+          act = true;
+          if (++n_done >= n_inc) live = false;
+        }
+      } else if (m.step(t, vid, s0, s1, st)) {
         RaySeg sv;
         sv.c[0] = sv.c[1] = sv.c[2] = 0.0;  // depth-only rays (LiDAR): no colour term
         shade_seg<kExactColor>(sc, m, vid, s0, s1, sv, want_color);
@@ -985,9 +1022,12 @@ extern "C" int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *
     if (opts->exact_color)
       k_ray_backward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
                                                                      d_rgb, d_depth, grad, fg, RowSink{});
+    else if (scene->density_mode == SALF_DENSITY_SDF)
+      k_ray_backward<false, true, true><<<grid, 128, 0, (cudaStream_t)stream>>>(
+          t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth, grad, fg, RowSink{});
     else
-      k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
-                                                                      d_rgb, d_depth, grad, fg, RowSink{});
+      k_ray_backward<false, true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(
+          t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth, grad, fg, RowSink{});
     return check_cuda("salf_ray_backward");
   }
   SALF_CATCH
@@ -1024,9 +1064,12 @@ extern "C" int salf_ray_backward_deterministic(const salf_octree_t *tree, const 
     if (opts->exact_color)
       k_ray_backward<true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth,
                                                  grad, fg, sink);
+    else if (scene->density_mode == SALF_DENSITY_SDF)
+      k_ray_backward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb,
+                                                              d_depth, grad, fg, sink);
     else
-      k_ray_backward<false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth,
-                                                  grad, fg, sink);
+      k_ray_backward<false, true, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb,
+                                                               d_depth, grad, fg, sink);
     const int rc = check_cuda("salf_ray_backward_deterministic");
     if (rc != SALF_OK) return rc;
     return det_reduce_rows(n_slots, sink.row_vid, sink.rows, scene->n, grad, (char *)workspace + a + b,
@@ -1046,8 +1089,15 @@ extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t
     const unsigned grid = (unsigned)((n + 127) / 128);
     // colour is not part of the LiDAR model: no colour seeds (d_rgb = nullptr)
     FeatGrad fg{feat, dF, Facc, feat_grad};
-    k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
-                                                                    nullptr, d_depth, grad, fg, RowSink{});
+    if (feat || opts->exact_color)  // the feature chain stays fp64
+      k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
+                                                                      nullptr, d_depth, grad, fg, RowSink{});
+    else if (scene->density_mode == SALF_DENSITY_SDF)
+      k_ray_backward<false, true, true><<<grid, 128, 0, (cudaStream_t)stream>>>(
+          t, *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg, RowSink{});
+    else
+      k_ray_backward<false, true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(
+          t, *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg, RowSink{});
     return check_cuda("salf_lidar_backward");
   }
   SALF_CATCH

@@ -180,15 +180,16 @@ def test_integrate_rays_matches_reference(golden, exact):
     np.testing.assert_array_equal(t1, golden["integ_t1"])
 
 
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
 @pytest.mark.parametrize("case", ["integ", "fd"])
-def test_ray_backward_matches_reference(golden, case):
+def test_ray_backward_matches_reference(golden, case, exact):
     from paper_2507_18713_b200 import render_ray as RY
     from paper_2507_18713_b200.backward import backward_records
     name = {"integ": "rand300i", "fd": "fd10"}[case]
     bg = (0.2, 0.1, 0.3) if case == "integ" else golden["fd_bg"]
     sc = load_golden_scene(name)
     rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), golden[case + "_o"], golden[case + "_d"],
-                            background=bg, exact_color=True)
+                            background=bg, exact_color=exact)
     g = backward_records(rec, sc, golden[case + "_dcolor"], golden[case + "_ddepth"])["static"]
     want = {k: golden[f"{case}_g_{k}"] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
     assert grads_close(g, want) < 1e-4
