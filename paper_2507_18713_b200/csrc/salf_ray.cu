@@ -485,7 +485,9 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
     OctDev t, salf_scene_t sc, int64_t n, const double *__restrict__ orig, const double *__restrict__ dirs,
     const uint8_t *__restrict__ valid, salf_raster_opts_t opt, float *__restrict__ out_rgb,
     float *__restrict__ out_op, float *__restrict__ out_depth, double *__restrict__ saved,
-    int32_t *__restrict__ status) {
+    int32_t *__restrict__ status, LidarFeat lf) {
+  float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const bool feat = kLidar && lf.feat != nullptr;
   constexpr float kU = 5.9604645e-8f;  // 2^-24
   constexpr float kYClamp = 27.631021115928547f;
   constexpr double kLn2 = 0.6931471805599453;
@@ -549,6 +551,14 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
       }
+      if (feat) {  // intensity / ray-drop extension: blended 8-channel feature
+        const float4 f0 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid);
+        const float4 f1 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid + 1);
+        acc_f[0] = fmaf(w, f0.x, acc_f[0]); acc_f[1] = fmaf(w, f0.y, acc_f[1]);
+        acc_f[2] = fmaf(w, f0.z, acc_f[2]); acc_f[3] = fmaf(w, f0.w, acc_f[3]);
+        acc_f[4] = fmaf(w, f1.x, acc_f[4]); acc_f[5] = fmaf(w, f1.y, acc_f[5]);
+        acc_f[6] = fmaf(w, f1.z, acc_f[6]); acc_f[7] = fmaf(w, f1.w, acc_f[7]);
+      }
       acc_w += w;
       acc_wt = __fmaf_rn(w, (float)tm, acc_wt);
       EY += y * (rel + 2.f * kU);
@@ -586,6 +596,25 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
     sv[3] = !ok ? 0.0 : (vdepth ? fmax(wsum, 0.5000000001) : fmin(wsum, 0.5));
     sv[4] = acc_w > 0.f ? (double)acc_wt * (sv[3] / (double)acc_w) : 0.0;  // keeps D = acc_wt / acc_w
     sv[5] = T; sv[6] = (double)n_seg; sv[7] = (double)n_inc;
+  }
+  if (feat) {
+    // linear head on [blended feature, expected depth (0 if none), view dir] + sigmoid (as k_ray_forward)
+    const float dep = vdepth ? acc_wt / acc_w : 0.0f;
+    const float dv[3] = {(float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float *W = lf.head + 13 * j;
+      float z = W[12];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) z = fmaf(W[k], acc_f[k], z);
+      z = fmaf(W[8], dep, z);
+      z = fmaf(W[9], dv[0], fmaf(W[10], dv[1], fmaf(W[11], dv[2], z)));
+      lf.out_head[2 * i + j] = 1.0f / (1.0f + expf(-z));
+    }
+    if (lf.out_feat) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lf.out_feat[8 * i + k] = acc_f[k];
+    }
   }
   if (status) status[i] = st | (flag ? kStatusRedo : 0);
 }
@@ -968,10 +997,10 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
       cudaStream_t st = (cudaStream_t)stream;
       if (scene->density_mode == SALF_DENSITY_SDF)
         k_ray_forward_fast<false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
-                                                              out_opacity, out_depth, saved, status);
+                                                              out_opacity, out_depth, saved, status, lf);
       else
         k_ray_forward_fast<false, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
-                                                               out_opacity, out_depth, saved, status);
+                                                               out_opacity, out_depth, saved, status, lf);
       k_ray_forward<false, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
                                                               out_opacity, out_depth, saved, status, lf);
     }
@@ -991,14 +1020,14 @@ extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t 
     const unsigned grid = (unsigned)((n + 127) / 128);
     LidarFeat lf{feat, head, out_feat, out_head};
     cudaStream_t st = (cudaStream_t)stream;
-    if (!feat && status && !opts->exact_color) {
-      // depth-only sweep: certified mixed precision + fp64 redo of flagged rays
+    if (status && !opts->exact_color) {
+      // certified mixed precision + fp64 redo of flagged rays (features blended in fp32 either way)
       if (scene->density_mode == SALF_DENSITY_SDF)
         k_ray_forward_fast<true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
-                                                             out_opacity, out_depth, saved, status);
+                                                             out_opacity, out_depth, saved, status, lf);
       else
         k_ray_forward_fast<true, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
-                                                              out_opacity, out_depth, saved, status);
+                                                              out_opacity, out_depth, saved, status, lf);
       k_ray_forward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
                                                              out_opacity, out_depth, saved, status, lf);
     } else {
