@@ -434,3 +434,48 @@ def test_certified_ray_forward_equals_fp64_decisions(s1m, sensor):
     assert float(((fa.depth[m] - fe.depth[m]).abs() / fe.depth[m]).max()) < 1e-5
     assert float((fa.opacity - fe.opacity).abs().max()) < 1e-5
     assert float((fa.out_color - fe.out_color).abs().max()) < 1e-5
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_certified_forward_stress_sharp_fields(seed):
+    """Stress for the certified forward's error model: random multi-level
+    scenes with sharp SDF transfers (b down to 4e-4), large |W_s| and dense
+    opacity, viewed from several poses; raster and ray path decisions (stop
+    index / segment counts, depth-NaN masks) must equal the fp64 path's."""
+    from paper_2507_18713_b200 import render_raster as RR, render_ray as RY
+    from paper_2507_18713_b200.scene import Scene, SceneBounds, SparseVoxelSet, flatten_scene
+    from paper_2507_18713_b200.scenes import f32_roundtrip
+    rng = np.random.default_rng(100 + seed)
+    b = SceneBounds(np.zeros(3), np.full(3, 8.0), 1.0, 4)
+    # at most one voxel per level-0 cell (levels 0..2), so no voxel contains another
+    taken, L, C = set(), [], []
+    for lv in (2, 1, 0):
+        for ijk in np.unique(rng.integers(0, 8 * 2 ** lv, (250, 3)), axis=0):
+            key0 = tuple(int(q) >> lv for q in ijk)
+            if key0 not in taken:
+                taken.add(key0)
+                L.append(lv)
+                C.append(ijk)
+    n = len(L)
+    v = SparseVoxelSet(b, 10 * n)
+    ws = rng.normal(scale=3.0, size=(n, 4))
+    v.set_arrays(np.array(L), np.array(C), ws, rng.normal(size=(n, 3, 3)), rng.normal(scale=0.5, size=(n, 3, 4)),
+                 np.log(rng.uniform(5.0, 400.0, n)), np.log(rng.uniform(4e-4, 0.2, n)))
+    sc = f32_roundtrip(Scene(bounds=b, static=v))
+    flat = flatten_scene(sc)
+    oc = RY.build_scene_octrees(sc)
+    for k in range(3):
+        pos = rng.uniform(-3.0, 11.0, 3) + 0.0137
+        cam = _cam(pos=pos, w=96, h=80, f=70.0, target=rng.uniform(2.0, 6.0, 3))
+        fa, sa = RR.rasterize(flat, cam, return_state=True)
+        fe, se = RR.rasterize(flat, cam, return_state=True, exact_color=True)
+        assert torch.equal(sa.saved[:, 6], se.saved[:, 6])
+        assert torch.equal(torch.isnan(fa.depth), torch.isnan(fe.depth))
+        assert float((fa.color - fe.color).abs().max()) < 1e-4
+        o = np.tile(pos, (4000, 1))
+        d = rng.normal(size=(4000, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        ra = RY.integrate_rays(sc, oc, o, d)
+        re = RY.integrate_rays(sc, oc, o, d, exact_color=True)
+        assert torch.equal(ra.saved[:, 6], re.saved[:, 6]) and torch.equal(ra.saved[:, 7], re.saved[:, 7])
+        assert torch.equal(torch.isnan(ra.depth), torch.isnan(re.depth))
