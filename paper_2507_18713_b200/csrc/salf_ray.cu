@@ -480,8 +480,11 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
 // the product early stop (:154-157) and depth validity sum w > 0.5
 // (:111-112) -- are certified outside the band or the ray is flagged
 // (status bit 8) and recomputed by the fp64 kernel (k_ray_forward<.., kRedo>).
+#ifndef SALF_RAYF_MINB_CAM
+#define SALF_RAYF_MINB_CAM 6  // camera rays (colour): measured best (C4 10.9 -> 9.7 ms)
+#endif
 template <bool kLidar, bool kSdf>
-__global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward_fast(
+__global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_CAM) k_ray_forward_fast(
     OctDev t, salf_scene_t sc, int64_t n, const double *__restrict__ orig, const double *__restrict__ dirs,
     const uint8_t *__restrict__ valid, salf_raster_opts_t opt, float *__restrict__ out_rgb,
     float *__restrict__ out_op, float *__restrict__ out_depth, double *__restrict__ saved,
