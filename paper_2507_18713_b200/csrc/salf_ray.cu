@@ -644,8 +644,11 @@ struct RowSink {
 // included-segment count saved[:, 7] (the certified forward's decisions equal
 // the fp64 ones), the march stays fp64 and bit-exact, and the segment fields
 // and gradient chain are fp32 (seg_grad_f32); kSdf selects the density.
+#ifndef SALF_RAYB_MINB
+#define SALF_RAYB_MINB 4  // 128 registers: measured best (5, 6 spill)
+#endif
 template <bool kExactColor, bool kMixed = false, bool kSdf = true>
-__global__ void __launch_bounds__(128) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
+__global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
                                                       const double *__restrict__ orig, const double *__restrict__ dirs,
                                                       const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                       const double *__restrict__ saved, const double *__restrict__ d_rgb,
