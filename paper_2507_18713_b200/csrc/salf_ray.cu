@@ -1007,8 +1007,10 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
       else
         k_ray_forward_fast<false, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
                                                                out_opacity, out_depth, saved, status, lf);
-      k_ray_forward<false, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
-                                                              out_opacity, out_depth, saved, status, lf);
+      static const bool no_redo = getenv("SALF_NO_REDO") && getenv("SALF_NO_REDO")[0] == '1';  // diagnostics
+      if (!no_redo)
+        k_ray_forward<false, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
+                                                                out_opacity, out_depth, saved, status, lf);
     }
     return check_cuda("salf_ray_forward");
   }
@@ -1034,8 +1036,10 @@ extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t 
       else
         k_ray_forward_fast<true, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
                                                               out_opacity, out_depth, saved, status, lf);
-      k_ray_forward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
-                                                             out_opacity, out_depth, saved, status, lf);
+      static const bool no_redo = getenv("SALF_NO_REDO") && getenv("SALF_NO_REDO")[0] == '1';  // diagnostics
+      if (!no_redo)
+        k_ray_forward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
+                                                               out_opacity, out_depth, saved, status, lf);
     } else {
       k_ray_forward<false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
                                                        out_opacity, out_depth, saved, status, lf);
