@@ -479,3 +479,32 @@ def test_certified_forward_stress_sharp_fields(seed):
         re = RY.integrate_rays(sc, oc, o, d, exact_color=True)
         assert torch.equal(ra.saved[:, 6], re.saved[:, 6]) and torch.equal(ra.saved[:, 7], re.saved[:, 7])
         assert torch.equal(torch.isnan(ra.depth), torch.isnan(re.depth))
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_ray_path_raw_density(exact):
+    """Raw density mode (scene.py:250-252) through the ray path: forward and
+    backward against the oracle (integrate_rays + backward_records)."""
+    import dataclasses
+    from conftest import grads_close
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.backward import backward_records
+    rng = np.random.default_rng(21)
+    cells = np.unique(rng.integers(0, 8, (150, 3)), axis=0)
+    sc = dataclasses.replace(_scene([0, 0, 0], [4, 4, 4], 0.5, 2, cells, a=3.0, seed=21), density_mode="raw")
+    o = rng.uniform(-1, 5, (600, 3)) + 0.0137
+    d = rng.normal(size=(600, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rec = RY.integrate_rays(sc, RY.build_scene_octrees(sc), o, d, background=(0.1, 0.2, 0.3), exact_color=exact)
+    vox = oracle_voxels(sc)
+    ref = O.integrate_rays(vox, O.build_octree(vox), o, d, background=(0.1, 0.2, 0.3))
+    np.testing.assert_allclose(rec.out_color.cpu().numpy(), ref["out_color"], atol=1e-5)
+    got_d, want_d = rec.depth.cpu().numpy(), ref["depth"]
+    np.testing.assert_array_equal(np.isnan(got_d), np.isnan(want_d))
+    m = ~np.isnan(want_d)
+    np.testing.assert_allclose(got_d[m], want_d[m], rtol=1e-5)
+    dc = rng.normal(size=(600, 3)) * 1e-2
+    dd = rng.normal(size=600) * 1e-3
+    g = backward_records(rec, sc, dc, dd)["static"]
+    want = O.backward_records(ref, vox, dc, dd)
+    assert grads_close(g, want) < 1e-4

@@ -120,6 +120,26 @@ def test_tile_size_is_scheduling_only(golden_meta):
     assert torch.equal(torch.nan_to_num(a.depth, 7.0), torch.nan_to_num(b.depth, 7.0))
 
 
+@pytest.mark.parametrize("tile", [1, 5, 8, 13])
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_tile_size_scheduling_backward(golden, golden_meta, tile, exact):
+    """The tile size only schedules work: frames and gradients for tile sizes
+    1..16 (incl. non-divisors of the image) agree with tile 16 (gradients up
+    to fp32 partial-sum order)."""
+    from paper_2507_18713_b200 import render_raster as RR
+    cam = _cam(golden_meta["rand300_cam"])
+    flat = _flat("rand300")
+    h, w = cam.height, cam.width
+    dc, dd = golden["rand300_rbw_dcolor"].reshape(h, w, 3), golden["rand300_rbw_ddepth"].reshape(h, w)
+    fa, sa = RR.rasterize(flat, cam, tile=16, return_state=True, exact_color=exact)
+    fb, sb = RR.rasterize(flat, cam, tile=tile, return_state=True, exact_color=exact)
+    assert torch.equal(fa.color, fb.color) and torch.equal(fa.opacity, fb.opacity)
+    ga = RR.rasterize_backward(sa, dc, dd, as_dict=False)
+    gb = RR.rasterize_backward(sb, dc, dd, as_dict=False)
+    err = ((ga - gb).abs().max(dim=0).values / ga.abs().max(dim=0).values.clamp_min(1e-30)).max()
+    assert float(err) < 1e-5
+
+
 @pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
 def test_raster_backward_matches_reference_composition(golden, golden_meta, exact):
     """exact: the fp64 backward; mixed: the default fp64-geometry / fp32-field backward."""
