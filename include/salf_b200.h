@@ -109,10 +109,14 @@ int salf_device_sm_count(void);
  * cull_and_bin (:143-176): rect (M x 4: umin, vmin, umax, vmax; NaN if
  * culled), z_center, culled, the reference tile span `span_ref` and the
  * tightened render span `span_fit` (M x 4 int32: tx0, ty0, tx1, ty1; empty
- * when tx0 > tx1), and 64-bit orderable depth keys. */
+ * when tx0 > tx1), 64-bit orderable depth keys, and `vrange` (M int32:
+ * conservative footprint pixel rows lo | hi << 16, widened by one pixel;
+ * lo > hi when empty) that the composite / backward use to skip entries a
+ * warp's pixel rows cannot hit.  Any output may be NULL. */
 int salf_project_voxels(const salf_scene_t *scene, const salf_camera_t *cam, double near,
                         int32_t tile, double *rect, double *z_center, uint8_t *culled,
-                        int32_t *span_ref, int32_t *span_fit, uint64_t *zkey, void *stream);
+                        int32_t *span_ref, int32_t *span_fit, uint64_t *zkey, int32_t *vrange,
+                        void *stream);
 
 /* Workspace for salf_raster_bin given M voxels and an instance capacity. */
 size_t salf_raster_bin_workspace_bytes(int64_t n_voxels, int64_t capacity, int32_t n_tiles);
@@ -137,7 +141,7 @@ int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double 
 int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                           const salf_raster_opts_t *opts, const int64_t *offsets,
                           const int32_t *entries, float *out_rgb, float *out_opacity,
-                          float *out_depth, double *saved, void *stream);
+                          float *out_depth, double *saved, const int32_t *vrange, void *stream);
 
 /* Raster backward (no reference function: defined as backward_records,
  * backward.py:35-101, applied to the raster pairs -- see DESIGN.md).
@@ -145,7 +149,7 @@ int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
 int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                          const salf_raster_opts_t *opts, const int64_t *offsets,
                          const int32_t *entries, const double *saved, const double *d_rgb,
-                         const double *d_depth, double *grad, void *stream);
+                         const double *d_depth, double *grad, const int32_t *vrange, void *stream);
 
 /* Deterministic variant of salf_raster_backward (SPEC.md:531, :541 ordered
  * reductions; SURVEY §7 hard part 5): one fixed-order 27-row per (tile,
@@ -158,7 +162,8 @@ int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_cam
                                        const salf_raster_opts_t *opts, const int64_t *offsets,
                                        const int32_t *entries, int64_t n_instances, const double *saved,
                                        const double *d_rgb, const double *d_depth, double *grad,
-                                       void *workspace, size_t workspace_bytes, void *stream);
+                                       const int32_t *vrange, void *workspace, size_t workspace_bytes,
+                                       void *stream);
 
 /* Deterministic variant of salf_ray_backward: each included segment's
  * 27-row goes to slot row_start[ray] + k (row_start: (n + 1) exclusive scan

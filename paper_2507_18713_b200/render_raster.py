@@ -63,6 +63,7 @@ class RasterState:
     entries: torch.Tensor
     saved: torch.Tensor
     n_instances: int
+    vrange: torch.Tensor | None = None  # per-voxel footprint rows (entry culling per warp)
 
 
 def _timed(events, name):
@@ -107,6 +108,7 @@ def _project(ds: DeviceScene, cam: CameraModel, near: float, tile: int, want_rec
         span_ref=torch.empty((m, 4), dtype=torch.int32, device=dev),
         span_fit=torch.empty((m, 4), dtype=torch.int32, device=dev),
         zkey=torch.empty(m, dtype=torch.int64, device=dev),
+        vrange=torch.empty(m, dtype=torch.int32, device=dev),
     )
     if want_rect:
         out["rect"] = torch.empty((m, 4), dtype=torch.float64, device=dev)
@@ -116,7 +118,8 @@ def _project(ds: DeviceScene, cam: CameraModel, near: float, tile: int, want_rec
     _lib.check(lib.salf_project_voxels(
         _lib.ref(sc), _lib.ref(cs), float(near), int(tile), _lib.ptr(out.get("rect")),
         _lib.ptr(out.get("zc")), _lib.ptr(out.get("culled")), out["span_ref"].data_ptr(),
-        out["span_fit"].data_ptr(), out["zkey"].data_ptr(), _lib.stream_ptr()), "project_voxels")
+        out["span_fit"].data_ptr(), out["zkey"].data_ptr(), out["vrange"].data_ptr(), _lib.stream_ptr()),
+        "project_voxels")
     return out
 
 
@@ -221,12 +224,12 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
     _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
                                          offsets.data_ptr(), entries.data_ptr() if n_inst else offsets.data_ptr(),
                                          rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
-                                         _lib.ptr(saved), _lib.stream_ptr()), "rasterize")
+                                         _lib.ptr(saved), p["vrange"].data_ptr(), _lib.stream_ptr()), "rasterize")
     if ev is not None:
         ev[2].record()
     fb = Framebuffer(rgb, op, depth)
     if return_state:
-        return fb, RasterState(ds, cam, opts, offsets, entries, saved, n_inst)
+        return fb, RasterState(ds, cam, opts, offsets, entries, saved, n_inst, p["vrange"])
     return fb
 
 
@@ -265,12 +268,13 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
             _lib.check(lib.salf_raster_backward_deterministic(
                 _lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts), state.offsets.data_ptr(),
                 state.entries.data_ptr(), state.n_instances, state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
-                grad.data_ptr(), ws.data_ptr(), wsb, _lib.stream_ptr()), "rasterize_backward")
+                grad.data_ptr(), _lib.ptr(state.vrange), ws.data_ptr(), wsb, _lib.stream_ptr()), "rasterize_backward")
         else:
             _lib.check(lib.salf_raster_backward(_lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts),
                                                 state.offsets.data_ptr(), state.entries.data_ptr(),
                                                 state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
-                                                grad.data_ptr(), _lib.stream_ptr()), "rasterize_backward")
+                                                grad.data_ptr(), _lib.ptr(state.vrange), _lib.stream_ptr()),
+                       "rasterize_backward")
         if ev is not None:
             ev[2].record()
     if as_dict:
