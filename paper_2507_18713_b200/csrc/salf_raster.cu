@@ -453,7 +453,9 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
 constexpr int kChunk = SALF_CHUNK;    // forward: entries staged per step in shared memory
 constexpr int kChunkB = SALF_CHUNKB;  // backward: + a kChunkB x warps x 27 fp32 reduction buffer
 
-template <bool kExactColor, bool kRot>
+// fp64 parity-mode composite (exact_color=True): the reference-order
+// arithmetic everywhere, fp64 colour.
+template <bool kRot>
 __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                    const int64_t *__restrict__ offsets,
                                                    const int32_t *__restrict__ entries, float *__restrict__ out_rgb,
@@ -473,7 +475,6 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
   // transmittance kept as a running product of (1 - alpha) (the reference's
   // exp(cumsum(log1p(-alpha))), render_raster.py:258-274, to ~1e-15)
   double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0;
-  float acc_cf[3] = {0.0f, 0.0f, 0.0f};  // fast mode: fp32 colour sums (outputs are fp32)
   bool alive = inside;
   int64_t n_stop = end - beg;
   int n_inc = 0;  // included segments of this pixel (work statistics, saved[7])
@@ -487,17 +488,11 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
     if (alive) {
       for (int j = 0; j < cn; ++j) {
         SegVals sv;
-        if (!hit_and_shade<kExactColor, kRot>(sc, r, sm[j], sv)) continue;
+        if (!hit_and_shade<true, kRot>(sc, r, sm[j], sv)) continue;
         if (T > keep) {  // included iff T_before > 1 - stop_threshold
           const double w = __dmul_rn(T, sv.alpha);
-          if (kExactColor) {
 #pragma unroll
-            for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
-          } else {
-            const float wf = (float)w;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) acc_cf[k] = __fmaf_rn(wf, sv.cf[k], acc_cf[k]);
-          }
+          for (int k = 0; k < 3; ++k) acc_c[k] = __dadd_rn(acc_c[k], __dmul_rn(w, sv.c[k]));
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
           T = __dmul_rn(T, sv.om);
@@ -512,9 +507,6 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
     if (!__syncthreads_or(alive)) break;
   }
   if (!inside) return;
-  if (!kExactColor) {
-    acc_c[0] = acc_cf[0]; acc_c[1] = acc_cf[1]; acc_c[2] = acc_cf[2];
-  }
   const int64_t pix = (int64_t)py * c.width + px;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -531,7 +523,8 @@ __global__ void __launch_bounds__(256, 3) k_composite(salf_scene_t sc, PinholeDe
 // ---------------------------------------------------------------------------
 // backward
 
-template <bool kExactColor, bool kRot>
+// fp64 parity-mode backward (exact_color=True), reference operation order.
+template <bool kRot>
 #ifndef SALF_BWD_MINB
 #define SALF_BWD_MINB 2
 #endif
@@ -598,7 +591,7 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
       float g[32];
       bool act = false;
       SegVals sv;
-      if (inside && jj < n_stop && hit_and_shade<kExactColor, kRot>(sc, r, sm[j], sv)) {
+      if (inside && jj < n_stop && hit_and_shade<true, kRot>(sc, r, sm[j], sv)) {
         if (T > keep) {
           const double w = __dmul_rn(T, sv.alpha);
           // A = dC . c + dD (t_mid - D) / ws   (backward.py:52-59, einsum order (0+2)+1)
@@ -1487,10 +1480,10 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
     cudaStream_t st = (cudaStream_t)stream;
     const bool rot = scene->rot != nullptr;
     if (opts->exact_color && rot)
-      k_composite<true, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+      k_composite<true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
                                                            out_depth, saved);
     else if (opts->exact_color)
-      k_composite<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
+      k_composite<false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
                                                             out_depth, saved);
     else {
       // certified mixed-precision pass, then fp64 recomputation of the flagged pixels
@@ -1533,10 +1526,10 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
   const int threads_np = ((std::max(32, (opts->tile * opts->tile + SALF_BWD_NP - 1) / SALF_BWD_NP) + 31) / 32) * 32;
   const bool rot = scene->rot != nullptr;
   if (opts->exact_color && rot)
-    k_backward<true, true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+    k_backward<true><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
                                                         grad, partial);
   else if (opts->exact_color)
-    k_backward<true, false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
+    k_backward<false><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, saved, d_rgb, d_depth,
                                                          grad, partial);
   else {
     const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
