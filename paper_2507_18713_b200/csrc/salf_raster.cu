@@ -978,6 +978,26 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
 // |ds| <= |w_s|_1 (|dx| + 4 u), sigma a relative error
 // rel <= |ds| / b + 3e-7 (1 + |s| / b) + 2.4e-7 (MUFU ex2 and roundings),
 // and |dy| <= y (rel + 2 u) + sigma 2 dd.
+#ifndef SALF_PREFETCH
+#define SALF_PREFETCH 1
+#endif
+// Prefetch the voxel records of the next chunk's entries into L2 while the
+// current chunk is processed (thread j < cn of the CTA takes entry j).
+__device__ __forceinline__ void prefetch_next(const salf_scene_t &sc, const int32_t *__restrict__ entries,
+                                              int64_t next, int64_t end, int chunk) {
+#if SALF_PREFETCH
+  if (threadIdx.x < chunk && next + threadIdx.x < end) {
+    const int64_t v = __ldg(entries + next + threadIdx.x);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.geo + 4 * v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.aux + 4 * v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.prm + v * SALF_PRM_STRIDE));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.prm + v * SALF_PRM_STRIDE + 24));
+  }
+#else
+  (void)sc; (void)entries; (void)next; (void)end; (void)chunk;
+#endif
+}
+
 #ifndef SALF_FLAGMASK
 #define SALF_FLAGMASK 7  // diagnostics: bit 0 hit, bit 1 inclusion, bit 2 depth certification
 #endif
@@ -1029,6 +1049,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j], vrange);
     __syncthreads();
+    prefetch_next(sc, entries, base + kChunk, end, kChunk);
     if (alive) {
       for (int j = 0; j < cn; ++j) {
         const EntryF &e = sm[j];
@@ -1269,6 +1290,7 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j], vrange);
     __syncthreads();
+    prefetch_next(sc, entries, base + kChunkB, lim, kChunkB);
     const int jb = (int)(base - beg);
     for (int j = 0; j < cn; ++j) {
       const EntryF &e = sm[j];
