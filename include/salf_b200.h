@@ -112,7 +112,9 @@ int salf_device_sm_count(void);
  * when tx0 > tx1), 64-bit orderable depth keys, and `vrange` (M int32:
  * conservative footprint pixel rows lo | hi << 16, widened by one pixel;
  * lo > hi when empty) that the composite / backward use to skip entries a
- * warp's pixel rows cannot hit.  Any output may be NULL. */
+ * warp's pixel rows cannot hit.  Any output may be NULL.  (The composite and
+ * backward also take an optional `tile_order`: the launch order of the
+ * tiles, e.g. by list length descending; NULL = row-major.) */
 int salf_project_voxels(const salf_scene_t *scene, const salf_camera_t *cam, double near,
                         int32_t tile, double *rect, double *z_center, uint8_t *culled,
                         int32_t *span_ref, int32_t *span_fit, uint64_t *zkey, int32_t *vrange,
@@ -141,7 +143,8 @@ int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double 
 int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                           const salf_raster_opts_t *opts, const int64_t *offsets,
                           const int32_t *entries, float *out_rgb, float *out_opacity,
-                          float *out_depth, double *saved, const int32_t *vrange, void *stream);
+                          float *out_depth, double *saved, const int32_t *vrange,
+                          const int32_t *tile_order, void *stream);
 
 /* Raster backward (no reference function: defined as backward_records,
  * backward.py:35-101, applied to the raster pairs -- see DESIGN.md).
@@ -149,7 +152,8 @@ int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
 int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                          const salf_raster_opts_t *opts, const int64_t *offsets,
                          const int32_t *entries, const double *saved, const double *d_rgb,
-                         const double *d_depth, double *grad, const int32_t *vrange, void *stream);
+                         const double *d_depth, double *grad, const int32_t *vrange,
+                         const int32_t *tile_order, void *stream);
 
 /* Deterministic variant of salf_raster_backward (SPEC.md:531, :541 ordered
  * reductions; SURVEY §7 hard part 5): one fixed-order 27-row per (tile,
@@ -162,8 +166,8 @@ int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_cam
                                        const salf_raster_opts_t *opts, const int64_t *offsets,
                                        const int32_t *entries, int64_t n_instances, const double *saved,
                                        const double *d_rgb, const double *d_depth, double *grad,
-                                       const int32_t *vrange, void *workspace, size_t workspace_bytes,
-                                       void *stream);
+                                       const int32_t *vrange, const int32_t *tile_order, void *workspace,
+                                       size_t workspace_bytes, void *stream);
 
 /* Deterministic variant of salf_ray_backward: each included segment's
  * 27-row goes to slot row_start[ray] + k (row_start: (n + 1) exclusive scan

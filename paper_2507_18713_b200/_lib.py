@@ -74,14 +74,14 @@ SIGNATURES = {
     "salf_raster_bin_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int64, C.c_int32]),
     "salf_raster_bin": (C.c_int, [vp, vp, C.c_double, C.c_int32, C.c_int32, vp, vp, vp, vp,
                                   C.c_size_t, C.c_int64, vp, vp, vp, vp]),
-    "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_raster_backward_det_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "salf_ray_backward_det_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "salf_ray_backward_deterministic": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64,
                                                   vp, C.c_size_t, vp]),
     "salf_raster_backward_deterministic": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp,
-                                                     C.c_size_t, vp]),
+                                                     vp, C.c_size_t, vp]),
     "salf_camera_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_lidar_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_octree_build_host": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int64, vp, vp]),

@@ -1012,9 +1012,11 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
                                                         const int32_t *__restrict__ entries,
                                                         float *__restrict__ out_rgb, float *__restrict__ out_op,
                                                         float *__restrict__ out_depth, double *__restrict__ saved,
-                                                        const int32_t *__restrict__ vrange) {
+                                                        const int32_t *__restrict__ vrange,
+                                                        const int32_t *__restrict__ tile_order) {
   __shared__ EntryF sm[kChunk];
-  const int tile_id = blockIdx.x;
+  // heaviest tiles first (tile_order: tiles by list length, descending) -> no ragged last wave
+  const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
   const int px = tx * c.tile + lx, py = ty * c.tile + ly;
@@ -1244,14 +1246,14 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
     const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial,
-    const int32_t *__restrict__ vrange) {
+    const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order) {
   __shared__ EntryF sm[kChunkB];
   __shared__ float red[kChunkB][8 / NP][kGradStride];
 #if SALF_BWD_SMEMRED
   __shared__ __align__(16) float xp[8 / NP][32][28];
 #endif
   __shared__ int s_max;
-  const int tile_id = blockIdx.x;
+  const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   const int nthreads = blockDim.x;
   const int npix = c.tile * c.tile;
@@ -1491,7 +1493,7 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
 extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                                      const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                      float *out_rgb, float *out_opacity, float *out_depth, double *saved,
-                                     const int32_t *vrange, void *stream) {
+                                     const int32_t *vrange, const int32_t *tile_order, void *stream) {
   SALF_TRY {
     if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
                                                      camera_kind_repr(cam->kind));
@@ -1516,7 +1518,7 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
       const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
 #define SALF_LAUNCH_FWD(ROT, SDF)                                                                             \
   k_composite_fast<ROT, SDF><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity, \
-                                                         out_depth, saved, vrange)
+                                                         out_depth, saved, vrange, tile_order)
       if (rot) {
         if (sdf) SALF_LAUNCH_FWD(true, true); else SALF_LAUNCH_FWD(true, false);
         if (!no_redo)
@@ -1538,7 +1540,8 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
 static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t *cam,
                                   const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                   const double *saved, const double *d_rgb, const double *d_depth, double *grad,
-                                  float *partial, const int32_t *vrange, cudaStream_t st) {
+                                  float *partial, const int32_t *vrange, const int32_t *tile_order,
+                                  cudaStream_t st) {
   if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
                                                    camera_kind_repr(cam->kind));
   if (opts->tile < 1 || opts->tile > 16) return set_error(SALF_EINVAL, "tile size must be in [1, 16]");
@@ -1557,7 +1560,7 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
     const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
 #define SALF_LAUNCH_BWD(ROT, SDF)                                                                               \
   k_backward_fast<ROT, SALF_BWD_NP, SDF><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved, \
-                                                                        d_rgb, d_depth, grad, partial, vrange)
+                                                                        d_rgb, d_depth, grad, partial, vrange, tile_order)
     if (rot) {
       if (sdf) SALF_LAUNCH_BWD(true, true); else SALF_LAUNCH_BWD(true, false);
     } else {
@@ -1571,10 +1574,10 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
 extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                                     const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                     const double *saved, const double *d_rgb, const double *d_depth, double *grad,
-                                    const int32_t *vrange, void *stream) {
+                                    const int32_t *vrange, const int32_t *tile_order, void *stream) {
   SALF_TRY {
     return raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, nullptr, vrange,
-                                  (cudaStream_t)stream);
+                                  tile_order, (cudaStream_t)stream);
   }
   SALF_CATCH
 }
@@ -1687,8 +1690,8 @@ extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, con
                                                   const salf_raster_opts_t *opts, const int64_t *offsets,
                                                   const int32_t *entries, int64_t n_instances, const double *saved,
                                                   const double *d_rgb, const double *d_depth, double *grad,
-                                                  const int32_t *vrange, void *workspace, size_t workspace_bytes,
-                                                  void *stream) {
+                                                  const int32_t *vrange, const int32_t *tile_order, void *workspace,
+                                                  size_t workspace_bytes, void *stream) {
   SALF_TRY {
     if (n_instances <= 0) return SALF_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1697,7 +1700,7 @@ extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, con
     float *partial = (float *)workspace;
     cudaMemsetAsync(partial, 0, sizeof(float) * kGradStride * n_instances, st);
     const int rc = raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, partial,
-                                          vrange, st);
+                                          vrange, tile_order, st);
     if (rc != SALF_OK) return rc;
     // instance rows keyed by their voxel (entries[i])
     return det_reduce_rows(n_instances, reinterpret_cast<const uint32_t *>(entries), partial, scene->n, grad,
