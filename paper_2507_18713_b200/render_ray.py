@@ -129,6 +129,8 @@ def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: tor
     lib = _lib.load()
     n = o.shape[0]
     o_np, d_np = o.cpu().numpy(), d.cpu().numpy()
+    if isinstance(t_stamps, torch.Tensor):  # only actor poses need the timestamps (host side)
+        t_stamps = t_stamps.detach().cpu().numpy()
     ts = np.broadcast_to(np.asarray(0.0 if t_stamps is None else t_stamps, np.float64), (n,))
     recs, rays, offsets, goff = [], [], [], 0
     for ai, actor in enumerate(scene.actors):
@@ -175,14 +177,16 @@ def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: tor
 
 def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf,
                    background=(0.0, 0.0, 0.0), stop_threshold: float = STOP_THRESHOLD,
-                   valid=None, exact_color: bool = False) -> RenderRecords:
+                   valid=None, exact_color: bool = False, check_unit: bool = True) -> RenderRecords:
     """Render a ray batch against the composed scene (render_ray.py:161-239).
 
     Static scenes use one fused march/shade/composite launch with the
     reference's early stop.  With live actors the static march runs without
     early stop (:175) and is merged per ray with the actors' segments (rays
     moved into each actor frame at their timestamps).  Finite `t_max` is
-    supported by `march_batch` only (the reference renderers pass infinity)."""
+    supported by `march_batch` only (the reference renderers pass infinity).
+    `check_unit=False` skips the unit-norm validation (a host-synchronising
+    reduction) for directions that are unit by construction."""
     if np.any(np.isfinite(np.asarray(t_max, np.float64))):
         raise NotImplementedError("finite t_max is only supported by march_batch")
     lib = _lib.load()
@@ -195,7 +199,7 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
     o = _lib.as_f64(origins, dev).reshape(-1, 3)
     d = _lib.as_f64(dirs, dev).reshape(-1, 3)
     n = o.shape[0]
-    if n and bool((torch.linalg.norm(d, dim=1) - 1.0).abs().gt(1e-6).any()):
+    if n and check_unit and bool((torch.linalg.norm(d, dim=1) - 1.0).abs().gt(1e-6).any()):
         raise ValueError("ray directions must be unit norm")
     vmask = None
     if valid is not None:
@@ -246,9 +250,9 @@ def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chun
     invalid rays keep the background, zero opacity and NaN depth."""
     del chunk
     h, w = batch.shape
-    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, batch.t_stamps.cpu().numpy(),
+    rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, batch.t_stamps,
                          background=background, stop_threshold=stop_threshold, valid=batch.valid,
-                         exact_color=exact_color)
+                         exact_color=exact_color, check_unit=not getattr(batch, "generated", False))
     check_status(rec)
     return rec.out_color.reshape(h, w, 3), rec.opacity.reshape(h, w), rec.depth.reshape(h, w)
 
@@ -286,7 +290,9 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
     o = _lib.as_f64(batch.origins, dev).reshape(-1, 3)
     d = _lib.as_f64(batch.dirs, dev).reshape(-1, 3)
     n = o.shape[0]
-    if n and bool((torch.linalg.norm(d, dim=1) - 1.0).abs().gt(1e-6).any()):
+    # octree.py:227-229 (skipped for batches our generators produced: unit by construction)
+    if n and not getattr(batch, "generated", False) and \
+            bool((torch.linalg.norm(d, dim=1) - 1.0).abs().gt(1e-6).any()):
         raise ValueError("ray directions must be unit norm")
     depth = torch.empty(n, dtype=torch.float32, device=dev)
     op = torch.empty(n, dtype=torch.float32, device=dev)
@@ -448,9 +454,13 @@ def trace_effects(scene, octrees, origins, dirs, t_stamps, spheres: list, sun_di
     w = torch.ones(n, dtype=torch.float64, device=dev)
     budget = torch.full((n,), int(max_bounces), dtype=torch.int32, device=dev)
     live = isinstance(scene, Scene) and any(a.voxels.n for a in scene.actors)
+    first = True
     while n:
         # timestamps only matter for actor poses (host-side in integrate_rays)
-        rec = integrate_rays(scene, octrees, o, d, ts.cpu().numpy() if live else None, background=background)
+        # wave > 0 directions are reflections / normalised refractions of unit rays
+        rec = integrate_rays(scene, octrees, o, d, ts.cpu().numpy() if live else None, background=background,
+                             check_unit=first)
+        first = False
         nxt = dict(o=torch.empty((2 * n, 3), dtype=torch.float64, device=dev),
                    d=torch.empty((2 * n, 3), dtype=torch.float64, device=dev),
                    ts=torch.empty(2 * n, dtype=torch.float64, device=dev),

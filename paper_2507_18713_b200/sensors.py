@@ -72,6 +72,9 @@ class RayBatch:
     keys: torch.Tensor  # (N, 2) int64
     valid: torch.Tensor  # (N,) bool
     shape: tuple
+    # directions generated here (cos/sin / normalised), i.e. unit by
+    # construction: the renderers skip their host-synchronising norm check
+    generated: bool = False
 
     @property
     def n(self) -> int:
@@ -192,7 +195,7 @@ def _camera_batch(cam: CameraModel, t0: float, rolling: bool, device=None, strea
                                         valid.data_ptr(), _lib.stream_ptr(stream)), "camera_rays")
     rows = torch.arange(h, device=dev).repeat_interleave(w)
     cols = torch.arange(w, device=dev).repeat(h)
-    return RayBatch(o, d, ts, torch.stack([rows, cols], 1), valid.bool(), (h, w))
+    return RayBatch(o, d, ts, torch.stack([rows, cols], 1), valid.bool(), (h, w), generated=True)
 
 
 def gen_camera_rays(cam: CameraModel, t0: float = 0.0, device=None) -> RayBatch:
@@ -231,7 +234,7 @@ def gen_lidar_rays(lidar: LidarModel, t0: float = 0.0, device=None) -> RayBatch:
     beams = torch.arange(nb, device=dev).repeat_interleave(steps)
     steps_i = torch.arange(steps, device=dev).repeat(nb)
     return RayBatch(o, d, ts, torch.stack([beams, steps_i], 1),
-                    torch.ones(n, dtype=torch.bool, device=dev), (nb, steps))
+                    torch.ones(n, dtype=torch.bool, device=dev), (nb, steps), generated=True)
 
 
 def sensor_from_dict(d: dict):
