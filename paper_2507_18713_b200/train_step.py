@@ -49,7 +49,8 @@ def rig_forward(ds, octree, sensors, targets, items) -> ForwardState:
             saved.append((st, diff))
         else:
             rays = gen_lidar_rays(s, device=dev)
-            rec = RY.integrate_rays(ds, octree, rays.origins[it.lo:it.hi], rays.dirs[it.lo:it.hi])
+            rec = RY.integrate_rays(ds, octree, rays.origins[it.lo:it.hi], rays.dirs[it.lo:it.hi],
+                                    check_unit=False)  # generated sweep: unit by construction
             gt = torch.as_tensor(targets[it.sensor], device=dev)[it.lo:it.hi].double()
             dep = rec.depth.double()
             ok = torch.isfinite(dep) & torch.isfinite(gt)
