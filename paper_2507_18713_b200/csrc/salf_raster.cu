@@ -1323,8 +1323,17 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
         for (int m = 0; m < 7; ++m) row[m] = make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]);
         __syncwarp();
         if (lane < kGradStride) {
-#pragma unroll 8
-          for (int rr = 0; rr < 32; ++rr) tot += xp[warp][rr][lane];
+          // four independent partial sums: a 32-long serial FADD chain would
+          // leave the warp waiting on the add latency
+          float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll
+          for (int rr = 0; rr < 32; rr += 4) {
+            t0 += xp[warp][rr][lane];
+            t1 += xp[warp][rr + 1][lane];
+            t2 += xp[warp][rr + 2][lane];
+            t3 += xp[warp][rr + 3][lane];
+          }
+          tot = (t0 + t1) + (t2 + t3);
         }
         __syncwarp();
       }
