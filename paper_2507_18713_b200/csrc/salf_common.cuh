@@ -121,6 +121,13 @@ __device__ __forceinline__ double seg_alpha(double sigma, double delta, double &
   return a;
 }
 
+// MUFU exp (ex2.approx of x log2 e): relative error ~2^-22 + |x| 2^-24.
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
+}
+
 // MUFU reciprocal (rcp.approx.ftz, ~1 ulp; rcp(inf) = 0) for the fp32
 // sigmoid -- the IEEE __frcp_rn adds a Newton step and a slow-path branch.
 __device__ __forceinline__ float fast_rcp(float x) {
@@ -164,15 +171,8 @@ __device__ __forceinline__ void eval_color32(const VoxPrm &p, const double xd[3]
     z = __fmaf_rn(p.wsh[4 * i + 1], g1, z);
     z = __fmaf_rn(p.wsh[4 * i + 2], g2, z);
     z = __fmaf_rn(p.wsh[4 * i + 3], g3, z);
-    c[i] = (double)fast_rcp(1.0f + __expf(-z));
+    c[i] = (double)fast_rcp(1.0f + fast_exp(-z));
   }
-}
-
-// MUFU exp (ex2.approx of x log2 e): relative error ~2^-22 + |x| 2^-24.
-__device__ __forceinline__ float fast_exp(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
-  return y;
 }
 
 // expm1(x) for x <= 0 in fp32 without cancellation: degree-7 Taylor on
@@ -197,7 +197,7 @@ __device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3],
     z = __fmaf_rn(p.wsh[4 * i + 1], gam[1], z);
     z = __fmaf_rn(p.wsh[4 * i + 2], gam[2], z);
     z = __fmaf_rn(p.wsh[4 * i + 3], gam[3], z);
-    c[i] = fast_rcp(1.0f + __expf(-z));
+    c[i] = fast_rcp(1.0f + fast_exp(-z));
   }
 }
 
