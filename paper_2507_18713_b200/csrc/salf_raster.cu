@@ -830,6 +830,7 @@ __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, flo
   return true;
 }
 
+
 // Per-pixel backward state (fp64 only where the text above says).
 struct BwdPix {
   RayF r;
@@ -1325,9 +1326,9 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
         if (lane < kGradStride) {
           // four independent partial sums: a 32-long serial FADD chain would
           // leave the warp waiting on the add latency
-          float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+          float t0 = xp[warp][0][lane], t1 = xp[warp][1][lane], t2 = xp[warp][2][lane], t3 = xp[warp][3][lane];
 #pragma unroll
-          for (int rr = 0; rr < 32; rr += 4) {
+          for (int rr = 4; rr < 32; rr += 4) {
             t0 += xp[warp][rr][lane];
             t1 += xp[warp][rr + 1][lane];
             t2 += xp[warp][rr + 2][lane];
