@@ -830,7 +830,6 @@ __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, flo
   return true;
 }
 
-
 // Per-pixel backward state (fp64 only where the text above says).
 struct BwdPix {
   RayF r;
