@@ -89,7 +89,8 @@ typedef struct {
   double root_min[3];
   double root_edge;
   int32_t max_depth;
-  int32_t pad;
+  int32_t jump_levels;  /* K of the jump table below (0: none)              */
+  const void *jump;     /* optional, salf_octree_jump_build: descents start at depth K */
 } salf_octree_t;
 
 typedef struct {
@@ -214,6 +215,16 @@ int salf_octree_ancestor_keys(int64_t n, const uint8_t *level, const int32_t *ij
                               const int64_t *base, uint64_t *keys, uint64_t *self_key, void *stream);
 int salf_octree_fill(int64_t n, int64_t n_internal, const uint64_t *internal, const uint64_t *self_key,
                      int32_t *nodes, int32_t *contained, void *stream);
+
+/* Jump table for the octree descent (a B200-side acceleration structure,
+ * no reference counterpart): for each of the 8^K cells of the depth-K grid
+ * the node word the reference's descent reaches after K levels (INT32_MIN if
+ * the path ends above depth K), then per axis the 2^K corners after K levels
+ * accumulated in the reference's order (octree.py:152-163).  A query starts
+ * there and continues level by level, so results are bit-identical.
+ * salf_octree_jump_bytes(K) bytes of device memory; K <= 8. */
+size_t salf_octree_jump_bytes(int32_t levels);
+int salf_octree_jump_build(const salf_octree_t *tree, int32_t levels, void *jump, void *stream);
 
 /* query_batch (octree.py:136-166): flag (i8), vid (i64), corner (x3), edge. */
 int salf_octree_query(const salf_octree_t *tree, int64_t n, const double *p, int8_t *flag,

@@ -53,7 +53,8 @@ class LidarT(C.Structure):
 
 class OctreeT(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("nodes", vp), ("root_min", c_double3),
-                ("root_edge", C.c_double), ("max_depth", C.c_int32), ("pad", C.c_int32)]
+                ("root_edge", C.c_double), ("max_depth", C.c_int32), ("jump_levels", C.c_int32),
+                ("jump", vp)]
 
 
 class SphereT(C.Structure):
@@ -86,6 +87,8 @@ SIGNATURES = {
     "salf_lidar_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_octree_build_host": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int64, vp, vp]),
     "salf_octree_query": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_octree_jump_bytes": (C.c_size_t, [C.c_int32]),
+    "salf_octree_jump_build": (C.c_int, [vp, C.c_int32, vp, vp]),
     "salf_march": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, C.c_double, C.c_int32, vp, vp, vp,
                              vp, vp, vp, vp]),
     "salf_ray_forward": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -21,7 +21,18 @@ struct OctDev {
   double rmin[3], rmax[3];
   double root_edge;
   int max_depth;
+  // jump table (salf_octree_jump_build): words after jk levels, corners per axis
+  int jk;
+  const int32_t *jump;
+  const double *jcorner;  // [3][2^jk]
+  double jedge;           // root_edge * 0.5^jk (exact)
 };
+
+constexpr int32_t kJumpNone = INT32_MIN;  // the descent ends above depth K
+constexpr int kJumpMaxLevels = 8;
+
+static size_t jump_words(int k) { return (size_t)1 << (3 * k); }
+static size_t jump_corner_offset(int k) { return (jump_words(k) * sizeof(int32_t) + 15) & ~(size_t)15; }
 
 static OctDev make_oct(const salf_octree_t *t) {
   OctDev o;
@@ -32,6 +43,12 @@ static OctDev make_oct(const salf_octree_t *t) {
   }
   o.root_edge = t->root_edge;
   o.max_depth = t->max_depth;
+  o.jk = (t->jump && t->jump_levels > 0 && t->jump_levels <= kJumpMaxLevels) ? t->jump_levels : 0;
+  o.jump = o.jk ? (const int32_t *)t->jump : nullptr;
+  o.jcorner = o.jk ? (const double *)((const char *)t->jump + jump_corner_offset(o.jk)) : nullptr;
+  double e = t->root_edge;
+  for (int l = 0; l < o.jk; ++l) e *= 0.5;  // the descent's edge halving, exact
+  o.jedge = e;
   return o;
 }
 
@@ -65,6 +82,22 @@ __device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3
 #pragma unroll
   for (int k = 0; k < 3; ++k) U[k] = min((uint32_t)__dmul_rn(u[k], 2147483648.0), 0x7fffffffu);
   int sh = 30;
+  if (t.jk) {
+    // jump table: the word, corner and edge the loop below reaches after jk
+    // levels (built with the same operations), unless the path ends earlier
+    const int s0 = 31 - t.jk;
+    const uint32_t cx = U[0] >> s0, cy = U[1] >> s0, cz = U[2] >> s0;
+    const int32_t wj = __ldg(t.jump + ((((cx << t.jk) | cy) << t.jk) | cz));
+    if (wj != kJumpNone) {
+      const int n = 1 << t.jk;
+      corner[0] = __ldg(t.jcorner + cx);
+      corner[1] = __ldg(t.jcorner + n + cy);
+      corner[2] = __ldg(t.jcorner + 2 * n + cz);
+      edge = t.jedge;
+      sh = 30 - t.jk;
+      w = wj;
+    }
+  }
   while (w >= 0) {
     const int b0 = (U[0] >> sh) & 1, b1 = (U[1] >> sh) & 1, b2 = (U[2] >> sh) & 1;
     --sh;
@@ -955,6 +988,40 @@ __global__ void __launch_bounds__(128) k_ray_backward_merge(OctDev t, salf_scene
 
 using namespace salf;
 
+// Jump table for the descent (see salf_b200.h): one thread per depth-K cell
+// walks the reference's levels (child = b0 + 2 b1 + 4 b2, octree.py:152-163);
+// thread 0..3*2^K-1 of the second kernel accumulate the per-axis corners in
+// the descent's order (edge halved, then corner += bit ? edge : 0).
+__global__ void k_jump_words(const int32_t *__restrict__ nodes, int K, int32_t *__restrict__ out) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ((int64_t)1 << (3 * K))) return;
+  const uint32_t mask = (1u << K) - 1;
+  const uint32_t cx = (uint32_t)(c >> (2 * K)) & mask, cy = (uint32_t)(c >> K) & mask, cz = (uint32_t)c & mask;
+  int32_t w = nodes[0];
+  for (int l = 0; l < K; ++l) {
+    if (w < 0) {
+      w = kJumpNone;
+      break;
+    }
+    const int sh = K - 1 - l;
+    w = nodes[w + ((cx >> sh) & 1) + 2 * ((cy >> sh) & 1) + 4 * ((cz >> sh) & 1)];
+  }
+  out[c] = w;
+}
+
+__global__ void k_jump_corners(double r0, double r1, double r2, double root_edge, int K, double *__restrict__ out) {
+  const int n = 1 << K;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  const int axis = i / n, pre = i - axis * n;
+  double corner = axis == 0 ? r0 : (axis == 1 ? r1 : r2), edge = root_edge;
+  for (int l = 0; l < K; ++l) {
+    edge = __dmul_rn(edge, 0.5);
+    corner = __dadd_rn(corner, ((pre >> (K - 1 - l)) & 1) ? edge : 0.0);
+  }
+  out[i] = corner;
+}
+
 extern "C" int salf_octree_query(const salf_octree_t *tree, int64_t n, const double *p, int8_t *flag, int64_t *vid,
                                  double *corner, double *edge, int32_t *out_of_root, void *stream) {
   SALF_TRY {
@@ -1200,6 +1267,28 @@ extern "C" int salf_ray_backward_merge(const salf_octree_t *tree, const salf_sce
                                                                             ex_start, ex_rec, saved, d_rgb, d_depth,
                                                                             grad, ex_grad);
     return check_cuda("salf_ray_backward_merge");
+  }
+  SALF_CATCH
+}
+
+extern "C" size_t salf_octree_jump_bytes(int32_t levels) {
+  if (levels <= 0 || levels > kJumpMaxLevels) return 0;
+  return jump_corner_offset(levels) + sizeof(double) * 3 * ((size_t)1 << levels);
+}
+
+extern "C" int salf_octree_jump_build(const salf_octree_t *tree, int32_t levels, void *jump, void *stream) {
+  SALF_TRY {
+    if (levels <= 0 || levels > kJumpMaxLevels)
+      return set_error(SALF_EINVAL, "jump table levels must be in 1..%d, got %d", kJumpMaxLevels, (int)levels);
+    if (tree->n_nodes <= 0) return set_error(SALF_EINVAL, "empty octree");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nw = (int64_t)jump_words(levels);
+    k_jump_words<<<(unsigned)((nw + 255) / 256), 256, 0, st>>>(tree->nodes, levels, (int32_t *)jump);
+    const int nc = 3 << levels;
+    k_jump_corners<<<(nc + 127) / 128, 128, 0, st>>>(tree->root_min[0], tree->root_min[1], tree->root_min[2],
+                                                     tree->root_edge, levels,
+                                                     (double *)((char *)jump + jump_corner_offset(levels)));
+    return check_cuda("salf_octree_jump_build");
   }
   SALF_CATCH
 }

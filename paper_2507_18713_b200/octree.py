@@ -11,7 +11,8 @@ bit-identical.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import os
+from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
@@ -24,12 +25,18 @@ MIN_EDGE_FACTOR = 64
 _MAX_ROUNDS = 200_000
 
 
+# depth of the descent jump table (csrc salf_octree_jump_build; 0 disables it)
+JUMP_LEVELS = int(os.environ.get("SALF_OCT_JUMP", "7"))
+
+
 @dataclass
 class OctreeBuffer:
     nodes: torch.Tensor  # (n_nodes,) int32 words on the device
     root_min: np.ndarray
     root_edge: float
     max_depth: int
+    jump: torch.Tensor | None = None  # descent jump table (built on first use)
+    jump_levels: int = 0  # its depth; -1: disabled for this tree
 
     @property
     def n_nodes(self) -> int:
@@ -46,6 +53,26 @@ class OctreeBuffer:
         return np.where(w >= 0, 0, np.where(w == -1, -1, 1)).astype(np.int8)
 
     def c_struct(self) -> _lib.OctreeT:
+        t = self._base_struct()
+        if self.jump is None and self.jump_levels == 0 and JUMP_LEVELS > 0 and self.nodes.is_cuda \
+                and self.max_depth > 0:
+            # no deeper than the tree, and no larger (8^K words) than ~8x its node table
+            k = min(JUMP_LEVELS, int(self.max_depth), int(np.log2(max(self.n_nodes, 1)) // 3) + 1)
+            self._build_jump(t, k)
+        if self.jump is not None:
+            t.jump_levels = self.jump_levels
+            t.jump = self.jump.data_ptr()
+        return t
+
+    def with_jump(self, levels: int) -> "OctreeBuffer":
+        """A view of this tree whose descents use a jump table of depth
+        `levels` (0: none, every query walks from the root)."""
+        t = replace(self, jump=None, jump_levels=-1 if levels <= 0 else 0)
+        if levels > 0:
+            t._build_jump(t._base_struct(), min(int(levels), max(int(self.max_depth), 1)))
+        return t
+
+    def _base_struct(self) -> _lib.OctreeT:
         t = _lib.OctreeT()
         t.n_nodes = self.n_nodes
         t.nodes = self.nodes.data_ptr()
@@ -53,6 +80,16 @@ class OctreeBuffer:
         t.root_edge = float(self.root_edge)
         t.max_depth = int(self.max_depth)
         return t
+
+    def _build_jump(self, t: _lib.OctreeT, levels: int) -> None:
+        """Device jump table: the descent starts at depth `levels` (same
+        words, corners and edges as the level-by-level walk)."""
+        lib = _lib.load()
+        nbytes = lib.salf_octree_jump_bytes(levels)
+        jump = torch.empty(nbytes, dtype=torch.uint8, device=self.nodes.device)
+        _lib.check(lib.salf_octree_jump_build(_lib.ref(t), levels, jump.data_ptr(), _lib.stream_ptr()),
+                   "octree jump table")
+        self.jump, self.jump_levels = jump, levels
 
 
 def compute_child_index(p_local) -> np.ndarray:
