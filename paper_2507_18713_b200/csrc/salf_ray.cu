@@ -26,6 +26,7 @@ struct OctDev {
   const int32_t *jump;
   const double *jcorner;  // [3][2^jk]
   double jedge;           // root_edge * 0.5^jk (exact)
+  double inv_root;        // RN(1 / root_edge), host IEEE division
 };
 
 constexpr int32_t kJumpNone = INT32_MIN;  // the descent ends above depth K
@@ -49,6 +50,7 @@ static OctDev make_oct(const salf_octree_t *t) {
   double e = t->root_edge;
   for (int l = 0; l < o.jk; ++l) e *= 0.5;  // the descent's edge halving, exact
   o.jedge = e;
+  o.inv_root = 1.0 / t->root_edge;
   return o;
 }
 
@@ -57,6 +59,25 @@ enum : int32_t { kStatusRoundCap = 1, kStatusOutsideRoot = 2, kStatusOrder = 4, 
 #ifndef SALF_MARCH_INTBITS
 #define SALF_MARCH_INTBITS 1
 #endif
+#ifndef SALF_DIV_MARKSTEIN
+#define SALF_DIV_MARKSTEIN 1
+#endif
+// (p - root_min) / root_edge, correctly rounded (== __ddiv_rn).  The divisor
+// is fixed per tree, so its correctly rounded reciprocal y comes from the
+// host; q0 = RN(x y) is within 1 ulp of x / e, r = x - q0 e is exact (FMA),
+// and RN(q0 + r y) = RN(x / e) (Markstein's theorem; x is 0 or >= ~1e-17 in
+// magnitude here, so nothing underflows).  Saves __ddiv_rn's per-call
+// reciprocal refinement and slow-path test: 3 divisions per march round.
+__device__ __forceinline__ double div_root(double x, const OctDev &t) {
+#if SALF_DIV_MARKSTEIN
+  const double q0 = __dmul_rn(x, t.inv_root);
+  const double r = fma(-q0, t.root_edge, x);
+  return fma(r, t.inv_root, q0);
+#else
+  return __ddiv_rn(x, t.root_edge);
+#endif
+}
+
 // query_batch for one point (octree.py:136-166).  Returns node word
 // (-1 empty, <= -2 leaf), writes corner/edge of the node.
 __device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3], double corner[3], double &edge,
@@ -65,7 +86,7 @@ __device__ __forceinline__ int32_t query_point(const OctDev &t, const double p[3
   outside = false;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    u[k] = __ddiv_rn(__dsub_rn(p[k], t.rmin[k]), t.root_edge);
+    u[k] = div_root(__dsub_rn(p[k], t.rmin[k]), t);
     if (u[k] < -1e-9 || u[k] > 1.0 + 1e-9) outside = true;
     u[k] = npmin(npmax(u[k], 0.0), 1.0);
     corner[k] = t.rmin[k];
