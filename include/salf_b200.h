@@ -156,6 +156,14 @@ int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                          const double *d_depth, double *grad, const int32_t *vrange,
                          const int32_t *tile_order, void *stream);
 
+/* Launch order for the tile kernels (a scheduling choice only, results do
+ * not depend on it): tiles by list length, longest first, ties in tile
+ * order (lengths saturate at 65535).  order: n_tiles int32; workspace of
+ * salf_raster_tile_order_workspace_bytes(n_tiles) bytes. */
+size_t salf_raster_tile_order_workspace_bytes(int32_t n_tiles);
+int salf_raster_tile_order(const int64_t *offsets, int32_t n_tiles, int32_t *order, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* Deterministic variant of salf_raster_backward (SPEC.md:531, :541 ordered
  * reductions; SURVEY §7 hard part 5): one fixed-order 27-row per (tile,
  * entry) instance into the workspace, instances stable-sorted by voxel, each

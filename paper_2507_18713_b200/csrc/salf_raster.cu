@@ -1690,6 +1690,48 @@ int salf::det_reduce_rows(int64_t n_rows, const uint32_t *row_vid, const float *
   return check_cuda("det_reduce_rows");
 }
 
+// tile launch order: 16-bit descending-length keys, stable radix sort (ties in tile order)
+__global__ void k_tile_len_keys(int32_t n, const int64_t *__restrict__ offsets, uint16_t *__restrict__ keys,
+                                int32_t *__restrict__ ids) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t len = offsets[t + 1] - offsets[t];
+  keys[t] = (uint16_t)(0xffff - (len < 0xffff ? len : 0xffff));
+  ids[t] = t;
+}
+
+static size_t tile_order_cub_bytes(int32_t n) {
+  size_t b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (uint16_t *)nullptr, (uint16_t *)nullptr, (int32_t *)nullptr,
+                                  (int32_t *)nullptr, std::max(n, 1), 0, 16);
+  return b;
+}
+
+extern "C" size_t salf_raster_tile_order_workspace_bytes(int32_t n_tiles) {
+  const size_t n = (size_t)std::max(n_tiles, 1);
+  return align_up(2 * n * sizeof(uint16_t)) + align_up(n * sizeof(int32_t)) + tile_order_cub_bytes(n_tiles);
+}
+
+extern "C" int salf_raster_tile_order(const int64_t *offsets, int32_t n_tiles, int32_t *order, void *workspace,
+                                      size_t workspace_bytes, void *stream) {
+  SALF_TRY {
+    if (n_tiles <= 0) return SALF_OK;
+    if (workspace_bytes < salf_raster_tile_order_workspace_bytes(n_tiles))
+      return set_error(SALF_EWORKSPACE, "tile order workspace too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *p = (char *)workspace;
+    uint16_t *ka = (uint16_t *)p, *kb = ka + n_tiles;
+    p += align_up(2 * (size_t)n_tiles * sizeof(uint16_t));
+    int32_t *ids = (int32_t *)p;
+    p += align_up((size_t)n_tiles * sizeof(int32_t));
+    k_tile_len_keys<<<(n_tiles + 255) / 256, 256, 0, st>>>(n_tiles, offsets, ka, ids);
+    size_t tb = tile_order_cub_bytes(n_tiles);
+    cub::DeviceRadixSort::SortPairs(p, tb, ka, kb, ids, order, n_tiles, 0, 16, st);
+    return check_cuda("salf_raster_tile_order");
+  }
+  SALF_CATCH
+}
+
 extern "C" size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances) {
   const int64_t ni = std::max<int64_t>(n_instances, 1);
   return align_up(sizeof(float) * kGradStride * ni) + det_reduce_workspace_bytes(ni);

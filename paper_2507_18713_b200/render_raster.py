@@ -90,8 +90,8 @@ class _Workspace:
     def __init__(self):
         self.buf = {}
 
-    def get(self, device, nbytes: int) -> torch.Tensor:
-        key = str(device)
+    def get(self, device, nbytes: int, slot: str = "bin") -> torch.Tensor:
+        key = (str(device), slot)
         t = self.buf.get(key)
         if t is None or t.numel() < nbytes:
             t = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
@@ -271,8 +271,12 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
         if TILE_ORDER and state.tile_order is None:
             # backward: longest tile lists first (measured: the forward is faster row-major, where
             # neighbouring tiles share voxels in L2; the backward gains from no ragged last wave)
-            state.tile_order = torch.argsort(state.offsets[1:] - state.offsets[:-1],
-                                             descending=True).to(torch.int32)
+            nt = state.offsets.numel() - 1
+            state.tile_order = torch.empty(nt, dtype=torch.int32, device=dev)
+            tws = _WS.get(dev, lib.salf_raster_tile_order_workspace_bytes(nt), slot="tile_order")
+            _lib.check(lib.salf_raster_tile_order(state.offsets.data_ptr(), nt, state.tile_order.data_ptr(),
+                                                  tws.data_ptr(), tws.numel(), _lib.stream_ptr()),
+                       "rasterize_backward")
         ev = _timed(events, "raster_backward")
         if deterministic:
             wsb = lib.salf_raster_backward_det_workspace_bytes(state.n_instances)

@@ -508,3 +508,18 @@ def test_ray_path_raw_density(exact):
     g = backward_records(rec, sc, dc, dd)["static"]
     want = O.backward_records(ref, vox, dc, dd)
     assert grads_close(g, want) < 1e-4
+
+
+def test_tile_launch_order(s1m):
+    """salf_raster_tile_order: a permutation of the tiles, longest lists first
+    (lengths saturated at 65535), ties in tile order -- the launch order of
+    the backward (scheduling only)."""
+    from paper_2507_18713_b200 import configs
+    from paper_2507_18713_b200 import render_raster as RR
+    fb, st = RR.rasterize(s1m, configs.c2_camera(), return_state=True)
+    dc = torch.zeros((1080, 1920, 3), dtype=torch.float64, device="cuda")
+    dd = torch.zeros((1080, 1920), dtype=torch.float64, device="cuda")
+    RR.rasterize_backward(st, dc, dd, as_dict=False)
+    lens = (st.offsets[1:] - st.offsets[:-1]).cpu().numpy()
+    want = np.argsort(-np.minimum(lens, 65535), kind="stable")
+    np.testing.assert_array_equal(st.tile_order.cpu().numpy(), want)
