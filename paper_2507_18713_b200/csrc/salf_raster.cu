@@ -199,21 +199,32 @@ __global__ void k_count_ranked(int64_t n_vis, const int32_t *__restrict__ sorted
 // stable sort by tile leaves every tile's list in (z, index) order.  Lanes
 // stride over the voxel's tiles (spans can be the full image for straddling
 // voxels in reference mode).
+constexpr int kEmitLanes = 8;
+
 __global__ void k_emit(int64_t n_vis, const int32_t *__restrict__ sorted_vis, const int4 *__restrict__ span,
                        const int64_t *__restrict__ base_r, int tiles_x, uint32_t *__restrict__ keys,
                        int32_t *__restrict__ vals) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  // kEmitLanes lanes per visible voxel (~11 instances each at C2); a span
+  // covers at most the tile grid, so the 32-bit row/column split is exact
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kEmitLanes;
+  const int lane = threadIdx.x % kEmitLanes;
   if (r >= n_vis) return;
   const int32_t v = sorted_vis[r];
   const int4 s = span[v];
   const int nx = s.z - s.x + 1;
-  const int64_t cnt = (int64_t)nx * (s.w - s.y + 1);
+  const int cnt = nx * (s.w - s.y + 1);
   const int64_t b = base_r[r];
-  for (int64_t k = lane; k < cnt; k += 32) {
-    const int ty = s.y + (int)(k / nx), tx = s.x + (int)(k % nx);
+  int ty = s.y + lane / nx, tx = s.x + lane % nx;
+  const int dy = kEmitLanes / nx, dx = kEmitLanes % nx;
+  for (int k = lane; k < cnt; k += kEmitLanes) {
     keys[b + k] = (uint32_t)(ty * tiles_x + tx);
     vals[b + k] = v;
+    tx += dx;  // advance by kEmitLanes instances in row-major order
+    ty += dy;
+    if (tx > s.z) {
+      tx -= nx;
+      ++ty;
+    }
   }
 }
 
@@ -1486,7 +1497,7 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
     k_count_ranked<<<gv, bs, 0, st>>>(n_vis, w.vis_sorted, w.cnt, w.cnt_r);
     tb = w.cub_bytes;
     cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt_r, w.base_r, (int)n_vis, st);
-    k_emit<<<(unsigned)((n_vis * 32 + bs - 1) / bs), bs, 0, st>>>(n_vis, w.vis_sorted,
+    k_emit<<<(unsigned)((n_vis * kEmitLanes + bs - 1) / bs), bs, 0, st>>>(n_vis, w.vis_sorted,
                                                                  reinterpret_cast<const int4 *>(span), w.base_r,
                                                                  c.tiles_x, w.keys_a, w.vals_a);
     // stable sort by tile: each tile's list stays in depth-rank order
