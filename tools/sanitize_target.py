@@ -36,3 +36,12 @@ densify_and_prune(sc.static, rng.random(sc.static.n), DensifyConfig(budget=sc.st
 RY.trace_effects(sc, oc, o, d, 0.0, [RY.InjectedSphere([4, 4, 3], 1.0, "glass")], [0, 0, 1])
 torch.cuda.synchronize()
 print("sanitize target ok")
+# descent jump tables of every depth (query + march)
+from paper_2507_18713_b200.octree import march_segments, query_batch
+pts = rng.uniform(-1, 9, (500, 3)).clip(oc.static.root_min, oc.static.root_min + oc.static.root_edge)
+for k in range(0, 9):
+    t = oc.static.with_jump(k)
+    query_batch(t, pts)
+    march_segments(t, o, d)
+torch.cuda.synchronize()
+print("jump tables ok")
