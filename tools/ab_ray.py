@@ -36,6 +36,7 @@ ds = DeviceScene.from_scene(sc)
 oc = RY.build_scene_octrees(sc)
 lb = gen_lidar_rays(configs.c3_lidar())
 out = {"tag": tag}
+out["c3_lidar_ms"] = timeit(lambda: RY.render_lidar(ds, oc, lb))
 out["c3_fwd_ms"] = timeit(lambda: RY.integrate_rays(ds, oc, lb.origins, lb.dirs))
 rec = RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
 dd = torch.sign(torch.randn(lb.n, device="cuda", dtype=torch.float64)) / lb.n
