@@ -537,14 +537,14 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
 #ifndef SALF_RAYF_MINB_CAM
 #define SALF_RAYF_MINB_CAM 6  // camera rays (colour): measured best (C4 10.9 -> 9.7 ms)
 #endif
-template <bool kLidar, bool kSdf>
+template <bool kLidar, bool kSdf, bool kFeat = false>
 __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_CAM) k_ray_forward_fast(
     OctDev t, salf_scene_t sc, int64_t n, const double *__restrict__ orig, const double *__restrict__ dirs,
     const uint8_t *__restrict__ valid, salf_raster_opts_t opt, float *__restrict__ out_rgb,
     float *__restrict__ out_op, float *__restrict__ out_depth, double *__restrict__ saved,
     int32_t *__restrict__ status, LidarFeat lf) {
   float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const bool feat = kLidar && lf.feat != nullptr;
+  constexpr bool feat = kLidar && kFeat;  // the extension is a separate instantiation (no per-segment test)
   constexpr float kU = 5.9604645e-8f;  // 2^-24
   constexpr float kYClamp = 27.631021115928547f;
   constexpr double kLn2 = 0.6931471805599453;
@@ -1118,12 +1118,21 @@ extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t 
     cudaStream_t st = (cudaStream_t)stream;
     if (status && !opts->exact_color) {
       // certified mixed precision + fp64 redo of flagged rays (features blended in fp32 either way)
-      if (scene->density_mode == SALF_DENSITY_SDF)
+      const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
+      if (feat) {
+        if (sdf)
+          k_ray_forward_fast<true, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts,
+                                                                     nullptr, out_opacity, out_depth, saved, status, lf);
+        else
+          k_ray_forward_fast<true, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts,
+                                                                      nullptr, out_opacity, out_depth, saved, status, lf);
+      } else if (sdf) {
         k_ray_forward_fast<true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
                                                              out_opacity, out_depth, saved, status, lf);
-      else
+      } else {
         k_ray_forward_fast<true, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
                                                               out_opacity, out_depth, saved, status, lf);
+      }
       static const bool no_redo = getenv("SALF_NO_REDO") && getenv("SALF_NO_REDO")[0] == '1';  // diagnostics
       if (!no_redo)
         k_ray_forward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
