@@ -252,14 +252,12 @@ def run_ours(args, world, rank, local):
     out_host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
     loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
 
-    g32 = torch.empty(grad.shape, dtype=torch.float32, device=dev) if world > 1 else None
+    from paper_2507_18713_b200.parallel import allreduce_grad_
+    SPARSE_ALLREDUCE = os.environ.get("SALF_SPARSE_ALLREDUCE", "1") == "1"
 
     def allreduce_grad(buf):
-        # fp32 transport of the (M, 27) buffer (its values are sums of the
-        # kernels' fp32 partials): half the NVLink bytes of an f64 all-reduce
-        g32.copy_(buf)
-        dist.all_reduce(g32)
-        buf.copy_(g32)
+        # fp32 transport of the rows any rank touched (parallel.allreduce_grad_)
+        allreduce_grad_(buf, sparse=SPARSE_ALLREDUCE)
 
     def step(gt, events=None, e2e=False):
         fb, st = RR.rasterize(ds, cam, return_state=True, events=events)
@@ -450,7 +448,9 @@ def run_ours(args, world, rank, local):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256; random target image)",
         "config": {"workload": WORKLOAD, "regime": args.regime, "resolution": [w, h],
-                   "voxels": ds.n, "parallelism": f"data-parallel x{world} (C2 view per rank), grad all-reduce (NCCL, fp32 transport)",
+                   "voxels": ds.n, "parallelism": f"data-parallel x{world} (C2 view per rank), grad all-reduce "
+                   f"({os.environ.get('SALF_BENCH_BACKEND', 'nccl').upper()}, fp32 transport"
+                   + (", rows any rank touched)" if SPARSE_ALLREDUCE else ")"),
                    "l2": "flushed (256 MB write) between timed steps", "render_instances": n_inst,
                    "visible_voxels": m_vis},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(gt_host.nbytes),

@@ -80,9 +80,45 @@ def band_camera(cam: CameraModel, r0: int, r1: int) -> CameraModel:
     return replace(cam, height=r1 - r0, cy=cam.cy - r0)
 
 
+def _world(group=None) -> int:
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group)
+    return 1
+
+
 def allreduce_(t, group=None):
     """Sum a tensor across ranks in place (no-op when not distributed)."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if _world(group) > 1:
         dist.all_reduce(t, group=group)
     return t
+
+
+def allreduce_grad_(grad, group=None, sparse: bool = True, transport=None):
+    """Sum the dense (M, 27) f64 per-voxel gradient buffer across ranks.
+
+    The buffer's values are sums of the kernels' fp32 partials, so it travels
+    in fp32 (half the NVLink bytes of f64).  With `sparse`, only the rows some
+    rank wrote move: the union of the ranks' non-zero-row masks (a 1-byte MAX
+    all-reduce) selects the rows, which are gathered, summed and scattered
+    back.  A frame touches ~20% of an S1M scene, so the sum moves ~5x fewer
+    bytes; rows outside the union are zero on every rank, so the result is
+    identical to the dense sum."""
+    import torch
+    import torch.distributed as dist
+    if _world(group) <= 1:
+        return grad
+    transport = torch.float32 if transport is None else transport
+    if not sparse:
+        t = grad.to(transport)
+        dist.all_reduce(t, group=group)
+        grad.copy_(t)
+        return grad
+    mask = (grad != 0).any(dim=1).to(torch.uint8)
+    dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=group)
+    idx = mask.nonzero().squeeze(1)
+    rows = grad.index_select(0, idx).to(transport)
+    dist.all_reduce(rows, group=group)
+    grad.index_copy_(0, idx, rows.to(grad.dtype))
+    return grad

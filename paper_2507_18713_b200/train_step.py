@@ -19,7 +19,7 @@ import torch
 from . import render_raster as RR
 from . import render_ray as RY
 from .backward import backward_grad_buffer
-from .parallel import allreduce_, band_camera
+from .parallel import allreduce_, allreduce_grad_, band_camera
 from .sensors import gen_lidar_rays
 
 
@@ -84,6 +84,6 @@ def rig_step(ds, octree, sensors, targets, items, grad: torch.Tensor, depth_weig
     fs = rig_forward(ds, octree, sensors, targets, items)
     counts = allreduce_(fs.counts.clone())
     rig_backward(fs, grad, counts, depth_weight)
-    allreduce_(grad)
+    allreduce_grad_(grad)
     losses = allreduce_(fs.losses.clone())
     return losses, counts

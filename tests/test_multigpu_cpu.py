@@ -73,3 +73,36 @@ def test_gloo_allreduce_world2():
         g, c = res[r]
         assert np.all(g == 3.0)
         np.testing.assert_array_equal(c, [9.0, 1.0])
+
+
+def _grad_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2507_18713_b200.parallel import allreduce_grad_
+    rng = np.random.default_rng(rank)
+    m = 400
+    g = np.zeros((m, 27))
+    rows = rng.choice(m, size=60, replace=False)  # each rank touches its own rows (partly shared)
+    g[rows] = rng.normal(size=(60, 27)).astype(np.float32)  # fp32-representable partial sums
+    g[rows[:5], :3] = 0.0  # rows with some zero components stay touched
+    dense = torch.as_tensor(g.copy())
+    sparse = torch.as_tensor(g.copy())
+    allreduce_grad_(dense, sparse=False)
+    allreduce_grad_(sparse, sparse=True)
+    out[rank] = (g, dense.numpy().copy(), sparse.numpy().copy())
+    dist.destroy_process_group()
+
+
+def test_gloo_sparse_grad_allreduce_equals_dense_world2():
+    """parallel.allreduce_grad_: the touched-rows all-reduce (union of the
+    ranks' non-zero-row masks) gives exactly the dense fp32-transport sum."""
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_grad_worker, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    want = (res[0][0].astype(np.float32) + res[1][0].astype(np.float32)).astype(np.float64)
+    for r in (0, 1):
+        _, dense, sparse = res[r]
+        np.testing.assert_array_equal(dense, sparse)
+        np.testing.assert_array_equal(sparse, want)
