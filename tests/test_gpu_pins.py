@@ -4,7 +4,9 @@ projection at the centre pixel (:36-45), behind-camera culling (:47-51), the
 projected rect width f/9.5 (:53-59), a small voxel in a single tile (:70-78),
 per-tile order equal to the global (z, index) sort (:80-91), separated voxels
 raster == ray (:125-138), tile size as scheduling only (:140-150) and the
-raster-vs-ray mean L1 bound on a random scene (:160-166)."""
+raster-vs-ray mean L1 bound on a random scene (:160-166); and for the ray
+path (test_render_ray.py) time invariance of a static scene (:128-135) and
+the early-stopped static march against the merged path (:137-154)."""
 
 import numpy as np
 import pytest
@@ -170,3 +172,43 @@ def test_raster_ray_mean_l1_small():
     color, _op, _d = RY.render_rays_image(scene, RY.build_scene_octrees(scene), camera_rays(cam))
     color = color.cpu().numpy() if hasattr(color, "cpu") else np.asarray(color)
     assert float(np.mean(np.abs(fb.color.cpu().numpy() - color))) < 0.02
+
+
+def _random_rays(rng, n, lo, hi):
+    """Origins in the box (jittered off the grid planes), unit directions."""
+    o = rng.uniform(lo, hi, (n, 3)) + 0.0137
+    d = rng.normal(size=(n, 3))
+    return o, d / np.linalg.norm(d, axis=1, keepdims=True)
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_time_invariance_static_scene(exact):
+    """reference test_render_ray.py:128-135."""
+    from paper_2507_18713_b200 import render_ray as RY
+    scene = _random_scene(43, 100)
+    oc = RY.build_scene_octrees(scene)
+    o, d = _random_rays(np.random.default_rng(44), 50, [0, 0, 0], [8, 8, 8])
+    a = RY.integrate_rays(scene, oc, o, d, np.zeros(50), exact_color=exact)
+    b = RY.integrate_rays(scene, oc, o, d, np.full(50, 7.5), exact_color=exact)
+    assert torch.equal(a.out_color, b.out_color) and torch.equal(a.opacity, b.opacity)
+
+
+@pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
+def test_early_stopped_static_path_equals_merged_path(exact):
+    """reference test_render_ray.py:137-154: the early-stopped static march
+    equals the march-everything path taken when an (empty) actor exists."""
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.scene import Actor, Scene, SparseVoxelSet, make_actor_bounds
+    scene = _random_scene(45, 300, a_range=(2.0, 8.0))
+    o, d = _random_rays(np.random.default_rng(46), 100, [0, 0, 0], [8, 8, 8])
+    fused = RY.integrate_rays(scene, RY.build_scene_octrees(scene), o, d, exact_color=exact)
+    ghost = Actor("ghost", np.array([0.5, 0.5, 0.5]), SparseVoxelSet(make_actor_bounds([0.5, 0.5, 0.5], 0.25),
+                                                                        budget=1),
+                  times=np.array([0.0]), positions=np.zeros((1, 3)), quaternions=np.array([[1.0, 0, 0, 0]]))
+    scene_a = Scene(bounds=scene.bounds, static=scene.static, actors=[ghost])
+    merged = RY.integrate_rays(scene_a, RY.build_scene_octrees(scene_a), o, d, np.zeros(100), exact_color=exact)
+    tol = 1e-12 if exact else 2e-6  # mixed: the certified fp32 static path against the fp64 merge
+    np.testing.assert_allclose(fused.out_color.double().cpu().numpy(), merged.out_color.double().cpu().numpy(),
+                               atol=tol, rtol=0)
+    np.testing.assert_allclose(fused.opacity.double().cpu().numpy(), merged.opacity.double().cpu().numpy(),
+                               atol=tol, rtol=0)
