@@ -23,12 +23,13 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
                          grad: torch.Tensor | None = None, deterministic: bool = False) -> torch.Tensor:
     """Accumulate into / return the raw (M, 27) f64 gradient buffer.
     `deterministic=True`: per-segment rows + ordered per-voxel reduction
-    instead of atomics (bitwise identical reruns)."""
+    instead of atomics (bitwise identical reruns).
+    `d_color=None`: depth-only seeds (LiDAR), the kernel drops the colour terms."""
     lib = _lib.load()
     ds = records.scene
     dev = ds.device
     n = records.n_rays
-    dc = _lib.as_f64(d_color, dev).reshape(n * 3)
+    dc = _lib.as_f64(d_color, dev).reshape(n * 3) if d_color is not None else None
     dd = _lib.as_f64(d_depth, dev).reshape(n)
     if grad is None:
         grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
@@ -43,7 +44,7 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         _lib.check(lib.salf_ray_backward_deterministic(
             _lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(), records.dirs.data_ptr(),
-            _lib.ptr(records.valid), _lib.ref(records.opts), records.saved.data_ptr(), dc.data_ptr(),
+            _lib.ptr(records.valid), _lib.ref(records.opts), records.saved.data_ptr(), _lib.ptr(dc),
             dd.data_ptr(), grad.data_ptr(), start.data_ptr(), slots, ws.data_ptr(), wsb, _lib.stream_ptr()),
             "backward_records")
     elif n:
@@ -51,7 +52,7 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
         _lib.check(lib.salf_ray_backward(_lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(),
                                          records.dirs.data_ptr(), _lib.ptr(records.valid),
                                          _lib.ref(records.opts), records.saved.data_ptr(),
-                                         dc.data_ptr(), dd.data_ptr(), grad.data_ptr(),
+                                         _lib.ptr(dc), dd.data_ptr(), grad.data_ptr(),
                                          _lib.stream_ptr()), "backward_records")
     return grad
 

@@ -284,7 +284,8 @@ __device__ __forceinline__ void segment_grad(int mode, double delta, double sigm
 // from fp32 fields: x (local coordinates), delta, dq = t_mid - D; the running
 // transmittance T (fp32, advanced here) and the fp64 prefix sum of A w (the
 // suffix is total - prefix).  Writes the 27 components into g (g[27..31] = 0).
-template <bool kSdf>
+// kColor = false: depth-only seeds (LiDAR), the colour terms are compile-time zeros.
+template <bool kSdf, bool kColor = true>
 __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv_b, const float x[3], float delta,
                                              float dq, const float gam[4], bool want_color, const float dC[3],
                                              float dws, double total, float tail, float &T, double &prefix,
@@ -305,9 +306,10 @@ __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv
   const float alpha = clamped ? 1.f : -expm1_neg(-y);
   const float omc = clamped ? 1e-12f : om;
   float col[3] = {0.f, 0.f, 0.f};
-  if (want_color) eval_color32g(p, x, gam, col);
+  if (kColor && want_color) eval_color32g(p, x, gam, col);
   const float w = T * alpha;
-  const float A = __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], __fmaf_rn(dC[0], col[0], dws * dq)));
+  const float A = kColor ? __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], __fmaf_rn(dC[0], col[0], dws * dq)))
+                         : dws * dq;
   prefix += (double)(A * w);
   const float suffix = (float)(total - prefix);
   const float g_alpha = __fmaf_rn(A, T, -(suffix + tail) * fast_rcp(omc));
@@ -327,11 +329,11 @@ __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     const float wc = w * col[i];
-    const float gz = dC[i] * __fmaf_rn(-wc, col[i], wc);
+    const float gz = kColor ? dC[i] * __fmaf_rn(-wc, col[i], wc) : 0.f;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = gz * x[k];
+    for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = kColor ? gz * x[k] : 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) g[13 + 4 * i + k] = gz * gam[k];
+    for (int k = 0; k < 4; ++k) g[13 + 4 * i + k] = kColor ? gz * gam[k] : 0.f;
   }
   g[25] = ga;
   g[26] = gb;

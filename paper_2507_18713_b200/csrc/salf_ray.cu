@@ -701,7 +701,7 @@ struct RowSink {
 #ifndef SALF_RAYB_MINB
 #define SALF_RAYB_MINB 4  // 128 registers: measured best (5, 6 spill)
 #endif
-template <bool kExactColor, bool kMixed = false, bool kSdf = true>
+template <bool kExactColor, bool kMixed = false, bool kSdf = true, bool kColor = true>
 __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
                                                       const double *__restrict__ orig, const double *__restrict__ dirs,
                                                       const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
@@ -777,7 +777,7 @@ __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backwa
             x[k] = (float)__dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(tm, m.d[k])), ctr[k]), ax.z);
           VoxPrm p;
           load_prm(sc.prm, vid, p);
-          seg_grad_f32<kSdf>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), (float)__dsub_rn(tm, D),
+          seg_grad_f32<kSdf, kColor>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), (float)__dsub_rn(tm, D),
                              gam, want_color, dCf, dwsf, total, tailf, Tf, prefix, g);
           act = true;
           if (++n_done >= n_inc) live = false;
@@ -1146,6 +1146,27 @@ extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t 
   SALF_CATCH
 }
 
+// Mixed-precision ray backward: density mode and colour seeds (d_rgb == NULL:
+// depth-only, e.g. LiDAR) select the instantiation.
+static void launch_ray_backward_mixed(bool sdf, bool color, unsigned grid, cudaStream_t st, const OctDev &t,
+                                      const salf_scene_t &sc, int64_t n, const double *o, const double *d,
+                                      const uint8_t *valid, const salf_raster_opts_t &opts, const double *saved,
+                                      const double *d_rgb, const double *d_depth, double *grad, FeatGrad fg,
+                                      RowSink sink) {
+  if (sdf && color)
+    k_ray_backward<false, true, true, true><<<grid, 128, 0, st>>>(t, sc, n, o, d, valid, opts, saved, d_rgb, d_depth,
+                                                                  grad, fg, sink);
+  else if (sdf)
+    k_ray_backward<false, true, true, false><<<grid, 128, 0, st>>>(t, sc, n, o, d, valid, opts, saved, d_rgb,
+                                                                   d_depth, grad, fg, sink);
+  else if (color)
+    k_ray_backward<false, true, false, true><<<grid, 128, 0, st>>>(t, sc, n, o, d, valid, opts, saved, d_rgb,
+                                                                   d_depth, grad, fg, sink);
+  else
+    k_ray_backward<false, true, false, false><<<grid, 128, 0, st>>>(t, sc, n, o, d, valid, opts, saved, d_rgb,
+                                                                    d_depth, grad, fg, sink);
+}
+
 extern "C" int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
                                  const double *origins, const double *dirs, const uint8_t *valid,
                                  const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,
@@ -1158,12 +1179,10 @@ extern "C" int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *
     if (opts->exact_color)
       k_ray_backward<true><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts, saved,
                                                                      d_rgb, d_depth, grad, fg, RowSink{});
-    else if (scene->density_mode == SALF_DENSITY_SDF)
-      k_ray_backward<false, true, true><<<grid, 128, 0, (cudaStream_t)stream>>>(
-          t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth, grad, fg, RowSink{});
     else
-      k_ray_backward<false, true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(
-          t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth, grad, fg, RowSink{});
+      launch_ray_backward_mixed(scene->density_mode == SALF_DENSITY_SDF, d_rgb != nullptr, grid,
+                                (cudaStream_t)stream, t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb,
+                                d_depth, grad, fg, RowSink{});
     return check_cuda("salf_ray_backward");
   }
   SALF_CATCH
@@ -1200,12 +1219,9 @@ extern "C" int salf_ray_backward_deterministic(const salf_octree_t *tree, const 
     if (opts->exact_color)
       k_ray_backward<true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb, d_depth,
                                                  grad, fg, sink);
-    else if (scene->density_mode == SALF_DENSITY_SDF)
-      k_ray_backward<false, true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb,
-                                                              d_depth, grad, fg, sink);
     else
-      k_ray_backward<false, true, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, saved, d_rgb,
-                                                               d_depth, grad, fg, sink);
+      launch_ray_backward_mixed(scene->density_mode == SALF_DENSITY_SDF, d_rgb != nullptr, grid, st, t, *scene, n,
+                                origins, dirs, valid, *opts, saved, d_rgb, d_depth, grad, fg, sink);
     const int rc = check_cuda("salf_ray_backward_deterministic");
     if (rc != SALF_OK) return rc;
     return det_reduce_rows(n_slots, sink.row_vid, sink.rows, scene->n, grad, (char *)workspace + a + b,
@@ -1228,12 +1244,10 @@ extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t
     if (feat || opts->exact_color)  // the feature chain stays fp64
       k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
                                                                       nullptr, d_depth, grad, fg, RowSink{});
-    else if (scene->density_mode == SALF_DENSITY_SDF)
-      k_ray_backward<false, true, true><<<grid, 128, 0, (cudaStream_t)stream>>>(
-          t, *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg, RowSink{});
     else
-      k_ray_backward<false, true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(
-          t, *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg, RowSink{});
+      launch_ray_backward_mixed(scene->density_mode == SALF_DENSITY_SDF, false, grid, (cudaStream_t)stream, t,
+                                *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg,
+                                RowSink{});
     return check_cuda("salf_lidar_backward");
   }
   SALF_CATCH

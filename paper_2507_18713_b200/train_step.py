@@ -73,8 +73,7 @@ def rig_backward(fs: ForwardState, grad: torch.Tensor, global_counts: torch.Tens
             RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
         else:
             dd = depth_weight * torch.sign(diff) / n_d
-            dc = torch.zeros((diff.shape[0], 3), dtype=torch.float64, device=diff.device)
-            backward_grad_buffer(st, dc, dd, grad)
+            backward_grad_buffer(st, None, dd, grad)  # depth-only seeds: no colour terms
     return grad
 
 

@@ -98,3 +98,31 @@ def test_lidar_and_ray_backward_identical_with_jump_table():
         outs[k] = (ret.depth.cpu().numpy(), rec.depth.cpu().numpy(), g.cpu().numpy())
     for a, b in zip(outs[0], outs[7]):
         np.testing.assert_array_equal(a, b)
+
+
+def test_depth_only_ray_backward_equals_zero_colour_seeds():
+    """backward_grad_buffer(d_color=None) (the depth-only instantiation, no
+    colour terms) equals the colour path with zero colour seeds, bitwise
+    (deterministic reduction)."""
+    from paper_2507_18713_b200 import configs
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.backward import backward_grad_buffer
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.scenes import get_scene
+    from paper_2507_18713_b200.sensors import gen_lidar_rays
+    scene = get_scene("S1M", "init")
+    ds = DeviceScene.from_scene(scene)
+    oc = RY.build_scene_octrees(scene)
+    batch = gen_lidar_rays(configs.c3_lidar())
+    rec = RY.integrate_rays(ds, oc, batch.origins, batch.dirs, check_unit=False)
+    dd = torch.sign(torch.nan_to_num(rec.depth.double()) - 10.0) / 1e5
+    zc = torch.zeros((batch.origins.shape[0], 3), dtype=torch.float64, device=ds.device)
+    outs = []
+    for dc in (zc, None):
+        for det in (True, False):
+            g = torch.zeros((ds.n, 27), dtype=torch.float64, device=ds.device)
+            backward_grad_buffer(rec, dc, dd, g, deterministic=det)
+            outs.append(g.cpu().numpy())
+    np.testing.assert_array_equal(outs[0], outs[2])  # deterministic: bitwise
+    np.testing.assert_allclose(outs[1], outs[3], rtol=1e-9, atol=1e-15)  # atomics: order only
+    assert np.count_nonzero(outs[2][:, 4:25]) == 0 and np.count_nonzero(outs[2][:, :4]) > 0

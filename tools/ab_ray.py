@@ -43,6 +43,7 @@ dd = torch.sign(torch.randn(lb.n, device="cuda", dtype=torch.float64)) / lb.n
 dc = torch.zeros((lb.n, 3), device="cuda", dtype=torch.float64)
 grad = torch.zeros((ds.n, 27), device="cuda", dtype=torch.float64)
 out["c3_bwd_ms"] = timeit(lambda: backward_grad_buffer(rec, dc, dd, grad))
+out["c3_bwd_depth_only_ms"] = timeit(lambda: backward_grad_buffer(rec, None, dd, grad))
 out["c3_digest"] = [float(rec.saved[:, 6].sum()), float(torch.nan_to_num(rec.depth.double()).sum())]
 del ds, oc
 s2 = get_scene("S2M", "init")
