@@ -13,12 +13,12 @@ between them.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from types import SimpleNamespace
 
 import torch
 
 from . import render_raster as RR
 from . import render_ray as RY
-from .backward import backward_grad_buffer
 from .parallel import allreduce_, allreduce_grad_, band_camera
 from .sensors import gen_lidar_rays
 
@@ -48,9 +48,11 @@ def rig_forward(ds, octree, sensors, targets, items) -> ForwardState:
             losses[0] += diff.abs().sum()
             saved.append((st, diff))
         else:
+            # LiDAR block: the depth-only sweep kernel (no colour field), replayed by lidar_backward
             rays = gen_lidar_rays(s, device=dev)
-            rec = RY.integrate_rays(ds, octree, rays.origins[it.lo:it.hi], rays.dirs[it.lo:it.hi],
-                                    check_unit=False)  # generated sweep: unit by construction
+            blk = SimpleNamespace(origins=rays.origins[it.lo:it.hi], dirs=rays.dirs[it.lo:it.hi],
+                                  shape=(it.hi - it.lo,), generated=True)  # generated: unit by construction
+            rec = RY.render_lidar(ds, octree, blk)
             gt = torch.as_tensor(targets[it.sensor], device=dev)[it.lo:it.hi].double()
             dep = rec.depth.double()
             ok = torch.isfinite(dep) & torch.isfinite(gt)
@@ -73,7 +75,7 @@ def rig_backward(fs: ForwardState, grad: torch.Tensor, global_counts: torch.Tens
             RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
         else:
             dd = depth_weight * torch.sign(diff) / n_d
-            backward_grad_buffer(st, None, dd, grad)  # depth-only seeds: no colour terms
+            RY.lidar_backward(st, dd, grad=grad)  # depth-only seeds: no colour terms
     return grad
 
 
