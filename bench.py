@@ -246,7 +246,7 @@ def run_ours(args, world, rank, local):
     g = torch.Generator().manual_seed(rank)
     gt_host = (0.3 + 0.4 * torch.rand((h, w, 3), generator=g)).pin_memory()
     gt_dev = gt_host.to(dev)
-    dd = torch.zeros((h, w), dtype=torch.float64, device=dev)
+    dd = None  # colour L1 loss only (losses.py:22-31): no depth seeds, the backward drops the depth term
     grad = torch.zeros((ds.n, _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     out_host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
@@ -542,7 +542,7 @@ def extras(ds, args):
     dss = DeviceScene.from_scene(sur)
     ocs = RY.build_scene_octrees(sur)
     dcs = torch.full((1080, 1920, 3), 1e-7, dtype=torch.float64, device=dss.device)
-    dds = torch.zeros((1080, 1920), dtype=torch.float64, device=dss.device)
+    dds = None  # colour-only loss
 
     def fb_step():
         fb, st = RR.rasterize(dss, cam, return_state=True)

@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
     const double acc_w = s[3], acc_wt = s[4];
     // depth_valid / depth_safe / wsum_safe (backward.py:46-49)
     const bool ok = acc_w > kDepthWeightMin;
-    dd = ok ? d_depth[pix] : 0.0;
+    dd = (ok && d_depth) ? d_depth[pix] : 0.0;
     D = ok ? __ddiv_rn(acc_wt, acc_w) : 0.0;
     ws = ok ? acc_w : 1.0;
     // sum_j A_j w_j = dC . acc_rgb + dD (acc_wt - D acc_w) / ws  (suffix sums by subtraction)
@@ -861,7 +861,7 @@ __device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_r
   for (int k = 0; k < 3; ++k) dCd[k] = d_rgb[pix * 3 + k];
   const double acc_w = s[3], acc_wt = s[4];
   const bool ok = acc_w > kDepthWeightMin;  // depth_valid (backward.py:46-49)
-  const double dd = ok ? d_depth[pix] : 0.0;
+  const double dd = (ok && d_depth) ? d_depth[pix] : 0.0;
   const double D = ok ? acc_wt / acc_w : 0.0;
   q.D = D;
   const double ws = ok ? acc_w : 1.0;
@@ -878,7 +878,7 @@ __device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_r
 
 // One included segment of pixel q against staged entry e: adds its 27
 // gradient components to g.  Returns false on a miss.
-template <bool kRot, bool sdf>
+template <bool kRot, bool sdf, bool kDepth = true>
 __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF &e, BwdPix &q,
                                             float g[32]) {
   float qv[3], u0, u1;
@@ -896,7 +896,7 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
   if (!pair_hit_bwd(*ray, e, qv, u0, u1, ts)) return false;
   const float delta = u1 - u0;
   const float um = 0.5f * (u0 + u1);
-  const float dq = (float)(ts - q.D) + um;  // t_mid - D
+  const float dq = kDepth ? (float)(ts - q.D) + um : 0.f;  // t_mid - D (no depth seeds: unused)
   // (fp32 below: explicit FMAs -- this file is compiled with --fmad=false)
   float x[3];
 #pragma unroll
@@ -926,7 +926,8 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
   const float T = q.T;
   const float w = T * alpha;
   // A = dC . c + dD (t_mid - D) / ws (backward.py:52-59)
-  const float A = __fmaf_rn(q.dC[2], col[2], __fmaf_rn(q.dC[1], col[1], __fmaf_rn(q.dC[0], col[0], q.dws * dq)));
+  const float A = __fmaf_rn(q.dC[2], col[2], __fmaf_rn(q.dC[1], col[1], kDepth ? __fmaf_rn(q.dC[0], col[0], q.dws * dq)
+                                                                             : q.dC[0] * col[0]));
   q.prefix += (double)(A * w);
   const float suffix = (float)(q.total - q.prefix);
   const float g_alpha = __fmaf_rn(A, T, -(suffix + q.tail) * fast_rcp(omc));  // backward.py:62-64
@@ -1252,7 +1253,7 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
 #define SALF_BWDF_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 
-template <bool kRot, int NP, bool sdf>
+template <bool kRot, int NP, bool sdf, bool kDepth = true>
 __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
@@ -1324,7 +1325,7 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
       bool act = false;
 #pragma unroll
       for (int k = 0; k < NP; ++k)
-        if (rows_hit[k] && jb + j < q[k].n_stop) act |= bwd_segment<kRot, sdf>(sc, e, q[k], g);
+        if (rows_hit[k] && jb + j < q[k].n_stop) act |= bwd_segment<kRot, sdf, kDepth>(sc, e, q[k], g);
       float tot = 0.0f;
 #if SALF_BWD_SMEMRED
       // transpose through shared memory: 7 x STS.128 per lane, lane k sums column k
@@ -1578,13 +1579,16 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
                                                          grad, partial);
   else {
     const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
-#define SALF_LAUNCH_BWD(ROT, SDF)                                                                               \
-  k_backward_fast<ROT, SALF_BWD_NP, SDF><<<n_tiles, threads_np, 0, st>>>(*scene, c, *opts, offsets, entries, saved, \
-                                                                        d_rgb, d_depth, grad, partial, vrange, tile_order)
+    const bool depth = d_depth != nullptr;  // no depth seeds (colour-only loss): the depth term is dropped
+#define SALF_LAUNCH_BWD(ROT, SDF, DEPTH)                                                                    \
+  k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH><<<n_tiles, threads_np, 0, st>>>(                            \
+      *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order)
     if (rot) {
-      if (sdf) SALF_LAUNCH_BWD(true, true); else SALF_LAUNCH_BWD(true, false);
+      if (sdf) SALF_LAUNCH_BWD(true, true, true); else SALF_LAUNCH_BWD(true, false, true);
+    } else if (depth) {
+      if (sdf) SALF_LAUNCH_BWD(false, true, true); else SALF_LAUNCH_BWD(false, false, true);
     } else {
-      if (sdf) SALF_LAUNCH_BWD(false, true); else SALF_LAUNCH_BWD(false, false);
+      if (sdf) SALF_LAUNCH_BWD(false, true, false); else SALF_LAUNCH_BWD(false, false, false);
     }
 #undef SALF_LAUNCH_BWD
   }

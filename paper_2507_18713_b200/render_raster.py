@@ -256,6 +256,8 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
     hit pairs taken in tile-list order (DESIGN.md §raster backward).
     d_color (H, W, 3) and d_depth (H, W); returns {param: array} like
     backward_records' 'static' entry, or the raw (M, 27) f64 buffer.
+    `d_depth=None`: no depth loss (the kernel drops the depth term; same
+    values as zero depth seeds).
     `deterministic=True`: ordered per-voxel reduction instead of atomics,
     bitwise identical across runs."""
     lib = _lib.load()
@@ -263,7 +265,7 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
     dev = ds.device
     h, w = state.cam.height, state.cam.width
     dc = _lib.as_f64(d_color, dev).reshape(h * w * 3)
-    dd = _lib.as_f64(d_depth, dev).reshape(h * w)
+    dd = _lib.as_f64(d_depth, dev).reshape(h * w) if d_depth is not None else None  # None: no depth loss
     if grad is None:
         grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
     if state.n_instances:
@@ -283,13 +285,13 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
             _lib.check(lib.salf_raster_backward_deterministic(
                 _lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts), state.offsets.data_ptr(),
-                state.entries.data_ptr(), state.n_instances, state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
+                state.entries.data_ptr(), state.n_instances, state.saved.data_ptr(), dc.data_ptr(), _lib.ptr(dd),
                 grad.data_ptr(), _lib.ptr(state.vrange), _lib.ptr(state.tile_order), ws.data_ptr(), wsb,
                 _lib.stream_ptr()), "rasterize_backward")
         else:
             _lib.check(lib.salf_raster_backward(_lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts),
                                                 state.offsets.data_ptr(), state.entries.data_ptr(),
-                                                state.saved.data_ptr(), dc.data_ptr(), dd.data_ptr(),
+                                                state.saved.data_ptr(), dc.data_ptr(), _lib.ptr(dd),
                                                 grad.data_ptr(), _lib.ptr(state.vrange), _lib.ptr(state.tile_order),
                                                 _lib.stream_ptr()), "rasterize_backward")
         if ev is not None:

@@ -71,8 +71,7 @@ def rig_backward(fs: ForwardState, grad: torch.Tensor, global_counts: torch.Tens
     for it, (st, diff) in zip(fs.items, fs.saved):
         if it.kind == "raster_band":
             dc = torch.sign(diff) / n_c
-            dd = torch.zeros(diff.shape[:2], dtype=torch.float64, device=diff.device)
-            RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
+            RR.rasterize_backward(st, dc, None, grad, as_dict=False)  # cameras carry the colour loss only
         else:
             dd = depth_weight * torch.sign(diff) / n_d
             RY.lidar_backward(st, dd, grad=grad)  # depth-only seeds: no colour terms

@@ -212,3 +212,23 @@ def test_early_stopped_static_path_equals_merged_path(exact):
                                atol=tol, rtol=0)
     np.testing.assert_allclose(fused.opacity.double().cpu().numpy(), merged.opacity.double().cpu().numpy(),
                                atol=tol, rtol=0)
+
+
+def test_colour_only_backward_equals_zero_depth_seeds():
+    """rasterize_backward(d_depth=None) -- the colour-only instantiation --
+    gives the gradients of zero depth seeds (bitwise, deterministic mode)."""
+    from paper_2507_18713_b200 import render_raster as RR
+    scene = _random_scene(66, 300)
+    cam = _cam_at([13.0, 11.0, 7.0], [4.0, 4.0, 2.0], width=80, height=72, f=70.0)
+    fb, st = RR.rasterize(scene, cam, return_state=True)
+    rng = np.random.default_rng(7)
+    dc = torch.as_tensor(np.sign(rng.normal(size=(72, 80, 3))) / 1e4, device="cuda")
+    zd = torch.zeros((72, 80), dtype=torch.float64, device="cuda")
+    for det in (True, False):
+        a = RR.rasterize_backward(st, dc, zd, as_dict=False, deterministic=det).cpu().numpy()
+        b = RR.rasterize_backward(st, dc, None, as_dict=False, deterministic=det).cpu().numpy()
+        if det:
+            np.testing.assert_array_equal(a, b)
+        else:
+            np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-18)
+        assert np.count_nonzero(b) > 0
