@@ -191,11 +191,13 @@ def _dist_init(args):
     return world, rank, local
 
 
-def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles):
-    """Compulsory HBM bytes per launch."""
+def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles, depth_seeds=False):
+    """Compulsory HBM bytes per launch; the backward
+    reads dL/dC (24 B/pixel) and, with depth seeds, dL/dD (8 B/pixel)."""
     rec = 32 + 16 + 112  # geo + ab + prm per visible voxel
     fwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 20 * hw + 64 * hw
-    bwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 64 * hw + 32 * hw + 216 * m_vis
+    seeds = (32 if depth_seeds else 24) * hw
+    bwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 64 * hw + seeds + 216 * m_vis
     return fwd, bwd
 
 

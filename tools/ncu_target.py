@@ -13,7 +13,7 @@ sc = get_scene("S1M", regime)
 ds = DeviceScene.from_scene(sc)
 cam = configs.c2_camera()
 dc = torch.full((1080, 1920, 3), 1e-6, device="cuda", dtype=torch.float64)
-dd = torch.zeros((1080, 1920), device="cuda", dtype=torch.float64)
+dd = None  # colour-only loss, as bench.py
 oc = RY.build_scene_octrees(sc)
 lb = gen_lidar_rays(configs.c3_lidar())
 for _ in range(3):
