@@ -48,6 +48,8 @@ for exact in (False, True):
     key = "exact" if exact else "fast"
     out[f"{key}_fwd_ms"] = timeit(lambda: RR.rasterize(ds, cam, return_state=True, exact_color=exact))
     out[f"{key}_bwd_ms"] = timeit(lambda: RR.rasterize_backward(st, dc, dd, grad=grad.zero_(), as_dict=False))
+    out[f"{key}_bwd_colour_only_ms"] = timeit(lambda: RR.rasterize_backward(st, dc, None, grad=grad.zero_(),
+                                                                            as_dict=False))
     out[f"{key}_bwd_det_ms"] = timeit(lambda: RR.rasterize_backward(st, dc, dd, grad=grad.zero_(), as_dict=False,
                                                                     deterministic=True), n=5)
     grad.zero_()
