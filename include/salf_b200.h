@@ -149,7 +149,9 @@ int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
 
 /* Raster backward (no reference function: defined as backward_records,
  * backward.py:35-101, applied to the raster pairs -- see DESIGN.md).
- * d_rgb (H*W*3) and d_depth (H*W) f64; grad (M x 27 f64, accumulated). */
+ * d_rgb (H*W*3) and d_depth (H*W) f64; grad (M x 27 f64, accumulated).
+ * d_depth may be NULL (no depth loss): a colour-only kernel runs, with the
+ * values zero depth seeds would give. */
 int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                          const salf_raster_opts_t *opts, const int64_t *offsets,
                          const int32_t *entries, const double *saved, const double *d_rgb,
@@ -306,7 +308,9 @@ int salf_ray_backward_merge(const salf_octree_t *tree, const salf_scene_t *scene
                             double *ex_grad, void *stream);
 
 /* backward_records (backward.py:35-101) for the ray path, re-marching each
- * ray: d_rgb (N x 3), d_depth (N) f64; grad (M x 27 f64, accumulated). */
+ * ray: d_rgb (N x 3), d_depth (N) f64; grad (M x 27 f64, accumulated).
+ * d_rgb may be NULL (depth-only seeds, e.g. LiDAR): a kernel without the
+ * colour terms runs, with the values zero colour seeds would give. */
 int salf_ray_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
                       const double *origins, const double *dirs, const uint8_t *valid,
                       const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,
