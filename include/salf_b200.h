@@ -202,6 +202,10 @@ int salf_camera_rays(const salf_camera_t *cam, double *origins, double *dirs,
 /* gen_lidar_rays (sensors.py:193-232), beam-major. */
 int salf_lidar_rays(const salf_lidar_t *lidar, const double *beam_elevations, double *origins,
                     double *dirs, double *t_stamps, void *stream);
+/* The same as a whole RayBatch in one launch: plus keys (N x 2 i64: beam,
+ * step; sensors.py:228-231) and valid (N u8, all 1); keys / valid nullable. */
+int salf_lidar_batch(const salf_lidar_t *lidar, const double *beam_elevations, double *origins,
+                     double *dirs, double *t_stamps, int64_t *keys, uint8_t *valid, void *stream);
 
 /* ---- octree (reference octree.py) -------------------------------------- */
 

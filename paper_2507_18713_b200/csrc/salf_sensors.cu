@@ -110,7 +110,8 @@ __global__ void k_camera_rays(CamDev cd, double *__restrict__ origins, double *_
 }
 
 __global__ void k_lidar_rays(salf_lidar_t l, bool spin, const double *__restrict__ elev, double *__restrict__ origins,
-                             double *__restrict__ dirs, double *__restrict__ tst) {
+                             double *__restrict__ dirs, double *__restrict__ tst, int64_t *__restrict__ keys,
+                             uint8_t *__restrict__ valid) {
   const int64_t n = (int64_t)l.n_beams * l.steps;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -145,6 +146,11 @@ __global__ void k_lidar_rays(salf_lidar_t l, bool spin, const double *__restrict
     dirs[3 * i + k] = w[k];
   }
   if (tst) tst[i] = __dadd_rn(l.t0, dt);
+  if (keys) {  // RayBatch.keys = (beam, step), sensors.py:228-231
+    keys[2 * i] = beam;
+    keys[2 * i + 1] = j;
+  }
+  if (valid) valid[i] = 1;
 }
 
 }  // namespace salf
@@ -176,8 +182,24 @@ extern "C" int salf_lidar_rays(const salf_lidar_t *lidar, const double *beam_ele
     const int64_t n = (int64_t)lidar->n_beams * lidar->steps;
     if (n == 0) return SALF_OK;
     k_lidar_rays<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*lidar, spin, beam_elevations, origins,
-                                                                                 dirs, t_stamps);
+                                                                                 dirs, t_stamps, nullptr, nullptr);
     return check_cuda("salf_lidar_rays");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_lidar_batch(const salf_lidar_t *lidar, const double *beam_elevations, double *origins,
+                                double *dirs, double *t_stamps, int64_t *keys, uint8_t *valid, void *stream) {
+  SALF_TRY {
+    if (lidar->steps < 1) return set_error(SALF_EINVAL, "steps must be at least 1");
+    if (!(lidar->scan_period > 0)) return set_error(SALF_EINVAL, "scan_period must be positive");
+    const bool spin = lidar->angular_velocity[0] != 0.0 || lidar->angular_velocity[1] != 0.0 ||
+                      lidar->angular_velocity[2] != 0.0;
+    const int64_t n = (int64_t)lidar->n_beams * lidar->steps;
+    if (n == 0) return SALF_OK;
+    k_lidar_rays<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*lidar, spin, beam_elevations, origins,
+                                                                                 dirs, t_stamps, keys, valid);
+    return check_cuda("salf_lidar_batch");
   }
   SALF_CATCH
 }

@@ -226,15 +226,31 @@ def gen_lidar_rays(lidar: LidarModel, t0: float = 0.0, device=None) -> RayBatch:
     o = torch.empty((n, 3), dtype=torch.float64, device=dev)
     d = torch.empty((n, 3), dtype=torch.float64, device=dev)
     ts = torch.empty(n, dtype=torch.float64, device=dev)
-    el = torch.as_tensor(lidar.beam_elevations, dtype=torch.float64, device=dev)
+    keys = torch.empty((n, 2), dtype=torch.int64, device=dev)
+    valid = torch.empty(n, dtype=torch.bool, device=dev)
+    el = _elevations_on(lidar.beam_elevations, dev)
     ls = lidar.c_struct(t0)
-    with torch.cuda.device(dev):
-        _lib.check(lib.salf_lidar_rays(_lib.ref(ls), el.data_ptr(), o.data_ptr(), d.data_ptr(),
-                                       ts.data_ptr(), _lib.stream_ptr()), "lidar_rays")
-    beams = torch.arange(nb, device=dev).repeat_interleave(steps)
-    steps_i = torch.arange(steps, device=dev).repeat(nb)
-    return RayBatch(o, d, ts, torch.stack([beams, steps_i], 1),
-                    torch.ones(n, dtype=torch.bool, device=dev), (nb, steps), generated=True)
+    with torch.cuda.device(dev):  # one launch: rays, time stamps, keys and the valid mask
+        _lib.check(lib.salf_lidar_batch(_lib.ref(ls), el.data_ptr(), o.data_ptr(), d.data_ptr(), ts.data_ptr(),
+                                        keys.data_ptr(), valid.data_ptr(), _lib.stream_ptr()), "lidar_rays")
+    return RayBatch(o, d, ts, keys, valid, (nb, steps), generated=True)
+
+
+_ELEV_CACHE: dict = {}
+
+
+def _elevations_on(elev, dev) -> torch.Tensor:
+    """Device copy of a LiDAR's beam elevations, cached by value: a sweep per
+    frame does not pay a synchronous host-to-device copy each time."""
+    a = np.ascontiguousarray(np.asarray(elev, np.float64))
+    key = (str(dev), a.tobytes())
+    t = _ELEV_CACHE.get(key)
+    if t is None:
+        if len(_ELEV_CACHE) > 64:
+            _ELEV_CACHE.clear()
+        t = torch.as_tensor(a, device=dev)
+        _ELEV_CACHE[key] = t
+    return t
 
 
 def sensor_from_dict(d: dict):
