@@ -198,6 +198,10 @@ int salf_ray_backward_deterministic(const salf_octree_t *tree, const salf_scene_
  * origins/dirs (N x 3 f64), t_stamps (N f64), valid (N u8), N = W*H. */
 int salf_camera_rays(const salf_camera_t *cam, double *origins, double *dirs,
                      double *t_stamps, uint8_t *valid, void *stream);
+/* The same as a whole RayBatch in one launch: plus keys (N x 2 i64: row,
+ * col; sensors.py:157-160), nullable. */
+int salf_camera_batch(const salf_camera_t *cam, double *origins, double *dirs, double *t_stamps,
+                      uint8_t *valid, int64_t *keys, void *stream);
 
 /* gen_lidar_rays (sensors.py:193-232), beam-major. */
 int salf_lidar_rays(const salf_lidar_t *lidar, const double *beam_elevations, double *origins,

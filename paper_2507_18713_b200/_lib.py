@@ -88,6 +88,7 @@ SIGNATURES = {
     "salf_camera_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_lidar_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_lidar_batch": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_camera_batch": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "salf_octree_build_host": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, C.c_int64, vp, vp]),
     "salf_octree_query": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp]),
     "salf_octree_jump_bytes": (C.c_size_t, [C.c_int32]),

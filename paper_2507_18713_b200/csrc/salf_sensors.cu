@@ -43,7 +43,7 @@ __device__ __forceinline__ void matvec_es(const double R[9], const double v[3], 
 }
 
 __global__ void k_camera_rays(CamDev cd, double *__restrict__ origins, double *__restrict__ dirs,
-                              double *__restrict__ tst, uint8_t *__restrict__ valid) {
+                              double *__restrict__ tst, uint8_t *__restrict__ valid, int64_t *__restrict__ keys) {
   const salf_camera_t &c = cd.c;
   const int64_t n = (int64_t)c.width * c.height;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -107,6 +107,10 @@ __global__ void k_camera_rays(CamDev cd, double *__restrict__ origins, double *_
   }
   if (tst) tst[i] = ts;
   if (valid) valid[i] = ok ? 1 : 0;
+  if (keys) {  // RayBatch.keys = (row, col), sensors.py:157-160
+    keys[2 * i] = row;
+    keys[2 * i + 1] = col;
+  }
 }
 
 __global__ void k_lidar_rays(salf_lidar_t l, bool spin, const double *__restrict__ elev, double *__restrict__ origins,
@@ -166,8 +170,25 @@ extern "C" int salf_camera_rays(const salf_camera_t *cam, double *origins, doubl
     cd.c = *cam;
     cd.spin = cam->angular_velocity[0] != 0.0 || cam->angular_velocity[1] != 0.0 || cam->angular_velocity[2] != 0.0;
     const int64_t n = (int64_t)cam->width * cam->height;
-    k_camera_rays<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(cd, origins, dirs, t_stamps, valid);
+    k_camera_rays<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(cd, origins, dirs, t_stamps, valid,
+                                                                                  nullptr);
     return check_cuda("salf_camera_rays");
+  }
+  SALF_CATCH
+}
+
+extern "C" int salf_camera_batch(const salf_camera_t *cam, double *origins, double *dirs, double *t_stamps,
+                                 uint8_t *valid, int64_t *keys, void *stream) {
+  SALF_TRY {
+    if (cam->width < 1 || cam->height < 1) return set_error(SALF_EINVAL, "image dimensions must be at least 1");
+    if (cam->kind < 0 || cam->kind > 2) return set_error(SALF_EINVAL, "unknown camera kind %d", cam->kind);
+    CamDev cd;
+    cd.c = *cam;
+    cd.spin = cam->angular_velocity[0] != 0.0 || cam->angular_velocity[1] != 0.0 || cam->angular_velocity[2] != 0.0;
+    const int64_t n = (int64_t)cam->width * cam->height;
+    k_camera_rays<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(cd, origins, dirs, t_stamps, valid,
+                                                                                  keys);
+    return check_cuda("salf_camera_batch");
   }
   SALF_CATCH
 }

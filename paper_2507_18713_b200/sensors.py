@@ -188,14 +188,13 @@ def _camera_batch(cam: CameraModel, t0: float, rolling: bool, device=None, strea
     o = torch.empty((n, 3), dtype=torch.float64, device=dev)
     d = torch.empty((n, 3), dtype=torch.float64, device=dev)
     ts = torch.empty(n, dtype=torch.float64, device=dev)
-    valid = torch.empty(n, dtype=torch.uint8, device=dev)
+    valid = torch.empty(n, dtype=torch.bool, device=dev)  # the kernel writes 0 / 1 bytes
+    keys = torch.empty((n, 2), dtype=torch.int64, device=dev)
     cs = cam.c_struct(t0, rolling)
-    with torch.cuda.device(dev):
-        _lib.check(lib.salf_camera_rays(_lib.ref(cs), o.data_ptr(), d.data_ptr(), ts.data_ptr(),
-                                        valid.data_ptr(), _lib.stream_ptr(stream)), "camera_rays")
-    rows = torch.arange(h, device=dev).repeat_interleave(w)
-    cols = torch.arange(w, device=dev).repeat(h)
-    return RayBatch(o, d, ts, torch.stack([rows, cols], 1), valid.bool(), (h, w), generated=True)
+    with torch.cuda.device(dev):  # one launch: rays, time stamps, valid mask and keys
+        _lib.check(lib.salf_camera_batch(_lib.ref(cs), o.data_ptr(), d.data_ptr(), ts.data_ptr(),
+                                         valid.data_ptr(), keys.data_ptr(), _lib.stream_ptr(stream)), "camera_rays")
+    return RayBatch(o, d, ts, keys, valid, (h, w), generated=True)
 
 
 def gen_camera_rays(cam: CameraModel, t0: float = 0.0, device=None) -> RayBatch:
