@@ -32,11 +32,16 @@
 
 namespace salf_fm {
 
-// 1/k! for k = 13 .. 2 (Horner order)
-SALF_FM_CONST double kInvFact[12] = {
-    1.6059043836821613e-10, 2.08767569878681e-09,  2.505210838544172e-08, 2.755731922398589e-07,
-    2.7557319223985893e-06, 2.48015873015873e-05,  0.0001984126984126984, 0.001388888888888889,
-    0.008333333333333333,   0.041666666666666664, 0.16666666666666666,   0.5};
+// 1/k! for k = 13 .. 2 (Horner order): a constant-bank copy for the device,
+// a plain one for host callers (the host-side checks of these functions)
+#define SALF_FM_INV_FACT                                                                                      \
+  {1.6059043836821613e-10, 2.08767569878681e-09,  2.505210838544172e-08, 2.755731922398589e-07,               \
+   2.7557319223985893e-06, 2.48015873015873e-05,  0.0001984126984126984, 0.001388888888888889,                \
+   0.008333333333333333,   0.041666666666666664, 0.16666666666666666,   0.5}
+SALF_FM_CONST double kInvFact[12] = SALF_FM_INV_FACT;
+#ifdef __CUDACC__
+static const double kInvFactHost[12] = SALF_FM_INV_FACT;
+#endif
 
 constexpr double kLog2e = 1.4426950408889634;
 constexpr double kLn2Hi = 6.93147180369123816490e-01;  // 0x3fe62e42fee00000 (trailing zeros)
@@ -74,9 +79,14 @@ SALF_FM_FN double fm_pow2(int n) {  // 2^n for -1022 <= n <= 1023
 
 // expm1(r) for |r| <= ~0.35
 SALF_FM_FN double fm_expm1_core(double r) {
-  double p = kInvFact[0];
+#if defined(__CUDACC__) && !defined(__CUDA_ARCH__)
+  const double *c = kInvFactHost;
+#else
+  const double *c = kInvFact;
+#endif
+  double p = c[0];
 #pragma unroll
-  for (int k = 1; k < 12; ++k) p = fm_fma(p, r, kInvFact[k]);
+  for (int k = 1; k < 12; ++k) p = fm_fma(p, r, c[k]);
   return fm_fma(fm_mul(r, r), p, r);
 }
 

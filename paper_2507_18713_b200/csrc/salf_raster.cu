@@ -16,6 +16,7 @@
 //   k_backward     replay of k_composite producing per-voxel gradients with
 //                  warp-aggregated atomics (definition: DESIGN.md §raster backward)
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "salf_common.cuh"
 #include "salf_internal.h"
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(256, SALF_BWD_MINB) k_backward(salf_scene_t sc
   const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
   const int px = tx * c.tile + lx, py = ty * c.tile + ly;
   const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
-  const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
+  const int64_t beg = offsets[tile_id];
   const double keep = 1.0 - opt.stop_threshold;
   const int nthreads = blockDim.x;
 
@@ -1412,7 +1413,7 @@ static size_t cub_bytes_needed(int64_t n_voxels, int64_t capacity) {
                                   (int32_t *)nullptr, n);
   cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
                                   (int32_t *)nullptr, (int64_t)std::max<int64_t>(capacity, 1));
-  cub::DeviceSelect::Flagged(nullptr, d, cub::CountingInputIterator<int32_t>(0), (const uint8_t *)nullptr,
+  cub::DeviceSelect::Flagged(nullptr, d, thrust::counting_iterator<int32_t>(0), (const uint8_t *)nullptr,
                              (int32_t *)nullptr, (int64_t *)nullptr, n);
   cub::DeviceReduce::Sum(nullptr, e, (const int64_t *)nullptr, (int64_t *)nullptr, n);
   return std::max(std::max(a, b), std::max(c, std::max(d, e)));
@@ -1473,7 +1474,7 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
     // instance counts, visible voxels (non-empty span, ascending index) and the total
     k_span_count<<<gb, bs, 0, st>>>(n, reinterpret_cast<const int4 *>(span), w.cnt, w.vis);
     size_t tb = w.cub_bytes;
-    cub::DeviceSelect::Flagged(w.cub_tmp, tb, cub::CountingInputIterator<int32_t>(0), w.vis, w.vis_idx, w.nums,
+    cub::DeviceSelect::Flagged(w.cub_tmp, tb, thrust::counting_iterator<int32_t>(0), w.vis, w.vis_idx, w.nums,
                                (int)n, st);
     tb = w.cub_bytes;
     cub::DeviceReduce::Sum(w.cub_tmp, tb, w.cnt, w.nums + 1, (int)n, st);
@@ -1665,7 +1666,7 @@ static DetWs carve_det(void *ws, int64_t ni, size_t *total) {
   size_t a = 0, b = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
                                   (int32_t *)nullptr, (int64_t)ni);
-  cub::DeviceSelect::Flagged(nullptr, b, cub::CountingInputIterator<int32_t>(0), (const uint8_t *)nullptr,
+  cub::DeviceSelect::Flagged(nullptr, b, thrust::counting_iterator<int32_t>(0), (const uint8_t *)nullptr,
                              (int32_t *)nullptr, (int64_t *)nullptr, (int)ni);
   w.cub_bytes = std::max(a, b);
   w.cub_tmp = take(w.cub_bytes);
@@ -1697,7 +1698,7 @@ int salf::det_reduce_rows(int64_t n_rows, const uint32_t *row_vid, const float *
                                   bits_for((uint64_t)std::max<int64_t>(n_vox, 1)), st);
   k_run_heads<<<g, bs, 0, st>>>(n_rows, w.vid_sorted, w.head_flag);
   tb = w.cub_bytes;
-  cub::DeviceSelect::Flagged(w.cub_tmp, tb, cub::CountingInputIterator<int32_t>(0), w.head_flag, w.heads, w.n_runs,
+  cub::DeviceSelect::Flagged(w.cub_tmp, tb, thrust::counting_iterator<int32_t>(0), w.head_flag, w.heads, w.n_runs,
                              (int)n_rows, st);
   const int64_t max_runs = std::min<int64_t>(n_rows, std::max<int64_t>(n_vox, 1) + 1);
   k_det_reduce<<<(unsigned)((max_runs * 32 + bs - 1) / bs), bs, 0, st>>>(n_rows, w.n_runs, w.heads, w.vid_sorted,
