@@ -55,7 +55,7 @@ def main(rep, out_md, traffic_json=None):
         key = {"k_composite": "raster_composite", "k_composite_fast": "raster_composite",
                "k_composite_redo": "raster_composite_redo", "k_backward": "raster_backward",
                "k_backward_fast": "raster_backward", "k_ray_forward": "ray_forward",
-               "k_ray_forward_fast": "ray_forward"}.get(
+               "k_ray_forward_fast": "ray_forward", "k_ray_backward": "ray_backward"}.get(
             name.split("<")[0].replace("salf::", ""), name)
         traffic[key] = rd + wr
         metrics[key] = {"duration_ms": dur_ms, "dram_bytes": rd + wr,

@@ -1,4 +1,4 @@
-"""Short workload for ncu captures: C2 raster fwd+bwd and C3 LiDAR on S1M (init)."""
+"""Short workload for ncu captures: C2 raster fwd+bwd and C3 LiDAR fwd+bwd on S1M (init)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -19,6 +19,7 @@ lb = gen_lidar_rays(configs.c3_lidar())
 for _ in range(3):
     fb, st = RR.rasterize(ds, cam, return_state=True)
     RR.rasterize_backward(st, dc, dd, as_dict=False)
-    RY.render_lidar(ds, oc, lb)
+    ret = RY.render_lidar(ds, oc, lb)
+    RY.lidar_backward(ret, torch.sign(torch.nan_to_num(ret.depth.double()) - 10.0) / 1e5)
 torch.cuda.synchronize()
 print("ok")
