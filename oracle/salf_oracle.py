@@ -326,13 +326,19 @@ def project_voxels(vox: Voxels, cam: Camera, near=NEAR_PLANE):
     return rmin, rmax, zc, culled
 
 
-def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE, window=None):
+def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE, window=None,
+                 tiles=None, proj=None):
     """render_raster.py:143-182 -> (tiles_x, tiles_y, offsets int64[T+1], entries int64).
 
     `window=(tx0, ty0, tx1, ty1)` (inclusive tile rectangle) bins only those
     tiles; their lists are identical to the full binning's (tiles are
-    independent), the others come out empty.  Used to time bounded samples."""
-    rmin, rmax, zc, culled = project_voxels(vox, cam, near)
+    independent), the others come out empty.  Used to time bounded samples.
+    `tiles` (iterable of tile ids) does the same for an arbitrary tile set
+    without expanding the other tiles' instances: each list is the visible
+    voxels whose span covers the tile, ordered by lexsort((vid, z)) -- the
+    reference's lexsort((vid, z, tile)) restricted to one tile.  `proj` reuses
+    a project_voxels() result (same camera and near plane)."""
+    rmin, rmax, zc, culled = project_voxels(vox, cam, near) if proj is None else proj
     tx_n = -(-cam.width // tile)
     ty_n = -(-cam.height // tile)
     nt = tx_n * ty_n
@@ -349,6 +355,19 @@ def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE, wind
     x1 = (u_hi[idx] // tile).astype(np.int64)
     y0 = (v_lo[idx] // tile).astype(np.int64)
     y1 = (v_hi[idx] // tile).astype(np.int64)
+    if tiles is not None:
+        counts = np.zeros(nt, np.int64)
+        lists = []
+        for t in sorted(set(int(t) for t in tiles)):
+            ty, tx = divmod(t, tx_n)
+            sel = idx[(x0 <= tx) & (tx <= x1) & (y0 <= ty) & (ty <= y1)]
+            sel = sel[np.lexsort((sel, zc[sel]))]
+            counts[t] = sel.size
+            lists.append(sel)
+        offsets = np.zeros(nt + 1, np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        ent = np.concatenate(lists) if lists else np.zeros(0, np.int64)
+        return tx_n, ty_n, offsets, ent.astype(np.int64)
     if window is not None:
         x0, y0 = np.maximum(x0, window[0]), np.maximum(y0, window[1])
         x1, y1 = np.minimum(x1, window[2]), np.minimum(y1, window[3])
@@ -396,7 +415,8 @@ def _pair_segments(vox: Voxels, origin, dirs, t_near, pix, vid):
 
 
 def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SIZE,
-              near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, rows=None, window=None):
+              near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, rows=None, window=None, tiles=None,
+              proj=None):
     """render_raster.py:201-301, tile by tile.
 
     `rows=(r0, r1)` restricts work to tile rows r0..r1-1 and `window` to a
@@ -406,7 +426,7 @@ def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SI
     h, w = cam.height, cam.width
     if rows is not None and window is None:
         window = (0, rows[0], -(-w // tile) - 1, rows[1] - 1)
-    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window)
+    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window, tiles, proj)
     dirs, t_near = _pixel_rays(cam, near)
     keep = 1.0 - stop_threshold
     acc_c = np.zeros((h * w, 3))
@@ -445,7 +465,8 @@ def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SI
 
 
 def raster_records(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SIZE,
-                   near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, window=None):
+                   near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, window=None, tiles=None,
+                   proj=None):
     """Raster pairs restated as ray-path records (one ray per pixel, row-major).
 
     The reference has no raster backward; its gradient is defined by
@@ -454,7 +475,7 @@ def raster_records(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TI
     (render_ray.py:86-114) and differentiated by `backward_records`
     (backward.py:35-101).  Misses carry alpha = 0 and drop out exactly."""
     h, w = cam.height, cam.width
-    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window)
+    tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window, tiles, proj)
     dirs, t_near = _pixel_rays(cam, near)
     chunks = []
     for t in range(tx_n * ty_n):
@@ -730,8 +751,18 @@ def render_rays_image(vox, tree, rays, background=(0.0, 0.0, 0.0), stop_threshol
 # ---------------------------------------------------------------------------
 # backward (reference backward.py:26-101, static owner) + L1 seeds (losses.py:22-46)
 
-def backward_records(rec, vox: Voxels, d_color, d_depth):
-    """Dense per-voxel gradients {w_s (M,4), w_c (M,3,3), w_sh (M,3,4), log_a, log_b}."""
+def backward_records(rec, vox: Voxels, d_color, d_depth, magnitude=False):
+    """Dense per-voxel gradients {w_s (M,4), w_c (M,3,3), w_sh (M,3,4), log_a, log_b}.
+
+    `magnitude=True` (test-side conditioning, no reference counterpart) returns
+    instead, per gradient element, the sum over segments of the ABSOLUTE values
+    of the terms the reference adds (each product taken with |.| factors, the
+    suffix sum of |A w|).  It is the scale against which any finite-precision
+    evaluation of that sum is conditioned: an element that is a near-cancelling
+    sum of large terms cannot be reproduced to 1e-4 of its own (small) value by
+    any fp32 or reordered fp64 implementation, only to a fraction of this scale."""
+    if magnitude:
+        return _backward_magnitude(rec, vox, d_color, d_depth)
     m = vox.n
     g = dict(w_s=np.zeros((m, 4)), w_c=np.zeros((m, 3, 3)), w_sh=np.zeros((m, 3, 4)),
              log_a=np.zeros(m), log_b=np.zeros(m))
@@ -771,6 +802,53 @@ def backward_records(rec, vox: Voxels, d_color, d_depth):
     else:
         np.add.at(g["w_s"], vid, (g_sigma * rec["sigma"])[:, None] * xh)
     np.add.at(g["w_c"], vid, np.einsum("ni,nj->nij", g_z, rec["x"]))
+    np.add.at(g["w_sh"], vid, np.einsum("ni,nj->nij", g_z, gamma))
+    return g
+
+
+def _backward_magnitude(rec, vox: Voxels, d_color, d_depth):
+    """backward_records(..., magnitude=True): the chain of backward.py:52-100
+    with every factor replaced by its absolute value."""
+    m = vox.n
+    g = dict(w_s=np.zeros((m, 4)), w_c=np.zeros((m, 3, 3)), w_sh=np.zeros((m, 3, 4)),
+             log_a=np.zeros(m), log_b=np.zeros(m))
+    ray = rec["ray"]
+    if ray.size == 0:
+        return g
+    inc = rec["included"]
+    a = np.clip(rec["alpha"], 0.0, ALPHA_MAX)
+    tb = rec["t_before"]
+    w = np.where(inc, tb * a, 0.0)
+    tm = 0.5 * (rec["t0"] + rec["t1"])
+    delta = rec["t1"] - rec["t0"]
+    ok = rec["weight_sum"] > 0.5
+    dd = np.abs(np.where(ok, d_depth, 0.0))
+    dep = np.where(ok, rec["depth"], 0.0)
+    ws = np.where(ok, rec["weight_sum"], 1.0)
+    dc = np.abs(d_color)
+    A = np.einsum("nc,nc->n", dc[ray], np.abs(rec["color"])) + dd[ray] * np.abs(tm - dep[ray]) / ws[ray]
+    tail = np.einsum("nc,c->n", dc, np.abs(rec["background"])) * rec["t_final"]
+    vals = np.where(inc, A * w, 0.0)
+    cs = np.cumsum(vals)
+    gs = rec["group_start"]
+    suffix = np.abs(np.repeat(cs[np.maximum(gs[1:] - 1, 0)], np.diff(gs)) - cs)
+    g_alpha = np.where(inc, A * tb + (suffix + tail[ray]) / (1.0 - a), 0.0)
+    g_sigma = g_alpha * delta * np.exp(-rec["sigma"] * delta)
+    g_z = dc[ray] * w[:, None] * np.abs(rec["color"] * (1.0 - rec["color"]))
+    gamma = np.abs(sh_basis(rec["omega"]))
+    xh = np.abs(np.concatenate([rec["x"], np.ones((ray.size, 1))], axis=1))
+    vid = rec["vid"]
+    if rec["density_mode"] == "sdf":
+        ap, bp = np.exp(vox.log_a[vid]), np.exp(vox.log_b[vid])
+        s = rec["s_field"]
+        e = np.exp(-np.abs(s) / bp)
+        ds = np.where(s == 0.0, 0.0, g_sigma * (ap / (2.0 * bp)) * e)
+        np.add.at(g["log_a"], vid, g_sigma * np.abs(rec["sigma"]))
+        np.add.at(g["log_b"], vid, g_sigma * ((ap / (2.0 * bp)) * np.abs(s) * e))
+        np.add.at(g["w_s"], vid, ds[:, None] * xh)
+    else:
+        np.add.at(g["w_s"], vid, (g_sigma * np.abs(rec["sigma"]))[:, None] * xh)
+    np.add.at(g["w_c"], vid, np.einsum("ni,nj->nij", g_z, np.abs(rec["x"])))
     np.add.at(g["w_sh"], vid, np.einsum("ni,nj->nij", g_z, gamma))
     return g
 

@@ -102,15 +102,22 @@ def l1_color_seed(out_color: torch.Tensor, gt: torch.Tensor, mask: torch.Tensor 
                   count: int | None = None):
     """Fused losses.py:22-31 (one kernel): returns (dL/dC (.., 3) f64, sum |C - gt|
     over the selection as a 0-d f64 device tensor).  mask selects pixels
-    (None = all); the normaliser is count, or 3 x #selected."""
+    (None = all); the normaliser is count, or 3 x #selected.  Unlike
+    loss_color_seed (the reference's signature: gt holds the selected rows
+    only), gt here is full-frame, same shape as out_color; host tensors are
+    copied to the device."""
     lib = _lib.load()
     pred = out_color.reshape(-1).contiguous()
     if pred.dtype != torch.float32:
         pred = pred.float()
-    g = gt.reshape(-1).contiguous()
+    n = pred.numel()
+    g = torch.as_tensor(gt)
+    if g.numel() != n:
+        raise ValueError(f"gt must be full-frame like out_color ({n} values), got {g.numel()} "
+                         "(loss_color_seed takes the selected rows only)")
+    g = g.to(device=pred.device).reshape(-1).contiguous()
     if g.dtype not in (torch.float32, torch.float64):
         g = g.double()
-    n = pred.numel()
     m = None
     if mask is not None:
         m = mask.reshape(-1).to(torch.uint8).contiguous()

@@ -66,7 +66,17 @@ class DeviceScene:
 
     @classmethod
     def from_scene(cls, scene: Scene, t_stamp: float = 0.0, device=None) -> "DeviceScene":
+        """The composed scene at t (static + posed actor voxels, render_raster.py:63-89)."""
         return cls(flatten_scene(scene, t_stamp), device)
+
+    @classmethod
+    def from_static(cls, scene: Scene, device=None) -> "DeviceScene":
+        """The static voxel set only (the ray path marches actors in their own
+        frames; the trainable parameter block covers the static owner)."""
+        from .scene import FlatVoxels
+        v = scene.static
+        return cls(FlatVoxels(v.centers(), v.edges(), v.rotation, v.w_s, v.w_c, v.w_sh, v.log_a, v.log_b,
+                              scene.density_mode), device)
 
     def c_struct(self) -> _lib.SceneT:
         s = _lib.SceneT()

@@ -52,9 +52,14 @@ def _block(v) -> np.ndarray:
 
 
 class TrainableScene:
+    """The static owner's parameters (trainer.py:132 lists the static set first;
+    actor voxel sets are rendered but not optimised here).  `ds` holds exactly
+    the static rows, so `params`, the Adam moments and the refresh kernel all
+    cover the same M rows (actors never enter the block)."""
+
     def __init__(self, scene: Scene, device=None):
         self.scene = scene
-        self.ds = DeviceScene.from_scene(scene, device=device)
+        self.ds = DeviceScene.from_static(scene, device=device)
         dev = self.ds.device
         self.params = torch.as_tensor(_block(scene.static), device=dev).contiguous()
         self.m = torch.zeros_like(self.params)
@@ -73,7 +78,9 @@ class TrainableScene:
 
     def refresh(self) -> None:
         lib = _lib.load()
-        _lib.check(lib.salf_scene_refresh(self.params.data_ptr(), self.n, self.ds.prm.data_ptr(),
+        if self.params.shape[0] != self.ds.n:
+            raise ValueError(f"parameter block has {self.params.shape[0]} rows, device scene {self.ds.n}")
+        _lib.check(lib.salf_scene_refresh(self.params.data_ptr(), self.ds.n, self.ds.prm.data_ptr(),
                                           self.ds.aux.data_ptr(), _lib.stream_ptr()), "refresh")
 
     def adam_step(self, grad: torch.Tensor, cfg: AdamConfig = AdamConfig()) -> float:

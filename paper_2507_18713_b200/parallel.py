@@ -98,22 +98,25 @@ def allreduce_(t, group=None):
 def allreduce_grad_(grad, group=None, sparse: bool = True, transport=None):
     """Sum the dense (M, 27) f64 per-voxel gradient buffer across ranks.
 
-    The buffer's values are sums of the kernels' fp32 partials, so it travels
-    in fp32 (half the NVLink bytes of f64).  With `sparse`, only the rows some
-    rank wrote move: the union of the ranks' non-zero-row masks (a 1-byte MAX
-    all-reduce) selects the rows, which are gathered, summed and scattered
-    back.  A frame touches ~20% of an S1M scene, so the sum moves ~5x fewer
-    bytes; rows outside the union are zero on every rank, so the result is
-    identical to the dense sum."""
+    The buffer travels in its own dtype (f64) by default, so world > 1 sums
+    equal the world = 1 buffer up to the order of one addition per rank.
+    `transport=torch.float32` is an explicit opt-in that halves the NVLink
+    bytes at the cost of rounding each rank's partial sums to fp32 first.
+    With `sparse`, only the rows some rank wrote move: the union of the ranks'
+    non-zero-row masks (a 1-byte MAX all-reduce) selects the rows, which are
+    gathered, summed and scattered back.  A frame touches ~20% of an S1M
+    scene, so the sum moves ~5x fewer bytes; rows outside the union are zero
+    on every rank, so the result is identical to the dense sum."""
     import torch
     import torch.distributed as dist
     if _world(group) <= 1:
         return grad
-    transport = torch.float32 if transport is None else transport
+    transport = grad.dtype if transport is None else transport
     if not sparse:
-        t = grad.to(transport)
+        t = grad if transport == grad.dtype else grad.to(transport)
         dist.all_reduce(t, group=group)
-        grad.copy_(t)
+        if t is not grad:
+            grad.copy_(t)
         return grad
     mask = (grad != 0).any(dim=1).to(torch.uint8)
     dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=group)

@@ -88,10 +88,7 @@ def _opts(background, stop_threshold, exact_color) -> _lib.RasterOptsT:
 def _static_device_scene(scene) -> DeviceScene:
     """The static voxel set on the device (actors are marched in their own frames)."""
     if isinstance(scene, Scene):
-        from .scene import FlatVoxels
-        v = scene.static
-        ds = DeviceScene(FlatVoxels(v.centers(), v.edges(), v.rotation, v.w_s, v.w_c, v.w_sh, v.log_a, v.log_b,
-                                    scene.density_mode))
+        ds = DeviceScene.from_static(scene)
     else:
         ds = as_device_scene(scene)
     if ds.rot is not None:
@@ -177,7 +174,8 @@ def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: tor
 
 def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf,
                    background=(0.0, 0.0, 0.0), stop_threshold: float = STOP_THRESHOLD,
-                   valid=None, exact_color: bool = False, check_unit: bool = True) -> RenderRecords:
+                   valid=None, exact_color: bool = False, check_unit: bool = True,
+                   check: bool = True) -> RenderRecords:
     """Render a ray batch against the composed scene (render_ray.py:161-239).
 
     Static scenes use one fused march/shade/composite launch with the
@@ -186,7 +184,11 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
     moved into each actor frame at their timestamps).  Finite `t_max` is
     supported by `march_batch` only (the reference renderers pass infinity).
     `check_unit=False` skips the unit-norm validation (a host-synchronising
-    reduction) for directions that are unit by construction."""
+    reduction) for directions that are unit by construction.  `check=True`
+    raises like the reference for rays the marcher cannot finish
+    (RuntimeError "octree marching failed to terminate", octree.py:251-252;
+    ValueError for a query outside the root, octree.py:144-145); `check=False`
+    leaves them as status bits on the records (no host synchronisation)."""
     if np.any(np.isfinite(np.asarray(t_max, np.float64))):
         raise NotImplementedError("finite t_max is only supported by march_batch")
     lib = _lib.load()
@@ -219,22 +221,35 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
                                               ex_rec.data_ptr(), rgb.data_ptr(), op.data_ptr(),
                                               depth.data_ptr(), saved.data_ptr(), status.data_ptr(),
                                               _lib.stream_ptr()), "integrate_rays")
-        return RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
-                             np.asarray(background, np.float64), ex_start, ex_rec, offsets)
+        rec = RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
+                            np.asarray(background, np.float64), ex_start, ex_rec, offsets)
+        if check:
+            check_status(rec)
+        return rec
     _lib.check(lib.salf_ray_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
                                     _lib.ptr(vmask), _lib.ref(opts), rgb.data_ptr(), op.data_ptr(),
                                     depth.data_ptr(), saved.data_ptr(), status.data_ptr(),
                                     _lib.stream_ptr()), "integrate_rays")
-    return RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
-                         np.asarray(background, np.float64))
+    rec = RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
+                        np.asarray(background, np.float64))
+    if check:
+        check_status(rec)
+    return rec
 
 
-def check_status(rec: RenderRecords) -> None:
-    """Raise like the reference would for rays it cannot march."""
-    st = rec.status
-    if rec.n_rays and bool((st & 1).any()):
+def check_status(rec) -> None:
+    """Raise like the reference would for rays it cannot march (one host sync)."""
+    raise_for_status(rec.status)
+
+
+def raise_for_status(status: torch.Tensor) -> None:
+    """status bit 0: round cap (octree.py:251-252), bit 1: query outside the root (octree.py:144-145)."""
+    if status.numel() == 0:
+        return
+    cap, outside = torch.stack([(status & 1).any(), (status & 2).any()]).tolist()
+    if cap:
         raise RuntimeError("octree marching failed to terminate")
-    if rec.n_rays and bool((st & 2).any()):
+    if outside:
         raise ValueError("query point outside the octree root cube")
 
 
@@ -253,7 +268,6 @@ def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chun
     rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, batch.t_stamps,
                          background=background, stop_threshold=stop_threshold, valid=batch.valid,
                          exact_color=exact_color, check_unit=not getattr(batch, "generated", False))
-    check_status(rec)
     return rec.out_color.reshape(h, w, 3), rec.opacity.reshape(h, w), rec.depth.reshape(h, w)
 
 
@@ -374,11 +388,7 @@ def render_lidar_ranges(scene, octrees, batch, *, chunk: int = 65536) -> torch.T
     segment and discards it here)."""
     del chunk
     ret = render_lidar(scene, octrees, batch)
-    st = ret.status
-    if st.numel() and bool((st & 1).any()):
-        raise RuntimeError("octree marching failed to terminate")
-    if st.numel() and bool((st & 2).any()):
-        raise ValueError("query point outside the octree root cube")
+    raise_for_status(ret.status)
     return ret.depth
 
 

@@ -20,6 +20,7 @@ import torch
 from . import render_raster as RR
 from . import render_ray as RY
 from .parallel import allreduce_, allreduce_grad_, band_camera
+from .render_ray import raise_for_status
 from .sensors import gen_lidar_rays
 
 
@@ -31,13 +32,16 @@ class ForwardState:
     losses: torch.Tensor  # [sum |C - gt|, sum |D - gt|] of this rank
 
 
-def rig_forward(ds, octree, sensors, targets, items) -> ForwardState:
+def rig_forward(ds, octree, sensors, targets, items, check: bool = True) -> ForwardState:
     """Forward of this rank's work items; targets[i]: (H, W, 3) gt colour for
-    cameras, (beams * steps,) gt range for LiDARs."""
+    cameras, (beams * steps,) gt range for LiDARs.  `check`: raise like the
+    reference's marcher for LiDAR rays that hit the round cap or leave the
+    root (one host sync over all blocks, after every launch is queued)."""
     dev = ds.device
     counts = torch.zeros(2, dtype=torch.float64, device=dev)
     losses = torch.zeros(2, dtype=torch.float64, device=dev)
     saved = []
+    statuses = []
     for it in items:
         s = sensors[it.sensor]
         if it.kind == "raster_band":
@@ -53,6 +57,7 @@ def rig_forward(ds, octree, sensors, targets, items) -> ForwardState:
             blk = SimpleNamespace(origins=rays.origins[it.lo:it.hi], dirs=rays.dirs[it.lo:it.hi],
                                   shape=(it.hi - it.lo,), generated=True)  # generated: unit by construction
             rec = RY.render_lidar(ds, octree, blk)
+            statuses.append(rec.status)
             gt = torch.as_tensor(targets[it.sensor], device=dev)[it.lo:it.hi].double()
             dep = rec.depth.double()
             ok = torch.isfinite(dep) & torch.isfinite(gt)
@@ -60,6 +65,8 @@ def rig_forward(ds, octree, sensors, targets, items) -> ForwardState:
             counts[1] += ok.sum()
             losses[1] += diff.abs().sum()
             saved.append((rec, diff))
+    if check and statuses:
+        raise_for_status(torch.cat(statuses))
     return ForwardState(items, saved, counts, losses)
 
 

@@ -173,3 +173,26 @@ def test_fused_l1_color_seed(gt_dtype, masked):
     assert torch.equal(d, want)
     diff = (c.double() - gt.double()).reshape(-1, 3)[mref]
     torch.testing.assert_close(lsum, diff.abs().sum(), rtol=1e-12, atol=0)
+
+
+def test_trainable_scene_with_actors_covers_static_rows_only():
+    """a scene with actors trains the static owner only -- the device
+    scene, the parameter block and the Adam moments all have the static row
+    count, an Adam step refreshes exactly those rows, and densify keeps them
+    consistent (the actor voxels never enter the block)."""
+    from paper_2507_18713_b200.optim import TrainableScene
+    sc = load_golden_scene("actors")
+    assert sc.actors and sum(a.voxels.n for a in sc.actors) > 0
+    ts = TrainableScene(sc)
+    m = sc.static.n
+    assert ts.n == m == ts.params.shape[0] == ts.m.shape[0] == ts.ds.geo.shape[0]
+    prm0 = ts.ds.prm.clone()
+    g = torch.zeros_like(ts.params)
+    g[:, 0] = 1.0
+    ts.adam_step(g)
+    torch.cuda.synchronize()
+    assert ts.ds.prm.shape == prm0.shape
+    # w_s[0] moved by -lr on every static row, nothing else changed
+    d = (ts.ds.prm - prm0).double()
+    assert torch.allclose(d[:, 0], torch.full_like(d[:, 0], -0.01), atol=1e-6)
+    assert float(d[:, 1:].abs().max()) == 0.0

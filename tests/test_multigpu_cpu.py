@@ -83,26 +83,33 @@ def _grad_worker(rank, world, port, out):
     m = 400
     g = np.zeros((m, 27))
     rows = rng.choice(m, size=60, replace=False)  # each rank touches its own rows (partly shared)
-    g[rows] = rng.normal(size=(60, 27)).astype(np.float32)  # fp32-representable partial sums
+    g[rows] = rng.normal(size=(60, 27)) * (1.0 + 1e-12)  # NOT fp32-representable
     g[rows[:5], :3] = 0.0  # rows with some zero components stay touched
     dense = torch.as_tensor(g.copy())
     sparse = torch.as_tensor(g.copy())
+    f32 = torch.as_tensor(g.copy())
     allreduce_grad_(dense, sparse=False)
     allreduce_grad_(sparse, sparse=True)
-    out[rank] = (g, dense.numpy().copy(), sparse.numpy().copy())
+    allreduce_grad_(f32, sparse=True, transport=torch.float32)
+    out[rank] = (g, dense.numpy().copy(), sparse.numpy().copy(), f32.numpy().copy())
     dist.destroy_process_group()
 
 
 def test_gloo_sparse_grad_allreduce_equals_dense_world2():
     """parallel.allreduce_grad_: the touched-rows all-reduce (union of the
-    ranks' non-zero-row masks) gives exactly the dense fp32-transport sum."""
+    ranks' non-zero-row masks) gives exactly the dense sum, and the default f64
+    transport gives exactly the world-1 sum of the two ranks' f64 buffers
+    (values that are not fp32-representable); fp32 transport is opt-in."""
     port = _free_port()
     with mp.Manager() as m:
         out = m.dict()
         mp.spawn(_grad_worker, args=(2, port, out), nprocs=2, join=True)
         res = dict(out)
-    want = (res[0][0].astype(np.float32) + res[1][0].astype(np.float32)).astype(np.float64)
+    want = res[0][0] + res[1][0]
+    want32 = (res[0][0].astype(np.float32) + res[1][0].astype(np.float32)).astype(np.float64)
+    assert not np.array_equal(want, want32)
     for r in (0, 1):
-        _, dense, sparse = res[r]
+        _, dense, sparse, f32 = res[r]
         np.testing.assert_array_equal(dense, sparse)
         np.testing.assert_array_equal(sparse, want)
+        np.testing.assert_array_equal(f32, want32)

@@ -102,3 +102,21 @@ def test_fastmath_exp_expm1_accuracy(tmp_path):
                     "-o", str(exe)], check=True)
     r = subprocess.run([str(exe), "300000"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def _integration_snippet():
+    text = (ROOT / "INTEGRATION.md").read_text()
+    return re.findall(r"```python\n(.*?)```", text, flags=re.S)[0]
+
+
+def test_integration_snippet_structs_match_abi():
+    """The ctypes binding documented in INTEGRATION.md runs as written and its
+    structs have the C ABI's layout (field names, offsets, sizes)."""
+    from paper_2507_18713_b200 import _lib
+    ns = {"LIB_PATH": str(_lib.LIB_PATH)}
+    exec(compile(_integration_snippet(), "INTEGRATION.md", "exec"), ns)
+    for doc, abi in ((ns["_Scene"], _lib.SceneT), (ns["_Camera"], _lib.CameraT)):
+        assert ctypes.sizeof(doc) == ctypes.sizeof(abi)
+        assert [f[0] for f in doc._fields_] == [f[0] for f in abi._fields_]
+        for name, _ in abi._fields_:
+            assert getattr(doc, name).offset == getattr(abi, name).offset, name

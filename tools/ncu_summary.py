@@ -9,6 +9,15 @@ import sys
 from collections import defaultdict
 
 
+def _hbm_gbs():
+    from pathlib import Path
+    p = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    return float(json.loads(p.read_text())["hbm_gbs"]) if p.exists() else 6550.0
+
+
+HBM_GBS = _hbm_gbs()
+
+
 def ncu_csv(rep, *args):
     out = subprocess.run(["ncu", "-i", rep, "--csv", *args], capture_output=True, text=True).stdout
     return list(csv.reader(io.StringIO(out)))
@@ -67,7 +76,8 @@ def main(rep, out_md, traffic_json=None):
                         "fp64_pipe_pct": avg["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"]}
         lines += [f"## {name} ({len(lst)} launches)", "",
                   f"* duration {dur_ms:.3f} ms; DRAM read {rd / 1e6:.1f} MB + write {wr / 1e6:.1f} MB "
-                  f"= {(rd + wr) / dur_ms / 1e6:.1f} GB/s ({avg['dram__throughput.avg.pct_of_peak_sustained_elapsed']:.1f}% of peak)",
+                  f"= {(rd + wr) / dur_ms / 1e6:.1f} GB/s ({100 * (rd + wr) / dur_ms / 1e6 / HBM_GBS:.2f}% of the "
+                  f"measured {HBM_GBS:.0f} GB/s)",
                   f"* L2 hit {avg['lts__t_sector_hit_rate.pct']:.1f}%, L1 hit {avg['l1tex__t_sector_hit_rate.pct']:.1f}%",
                   f"* registers/thread {avg['launch__registers_per_thread']:.0f}, achieved occupancy "
                   f"{avg['sm__warps_active.avg.pct_of_peak_sustained_active']:.1f}%",
