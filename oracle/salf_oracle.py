@@ -751,7 +751,7 @@ def render_rays_image(vox, tree, rays, background=(0.0, 0.0, 0.0), stop_threshol
 # ---------------------------------------------------------------------------
 # backward (reference backward.py:26-101, static owner) + L1 seeds (losses.py:22-46)
 
-def backward_records(rec, vox: Voxels, d_color, d_depth, magnitude=False):
+def backward_records(rec, vox: Voxels, d_color, d_depth, magnitude=False, x_floor=0.0):
     """Dense per-voxel gradients {w_s (M,4), w_c (M,3,3), w_sh (M,3,4), log_a, log_b}.
 
     `magnitude=True` (test-side conditioning, no reference counterpart) returns
@@ -760,9 +760,13 @@ def backward_records(rec, vox: Voxels, d_color, d_depth, magnitude=False):
     suffix sum of |A w|).  It is the scale against which any finite-precision
     evaluation of that sum is conditioned: an element that is a near-cancelling
     sum of large terms cannot be reproduced to 1e-4 of its own (small) value by
-    any fp32 or reordered fp64 implementation, only to a fraction of this scale."""
+    any fp32 or reordered fp64 implementation, only to a fraction of this scale.
+    `x_floor` adds the resolution of the quantities that cross zero inside a
+    voxel: the local coordinates x (in [-1, 1]) count as |x| + x_floor and the
+    SDF value s as |s| + x_floor |w_s|_1 (a chord entering and leaving through
+    the two x faces has x_0 = 0 exactly; its fp64 value is rounding noise)."""
     if magnitude:
-        return _backward_magnitude(rec, vox, d_color, d_depth)
+        return _backward_magnitude(rec, vox, d_color, d_depth, x_floor)
     m = vox.n
     g = dict(w_s=np.zeros((m, 4)), w_c=np.zeros((m, 3, 3)), w_sh=np.zeros((m, 3, 4)),
              log_a=np.zeros(m), log_b=np.zeros(m))
@@ -806,9 +810,9 @@ def backward_records(rec, vox: Voxels, d_color, d_depth, magnitude=False):
     return g
 
 
-def _backward_magnitude(rec, vox: Voxels, d_color, d_depth):
+def _backward_magnitude(rec, vox: Voxels, d_color, d_depth, x_floor=0.0):
     """backward_records(..., magnitude=True): the chain of backward.py:52-100
-    with every factor replaced by its absolute value."""
+    with every factor replaced by its absolute value (x and s floored)."""
     m = vox.n
     g = dict(w_s=np.zeros((m, 4)), w_c=np.zeros((m, 3, 3)), w_sh=np.zeros((m, 3, 4)),
              log_a=np.zeros(m), log_b=np.zeros(m))
@@ -836,19 +840,21 @@ def _backward_magnitude(rec, vox: Voxels, d_color, d_depth):
     g_sigma = g_alpha * delta * np.exp(-rec["sigma"] * delta)
     g_z = dc[ray] * w[:, None] * np.abs(rec["color"] * (1.0 - rec["color"]))
     gamma = np.abs(sh_basis(rec["omega"]))
-    xh = np.abs(np.concatenate([rec["x"], np.ones((ray.size, 1))], axis=1))
+    xa = np.abs(rec["x"]) + x_floor
+    xh = np.concatenate([xa, np.ones((ray.size, 1))], axis=1)
     vid = rec["vid"]
     if rec["density_mode"] == "sdf":
         ap, bp = np.exp(vox.log_a[vid]), np.exp(vox.log_b[vid])
         s = rec["s_field"]
+        sa = np.abs(s) + x_floor * np.abs(vox.w_s[vid]).sum(axis=1)
         e = np.exp(-np.abs(s) / bp)
-        ds = np.where(s == 0.0, 0.0, g_sigma * (ap / (2.0 * bp)) * e)
+        ds = g_sigma * (ap / (2.0 * bp)) * e
         np.add.at(g["log_a"], vid, g_sigma * np.abs(rec["sigma"]))
-        np.add.at(g["log_b"], vid, g_sigma * ((ap / (2.0 * bp)) * np.abs(s) * e))
+        np.add.at(g["log_b"], vid, g_sigma * ((ap / (2.0 * bp)) * sa * e))
         np.add.at(g["w_s"], vid, ds[:, None] * xh)
     else:
         np.add.at(g["w_s"], vid, (g_sigma * np.abs(rec["sigma"]))[:, None] * xh)
-    np.add.at(g["w_c"], vid, np.einsum("ni,nj->nij", g_z, np.abs(rec["x"])))
+    np.add.at(g["w_c"], vid, np.einsum("ni,nj->nij", g_z, xa))
     np.add.at(g["w_sh"], vid, np.einsum("ni,nj->nij", g_z, gamma))
     return g
 

@@ -280,56 +280,119 @@ __device__ __forceinline__ void segment_grad(int mode, double delta, double sigm
   for (int k = kGradStride; k < 32; ++k) g[k] = 0.0f;
 }
 
-// Mixed-precision gradient of one included segment (backward.py:52-100)
-// from fp32 fields: x (local coordinates), delta, dq = t_mid - D; the running
-// transmittance T (fp32, advanced here) and the fp64 prefix sum of A w (the
-// suffix is total - prefix).  Writes the 27 components into g (g[27..31] = 0).
+// One ray segment's fp32 fields, shared BIT FOR BIT by the certified ray
+// forward (k_ray_forward_fast) and the mixed ray backward: the backward
+// recovers the reference's suffix sums S_i = sum_{j>i} A_j w_j
+// (backward.py:26-32, :62-64) as differences of the forward's fp64 totals of
+// the exact fp32 products (w, w c, w t_mid) and its own running fp64 sums of
+// the same products -- identical values, so the differences carry only fp64
+// rounding (no fp32 "total - prefix" cancellation).
+constexpr float kYClampF = 27.631021115928547f;  // -ln(1 - kAlphaMax) (scene.py:32)
+
+struct SegF32 {
+  float s, sigma, ee, yr, y, alpha;
+};
+
+template <bool kSdf>
+__device__ __forceinline__ void seg_fields_f32(const VoxPrm &p, float a, float inv_b, const float x[3], float delta,
+                                               SegF32 &o) {
+  o.s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
+  if (kSdf) {
+    // a/2 (1 + sign(s)(1 - e)): a - a/2 e for s > 0, a/2 e otherwise (scene.py:235-242)
+    o.ee = fast_exp(-fabsf(o.s) * inv_b);
+    const float he = 0.5f * a * o.ee;
+    o.sigma = o.s > 0.f ? a - he : he;
+  } else {
+    o.ee = 0.f;
+    o.sigma = fast_exp(o.s);
+  }
+  o.yr = o.sigma * delta;
+  const bool cl = o.yr >= kYClampF;
+  o.y = cl ? kYClampF : o.yr;                   // -log1p(-clip(alpha))
+  o.alpha = cl ? 1.f : -expm1_neg(-o.yr);      // segment_opacity (scene.py:282-284)
+}
+
+// Neumaier compensated fp32 sum h + c (+= y, y >= 0).
+__device__ __forceinline__ void neumaier_add(float &h, float &c, float y) {
+  const float t = h + y;
+  c += fabsf(h) >= y ? (h - t) + y : (y - t) + h;
+  h = t;
+}
+
+// fp32 colour + its complement without cancellation: c = 1 / (1 + E),
+// 1 - c = E c (E = e^-z); c is eval_color32g's value bit for bit.
+__device__ __forceinline__ void eval_color32c(const VoxPrm &p, const float x[3], const float gam[4], float c[3],
+                                              float omc[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float z = __fmaf_rn(p.wc[3 * i + 2], x[2], __fmaf_rn(p.wc[3 * i + 1], x[1], p.wc[3 * i] * x[0]));
+    z = __fmaf_rn(p.wsh[4 * i + 0], gam[0], z);
+    z = __fmaf_rn(p.wsh[4 * i + 1], gam[1], z);
+    z = __fmaf_rn(p.wsh[4 * i + 2], gam[2], z);
+    z = __fmaf_rn(p.wsh[4 * i + 3], gam[3], z);
+    const float E = fast_exp(-z);
+    c[i] = fast_rcp(1.0f + E);
+    omc[i] = E * c[i];
+  }
+}
+
+// Mixed-precision gradient of one included ray segment (backward.py:52-100).
+// Running state per ray: Y = Yh + Yc before this segment (the forward's
+// compensated sum, advanced here), the fp64 prefix sums P = (w c[3], w, w t)
+// of the exact fp32 products, and the forward's totals Acc of the same sums.
 // kColor = false: depth-only seeds (LiDAR), the colour terms are compile-time zeros.
+struct RayBwdState {
+  float Yh, Yc;
+  double Pc[3], Pw, Pwt;
+  double Ac[3], Aw, Awt;
+};
+
 template <bool kSdf, bool kColor = true>
 __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv_b, const float x[3], float delta,
-                                             float dq, const float gam[4], bool want_color, const float dC[3],
-                                             float dws, double total, float tail, float &T, double &prefix,
-                                             float g[32]) {
-  const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
-  const float ha = 0.5f * a;
-  float ee = 0.f, sigma;
-  if (kSdf) {
-    ee = fast_exp(-fabsf(s) * inv_b);
-    const float he = ha * ee;
-    sigma = s > 0.f ? a - he : he;
-  } else {
-    sigma = fast_exp(s);
+                                             double tm, double D, const float gam[4], bool want_color,
+                                             const float dC[3], float dws, float tail, RayBwdState &r, float g[32]) {
+  SegF32 f;
+  seg_fields_f32<kSdf>(p, a, inv_b, x, delta, f);
+  const float om = fast_exp(-f.yr);                   // exp(-sigma delta), unclamped (backward.py:66)
+  const float omc = f.alpha >= 1.f ? 1e-12f : om;     // 1 - alpha as the reference clamps it
+  const float T = fast_exp(-(r.Yh + r.Yc));           // T_before, the forward's value
+  const float w = T * f.alpha;
+  float col[3] = {0.f, 0.f, 0.f}, ocol[3] = {0.f, 0.f, 0.f};
+  if (kColor && want_color) eval_color32c(p, x, gam, col, ocol);
+  const double wd = (double)w;
+  if (kColor) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r.Pc[k] = fma(wd, (double)col[k], r.Pc[k]);
   }
-  const float y = sigma * delta;
-  const float om = fast_exp(-y);
-  const bool clamped = y > 27.631021115928547f;
-  const float alpha = clamped ? 1.f : -expm1_neg(-y);
-  const float omc = clamped ? 1e-12f : om;
-  float col[3] = {0.f, 0.f, 0.f};
-  if (kColor && want_color) eval_color32g(p, x, gam, col);
-  const float w = T * alpha;
+  r.Pw = __dadd_rn(r.Pw, wd);
+  r.Pwt = fma(wd, tm, r.Pwt);
+  // S = sum_{j>i} A_j w_j = dC . (Ac - Pc) + dD / ws ((Awt - Pwt) - D (Aw - Pw))
+  const double sw = __dsub_rn(r.Aw, r.Pw), swt = __dsub_rn(r.Awt, r.Pwt);
+  double S = (double)dws * __dsub_rn(swt, __dmul_rn(D, sw));
+  if (kColor) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) S = fma((double)dC[k], __dsub_rn(r.Ac[k], r.Pc[k]), S);
+  }
+  const float dq = (float)__dsub_rn(tm, D);
   const float A = kColor ? __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], __fmaf_rn(dC[0], col[0], dws * dq)))
                          : dws * dq;
-  prefix += (double)(A * w);
-  const float suffix = (float)(total - prefix);
-  const float g_alpha = __fmaf_rn(A, T, -(suffix + tail) * fast_rcp(omc));
+  const float g_alpha = __fmaf_rn(A, T, -((float)S + tail) * fast_rcp(omc));
   const float g_sigma = g_alpha * delta * om;
   float ds, ga, gb;
   if (kSdf) {
-    const float k2e = ha * inv_b * ee;
-    ds = (s == 0.f) ? 0.f : g_sigma * k2e;
-    ga = g_sigma * sigma;
-    gb = -g_sigma * k2e * s;
+    const float k2e = 0.5f * a * inv_b * f.ee;
+    ds = (f.s == 0.f) ? 0.f : g_sigma * k2e;
+    ga = g_sigma * f.sigma;
+    gb = -g_sigma * k2e * f.s;
   } else {
-    ds = g_sigma * sigma;
+    ds = g_sigma * f.sigma;
     ga = 0.f;
     gb = 0.f;
   }
   g[0] = ds * x[0]; g[1] = ds * x[1]; g[2] = ds * x[2]; g[3] = ds;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const float wc = w * col[i];
-    const float gz = kColor ? dC[i] * __fmaf_rn(-wc, col[i], wc) : 0.f;
+    const float gz = kColor ? dC[i] * (w * col[i]) * ocol[i] : 0.f;  // dC w c (1 - c)
 #pragma unroll
     for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = kColor ? gz * x[k] : 0.f;
 #pragma unroll
@@ -339,7 +402,7 @@ __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv
   g[26] = gb;
 #pragma unroll
   for (int k = kGradStride; k < 32; ++k) g[k] = 0.f;
-  T = T * omc;
+  neumaier_add(r.Yh, r.Yc, f.y);
 }
 
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes

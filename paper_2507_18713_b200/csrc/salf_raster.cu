@@ -797,24 +797,43 @@ __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float
   return true;
 }
 
-// The backward's variant: t* and q in fp64 (6 DFMA), rounded to fp32 once.
-// (The two-float form above measured slower in the issue-bound backward.)
-__device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, float q[3], float &u0, float &u1,
+// The backward's variant: t* and q in fp64 (6 DFMA), rounded to fp32 once
+// for the hit test.  (The two-float form above measured slower in the
+// issue-bound backward.)  For a hit the chord is then re-derived in fp64
+// (all three slabs and the near plane): the fp32 u0, u1 carry ~2^-24 h |1/d|
+// each, a large RELATIVE error of a grazing chord's delta = u1 - u0
+// (delta ~ 1e-3 h) and hence of its alpha and of every gradient term it
+// scales; the fp64 chord is exact to ~1e-16.  Outputs delta and
+// um = t_mid - t*.
+__device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, float q[3], float &delta, float &um,
                                            double &ts) {
   ts = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
   if (r.fast) {
     // slab k: u in [(-s h - q) / d, (s h - q) / d], s = sign(d): h |1/d| -/+ q/d
     float un = -INFINITY, uf = INFINITY;
+    double qd[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      q[k] = (float)fma(ts, r.d[k], e.o[k]);
+      qd[k] = fma(ts, r.d[k], e.o[k]);
+      q[k] = (float)qd[k];
       const float qi = q[k] * r.inv[k];
       un = fmaxf(un, __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi));
       uf = fminf(uf, __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi));
     }
-    u0 = fmaxf(un, (float)(r.tn0 - ts));
-    u1 = uf;
-    return u1 > u0;
+    if (!(uf > fmaxf(un, (float)(r.tn0 - ts)))) return false;
+    // fp64 chord; 1/d by one Newton step on the fp32 reciprocal (|err| ~ 2^-46)
+    double u0 = r.tn0 - ts, u1 = INFINITY;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double iv = (double)r.inv[k];
+      iv = fma(iv, fma(-r.d[k], iv, 1.0), iv);
+      const double hi = fabs(e.half * iv), qi = qd[k] * iv;
+      u0 = fmax(u0, -hi - qi);
+      u1 = fmin(u1, hi - qi);
+    }
+    delta = (float)(u1 - u0);
+    um = (float)(0.5 * (u0 + u1));
+    return true;
   }
   double ti = 0.0, to = 0.0;
 #pragma unroll
@@ -837,16 +856,26 @@ __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, flo
   }
   const double t0 = npmax(ti, r.tn0);
   if (!(to > t0 + 1e-12)) return false;
-  u0 = (float)(t0 - ts);
-  u1 = (float)(to - ts);
+  delta = (float)(to - t0);
+  um = (float)(0.5 * (t0 + to) - ts);
   return true;
 }
 
-// Per-pixel backward state (fp64 only where the text above says).
+// Per-pixel backward state.  The default backward walks each pixel's list
+// BACK TO FRONT, from its last included hit (the forward's stop index) to the
+// first entry, so the reference's suffix sum S_i = sum_{j>i} A_j w_j
+// (backward.py:26-32, :62-64) is accumulated directly -- no "total - prefix"
+// cancellation -- and the transmittance before each hit is recovered in log
+// space, T_i = exp(-(Y_final - sum_{j>=i} y_j)) with the subtraction
+// compensated (Neumaier), so its error stays ~1e-7 relative however many hits
+// the pixel has.  (A running product of (1 - alpha) front to back loses
+// ~n 2^-22 relative; exp(-Y) does not.)
 struct BwdPix {
   RayF r;
-  float dC[3], dws, tail, T;
-  double total, prefix, D;
+  float dC[3], dws, tail;
+  float Yh, Yc;  // Y after the current hit (compensated fp32), starts at Y_final
+  float S;       // suffix sum of A w over the hits behind the current one
+  double D;
   int n_stop;
 };
 
@@ -863,26 +892,26 @@ __device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_r
   const double acc_w = s[3], acc_wt = s[4];
   const bool ok = acc_w > kDepthWeightMin;  // depth_valid (backward.py:46-49)
   const double dd = (ok && d_depth) ? d_depth[pix] : 0.0;
-  const double D = ok ? acc_wt / acc_w : 0.0;
-  q.D = D;
+  q.D = ok ? acc_wt / acc_w : 0.0;
   const double ws = ok ? acc_w : 1.0;
-  // sum_j A_j w_j = dC . acc_rgb + dD (acc_wt - D acc_w) / ws (suffix sums by subtraction)
-  q.total = dCd[0] * s[0] + dCd[1] * s[1] + dCd[2] * s[2] + dd * (acc_wt - D * acc_w) / ws;
   // tail = (dC . background) * T_final (backward.py:62)
   q.tail = (float)((dCd[0] * opt.background[0] + dCd[1] * opt.background[1] + dCd[2] * opt.background[2]) * s[5]);
   q.dws = (float)(dd / ws);
   for (int k = 0; k < 3; ++k) q.dC[k] = (float)dCd[k];
   q.n_stop = (int)s[6];
-  q.prefix = 0.0;
-  q.T = 1.f;
+  const double Yf = -log(s[5]);  // T_final = exp(-Y_final) of the included hits
+  q.Yh = (float)Yf;
+  q.Yc = (float)(Yf - (double)q.Yh);
+  q.S = 0.f;
+  if (!(dCd[0] != 0.0 || dCd[1] != 0.0 || dCd[2] != 0.0 || dd != 0.0)) q.n_stop = 0;  // zero seeds: no work
 }
 
-// One included segment of pixel q against staged entry e: adds its 27
-// gradient components to g.  Returns false on a miss.
+// One included hit of pixel q against staged entry e, visited back to front:
+// adds its 27 gradient components to g.  Returns false on a miss.
 template <bool kRot, bool sdf, bool kDepth = true>
 __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF &e, BwdPix &q,
                                             float g[32]) {
-  float qv[3], u0, u1;
+  float qv[3];
   double ts;
   const RayF *ray = &q.r;
   RayF rr;
@@ -894,9 +923,8 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
     rayf_from_dir(d2, q.r.tn0, rr);
     ray = &rr;
   }
-  if (!pair_hit_bwd(*ray, e, qv, u0, u1, ts)) return false;
-  const float delta = u1 - u0;
-  const float um = 0.5f * (u0 + u1);
+  float delta, um;
+  if (!pair_hit_bwd(*ray, e, qv, delta, um, ts)) return false;
   const float dq = kDepth ? (float)(ts - q.D) + um : 0.f;  // t_mid - D (no depth seeds: unused)
   // (fp32 below: explicit FMAs -- this file is compiled with --fmad=false)
   float x[3];
@@ -917,22 +945,40 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
   } else {
     sigma = fast_exp(s);
   }
-  const float y = sigma * delta;
-  const float om = fast_exp(-y);                 // exp(-sigma delta), unclamped
-  const bool clamped = y > 27.631021115928547f;  // alpha >= 1 - 1e-12 (scene.py:32)
-  const float alpha = clamped ? 1.f : -expm1_neg(-y);
+  constexpr float kYClamp = 27.631021115928547f;  // alpha >= 1 - 1e-12 (scene.py:32)
+  const float yr = sigma * delta;
+  const float om = fast_exp(-yr);                 // exp(-sigma delta), unclamped (backward.py:66)
+  const bool clamped = yr > kYClamp;
+  const float y = clamped ? kYClamp : yr;         // -log1p(-clip(alpha))
+  const float alpha = clamped ? 1.f : -expm1_neg(-yr);
   const float omc = clamped ? 1e-12f : om;       // 1 - alpha as the reference clamps it
-  float col[3];
-  eval_color32g(p, x, gam, col);
-  const float T = q.T;
+  // Y before this hit = Y after it - y (compensated)
+  {
+    const float Yt = q.Yh - y;
+    q.Yc += fabsf(q.Yh) >= y ? (q.Yh - Yt) - y : (-y - Yt) + q.Yh;
+    q.Yh = Yt;
+  }
+  const float T = fast_exp(-(q.Yh + q.Yc));
+  // colour and its complement without cancellation: c = 1 / (1 + E), 1 - c = E c (E = e^-z)
+  float col[3], omcol[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float z = __fmaf_rn(p.wc[3 * i + 2], x[2], __fmaf_rn(p.wc[3 * i + 1], x[1], p.wc[3 * i] * x[0]));
+    z = __fmaf_rn(p.wsh[4 * i + 0], gam[0], z);
+    z = __fmaf_rn(p.wsh[4 * i + 1], gam[1], z);
+    z = __fmaf_rn(p.wsh[4 * i + 2], gam[2], z);
+    z = __fmaf_rn(p.wsh[4 * i + 3], gam[3], z);
+    const float E = fast_exp(-z);
+    col[i] = fast_rcp(1.0f + E);
+    omcol[i] = E * col[i];
+  }
   const float w = T * alpha;
   // A = dC . c + dD (t_mid - D) / ws (backward.py:52-59)
   const float A = __fmaf_rn(q.dC[2], col[2], __fmaf_rn(q.dC[1], col[1], kDepth ? __fmaf_rn(q.dC[0], col[0], q.dws * dq)
                                                                              : q.dC[0] * col[0]));
-  q.prefix += (double)(A * w);
-  const float suffix = (float)(q.total - q.prefix);
-  const float g_alpha = __fmaf_rn(A, T, -(suffix + q.tail) * fast_rcp(omc));  // backward.py:62-64
-  const float g_sigma = g_alpha * delta * om;                                  // :66
+  const float g_alpha = __fmaf_rn(A, T, -(q.S + q.tail) * fast_rcp(omc));  // backward.py:62-64
+  q.S = __fmaf_rn(A, w, q.S);
+  const float g_sigma = g_alpha * delta * om;                               // :66
   float ds, ga, gb;
   if (sdf) {
     const float k2e = ha * inv_b * ee;
@@ -949,8 +995,7 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
   g[3] += ds;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const float wc = w * col[i];
-    const float gz = q.dC[i] * __fmaf_rn(-wc, col[i], wc);  // dC w c (1 - c)  :69-70
+    const float gz = q.dC[i] * (w * col[i]) * omcol[i];  // dC w c (1 - c)  :69-70
 #pragma unroll
     for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = __fmaf_rn(gz, x[k], g[4 + 3 * i + k]);
 #pragma unroll
@@ -958,7 +1003,6 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
   }
   g[25] += ga;
   g[26] += gb;
-  q.T = T * omc;
   return true;
 }
 
@@ -1008,6 +1052,23 @@ __device__ __forceinline__ void prefetch_next(const salf_scene_t &sc, const int3
   }
 #else
   (void)sc; (void)entries; (void)next; (void)end; (void)chunk;
+#endif
+}
+
+// Same for the backward's back-to-front walk: the chunk before `prev` + chunk.
+__device__ __forceinline__ void prefetch_prev(const salf_scene_t &sc, const int32_t *__restrict__ entries,
+                                              int64_t prev, int64_t beg, int chunk) {
+#if SALF_PREFETCH
+  const int64_t j = prev + threadIdx.x;
+  if (threadIdx.x < chunk && j >= beg) {
+    const int64_t v = __ldg(entries + j);
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.geo + 4 * v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.aux + 4 * v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.prm + v * SALF_PRM_STRIDE));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.prm + v * SALF_PRM_STRIDE + 24));
+  }
+#else
+  (void)sc; (void)entries; (void)prev; (void)beg; (void)chunk;
 #endif
 }
 
@@ -1300,14 +1361,15 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     wr0[k] = ty * c.tile + f / c.tile;
     wr1[k] = f < npix ? ty * c.tile + l / c.tile : -1;
   }
-  for (int64_t base = beg; base < lim; base += kChunkB) {
+  // back to front: chunks from the last one any pixel of the tile includes down to the first
+  for (int64_t base = beg + ((lim - beg - 1) / kChunkB) * kChunkB; base >= beg && lim > beg; base -= kChunkB) {
     const int cn = (int)min((int64_t)kChunkB, lim - base);
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j], vrange);
     __syncthreads();
-    prefetch_next(sc, entries, base + kChunkB, lim, kChunkB);
+    prefetch_prev(sc, entries, base - kChunkB, beg, kChunkB);
     const int jb = (int)(base - beg);
-    for (int j = 0; j < cn; ++j) {
+    for (int j = cn - 1; j >= 0; --j) {
       const EntryF &e = sm[j];
       bool rows_hit[NP];
       bool any_rows = false;

@@ -552,7 +552,11 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   if (i >= n) return;
   const double y_stop_d = -log(1.0 - opt.stop_threshold);
   const float y_stop = (float)y_stop_d, y_stop_err = (float)fabs(y_stop_d - (double)y_stop);
-  float T = 1.f, acc_c[3] = {0.f, 0.f, 0.f}, acc_w = 0.f, acc_wt = 0.f, EY = 0.f, Yh = 0.f, Yc = 0.f;
+  // fp64 totals of the exact fp32 products w c, w, w t_mid: the mixed backward
+  // rebuilds its suffix sums from them (seg_grad_f32); T = exp(-Y) exactly as
+  // the backward recomputes it (also for the first segment)
+  float T = fast_exp(-0.f), EY = 0.f, Yh = 0.f, Yc = 0.f;
+  double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0;
   double last_t0 = -INFINITY;
   int64_t n_seg = 0, n_inc = 0;
   int32_t st = 0;
@@ -584,29 +588,23 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
         x[k] = (float)__dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(tm, m.d[k])), ctr[k]), ax.z);
       VoxPrm p;
       load_prm(sc.prm, vid, p);
-      const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
       const float wn = fabsf(p.ws[0]) + fabsf(p.ws[1]) + fabsf(p.ws[2]) + fabsf(p.ws[3]);
       const float a = (float)ax.x, inv_b = (float)ax.y;
-      float sigma, rel;
-      if (kSdf) {
-        const float sb = fabsf(s) * inv_b;
-        const float he = 0.5f * a * fast_exp(-sb);
-        sigma = s > 0.f ? a - he : he;
-        rel = __fmaf_rn(wn * 4e-7f, inv_b, __fmaf_rn(3e-7f, sb, 5.4e-7f));
-      } else {
-        sigma = fast_exp(s);
-        rel = __fmaf_rn(wn, 4e-7f, __fmaf_rn(3e-7f, fabsf(s), 5.4e-7f));
-      }
-      const float y = fminf(sigma * delta, kYClamp);
-      const float alpha = y >= kYClamp ? 1.f : -expm1_neg(-y);
+      SegF32 f;
+      seg_fields_f32<kSdf>(p, a, inv_b, x, delta, f);
+      const float sigma = f.sigma, y = f.y, alpha = f.alpha;
+      const float rel = kSdf ? __fmaf_rn(wn * 4e-7f, inv_b, __fmaf_rn(3e-7f, fabsf(f.s) * inv_b, 5.4e-7f))
+                             : __fmaf_rn(wn, 4e-7f, __fmaf_rn(3e-7f, fabsf(f.s), 5.4e-7f));
+      (void)sigma;
       const float w = T * alpha;
+      const double wd = (double)w;
       if (!kLidar) {
         float col[3];
-        const float od[3] = {(float)m.d[0], (float)m.d[1], (float)m.d[2]};
-        const float gam[4] = {(float)kShC0, (float)kShC1 * od[1], (float)kShC1 * od[2], (float)kShC1 * od[0]};
+        const float gam[4] = {(float)kShC0, (float)(kShC1 * m.d[1]), (float)(kShC1 * m.d[2]),
+                              (float)(kShC1 * m.d[0])};
         eval_color32g(p, x, gam, col);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
+        for (int k = 0; k < 3; ++k) acc_c[k] = fma(wd, (double)col[k], acc_c[k]);
       }
       if (feat) {  // intensity / ray-drop extension: blended 8-channel feature
         const float4 f0 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid);
@@ -616,12 +614,10 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
         acc_f[4] = fmaf(w, f1.x, acc_f[4]); acc_f[5] = fmaf(w, f1.y, acc_f[5]);
         acc_f[6] = fmaf(w, f1.z, acc_f[6]); acc_f[7] = fmaf(w, f1.w, acc_f[7]);
       }
-      acc_w += w;
-      acc_wt = __fmaf_rn(w, (float)tm, acc_wt);
+      acc_w = __dadd_rn(acc_w, wd);
+      acc_wt = fma(wd, tm, acc_wt);
       EY += y * (rel + 2.f * kU);
-      const float Yt = Yh + y;
-      Yc += fabsf(Yh) >= y ? (Yh - Yt) + y : (y - Yt) + Yh;
-      Yh = Yt;
+      neumaier_add(Yh, Yc, y);
       T = fast_exp(-(Yh + Yc));
       ++n_inc;
       // product early stop after this segment: prod(1 - alpha) <= keep  <=>  Y >= y_stop
@@ -633,12 +629,14 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   const double Y = (double)Yh + (double)Yc;
   if (ok && fabs(Y - kLn2) <= (double)__fmaf_rn(2.f, EY, __fmaf_rn(4.f * kU, (float)Y, 1e-9f))) flag = true;
   const bool vdepth = ok && Y > kLn2;  // sum w = 1 - T_final > 0.5
+  // the saved (raw) weight sum must take the same side of 0.5 as the certified Y
+  if (ok && (acc_w > kDepthWeightMin) != vdepth) flag = true;
   if (ok) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      if (out_rgb) out_rgb[3 * i + k] = __fmaf_rn(T, (float)opt.background[k], acc_c[k]);
+      if (out_rgb) out_rgb[3 * i + k] = (float)fma((double)T, opt.background[k], acc_c[k]);
     out_op[i] = 1.f - T;
-    out_depth[i] = vdepth ? acc_wt / acc_w : NAN;
+    out_depth[i] = vdepth ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -648,15 +646,13 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   }
   if (saved) {
     double *sv = saved + i * SALF_SAVED_STRIDE;
-    const double wsum = -expm1(-Y);
     sv[0] = acc_c[0]; sv[1] = acc_c[1]; sv[2] = acc_c[2];
-    sv[3] = !ok ? 0.0 : (vdepth ? fmax(wsum, 0.5000000001) : fmin(wsum, 0.5));
-    sv[4] = acc_w > 0.f ? (double)acc_wt * (sv[3] / (double)acc_w) : 0.0;  // keeps D = acc_wt / acc_w
+    sv[3] = acc_w; sv[4] = acc_wt;  // raw sums (the backward's suffix sums need them bit for bit)
     sv[5] = T; sv[6] = (double)n_seg; sv[7] = (double)n_inc;
   }
   if (feat) {
     // linear head on [blended feature, expected depth (0 if none), view dir] + sigmoid (as k_ray_forward)
-    const float dep = vdepth ? acc_wt / acc_w : 0.0f;
+    const float dep = vdepth ? (float)__ddiv_rn(acc_wt, acc_w) : 0.0f;
     const float dv[3] = {(float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]};
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -742,13 +738,24 @@ __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backwa
     }
   }
   int64_t n_inc = 0, n_done = 0;
-  float Tf = 1.f;
+  RayBwdState rs;
   float dCf[3] = {(float)dC[0], (float)dC[1], (float)dC[2]};
   const float dwsf = (float)(dd / ws), tailf = (float)tail;
   float gam[4] = {0.f, 0.f, 0.f, 0.f};
   if (kMixed && live) {
-    n_inc = (int64_t)saved[i * SALF_SAVED_STRIDE + 7];
+    const double *s = saved + i * SALF_SAVED_STRIDE;
+    n_inc = (int64_t)s[7];
     if (n_inc == 0) live = false;
+    rs.Yh = 0.f;
+    rs.Yc = 0.f;
+    rs.Pw = rs.Pwt = 0.0;
+    rs.Aw = s[3];
+    rs.Awt = s[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      rs.Pc[k] = 0.0;
+      rs.Ac[k] = s[k];
+    }
     gam[0] = (float)kShC0;
     gam[1] = (float)(kShC1 * m.d[1]);
     gam[2] = (float)(kShC1 * m.d[2]);
@@ -777,8 +784,8 @@ __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backwa
             x[k] = (float)__dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(tm, m.d[k])), ctr[k]), ax.z);
           VoxPrm p;
           load_prm(sc.prm, vid, p);
-          seg_grad_f32<kSdf, kColor>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), (float)__dsub_rn(tm, D),
-                             gam, want_color, dCf, dwsf, total, tailf, Tf, prefix, g);
+          seg_grad_f32<kSdf, kColor>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), tm, D, gam,
+                                     want_color, dCf, dwsf, tailf, rs, g);
           act = true;
           if (++n_done >= n_inc) live = false;
         }

@@ -9,11 +9,16 @@ intensity and on gradients.  These helpers check it ELEMENT BY ELEMENT:
 * images: `floor` is an absolute 1e-7 (below fp32 resolution of the [0, 1]
   colour / opacity planes: a pixel at 1e-3 still has to match to 1e-4 of
   itself); NaN masks (depth "no return") must be identical.
-* gradients: `mag` is the oracle's backward_records(..., magnitude=True), the
-  per-element sum of the ABSOLUTE values of the terms the reference adds --
-  the scale any finite-precision evaluation of a near-cancelling sum is
-  conditioned on.  cond = 1e-5 (ten times tighter than the 1e-4 bar), and
-  frac = 1e-9 of the class maximum removes exact-zero noise only.
+* gradients: `mag` is the oracle's backward_records(..., magnitude=True,
+  x_floor=X_FLOOR), the per-element sum of the ABSOLUTE values of the terms
+  the reference adds -- the scale any finite-precision evaluation of a
+  near-cancelling sum is conditioned on.  cond = 1e-5 (ten times tighter than
+  the 1e-4 bar), and frac = 1e-9 of the class maximum removes exact-zero
+  noise only.  Quantities that cross zero inside a voxel (local coordinates x,
+  SDF value s) enter `mag` as |x| + X_FLOOR: with cond = 1e-5 that states
+  "x resolved to 2^-20 of the voxel half-edge" (fp32 local coordinates carry
+  ~2e-7; the reference's own fp64 x of a symmetric chord is rounding noise
+  ~1e-14, so no implementation reproduces g.x there to 1e-4 of itself).
 
 Every check returns a report: the worst relative error over the elements
 ABOVE the floor, how many elements fall under the floor, and the worst
@@ -28,6 +33,12 @@ REL = 1e-4
 IMAGE_FLOOR = 1e-7
 GRAD_COND = 1e-5
 GRAD_FRAC = 1e-9
+X_FLOOR = 2.0 ** -20 / GRAD_COND  # |x| + X_FLOOR in the magnitude: x resolved to 2^-20
+
+
+def grad_magnitude(O, rec, vox, d_color, d_depth):
+    """The oracle's conditioning scale for grad_report (see the module docstring)."""
+    return O.backward_records(rec, vox, d_color, d_depth, magnitude=True, x_floor=X_FLOOR)
 
 
 def elementwise(got, want, rel=REL, floor=0.0, mag=None, cond=0.0, name=""):

@@ -23,7 +23,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 
 from conftest import GOLDEN, load_golden_scene, oracle_voxels  # noqa: E402
 from oracle import salf_oracle as O  # noqa: E402
-from parity import grad_report, image_report  # noqa: E402
+from parity import grad_magnitude, grad_report, image_report  # noqa: E402
 
 
 def _np(t):
@@ -49,7 +49,7 @@ def golden_cases(out):
     dc, dd = gd["rand300_rbw_dcolor"], gd["rand300_rbw_ddepth"]
     vox = oracle_voxels(sc)
     rec = O.raster_records(vox, ocam_of(cam), background=(0.05, 0.1, 0.15))
-    mag = O.backward_records(rec, vox, dc, dd, magnitude=True)
+    mag = grad_magnitude(O, rec, vox, dc, dd)
     want = {k: gd["rand300_rbw_g_" + k] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
     for exact in (False, True):
         fb, st = RR.rasterize(flatten_scene(sc), cam, background=(0.05, 0.1, 0.15), return_state=True,
@@ -62,7 +62,7 @@ def golden_cases(out):
         sc = load_golden_scene(name)
         vox = oracle_voxels(sc)
         orec = O.integrate_rays(vox, O.build_octree(vox), gd[case + "_o"], gd[case + "_d"], background=bg)
-        mag = O.backward_records(orec, vox, gd[case + "_dcolor"], gd[case + "_ddepth"], magnitude=True)
+        mag = grad_magnitude(O, orec, vox, gd[case + "_dcolor"], gd[case + "_ddepth"])
         want = {k: gd[f"{case}_g_{k}"] for k in ("w_s", "w_c", "w_sh", "log_a", "log_b")}
         for exact in (False, True):
             r = RY.integrate_rays(sc, RY.build_scene_octrees(sc), gd[case + "_o"], gd[case + "_d"],
@@ -111,7 +111,7 @@ def c2_cases(out, s1m, n_fwd_tiles, n_bwd_tiles):
     t0 = time.time()
     rec = O.raster_records(vox, ocam, tiles=btiles, proj=proj)
     want = O.backward_records(rec, vox, dc.reshape(-1, 3), np.zeros(h * w))
-    mag = O.backward_records(rec, vox, dc.reshape(-1, 3), np.zeros(h * w), magnitude=True)
+    mag = grad_magnitude(O, rec, vox, dc.reshape(-1, 3), np.zeros(h * w))
     out["c2_oracle_bwd_s"] = time.time() - t0
     for exact in (False, True):
         fb, st = RR.rasterize(ds, cam, return_state=True, exact_color=exact)
@@ -145,7 +145,7 @@ def c3_cases(out, s1m, n_rays):
     ok = np.isfinite(orec["depth"])
     dd_s = np.where(ok, np.sign(np.nan_to_num(orec["depth"]) - gtr) / max(ok.sum(), 1), 0.0)
     want = O.backward_records(orec, vox, np.zeros((n_rays, 3)), dd_s)
-    mag = O.backward_records(orec, vox, np.zeros((n_rays, 3)), dd_s, magnitude=True)
+    mag = grad_magnitude(O, orec, vox, np.zeros((n_rays, 3)), dd_s)
     dd = np.zeros(lb.n)
     dd[idx] = dd_s
     g, _, _ = RY.lidar_backward(ret, torch.as_tensor(dd, device="cuda"))
