@@ -273,15 +273,18 @@ int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64
  * reference): feat (M x 8 f32) alpha-blended with the colour
  * weights into out_feat (N x 8, nullable), then a linear head (2 x 13 f32:
  * 8 feature weights, depth weight, 3 view-dir weights, bias) and a sigmoid ->
- * out_head (N x 2: intensity, drop probability).  feat == NULL: depth only. */
+ * out_head (N x 2: intensity, drop probability).  feat == NULL: depth only.
+ * feat_acc64 (N x 8 f64, nullable): the blended feature as fp64 totals of the
+ * exact per-segment products -- what salf_lidar_backward takes as Facc. */
 int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
                        const double *origins, const double *dirs, const salf_raster_opts_t *opts,
                        const float *feat, const float *head, float *out_depth, float *out_opacity,
-                       float *out_feat, float *out_head, double *saved, int32_t *status, void *stream);
+                       float *out_feat, float *out_head, double *feat_acc64, double *saved, int32_t *status,
+                       void *stream);
 
 /* Backward of salf_lidar_forward: depth seeds d_depth (N f64) plus, for the
  * intensity / ray-drop extension, dF = dL/d(blended feature) (N x 8 f64)
- * with the forward's blended feature Facc (N x 8 f64): field-parameter
+ * with the forward's feat_acc64 as Facc (N x 8 f64): field-parameter
  * gradients into grad (M x 27) and feature gradients into feat_grad (M x 8).
  * feat == NULL: depth-only backward. */
 int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,

@@ -967,12 +967,15 @@ def loss_opacity_lidar(vox: Voxels, tree: Octree, points, delta=0.2):
     return float(np.mean(1.0 - alpha)), g
 
 
-def feature_backward(rec, vox: Voxels, feat, dF, d_depth):
+def feature_backward(rec, vox: Voxels, feat, dF, d_depth, magnitude=False, x_floor=0.0):
     """Reverse mode of a blended per-voxel feature F = sum_i w_i f_vid_i (the
     LiDAR intensity / ray-drop extension; no reference code):
     the same chain as backward_records (backward.py:52-100) with the colour
     replaced by f and no background term, plus the expected-depth term.
-    Returns ({w_s, log_a, log_b}, feature grads (M, 8))."""
+    Returns ({w_s, log_a, log_b}, feature grads (M, 8)).  `magnitude=True`:
+    the conditioning scales instead (backward_records(..., magnitude=True))."""
+    if magnitude:
+        return _feature_magnitude(rec, vox, feat, dF, d_depth, x_floor)
     m = vox.n
     g = dict(w_s=np.zeros((m, 4)), log_a=np.zeros(m), log_b=np.zeros(m))
     fg = np.zeros((m, 8))
@@ -1006,6 +1009,46 @@ def feature_backward(rec, vox: Voxels, feat, dF, d_depth):
     np.add.at(g["log_a"], vid, g_sigma * rec["sigma"])
     np.add.at(g["log_b"], vid, g_sigma * (-(ap / (2.0 * bp)) * s * e))
     np.add.at(fg, vid, w[:, None] * dF[ray])
+    return g, fg
+
+
+def _feature_magnitude(rec, vox: Voxels, feat, dF, d_depth, x_floor=0.0):
+    """feature_backward's chain with every factor replaced by its absolute value."""
+    m = vox.n
+    g = dict(w_s=np.zeros((m, 4)), log_a=np.zeros(m), log_b=np.zeros(m))
+    fg = np.zeros((m, 8))
+    ray = rec["ray"]
+    if ray.size == 0:
+        return g, fg
+    inc = rec["included"]
+    a = np.clip(rec["alpha"], 0.0, ALPHA_MAX)
+    tb = rec["t_before"]
+    w = np.where(inc, tb * a, 0.0)
+    tm = 0.5 * (rec["t0"] + rec["t1"])
+    delta = rec["t1"] - rec["t0"]
+    ok = rec["weight_sum"] > 0.5
+    dd = np.abs(np.where(ok, d_depth, 0.0))
+    dep = np.where(ok, rec["depth"], 0.0)
+    ws = np.where(ok, rec["weight_sum"], 1.0)
+    vid = rec["vid"]
+    adF = np.abs(dF)
+    A = np.einsum("nc,nc->n", adF[ray], np.abs(feat[vid])) + dd[ray] * np.abs(tm - dep[ray]) / ws[ray]
+    vals = np.where(inc, A * w, 0.0)
+    cs = np.cumsum(vals)
+    gs = rec["group_start"]
+    suffix = np.abs(np.repeat(cs[np.maximum(gs[1:] - 1, 0)], np.diff(gs)) - cs)
+    g_alpha = np.where(inc, A * tb + suffix / (1.0 - a), 0.0)
+    g_sigma = g_alpha * delta * np.exp(-rec["sigma"] * delta)
+    xh = np.concatenate([np.abs(rec["x"]) + x_floor, np.ones((ray.size, 1))], axis=1)
+    ap, bp = np.exp(vox.log_a[vid]), np.exp(vox.log_b[vid])
+    s = rec["s_field"]
+    sa = np.abs(s) + x_floor * np.abs(vox.w_s[vid]).sum(axis=1)
+    e = np.exp(-np.abs(s) / bp)
+    ds = g_sigma * (ap / (2.0 * bp)) * e
+    np.add.at(g["w_s"], vid, ds[:, None] * xh)
+    np.add.at(g["log_a"], vid, g_sigma * np.abs(rec["sigma"]))
+    np.add.at(g["log_b"], vid, g_sigma * ((ap / (2.0 * bp)) * sa * e))
+    np.add.at(fg, vid, w[:, None] * adF[ray])
     return g, fg
 
 

@@ -347,10 +347,15 @@ struct RayBwdState {
   double Ac[3], Aw, Awt;
 };
 
-template <bool kSdf, bool kColor = true>
-__device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv_b, const float x[3], float delta,
-                                             double tm, double D, const float gam[4], bool want_color,
-                                             const float dC[3], float dws, float tail, RayBwdState &r, float g[32]) {
+// kFeat (LiDAR intensity / ray-drop extension): the blended feature enters A
+// like a colour without background, fdot = dF . f of this segment; its suffix
+// sum is CF - PF with CF = dF . (forward's fp64 feature totals) and PF the
+// running fp64 sum of w fdot.  Returns w.
+template <bool kSdf, bool kColor = true, bool kFeat = false>
+__device__ __forceinline__ float seg_grad_f32(const VoxPrm &p, float a, float inv_b, const float x[3], float delta,
+                                              double tm, double D, const float gam[4], bool want_color,
+                                              const float dC[3], float dws, float tail, RayBwdState &r, float g[32],
+                                              double fdot = 0.0, double *PF = nullptr, double CF = 0.0) {
   SegF32 f;
   seg_fields_f32<kSdf>(p, a, inv_b, x, delta, f);
   const float om = fast_exp(-f.yr);                   // exp(-sigma delta), unclamped (backward.py:66)
@@ -373,9 +378,14 @@ __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv
 #pragma unroll
     for (int k = 0; k < 3; ++k) S = fma((double)dC[k], __dsub_rn(r.Ac[k], r.Pc[k]), S);
   }
+  if (kFeat) {
+    *PF = fma(wd, fdot, *PF);
+    S = __dadd_rn(S, __dsub_rn(CF, *PF));
+  }
   const float dq = (float)__dsub_rn(tm, D);
-  const float A = kColor ? __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], __fmaf_rn(dC[0], col[0], dws * dq)))
-                         : dws * dq;
+  float A = kColor ? __fmaf_rn(dC[2], col[2], __fmaf_rn(dC[1], col[1], __fmaf_rn(dC[0], col[0], dws * dq)))
+                   : dws * dq;
+  if (kFeat) A += (float)fdot;
   const float g_alpha = __fmaf_rn(A, T, -((float)S + tail) * fast_rcp(omc));
   const float g_sigma = g_alpha * delta * om;
   float ds, ga, gb;
@@ -403,6 +413,7 @@ __device__ __forceinline__ void seg_grad_f32(const VoxPrm &p, float a, float inv
 #pragma unroll
   for (int k = kGradStride; k < 32; ++k) g[k] = 0.f;
   neumaier_add(r.Yh, r.Yc, f.y);
+  return w;
 }
 
 // Warp-aggregated gradient scatter.  PRECONDITION: called by all 32 lanes

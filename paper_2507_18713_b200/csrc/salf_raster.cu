@@ -741,6 +741,41 @@ __device__ __forceinline__ void stage_entry_f(const salf_scene_t &sc, const Pinh
   }
 }
 
+// Short chords (grazing pairs) are re-derived in fp64: the fp32 slab values
+// carry ~2^-24 h |1/d| each, a large RELATIVE error of a chord of length
+// delta << h -- enough to turn an fp64 miss into an fp32 hit with y ~ 1e-7
+// (an opacity of 5e-7 where the reference has 0) or to skew a grazing
+// segment's alpha and gradient by 1e-3.  Chords shorter than h / 16 are
+// recomputed from the three slabs and the near plane in fp64 (1/d by one
+// Newton step on the fp32 reciprocal, |err| ~ 2^-46) and kept iff
+// t1 > t0 + 1e-12 (render_raster.py:241).  The backward refines a superset
+// (every chord whose fp32 length is not accurate to ~1e-6), so both passes
+// see the same hits.
+constexpr float kRefineChord = 0.0625f;
+
+__device__ __forceinline__ bool chord64(const RayF &r, const EntryF &e, double ts, double &u0, double &u1) {
+  u0 = r.tn0 - ts;
+  u1 = INFINITY;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double qk = fma(ts, r.d[k], e.o[k]);
+    double iv = (double)r.inv[k];
+    iv = fma(iv, fma(-r.d[k], iv, 1.0), iv);
+    const double hi = fabs(e.half * iv), qi = qk * iv;
+    u0 = fmax(u0, -hi - qi);
+    u1 = fmin(u1, hi - qi);
+  }
+  return u1 > u0 + 1e-12;
+}
+
+__device__ __noinline__ bool refine_chord(const RayF &r, const EntryF &e, double ts, float &u0, float &u1) {
+  double a, b;
+  if (!chord64(r, e, ts, a, b)) return false;
+  u0 = (float)a;
+  u1 = (float)b;
+  return true;
+}
+
 // Pair test in closest-approach coordinates.  With t* ~ -(o . d) (any
 // value near the closest approach to the voxel centre) the ray is q + u d
 // with q = o + t* d (|q| ~ the voxel size for any pair that can hit) and
@@ -766,7 +801,9 @@ __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float
     }
     u0 = fmaxf(un, r.tn0f - ts);
     u1 = uf;
-    return u1 > u0;
+    if (!(u1 > u0)) return false;
+    if (u1 - u0 < kRefineChord * e.hf) return refine_chord(r, e, (double)ts, u0, u1);
+    return true;
   }
   const double tsd = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
   ts = (float)tsd;
@@ -799,40 +836,42 @@ __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float
 
 // The backward's variant: t* and q in fp64 (6 DFMA), rounded to fp32 once
 // for the hit test.  (The two-float form above measured slower in the
-// issue-bound backward.)  For a hit the chord is then re-derived in fp64
-// (all three slabs and the near plane): the fp32 u0, u1 carry ~2^-24 h |1/d|
-// each, a large RELATIVE error of a grazing chord's delta = u1 - u0
-// (delta ~ 1e-3 h) and hence of its alpha and of every gradient term it
-// scales; the fp64 chord is exact to ~1e-16.  Outputs delta and
-// um = t_mid - t*.
+// issue-bound backward.)  Short chords are re-derived in fp64 (chord64, the
+// forward's rule).  Outputs delta and um = t_mid - t*.
 __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, float q[3], float &delta, float &um,
                                            double &ts) {
   ts = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
   if (r.fast) {
     // slab k: u in [(-s h - q) / d, (s h - q) / d], s = sign(d): h |1/d| -/+ q/d
     float un = -INFINITY, uf = INFINITY;
-    double qd[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      qd[k] = fma(ts, r.d[k], e.o[k]);
-      q[k] = (float)qd[k];
+      q[k] = (float)fma(ts, r.d[k], e.o[k]);
       const float qi = q[k] * r.inv[k];
       un = fmaxf(un, __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi));
       uf = fminf(uf, __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi));
     }
-    if (!(uf > fmaxf(un, (float)(r.tn0 - ts)))) return false;
-    // fp64 chord; 1/d by one Newton step on the fp32 reciprocal (|err| ~ 2^-46)
-    double u0 = r.tn0 - ts, u1 = INFINITY;
+    const float u0f = fmaxf(un, (float)(r.tn0 - ts));
+    if (!(uf > u0f)) return false;
+    // the fp32 slab values carry ~1.2e-7 hf |1/d_k| each (k the binding axes):
+    // re-derive the chord in fp64 unless its relative error is below ~1e-6
+    // (and always below the forward's threshold, so both see the same hits)
+    float ia = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      double iv = (double)r.inv[k];
-      iv = fma(iv, fma(-r.d[k], iv, 1.0), iv);
-      const double hi = fabs(e.half * iv), qi = qd[k] * iv;
-      u0 = fmax(u0, -hi - qi);
-      u1 = fmin(u1, hi - qi);
+      const float qi = q[k] * r.inv[k];
+      const float nk = __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi), fk = __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi);
+      if (nk == un || fk == uf) ia += fabsf(r.inv[k]);
     }
-    delta = (float)(u1 - u0);
-    um = (float)(0.5 * (u0 + u1));
+    if (uf - u0f < e.hf * fmaxf(2.f * kRefineChord, 0.12f * ia)) {  // fp64 chord (as the forward)
+      double u0, u1;
+      if (!chord64(r, e, ts, u0, u1)) return false;
+      delta = (float)(u1 - u0);
+      um = (float)(0.5 * (u0 + u1));
+      return true;
+    }
+    delta = uf - u0f;
+    um = 0.5f * (u0f + uf);
     return true;
   }
   double ti = 0.0, to = 0.0;
@@ -1209,7 +1248,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   const int64_t pix = (int64_t)py * c.width + px;
 #pragma unroll
   for (int k = 0; k < 3; ++k) out_rgb[pix * 3 + k] = __fmaf_rn(T, (float)opt.background[k], acc_c[k]);
-  out_op[pix] = flag ? NAN : 1.f - T;
+  out_op[pix] = flag ? NAN : (float)(-expm1(-Y));  // 1 - T without cancellation near T = 1
   out_depth[pix] = valid ? (float)(acc_wt / (double)acc_w) : NAN;
   if (saved) {
     double *sv = saved + pix * SALF_SAVED_STRIDE;

@@ -416,6 +416,7 @@ struct LidarFeat {
   const float *head;  // 2 x 13: [W_f(8) | W_depth | W_dir(3) | bias] for intensity, drop
   float *out_feat;    // N x 8 alpha-blended feature (nullable)
   float *out_head;    // N x 2 (intensity, ray-drop probability)
+  double *out_acc64;  // N x 8 fp64 totals of the exact products w f (nullable; the mixed feature backward's suffix sums)
 };
 
 #ifndef SALF_RAY_MINB
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
   const double keep = 1.0 - opt.stop_threshold;
   double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0, T = 1.0, t_run = 1.0, last_t0 = -INFINITY;
   float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  double acc_f64[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   const bool feat = kLidar && lf.feat != nullptr;
   int64_t n_seg = 0, n_inc = 0;
   int32_t st = 0;
@@ -468,6 +470,11 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
             acc_f[2] = fmaf(wf, f0.z, acc_f[2]); acc_f[3] = fmaf(wf, f0.w, acc_f[3]);
             acc_f[4] = fmaf(wf, f1.x, acc_f[4]); acc_f[5] = fmaf(wf, f1.y, acc_f[5]);
             acc_f[6] = fmaf(wf, f1.z, acc_f[6]); acc_f[7] = fmaf(wf, f1.w, acc_f[7]);
+            if (lf.out_acc64) {
+              const float fv[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+#pragma unroll
+              for (int k = 0; k < 8; ++k) acc_f64[k] = fma(w, (double)fv[k], acc_f64[k]);
+            }
           }
           acc_w = __dadd_rn(acc_w, w);
           acc_wt = __dadd_rn(acc_wt, __dmul_rn(w, sv.tm));
@@ -519,6 +526,10 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
 #pragma unroll
       for (int k = 0; k < 8; ++k) lf.out_feat[8 * i + k] = acc_f[k];
     }
+    if (lf.out_acc64) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lf.out_acc64[8 * i + k] = acc_f64[k];
+    }
   }
   if (status) status[i] = st;
 }
@@ -543,7 +554,7 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
     const uint8_t *__restrict__ valid, salf_raster_opts_t opt, float *__restrict__ out_rgb,
     float *__restrict__ out_op, float *__restrict__ out_depth, double *__restrict__ saved,
     int32_t *__restrict__ status, LidarFeat lf) {
-  float acc_f[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  double acc_f[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // fp64 totals of the exact products w f
   constexpr bool feat = kLidar && kFeat;  // the extension is a separate instantiation (no per-segment test)
   constexpr float kU = 5.9604645e-8f;  // 2^-24
   constexpr float kYClamp = 27.631021115928547f;
@@ -609,10 +620,9 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
       if (feat) {  // intensity / ray-drop extension: blended 8-channel feature
         const float4 f0 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid);
         const float4 f1 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid + 1);
-        acc_f[0] = fmaf(w, f0.x, acc_f[0]); acc_f[1] = fmaf(w, f0.y, acc_f[1]);
-        acc_f[2] = fmaf(w, f0.z, acc_f[2]); acc_f[3] = fmaf(w, f0.w, acc_f[3]);
-        acc_f[4] = fmaf(w, f1.x, acc_f[4]); acc_f[5] = fmaf(w, f1.y, acc_f[5]);
-        acc_f[6] = fmaf(w, f1.z, acc_f[6]); acc_f[7] = fmaf(w, f1.w, acc_f[7]);
+        const float fv[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc_f[k] = fma(wd, (double)fv[k], acc_f[k]);
       }
       acc_w = __dadd_rn(acc_w, wd);
       acc_wt = fma(wd, tm, acc_wt);
@@ -635,7 +645,7 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
 #pragma unroll
     for (int k = 0; k < 3; ++k)
       if (out_rgb) out_rgb[3 * i + k] = (float)fma((double)T, opt.background[k], acc_c[k]);
-    out_op[i] = 1.f - T;
+    out_op[i] = (float)(-expm1(-Y));  // 1 - T without cancellation near T = 1
     out_depth[i] = vdepth ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
   } else {
 #pragma unroll
@@ -659,14 +669,18 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
       const float *W = lf.head + 13 * j;
       float z = W[12];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) z = fmaf(W[k], acc_f[k], z);
+      for (int k = 0; k < 8; ++k) z = fmaf(W[k], (float)acc_f[k], z);
       z = fmaf(W[8], dep, z);
       z = fmaf(W[9], dv[0], fmaf(W[10], dv[1], fmaf(W[11], dv[2], z)));
       lf.out_head[2 * i + j] = 1.0f / (1.0f + expf(-z));
     }
     if (lf.out_feat) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) lf.out_feat[8 * i + k] = acc_f[k];
+      for (int k = 0; k < 8; ++k) lf.out_feat[8 * i + k] = (float)acc_f[k];
+    }
+    if (lf.out_acc64) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) lf.out_acc64[8 * i + k] = acc_f[k];
     }
   }
   if (status) status[i] = st | (flag ? kStatusRedo : 0);
@@ -697,7 +711,7 @@ struct RowSink {
 #ifndef SALF_RAYB_MINB
 #define SALF_RAYB_MINB 4  // 128 registers: measured best (5, 6 spill)
 #endif
-template <bool kExactColor, bool kMixed = false, bool kSdf = true, bool kColor = true>
+template <bool kExactColor, bool kMixed = false, bool kSdf = true, bool kColor = true, bool kFeat = false>
 __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backward(OctDev t, salf_scene_t sc, int64_t n,
                                                       const double *__restrict__ orig, const double *__restrict__ dirs,
                                                       const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
@@ -736,6 +750,12 @@ __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backwa
         live = live || (m.active && dF[k] != 0.0);
       }
     }
+  }
+  // kFeat (mixed): CF = dF . Facc with Facc the forward's fp64 totals; PF runs over the segments
+  double CF = 0.0, PF = 0.0;
+  if (kMixed && kFeat && i < n && fg.feat) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) CF = fma(dF[k], fg.Facc[8 * i + k], CF);
   }
   int64_t n_inc = 0, n_done = 0;
   RayBwdState rs;
@@ -784,8 +804,23 @@ __global__ void __launch_bounds__(128, kMixed ? SALF_RAYB_MINB : 1) k_ray_backwa
             x[k] = (float)__dmul_rn(__dsub_rn(__dadd_rn(m.o[k], __dmul_rn(tm, m.d[k])), ctr[k]), ax.z);
           VoxPrm p;
           load_prm(sc.prm, vid, p);
-          seg_grad_f32<kSdf, kColor>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), tm, D, gam,
-                                     want_color, dCf, dwsf, tailf, rs, g);
+          if (kFeat) {
+            const float4 f0 = __ldg(reinterpret_cast<const float4 *>(fg.feat) + 2 * vid);
+            const float4 f1 = __ldg(reinterpret_cast<const float4 *>(fg.feat) + 2 * vid + 1);
+            const float fv[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+            double fdot = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) fdot = fma(dF[k], (double)fv[k], fdot);
+            const float w = seg_grad_f32<kSdf, kColor, true>(p, (float)ax.x, (float)ax.y, x,
+                                                             (float)__dsub_rn(s1, s0), tm, D, gam, want_color, dCf,
+                                                             dwsf, tailf, rs, g, fdot, &PF, CF);
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (dF[k] != 0.0) atomicAdd(fg.feat_grad + 8 * vid + k, __dmul_rn((double)w, dF[k]));
+          } else {
+            seg_grad_f32<kSdf, kColor>(p, (float)ax.x, (float)ax.y, x, (float)__dsub_rn(s1, s0), tm, D, gam,
+                                       want_color, dCf, dwsf, tailf, rs, g);
+          }
           act = true;
           if (++n_done >= n_inc) live = false;
         }
@@ -1087,7 +1122,7 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
     if (n == 0) return SALF_OK;
     OctDev t = make_oct(tree);
     const unsigned grid = (unsigned)((n + 127) / 128);
-    LidarFeat lf{nullptr, nullptr, nullptr, nullptr};
+    LidarFeat lf{nullptr, nullptr, nullptr, nullptr, nullptr};
     if (opts->exact_color)
       k_ray_forward<true, false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, valid, *opts,
                                                                            out_rgb, out_opacity, out_depth, saved,
@@ -1115,13 +1150,14 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
 extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
                                   const double *origins, const double *dirs, const salf_raster_opts_t *opts,
                                   const float *feat, const float *head, float *out_depth, float *out_opacity,
-                                  float *out_feat, float *out_head, double *saved, int32_t *status, void *stream) {
+                                  float *out_feat, float *out_head, double *feat_acc64, double *saved,
+                                  int32_t *status, void *stream) {
   SALF_TRY {
     if (n == 0) return SALF_OK;
     if (feat && !head) return set_error(SALF_EINVAL, "LiDAR features need the 2 x 13 head");
     OctDev t = make_oct(tree);
     const unsigned grid = (unsigned)((n + 127) / 128);
-    LidarFeat lf{feat, head, out_feat, out_head};
+    LidarFeat lf{feat, head, out_feat, out_head, feat_acc64};
     cudaStream_t st = (cudaStream_t)stream;
     if (status && !opts->exact_color) {
       // certified mixed precision + fp64 redo of flagged rays (features blended in fp32 either way)
@@ -1248,9 +1284,15 @@ extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t
     const unsigned grid = (unsigned)((n + 127) / 128);
     // colour is not part of the LiDAR model: no colour seeds (d_rgb = nullptr)
     FeatGrad fg{feat, dF, Facc, feat_grad};
-    if (feat || opts->exact_color)  // the feature chain stays fp64
+    if (opts->exact_color)
       k_ray_backward<false><<<grid, 128, 0, (cudaStream_t)stream>>>(t, *scene, n, origins, dirs, nullptr, *opts, saved,
                                                                       nullptr, d_depth, grad, fg, RowSink{});
+    else if (feat && scene->density_mode == SALF_DENSITY_SDF)
+      k_ray_backward<false, true, true, false, true><<<grid, 128, 0, (cudaStream_t)stream>>>(
+          t, *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg, RowSink{});
+    else if (feat)
+      k_ray_backward<false, true, false, false, true><<<grid, 128, 0, (cudaStream_t)stream>>>(
+          t, *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg, RowSink{});
     else
       launch_ray_backward_mixed(scene->density_mode == SALF_DENSITY_SDF, false, grid, (cudaStream_t)stream, t,
                                 *scene, n, origins, dirs, nullptr, *opts, saved, nullptr, d_depth, grad, fg,

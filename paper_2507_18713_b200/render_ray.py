@@ -287,6 +287,7 @@ class LidarReturn:
     scene: DeviceScene | None = None
     octree: OctreeBuffer | None = None
     opts: object = None
+    feat_acc64: torch.Tensor | None = None  # (N, 8) f64 blended feature (exact-product totals)
 
 
 def render_lidar(scene, octrees, batch, *, features=None, head=None,
@@ -312,7 +313,7 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
     op = torch.empty(n, dtype=torch.float32, device=dev)
     saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev)
     status = torch.zeros(n, dtype=torch.int32, device=dev)
-    f = h = of = oh = None
+    f = h = of = oh = fa = None
     if features is not None:
         f = torch.as_tensor(features, dtype=torch.float32, device=dev).reshape(-1, 8).contiguous()
         if f.shape[0] != ds.n:
@@ -322,17 +323,18 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
         h = torch.as_tensor(head, dtype=torch.float32, device=dev).reshape(2, 13).contiguous()
         oh = torch.empty((n, 2), dtype=torch.float32, device=dev)
         of = torch.empty((n, 8), dtype=torch.float32, device=dev) if want_feature else None
+        fa = torch.empty((n, 8), dtype=torch.float64, device=dev)
     opts = _opts((0.0, 0.0, 0.0), stop_threshold, False)
     sc, t = ds.c_struct(), tree.c_struct()
     _lib.check(lib.salf_lidar_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
                                       _lib.ref(opts), _lib.ptr(f), _lib.ptr(h), depth.data_ptr(),
-                                      op.data_ptr(), _lib.ptr(of), _lib.ptr(oh), saved.data_ptr(),
-                                      status.data_ptr(), _lib.stream_ptr()), "render_lidar")
+                                      op.data_ptr(), _lib.ptr(of), _lib.ptr(oh), _lib.ptr(fa),
+                                      saved.data_ptr(), status.data_ptr(), _lib.stream_ptr()), "render_lidar")
     shp = batch.shape
     return LidarReturn(depth.reshape(shp), op.reshape(shp),
                        None if oh is None else oh[:, 0].reshape(shp),
                        None if oh is None else oh[:, 1].reshape(shp),
-                       None if of is None else of.reshape(*shp, 8), saved, status, o, d, ds, tree, opts)
+                       None if of is None else of.reshape(*shp, 8), saved, status, o, d, ds, tree, opts, fa)
 
 
 def lidar_backward(ret: LidarReturn, d_depth=None, *, features=None, head=None, d_intensity=None,
@@ -355,15 +357,15 @@ def lidar_backward(ret: LidarReturn, d_depth=None, *, features=None, head=None, 
     fgrad = hgrad = None
     f = dF = Facc = None
     if features is not None:
-        if ret.feature is None:
-            raise ValueError("render_lidar(..., want_feature=True) is needed for the feature backward")
+        if ret.feat_acc64 is None:
+            raise ValueError("the forward ran without features: render_lidar(..., features=, head=)")
         f = torch.as_tensor(features, dtype=torch.float32, device=dev).reshape(-1, 8).contiguous()
         W = torch.as_tensor(head, dtype=torch.float64, device=dev).reshape(2, 13)
         outs = torch.stack([ret.intensity.reshape(n), ret.drop_prob.reshape(n)], 1).double()
         dout = torch.stack([torch.zeros(n, dtype=torch.float64, device=dev) if x is None
                             else _lib.as_f64(x, dev).reshape(n) for x in (d_intensity, d_drop)], 1)
         dz = dout * outs * (1.0 - outs)  # sigmoid'
-        Facc = ret.feature.reshape(n, 8).double().contiguous()
+        Facc = ret.feat_acc64  # the fp64 totals the mixed backward's suffix sums are built from
         wsum, wt = ret.saved[:, 3], ret.saved[:, 4]
         valid = wsum > 0.5
         D = torch.where(valid, wt / torch.where(valid, wsum, torch.ones_like(wsum)), torch.zeros_like(wsum))

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import grads_close, load_golden_scene, oracle_voxels
+from conftest import assert_grads, grads_close_normwise, load_golden_scene, magnitude, oracle_voxels
 from oracle import salf_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -59,7 +59,7 @@ def _oracle_grad(sc, sensors, targets, depth_weight=10.0):
             recs.append(("l", O.integrate_rays(vox, tree, rays["origins"], rays["dirs"]), gt))
     n_c = sum(r["out_color"].size for k, r, _ in recs if k == "c")
     n_d = sum(int((np.isfinite(r["depth"]) & np.isfinite(gt)).sum()) for k, r, gt in recs if k == "l")
-    tot = None
+    tot = mag = None
     for k, r, gt in recs:
         if k == "c":
             dc = np.sign(r["out_color"] - gt) / n_c
@@ -69,8 +69,10 @@ def _oracle_grad(sc, sensors, targets, depth_weight=10.0):
             dd = np.where(ok, depth_weight * np.sign(np.nan_to_num(r["depth"]) - gt) / n_d, 0.0)
             dc = np.zeros((r["n_rays"], 3))
         g = O.backward_records(r, vox, dc, dd)
+        m = magnitude(r, vox, dc, dd)
         tot = g if tot is None else {q: tot[q] + g[q] for q in g}
-    return tot
+        mag = m if mag is None else {q: mag[q] + m[q] for q in m}
+    return tot, mag
 
 
 def test_rig_step_matches_oracle_and_sharding_is_exact():
@@ -85,8 +87,8 @@ def test_rig_step_matches_oracle_and_sharding_is_exact():
     targets = _targets(sensors)
     grad = torch.zeros((ds.n, 27), dtype=torch.float64, device="cuda")
     rig_step(ds, oc, sensors, targets, split_work(sensors, 1), grad)
-    want = _oracle_grad(sc, sensors, targets)
-    assert grads_close(grads_to_dict(grad), want) < 1e-4
+    want, mag = _oracle_grad(sc, sensors, targets)
+    assert_grads(grads_to_dict(grad), want, mag)
     # four virtual ranks: bands + ray blocks, counts summed between the phases
     per = assign(split_work(sensors, 4, tile=16), 4)
     assert sum(len(p) for p in per) > len(sensors)  # cameras really are cut into bands
@@ -95,7 +97,7 @@ def test_rig_step_matches_oracle_and_sharding_is_exact():
     g2 = torch.zeros_like(grad)
     for fs in states:
         rig_backward(fs, g2, counts)
-    assert grads_close(grads_to_dict(g2), grads_to_dict(grad)) < 1e-6
+    assert grads_close_normwise(grads_to_dict(g2), grads_to_dict(grad)) < 1e-6
 
 
 def test_adam_and_regularisers_match_reference(golden):
