@@ -1,14 +1,29 @@
-"""Benchmark: C2 -- 1920x1080 pinhole raster forward + backward on the 1M-voxel
-synthetic scene (S1M), one frame per rank per step.
+"""Benchmark of the SaLF render hot path (BASELINE.json metric: camera FPS at
+1920x1080 and LiDAR rays/s at 1/2/4/8 B200 vs the CPU reference).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun, one rank per GPU: each rank renders its own C5-rig
-camera (yaw = 45 deg x rank) forward + backward and the per-voxel gradient
-buffer is all-reduced over NCCL (the training step's one exchange).  `value`
-is whole-job frames/s; rank 0 prints one JSON line.  `--impl reference` times
-the reference's CPU algorithm (the oracle port, oracle/salf_oracle.py) on the
-host cores on a bounded sample of the same workload.
+Headline (`value`, N = 1): C2 -- one 1920x1080 pinhole camera rasterized
+forward + backward (colour L1 loss) on the 1M-voxel synthetic scene S1M
+(BASELINE.json configs[1]).  N > 1 runs under torchrun, one rank per GPU:
+rank r renders camera r of the C5 rig (8 C2-style cameras at yaw 45 deg x r,
+distinct views), forward + backward, and the per-voxel gradient buffer is
+all-reduced over NCCL (weak scaling: `value` = all ranks' frames/s).  Beside
+it, at every N:
+
+* `c5`: the C5 training step (8 cameras + 2 LiDARs, BASELINE configs[4])
+  SHARDED over the N ranks by parallel.split_work/assign (row bands, ray
+  blocks), global L1 seeds, backward, NCCL gradient all-reduce, device Adam
+  (strong scaling: steps/s of the whole rig);
+* `lidar`: one C3 sweep per rank (configs[2]), rays/s, with its HBM roofline;
+
+and on rank 0 at N = 1: the C1 frame (configs[0]) on the GPU next to the
+reference algorithm over the whole frame on the host cores (not
+extrapolated), the C3 sweep on the host cores (whole sweep), the C2 CPU
+baseline (sampled tiles, extrapolated, labelled), the surface regime and
+C4.  `--impl reference` times the reference's CPU algorithm (the oracle port,
+oracle/salf_oracle.py -- the reference is pure Python and cannot travel to
+the GPU box) on the same C2 workload.
 """
 
 from __future__ import annotations
@@ -33,103 +48,176 @@ UNIT = "frames/s"
 WORKLOAD = "C2: S1M init-regime scene (1,023,816 voxels), 1920x1080 pinhole raster forward+backward"
 
 
+def config_dict(regime: str, world: int, extra: dict | None = None) -> dict:
+    """The workload description both arms print (same keys, same values)."""
+    c = {"workload": WORKLOAD, "regime": regime, "resolution": [1920, 1080], "voxels": 1023816,
+         "loss": "colour L1 (losses.py:22-31), no depth seeds",
+         "multi_gpu": "rank r renders C5-rig camera r (yaw 45 deg x r), fwd+bwd, NCCL grad all-reduce"
+                      if world > 1 else "single GPU",
+         "l2": "flushed (256 MB write) between timed steps"}
+    if extra:
+        c.update(extra)
+    return c
+
+
 # ------------------------------------------------------------------------------
-# CPU baseline: the reference algorithm (oracle port) on a bounded tile sample
+# CPU baselines: the reference algorithm (oracle port) on the host cores.
+# Workers are spawned with OMP_NUM_THREADS=1 (BASELINE.md §3); frame-level
+# work (projection, pixel rays, octree) is done once per worker at start-up.
 
 _W = {}
 
 
-def _cpu_init(regime):
-    from oracle import salf_oracle as O
-    from paper_2507_18713_b200.scenes import get_scene
-    sc = get_scene("S1M", regime)
-    b, v = sc.bounds, sc.static
-    _W["vox"] = O.Voxels.from_grid(b.aabb_min, b.aabb_max, b.base_edge, v.level, v.ijk, v.w_s, v.w_c,
-                                   v.w_sh, v.log_a, v.log_b)
+def _pin_threads():
+    for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[k] = "1"
 
 
-def _cpu_tile(args):
-    """Reference forward (rasterize) + backward (raster records -> backward_records)
-    of ONE 16x16 tile of the C2 frame; returns seconds."""
+def _cpu_init(kind, regime):
     from oracle import salf_oracle as O
     from paper_2507_18713_b200 import configs
-    tx, ty = args
-    c = configs.c2_camera()
-    cam = O.Camera("pinhole", c.width, c.height, c.fx, c.fy, c.cx, c.cy, position=c.position,
-                   quaternion=c.quaternion)
-    vox = _W["vox"]
-    t0 = time.perf_counter()
-    win = (tx, ty, tx, ty)
-    fb = O.rasterize(vox, cam, window=win)
-    rec = O.raster_records(vox, cam, window=win)
-    dc = np.zeros((rec["n_rays"], 3))
-    dc[:] = 1e-6
-    O.backward_records(rec, vox, dc, np.zeros(rec["n_rays"]))
-    del fb
-    return time.perf_counter() - t0
+    from paper_2507_18713_b200.scenes import get_scene
+    name = {"c1": "S20k", "c2": "S1M", "c3": "S1M"}[kind]
+    sc = get_scene(name, regime if kind != "c1" else "init")
+    b, v = sc.bounds, sc.static
+    vox = O.Voxels.from_grid(b.aabb_min, b.aabb_max, b.base_edge, v.level, v.ijk, v.w_s, v.w_c,
+                             v.w_sh, v.log_a, v.log_b)
+    _W["vox"] = vox
+    if kind in ("c1", "c2"):
+        c = configs.c1_camera() if kind == "c1" else configs.c2_camera()
+        cam = O.Camera("pinhole", c.width, c.height, c.fx, c.fy, c.cx, c.cy, position=c.position,
+                       quaternion=c.quaternion)
+        _W["cam"] = cam
+        _W["proj"] = O.project_voxels(vox, cam)
+        _W["rays"] = O.pixel_rays(cam)
+    else:
+        _W["tree"] = O.build_octree(vox)
+        lid = configs.c3_lidar()
+        r = O.lidar_rays(O.Lidar(lid.beam_elevations, lid.azimuth_start, lid.azimuth_end, lid.steps,
+                                 lid.scan_period, lid.position, lid.quaternion, lid.linear_velocity,
+                                 lid.angular_velocity))
+        _W["o"], _W["d"] = r["origins"], r["dirs"]
 
 
 def _cpu_ready(_):
     return "vox" in _W
 
 
-def _sample_tiles(k, seed):
-    """k tiles stratified over the 68 tile rows (one per row band, random row
-    inside the band and random column): the per-tile cost depends strongly on
-    the row (sky, horizon, road), so stratifying cuts the estimate's variance."""
-    rng = np.random.default_rng(seed)
-    return [(int(rng.integers(0, 120)), int(min(67, (b + rng.random()) * 68 / k))) for b in range(k)]
+def _c2_tiles(tiles):
+    """Reference fwd + bwd (raster records -> composite -> backward_records) of
+    the given 16x16 tiles of the C2 frame; returns seconds (projection excluded:
+    once per worker, like a row-band worker of the reference)."""
+    from oracle import salf_oracle as O
+    vox, cam = _W["vox"], _W["cam"]
+    t0 = time.perf_counter()
+    rec = O.raster_records(vox, cam, tiles=tiles, proj=_W["proj"], pix_rays=_W["rays"])
+    dc = np.full((rec["n_rays"], 3), 1e-6)
+    O.backward_records(rec, vox, dc, np.zeros(rec["n_rays"]))
+    return time.perf_counter() - t0
 
 
-class CpuBaseline:
-    def __init__(self, regime="init", workers=None):
-        n = workers or min(len(os.sched_getaffinity(0)), 64)
-        self.workers = n
-        from paper_2507_18713_b200.scenes import get_scene
-        get_scene("S1M", regime)  # build the cached container once, before the workers start
+def _c1_band(rows):
+    """Reference rasterize (render_raster.py:201-301) of tile rows [r0, r1) of the C1 frame."""
+    from oracle import salf_oracle as O
+    t0 = time.perf_counter()
+    fb = O.rasterize(_W["vox"], _W["cam"], rows=rows, proj=_W["proj"], pix_rays=_W["rays"])
+    return time.perf_counter() - t0, fb["color"][rows[0] * 16:rows[1] * 16]
+
+
+def _c3_block(lohi):
+    """Reference render_lidar_ranges (render_ray.py:297-306) of a block of the C3 sweep."""
+    from oracle import salf_oracle as O
+    lo, hi = lohi
+    t0 = time.perf_counter()
+    rec = O.integrate_rays(_W["vox"], _W["tree"], _W["o"][lo:hi], _W["d"][lo:hi])
+    return time.perf_counter() - t0, rec["depth"]
+
+
+class CpuPool:
+    """Spawned workers (OMP_NUM_THREADS=1) holding one workload's scene state."""
+
+    def __init__(self, kind, regime="init", workers=None):
         import multiprocessing as mp
-        self.pool = ProcessPoolExecutor(n, mp_context=mp.get_context("spawn"), initializer=_cpu_init,
-                                        initargs=(regime,))
-        list(self.pool.map(_cpu_ready, range(n)))  # every worker has loaded the scene
-
-    def sample(self, seed):
-        """One bounded sample: `workers` tiles in parallel -> extrapolated frames/s."""
-        tiles = _sample_tiles(self.workers, seed)
+        from paper_2507_18713_b200.scenes import get_scene
+        self.workers = workers or min(len(os.sched_getaffinity(0)), 64)
+        get_scene({"c1": "S20k", "c2": "S1M", "c3": "S1M"}[kind], regime if kind != "c1" else "init")
+        _pin_threads()  # inherited by the spawned workers before they import numpy
         t0 = time.perf_counter()
-        secs = list(self.pool.map(_cpu_tile, tiles))
-        wall = time.perf_counter() - t0
-        tiles_per_s = len(tiles) / wall
-        return tiles_per_s / (120 * 68), dict(wall_s=wall, tile_s_mean=float(np.mean(secs)))
+        self.pool = ProcessPoolExecutor(self.workers, mp_context=mp.get_context("spawn"), initializer=_cpu_init,
+                                        initargs=(kind, regime))
+        list(self.pool.map(_cpu_ready, range(self.workers)))
+        self.init_s = time.perf_counter() - t0
 
     def close(self):
         self.pool.shutdown()
 
 
+def c2_tiles_sample(seed, k):
+    """k tiles stratified over the 68 tile rows (the per-tile cost depends
+    strongly on the row: sky, horizon, road)."""
+    rng = np.random.default_rng(seed)
+    return [int(min(67, (b + rng.random()) * 68 / k)) * 120 + int(rng.integers(0, 120)) for b in range(k)]
+
+
+def c2_cpu_step(pool: CpuPool, seed: int):
+    """One bounded C2 sample: `workers` tiles in parallel, one per worker.
+    Extrapolated frame time on these cores = (8160 / k) x sum(tile times) / workers."""
+    tiles = c2_tiles_sample(seed, pool.workers)
+    t0 = time.perf_counter()
+    secs = list(pool.pool.map(_c2_tiles, [[t] for t in tiles]))
+    wall = time.perf_counter() - t0
+    frame_s = 8160 / len(tiles) * float(np.sum(secs)) / pool.workers
+    return 1.0 / frame_s, wall, float(np.mean(secs))
+
+
+def c1_cpu_frame(pool: CpuPool):
+    """The whole C1 frame (256 x 256, 16 tile rows) in row bands over the workers."""
+    bands = [(r, r + 1) for r in range(16)]
+    t0 = time.perf_counter()
+    out = list(pool.pool.map(_c1_band, bands))
+    wall = time.perf_counter() - t0
+    img = np.concatenate([c for _, c in out], axis=0)
+    return wall, img
+
+
+def c3_cpu_sweep(pool: CpuPool, n_rays=230400):
+    """The whole C3 sweep in ray blocks over the workers."""
+    cuts = np.linspace(0, n_rays, 4 * pool.workers + 1).round().astype(int)
+    t0 = time.perf_counter()
+    out = list(pool.pool.map(_c3_block, list(zip(cuts[:-1], cuts[1:]))))
+    wall = time.perf_counter() - t0
+    return wall, np.concatenate([d for _, d in out])
+
+
 def run_reference(args, rank):
+    """The reference arm: the reference algorithm on the host cores, same C2
+    workload; each step is one bounded sample (workers tiles)."""
     if rank != 0:
         return
-    base = CpuBaseline("init")
+    pool = CpuPool("c2", args.regime)
     for w in range(args.warmup):
-        base.sample(1000 + w)
-    vals, info = [], []
+        c2_cpu_step(pool, 1000 + w)
+    vals, walls = [], []
     for k in range(args.steps):
-        v, i = base.sample(k)
+        v, wall, _ = c2_cpu_step(pool, k)
         vals.append(v)
-        info.append(i)
-    base.close()
+        walls.append(wall)
+    pool.close()
     value = float(np.mean(vals))
+    sample = (f"{pool.workers} random 16x16 tiles of 8160 per step (one per worker, stratified over tile rows), "
+              f"forward + backward, projection once per worker; frame time = 8160/{pool.workers} x sum(tile s) "
+              f"/ {pool.workers} workers (extrapolated)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(walls)),
+        "frames_per_step": pool.workers / 8160, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256)",
-        "config": {"workload": WORKLOAD, "resolution": [1920, 1080], "voxels": 1023816,
-                   "sample": "one 16x16 tile per worker per step, extrapolated to 8160 tiles"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": base.workers, "kind": "port",
-                         "sample": f"{base.workers} tiles of 8160 per step, stratified over tile rows "
-                                   "(fwd+bwd), extrapolated linearly to the full frame"},
+        "config": config_dict(args.regime, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.workers, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "detail": {"tile_s_mean": float(np.mean([i["tile_s_mean"] for i in info]))},
+        "note": "ms_per_step is the wall time of one sample step (a fraction frames_per_step of a frame); "
+                "value is the extrapolated whole-frame rate on these cores",
     }
     print(json.dumps(line), flush=True)
 
@@ -191,14 +279,34 @@ def _dist_init(args):
     return world, rank, local
 
 
-def _algorithmic_bytes(n_inst, m_vis, hw, n_tiles, depth_seeds=False):
-    """Compulsory HBM bytes per launch; the backward
-    reads dL/dC (24 B/pixel) and, with depth seeds, dL/dD (8 B/pixel)."""
-    rec = 32 + 16 + 112  # geo + ab + prm per visible voxel
+# SURVEY §8(d) algorithmic (compulsory) bytes -- the roofline numerators
+def bytes_raster_fwd(m, m_vis, hw):
+    return 16 * m + 112 * m_vis + 20 * hw
+
+
+def bytes_raster_bwd(m, m_vis, hw):
+    return 16 * m + 220 * m_vis + 32 * hw
+
+
+def bytes_lidar_fwd(r, u, n_nodes):
+    return 24 * r + 12 * r + 128 * u + 4 * n_nodes
+
+
+def traffic_model_raster(n_inst, m_vis, hw, n_tiles):
+    """What THIS implementation must move per launch (its layout), for comparison
+    with the ncu DRAM bytes: entry lists, 160-B records, CSR offsets, the f32
+    image planes, the 64-B/pixel fp64 saved state, fp64 dL/dC, the (M_vis, 27)
+    fp64 gradient rows."""
+    rec = 32 + 16 + 112
     fwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 20 * hw + 64 * hw
-    seeds = (32 if depth_seeds else 24) * hw
-    bwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 64 * hw + seeds + 216 * m_vis
+    bwd = 4 * n_inst + rec * m_vis + 8 * (n_tiles + 1) + 64 * hw + 24 * hw + 216 * m_vis
     return fwd, bwd
+
+
+# flop models for the secondary ALU roofline (FP32; stated in DESIGN.md §6)
+FLOP_PAIR = 24.0        # one ray-vs-voxel slab test (SURVEY §8d)
+FLOP_SEG_FWD = 120.0    # fields + opacity + colour + compositing of one included segment (SURVEY §8d)
+FLOP_SEG_BWD = 204.0    # the same fields (120) + the reverse chain and 27 gradient FMAs (84)
 
 
 def _alu_peak(dev, fp32: bool) -> float:
@@ -221,11 +329,23 @@ def _alu_peak(dev, fp32: bool) -> float:
     return best
 
 
-def _ncu_metrics():
-    """Per-kernel ncu metrics of the committed capture (profiles/), if present:
-    the roofline above is HBM; these kernels are FP64-pipe / latency bound."""
-    p = ROOT / "profiles" / "ncu_metrics.json"
+def _json_file(rel):
+    p = ROOT / rel
     return json.loads(p.read_text()) if p.exists() else None
+
+
+def _timeit(fn, n=10, warm=3):
+    import torch
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / n
 
 
 def run_ours(args, world, rank, local):
@@ -233,44 +353,35 @@ def run_ours(args, world, rank, local):
     import torch.distributed as dist
     from paper_2507_18713_b200 import _lib, configs
     from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200 import render_ray as RY
     from paper_2507_18713_b200.backward import l1_color_seed
     from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.parallel import allreduce_grad_
     from paper_2507_18713_b200.scenes import get_scene
+    from paper_2507_18713_b200.sensors import gen_lidar_rays
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     scene = get_scene("S1M", args.regime)
     ds = DeviceScene.from_scene(scene, device=dev)
-    # every rank renders the C2 view: identical per-rank work, so the N-GPU
-    # number measures the data-parallel step (weak scaling), not pose imbalance
-    cam = configs.c2_camera()
+    # N = 1: the C2 camera; N > 1: rank r renders C5-rig camera r (distinct views)
+    cam = configs.c2_camera(45.0 * (rank % 8) if world > 1 else 0.0)
     h, w = cam.height, cam.width
     g = torch.Generator().manual_seed(rank)
     gt_host = (0.3 + 0.4 * torch.rand((h, w, 3), generator=g)).pin_memory()
     gt_dev = gt_host.to(dev)
-    dd = None  # colour L1 loss only (losses.py:22-31): no depth seeds, the backward drops the depth term
     grad = torch.zeros((ds.n, _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     out_host = torch.empty((h, w, 3), dtype=torch.float32).pin_memory()
     loss_host = torch.empty(1, dtype=torch.float64).pin_memory()
 
-    from paper_2507_18713_b200.parallel import allreduce_grad_
-    SPARSE_ALLREDUCE = os.environ.get("SALF_SPARSE_ALLREDUCE", "1") == "1"
-
-    def allreduce_grad(buf):
-        # fp32 transport of the rows any rank touched (parallel.allreduce_grad_)
-        allreduce_grad_(buf, sparse=SPARSE_ALLREDUCE)
-
-    def step(gt, events=None, e2e=False):
+    def step(gt, events=None):
         fb, st = RR.rasterize(ds, cam, return_state=True, events=events)
         dc, lsum = l1_color_seed(fb.color, gt)  # losses.py:22-31, one fused kernel
         grad.zero_()
-        RR.rasterize_backward(st, dc, dd, grad, as_dict=False, events=events)
+        RR.rasterize_backward(st, dc, None, grad, as_dict=False, events=events)
         if world > 1:
-            allreduce_grad(grad)
-        if e2e:
-            loss_host.copy_((lsum / dc.numel()).reshape(1), non_blocking=True)
-            out_host.copy_(fb.color, non_blocking=True)
+            allreduce_grad_(grad)  # f64 transport of the rows any rank touched
         return st
 
     def barrier():
@@ -283,8 +394,8 @@ def run_ours(args, world, rank, local):
     barrier()
 
     # kernel launches of one step (CUPTI via torch.profiler; outside the timed region)
-    launches = None
-    ours = None
+    launches = ours = None
+    kernel_names = None
     try:
         if args.no_profile:
             raise RuntimeError("--no-profile")
@@ -295,9 +406,10 @@ def run_ours(args, world, rank, local):
         kern = [e for e in prof.events() if e.device_type.name == "CUDA"
                 and not e.name.lower().startswith(("memcpy", "memset"))]
         launches = len(kern)
-        ours = sum(1 for e in kern if "salf" in e.name or "k_" in e.name or "cub" in e.name.lower())
+        mine = [e.name for e in kern if "salf" in e.name or "k_" in e.name]
+        ours = len(mine)
+        kernel_names = sorted({n.split("(")[0].split("<")[0].replace("void ", "") for n in mine})
     except Exception as ex:  # profiler unavailable: leave the count unset
-        ours = None
         print(f"[bench] launch count unavailable: {ex}", file=sys.stderr)
 
     # ---- device-timed steps, inputs resident, L2 flushed between steps ----
@@ -364,32 +476,66 @@ def run_ours(args, world, rank, local):
                     gt_bufs[(k + 1) % 2].copy_(gt_host, non_blocking=True)
                     up[(k + 1) % 2].record(xs)
             grad.zero_()
-            RR.rasterize_backward(st, dc, dd, grad, as_dict=False)
+            RR.rasterize_backward(st, dc, None, grad, as_dict=False)
             if world > 1:
-                allreduce_grad(grad)
+                allreduce_grad_(grad)
         cs.wait_stream(xs)
         b.record(cs)
         return a, b
 
-    # untimed warm-up of the end-to-end pipeline (pinned copies, side stream,
-    # allocator blocks held by record_stream), then the timed pass
     e2e_pass(max(args.warmup, 3))
     barrier()
     a, b = e2e_pass(args.steps)
     barrier()
-    e2e_ms = a.elapsed_time(b) / args.steps
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    te = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = world * 1e3 / float(te.item())
 
-    # ---- the LiDAR half of the metric at N GPUs: each rank sweeps its own
-    # 128 x 1800 C3 LiDAR (sensor-sharded, no exchange), device-timed, max over ranks ----
-    from paper_2507_18713_b200 import render_ray as RY
-    from paper_2507_18713_b200.sensors import gen_lidar_rays
+    # ---- roofline of the dominant kernel (SURVEY §8d bytes) ----
+    peaks = _json_file("MEASURED_PEAKS.json") or {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    n_inst = st.n_instances
+    m_vis = int(torch.unique(st.entries).numel()) if n_inst else 0
+    hw = h * w
+    n_tiles = st.offsets.numel() - 1
+    k_fwd = float(np.mean(kms.get("raster_composite", [np.nan])))
+    k_bwd = float(np.mean(kms.get("raster_backward", [np.nan])))
+    fwd_b, bwd_b = bytes_raster_fwd(ds.n, m_vis, hw), bytes_raster_bwd(ds.n, m_vis, hw)
+    fwd_t, bwd_t = traffic_model_raster(n_inst, m_vis, hw, n_tiles)
+    dom, dom_ms, dom_b, dom_t = ("raster_backward", k_bwd, bwd_b, bwd_t) if k_bwd >= k_fwd else \
+        ("raster_composite", k_fwd, fwd_b, fwd_t)
+    achieved = dom_b / (dom_ms * 1e-3) / 1e9
+    traffic = (_json_file("profiles/traffic.json") or {}).get(dom)
+
+    # secondary ALU rooflines: P pair tests and S_inc included segments (read
+    # from the frame's saved state) against a live FP32 FFMA probe
+    sv = st.saved
+    pairs = float(sv[:, 6].sum().item())  # list entries each pixel visited = pair tests
+    s_inc = float(sv[:, 7].sum().item())
+    fp32_peak = _alu_peak(dev, fp32=True)
+    f_fwd = FLOP_PAIR * pairs + FLOP_SEG_FWD * s_inc
+    f_bwd = FLOP_PAIR * pairs + FLOP_SEG_BWD * s_inc
+
+    def alu(kernel, flops, kms_):
+        ach = flops / (kms_ * 1e-3) / 1e12
+        return {"bound": "fp32", "kernel": kernel, "unit": "TFLOP/s", "achieved": ach, "peak": fp32_peak,
+                "frac": ach / fp32_peak, "flops": flops, "kernel_ms": kms_}
+
+    roofline_alu = {
+        "raster_backward": {**alu("raster_backward", f_bwd, k_bwd),
+                            "formula": f"{FLOP_PAIR:.0f} P + {FLOP_SEG_BWD:.0f} S_inc (DESIGN.md §6)"},
+        "raster_composite": {**alu("raster_composite", f_fwd, k_fwd),
+                             "formula": f"{FLOP_PAIR:.0f} P + {FLOP_SEG_FWD:.0f} S_inc (SURVEY §8d)"},
+        "pair_tests": pairs, "included_segments": s_inc,
+        "peak_source": "live FFMA probe (salf_fp32_peak)", "fp64_peak": _alu_peak(dev, fp32=False),
+        "ncu": _json_file("profiles/ncu_metrics.json"),
+    }
+
+    # ---- C3 LiDAR: one sweep per rank (sensor-sharded, no exchange) ----
     oc = RY.build_scene_octrees(scene)
     lid = configs.c3_lidar()
-    lb = gen_lidar_rays(lid)
+    lb = gen_lidar_rays(lid, device=dev)
     for _ in range(max(args.warmup, 3)):
         RY.render_lidar(ds, oc, lb)
     barrier()
@@ -403,88 +549,112 @@ def run_ours(args, world, rank, local):
     if world > 1:
         dist.all_reduce(t_l, op=dist.ReduceOp.MAX)
     lidar_ms = float(t_l.item())
-    del oc
+    lidar = {"metric": "LiDAR rays/s (128 beams x 1800 steps, S1M init)", "rays_per_s": world * lb.n / (lidar_ms * 1e-3),
+             "sweeps_per_s": world * 1e3 / lidar_ms, "ms_per_sweep": lidar_ms, "n_gpus": world,
+             "scaling": "weak", "sharding": "one LiDAR sweep per rank, no exchange"}
+
+    # ---- C5: the rig training step sharded over the ranks (strong scaling) ----
+    c5 = c5_step(args, world, rank, dev, scene, ds, oc, barrier)
 
     if rank != 0:
         return
 
-    # ---- roofline of the dominant kernel ----
-    peaks = {}
-    pp = ROOT / "MEASURED_PEAKS.json"
-    if pp.exists():
-        peaks = json.loads(pp.read_text())
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    n_inst = st.n_instances
-    m_vis = int(torch.unique(st.entries).numel()) if n_inst else 0
-    fwd_b, bwd_b = _algorithmic_bytes(n_inst, m_vis, h * w, (st.offsets.numel() - 1))
-    k_fwd = float(np.mean(kms.get("raster_composite", [np.nan])))
-    k_bwd = float(np.mean(kms.get("raster_backward", [np.nan])))
-    dom, dom_ms, dom_b = ("raster_backward", k_bwd, bwd_b) if k_bwd >= k_fwd else \
-        ("raster_composite", k_fwd, fwd_b)
-    achieved = dom_b / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
-        traffic = json.loads(tp.read_text()).get(dom)
-
-    # secondary (ALU) roofline of the forward composite: SURVEY §8d's
-    # F = 24 P + 120 S_inc flop (P = pair tests, S_inc = included segments,
-    # both read from the frame's saved state) against a live FP32 FFMA peak
-    # probe -- the default path shades in fp32 (fp64 only for the per-pair
-    # closest-approach parameter and the log-transmittance sum)
-    sv = st.saved
-    pairs = float(sv[:, 6].sum().item())
-    s_inc = float(sv[:, 7].sum().item())
-    flops = 24.0 * pairs + 120.0 * s_inc
-    fp32_peak = _alu_peak(dev, fp32=True)
-    alu = {"bound": "fp32", "kernel": "raster_composite", "unit": "TFLOP/s",
-           "achieved": flops / (k_fwd * 1e-3) / 1e12, "peak": fp32_peak,
-           "frac": flops / (k_fwd * 1e-3) / 1e12 / fp32_peak, "flops": flops,
-           "pair_tests": pairs, "included_segments": s_inc,
-           "formula": "24 P + 120 S_inc (SURVEY 8d)", "peak_source": "live FFMA probe (salf_fp32_peak)",
-           "fp64_peak": _alu_peak(dev, fp32=False)}
+    if not args.no_extras:
+        # LiDAR HBM roofline: U = distinct voxels touched by the sweep's segments
+        ret = RY.render_lidar(ds, oc, lb)
+        ray, vid, _, _ = RY.segments(ds, oc, lb.origins, lb.dirs)
+        u = int(torch.unique(vid).numel())
+        del ray, vid
+        n_nodes = int(oc.static.n_nodes)
+        lb_bytes = bytes_lidar_fwd(lb.n, u, n_nodes)
+        la_ach = lb_bytes / (lidar_ms * 1e-3) / 1e9
+        lidar["roofline"] = {"bound": "hbm", "kernel": "ray_forward (LiDAR)", "achieved": la_ach, "peak": peak,
+                             "unit": "GB/s", "frac": la_ach / peak, "algorithmic_bytes": lb_bytes,
+                             "touched_voxels": u, "octree_nodes": n_nodes, "rays": lb.n,
+                             "segments": int(ret.saved[:, 6].sum().item()),
+                             "formula": "36 R + 128 U + 4 N_nodes (SURVEY §8d)",
+                             "traffic": (_json_file("profiles/traffic.json") or {}).get("ray_forward")}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms_max, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256; random target image)",
-        "config": {"workload": WORKLOAD, "regime": args.regime, "resolution": [w, h],
-                   "voxels": ds.n, "parallelism": f"data-parallel x{world} (C2 view per rank), grad all-reduce "
-                   f"({os.environ.get('SALF_BENCH_BACKEND', 'nccl').upper()}, fp32 transport"
-                   + (", rows any rank touched)" if SPARSE_ALLREDUCE else ")"),
-                   "l2": "flushed (256 MB write) between timed steps", "render_instances": n_inst,
-                   "visible_voxels": m_vis},
+        "config": config_dict(args.regime, world, {"render_instances": n_inst, "visible_voxels": m_vis}),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(gt_host.nbytes),
                 "d2h_bytes_per_step": int(out_host.nbytes + loss_host.nbytes)},
         "gpu_launches": ours if ours is not None else launches,
         "gpu_launches_all": launches,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "algorithmic_bytes": dom_b, "kernel_ms": dom_ms,
+        "kernels": kernel_names,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": dom_b,
+                     "formula": "16 M + 220 M_vis + 32 H W (SURVEY §8d, raster backward)"
+                     if dom == "raster_backward" else "16 M + 112 M_vis + 20 H W (SURVEY §8d, raster forward)",
+                     "traffic_model": dom_t, "kernel_ms": dom_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
-        "roofline_alu": alu,
-        "lidar": {"metric": "LiDAR rays/s (128-beam, 1800 steps, S1M init)", "rays_per_s": world * lb.n / (lidar_ms * 1e-3),
-                  "sweeps_per_s": world * 1e3 / lidar_ms, "ms_per_sweep": lidar_ms, "n_gpus": world,
-                  "scaling": "weak", "sharding": "one LiDAR sweep per rank, no exchange"},
+        "roofline_alu": roofline_alu,
+        "lidar": lidar,
+        "c5": c5,
         "kernels_ms": {k: float(np.mean(v)) for k, v in kms.items()},
-        "ncu": _ncu_metrics(),
         "clocks": clk,
     }
-    if not args.no_extras and world == 1:
-        line["extras"] = extras(ds, args)
-    if not args.no_cpu and world == 1:
-        base = CpuBaseline(args.regime)
-        v, info = base.sample(7)
-        base.close()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": base.workers, "kind": "port",
-                                "sample": f"{base.workers} 16x16 tiles of 8160 stratified over tile rows (fwd+bwd), "
-                                          f"{info['wall_s']:.1f} s wall, extrapolated to the frame"}
+    if world == 1 and not args.no_extras:
+        line["extras"] = extras(ds, oc, args)
+    if world == 1 and not args.no_cpu:
+        line.update(cpu_baselines(args, ds, dev, lidar_ms, value))
     print(json.dumps(line), flush=True)
 
 
-def extras(ds, args):
-    """Secondary configurations on rank 0: C2 forward only, C3 LiDAR, C4 fisheye, surface regime."""
+def c5_step(args, world, rank, dev, scene, ds, oc, barrier):
+    """C5: 8 cameras + 2 LiDARs sharded over the ranks (split_work -> assign:
+    pinhole row bands and LiDAR ray blocks, LPT-balanced), global L1 seeds
+    (counts all-reduced), raster + ray backward into the (M, 27) buffer, NCCL
+    all-reduce of the touched rows (f64), device Adam.  Strong scaling."""
+    import torch
+    import torch.distributed as dist
+    from paper_2507_18713_b200 import configs
+    from paper_2507_18713_b200.optim import TrainableScene
+    from paper_2507_18713_b200.parallel import assign, split_work
+    from paper_2507_18713_b200.train_step import rig_step
+    ts = TrainableScene(scene, device=dev)
+    cams, lidars = configs.c5_rig()
+    sensors = cams + lidars
+    g = torch.Generator().manual_seed(5)
+    targets = [torch.rand((c.height, c.width, 3), generator=g, dtype=torch.float64).to(dev) for c in cams] + \
+              [(1.0 + 20.0 * torch.rand(l.beam_elevations.shape[0] * l.steps, generator=g,
+                                        dtype=torch.float64)).to(dev) for l in lidars]
+    items = assign(split_work(sensors, world), world)[rank]
+    gbuf = ts.zero_grad()
+
+    def one():
+        gbuf.zero_()
+        rig_step(ts.ds, oc, sensors, targets, items, gbuf)
+        ts.adam_step(gbuf)
+
+    n = max(2, min(args.steps, 5))
+    for _ in range(2):
+        one()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        one()
+    b.record()
+    barrier()
+    t = torch.tensor([a.elapsed_time(b) / n], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    del ts, gbuf, targets
+    return {"metric": "C5 rig training steps/s (8 x 1920x1080 cameras + 2 x 128x1800 LiDARs, S1M)",
+            "steps_per_s": 1e3 / ms, "ms_per_step": ms, "camera_frames_per_s": 8e3 / ms,
+            "lidar_rays_per_s": 2 * 230400 * 1e3 / ms, "n_gpus": world, "scaling": "strong",
+            "items_this_rank": len(items), "steps": n,
+            "includes": "forward, global L1 seeds, raster + ray backward, grad all-reduce, device Adam + refresh"}
+
+
+def extras(ds, oc, args):
+    """Secondary configurations on rank 0: C2 forward only, surface regime, C4, intensity/ray-drop."""
     import torch
     from paper_2507_18713_b200 import configs
     from paper_2507_18713_b200 import render_raster as RR
@@ -493,42 +663,43 @@ def extras(ds, args):
     from paper_2507_18713_b200.scenes import get_scene
     from paper_2507_18713_b200.sensors import camera_rays, gen_lidar_rays
 
-    def timeit(fn, n=10):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(n):
-            fn()
-        b.record()
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / n
-
     out = {}
     cam = configs.c2_camera()
-    out["c2_forward_fps"] = 1e3 / timeit(lambda: RR.rasterize(ds, cam))
-    scene = get_scene("S1M", args.regime)
-    oc = RY.build_scene_octrees(scene)
+    out["c2_forward_fps"] = 1e3 / _timeit(lambda: RR.rasterize(ds, cam))
     lidar = configs.c3_lidar()
     lb = gen_lidar_rays(lidar)
-
-    def c3(dsx, ocx, **kw):
-        ms = timeit(lambda: RY.render_lidar(dsx, ocx, lb, **kw))
-        ms_gen = timeit(lambda: RY.render_lidar(dsx, ocx, gen_lidar_rays(lidar), **kw))
-        ret = RY.render_lidar(dsx, ocx, lb, **kw)
-        return {"rays_per_s": lb.n / (ms * 1e-3), "sweeps_per_s": 1e3 / ms, "ms": ms,
-                "ms_with_raygen": ms_gen, "rays": lb.n,
-                "segments": int(ret.saved[:, 6].sum().item()),
-                "returns": int(torch.isfinite(ret.depth).sum().item()),
-                "status_max": int(ret.status.max().item())}
-
-    out["c3_lidar"] = c3(ds, oc)
     rng = np.random.default_rng(0)
     feat = torch.as_tensor(rng.uniform(-1, 1, (ds.n, 8)).astype(np.float32), device=ds.device)
     head = rng.uniform(-0.5, 0.5, (2, 13)).astype(np.float32)
-    out["c3_lidar_intensity_raydrop"] = c3(ds, oc, features=feat, head=head)
+    ms = _timeit(lambda: RY.render_lidar(ds, oc, lb, features=feat, head=head))
+    out["c3_lidar_intensity_raydrop"] = {"sweeps_per_s": 1e3 / ms, "rays_per_s": lb.n / (ms * 1e-3), "ms": ms}
+    ms = _timeit(lambda: RY.render_lidar(ds, oc, gen_lidar_rays(lidar)))
+    out["c3_lidar_with_raygen"] = {"sweeps_per_s": 1e3 / ms, "ms": ms}
     del feat
+
+    # BASELINE.md §3 surface regime: bake (a = 50, b = 0.02) + the reference prune (densify.py:39-46)
+    def regime_block(name, note):
+        sc = get_scene("S1M", name)
+        dss = DeviceScene.from_scene(sc)
+        ocs = RY.build_scene_octrees(sc)
+        dcs = torch.full((1080, 1920, 3), 1e-7, dtype=torch.float64, device=dss.device)
+
+        def fb_step():
+            fb, st = RR.rasterize(dss, cam, return_state=True)
+            RR.rasterize_backward(st, dcs, None, as_dict=False)
+
+        ms_l = _timeit(lambda: RY.render_lidar(dss, ocs, lb))
+        return {"voxels": dss.n, "c2_forward_fps": 1e3 / _timeit(lambda: RR.rasterize(dss, cam)),
+                "c2_fwd_bwd_fps": 1e3 / _timeit(fb_step, n=5),
+                "c3_lidar_sweeps_per_s": 1e3 / ms_l, "c3_lidar_rays_per_s": lb.n / (ms_l * 1e-3),
+                "note": note}
+
+    out["surface_regime"] = regime_block(
+        "surface", "BASELINE.md §3: S1M fields baked from the analytic primitives (a = 50, b = 0.02, "
+                   "SH DC = logit(albedo)/C0), pruned by center_opacity < 0.005 (densify.py:39-46)")
+    out["surface_dense_regime"] = regime_block(
+        "surface-dense", "trained-like: S1M inner region densified to level 7 near the analytic surfaces, "
+                         "fields baked a = 400, b = 0.004 (scenes.make_dense_surface_scene)")
     s2 = get_scene("S2M", "init")
     ds2 = DeviceScene.from_scene(s2)
     oc2 = RY.build_scene_octrees(s2)
@@ -536,92 +707,62 @@ def extras(ds, args):
 
     def c4_frame():
         b = camera_rays(c4)
-        return RY.integrate_rays(ds2, oc2, b.origins, b.dirs, valid=b.valid, check_unit=False)
+        return RY.integrate_rays(ds2, oc2, b.origins, b.dirs, valid=b.valid, check_unit=False, check=False)
 
-    out["c4_fisheye_rs_fps_S2M"] = 1e3 / timeit(c4_frame, n=5)
+    out["c4_fisheye_rs_fps_S2M"] = 1e3 / _timeit(c4_frame, n=5)
     del ds2, oc2
-    sur = get_scene("S1M", "surface-dense")
-    dss = DeviceScene.from_scene(sur)
-    ocs = RY.build_scene_octrees(sur)
-    dcs = torch.full((1080, 1920, 3), 1e-7, dtype=torch.float64, device=dss.device)
-    dds = None  # colour-only loss
+    return out
 
-    def fb_step():
-        fb, st = RR.rasterize(dss, cam, return_state=True)
-        RR.rasterize_backward(st, dcs, dds, as_dict=False)
 
-    # C5: the 8-camera + 2-LiDAR rig training step on one GPU (all sensors on
-    # this rank): forward, global L1 seeds, backward, then device Adam
-    from paper_2507_18713_b200.optim import TrainableScene
-    from paper_2507_18713_b200.parallel import split_work
-    from paper_2507_18713_b200.train_step import rig_step
-    ts = TrainableScene(scene)
-    cams, lidars = configs.c5_rig()
-    sensors = cams + lidars
-    g = torch.Generator().manual_seed(5)
-    targets = [torch.rand((c.height, c.width, 3), generator=g, dtype=torch.float64).to(ts.ds.device)
-               for c in cams] + [(1.0 + 20.0 * torch.rand(l.beam_elevations.shape[0] * l.steps, generator=g,
-                                                            dtype=torch.float64)).to(ts.ds.device) for l in lidars]
-    items = split_work(sensors, 1)
-    gbuf = ts.zero_grad()
-
-    def c5_step():
-        gbuf.zero_()
-        rig_step(ts.ds, oc, sensors, targets, items, gbuf)
-        ts.adam_step(gbuf)
-
-    ms5 = timeit(c5_step, n=3)
-    out["c5_train_step"] = {"ms": ms5, "steps_per_s": 1e3 / ms5, "sensors": "8 x 1920x1080 pinhole + 2 x 128x1800 LiDAR",
-                            "includes": "forward, L1 seeds, raster + ray backward, device Adam, scene refresh"}
-    del ts, gbuf, targets
-    # §8f rows beyond the hot path: densify round, salf.v1 device load, secondary effects
-    import time
-    from paper_2507_18713_b200.densify import DensifyConfig
-    from paper_2507_18713_b200.device import load_device_scene
-    from paper_2507_18713_b200.octree import build_octree_from_device
-    from paper_2507_18713_b200.scenes import DATA
-    ts = TrainableScene(scene)
-    gacc = torch.rand(ts.n, dtype=torch.float64, device=ts.ds.device, generator=torch.Generator(
-        device=ts.ds.device).manual_seed(1))
-
-    def dens():
-        t2 = TrainableScene.__new__(TrainableScene)
-        t2.__dict__.update(ts.__dict__)
-        t2.densify(gacc, DensifyConfig(budget=ts.n + 40 * 20000))
-        build_octree_from_device(t2.level8, t2.ijk, scene.bounds)
-
-    out["densify_round_S1M"] = {"ms": timeit(dens, n=3), "splits": 20000,
-                                "includes": "flags, ranking, gather + 8-child expansion, moment remap, "
-                                            "device scene rebuild, device octree build"}
-    del ts, gacc
-    sp = DATA / "S1M_init"
-    if (sp / "voxels.bin").exists():
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        load_device_scene(sp)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        from paper_2507_18713_b200.scene import load_scene
-        sc_h, _ = load_scene(sp)
-        DeviceScene.from_scene(sc_h)
-        torch.cuda.synchronize()
-        t2 = time.perf_counter()
-        out["scene_load_S1M"] = {"device_decode_s": t1 - t0, "host_load_plus_upload_s": t2 - t1,
-                                 "bytes": (sp / "voxels.bin").stat().st_size}
-    sph = [RY.InjectedSphere([2.0, 0.0, 0.8], 0.6, "mirror"), RY.InjectedSphere([4.0, 1.5, 0.6], 0.5, "glass"),
-           RY.InjectedSphere([3.0, -1.5, 0.5], 0.4, "opaque", albedo=[0.8, 0.2, 0.1])]
-    cb = camera_rays(cam)
-    out["effects_c2_camera_S1M"] = {
-        "fps": 1e3 / timeit(lambda: RY.trace_effects(ds, oc, cb.origins, cb.dirs, None, sph, [0.3, -0.5, 0.8],
-                                                     max_bounces=2), n=3),
-        "rays": cb.n, "spheres": "mirror, glass, opaque; 2 bounces; sun shadows"}
-    out["surface_dense_regime"] = {
-        "voxels": dss.n,
-        "c2_forward_fps": 1e3 / timeit(lambda: RR.rasterize(dss, cam)),
-        "c2_fwd_bwd_fps": 1e3 / timeit(fb_step, n=5),
-        "c3_lidar": c3(dss, ocs),
-        "note": "trained-like scene: S1M inner region densified to level 7 near the analytic "
-                "surfaces (scenes.make_dense_surface_scene), fields baked a=400, b=0.004"}
+def cpu_baselines(args, ds, dev, lidar_ms, value):
+    """The reference algorithm on this box's cores (OMP_NUM_THREADS=1 workers):
+    C2 sampled (extrapolated, labelled), C1 whole frame and C3 whole sweep
+    (not extrapolated), each next to the GPU number of the same workload."""
+    from paper_2507_18713_b200 import configs
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scenes import get_scene
+    out = {}
+    pool = CpuPool("c2", args.regime)
+    vals = []
+    walls = []
+    for k in range(2):
+        v, wall, tile_s = c2_cpu_step(pool, 7 + k)
+        vals.append(v)
+        walls.append(wall)
+    pool.close()
+    v = float(np.mean(vals))
+    out["cpu_baseline"] = {
+        "value": v, "unit": UNIT, "cores": pool.workers, "kind": "port",
+        "sample": f"2 x {pool.workers} random 16x16 tiles of the 8160 (one per worker, stratified over tile rows), "
+                  f"fwd + bwd, projection once per worker, {float(np.sum(walls)):.1f} s wall; frame time = "
+                  f"8160/k x sum(tile s) / {pool.workers} workers (EXTRAPOLATED)",
+        "gpu_over_cpu": value / v}
+    # C1: the whole 256^2 frame on S20k, row bands over the cores, vs the GPU
+    import torch
+    pool = CpuPool("c1")
+    wall, img = c1_cpu_frame(pool)
+    pool.close()
+    c1cam = configs.c1_camera()
+    from paper_2507_18713_b200.device import DeviceScene
+    ds20 = DeviceScene.from_scene(get_scene("S20k", "init"), device=dev)
+    gpu_ms = _timeit(lambda: RR.rasterize(ds20, c1cam), n=20)
+    gimg = RR.rasterize(ds20, c1cam).color.double().cpu().numpy()
+    out["c1"] = {"workload": "C1: S20k (19,992 voxels), 256x256 pinhole raster forward (BASELINE configs[0])",
+                 "gpu_fps": 1e3 / gpu_ms, "cpu_fps": 1.0 / wall, "cpu_cores": pool.workers,
+                 "cpu_kind": "port", "cpu_s_per_frame": wall, "gpu_over_cpu": (1e3 / gpu_ms) * wall,
+                 "max_abs_diff_gpu_vs_cpu": float(np.abs(gimg - img).max()),
+                 "note": "whole frame on both sides, not extrapolated (16 tile-row bands over the workers)"}
+    del ds20
+    # C3: the whole sweep on the cores vs the GPU sweep
+    pool = CpuPool("c3")
+    wall, dep = c3_cpu_sweep(pool)
+    pool.close()
+    out["cpu_baseline_lidar"] = {
+        "workload": "C3: 128 x 1800 LiDAR sweep on S1M (BASELINE configs[2])",
+        "value": 230400 / wall, "unit": "rays/s", "cores": pool.workers, "kind": "port",
+        "sample": "the whole sweep (230,400 rays) in ray blocks over the workers, not extrapolated",
+        "gpu_rays_per_s": 230400 / (lidar_ms * 1e-3), "gpu_over_cpu": (230400 / (lidar_ms * 1e-3)) / (230400 / wall),
+        "returns": int(np.isfinite(dep).sum())}
     return out
 
 

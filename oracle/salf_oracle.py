@@ -387,6 +387,11 @@ def cull_and_bin(vox: Voxels, cam: Camera, tile=TILE_SIZE, near=NEAR_PLANE, wind
     return tx_n, ty_n, offsets, vid[order]
 
 
+def pixel_rays(cam: Camera, near=NEAR_PLANE):
+    """(dirs, t_near) of every pixel (render_raster.py:212-215); reusable across calls (pix_rays=)."""
+    return _pixel_rays(cam, near)
+
+
 def _pixel_rays(cam: Camera, near):
     rays = camera_rays(Camera(cam.kind, cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy,
                               position=cam.position, quaternion=cam.quaternion))
@@ -416,7 +421,7 @@ def _pair_segments(vox: Voxels, origin, dirs, t_near, pix, vid):
 
 def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SIZE,
               near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, rows=None, window=None, tiles=None,
-              proj=None):
+              proj=None, pix_rays=None):
     """render_raster.py:201-301, tile by tile.
 
     `rows=(r0, r1)` restricts work to tile rows r0..r1-1 and `window` to a
@@ -427,7 +432,7 @@ def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SI
     if rows is not None and window is None:
         window = (0, rows[0], -(-w // tile) - 1, rows[1] - 1)
     tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window, tiles, proj)
-    dirs, t_near = _pixel_rays(cam, near)
+    dirs, t_near = _pixel_rays(cam, near) if pix_rays is None else pix_rays
     keep = 1.0 - stop_threshold
     acc_c = np.zeros((h * w, 3))
     acc_l = np.zeros(h * w)
@@ -466,7 +471,7 @@ def rasterize(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SI
 
 def raster_records(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TILE_SIZE,
                    near=NEAR_PLANE, stop_threshold=STOP_THRESHOLD, window=None, tiles=None,
-                   proj=None):
+                   proj=None, pix_rays=None):
     """Raster pairs restated as ray-path records (one ray per pixel, row-major).
 
     The reference has no raster backward; its gradient is defined by
@@ -476,7 +481,7 @@ def raster_records(vox: Voxels, cam: Camera, background=(0.0, 0.0, 0.0), tile=TI
     (backward.py:35-101).  Misses carry alpha = 0 and drop out exactly."""
     h, w = cam.height, cam.width
     tx_n, ty_n, offsets, entries = cull_and_bin(vox, cam, tile, near, window, tiles, proj)
-    dirs, t_near = _pixel_rays(cam, near)
+    dirs, t_near = _pixel_rays(cam, near) if pix_rays is None else pix_rays
     chunks = []
     for t in range(tx_n * ty_n):
         ent = entries[offsets[t]:offsets[t + 1]]

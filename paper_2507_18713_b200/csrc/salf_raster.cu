@@ -661,6 +661,7 @@ struct RayF {
   double tn0;  // max(t_near, 0)
   float df[3], dl[3], inv[3], gam[4];  // d = df + dl (two-float split)
   float tn0f;
+  float refine;  // backward: chords shorter than refine * h/2 are re-derived in fp64
   bool fast;   // no zero component (else the fp64 reference slab test runs)
 };
 
@@ -676,6 +677,7 @@ __device__ __forceinline__ void rayf_from_dir(const double d[3], double t_near, 
   }
   r.tn0 = t_near > 0.0 ? t_near : 0.0;
   r.tn0f = (float)r.tn0;
+  r.refine = fmaxf(0.125f, 0.24f * fmaxf(fabsf(r.inv[0]), fmaxf(fabsf(r.inv[1]), fabsf(r.inv[2]))));
   r.gam[0] = (float)kShC0;
   r.gam[1] = (float)(kShC1 * d[1]);
   r.gam[2] = (float)(kShC1 * d[2]);
@@ -853,17 +855,11 @@ __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, flo
     }
     const float u0f = fmaxf(un, (float)(r.tn0 - ts));
     if (!(uf > u0f)) return false;
-    // the fp32 slab values carry ~1.2e-7 hf |1/d_k| each (k the binding axes):
-    // re-derive the chord in fp64 unless its relative error is below ~1e-6
-    // (and always below the forward's threshold, so both see the same hits)
-    float ia = 0.f;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float qi = q[k] * r.inv[k];
-      const float nk = __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi), fk = __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi);
-      if (nk == un || fk == uf) ia += fabsf(r.inv[k]);
-    }
-    if (uf - u0f < e.hf * fmaxf(2.f * kRefineChord, 0.12f * ia)) {  // fp64 chord (as the forward)
+    // the fp32 slab values carry ~1.2e-7 hf |1/d_k| each: re-derive the chord
+    // in fp64 unless its relative error is below ~1e-6 (r.refine =
+    // max(0.24 max_k |1/d_k|, 2 kRefineChord) >= the forward's threshold, so
+    // both passes see the same hits)
+    if (uf - u0f < e.hf * r.refine) {  // fp64 chord (as the forward)
       double u0, u1;
       if (!chord64(r, e, ts, u0, u1)) return false;
       delta = (float)(u1 - u0);
