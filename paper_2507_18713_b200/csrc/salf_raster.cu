@@ -661,10 +661,19 @@ struct RayF {
   double tn0;  // max(t_near, 0)
   float df[3], dl[3], inv[3], gam[4];  // d = df + dl (two-float split)
   float tn0f;
-  float refine;  // backward: chords shorter than refine * h/2 are re-derived in fp64
+  float refine;  // backward: chords shorter than refine * h/2 are re-derived in fp64 (pair_hit_bwd)
   bool fast;   // no zero component (else the fp64 reference slab test runs)
 };
 
+#ifndef SALF_REFINE_MIN
+#define SALF_REFINE_MIN 0.0f
+#endif
+#ifndef SALF_REFINE_K
+#define SALF_REFINE_K 0.05f
+#endif
+#ifndef SALF_CHORD_INLINE
+#define SALF_CHORD_INLINE __forceinline__
+#endif
 __device__ __forceinline__ void rayf_from_dir(const double d[3], double t_near, RayF &r) {
   r.fast = true;
 #pragma unroll
@@ -677,7 +686,7 @@ __device__ __forceinline__ void rayf_from_dir(const double d[3], double t_near, 
   }
   r.tn0 = t_near > 0.0 ? t_near : 0.0;
   r.tn0f = (float)r.tn0;
-  r.refine = fmaxf(0.125f, 0.24f * fmaxf(fabsf(r.inv[0]), fmaxf(fabsf(r.inv[1]), fabsf(r.inv[2]))));
+  r.refine = fmaxf(SALF_REFINE_MIN, SALF_REFINE_K * fmaxf(fabsf(r.inv[0]), fmaxf(fabsf(r.inv[1]), fabsf(r.inv[2]))));
   r.gam[0] = (float)kShC0;
   r.gam[1] = (float)(kShC1 * d[1]);
   r.gam[2] = (float)(kShC1 * d[2]);
@@ -743,19 +752,21 @@ __device__ __forceinline__ void stage_entry_f(const salf_scene_t &sc, const Pinh
   }
 }
 
-// Short chords (grazing pairs) are re-derived in fp64: the fp32 slab values
-// carry ~2^-24 h |1/d| each, a large RELATIVE error of a chord of length
-// delta << h -- enough to turn an fp64 miss into an fp32 hit with y ~ 1e-7
-// (an opacity of 5e-7 where the reference has 0) or to skew a grazing
-// segment's alpha and gradient by 1e-3.  Chords shorter than h / 16 are
-// recomputed from the three slabs and the near plane in fp64 (1/d by one
-// Newton step on the fp32 reciprocal, |err| ~ 2^-46) and kept iff
-// t1 > t0 + 1e-12 (render_raster.py:241).  The backward refines a superset
-// (every chord whose fp32 length is not accurate to ~1e-6), so both passes
-// see the same hits.
-constexpr float kRefineChord = 0.0625f;
+// Short chords (grazing pairs): the fp32 slab values carry ~2^-24 h |1/d|
+// each, a large RELATIVE error of a chord of length delta << h -- enough to
+// turn an fp64 miss into an fp32 hit with y ~ 1e-7 (an opacity of 5e-7 where
+// the reference has 0) or to skew a grazing segment's alpha and gradient by
+// 1e-3.  The certified forward flags every pixel with a hit whose fp32 chord
+// is within its error band of zero (fp64 redo decides it); the backward
+// re-derives every chord whose fp32 length is not accurate to ~1e-6 from the
+// three slabs and the near plane in fp64 (1/d by one Newton step on the fp32
+// reciprocal, |err| ~ 2^-46), kept iff t1 > t0 + 1e-12 (render_raster.py:241),
+// so both passes see the reference's hits.
+#ifndef SALF_BWD_REFINE
+#define SALF_BWD_REFINE 1  // A/B only: 0 keeps every fp32 chord (not parity-safe)
+#endif
 
-__device__ __forceinline__ bool chord64(const RayF &r, const EntryF &e, double ts, double &u0, double &u1) {
+__device__ SALF_CHORD_INLINE bool chord64(const RayF &r, const EntryF &e, double ts, double &u0, double &u1) {
   u0 = r.tn0 - ts;
   u1 = INFINITY;
 #pragma unroll
@@ -768,14 +779,6 @@ __device__ __forceinline__ bool chord64(const RayF &r, const EntryF &e, double t
     u1 = fmin(u1, hi - qi);
   }
   return u1 > u0 + 1e-12;
-}
-
-__device__ __noinline__ bool refine_chord(const RayF &r, const EntryF &e, double ts, float &u0, float &u1) {
-  double a, b;
-  if (!chord64(r, e, ts, a, b)) return false;
-  u0 = (float)a;
-  u1 = (float)b;
-  return true;
 }
 
 // Pair test in closest-approach coordinates.  With t* ~ -(o . d) (any
@@ -803,9 +806,7 @@ __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float
     }
     u0 = fmaxf(un, r.tn0f - ts);
     u1 = uf;
-    if (!(u1 > u0)) return false;
-    if (u1 - u0 < kRefineChord * e.hf) return refine_chord(r, e, (double)ts, u0, u1);
-    return true;
+    return u1 > u0;
   }
   const double tsd = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
   ts = (float)tsd;
@@ -838,8 +839,13 @@ __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float
 
 // The backward's variant: t* and q in fp64 (6 DFMA), rounded to fp32 once
 // for the hit test.  (The two-float form above measured slower in the
-// issue-bound backward.)  Short chords are re-derived in fp64 (chord64, the
-// forward's rule).  Outputs delta and um = t_mid - t*.
+// issue-bound backward.)  A chord whose fp32 length is not accurate to ~5e-6
+// (delta < refine h/2 with r.refine = 0.05 max_k |1/d_k|; the fp32 slab
+// values carry ~1.2e-7 h/2 |1/d_k| each) is re-derived in fp64 (chord64;
+// kExact: every chord).  A superset of the chords the forward flags
+// (delta <= 2 dd ~ 1.4e-6 h/2 max|1/d|), so both passes see the reference's
+// hits.  Outputs delta and um = t_mid - t*.
+template <bool kExact>
 __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, float q[3], float &delta, float &um,
                                            double &ts) {
   ts = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
@@ -855,11 +861,7 @@ __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, flo
     }
     const float u0f = fmaxf(un, (float)(r.tn0 - ts));
     if (!(uf > u0f)) return false;
-    // the fp32 slab values carry ~1.2e-7 hf |1/d_k| each: re-derive the chord
-    // in fp64 unless its relative error is below ~1e-6 (r.refine =
-    // max(0.24 max_k |1/d_k|, 2 kRefineChord) >= the forward's threshold, so
-    // both passes see the same hits)
-    if (uf - u0f < e.hf * r.refine) {  // fp64 chord (as the forward)
+    if (kExact || (SALF_BWD_REFINE && uf - u0f < e.hf * r.refine)) {
       double u0, u1;
       if (!chord64(r, e, ts, u0, u1)) return false;
       delta = (float)(u1 - u0);
@@ -941,11 +943,16 @@ __device__ __forceinline__ void bwd_pixel_init(const PinholeDev &c, const salf_r
   if (!(dCd[0] != 0.0 || dCd[1] != 0.0 || dCd[2] != 0.0 || dd != 0.0)) q.n_stop = 0;  // zero seeds: no work
 }
 
-// One included hit of pixel q against staged entry e, visited back to front:
-// adds its 27 gradient components to g.  Returns false on a miss.
-template <bool kRot, bool sdf, bool kDepth = true>
-__device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF &e, BwdPix &q,
-                                            float g[32]) {
+// The pair part of one hit (pixel q vs staged entry e): slab test, fp64
+// chord for short chords, local coordinates.  Both pixels' pair parts run
+// before the 27 gradient accumulators are live (register pressure).
+struct PairHit {
+  float x[3], delta, dq;
+  float gam[4];  // SH basis of the (possibly rotated) ray direction
+};
+
+template <bool kRot, bool kDepth = true, bool kExact = false>
+__device__ __forceinline__ bool bwd_pair(const salf_scene_t &sc, const EntryF &e, const BwdPix &q, PairHit &h) {
   float qv[3];
   double ts;
   const RayF *ray = &q.r;
@@ -958,14 +965,27 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
     rayf_from_dir(d2, q.r.tn0, rr);
     ray = &rr;
   }
-  float delta, um;
-  if (!pair_hit_bwd(*ray, e, qv, delta, um, ts)) return false;
-  const float dq = kDepth ? (float)(ts - q.D) + um : 0.f;  // t_mid - D (no depth seeds: unused)
+  float um;
+  if (!pair_hit_bwd<kExact>(*ray, e, qv, h.delta, um, ts)) return false;
+  h.dq = kDepth ? (float)(ts - q.D) + um : 0.f;  // t_mid - D (no depth seeds: unused)
   // (fp32 below: explicit FMAs -- this file is compiled with --fmad=false)
-  float x[3];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
-  const float *gam = ray->gam;
+  for (int k = 0; k < 3; ++k) h.x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
+  if (kRot) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h.gam[k] = ray->gam[k];
+  }
+  return true;
+}
+
+// One included hit of pixel q against staged entry e, visited back to front
+// (its pair part h from bwd_pair): adds its 27 gradient components to g.
+template <bool kRot, bool sdf, bool kDepth = true>
+__device__ __forceinline__ void bwd_segment(const EntryF &e, BwdPix &q, const PairHit &h, float g[32]) {
+  const float delta = h.delta, dq = h.dq;
+  const float *x = h.x;
+  const float *gam = kRot ? h.gam : q.r.gam;
+
   // fp32 fields (scene.py:229-284)
   const VoxPrm &p = e.p;
   const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
@@ -1038,7 +1058,6 @@ __device__ __forceinline__ bool bwd_segment(const salf_scene_t &sc, const EntryF
   }
   g[25] += ga;
   g[26] += gb;
-  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1188,6 +1207,8 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           }
           continue;
         }
+        // a chord within its fp32 error of zero may be an fp64 miss: fp64 redo decides
+        if ((SALF_FLAGMASK & 1) && u1 - u0 <= 2.f * dd) flag = true;
         // inclusion of this hit: Y_before < y_stop (certified outside the band)
         const float Ys = Yh + Yc;
         const float gap = y_stop - Ys;
@@ -1417,13 +1438,20 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
         if (lane < kGradStride) red[j][warp][lane] = 0.f;
         continue;
       }
+      PairHit ph[NP];
+      bool hit[NP];
+      bool act = false;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        hit[k] = rows_hit[k] && jb + j < q[k].n_stop && bwd_pair<kRot, kDepth>(sc, e, q[k], ph[k]);
+        act |= hit[k];
+      }
       float g[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) g[k] = 0.f;
-      bool act = false;
 #pragma unroll
       for (int k = 0; k < NP; ++k)
-        if (rows_hit[k] && jb + j < q[k].n_stop) act |= bwd_segment<kRot, sdf, kDepth>(sc, e, q[k], g);
+        if (hit[k]) bwd_segment<kRot, sdf, kDepth>(e, q[k], ph[k], g);
       float tot = 0.0f;
 #if SALF_BWD_SMEMRED
       // transpose through shared memory: 7 x STS.128 per lane, lane k sums column k
