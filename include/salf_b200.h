@@ -128,14 +128,28 @@ size_t salf_raster_bin_workspace_bytes(int64_t n_voxels, int64_t capacity, int32
  * lists.  mode 0 = reference lists (straddlers in every tile; bit-exact
  * export), mode 1 = render lists (tightened spans; per-tile subsequence of
  * mode 0 that drops only voxels no pixel of the tile can hit).
- * Writes offsets[n_tiles + 1] (int64) and entries[capacity] (int32) and the
- * instance count to *n_instances (host).  Returns SALF_EWORKSPACE with
- * *n_instances = required capacity when capacity is too small. */
+ * Writes offsets[n_tiles + 1] (int64), entries[capacity] (int32) and
+ * counts[2] (int64, DEVICE memory): counts[0] = visible voxels, counts[1] =
+ * instances.  Stream-ordered, no host synchronisation (hand-written radix sort,
+ * see salf_sort.cuh).  When counts[1] > capacity the frame's lists are
+ * incomplete: the caller checks counts[1] after the stream reaches it and
+ * re-bins with capacity >= counts[1]. */
 int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double near,
                     int32_t tile, int32_t mode, const uint64_t *zkey, const int32_t *span,
                     const uint8_t *visible_hint, void *workspace, size_t workspace_bytes,
                     int64_t capacity, int64_t *offsets, int32_t *entries,
-                    int64_t *n_instances, void *stream);
+                    int64_t *counts, void *stream);
+
+/* The binning's stable LSD radix sort (replaces np.lexsort at
+ * render_raster.py:177), exported for tests and callers that sort their own
+ * keys: (keys_in, vals_in)[0, n) -> (keys_out, vals_out) by key bits
+ * [begin_bit, end_bit), higher key bits zero, ties in input order.  key_bytes
+ * 4 or 8; n = min(*n_dev, n_max) read on the device (n_dev NULL: n_max);
+ * n_max < 2^30.  Inputs are not modified.  Device pointers, stream-ordered. */
+size_t salf_sort_pairs_workspace_bytes(int64_t n_max, int32_t key_bytes, int32_t begin_bit, int32_t end_bit);
+int salf_sort_pairs(const void *keys_in, const int32_t *vals_in, void *keys_out, int32_t *vals_out,
+                    int32_t key_bytes, const int64_t *n_dev, int64_t n_max, int32_t begin_bit, int32_t end_bit,
+                    void *workspace, size_t workspace_bytes, void *stream);
 
 /* rasterize (render_raster.py:201-301) over prebuilt render bins.
  * out_rgb (H*W*3), out_opacity, out_depth f32; saved (H*W*8 f64, nullable):
@@ -171,8 +185,8 @@ int salf_raster_tile_order(const int64_t *offsets, int32_t n_tiles, int32_t *ord
  * entry) instance into the workspace, instances stable-sorted by voxel, each
  * voxel's rows summed sequentially in fp64 and added to grad -- bitwise
  * identical across runs.  n_instances = length of `entries`; workspace of
- * salf_raster_backward_det_workspace_bytes(n_instances) bytes. */
-size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances);
+ * salf_raster_backward_det_workspace_bytes(n_instances, M) bytes. */
+size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances, int64_t n_voxels);
 int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_camera_t *cam,
                                        const salf_raster_opts_t *opts, const int64_t *offsets,
                                        const int32_t *entries, int64_t n_instances, const double *saved,
@@ -184,8 +198,8 @@ int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_cam
  * 27-row goes to slot row_start[ray] + k (row_start: (n + 1) exclusive scan
  * of the forward's per-ray segment counts, saved[:, 6]), then the ordered
  * per-voxel reduction of salf_raster_backward_deterministic.  Bitwise
- * identical across runs.  Workspace: salf_ray_backward_det_workspace_bytes(n_slots). */
-size_t salf_ray_backward_det_workspace_bytes(int64_t n_slots);
+ * identical across runs.  Workspace: salf_ray_backward_det_workspace_bytes(n_slots, M). */
+size_t salf_ray_backward_det_workspace_bytes(int64_t n_slots, int64_t n_voxels);
 int salf_ray_backward_deterministic(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,
                                     const double *origins, const double *dirs, const uint8_t *valid,
                                     const salf_raster_opts_t *opts, const double *saved, const double *d_rgb,

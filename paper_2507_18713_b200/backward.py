@@ -40,7 +40,7 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
         start = torch.zeros(n + 1, dtype=torch.int64, device=dev)
         start[1:] = torch.cumsum(records.saved[:, 6].to(torch.int64), 0)
         slots = int(start[-1].item())
-        wsb = lib.salf_ray_backward_det_workspace_bytes(slots)
+        wsb = lib.salf_ray_backward_det_workspace_bytes(slots, max(ds.n, 1))
         ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         _lib.check(lib.salf_ray_backward_deterministic(
             _lib.ref(t), _lib.ref(sc), n, records.origins.data_ptr(), records.dirs.data_ptr(),

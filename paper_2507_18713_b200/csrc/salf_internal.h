@@ -38,7 +38,7 @@ inline const char *camera_kind_repr(int kind) {
 
 // Ordered (deterministic) reduction of per-row 27-vectors into the (M, 27)
 // f64 gradient buffer (salf_raster.cu); row_vid == n_vox marks an unused row.
-size_t det_reduce_workspace_bytes(int64_t n_rows);
+size_t det_reduce_workspace_bytes(int64_t n_rows, int64_t n_vox);
 int det_reduce_rows(int64_t n_rows, const uint32_t *row_vid, const float *rows, int64_t n_vox, double *grad,
                     void *workspace, size_t workspace_bytes, cudaStream_t st);
 

@@ -15,11 +15,9 @@
 //                  early exit when every pixel of the tile is frozen  (:201-301)
 //   k_backward     replay of k_composite producing per-voxel gradients with
 //                  warp-aggregated atomics (definition: DESIGN.md §raster backward)
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-
 #include "salf_common.cuh"
 #include "salf_internal.h"
+#include "salf_sort.cuh"
 
 namespace salf {
 
@@ -172,67 +170,158 @@ __global__ void k_project(int64_t n, const double4 *__restrict__ geo, const doub
 // ---------------------------------------------------------------------------
 // binning
 
-__global__ void k_span_count(int64_t n, const int4 *__restrict__ span, int64_t *__restrict__ cnt,
-                             uint8_t *__restrict__ vis) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  int4 s = span[i];
-  const int64_t c = (s.x <= s.z && s.y <= s.w) ? (int64_t)(s.z - s.x + 1) * (s.w - s.y + 1) : 0;
-  cnt[i] = c;
-  vis[i] = c > 0;
+// Visible voxels (non-empty span) in ascending index order, their depth keys
+// and instance counts, in one pass: CTA tile of 2048 voxels (warp w owns 256
+// consecutive voxels, ballots give the in-warp order), decoupled look-back for
+// the tile's output position.  nums[0] = visible voxels (written by the last
+// tile), nums[1] = instances (atomic).
+__global__ void __launch_bounds__(sortk::kBlock) k_select_vis(int64_t n, const int4 *__restrict__ span,
+                                                              const uint64_t *__restrict__ zkey,
+                                                              int64_t *__restrict__ cnt, int32_t *__restrict__ vis_idx,
+                                                              uint64_t *__restrict__ zk_vis,
+                                                              uint64_t *__restrict__ status,
+                                                              uint32_t *__restrict__ ticket, int64_t *__restrict__ nums) {
+  using namespace sortk;
+  __shared__ uint32_t s_tile;
+  __shared__ int64_t s_w[kWarps + 1];
+  __shared__ int64_t s_c[kWarps];
+  __shared__ int64_t s_base;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t wbase = (int64_t)tile * kScanTile + (int64_t)w * (32 * kScanItems);
+  uint32_t ball[kScanItems];
+  int wcount = 0;
+  int64_t csum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int64_t idx = wbase + 32 * k + lane;
+    int64_t c = 0;
+    if (idx < n) {
+      const int4 s = span[idx];
+      c = (s.x <= s.z && s.y <= s.w) ? (int64_t)(s.z - s.x + 1) * (s.w - s.y + 1) : 0;
+      cnt[idx] = c;
+    }
+    ball[k] = __ballot_sync(0xffffffffu, c > 0);
+    wcount += __popc(ball[k]);
+    csum += c;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, o);
+  if (lane == 0) {
+    s_w[w] = wcount;
+    s_c[w] = csum;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int64_t run = 0, inst = 0;
+    for (int i = 0; i < kWarps; ++i) {
+      const int64_t c = s_w[i];
+      s_w[i] = run;
+      run += c;
+      inst += s_c[i];
+    }
+    if (inst) atomicAdd(reinterpret_cast<unsigned long long *>(nums + 1), (unsigned long long)inst);
+    const int64_t pre = (int64_t)lookback64(status, tile, (uint64_t)run);
+    s_base = pre;
+    if ((int64_t)(tile + 1) * kScanTile >= n) nums[0] = pre + run;
+  }
+  __syncthreads();
+  int64_t pos = s_base + s_w[w];
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (ball[k] >> lane & 1u) {
+      const int64_t idx = wbase + 32 * k + lane;
+      const int64_t q = pos + __popc(ball[k] & lt);
+      vis_idx[q] = (int32_t)idx;
+      zk_vis[q] = zkey[idx];
+    }
+    pos += __popc(ball[k]);
+  }
 }
 
-// depth keys and instance counts of the visible voxels (vis_idx ascending)
-__global__ void k_gather_vis(int64_t n_vis, const int32_t *__restrict__ vis_idx, const uint64_t *__restrict__ zkey,
-                             uint64_t *__restrict__ zk_vis) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n_vis) zk_vis[r] = zkey[vis_idx[r]];
+// base_r[r] = exclusive prefix of the instance counts in depth-rank order
+// (r < nums[0]); thread t owns 8 consecutive ranks, look-back across CTAs.
+__global__ void __launch_bounds__(sortk::kBlock) k_scan_ranked(const int64_t *__restrict__ nums,
+                                                               const int32_t *__restrict__ sorted_vis,
+                                                               const int64_t *__restrict__ cnt,
+                                                               int64_t *__restrict__ base_r,
+                                                               uint64_t *__restrict__ status,
+                                                               uint32_t *__restrict__ ticket) {
+  using namespace sortk;
+  __shared__ uint32_t s_tile;
+  __shared__ int64_t s_w[kWarps + 1];
+  __shared__ int64_t s_pre;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t n = nums[0];
+  const int64_t r0 = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  if ((int64_t)tile * kScanTile >= n) return;  // uniform
+  int64_t c[kScanItems], sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    c[k] = (r0 + k < n) ? cnt[sorted_vis[r0 + k]] : 0;
+    sum += c[k];
+  }
+  int64_t total;
+  int64_t ex = block_excl_scan(sum, s_w, total);
+  if (threadIdx.x == 0) s_pre = (int64_t)lookback64(status, tile, (uint64_t)total);
+  __syncthreads();
+  ex += s_pre;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (r0 + k < n) base_r[r0 + k] = ex;
+    ex += c[k];
+  }
 }
 
-__global__ void k_count_ranked(int64_t n_vis, const int32_t *__restrict__ sorted_vis, const int64_t *__restrict__ cnt,
-                               int64_t *__restrict__ cnt_r) {
-  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n_vis) cnt_r[r] = cnt[sorted_vis[r]];
-}
-
-// One warp per visible voxel, in global depth-rank order: its instances are
-// written at base_r[rank] with the tile id as the (only) sort key, so a
-// stable sort by tile leaves every tile's list in (z, index) order.  Lanes
-// stride over the voxel's tiles (spans can be the full image for straddling
-// voxels in reference mode).
+// One group of kEmitLanes lanes per visible voxel, in global depth-rank order:
+// its instances are written at base_r[rank] with the tile id as the (only)
+// sort key, so a stable sort by tile leaves every tile's list in (z, index)
+// order.  Lanes stride over the voxel's tiles (spans can be the full image for
+// straddling voxels in reference mode).  Instances past `cap` are not written
+// (the caller sees nums[1] > cap and re-bins with a larger capacity).
 constexpr int kEmitLanes = 8;
 
-__global__ void k_emit(int64_t n_vis, const int32_t *__restrict__ sorted_vis, const int4 *__restrict__ span,
-                       const int64_t *__restrict__ base_r, int tiles_x, uint32_t *__restrict__ keys,
-                       int32_t *__restrict__ vals) {
-  // kEmitLanes lanes per visible voxel (~11 instances each at C2); a span
-  // covers at most the tile grid, so the 32-bit row/column split is exact
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kEmitLanes;
+__global__ void k_emit(const int64_t *__restrict__ nums, const int32_t *__restrict__ sorted_vis,
+                       const int4 *__restrict__ span, const int64_t *__restrict__ base_r, int tiles_x, int64_t cap,
+                       uint32_t *__restrict__ keys, int32_t *__restrict__ vals) {
+  // ~11 instances per visible voxel at C2; a span covers at most the tile
+  // grid, so the 32-bit row/column split is exact.  Grid-stride over the ranks
+  // (the visible count is only known on the device).
   const int lane = threadIdx.x % kEmitLanes;
-  if (r >= n_vis) return;
-  const int32_t v = sorted_vis[r];
-  const int4 s = span[v];
-  const int nx = s.z - s.x + 1;
-  const int cnt = nx * (s.w - s.y + 1);
-  const int64_t b = base_r[r];
-  int ty = s.y + lane / nx, tx = s.x + lane % nx;
-  const int dy = kEmitLanes / nx, dx = kEmitLanes % nx;
-  for (int k = lane; k < cnt; k += kEmitLanes) {
-    keys[b + k] = (uint32_t)(ty * tiles_x + tx);
-    vals[b + k] = v;
-    tx += dx;  // advance by kEmitLanes instances in row-major order
-    ty += dy;
-    if (tx > s.z) {
-      tx -= nx;
-      ++ty;
+  const int64_t n_vis = nums[0];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / kEmitLanes;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kEmitLanes; r < n_vis; r += stride) {
+    const int32_t v = sorted_vis[r];
+    const int4 s = span[v];
+    const int nx = s.z - s.x + 1;
+    const int cnt = nx * (s.w - s.y + 1);
+    const int64_t b = base_r[r];
+    if (b + cnt > cap) continue;
+    int ty = s.y + lane / nx, tx = s.x + lane % nx;
+    const int dy = kEmitLanes / nx, dx = kEmitLanes % nx;
+    for (int k = lane; k < cnt; k += kEmitLanes) {
+      keys[b + k] = (uint32_t)(ty * tiles_x + tx);
+      vals[b + k] = v;
+      tx += dx;  // advance by kEmitLanes instances in row-major order
+      ty += dy;
+      if (tx > s.z) {
+        tx -= nx;
+        ++ty;
+      }
     }
   }
 }
 
-__global__ void k_offsets(int n_tiles, int64_t n_inst, const uint32_t *__restrict__ keys,
-                          int64_t *__restrict__ offsets) {
+__global__ void k_offsets(int n_tiles, const int64_t *__restrict__ nums, int64_t cap,
+                          const uint32_t *__restrict__ keys, int64_t *__restrict__ offsets) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t > n_tiles) return;
+  const int64_t n_inst = min(nums[1], cap);
   // lower_bound of tile t in the sorted keys
   int64_t lo = 0, hi = n_inst;
   while (lo < hi) {
@@ -671,6 +760,13 @@ struct RayF {
 #ifndef SALF_REFINE_K
 #define SALF_REFINE_K 0.05f
 #endif
+#ifdef SALF_DIAG_CHORD
+__device__ unsigned long long g_diag[4];
+#endif
+#ifndef SALF_REFTOL
+#define SALF_REFTOL 5e-5f
+#endif
+constexpr float kRefTol = SALF_REFTOL;  // fp64 chord when the fp32 chord's bound exceeds this relative error
 #ifndef SALF_CHORD_INLINE
 #define SALF_CHORD_INLINE __forceinline__
 #endif
@@ -781,6 +877,47 @@ __device__ SALF_CHORD_INLINE bool chord64(const RayF &r, const EntryF &e, double
   return u1 > u0 + 1e-12;
 }
 
+// Error bound of an fp32 chord [u0, u1] from pair_hit_f / pair_hit_bwd,
+// evaluated only for chords the cheap whole-ray bound (max_k |1/d_k|) cannot
+// certify.  Each slab value -/+ h|1/d_k| - q_k/d_k carries at most
+// e_k = (12 u h + 2e-12) |1/d_k| (u = 2^-24; q's two-float / fp64->fp32 error
+// included), the near-plane value tn0 - t* at most 2u(|tn0| + |t*|).  The
+// computed max (min) can differ from the exact one only through faces whose
+// values lie within their errors of it, so |du0| <= E0 = max e_k over the
+// near faces k with n_k + e_k >= u0 - e(argmax), and likewise E1 for u1.
+// (A ray nearly parallel to one axis has a huge |1/d_k| there, but that face
+// is far from deciding the chord, so E0 + E1 stays ~1e-6 h |1/d_active|.)
+__device__ __forceinline__ float chord_err(const float inv[3], float hf, const float q[3], float u_near, float u0,
+                                        float u1, float t_abs) {
+  constexpr float u = 5.9604645e-8f;
+  const float ek = __fmaf_rn(12.f * u, hf, 2e-12f);
+  const float en = 2.f * u * t_abs;  // error of the near-plane value u_near = tn0 - t*
+  float nk[3], fk[3], er[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float qi = q[k] * inv[k], a = fabsf(inv[k]);
+    nk[k] = __fmaf_rn(-hf, a, -qi);
+    fk[k] = __fmaf_rn(hf, a, -qi);
+    er[k] = ek * a;
+  }
+  // errors of the values that produced u0 and u1
+  float e0 = u_near == u0 ? en : 0.f, e1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (nk[k] == u0) e0 = fmaxf(e0, er[k]);
+    if (fk[k] == u1) e1 = fmaxf(e1, er[k]);
+  }
+  // every value within reach of the computed max / min
+  float E0 = e0, E1 = e1;
+  if (u_near + en >= u0 - e0) E0 = fmaxf(E0, en);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (nk[k] + er[k] >= u0 - e0) E0 = fmaxf(E0, er[k]);
+    if (fk[k] - er[k] <= u1 + e1) E1 = fmaxf(E1, er[k]);
+  }
+  return E0 + E1;
+}
+
 // Pair test in closest-approach coordinates.  With t* ~ -(o . d) (any
 // value near the closest approach to the voxel centre) the ray is q + u d
 // with q = o + t* d (|q| ~ the voxel size for any pair that can hit) and
@@ -861,7 +998,16 @@ __device__ __forceinline__ bool pair_hit_bwd(const RayF &r, const EntryF &e, flo
     }
     const float u0f = fmaxf(un, (float)(r.tn0 - ts));
     if (!(uf > u0f)) return false;
-    if (kExact || (SALF_BWD_REFINE && uf - u0f < e.hf * r.refine)) {
+#ifdef SALF_DIAG_CHORD
+    atomicAdd(&g_diag[0], 1ull);
+    if (uf - u0f < e.hf * r.refine) {
+      atomicAdd(&g_diag[1], 1ull);
+      if (chord_err(r.inv, e.hf, q, (float)(r.tn0 - ts), u0f, uf, (float)(fabs(ts) + r.tn0)) > kRefTol * (uf - u0f))
+        atomicAdd(&g_diag[2], 1ull);
+    }
+#endif
+    if (kExact || (SALF_BWD_REFINE && uf - u0f < e.hf * r.refine &&
+                   chord_err(r.inv, e.hf, q, (float)(r.tn0 - ts), u0f, uf, (float)(fabs(ts) + r.tn0)) > kRefTol * (uf - u0f))) {
       double u0, u1;
       if (!chord64(r, e, ts, u0, u1)) return false;
       delta = (float)(u1 - u0);
@@ -1208,7 +1354,9 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           continue;
         }
         // a chord within its fp32 error of zero may be an fp64 miss: fp64 redo decides
-        if ((SALF_FLAGMASK & 1) && u1 - u0 <= 2.f * dd) flag = true;
+        if ((SALF_FLAGMASK & 1) && u1 - u0 <= 2.f * dd &&
+            u1 - u0 <= chord_err(ray->inv, e.hf, qv, ray->tn0f - ts, u0, u1, fabsf(ts) + ray->tn0f))
+          flag = true;
         // inclusion of this hit: Y_before < y_stop (certified outside the band)
         const float Ys = Yh + Yc;
         const float gap = y_stop - Ys;
@@ -1518,42 +1666,34 @@ extern "C" int salf_project_voxels(const salf_scene_t *scene, const salf_camera_
 
 // workspace layout for salf_raster_bin
 struct BinWs {
-  int64_t *cnt, *cnt_r, *base_r, *nums;  // nums[0] = visible voxels, nums[1] = instances
-  uint8_t *vis;
+  int64_t *cnt, *base_r;
+  uint64_t *st_sel, *st_scan;  // look-back status of k_select_vis / k_scan_ranked
+  uint32_t *tickets;           // [0] select, [1] scan
+  size_t clear_bytes;          // st_sel .. tickets are contiguous (one memset)
   int32_t *vis_idx, *vis_sorted;
   uint64_t *zk_vis, *zk_sorted;
   uint32_t *keys_a, *keys_b;
   int32_t *vals_a;
-  void *cub_tmp;
-  size_t cub_bytes;
+  void *sort_tmp;
+  size_t sort_bytes;
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static size_t cub_bytes_needed(int64_t n_voxels, int64_t capacity) {
-  const int n = (int)std::max<int64_t>(n_voxels, 1);
-  size_t a = 0, b = 0, c = 0, d = 0, e = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, a, (int64_t *)nullptr, (int64_t *)nullptr, n);
-  cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t *)nullptr, (uint64_t *)nullptr, (int32_t *)nullptr,
-                                  (int32_t *)nullptr, n);
-  cub::DeviceRadixSort::SortPairs(nullptr, c, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
-                                  (int32_t *)nullptr, (int64_t)std::max<int64_t>(capacity, 1));
-  cub::DeviceSelect::Flagged(nullptr, d, thrust::counting_iterator<int32_t>(0), (const uint8_t *)nullptr,
-                             (int32_t *)nullptr, (int64_t *)nullptr, n);
-  cub::DeviceReduce::Sum(nullptr, e, (const int64_t *)nullptr, (int64_t *)nullptr, n);
-  return std::max(std::max(a, b), std::max(c, std::max(d, e)));
-}
-
-static BinWs carve(void *ws, int64_t n, int64_t cap, size_t *total) {
+static BinWs carve(void *ws, int64_t n, int64_t cap, int n_tiles, size_t *total) {
   BinWs w;
   size_t off = 0;
   char *p = (char *)ws;
   auto take = [&](size_t bytes) { char *q = p ? p + off : nullptr; off += align_up(bytes); return q; };
-  w.cnt = (int64_t *)take(sizeof(int64_t) * (n + 1));
-  w.cnt_r = (int64_t *)take(sizeof(int64_t) * (n + 1));
-  w.base_r = (int64_t *)take(sizeof(int64_t) * (n + 1));
-  w.nums = (int64_t *)take(sizeof(int64_t) * 2);
-  w.vis = (uint8_t *)take(n);
+  const int64_t scan_tiles = (n + sortk::kScanTile - 1) / sortk::kScanTile;
+  const size_t st_b = sizeof(uint64_t) * scan_tiles;
+  char *c = take(2 * st_b + 2 * sizeof(uint32_t));
+  w.st_sel = (uint64_t *)c;
+  w.st_scan = c ? (uint64_t *)(c + st_b) : nullptr;
+  w.tickets = c ? (uint32_t *)(c + 2 * st_b) : nullptr;
+  w.clear_bytes = 2 * st_b + 2 * sizeof(uint32_t);
+  w.cnt = (int64_t *)take(sizeof(int64_t) * n);
+  w.base_r = (int64_t *)take(sizeof(int64_t) * n);
   w.vis_idx = (int32_t *)take(sizeof(int32_t) * n);
   w.vis_sorted = (int32_t *)take(sizeof(int32_t) * n);
   w.zk_vis = (uint64_t *)take(sizeof(uint64_t) * n);
@@ -1561,23 +1701,23 @@ static BinWs carve(void *ws, int64_t n, int64_t cap, size_t *total) {
   w.keys_a = (uint32_t *)take(sizeof(uint32_t) * cap);
   w.keys_b = (uint32_t *)take(sizeof(uint32_t) * cap);
   w.vals_a = (int32_t *)take(sizeof(int32_t) * cap);
-  w.cub_bytes = cub_bytes_needed(n, cap);
-  w.cub_tmp = take(w.cub_bytes);
+  w.sort_bytes = std::max(radix_sort_workspace_bytes(n, 8, 0, 64),
+                          radix_sort_workspace_bytes(cap, 4, 0, bits_for((uint64_t)std::max(n_tiles, 1))));
+  w.sort_tmp = take(w.sort_bytes);
   *total = off;
   return w;
 }
 
 extern "C" size_t salf_raster_bin_workspace_bytes(int64_t n_voxels, int64_t capacity, int32_t n_tiles) {
-  (void)n_tiles;
   size_t total = 0;
-  carve(nullptr, std::max<int64_t>(n_voxels, 1), std::max<int64_t>(capacity, 1), &total);
+  carve(nullptr, std::max<int64_t>(n_voxels, 1), std::max<int64_t>(capacity, 1), n_tiles, &total);
   return total;
 }
 
 extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *cam, double near, int32_t tile,
                                int32_t mode, const uint64_t *zkey, const int32_t *span, const uint8_t *visible_hint,
                                void *workspace, size_t workspace_bytes, int64_t capacity, int64_t *offsets,
-                               int32_t *entries, int64_t *n_instances, void *stream) {
+                               int32_t *entries, int64_t *counts, void *stream) {
   SALF_TRY {
     (void)visible_hint;
     (void)mode;
@@ -1585,53 +1725,37 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
     PinholeDev c = make_pinhole(cam, near, tile);
     const int n_tiles = c.tiles_x * c.tiles_y;
     const int64_t n = scene->n;
+    cudaMemsetAsync(counts, 0, 2 * sizeof(int64_t), st);
     if (n == 0) {
       cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (n_tiles + 1), st);
-      *n_instances = 0;
       return check_cuda("salf_raster_bin");
     }
+    capacity = std::max<int64_t>(capacity, 1);
     size_t need = 0;
-    BinWs w = carve(workspace, std::max<int64_t>(n, 1), std::max<int64_t>(capacity, 1), &need);
+    BinWs w = carve(workspace, n, capacity, n_tiles, &need);
     if (need > workspace_bytes) return set_error(SALF_EWORKSPACE, "raster bin workspace too small: %zu < %zu",
                                                  workspace_bytes, need);
-    const int bs = 256;
-    const unsigned gb = (unsigned)((n + bs - 1) / bs);
-    // instance counts, visible voxels (non-empty span, ascending index) and the total
-    k_span_count<<<gb, bs, 0, st>>>(n, reinterpret_cast<const int4 *>(span), w.cnt, w.vis);
-    size_t tb = w.cub_bytes;
-    cub::DeviceSelect::Flagged(w.cub_tmp, tb, thrust::counting_iterator<int32_t>(0), w.vis, w.vis_idx, w.nums,
-                               (int)n, st);
-    tb = w.cub_bytes;
-    cub::DeviceReduce::Sum(w.cub_tmp, tb, w.cnt, w.nums + 1, (int)n, st);
-    int64_t hn[2];
-    cudaMemcpyAsync(hn, w.nums, sizeof(hn), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    const int64_t n_vis = hn[0], total = hn[1];
-    *n_instances = total;
-    if (total > capacity) return set_error(SALF_EWORKSPACE, "instance capacity %lld < %lld", (long long)capacity,
-                                           (long long)total);
-    if (total == 0) {
-      cudaMemsetAsync(offsets, 0, sizeof(int64_t) * (n_tiles + 1), st);
-      return check_cuda("salf_raster_bin");
-    }
-    // global depth rank of the visible voxels: stable sort of (zkey, index)
-    const unsigned gv = (unsigned)((n_vis + bs - 1) / bs);
-    k_gather_vis<<<gv, bs, 0, st>>>(n_vis, w.vis_idx, zkey, w.zk_vis);
-    tb = w.cub_bytes;
-    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.zk_vis, w.zk_sorted, w.vis_idx, w.vis_sorted, (int)n_vis, 0, 64,
-                                    st);
+    cudaMemsetAsync(w.st_sel, 0, w.clear_bytes, st);
+    // visible voxels (non-empty span, ascending index), their depth keys, instance counts and totals
+    const unsigned gs = (unsigned)((n + sortk::kScanTile - 1) / sortk::kScanTile);
+    k_select_vis<<<gs, sortk::kBlock, 0, st>>>(n, reinterpret_cast<const int4 *>(span), zkey, w.cnt, w.vis_idx,
+                                               w.zk_vis, w.st_sel, w.tickets, counts);
+    // global depth rank of the visible voxels: stable sort of (zkey, index) -> lexsort's (z, vox) order
+    int rc = radix_sort_pairs_u64(w.zk_vis, w.vis_idx, w.zk_sorted, w.vis_sorted, counts, n, 0, 64, w.sort_tmp,
+                                  w.sort_bytes, st);
+    if (rc != SALF_OK) return rc;
     // instance slots in rank order
-    k_count_ranked<<<gv, bs, 0, st>>>(n_vis, w.vis_sorted, w.cnt, w.cnt_r);
-    tb = w.cub_bytes;
-    cub::DeviceScan::ExclusiveSum(w.cub_tmp, tb, w.cnt_r, w.base_r, (int)n_vis, st);
-    k_emit<<<(unsigned)((n_vis * kEmitLanes + bs - 1) / bs), bs, 0, st>>>(n_vis, w.vis_sorted,
-                                                                 reinterpret_cast<const int4 *>(span), w.base_r,
-                                                                 c.tiles_x, w.keys_a, w.vals_a);
+    k_scan_ranked<<<gs, sortk::kBlock, 0, st>>>(counts, w.vis_sorted, w.cnt, w.base_r, w.st_scan, w.tickets + 1);
+    const int bs = 256;
+    const unsigned ge = (unsigned)std::min<int64_t>((n * kEmitLanes + bs - 1) / bs, 148 * 16);
+    k_emit<<<ge, bs, 0, st>>>(counts, w.vis_sorted,
+                                                                     reinterpret_cast<const int4 *>(span), w.base_r,
+                                                                     c.tiles_x, capacity, w.keys_a, w.vals_a);
     // stable sort by tile: each tile's list stays in depth-rank order
-    tb = w.cub_bytes;
-    cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, w.keys_a, w.keys_b, w.vals_a, entries, (int64_t)total, 0,
-                                    bits_for((uint64_t)n_tiles), st);
-    k_offsets<<<(n_tiles + 1 + bs - 1) / bs, bs, 0, st>>>(n_tiles, total, w.keys_b, offsets);
+    rc = radix_sort_pairs_u32(w.keys_a, w.vals_a, w.keys_b, entries, counts + 1, capacity, 0,
+                              bits_for((uint64_t)n_tiles), w.sort_tmp, w.sort_bytes, st);
+    if (rc != SALF_OK) return rc;
+    k_offsets<<<(n_tiles + 1 + bs - 1) / bs, bs, 0, st>>>(n_tiles, counts, capacity, w.keys_b, offsets);
     return check_cuda("salf_raster_bin");
   }
   SALF_CATCH
@@ -1745,39 +1869,36 @@ __global__ void k_iota32(int64_t n, int32_t *__restrict__ v) {
   if (i < n) v[i] = (int32_t)i;
 }
 
-__global__ void k_run_heads(int64_t n, const uint32_t *__restrict__ key, uint8_t *__restrict__ head) {
+// first row of each voxel's run in the vid-sorted rows
+__global__ void k_run_first(int64_t n, const uint32_t *__restrict__ key, int32_t *__restrict__ first) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) head[p] = (p == 0 || key[p] != key[p - 1]) ? 1 : 0;
+  if (p < n && (p == 0 || key[p] != key[p - 1])) first[key[p]] = (int32_t)p;
 }
 
-// one warp per run of equal voxel ids; lane k sums component k over the
-// run's rows in order (fp64) and adds it to grad (single writer per voxel);
-// runs with vid >= n_vox (unused row slots) are skipped
-__global__ void k_det_reduce(int64_t n, const int64_t *__restrict__ n_runs, const int32_t *__restrict__ heads,
-                             const uint32_t *__restrict__ vid, const int32_t *__restrict__ row,
-                             const float *__restrict__ rows, int64_t n_vox, double *__restrict__ grad) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// one warp per voxel; lane k sums component k over the voxel's rows in order
+// (fp64) and adds it to grad (single writer per voxel)
+__global__ void k_det_reduce(int64_t n, const int32_t *__restrict__ first, const uint32_t *__restrict__ vid,
+                             const int32_t *__restrict__ row, const float *__restrict__ rows, int64_t n_vox,
+                             double *__restrict__ grad) {
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t nr = *n_runs;
-  if (r >= nr || lane >= kGradStride) return;
-  const int64_t p0 = heads[r], p1 = (r + 1 < nr) ? heads[r + 1] : n;
-  if ((int64_t)vid[p0] >= n_vox) return;
+  if (v >= n_vox || lane >= kGradStride) return;
+  const int64_t p0 = first[v];
+  if (p0 < 0) return;
   double s = 0.0;
-  for (int64_t p = p0; p < p1; ++p) s += (double)rows[(int64_t)row[p] * kGradStride + lane];
-  double *g = grad + (int64_t)vid[p0] * kGradStride + lane;
+  for (int64_t p = p0; p < n && (int64_t)vid[p] == v; ++p) s += (double)rows[(int64_t)row[p] * kGradStride + lane];
+  double *g = grad + v * kGradStride + lane;
   *g = *g + s;
 }
 
 struct DetWs {
   uint32_t *vid_sorted;
-  int32_t *row, *row_sorted, *heads;
-  uint8_t *head_flag;
-  int64_t *n_runs;
-  void *cub_tmp;
-  size_t cub_bytes;
+  int32_t *row, *row_sorted, *first;
+  void *sort_tmp;
+  size_t sort_bytes;
 };
 
-static DetWs carve_det(void *ws, int64_t ni, size_t *total) {
+static DetWs carve_det(void *ws, int64_t ni, int64_t n_vox, size_t *total) {
   DetWs w;
   size_t off = 0;
   char *p = (char *)ws;
@@ -1785,23 +1906,16 @@ static DetWs carve_det(void *ws, int64_t ni, size_t *total) {
   w.vid_sorted = (uint32_t *)take(sizeof(uint32_t) * ni);
   w.row = (int32_t *)take(sizeof(int32_t) * ni);
   w.row_sorted = (int32_t *)take(sizeof(int32_t) * ni);
-  w.heads = (int32_t *)take(sizeof(int32_t) * ni);
-  w.head_flag = (uint8_t *)take(ni);
-  w.n_runs = (int64_t *)take(sizeof(int64_t));
-  size_t a = 0, b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, a, (uint32_t *)nullptr, (uint32_t *)nullptr, (int32_t *)nullptr,
-                                  (int32_t *)nullptr, (int64_t)ni);
-  cub::DeviceSelect::Flagged(nullptr, b, thrust::counting_iterator<int32_t>(0), (const uint8_t *)nullptr,
-                             (int32_t *)nullptr, (int64_t *)nullptr, (int)ni);
-  w.cub_bytes = std::max(a, b);
-  w.cub_tmp = take(w.cub_bytes);
+  w.first = (int32_t *)take(sizeof(int32_t) * (n_vox + 1));
+  w.sort_bytes = radix_sort_workspace_bytes(ni, 4, 0, 32);
+  w.sort_tmp = take(w.sort_bytes);
   *total = off;
   return w;
 }
 
-size_t salf::det_reduce_workspace_bytes(int64_t n_rows) {
+size_t salf::det_reduce_workspace_bytes(int64_t n_rows, int64_t n_vox) {
   size_t total = 0;
-  carve_det(nullptr, std::max<int64_t>(n_rows, 1), &total);
+  carve_det(nullptr, std::max<int64_t>(n_rows, 1), std::max<int64_t>(n_vox, 1), &total);
   return total;
 }
 
@@ -1812,45 +1926,36 @@ int salf::det_reduce_rows(int64_t n_rows, const uint32_t *row_vid, const float *
                           void *workspace, size_t workspace_bytes, cudaStream_t st) {
   if (n_rows <= 0) return SALF_OK;
   size_t need = 0;
-  DetWs w = carve_det(workspace, n_rows, &need);
+  DetWs w = carve_det(workspace, n_rows, std::max<int64_t>(n_vox, 1), &need);
   if (need > workspace_bytes)
     return set_error(SALF_EWORKSPACE, "deterministic reduction workspace too small: %zu < %zu", workspace_bytes, need);
   const int bs = 256;
   const unsigned g = (unsigned)((n_rows + bs - 1) / bs);
   k_iota32<<<g, bs, 0, st>>>(n_rows, w.row);
-  size_t tb = w.cub_bytes;
-  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, row_vid, w.vid_sorted, w.row, w.row_sorted, (int64_t)n_rows, 0,
-                                  bits_for((uint64_t)std::max<int64_t>(n_vox, 1)), st);
-  k_run_heads<<<g, bs, 0, st>>>(n_rows, w.vid_sorted, w.head_flag);
-  tb = w.cub_bytes;
-  cub::DeviceSelect::Flagged(w.cub_tmp, tb, thrust::counting_iterator<int32_t>(0), w.head_flag, w.heads, w.n_runs,
-                             (int)n_rows, st);
-  const int64_t max_runs = std::min<int64_t>(n_rows, std::max<int64_t>(n_vox, 1) + 1);
-  k_det_reduce<<<(unsigned)((max_runs * 32 + bs - 1) / bs), bs, 0, st>>>(n_rows, w.n_runs, w.heads, w.vid_sorted,
-                                                                        w.row_sorted, rows, n_vox, grad);
+  const int rc = radix_sort_pairs_u32(row_vid, w.row, w.vid_sorted, w.row_sorted, nullptr, n_rows, 0,
+                                      bits_for((uint64_t)std::max<int64_t>(n_vox, 1)), w.sort_tmp, w.sort_bytes, st);
+  if (rc != SALF_OK) return rc;
+  cudaMemsetAsync(w.first, 0xff, sizeof(int32_t) * (n_vox + 1), st);
+  k_run_first<<<g, bs, 0, st>>>(n_rows, w.vid_sorted, w.first);
+  k_det_reduce<<<(unsigned)((n_vox * 32 + bs - 1) / bs), bs, 0, st>>>(n_rows, w.first, w.vid_sorted, w.row_sorted,
+                                                                     rows, n_vox, grad);
   return check_cuda("det_reduce_rows");
 }
 
 // tile launch order: 16-bit descending-length keys, stable radix sort (ties in tile order)
-__global__ void k_tile_len_keys(int32_t n, const int64_t *__restrict__ offsets, uint16_t *__restrict__ keys,
+__global__ void k_tile_len_keys(int32_t n, const int64_t *__restrict__ offsets, uint32_t *__restrict__ keys,
                                 int32_t *__restrict__ ids) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int64_t len = offsets[t + 1] - offsets[t];
-  keys[t] = (uint16_t)(0xffff - (len < 0xffff ? len : 0xffff));
+  keys[t] = 0xffffu - (uint32_t)(len < 0xffff ? len : 0xffff);
   ids[t] = t;
-}
-
-static size_t tile_order_cub_bytes(int32_t n) {
-  size_t b = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, b, (uint16_t *)nullptr, (uint16_t *)nullptr, (int32_t *)nullptr,
-                                  (int32_t *)nullptr, std::max(n, 1), 0, 16);
-  return b;
 }
 
 extern "C" size_t salf_raster_tile_order_workspace_bytes(int32_t n_tiles) {
   const size_t n = (size_t)std::max(n_tiles, 1);
-  return align_up(2 * n * sizeof(uint16_t)) + align_up(n * sizeof(int32_t)) + tile_order_cub_bytes(n_tiles);
+  return align_up(2 * n * sizeof(uint32_t)) + align_up(n * sizeof(int32_t)) +
+         radix_sort_workspace_bytes((int64_t)n, 4, 0, 16);
 }
 
 extern "C" int salf_raster_tile_order(const int64_t *offsets, int32_t n_tiles, int32_t *order, void *workspace,
@@ -1861,21 +1966,22 @@ extern "C" int salf_raster_tile_order(const int64_t *offsets, int32_t n_tiles, i
       return set_error(SALF_EWORKSPACE, "tile order workspace too small");
     cudaStream_t st = (cudaStream_t)stream;
     char *p = (char *)workspace;
-    uint16_t *ka = (uint16_t *)p, *kb = ka + n_tiles;
-    p += align_up(2 * (size_t)n_tiles * sizeof(uint16_t));
+    uint32_t *ka = (uint32_t *)p, *kb = ka + n_tiles;
+    p += align_up(2 * (size_t)n_tiles * sizeof(uint32_t));
     int32_t *ids = (int32_t *)p;
     p += align_up((size_t)n_tiles * sizeof(int32_t));
     k_tile_len_keys<<<(n_tiles + 255) / 256, 256, 0, st>>>(n_tiles, offsets, ka, ids);
-    size_t tb = tile_order_cub_bytes(n_tiles);
-    cub::DeviceRadixSort::SortPairs(p, tb, ka, kb, ids, order, n_tiles, 0, 16, st);
+    const int rc = radix_sort_pairs_u32(ka, ids, kb, order, nullptr, n_tiles, 0, 16, p,
+                                        radix_sort_workspace_bytes(n_tiles, 4, 0, 16), st);
+    if (rc != SALF_OK) return rc;
     return check_cuda("salf_raster_tile_order");
   }
   SALF_CATCH
 }
 
-extern "C" size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances) {
+extern "C" size_t salf_raster_backward_det_workspace_bytes(int64_t n_instances, int64_t n_voxels) {
   const int64_t ni = std::max<int64_t>(n_instances, 1);
-  return align_up(sizeof(float) * kGradStride * ni) + det_reduce_workspace_bytes(ni);
+  return align_up(sizeof(float) * kGradStride * ni) + det_reduce_workspace_bytes(ni, n_voxels);
 }
 
 extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_camera_t *cam,
@@ -1900,3 +2006,15 @@ extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, con
   }
   SALF_CATCH
 }
+
+#ifdef SALF_DIAG_CHORD
+// diagnostics build only: backward hits / chords under the cheap bound / chords re-derived in fp64
+extern "C" int salf_debug_counters(unsigned long long *out, int reset) {
+  cudaMemcpyFromSymbol(out, salf::g_diag, sizeof(unsigned long long) * 4);
+  if (reset) {
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(salf::g_diag, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -1238,9 +1238,10 @@ __global__ void k_fill_u32(int64_t n, uint32_t v, uint32_t *__restrict__ out) {
   if (i < n) out[i] = v;
 }
 
-extern "C" size_t salf_ray_backward_det_workspace_bytes(int64_t n_slots) {
+extern "C" size_t salf_ray_backward_det_workspace_bytes(int64_t n_slots, int64_t n_voxels) {
   const int64_t ns = std::max<int64_t>(n_slots, 1);
-  return align256(sizeof(float) * kGradStride * ns) + align256(sizeof(uint32_t) * ns) + det_reduce_workspace_bytes(ns);
+  return align256(sizeof(float) * kGradStride * ns) + align256(sizeof(uint32_t) * ns) +
+         det_reduce_workspace_bytes(ns, n_voxels);
 }
 
 extern "C" int salf_ray_backward_deterministic(const salf_octree_t *tree, const salf_scene_t *scene, int64_t n,

@@ -127,32 +127,58 @@ def _project(ds: DeviceScene, cam: CameraModel, near: float, tile: int, want_rec
 
 
 def _bin(ds: DeviceScene, cam: CameraModel, near: float, tile: int, proj: dict, mode: int):
+    """Enqueue the binning of one frame (no host synchronisation: the counts stay
+    on the device).  Returns (offsets, entries[capacity], counts (2,) int64 on the
+    device: visible voxels, instances; capacity, (tiles_x, tiles_y))."""
     lib = _lib.load()
     dev = ds.device
     tx = -(-cam.width // tile)
     ty = -(-cam.height // tile)
     n_tiles = tx * ty
     offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
+    counts = torch.empty(2, dtype=torch.int64, device=dev)
     span = proj["span_ref"] if mode == 0 else proj["span_fit"]
-    key = (str(dev), mode)
-    cap = _CAPACITY.get(key, 1 << 20)
+    cap = _CAPACITY.get((str(dev), mode), 1 << 20)
     sc, cs = ds.c_struct(), cam.c_struct(rolling=False)
-    n_inst = _lib.C.c_int64(0)
-    for _ in range(3):
-        entries = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-        wsb = lib.salf_raster_bin_workspace_bytes(max(ds.n, 1), cap, n_tiles)
-        ws = _WS.get(dev, wsb)
-        rc = lib.salf_raster_bin(_lib.ref(sc), _lib.ref(cs), float(near), int(tile), int(mode),
-                                 proj["zkey"].data_ptr(), span.data_ptr(), None, ws.data_ptr(),
-                                 ws.numel(), cap, offsets.data_ptr(), entries.data_ptr(),
-                                 _lib.ref(n_inst), _lib.stream_ptr())
-        if rc == _lib.SALF_EWORKSPACE and n_inst.value > cap:
-            cap = int(n_inst.value * 1.25) + 1024
-            _CAPACITY[key] = cap
-            continue
-        _lib.check(rc, "cull_and_bin")
-        return offsets, entries[: n_inst.value], int(n_inst.value), (tx, ty)
-    raise RuntimeError("raster binning failed to size its workspace")
+    entries = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    wsb = lib.salf_raster_bin_workspace_bytes(max(ds.n, 1), cap, n_tiles)
+    ws = _WS.get(dev, wsb)
+    _lib.check(lib.salf_raster_bin(_lib.ref(sc), _lib.ref(cs), float(near), int(tile), int(mode),
+                                   proj["zkey"].data_ptr(), span.data_ptr(), None, ws.data_ptr(),
+                                   ws.numel(), cap, offsets.data_ptr(), entries.data_ptr(),
+                                   counts.data_ptr(), _lib.stream_ptr()), "cull_and_bin")
+    return offsets, entries, counts, cap, (tx, ty)
+
+
+class _Counts:
+    """Pinned host copy of a frame's bin counts, read once the stream reaches it
+    (an event wait after the frame's kernels are enqueued: the GPU never idles)."""
+
+    def __init__(self, counts: torch.Tensor):
+        self.host = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        self.host.copy_(counts, non_blocking=True)
+        self.event = torch.cuda.Event()
+        self.event.record()
+
+    def n_instances(self) -> int:
+        self.event.synchronize()
+        return int(self.host[1])
+
+
+def _grow(dev, mode: int, need: int) -> None:
+    _CAPACITY[(str(dev), mode)] = int(need * 1.25) + 1024
+
+
+def _bin_sync(ds: DeviceScene, cam: CameraModel, near: float, tile: int, proj: dict, mode: int):
+    """_bin, then wait for the count (the host API returns arrays); re-bins once
+    with a larger capacity if the lists did not fit."""
+    for _ in range(2):
+        offsets, entries, counts, cap, txy = _bin(ds, cam, near, tile, proj, mode)
+        n = _Counts(counts).n_instances()
+        if n <= cap:
+            return offsets, entries[:n], n, txy
+        _grow(ds.device, mode, n)
+    raise RuntimeError("raster binning failed to size its instance capacity")
 
 
 def project_voxels(flat, cam: CameraModel, near: float = NEAR_PLANE):
@@ -176,7 +202,7 @@ def cull_and_bin(flat, cam: CameraModel, tile: int = TILE_SIZE, near: float = NE
     if ds.n == 0:
         return TileBins(tx, ty, tile, np.zeros(tx * ty + 1, np.int64), np.zeros(0, np.int64))
     p = _project(ds, cam, near, tile)
-    offsets, entries, _, _ = _bin(ds, cam, near, tile, p, mode=0)
+    offsets, entries, _, _ = _bin_sync(ds, cam, near, tile, p, mode=0)
     return TileBins(tx, ty, tile, offsets.cpu().numpy(), entries.cpu().numpy().astype(np.int64))
 
 
@@ -185,7 +211,7 @@ def render_bins(flat, cam: CameraModel, tile: int = TILE_SIZE, near: float = NEA
     _require_pinhole(cam)
     ds = as_device_scene(flat)
     p = _project(ds, cam, near, tile)
-    offsets, entries, _, (tx, ty) = _bin(ds, cam, near, tile, p, mode=1)
+    offsets, entries, _, (tx, ty) = _bin_sync(ds, cam, near, tile, p, mode=1)
     return TileBins(tx, ty, tile, offsets.cpu().numpy(), entries.cpu().numpy().astype(np.int64))
 
 
@@ -223,20 +249,31 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
     saved = torch.empty((h * w, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev) \
         if return_state else None
     p = _project(ds, cam, near, tile)
-    offsets, entries, n_inst, _ = _bin(ds, cam, near, tile, p, mode=1)
     opts = _opts(background, near, stop_threshold, tile, exact_color)
     sc, cs = ds.c_struct(), cam.c_struct(rolling=False)
-    ev = _timed(events, "raster_composite")
-    _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
-                                         offsets.data_ptr(), entries.data_ptr() if n_inst else offsets.data_ptr(),
-                                         rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
-                                         _lib.ptr(saved), p["vrange"].data_ptr(), None, _lib.stream_ptr()),
-               "rasterize")
-    if ev is not None:
-        ev[2].record()
+    for attempt in range(2):
+        offsets, entries, counts, cap, _ = _bin(ds, cam, near, tile, p, mode=1)
+        ev = _timed(events, "raster_composite")
+        _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
+                                             offsets.data_ptr(), entries.data_ptr(),
+                                             rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
+                                             _lib.ptr(saved), p["vrange"].data_ptr(), None, _lib.stream_ptr()),
+                   "rasterize")
+        if ev is not None:
+            ev[2].record()
+        # capacity check after the composite is enqueued: the host waits for the
+        # binning only, the GPU keeps compositing
+        n_inst = _Counts(counts).n_instances()
+        if n_inst <= cap:
+            break
+        if events is not None:
+            events.pop()
+        _grow(dev, 1, n_inst)
+    else:
+        raise RuntimeError("raster binning failed to size its instance capacity")
     fb = Framebuffer(rgb, op, depth)
     if return_state:
-        return fb, RasterState(ds, cam, opts, offsets, entries, saved, n_inst, p["vrange"])
+        return fb, RasterState(ds, cam, opts, offsets, entries[:n_inst], saved, n_inst, p["vrange"])
     return fb
 
 
@@ -281,7 +318,7 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
                        "rasterize_backward")
         ev = _timed(events, "raster_backward")
         if deterministic:
-            wsb = lib.salf_raster_backward_det_workspace_bytes(state.n_instances)
+            wsb = lib.salf_raster_backward_det_workspace_bytes(state.n_instances, max(ds.n, 1))
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
             _lib.check(lib.salf_raster_backward_deterministic(
                 _lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts), state.offsets.data_ptr(),

@@ -231,7 +231,7 @@ def test_c2_reference_bins_full_size(s1m):
     cam = configs.c2_camera()
     ds = DeviceScene.from_scene(s1m)
     p = RR._project(ds, cam, 0.05, 16)
-    off, ent, n_inst, _ = RR._bin(ds, cam, 0.05, 16, p, mode=0)
+    off, ent, n_inst, _ = RR._bin_sync(ds, cam, 0.05, 16, p, mode=0)
     assert 100_000_000 < n_inst < 104_000_000
     vox = oracle_voxels(s1m)
     ocam = O.Camera("pinhole", cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy,

@@ -1,0 +1,98 @@
+"""The binning's hand-written radix sort (salf_sort.cu, exported as
+salf_sort_pairs) against NumPy's stable argsort -- the ordering the
+reference's np.lexsort (render_raster.py:177) relies on: ties keep input
+order.  Plus the device-resident element count and the capacity re-bin of
+`rasterize` (no host sync inside the binning)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _sort(keys: np.ndarray, vals: np.ndarray, begin=0, end=None, n_dev=None):
+    from paper_2507_18713_b200 import _lib
+    lib = _lib.load()
+    kb = keys.dtype.itemsize
+    end = 8 * kb if end is None else end
+    n = keys.size
+    kin = torch.from_numpy(keys.view(np.int32 if kb == 4 else np.int64)).cuda()
+    vin = torch.from_numpy(vals).cuda()
+    kout = torch.full_like(kin, -1)
+    vout = torch.full_like(vin, -1)
+    nd = torch.tensor([n_dev], dtype=torch.int64, device="cuda") if n_dev is not None else None
+    wsb = lib.salf_sort_pairs_workspace_bytes(max(n, 1), kb, begin, end)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.salf_sort_pairs(kin.data_ptr(), vin.data_ptr(), kout.data_ptr(), vout.data_ptr(), kb,
+                                   _lib.ptr(nd), n, begin, end, ws.data_ptr(), wsb, _lib.stream_ptr()), "sort")
+    torch.cuda.synchronize()
+    ko = kout.cpu().numpy().view(keys.dtype)
+    return ko, vout.cpu().numpy(), kin.cpu().numpy().view(keys.dtype)
+
+
+@pytest.mark.parametrize("n", [1, 31, 4095, 4096, 4097, 100_003, 3_000_000])
+def test_u32_stable_with_ties(n):
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 8160, n).astype(np.uint32)  # C2 tile ids: heavy ties
+    vals = np.arange(n, dtype=np.int32)
+    ko, vo, kin = _sort(keys, vals, 0, 13)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(vo, order)
+    assert np.array_equal(ko, keys[order])
+    assert np.array_equal(kin, keys), "input keys modified"
+
+
+@pytest.mark.parametrize("n", [2, 5000, 640_000])
+def test_u64_depth_keys_stable(n):
+    """Orderable fp64 depth keys with exact duplicates: the (z, index) order."""
+    rng = np.random.default_rng(7)
+    z = rng.uniform(0.05, 200.0, n)
+    z[rng.integers(0, n, n // 3)] = z[0]  # ties
+    bits = z.view(np.uint64)
+    keys = np.where(bits >> 63 == 1, ~bits, bits | (np.uint64(1) << np.uint64(63))).astype(np.uint64)
+    vals = rng.permutation(n).astype(np.int32)
+    ko, vo, _ = _sort(keys, vals)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(vo, vals[order])
+    assert np.array_equal(np.argsort(z, kind="stable"), order)
+
+
+def test_device_count_and_bit_range():
+    rng = np.random.default_rng(3)
+    n_max, n = 50_000, 37_123
+    keys = rng.integers(0, 1 << 20, n_max).astype(np.uint32)
+    vals = np.arange(n_max, dtype=np.int32)
+    ko, vo, _ = _sort(keys, vals, 4, 20, n_dev=n)
+    k = keys[:n] >> 4
+    order = np.argsort(k, kind="stable")
+    assert np.array_equal(vo[:n], order)
+    assert np.all(vo[n:] == -1), "wrote past the device count"
+
+
+def test_rasterize_regrows_capacity():
+    """A capacity far below the frame's instances: the frame is re-binned after
+    the count comes back and equals the unconstrained render."""
+    from conftest import load_golden_scene
+    from paper_2507_18713_b200 import render_raster as RR
+    from paper_2507_18713_b200.scene import flatten_scene
+    from paper_2507_18713_b200.sensors import CameraModel, look_at_quaternion
+    scene = load_golden_scene("rand400")
+    pos = np.array([13.0, 11.0, 7.0])
+    cam = CameraModel(kind="pinhole", width=96, height=80, fx=90.0, fy=90.0, cx=48.0, cy=40.0,
+                      position=pos, quaternion=look_at_quaternion(pos, [4.0, 4.0, 2.0]))
+    flat = flatten_scene(scene)
+    ref = RR.rasterize(flat, cam).color.cpu().numpy()
+    n_ref = RR.render_bins(flat, cam).entries.size
+    key = ("cuda:0", 1)
+    saved = RR._CAPACITY.get(key)
+    try:
+        RR._CAPACITY[key] = 7
+        fb = RR.rasterize(flat, cam)
+        assert RR._CAPACITY[key] >= n_ref
+        assert np.array_equal(fb.color.cpu().numpy(), ref)
+    finally:
+        if saved is None:
+            RR._CAPACITY.pop(key, None)
+        else:
+            RR._CAPACITY[key] = saved

@@ -9,7 +9,7 @@ mkdir -p $OUT
 cd $ROOT/paper_2507_18713_b200/csrc
 make -s all >/dev/null
 OBJS=""
-for f in salf_raster salf_ray salf_sensors salf_train salf_bench salf_octree salf_densify salf_effects; do
+for f in salf_sort salf_raster salf_ray salf_sensors salf_train salf_bench salf_octree salf_densify salf_effects; do
   if [ -n "$*" ]; then
     nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo --fmad=false -Xcompiler -fPIC $* -c $f.cu -o $OUT/$f.o
   else

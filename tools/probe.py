@@ -25,7 +25,7 @@ for regime in sys.argv[1:] or ["surface","init"]:
     fb=RR.rasterize(ds, cam); torch.cuda.synchronize()
     res[f"c2_fwd_ms_{regime}"]=timeit(lambda: RR.rasterize(ds, cam))
     p=RR._project(ds, cam, 0.05, 16)
-    _,_,ninst,_=RR._bin(ds, cam, 0.05, 16, p, 1)
+    _,_,ninst,_=RR._bin_sync(ds, cam, 0.05, 16, p, 1)
     res[f"c2_instances_fit_{regime}"]=ninst
     fb,st=RR.rasterize(ds, cam, return_state=True)
     dc=torch.full((1080,1920,3),1e-6,device='cuda',dtype=torch.float64); dd=torch.zeros((1080,1920),device='cuda',dtype=torch.float64)
