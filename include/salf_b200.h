@@ -159,7 +159,15 @@ int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                           const salf_raster_opts_t *opts, const int64_t *offsets,
                           const int32_t *entries, float *out_rgb, float *out_opacity,
                           float *out_depth, double *saved, const int32_t *vrange,
-                          const int32_t *tile_order, void *stream);
+                          const int32_t *tile_order, uint32_t *hitbits, void *stream);
+
+/* Words of the hit-word array (nullable `hitbits` of salf_raster_composite /
+ * salf_raster_backward, uint32): bit b of word w of pixel slot p of tile t says
+ * list position 32w + b of the tile is an included hit of that pixel -- the
+ * reference's hit and inclusion decisions (render_raster.py:241, :267) as the
+ * certified forward (or its fp64 redo) took them.  The backward then visits
+ * only those pairs and re-derives each chord in fp64.  Default mode only. */
+size_t salf_raster_hitbits_words(int64_t capacity, int32_t n_tiles);
 
 /* Raster backward (no reference function: defined as backward_records,
  * backward.py:35-101, applied to the raster pairs -- see DESIGN.md).
@@ -170,7 +178,7 @@ int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                          const salf_raster_opts_t *opts, const int64_t *offsets,
                          const int32_t *entries, const double *saved, const double *d_rgb,
                          const double *d_depth, double *grad, const int32_t *vrange,
-                         const int32_t *tile_order, void *stream);
+                         const int32_t *tile_order, const uint32_t *hitbits, void *stream);
 
 /* Launch order for the tile kernels (a scheduling choice only, results do
  * not depend on it): tiles by list length, longest first, ties in tile
@@ -191,8 +199,9 @@ int salf_raster_backward_deterministic(const salf_scene_t *scene, const salf_cam
                                        const salf_raster_opts_t *opts, const int64_t *offsets,
                                        const int32_t *entries, int64_t n_instances, const double *saved,
                                        const double *d_rgb, const double *d_depth, double *grad,
-                                       const int32_t *vrange, const int32_t *tile_order, void *workspace,
-                                       size_t workspace_bytes, void *stream);
+                                       const int32_t *vrange, const int32_t *tile_order,
+                                       const uint32_t *hitbits, void *workspace, size_t workspace_bytes,
+                                       void *stream);
 
 /* Deterministic variant of salf_ray_backward: each included segment's
  * 27-row goes to slot row_start[ray] + k (row_start: (n + 1) exclusive scan

@@ -78,8 +78,9 @@ SIGNATURES = {
     "salf_sort_pairs_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
     "salf_sort_pairs": (C.c_int, [vp, vp, vp, vp, C.c_int32, vp, C.c_int64, C.c_int32, C.c_int32, vp,
                                   C.c_size_t, vp]),
-    "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "salf_raster_hitbits_words": (C.c_size_t, [C.c_int64, C.c_int32]),
+    "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_raster_backward_det_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int64]),
     "salf_raster_tile_order_workspace_bytes": (C.c_size_t, [C.c_int32]),
     "salf_raster_tile_order": (C.c_int, [vp, C.c_int32, vp, vp, C.c_size_t, vp]),
@@ -87,7 +88,7 @@ SIGNATURES = {
     "salf_ray_backward_deterministic": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_int64,
                                                   vp, C.c_size_t, vp]),
     "salf_raster_backward_deterministic": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp,
-                                                     vp, C.c_size_t, vp]),
+                                                     vp, vp, C.c_size_t, vp]),
     "salf_camera_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_lidar_rays": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "salf_lidar_batch": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),

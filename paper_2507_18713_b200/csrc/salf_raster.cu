@@ -552,6 +552,16 @@ __device__ __forceinline__ void stage_entry(const salf_scene_t &sc, const Pinhol
 #define SALF_CHUNKB 32
 #endif
 constexpr int kChunk = SALF_CHUNK;    // forward: entries staged per step in shared memory
+// Hit words (forward -> backward): bit b of word w of pixel slot p of a tile is
+// "list position 32 w + b of the tile is an included hit of that pixel"
+// (the reference's hit AND inclusion decisions, as certified by the forward or
+// recomputed by the fp64 redo).  Tile t's words start at 256 (off[t] / 32 + t):
+// ceil(len / 32) <= floor(off[t+1] / 32) - floor(off[t] / 32) + 1, so tiles never
+// overlap and the whole array is 256 (I / 32 + T + 1) words.
+constexpr int kHitSlots = 256;  // pixel slots per tile word row (tile <= 16)
+__device__ __forceinline__ int64_t hit_word_base(int64_t beg, int tile_id) {
+  return (int64_t)kHitSlots * (beg / 32 + tile_id);
+}
 constexpr int kChunkB = SALF_CHUNKB;  // backward: + a kChunkB x warps x 27 fp32 reduction buffer
 
 // fp64 parity-mode composite (exact_color=True): the reference-order
@@ -1124,6 +1134,43 @@ __device__ __forceinline__ bool bwd_pair(const salf_scene_t &sc, const EntryF &e
   return true;
 }
 
+// The pair part of a KNOWN hit (hit words from the forward): the chord in
+// fp64 -- the reference's slab test with reciprocal multiply (octree.py:184-194)
+// in closest-approach coordinates u = t - t*, 1/d precomputed per pixel
+// (iv, IEEE division) -- so delta and t_mid carry ~1e-16 h |1/d| absolute error
+// however short the chord, with no per-pair refinement branch.  Kept iff
+// t1 > t0 + 1e-12 (render_raster.py:241).  Rotated voxels and rays with a zero
+// direction component take the general fp64 path.
+template <bool kRot, bool kDepth>
+__device__ __forceinline__ bool bwd_pair64(const salf_scene_t &sc, const EntryF &e, const BwdPix &q,
+                                           const double *__restrict__ iv, PairHit &h) {
+  if ((kRot && e.rot) || !q.r.fast) return bwd_pair<kRot, kDepth, true>(sc, e, q, h);
+  const RayF &r = q.r;
+  const double ts = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
+  double u0 = r.tn0 - ts, u1 = INFINITY;
+  float qf[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double qk = fma(ts, r.d[k], e.o[k]);
+    const double ik = iv[k];
+    const double hk = e.half * fabs(ik);
+    u0 = fmax(u0, fma(-qk, ik, -hk));
+    u1 = fmin(u1, fma(-qk, ik, hk));
+    qf[k] = (float)qk;
+  }
+  if (!(u1 > u0 + 1e-12)) return false;
+  h.delta = (float)(u1 - u0);
+  const float um = (float)(0.5 * (u0 + u1));
+  h.dq = kDepth ? (float)(ts - q.D) + um : 0.f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) h.x[k] = __fmaf_rn(um, r.df[k], qf[k]) * e.inv_hf;
+  if (kRot) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h.gam[k] = r.gam[k];
+  }
+  return true;
+}
+
 // One included hit of pixel q against staged entry e, visited back to front
 // (its pair part h from bwd_pair): adds its 27 gradient components to g.
 template <bool kRot, bool sdf, bool kDepth = true>
@@ -1287,7 +1334,9 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
                                                         float *__restrict__ out_rgb, float *__restrict__ out_op,
                                                         float *__restrict__ out_depth, double *__restrict__ saved,
                                                         const int32_t *__restrict__ vrange,
-                                                        const int32_t *__restrict__ tile_order) {
+                                                        const int32_t *__restrict__ tile_order,
+                                                        uint32_t *__restrict__ hitbits) {
+  static_assert(kChunk == 64, "hit words: two 32-entry words per staged chunk");
   __shared__ EntryF sm[kChunk];
   // heaviest tiles first (tile_order: tiles by list length, descending) -> no ragged last wave
   const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
@@ -1320,6 +1369,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   const int wfirst = threadIdx.x & ~31, wlast = min(wfirst + 31, c.tile * c.tile - 1);
   const int wr0 = ty * c.tile + wfirst / c.tile, wr1 = ty * c.tile + wlast / c.tile;
 
+  const int64_t hb_base = hit_word_base(beg, tile_id);
   for (int64_t base = beg; base < end; base += kChunk) {
     const int cn = (int)min((int64_t)kChunk, end - base);
     __syncthreads();
@@ -1327,6 +1377,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
     __syncthreads();
     prefetch_next(sc, entries, base + kChunk, end, kChunk);
     if (alive) {
+      uint32_t hb0 = 0u, hb1 = 0u;  // included hits of this chunk (list positions base - beg + j)
       for (int j = 0; j < cn; ++j) {
         const EntryF &e = sm[j];
         if (e.vhi < wr0 || e.vlo > wr1) continue;  // footprint misses this warp's pixel rows (warp-uniform)
@@ -1367,6 +1418,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           n_stop = (int)(base - beg) + j;
           break;
         }
+        if (j < 32) hb0 |= 1u << j; else hb1 |= 1u << (j - 32);
         const float delta = u1 - u0;
         const float um = 0.5f * (u0 + u1);
         float x[3];
@@ -1400,6 +1452,11 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
         Yh = Yt;
         T = fast_exp(-(Yh + Yc));
         ++n_inc;
+      }
+      if (hitbits) {
+        uint32_t *hw = hitbits + hb_base + (int64_t)((base - beg) >> 5) * kHitSlots + threadIdx.x;
+        hw[0] = hb0;
+        if (cn > 32) hw[kHitSlots] = hb1;
       }
     }
     if (!__syncthreads_or(alive)) break;
@@ -1435,7 +1492,8 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
                                                        const int64_t *__restrict__ offsets,
                                                        const int32_t *__restrict__ entries,
                                                        float *__restrict__ out_rgb, float *__restrict__ out_op,
-                                                       float *__restrict__ out_depth, double *__restrict__ saved) {
+                                                       float *__restrict__ out_depth, double *__restrict__ saved,
+                                                       uint32_t *__restrict__ hitbits) {
   const int64_t npx = (int64_t)c.width * c.height;
   const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(int64_t)31;
   const int lane = threadIdx.x & 31;
@@ -1468,6 +1526,7 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
         hit = hit_and_shade<false, kRot>(sc, r, e, sv);
       }
       unsigned hits = __ballot_sync(0xffffffffu, hit);
+      const unsigned all_hits = hits;
       while (hits) {
         const int k = __ffs(hits) - 1;
         hits &= hits - 1;
@@ -1491,6 +1550,12 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
         T = __dmul_rn(T, om);
         ++n_inc;
       }
+      if (hitbits && lane == 0) {  // included hits of this 32-entry word (positions before the stop)
+        const int ks = alive ? 32 : (int)(n_stop - (base - beg));
+        const unsigned inc = ks >= 32 ? all_hits : (all_hits & ((1u << ks) - 1u));
+        const int pslot = (py % c.tile) * c.tile + px % c.tile;
+        hitbits[hit_word_base(beg, tile_id) + (int64_t)((base - beg) >> 5) * kHitSlots + pslot] = inc;
+      }
     }
     if (lane == 0) {
 #pragma unroll
@@ -1512,6 +1577,9 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
 #ifndef SALF_BWD_SMEMRED
 #define SALF_BWD_SMEMRED 1  // warp reduction by a shared-memory transpose (0: shuffles; measured slower)
 #endif
+#ifndef SALF_BWD_ALL64
+#define SALF_BWD_ALL64 false  // A/B: every fp32 hit's chord re-derived in fp64 (no refinement branch)
+#endif
 #ifndef SALF_BWD_NP
 #define SALF_BWD_NP 2  // pixels per thread
 #endif
@@ -1519,13 +1587,16 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
 #define SALF_BWDF_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 
-template <bool kRot, int NP, bool sdf, bool kDepth = true>
+template <bool kRot, int NP, bool sdf, bool kDepth = true, bool kBits = false>
 __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
     const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial,
-    const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order) {
+    const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order,
+    const uint32_t *__restrict__ hitbits) {
+  static_assert(!kBits || kChunkB == 32, "hit words: one 32-entry word per staged chunk");
   __shared__ EntryF sm[kChunkB];
+  __shared__ double s_iv[kBits ? 256 * 3 : 1];  // per pixel slot: fp64 1/d (bwd_pair64)
   __shared__ float red[kChunkB][8 / NP][kGradStride];
 #if SALF_BWD_SMEMRED
   __shared__ __align__(16) float xp[8 / NP][32][28];
@@ -1547,7 +1618,13 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     const int px = tx * c.tile + li % c.tile, py = ty * c.tile + li / c.tile;
     in[k] = li < npix && px < c.width && py < c.height;
     q[k].n_stop = 0;
-    if (in[k]) bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, q[k]);
+    if (in[k]) {
+      bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, q[k]);
+      if (kBits) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) s_iv[li * 3 + a] = 1.0 / q[k].r.d[a];
+      }
+    }
   }
   __syncthreads();
   int my_max = 0;
@@ -1573,8 +1650,65 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     __syncthreads();
     prefetch_prev(sc, entries, base - kChunkB, beg, kChunkB);
     const int jb = (int)(base - beg);
+    uint32_t wb[NP];  // hit words of this chunk (kBits)
+    if (kBits) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int li = threadIdx.x + k * nthreads;
+        wb[k] = (in[k] && jb < q[k].n_stop)
+                    ? __ldg(hitbits + hit_word_base(beg, tile_id) + (int64_t)(jb >> 5) * kHitSlots + li) : 0u;
+      }
+    }
     for (int j = cn - 1; j >= 0; --j) {
       const EntryF &e = sm[j];
+      if (kBits) {
+        bool hb[NP];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          hb[k] = (wb[k] >> j) & 1u;
+          any |= hb[k];
+        }
+        if (!__any_sync(0xffffffffu, any)) {  // no pixel of this warp includes entry j
+          if (lane < kGradStride) red[j][warp][lane] = 0.f;
+          continue;
+        }
+        PairHit ph[NP];
+        bool hit[NP];
+        bool act = false;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          hit[k] = hb[k] && bwd_pair64<kRot, kDepth>(sc, e, q[k], s_iv + (threadIdx.x + k * nthreads) * 3, ph[k]);
+          act |= hit[k];
+        }
+        float g[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) g[k] = 0.f;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+          if (hit[k]) bwd_segment<kRot, sdf, kDepth>(e, q[k], ph[k], g);
+        float tot = 0.0f;
+        if (__ballot_sync(0xffffffffu, act)) {
+          float4 *row = reinterpret_cast<float4 *>(&xp[warp][lane][0]);
+#pragma unroll
+          for (int m = 0; m < 7; ++m) row[m] = make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]);
+          __syncwarp();
+          if (lane < kGradStride) {
+            float t0 = xp[warp][0][lane], t1 = xp[warp][1][lane], t2 = xp[warp][2][lane], t3 = xp[warp][3][lane];
+#pragma unroll
+            for (int rr = 4; rr < 32; rr += 4) {
+              t0 += xp[warp][rr][lane];
+              t1 += xp[warp][rr + 1][lane];
+              t2 += xp[warp][rr + 2][lane];
+              t3 += xp[warp][rr + 3][lane];
+            }
+            tot = (t0 + t1) + (t2 + t3);
+          }
+          __syncwarp();
+        }
+        if (lane < kGradStride) red[j][warp][lane] = tot;
+        continue;
+      }
       bool rows_hit[NP];
       bool any_rows = false;
 #pragma unroll
@@ -1591,7 +1725,7 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
       bool act = false;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        hit[k] = rows_hit[k] && jb + j < q[k].n_stop && bwd_pair<kRot, kDepth>(sc, e, q[k], ph[k]);
+        hit[k] = rows_hit[k] && jb + j < q[k].n_stop && bwd_pair<kRot, kDepth, SALF_BWD_ALL64>(sc, e, q[k], ph[k]);
         act |= hit[k];
       }
       float g[32];
@@ -1764,7 +1898,8 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
 extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camera_t *cam,
                                      const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                      float *out_rgb, float *out_opacity, float *out_depth, double *saved,
-                                     const int32_t *vrange, const int32_t *tile_order, void *stream) {
+                                     const int32_t *vrange, const int32_t *tile_order, uint32_t *hitbits,
+                                     void *stream) {
   SALF_TRY {
     if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
                                                      camera_kind_repr(cam->kind));
@@ -1789,17 +1924,17 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
       const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
 #define SALF_LAUNCH_FWD(ROT, SDF)                                                                             \
   k_composite_fast<ROT, SDF><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity, \
-                                                         out_depth, saved, vrange, tile_order)
+                                                         out_depth, saved, vrange, tile_order, hitbits)
       if (rot) {
         if (sdf) SALF_LAUNCH_FWD(true, true); else SALF_LAUNCH_FWD(true, false);
         if (!no_redo)
           k_composite_redo<true><<<rb, 128, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
-                                                     out_depth, saved);
+                                                     out_depth, saved, hitbits);
       } else {
         if (sdf) SALF_LAUNCH_FWD(false, true); else SALF_LAUNCH_FWD(false, false);
         if (!no_redo)
           k_composite_redo<false><<<rb, 128, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity,
-                                                      out_depth, saved);
+                                                      out_depth, saved, hitbits);
       }
 #undef SALF_LAUNCH_FWD
     }
@@ -1812,7 +1947,7 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
                                   const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                   const double *saved, const double *d_rgb, const double *d_depth, double *grad,
                                   float *partial, const int32_t *vrange, const int32_t *tile_order,
-                                  cudaStream_t st) {
+                                  const uint32_t *hitbits, cudaStream_t st) {
   if (cam->kind != SALF_PINHOLE) return set_error(SALF_EINVAL, "rasterizer supports pinhole cameras only, got %s",
                                                    camera_kind_repr(cam->kind));
   if (opts->tile < 1 || opts->tile > 16) return set_error(SALF_EINVAL, "tile size must be in [1, 16]");
@@ -1831,8 +1966,14 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
     const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
     const bool depth = d_depth != nullptr;  // no depth seeds (colour-only loss): the depth term is dropped
 #define SALF_LAUNCH_BWD(ROT, SDF, DEPTH)                                                                    \
-  k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH><<<n_tiles, threads_np, 0, st>>>(                            \
-      *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order)
+  do {                                                                                                      \
+    if (hitbits)                                                                                            \
+      k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH, true><<<n_tiles, threads_np, 0, st>>>(                  \
+          *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, hitbits); \
+    else                                                                                                    \
+      k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH, false><<<n_tiles, threads_np, 0, st>>>(                 \
+          *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, nullptr); \
+  } while (0)
     if (rot) {
       if (sdf) SALF_LAUNCH_BWD(true, true, true); else SALF_LAUNCH_BWD(true, false, true);
     } else if (depth) {
@@ -1848,10 +1989,11 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
 extern "C" int salf_raster_backward(const salf_scene_t *scene, const salf_camera_t *cam,
                                     const salf_raster_opts_t *opts, const int64_t *offsets, const int32_t *entries,
                                     const double *saved, const double *d_rgb, const double *d_depth, double *grad,
-                                    const int32_t *vrange, const int32_t *tile_order, void *stream) {
+                                    const int32_t *vrange, const int32_t *tile_order, const uint32_t *hitbits,
+                                    void *stream) {
   SALF_TRY {
     return raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, nullptr, vrange,
-                                  tile_order, (cudaStream_t)stream);
+                                  tile_order, hitbits, (cudaStream_t)stream);
   }
   SALF_CATCH
 }
@@ -1988,8 +2130,9 @@ extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, con
                                                   const salf_raster_opts_t *opts, const int64_t *offsets,
                                                   const int32_t *entries, int64_t n_instances, const double *saved,
                                                   const double *d_rgb, const double *d_depth, double *grad,
-                                                  const int32_t *vrange, const int32_t *tile_order, void *workspace,
-                                                  size_t workspace_bytes, void *stream) {
+                                                  const int32_t *vrange, const int32_t *tile_order,
+                                                  const uint32_t *hitbits, void *workspace, size_t workspace_bytes,
+                                                  void *stream) {
   SALF_TRY {
     if (n_instances <= 0) return SALF_OK;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1998,7 +2141,7 @@ extern "C" int salf_raster_backward_deterministic(const salf_scene_t *scene, con
     float *partial = (float *)workspace;
     cudaMemsetAsync(partial, 0, sizeof(float) * kGradStride * n_instances, st);
     const int rc = raster_backward_launch(scene, cam, opts, offsets, entries, saved, d_rgb, d_depth, grad, partial,
-                                          vrange, tile_order, st);
+                                          vrange, tile_order, hitbits, st);
     if (rc != SALF_OK) return rc;
     // instance rows keyed by their voxel (entries[i])
     return det_reduce_rows(n_instances, reinterpret_cast<const uint32_t *>(entries), partial, scene->n, grad,
@@ -2018,3 +2161,7 @@ extern "C" int salf_debug_counters(unsigned long long *out, int reset) {
   return 0;
 }
 #endif
+
+extern "C" size_t salf_raster_hitbits_words(int64_t capacity, int32_t n_tiles) {
+  return (size_t)salf::kHitSlots * (size_t)(std::max<int64_t>(capacity, 0) / 32 + std::max(n_tiles, 0) + 1);
+}

@@ -557,7 +557,6 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   double acc_f[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // fp64 totals of the exact products w f
   constexpr bool feat = kLidar && kFeat;  // the extension is a separate instantiation (no per-segment test)
   constexpr float kU = 5.9604645e-8f;  // 2^-24
-  constexpr float kYClamp = 27.631021115928547f;
   constexpr double kLn2 = 0.6931471805599453;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;

@@ -67,6 +67,7 @@ class RasterState:
     n_instances: int
     vrange: torch.Tensor | None = None  # per-voxel footprint rows (entry culling per warp)
     tile_order: torch.Tensor | None = None  # launch order of the tiles (longest lists first)
+    hitbits: torch.Tensor | None = None  # included-hit words per (tile, pixel, 32 entries) (default mode)
 
 
 def _timed(events, name):
@@ -253,11 +254,15 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
     sc, cs = ds.c_struct(), cam.c_struct(rolling=False)
     for attempt in range(2):
         offsets, entries, counts, cap, _ = _bin(ds, cam, near, tile, p, mode=1)
+        # hit words for the backward (default mode): which list entries each pixel includes
+        hitbits = torch.empty(lib.salf_raster_hitbits_words(cap, offsets.numel() - 1), dtype=torch.int32,
+                              device=dev) if (return_state and not exact_color) else None
         ev = _timed(events, "raster_composite")
         _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
                                              offsets.data_ptr(), entries.data_ptr(),
                                              rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
-                                             _lib.ptr(saved), p["vrange"].data_ptr(), None, _lib.stream_ptr()),
+                                             _lib.ptr(saved), p["vrange"].data_ptr(), None, _lib.ptr(hitbits),
+                                             _lib.stream_ptr()),
                    "rasterize")
         if ev is not None:
             ev[2].record()
@@ -273,7 +278,8 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
         raise RuntimeError("raster binning failed to size its instance capacity")
     fb = Framebuffer(rgb, op, depth)
     if return_state:
-        return fb, RasterState(ds, cam, opts, offsets, entries[:n_inst], saved, n_inst, p["vrange"])
+        return fb, RasterState(ds, cam, opts, offsets, entries[:n_inst], saved, n_inst, p["vrange"],
+                               hitbits=hitbits)
     return fb
 
 
@@ -323,14 +329,14 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
             _lib.check(lib.salf_raster_backward_deterministic(
                 _lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts), state.offsets.data_ptr(),
                 state.entries.data_ptr(), state.n_instances, state.saved.data_ptr(), dc.data_ptr(), _lib.ptr(dd),
-                grad.data_ptr(), _lib.ptr(state.vrange), _lib.ptr(state.tile_order), ws.data_ptr(), wsb,
-                _lib.stream_ptr()), "rasterize_backward")
+                grad.data_ptr(), _lib.ptr(state.vrange), _lib.ptr(state.tile_order), _lib.ptr(state.hitbits),
+                ws.data_ptr(), wsb, _lib.stream_ptr()), "rasterize_backward")
         else:
             _lib.check(lib.salf_raster_backward(_lib.ref(sc), _lib.ref(cs), _lib.ref(state.opts),
                                                 state.offsets.data_ptr(), state.entries.data_ptr(),
                                                 state.saved.data_ptr(), dc.data_ptr(), _lib.ptr(dd),
                                                 grad.data_ptr(), _lib.ptr(state.vrange), _lib.ptr(state.tile_order),
-                                                _lib.stream_ptr()), "rasterize_backward")
+                                                _lib.ptr(state.hitbits), _lib.stream_ptr()), "rasterize_backward")
         if ev is not None:
             ev[2].record()
     if as_dict:
