@@ -1587,16 +1587,13 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
 #define SALF_BWDF_MINB 4  // resident CTAs per SM the register budget is sized for
 #endif
 
-template <bool kRot, int NP, bool sdf, bool kDepth = true, bool kBits = false>
+template <bool kRot, int NP, bool sdf, bool kDepth = true>
 __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
     const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial,
-    const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order,
-    const uint32_t *__restrict__ hitbits) {
-  static_assert(!kBits || kChunkB == 32, "hit words: one 32-entry word per staged chunk");
+    const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order) {
   __shared__ EntryF sm[kChunkB];
-  __shared__ double s_iv[kBits ? 256 * 3 : 1];  // per pixel slot: fp64 1/d (bwd_pair64)
   __shared__ float red[kChunkB][8 / NP][kGradStride];
 #if SALF_BWD_SMEMRED
   __shared__ __align__(16) float xp[8 / NP][32][28];
@@ -1618,13 +1615,7 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     const int px = tx * c.tile + li % c.tile, py = ty * c.tile + li / c.tile;
     in[k] = li < npix && px < c.width && py < c.height;
     q[k].n_stop = 0;
-    if (in[k]) {
-      bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, q[k]);
-      if (kBits) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) s_iv[li * 3 + a] = 1.0 / q[k].r.d[a];
-      }
-    }
+    if (in[k]) bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, q[k]);
   }
   __syncthreads();
   int my_max = 0;
@@ -1650,65 +1641,8 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
     __syncthreads();
     prefetch_prev(sc, entries, base - kChunkB, beg, kChunkB);
     const int jb = (int)(base - beg);
-    uint32_t wb[NP];  // hit words of this chunk (kBits)
-    if (kBits) {
-#pragma unroll
-      for (int k = 0; k < NP; ++k) {
-        const int li = threadIdx.x + k * nthreads;
-        wb[k] = (in[k] && jb < q[k].n_stop)
-                    ? __ldg(hitbits + hit_word_base(beg, tile_id) + (int64_t)(jb >> 5) * kHitSlots + li) : 0u;
-      }
-    }
     for (int j = cn - 1; j >= 0; --j) {
       const EntryF &e = sm[j];
-      if (kBits) {
-        bool hb[NP];
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          hb[k] = (wb[k] >> j) & 1u;
-          any |= hb[k];
-        }
-        if (!__any_sync(0xffffffffu, any)) {  // no pixel of this warp includes entry j
-          if (lane < kGradStride) red[j][warp][lane] = 0.f;
-          continue;
-        }
-        PairHit ph[NP];
-        bool hit[NP];
-        bool act = false;
-#pragma unroll
-        for (int k = 0; k < NP; ++k) {
-          hit[k] = hb[k] && bwd_pair64<kRot, kDepth>(sc, e, q[k], s_iv + (threadIdx.x + k * nthreads) * 3, ph[k]);
-          act |= hit[k];
-        }
-        float g[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) g[k] = 0.f;
-#pragma unroll
-        for (int k = 0; k < NP; ++k)
-          if (hit[k]) bwd_segment<kRot, sdf, kDepth>(e, q[k], ph[k], g);
-        float tot = 0.0f;
-        if (__ballot_sync(0xffffffffu, act)) {
-          float4 *row = reinterpret_cast<float4 *>(&xp[warp][lane][0]);
-#pragma unroll
-          for (int m = 0; m < 7; ++m) row[m] = make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]);
-          __syncwarp();
-          if (lane < kGradStride) {
-            float t0 = xp[warp][0][lane], t1 = xp[warp][1][lane], t2 = xp[warp][2][lane], t3 = xp[warp][3][lane];
-#pragma unroll
-            for (int rr = 4; rr < 32; rr += 4) {
-              t0 += xp[warp][rr][lane];
-              t1 += xp[warp][rr + 1][lane];
-              t2 += xp[warp][rr + 2][lane];
-              t3 += xp[warp][rr + 3][lane];
-            }
-            tot = (t0 + t1) + (t2 + t3);
-          }
-          __syncwarp();
-        }
-        if (lane < kGradStride) red[j][warp][lane] = tot;
-        continue;
-      }
       bool rows_hit[NP];
       bool any_rows = false;
 #pragma unroll
@@ -1767,6 +1701,317 @@ __global__ void __launch_bounds__(256 / NP, SALF_BWDF_MINB) k_backward_fast(
       const int j = t / kGradStride, k = t - j * kGradStride;
       float sum = 0.0f;
       for (int w = 0; w < nwarps; ++w) sum += red[j][w][k];
+      if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
+      else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Backward over the forward's hit words (default mode).  Two pixels per thread
+// (rows ly and ly + 8 of the tile) processed TOGETHER in packed fp32x2
+// arithmetic (FFMA2 / FMUL2 / FADD2, sm_100): lane .x is the first pixel,
+// .y the second.  A pixel without a hit on the entry runs the same chain with
+// delta = 0 and x = 0 (y = 0, alpha = 0, w = 0: it adds exact zeros and
+// leaves its state unchanged), so one pass shades both pixels -- the scalar
+// kernel ran one divergent pass per pixel.  Each packed op is two IEEE
+// fp32 ops, so the per-pixel arithmetic is the scalar kernel's.
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 ex2_2(float2 t) {
+  float2 y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.x) : "f"(t.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y.y) : "f"(t.y));
+  return y;
+}
+// fast_exp of both lanes (MUFU ex2 of x log2 e, as fast_exp)
+__device__ __forceinline__ float2 exp2v(float2 x) { return ex2_2(mul2(x, f2(1.4426950408889634f))); }
+__device__ __forceinline__ float2 rcp2(float2 x) {
+  float2 y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y.x) : "f"(x.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y.y) : "f"(x.y));
+  return y;
+}
+// expm1_neg of both lanes (same polynomial / branchless select)
+__device__ __forceinline__ float2 expm1_neg2(float2 x) {
+  float2 p = fma2(x, f2(1.0f / 5040.0f), f2(1.0f / 720.0f));
+  p = fma2(x, p, f2(1.0f / 120.0f));
+  p = fma2(x, p, f2(1.0f / 24.0f));
+  p = fma2(x, p, f2(1.0f / 6.0f));
+  p = fma2(x, p, f2(0.5f));
+  const float2 small = fma2(mul2(x, x), p, x);
+  const float2 big = add2(exp2v(x), f2(-1.0f));
+  return make_float2(x.x > -0.25f ? small.x : big.x, x.y > -0.25f ? small.y : big.y);
+}
+
+// per-entry field constants, each duplicated (p, p) so a packed op reads it as
+// one 64-bit shared-memory operand: w_s 0..3, w_c 4..12, w_sh 13..24, a 25,
+// 1/b 26, a/2 27, (a/2)(1/b) 28
+constexpr int kPP = 30;
+
+struct Pix2 {
+  RayF r[2];
+  double D[2];
+  int n_stop[2];
+  float2 dC[3], dws, tail, Yh, Yc, S;
+  float2 g1, g2, g3;  // SH basis C1 y, C1 z, C1 x per pixel (C0 is a constant)
+};
+
+struct Hit2 {
+  float2 x[3], delta, dq;
+  float2 gm[4];  // kRot: SH basis of the (possibly rotated) ray
+};
+
+template <bool kRot, bool sdf, bool kDepth>
+__device__ __forceinline__ void bwd_segment2(const float2 *__restrict__ pp, Pix2 &q, const Hit2 &h, float g[32]) {
+  const float2 X0 = h.x[0], X1 = h.x[1], X2 = h.x[2], dl = h.delta;
+  const float2 G0 = f2((float)kShC0);
+  const float2 G1 = kRot ? h.gm[1] : q.g1, G2 = kRot ? h.gm[2] : q.g2, G3 = kRot ? h.gm[3] : q.g3;
+  // fields (scene.py:229-284)
+  const float2 s = fma2(pp[2], X2, fma2(pp[1], X1, fma2(pp[0], X0, pp[3])));
+  float2 ee = f2(0.f), sigma;
+  if (sdf) {
+    const float ib = pp[26].x;
+    ee = exp2v(make_float2(-fabsf(s.x) * ib, -fabsf(s.y) * ib));
+    const float2 he = mul2(pp[27], ee);
+    const float2 ahe = add2(pp[25], neg2(he));
+    sigma = make_float2(s.x > 0.f ? ahe.x : he.x, s.y > 0.f ? ahe.y : he.y);
+  } else {
+    sigma = exp2v(s);
+    // an idle lane (delta = 0) must add exact zeros: raw density may overflow to inf
+    sigma = make_float2(dl.x > 0.f ? sigma.x : 0.f, dl.y > 0.f ? sigma.y : 0.f);
+  }
+  constexpr float kYClamp = 27.631021115928547f;  // alpha >= 1 - 1e-12 (scene.py:32)
+  const float2 yr = mul2(sigma, dl);
+  const float2 nyr = neg2(yr);
+  const float2 om = exp2v(nyr);      // exp(-sigma delta), unclamped (backward.py:66)
+  const float2 em = expm1_neg2(nyr);
+  const bool c0 = yr.x > kYClamp, c1 = yr.y > kYClamp;
+  const float2 y = make_float2(c0 ? kYClamp : yr.x, c1 ? kYClamp : yr.y);
+  const float2 alpha = make_float2(c0 ? 1.f : -em.x, c1 ? 1.f : -em.y);
+  const float2 omc = make_float2(c0 ? 1e-12f : om.x, c1 ? 1e-12f : om.y);
+  // Y before this hit = Y after it - y (compensated)
+  {
+    const float2 Yt = add2(q.Yh, neg2(y));
+    const float2 u1 = add2(add2(q.Yh, neg2(Yt)), neg2(y));  // (Yh - Yt) - y
+    const float2 u2 = add2(add2(neg2(y), neg2(Yt)), q.Yh);  // (-y - Yt) + Yh
+    q.Yc = add2(q.Yc, make_float2(fabsf(q.Yh.x) >= y.x ? u1.x : u2.x, fabsf(q.Yh.y) >= y.y ? u1.y : u2.y));
+    q.Yh = Yt;
+  }
+  const float2 T = exp2v(neg2(add2(q.Yh, q.Yc)));
+  // colour and its complement: c = 1 / (1 + E), 1 - c = E c (E = e^-z)
+  float2 col[3], omcol[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float2 z = fma2(pp[4 + 3 * i + 2], X2, fma2(pp[4 + 3 * i + 1], X1, mul2(pp[4 + 3 * i], X0)));
+    z = fma2(pp[13 + 4 * i + 0], G0, z);
+    z = fma2(pp[13 + 4 * i + 1], G1, z);
+    z = fma2(pp[13 + 4 * i + 2], G2, z);
+    z = fma2(pp[13 + 4 * i + 3], G3, z);
+    const float2 E = exp2v(neg2(z));
+    col[i] = rcp2(add2(f2(1.0f), E));
+    omcol[i] = mul2(E, col[i]);
+  }
+  const float2 w = mul2(T, alpha);
+  // A = dC . c + dD (t_mid - D) / ws (backward.py:52-59)
+  const float2 A = fma2(q.dC[2], col[2], fma2(q.dC[1], col[1], kDepth ? fma2(q.dC[0], col[0], mul2(q.dws, h.dq))
+                                                                       : mul2(q.dC[0], col[0])));
+  const float2 ga = fma2(A, T, mul2(neg2(add2(q.S, q.tail)), rcp2(omc)));  // backward.py:62-64
+  q.S = fma2(A, w, q.S);
+  const float2 gs = mul2(mul2(ga, dl), om);  // :66
+  float2 ds, gla, glb;
+  if (sdf) {
+    const float2 k2e = mul2(pp[28], ee);
+    const float2 d = mul2(gs, k2e);
+    ds = make_float2(s.x == 0.f ? 0.f : d.x, s.y == 0.f ? 0.f : d.y);  // :92
+    gla = mul2(gs, sigma);                                               // :94
+    glb = mul2(mul2(neg2(gs), k2e), s);                                  // :95
+  } else {
+    ds = mul2(gs, sigma);
+    gla = f2(0.f);
+    glb = f2(0.f);
+  }
+  const float2 X[3] = {X0, X1, X2};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) g[k] = __fmaf_rn(ds.y, X[k].y, __fmaf_rn(ds.x, X[k].x, g[k]));
+  g[3] += ds.x + ds.y;
+  const float2 Gs[4] = {G0, G1, G2, G3};
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float2 gz = mul2(mul2(q.dC[i], mul2(w, col[i])), omcol[i]);  // dC w c (1 - c)  :69-70
+#pragma unroll
+    for (int k = 0; k < 3; ++k) g[4 + 3 * i + k] = __fmaf_rn(gz.y, X[k].y, __fmaf_rn(gz.x, X[k].x, g[4 + 3 * i + k]));
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      g[13 + 4 * i + k] = __fmaf_rn(gz.y, Gs[k].y, __fmaf_rn(gz.x, Gs[k].x, g[13 + 4 * i + k]));
+  }
+  g[25] += gla.x + gla.y;
+  g[26] += glb.x + glb.y;
+}
+
+// The known hit's chord (bwd_pair64) written into lane `k` of the packed hit.
+template <bool kRot, bool kDepth>
+__device__ __forceinline__ bool pair64_into(const salf_scene_t &sc, const EntryF &e, const BwdPix &q,
+                                            const double *__restrict__ iv, Hit2 &h, int k) {
+  PairHit ph;
+  if (!bwd_pair64<kRot, kDepth>(sc, e, q, iv, ph)) return false;
+  float *hx0 = k ? &h.x[0].y : &h.x[0].x;
+  float *hx1 = k ? &h.x[1].y : &h.x[1].x;
+  float *hx2 = k ? &h.x[2].y : &h.x[2].x;
+  *hx0 = ph.x[0];
+  *hx1 = ph.x[1];
+  *hx2 = ph.x[2];
+  (k ? h.delta.y : h.delta.x) = ph.delta;
+  (k ? h.dq.y : h.dq.x) = ph.dq;
+  if (kRot) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) (k ? h.gm[m].y : h.gm[m].x) = ph.gam[m];
+  }
+  return true;
+}
+
+template <bool kRot, bool sdf, bool kDepth>
+__global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
+    salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
+    const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
+    const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial,
+    const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order,
+    const uint32_t *__restrict__ hitbits) {
+  static_assert(kChunkB == 32, "hit words: one 32-entry word per staged chunk");
+  constexpr int kW = 4;  // warps
+  __shared__ EntryF sm[kChunkB];
+  __shared__ __align__(16) float2 spp[kChunkB][kPP];
+  __shared__ float red[kChunkB][kW][kGradStride];
+  __shared__ __align__(16) float xp[kW][32][28];
+  __shared__ double s_iv[256 * 3];  // per pixel slot: fp64 1/d (bwd_pair64)
+  __shared__ int s_max;
+  const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
+  const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
+  const int npix = c.tile * c.tile;
+  const int64_t beg = offsets[tile_id];
+  const int64_t hb = hit_word_base(beg, tile_id);
+
+  Pix2 q;
+  BwdPix bp[2];
+  bool in[2];
+  if (threadIdx.x == 0) s_max = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int li = threadIdx.x + k * 128;
+    const int px = tx * c.tile + li % c.tile, py = ty * c.tile + li / c.tile;
+    in[k] = li < npix && px < c.width && py < c.height;
+    bp[k].n_stop = 0;
+    if (in[k]) {
+      bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, bp[k]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) s_iv[li * 3 + a] = 1.0 / bp[k].r.d[a];
+    } else {
+      // idle slot (outside the image): finite state, never hit (n_stop 0); its lane of the
+      // packed chain must stay finite (0 * NaN would poison the warp sums)
+#pragma unroll
+      for (int a = 0; a < 4; ++a) bp[k].r.gam[a] = 0.f;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        bp[k].r.df[a] = 0.f;
+        bp[k].r.d[a] = 0.0;
+      }
+      bp[k].dC[0] = bp[k].dC[1] = bp[k].dC[2] = 0.f;
+      bp[k].dws = bp[k].tail = bp[k].Yh = bp[k].Yc = bp[k].S = 0.f;
+      bp[k].D = 0.0;
+    }
+  }
+  q.dC[0] = make_float2(bp[0].dC[0], bp[1].dC[0]);
+  q.dC[1] = make_float2(bp[0].dC[1], bp[1].dC[1]);
+  q.dC[2] = make_float2(bp[0].dC[2], bp[1].dC[2]);
+  q.dws = make_float2(bp[0].dws, bp[1].dws);
+  q.tail = make_float2(bp[0].tail, bp[1].tail);
+  q.Yh = make_float2(bp[0].Yh, bp[1].Yh);
+  q.Yc = make_float2(bp[0].Yc, bp[1].Yc);
+  q.S = f2(0.f);
+  q.g1 = make_float2(bp[0].r.gam[1], bp[1].r.gam[1]);
+  q.g2 = make_float2(bp[0].r.gam[2], bp[1].r.gam[2]);
+  q.g3 = make_float2(bp[0].r.gam[3], bp[1].r.gam[3]);
+  __syncthreads();
+  const int my_max = max(bp[0].n_stop, bp[1].n_stop);
+  if (my_max > 0) atomicMax(&s_max, my_max);
+  __syncthreads();
+  const int64_t lim = beg + (int64_t)s_max;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // back to front: chunks from the last one any pixel of the tile includes down to the first
+  for (int64_t base = beg + ((lim - beg - 1) / kChunkB) * kChunkB; base >= beg && lim > beg; base -= kChunkB) {
+    const int cn = (int)min((int64_t)kChunkB, lim - base);
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += 128) {
+      EntryF &e = sm[j];
+      stage_entry_f<kRot>(sc, c, entries[base + j], e, vrange);
+      float2 *pp = spp[j];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) pp[m] = f2(e.p.ws[m]);
+#pragma unroll
+      for (int m = 0; m < 9; ++m) pp[4 + m] = f2(e.p.wc[m]);
+#pragma unroll
+      for (int m = 0; m < 12; ++m) pp[13 + m] = f2(e.p.wsh[m]);
+      const float ha = 0.5f * e.a;
+      pp[25] = f2(e.a);
+      pp[26] = f2(e.inv_b);
+      pp[27] = f2(ha);
+      pp[28] = f2(ha * e.inv_b);
+    }
+    __syncthreads();
+    prefetch_prev(sc, entries, base - kChunkB, beg, kChunkB);
+    const int jb = (int)(base - beg);
+    uint32_t wb0 = 0u, wb1 = 0u;  // hit words of this chunk
+    if (in[0] && jb < bp[0].n_stop) wb0 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + threadIdx.x);
+    if (in[1] && jb < bp[1].n_stop) wb1 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + threadIdx.x + 128);
+    for (int j = cn - 1; j >= 0; --j) {
+      const bool h0 = (wb0 >> j) & 1u, h1 = (wb1 >> j) & 1u;
+      if (!__any_sync(0xffffffffu, h0 || h1)) {  // no pixel of this warp includes entry j
+        if (lane < kGradStride) red[j][warp][lane] = 0.f;
+        continue;
+      }
+      const EntryF &e = sm[j];
+      Hit2 hh;
+      hh.x[0] = hh.x[1] = hh.x[2] = f2(0.f);
+      hh.delta = hh.dq = f2(0.f);
+      if (kRot) hh.gm[0] = hh.gm[1] = hh.gm[2] = hh.gm[3] = f2(0.f);
+      bool act = false;
+      if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + threadIdx.x * 3, hh, 0);
+      if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + (threadIdx.x + 128) * 3, hh, 1);
+      float tot = 0.0f;
+      if (__any_sync(0xffffffffu, act)) {
+        float g[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) g[k] = 0.f;
+        bwd_segment2<kRot, sdf, kDepth>(spp[j], q, hh, g);
+        // warp reduction: transpose through shared memory, lane k sums component k
+        float4 *row = reinterpret_cast<float4 *>(&xp[warp][lane][0]);
+#pragma unroll
+        for (int m = 0; m < 7; ++m) row[m] = make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]);
+        __syncwarp();
+        if (lane < kGradStride) {
+          float t0 = xp[warp][0][lane], t1 = xp[warp][1][lane], t2 = xp[warp][2][lane], t3 = xp[warp][3][lane];
+#pragma unroll
+          for (int rr = 4; rr < 32; rr += 4) {
+            t0 += xp[warp][rr][lane];
+            t1 += xp[warp][rr + 1][lane];
+            t2 += xp[warp][rr + 2][lane];
+            t3 += xp[warp][rr + 3][lane];
+          }
+          tot = (t0 + t1) + (t2 + t3);
+        }
+        __syncwarp();
+      }
+      if (lane < kGradStride) red[j][warp][lane] = tot;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < cn * kGradStride; t += 128) {
+      const int j = t / kGradStride, k = t - j * kGradStride;
+      const float sum = (red[j][0][k] + red[j][1][k]) + (red[j][2][k] + red[j][3][k]);
       if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
       else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
     }
@@ -1968,11 +2213,11 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
 #define SALF_LAUNCH_BWD(ROT, SDF, DEPTH)                                                                    \
   do {                                                                                                      \
     if (hitbits)                                                                                            \
-      k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH, true><<<n_tiles, threads_np, 0, st>>>(                  \
+      k_backward_hits<ROT, SDF, DEPTH><<<n_tiles, 128, 0, st>>>(                                             \
           *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, hitbits); \
     else                                                                                                    \
-      k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH, false><<<n_tiles, threads_np, 0, st>>>(                 \
-          *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, nullptr); \
+      k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH><<<n_tiles, threads_np, 0, st>>>(                        \
+          *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order);    \
   } while (0)
     if (rot) {
       if (sdf) SALF_LAUNCH_BWD(true, true, true); else SALF_LAUNCH_BWD(true, false, true);
