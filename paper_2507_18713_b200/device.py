@@ -50,6 +50,24 @@ class DeviceScene:
                                        device=self.device)
         self.flat = flat
 
+    def set_params(self, w_s, w_c, w_sh, log_a, log_b) -> "DeviceScene":
+        """Refresh the field parameters in place (geometry, rotations and the
+        octree stay): the host-side counterpart of salf_scene_refresh, for callers
+        that update NumPy parameter arrays between renders (reference optim.py)."""
+        n = self.n
+        if n == 0:
+            return self
+        aux = np.empty((n, 2), np.float64)
+        aux[:, 0] = np.exp(np.asarray(log_a, np.float64).reshape(n))
+        aux[:, 1] = 1.0 / np.exp(np.asarray(log_b, np.float64).reshape(n))
+        prm = np.zeros((n, _lib.PRM_STRIDE), np.float32)
+        prm[:, 0:4] = np.asarray(w_s).reshape(-1, 4)
+        prm[:, 4:13] = np.asarray(w_c).reshape(-1, 9)
+        prm[:, 13:25] = np.asarray(w_sh).reshape(-1, 12)
+        self.aux[:n, :2].copy_(torch.from_numpy(aux), non_blocking=False)
+        self.prm[:n].copy_(torch.from_numpy(prm), non_blocking=False)
+        return self
+
     @classmethod
     def from_arrays(cls, geo: torch.Tensor, aux: torch.Tensor, prm: torch.Tensor, n: int,
                     density_mode: str) -> "DeviceScene":

@@ -88,7 +88,8 @@ def _opts(background, stop_threshold, exact_color) -> _lib.RasterOptsT:
 def _static_device_scene(scene) -> DeviceScene:
     """The static voxel set on the device (actors are marched in their own frames)."""
     if isinstance(scene, Scene):
-        ds = DeviceScene.from_static(scene)
+        # a caller that keeps the static set resident (dropin.Backend) attaches it
+        ds = getattr(scene, "_b200_static", None) or DeviceScene.from_static(scene)
     else:
         ds = as_device_scene(scene)
     if ds.rot is not None:
@@ -151,7 +152,7 @@ def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: tor
                 rec = torch.empty((sub.numel(), 24), dtype=torch.float64, device=dev)
                 dsa = octrees.actor_scenes[ai]
                 _lib.check(lib.salf_shade_segments(_lib.ref(dsa.c_struct()), sub.numel(), so.data_ptr(),
-                                                   sd.data_ptr(), vid.contiguous().data_ptr(), t0.data_ptr(),
+                                                   sd.data_ptr(), vid.data_ptr(), t0.data_ptr(),
                                                    t1.data_ptr(), ai, goff, int(exact_color), rec.data_ptr(),
                                                    _lib.stream_ptr()), "actor segments")
                 recs.append(rec)
@@ -375,9 +376,10 @@ def lidar_backward(ret: LidarReturn, d_depth=None, *, features=None, head=None, 
         dd = dd + torch.where(valid, dz @ W[:, 8], torch.zeros_like(dd))
         fgrad = torch.zeros((max(ds.n, 1), 8), dtype=torch.float64, device=dev)
     sc, t = ds.c_struct(), ret.octree.c_struct()
+    dd = dd.contiguous()
     _lib.check(lib.salf_lidar_backward(_lib.ref(t), _lib.ref(sc), n, ret.origins.data_ptr(),
                                        ret.dirs.data_ptr(), _lib.ref(ret.opts), ret.saved.data_ptr(),
-                                       dd.contiguous().data_ptr(), _lib.ptr(f), _lib.ptr(dF),
+                                       dd.data_ptr(), _lib.ptr(f), _lib.ptr(dF),
                                        _lib.ptr(Facc), grad.data_ptr(), _lib.ptr(fgrad),
                                        _lib.stream_ptr()), "lidar_backward")
     return grad, (None if fgrad is None else fgrad[: ds.n]), hgrad
