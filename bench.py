@@ -711,6 +711,26 @@ def extras(ds, oc, args):
 
     out["c4_fisheye_rs_fps_S2M"] = 1e3 / _timeit(c4_frame, n=5)
     del ds2, oc2
+
+    # dynamic actors: two moving, yawing cars (~12k voxels each) on S1M; the C3
+    # sweep through integrate_rays' merge path (static march without early stop + actor frames on
+    # the device + merged composite, render_ray.py:161-239) and the C2 frame with the actors
+    # flattened at t (render_raster.py:63-89)
+    from paper_2507_18713_b200.scenes import with_moving_actors
+    sa = with_moving_actors(get_scene("S1M", "init"))
+    oca = RY.build_scene_octrees(sa)
+    lbt = gen_lidar_rays(lidar)  # per-ray time stamps over the scan period
+
+    def lidar_actors():
+        return RY.integrate_rays(sa, oca, lbt.origins, lbt.dirs, lbt.t_stamps, check_unit=False, check=False)
+
+    ms_a = _timeit(lidar_actors, n=5)
+    ms_r = _timeit(lambda: RR.rasterize_scene(sa, cam, 0.05), n=5)
+    out["actors"] = {"actors": len(sa.actors), "actor_voxels": int(sum(a.voxels.n for a in sa.actors)),
+                     "c3_lidar_sweeps_per_s": 1e3 / ms_a, "c3_lidar_ms": ms_a,
+                     "c2_raster_forward_fps_incl_flatten_upload": 1e3 / ms_r,
+                     "note": "S1M init + 2 moving cars; LiDAR via the merge path (no early stop with live "
+                             "actors, render_ray.py:175); raster flattens + uploads the posed scene per frame"}
     return out
 
 

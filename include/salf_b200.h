@@ -319,6 +319,16 @@ int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t *scene, in
  * Actor segments are marched with salf_march in each actor's canonical frame,
  * then shaded into 24-double records (t0, t1, t_mid, delta, x[3], s, e, sigma,
  * alpha, 1-alpha, c[3], a, 1/b, dir[3], owner, global voxel id, pad[2]). */
+/* Rays into an actor's canonical frame + the actor-box test, on the device
+ * (render_ray.py:180-190; octree.py:175-194): pose_idx[n] (int64, nullable =
+ * row 0) selects a row of poses (P x 12 f64: translation[3], row-major
+ * rotation[9]) -- the host evaluates Actor.pose_at once per DISTINCT timestamp
+ * of the batch; o_actor / d_actor (n x 3 f64) and hit[n] (uint8) out.
+ * half_extents: HOST pointer to 3 doubles. */
+int salf_actor_rays(int64_t n, const double *origins, const double *dirs, const int64_t *pose_idx,
+                    const double *poses, const double *half_extents, double *o_actor, double *d_actor,
+                    uint8_t *hit, void *stream);
+
 int salf_shade_segments(const salf_scene_t *scene, int64_t n, const double *seg_origin,
                         const double *seg_dir, const int64_t *seg_vid, const double *seg_t0,
                         const double *seg_t1, int32_t owner, int64_t vid_offset, int32_t exact_color,

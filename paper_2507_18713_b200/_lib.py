@@ -124,6 +124,7 @@ SIGNATURES = {
     "salf_voxel_geometry": (C.c_int, [C.c_int64, vp, vp, vp, C.c_double, vp, vp, vp, vp, vp]),
     "salf_octree_ancestor_keys": (C.c_int, [C.c_int64, vp, vp, C.c_int32, vp, vp, vp, vp]),
     "salf_octree_fill": (C.c_int, [C.c_int64, C.c_int64, vp, vp, vp, vp, vp]),
+    "salf_actor_rays": (C.c_int, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_shade_segments": (C.c_int, [vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int32, C.c_int64, C.c_int32,
                                       vp, vp]),
     "salf_ray_forward_merge": (C.c_int, [vp, vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -1302,6 +1302,67 @@ extern "C" int salf_lidar_backward(const salf_octree_t *tree, const salf_scene_t
   SALF_CATCH
 }
 
+// Rays into one actor's canonical frame (render_ray.py:180-190): per ray the
+// pose of its timestamp (pose table row pose_idx[i]: translation, then the
+// row-major rotation matrix R, evaluated by the host for the batch's distinct
+// timestamps with the reference's own NumPy), o_a = R^T (o - pos) and
+// d_a = R^T d in np.einsum("nji,nj->ni") order ((p0 + p1) + p2, plain products;
+// this file is compiled with --fmad=false), then ray_box_range against the
+// actor box +-half (octree.py:175-194: reciprocal multiply, zero-direction
+// override, NaN-propagating min / max) and the reference's hit rule
+// (t_out > max(t_in, 0)) & (max(t_in, 0) < t_max = inf).
+__global__ void k_actor_rays(int64_t n, const double *__restrict__ o, const double *__restrict__ d,
+                             const int64_t *__restrict__ pose_idx, const double *__restrict__ poses, double hx,
+                             double hy, double hz, double *__restrict__ o_a, double *__restrict__ d_a,
+                             uint8_t *__restrict__ hit) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double *P = poses + 12 * (pose_idx ? pose_idx[i] : 0);
+  const double v[3] = {__dsub_rn(o[3 * i], P[0]), __dsub_rn(o[3 * i + 1], P[1]), __dsub_rn(o[3 * i + 2], P[2])};
+  const double w[3] = {d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+  const double *R = P + 3;
+  const double half[3] = {hx, hy, hz};
+  double oa[3], da[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    oa[k] = __dadd_rn(__dadd_rn(__dmul_rn(R[k], v[0]), __dmul_rn(R[3 + k], v[1])), __dmul_rn(R[6 + k], v[2]));
+    da[k] = __dadd_rn(__dadd_rn(__dmul_rn(R[k], w[0]), __dmul_rn(R[3 + k], w[1])), __dmul_rn(R[6 + k], w[2]));
+    o_a[3 * i + k] = oa[k];
+    d_a[3 * i + k] = da[k];
+  }
+  double t_in = 0.0, t_out = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double nk, fk;
+    if (da[k] == 0.0) {
+      const bool inside = (oa[k] >= -half[k]) && (oa[k] <= half[k]);
+      nk = inside ? -INFINITY : INFINITY;
+      fk = inside ? INFINITY : -INFINITY;
+    } else {
+      const double inv = 1.0 / da[k];
+      const double ta = __dmul_rn(__dsub_rn(-half[k], oa[k]), inv), tb = __dmul_rn(__dsub_rn(half[k], oa[k]), inv);
+      nk = npmin(ta, tb);
+      fk = npmax(ta, tb);
+    }
+    t_in = k ? npmax(t_in, nk) : nk;
+    t_out = k ? npmin(t_out, fk) : fk;
+  }
+  const double t0 = npmax(t_in, 0.0);
+  hit[i] = (t_out > t0) && (t0 < INFINITY);
+}
+
+extern "C" int salf_actor_rays(int64_t n, const double *origins, const double *dirs, const int64_t *pose_idx,
+                               const double *poses, const double *half_extents, double *o_actor, double *d_actor,
+                               uint8_t *hit, void *stream) {
+  SALF_TRY {
+    if (n <= 0) return SALF_OK;
+    k_actor_rays<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n, origins, dirs, pose_idx, poses, half_extents[0], half_extents[1], half_extents[2], o_actor, d_actor, hit);
+    return check_cuda("salf_actor_rays");
+  }
+  SALF_CATCH
+}
+
 extern "C" int salf_shade_segments(const salf_scene_t *scene, int64_t n, const double *seg_origin,
                                    const double *seg_dir, const int64_t *seg_vid, const double *seg_t0,
                                    const double *seg_t1, int32_t owner, int64_t vid_offset, int32_t exact_color,

@@ -184,3 +184,65 @@ def load_device_scene(path, device=None) -> DeviceScene:
     ds = DeviceScene.from_arrays(geo, aux, prm, count, meta.get("density_mode", "sdf"))
     ds.params, ds.level, ds.ijk, ds.bounds, ds.meta = params[:count], level[:count], ijk[:count], bounds, meta
     return ds
+
+
+_IDENTITY_ROT: dict = {}
+
+
+def _identity_rot(n: int, device) -> torch.Tensor:
+    """(n, 9) identity rotations (static rows of a composed scene), grown and cached per device."""
+    t = _IDENTITY_ROT.get(str(device))
+    if t is None or t.shape[0] < n:
+        t = torch.eye(3, dtype=torch.float64, device=device).reshape(1, 9).repeat(max(n, 1), 1)
+        _IDENTITY_ROT[str(device)] = t
+    return t[:n]
+
+
+def static_device_scene(scene: Scene, device=None) -> DeviceScene:
+    """The static set of `scene` on the device, uploaded once per set: cached on
+    the Scene object and keyed by the identity of its arrays (densification
+    builds new arrays).  Parameters updated IN PLACE on the host are not seen --
+    call `scene.__dict__.pop("_b200_static", None)` (the reference drop-in,
+    dropin.py, refreshes them on every call instead)."""
+    v = scene.static
+    key = tuple(id(a) for a in (v.level, v.ijk, v.rotation, v.w_s, v.w_c, v.w_sh, v.log_a, v.log_b))
+    cached = scene.__dict__.get("_b200_static")
+    if cached is not None and scene.__dict__.get("_b200_static_key", key) == key:
+        return cached
+    ds = DeviceScene.from_static(scene, device)
+    scene.__dict__["_b200_static"] = ds
+    scene.__dict__["_b200_static_key"] = key
+    return ds
+
+
+def composed_device_scene(scene: Scene, t_stamp: float = 0.0, device=None) -> DeviceScene:
+    """flatten_scene (render_raster.py:63-89) with the static set resident: only
+    the actor voxels posed at t (host NumPy, the reference's own expressions)
+    are uploaded and appended behind the static rows; static rows get identity
+    rotations so the kernels' per-entry rotation test sees them as axis-aligned."""
+    st = static_device_scene(scene, device)
+    live = [a for a in scene.actors if a.voxels.n]
+    if not live:
+        return st
+    from .scene import quat_multiply, quat_to_matrix
+    centers, edges, rots, ws, wc, wsh, la, lb = [], [], [], [], [], [], [], []
+    for actor in live:
+        pos, quat = actor.pose_at(np.asarray(t_stamp))
+        rmat = quat_to_matrix(quat)
+        centers.append(actor.voxels.centers() @ rmat.T + pos)
+        edges.append(actor.voxels.edges())
+        rots.append(quat_multiply(quat, actor.voxels.rotation))
+        ws.append(actor.voxels.w_s)
+        wc.append(actor.voxels.w_c)
+        wsh.append(actor.voxels.w_sh)
+        la.append(actor.voxels.log_a)
+        lb.append(actor.voxels.log_b)
+    cat = np.concatenate
+    da = DeviceScene(FlatVoxels(cat(centers), cat(edges), cat(rots), cat(ws), cat(wc), cat(wsh), cat(la), cat(lb),
+                                scene.density_mode), st.device)
+    n_s = st.n
+    out = DeviceScene.from_arrays(torch.cat([st.geo[:n_s], da.geo[: da.n]]), torch.cat([st.aux[:n_s], da.aux[: da.n]]),
+                                  torch.cat([st.prm[:n_s], da.prm[: da.n]]), n_s + da.n, scene.density_mode)
+    rot_a = da.rot if da.rot is not None else _identity_rot(da.n, st.device)
+    out.rot = torch.cat([_identity_rot(n_s, st.device), rot_a[: da.n]]).contiguous()
+    return out

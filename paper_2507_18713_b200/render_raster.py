@@ -286,8 +286,12 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
 def rasterize_scene(scene: Scene, cam: CameraModel, t_stamp: float = 0.0, *,
                     background=(0.0, 0.0, 0.0), tile: int = TILE_SIZE,
                     near: float = NEAR_PLANE) -> Framebuffer:
-    """render_raster.py:304-308."""
-    return rasterize(flatten_scene(scene, t_stamp), cam, background=background, tile=tile, near=near)
+    """render_raster.py:304-308: the scene flattened at t.  The static set stays
+    resident between calls (device.static_device_scene); only the posed actor
+    voxels are uploaded (device.composed_device_scene)."""
+    from .device import composed_device_scene
+    _require_pinhole(cam)
+    return rasterize(composed_device_scene(scene, t_stamp), cam, background=background, tile=tile, near=near)
 
 
 def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor | None = None,

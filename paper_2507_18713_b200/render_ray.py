@@ -88,8 +88,9 @@ def _opts(background, stop_threshold, exact_color) -> _lib.RasterOptsT:
 def _static_device_scene(scene) -> DeviceScene:
     """The static voxel set on the device (actors are marched in their own frames)."""
     if isinstance(scene, Scene):
-        # a caller that keeps the static set resident (dropin.Backend) attaches it
-        ds = getattr(scene, "_b200_static", None) or DeviceScene.from_static(scene)
+        # resident between calls (device.static_device_scene; dropin.Backend attaches its own)
+        from .device import static_device_scene
+        ds = static_device_scene(scene)
     else:
         ds = as_device_scene(scene)
     if ds.rot is not None:
@@ -101,54 +102,51 @@ def _octree_of(octrees) -> OctreeBuffer:
     return octrees.static if isinstance(octrees, SceneOctrees) else octrees
 
 
-def _np_ray_box(o, d, bmin, bmax):
-    """ray_box_range (octree.py:175-194) on host arrays (actor box tests)."""
-    with np.errstate(divide="ignore", invalid="ignore"):
-        inv = 1.0 / d
-        ta = (bmin - o) * inv
-        tb = (bmax - o) * inv
-    near = np.minimum(ta, tb)
-    far = np.maximum(ta, tb)
-    zero = d == 0.0
-    inside = (o >= bmin) & (o <= bmax)
-    near = np.where(zero, np.where(inside, -np.inf, np.inf), near)
-    far = np.where(zero, np.where(inside, np.inf, -np.inf), far)
-    return near.max(axis=-1), far.min(axis=-1)
-
-
 def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: torch.Tensor, t_stamps,
                     dev, exact_color: bool):
     """Actor segments of every ray (render_ray.py:178-197): rays moved into each
-    actor's canonical frame at their timestamps (poses, transforms and box tests
-    on the host with the reference's own NumPy expressions), marched on that
-    actor's octree on the device and shaded into records; returned sorted by the
-    reference's lexsort((vid, owner, t0, ray)) as a CSR over rays."""
+    actor's canonical frame at their timestamps and tested against its box on
+    the device (salf_actor_rays, NumPy's einsum order), marched on that actor's
+    octree on the device and shaded into records; returned sorted by the
+    reference's lexsort((vid, owner, t0, ray)) as a CSR over rays.  The host
+    evaluates Actor.pose_at (lerp + slerp, scene.py:316-331, the reference's
+    NumPy expressions) once per DISTINCT timestamp of the batch -- one per
+    rolling-shutter row or LiDAR azimuth step -- and uploads that table only."""
     from .scene import quat_to_matrix
     lib = _lib.load()
     n = o.shape[0]
-    o_np, d_np = o.cpu().numpy(), d.cpu().numpy()
-    if isinstance(t_stamps, torch.Tensor):  # only actor poses need the timestamps (host side)
-        t_stamps = t_stamps.detach().cpu().numpy()
-    ts = np.broadcast_to(np.asarray(0.0 if t_stamps is None else t_stamps, np.float64), (n,))
+    if t_stamps is None:
+        uniq, inv = np.zeros(1), None
+    else:
+        ts_t = (t_stamps if isinstance(t_stamps, torch.Tensor) else
+                torch.as_tensor(np.broadcast_to(np.asarray(t_stamps, np.float64), (n,)).copy()))
+        ts_t = ts_t.to(device=dev, dtype=torch.float64).reshape(-1).expand(n).contiguous()
+        u, inv = torch.unique(ts_t, return_inverse=True)
+        uniq, inv = u.cpu().numpy(), inv.contiguous()
+    o_a = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    d_a = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    hit = torch.empty(n, dtype=torch.uint8, device=dev)
     recs, rays, offsets, goff = [], [], [], 0
     for ai, actor in enumerate(scene.actors):
         offsets.append((actor.actor_id, goff, actor.voxels.n))
         if actor.voxels.n == 0:
             continue
-        pos, quat = actor.pose_at(ts)
-        rmat = quat_to_matrix(quat)
-        o_a = np.einsum("nji,nj->ni", rmat, o_np - pos)
-        d_a = np.einsum("nji,nj->ni", rmat, d_np)
-        half = actor.extents / 2.0
-        t_in, t_out = _np_ray_box(o_a, d_a, -half, half)
-        t0c = np.maximum(t_in, 0.0)
-        hit_ids = np.flatnonzero((t_out > t0c) & (t0c < np.inf))
-        if hit_ids.size:
+        pos, quat = actor.pose_at(uniq)
+        table = np.concatenate([np.asarray(pos, np.float64).reshape(-1, 3),
+                                quat_to_matrix(quat).reshape(-1, 9)], axis=1)
+        table_d = torch.as_tensor(np.ascontiguousarray(table), device=dev)
+        half = np.ascontiguousarray(actor.extents / 2.0, np.float64)
+        if n:
+            _lib.check(lib.salf_actor_rays(n, o.data_ptr(), d.data_ptr(), _lib.ptr(inv), table_d.data_ptr(),
+                                           half.ctypes.data, o_a.data_ptr(), d_a.data_ptr(), hit.data_ptr(),
+                                           _lib.stream_ptr()), "integrate_rays (actor rays)")
+        hit_ids = torch.nonzero(hit[:n]).reshape(-1)
+        if hit_ids.numel():
             sub, vid, t0, t1 = march_segments(octrees.actors[ai], o_a[hit_ids], d_a[hit_ids])
             if sub.numel():
-                ray = torch.as_tensor(hit_ids, device=dev)[sub]
-                so = torch.as_tensor(o_a, device=dev)[ray].contiguous()
-                sd = torch.as_tensor(d_a, device=dev)[ray].contiguous()
+                ray = hit_ids[sub]
+                so = o_a[ray].contiguous()
+                sd = d_a[ray].contiguous()
                 rec = torch.empty((sub.numel(), 24), dtype=torch.float64, device=dev)
                 dsa = octrees.actor_scenes[ai]
                 _lib.check(lib.salf_shade_segments(_lib.ref(dsa.c_struct()), sub.numel(), so.data_ptr(),

@@ -307,3 +307,31 @@ def get_scene(name: str, regime: str = "init", cache: bool = True) -> Scene:
             shutil.rmtree(tmp, ignore_errors=True)  # another process published first
         return load_scene(d)[0]  # f32 round trip, identical to what the reference loads
     return scene
+
+
+def with_moving_actors(scene: Scene, seed: int = 7, n_actors: int = 2, cell: float = 0.1) -> Scene:
+    """The scene plus `n_actors` rigid car-sized actors (4.4 x 1.8 x 1.5 m box of
+    `cell`-edge voxels, ~12k each, init-regime random fields) driving through the
+    C3 LiDAR's view over t in [0, 1] s with a yaw change -- the dynamic-actor
+    workload of the bench (reference scene.py:290-331 Actor, render_ray.py:161-239)."""
+    from .scene import Actor, make_actor_bounds
+    rng = np.random.default_rng(seed)
+    extents = np.array([4.4, 1.8, 1.5])
+    dims = np.round(extents / cell).astype(int)
+    actors = []
+    for k in range(n_actors):
+        b = make_actor_bounds(extents, cell, 1)
+        cells = np.stack(np.meshgrid(*[np.arange(m) for m in dims], indexing="ij"), -1).reshape(-1, 3)
+        v = SparseVoxelSet(b, budget=cells.shape[0] + 10)
+        n = cells.shape[0]
+        v.set_arrays(np.zeros(n, np.uint8), cells.astype(np.int32),
+                     rng.uniform(-1, 1, (n, 4)) / np.sqrt(3.0), rng.uniform(-1, 1, (n, 3, 3)) / np.sqrt(3.0),
+                     rng.uniform(-0.5, 0.5, (n, 3, 4)), np.full(n, np.log(2.0)), np.full(n, np.log(0.2)))
+        y = 3.0 if k % 2 == 0 else -3.5
+        p0, p1 = np.array([6.0 + 4 * k, y, 0.8]), np.array([16.0 + 4 * k, y, 0.8])
+        yaw0, yaw1 = 0.0, 0.3 * (1 if k % 2 == 0 else -1)
+        q = lambda a: np.array([np.cos(a / 2), 0.0, 0.0, np.sin(a / 2)])
+        actors.append(Actor(f"car{k}", extents, v, np.array([0.0, 1.0]), np.stack([p0, p1]),
+                            np.stack([q(yaw0), q(yaw1)])))
+    return Scene(bounds=scene.bounds, static=scene.static, actors=actors, density_mode=scene.density_mode,
+                 inner_aabb=scene.inner_aabb)
