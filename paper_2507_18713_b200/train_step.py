@@ -19,9 +19,10 @@ import torch
 
 from . import render_raster as RR
 from . import render_ray as RY
+from .backward import l1_color_seed
 from .parallel import allreduce_, allreduce_grad_, band_camera
 from .render_ray import raise_for_status
-from .sensors import gen_lidar_rays
+from .sensors import CameraModel, gen_lidar_rays
 
 
 @dataclass
@@ -32,25 +33,35 @@ class ForwardState:
     losses: torch.Tensor  # [sum |C - gt|, sum |D - gt|] of this rank
 
 
+def color_terms(sensors) -> int:
+    """Global normaliser of the cameras' L1 colour loss (losses.py:29-30): every
+    pixel of every camera counts, 3 channels each -- known without a reduction."""
+    return sum(3 * s.width * s.height for s in sensors if isinstance(s, CameraModel))
+
+
 def rig_forward(ds, octree, sensors, targets, items, check: bool = True) -> ForwardState:
     """Forward of this rank's work items; targets[i]: (H, W, 3) gt colour for
-    cameras, (beams * steps,) gt range for LiDARs.  `check`: raise like the
-    reference's marcher for LiDAR rays that hit the round cap or leave the
-    root (one host sync over all blocks, after every launch is queued)."""
+    cameras, (beams * steps,) gt range for LiDARs.  Camera bands get their
+    colour seeds in the same pass (the fused salf_l1_seed kernel: sign(C - gt)
+    over the GLOBAL colour count, and |C - gt| summed); LiDAR seeds wait for the
+    all-reduced return count.  `check`: raise like the reference's marcher for
+    LiDAR rays that hit the round cap or leave the root (one host sync over all
+    blocks, after every launch is queued)."""
     dev = ds.device
     counts = torch.zeros(2, dtype=torch.float64, device=dev)
     losses = torch.zeros(2, dtype=torch.float64, device=dev)
     saved = []
     statuses = []
+    n_color = color_terms(sensors)
     for it in items:
         s = sensors[it.sensor]
         if it.kind == "raster_band":
             fb, st = RR.rasterize(ds, band_camera(s, it.lo, it.hi), return_state=True)
             gt = torch.as_tensor(targets[it.sensor], device=dev)[it.lo:it.hi]
-            diff = fb.color.double() - gt.double()
-            counts[0] += diff.numel()
-            losses[0] += diff.abs().sum()
-            saved.append((st, diff))
+            dc, lsum = l1_color_seed(fb.color, gt, None, count=n_color)
+            counts[0] += 3 * fb.color.shape[0] * fb.color.shape[1]
+            losses[0] += lsum
+            saved.append((st, dc))
         else:
             # LiDAR block: the depth-only sweep kernel (no colour field), replayed by lidar_backward
             rays = gen_lidar_rays(s, device=dev)
@@ -72,15 +83,14 @@ def rig_forward(ds, octree, sensors, targets, items, check: bool = True) -> Forw
 
 def rig_backward(fs: ForwardState, grad: torch.Tensor, global_counts: torch.Tensor,
                  depth_weight: float = 10.0) -> torch.Tensor:
-    """L1 seeds normalised by the global counts, backward into `grad` (M, 27)."""
-    n_c = global_counts[0].clamp_min(1.0)
+    """Backward into `grad` (M, 27): camera bands with the seeds of the forward,
+    LiDAR blocks with L1 seeds over the global return count."""
     n_d = global_counts[1].clamp_min(1.0)
-    for it, (st, diff) in zip(fs.items, fs.saved):
+    for it, (st, seed) in zip(fs.items, fs.saved):
         if it.kind == "raster_band":
-            dc = torch.sign(diff) / n_c
-            RR.rasterize_backward(st, dc, None, grad, as_dict=False)  # cameras carry the colour loss only
+            RR.rasterize_backward(st, seed, None, grad, as_dict=False)  # cameras carry the colour loss only
         else:
-            dd = depth_weight * torch.sign(diff) / n_d
+            dd = depth_weight * torch.sign(seed) / n_d
             RY.lidar_backward(st, dd, grad=grad)  # depth-only seeds: no colour terms
     return grad
 

@@ -100,6 +100,38 @@ def test_rig_step_matches_oracle_and_sharding_is_exact():
     assert grads_close_normwise(grads_to_dict(g2), grads_to_dict(grad)) < 1e-6
 
 
+def test_rig_step_two_processes_gloo(tmp_path):
+    """C5 step as two processes (gloo, both on cuda:0): each rank rasterizes /
+    marches its share, the counts, gradient rows and losses are all-reduced
+    inside rig_step (parallel.allreduce_grad_, f64 transport), and rank 0's
+    buffer equals the one-process step and the oracle composition."""
+    import socket
+    import torch.multiprocessing as mp
+    from _rig_worker import run
+    from paper_2507_18713_b200 import render_ray as RY
+    from paper_2507_18713_b200.device import DeviceScene, grads_to_dict
+    from paper_2507_18713_b200.parallel import split_work
+    from paper_2507_18713_b200.train_step import rig_step
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "rank0.npz")
+    mp.start_processes(run, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    r = np.load(out)
+    sc = load_golden_scene("rand300")
+    ds = DeviceScene.from_scene(sc)
+    oc = RY.build_scene_octrees(sc)
+    sensors = _rig()
+    targets = _targets(sensors)
+    grad = torch.zeros((ds.n, 27), dtype=torch.float64, device="cuda")
+    losses, counts = rig_step(ds, oc, sensors, targets, split_work(sensors, 1), grad)
+    np.testing.assert_array_equal(r["counts"], counts.cpu().numpy())
+    np.testing.assert_allclose(r["losses"], losses.cpu().numpy(), rtol=1e-12)
+    assert grads_close_normwise(grads_to_dict(torch.as_tensor(r["grad"])), grads_to_dict(grad)) < 1e-12
+    want, mag = _oracle_grad(sc, sensors, targets)
+    assert_grads(grads_to_dict(torch.as_tensor(r["grad"])), want, mag)
+
+
 def test_adam_and_regularisers_match_reference(golden):
     """Adam (optim.py:48-62) and eikonal / empty / LiDAR-opacity regularisers
     (losses.py:49-249) on the device vs the reference's own outputs."""
