@@ -291,6 +291,7 @@ def rasterize_scene(scene: Scene, cam: CameraModel, t_stamp: float = 0.0, *,
     voxels are uploaded (device.composed_device_scene)."""
     from .device import composed_device_scene
     _require_pinhole(cam)
+    _lib.load()  # no GPU / library: fail here, before any device allocation (no CPU fallback)
     return rasterize(composed_device_scene(scene, t_stamp), cam, background=background, tile=tile, near=near)
 
 
