@@ -110,10 +110,10 @@ int salf_device_sm_count(void);
  * cull_and_bin (:143-176): rect (M x 4: umin, vmin, umax, vmax; NaN if
  * culled), z_center, culled, the reference tile span `span_ref` and the
  * tightened render span `span_fit` (M x 4 int32: tx0, ty0, tx1, ty1; empty
- * when tx0 > tx1), 64-bit orderable depth keys, and `vrange` (M int32:
- * conservative footprint pixel rows lo | hi << 16, widened by one pixel;
- * lo > hi when empty) that the composite / backward use to skip entries a
- * warp's pixel rows cannot hit.  Any output may be NULL.  (The composite and
+ * when tx0 > tx1), 64-bit orderable depth keys, and `vrange` (M x 2 int32:
+ * the conservative footprint's pixel rows, then columns, each lo | hi << 16,
+ * widened by one pixel; lo > hi when empty) that the composite uses to skip
+ * entries a warp's 8 x 4 pixel block cannot hit.  Any output may be NULL.  (The composite and
  * backward also take an optional `tile_order`: the launch order of the
  * tiles, e.g. by list length descending; NULL = row-major.) */
 int salf_project_voxels(const salf_scene_t *scene, const salf_camera_t *cam, double near,

@@ -128,7 +128,10 @@ __global__ void k_project(int64_t n, const double4 *__restrict__ geo, const doub
   if (span_ref) span_ref[i] = sref;
   // conservative footprint rows widened by one pixel (front voxels: the
   // corner hull; straddlers: the near-plane-clipped hull below)
-  if (vrange && !straddle) vrange[i] = culled ? 1 : pack_rows(vmin - 1.0, vmax + 1.0, c.height);
+  if (vrange && !straddle) {
+    vrange[2 * i] = culled ? 1 : pack_rows(vmin - 1.0, vmax + 1.0, c.height);
+    vrange[2 * i + 1] = culled ? 1 : pack_rows(umin - 1.0, umax + 1.0, c.width);  // columns, same packing
+  }
   if (span_fit || vrange) {
     int4 sfit = sref;
     if (straddle && sref.x <= sref.z) {
@@ -158,9 +161,12 @@ __global__ void k_project(int64_t n, const double4 *__restrict__ geo, const doub
       int4 t;
       span_from_rect(fu0 - 1.0, fv0 - 1.0, fu1 + 1.0, fv1 + 1.0, c, false, t);
       sfit = t;
-      if (vrange) vrange[i] = pack_rows(fv0 - 1.0, fv1 + 1.0, c.height);
+      if (vrange) {
+        vrange[2 * i] = pack_rows(fv0 - 1.0, fv1 + 1.0, c.height);
+        vrange[2 * i + 1] = pack_rows(fu0 - 1.0, fu1 + 1.0, c.width);
+      }
     } else if (straddle && vrange) {
-      vrange[i] = 1;  // no pixel
+      vrange[2 * i] = vrange[2 * i + 1] = 1;  // no pixel
     }
     if (span_fit) span_fit[i] = sfit;
   }
@@ -812,18 +818,21 @@ struct __align__(16) EntryF {
   double half;      // 0.5 * edge (fp64, for the reference slab test fallback)
   float oh[3], ol[3];  // o = oh + ol (two-float split)
   int vlo, vhi;        // conservative footprint pixel rows (vlo > vhi: none)
+  int ulo, uhi;        // and columns
 };
 
 template <bool kRot>
 __device__ __forceinline__ void stage_entry_f(const salf_scene_t &sc, const PinholeDev &c, int32_t vid, EntryF &e,
                                               const int32_t *__restrict__ vrange) {
   if (vrange) {
-    const int32_t r = __ldg(vrange + vid);
-    e.vlo = r & 0xffff;
-    e.vhi = (r >> 16) & 0xffff;
+    const int2 r = __ldg(reinterpret_cast<const int2 *>(vrange) + vid);
+    e.vlo = r.x & 0xffff;
+    e.vhi = (r.x >> 16) & 0xffff;
+    e.ulo = r.y & 0xffff;
+    e.uhi = (r.y >> 16) & 0xffff;
   } else {
-    e.vlo = 0;
-    e.vhi = 0x7fff;
+    e.vlo = e.ulo = 0;
+    e.vhi = e.uhi = 0x7fff;
   }
   const double4 g = ldg_d4(sc.geo + 4 * (int64_t)vid);
   const double2 ab = __ldg(reinterpret_cast<const double2 *>(sc.aux + 4 * (int64_t)vid));
@@ -1341,7 +1350,13 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   // heaviest tiles first (tile_order: tiles by list length, descending) -> no ragged last wave
   const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
-  const int lx = threadIdx.x % c.tile, ly = threadIdx.x / c.tile;
+  // 16 x 16 tiles: warp w shades the 8 x 4 pixel block (w & 1, w >> 1) of the tile, so the
+  // per-entry footprint test below culls on columns as well as rows; other tile sizes: rows
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool blocks = c.tile == 16;
+  const int lx = blocks ? (wid & 1) * 8 + (lane & 7) : threadIdx.x % c.tile;
+  const int ly = blocks ? (wid >> 1) * 4 + (lane >> 3) : threadIdx.x / c.tile;
+  const int pslot = ly * c.tile + lx;  // pixel slot of the hit words (the backward's slot order)
   const int px = tx * c.tile + lx, py = ty * c.tile + ly;
   const bool inside = px < c.width && py < c.height && threadIdx.x < c.tile * c.tile;
   const int64_t beg = offsets[tile_id], end = offsets[tile_id + 1];
@@ -1365,9 +1380,20 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   bool alive = inside, flag = false;
   int n_stop = (int)(end - beg), n_inc = 0;
   const int nthreads = blockDim.x;
-  // pixel rows this warp covers (for the per-entry footprint test)
-  const int wfirst = threadIdx.x & ~31, wlast = min(wfirst + 31, c.tile * c.tile - 1);
-  const int wr0 = ty * c.tile + wfirst / c.tile, wr1 = ty * c.tile + wlast / c.tile;
+  // pixel rows / columns this warp covers (for the per-entry footprint test)
+  int wr0, wr1, wc0, wc1;
+  if (blocks) {
+    wr0 = ty * 16 + (wid >> 1) * 4;
+    wr1 = wr0 + 3;
+    wc0 = tx * 16 + (wid & 1) * 8;
+    wc1 = wc0 + 7;
+  } else {
+    const int wfirst = threadIdx.x & ~31, wlast = min(wfirst + 31, c.tile * c.tile - 1);
+    wr0 = ty * c.tile + wfirst / c.tile;
+    wr1 = ty * c.tile + wlast / c.tile;
+    wc0 = tx * c.tile;
+    wc1 = wc0 + c.tile - 1;
+  }
 
   const int64_t hb_base = hit_word_base(beg, tile_id);
   for (int64_t base = beg; base < end; base += kChunk) {
@@ -1377,10 +1403,11 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
     __syncthreads();
     prefetch_next(sc, entries, base + kChunk, end, kChunk);
     if (alive) {
-      uint32_t hb0 = 0u, hb1 = 0u;  // included hits of this chunk (list positions base - beg + j)
+      uint64_t hbm = 0ull;  // included hits of this chunk (bit j: list position base - beg + j)
       for (int j = 0; j < cn; ++j) {
         const EntryF &e = sm[j];
-        if (e.vhi < wr0 || e.vlo > wr1) continue;  // footprint misses this warp's pixel rows (warp-uniform)
+        // footprint misses this warp's pixel rows or columns (warp-uniform)
+        if (e.vhi < wr0 || e.vlo > wr1 || e.uhi < wc0 || e.ulo > wc1) continue;
         const RayF *ray = &r;
         RayF rr;
         if (kRot && e.rot) {  // the pixel ray in the voxel's frame (render_raster.py:191-196)
@@ -1418,7 +1445,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           n_stop = (int)(base - beg) + j;
           break;
         }
-        if (j < 32) hb0 |= 1u << j; else hb1 |= 1u << (j - 32);
+        hbm |= 1ull << j;
         const float delta = u1 - u0;
         const float um = 0.5f * (u0 + u1);
         float x[3];
@@ -1454,9 +1481,9 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
         ++n_inc;
       }
       if (hitbits) {
-        uint32_t *hw = hitbits + hb_base + (int64_t)((base - beg) >> 5) * kHitSlots + threadIdx.x;
-        hw[0] = hb0;
-        if (cn > 32) hw[kHitSlots] = hb1;
+        uint32_t *hw = hitbits + hb_base + (int64_t)((base - beg) >> 5) * kHitSlots + pslot;
+        hw[0] = (uint32_t)hbm;
+        if (cn > 32) hw[kHitSlots] = (uint32_t)(hbm >> 32);
       }
     }
     if (!__syncthreads_or(alive)) break;
@@ -1748,6 +1775,16 @@ __device__ __forceinline__ float2 expm1_neg2(float2 x) {
   return make_float2(x.x > -0.25f ? small.x : big.x, x.y > -0.25f ? small.y : big.y);
 }
 
+#ifndef SALF_BWD_BLOCK
+#define SALF_BWD_BLOCK 1  // 8 x 8 pixel block per warp in the hit-word backward (0: 16 x 2 strips)
+#endif
+#ifndef SALF_BWD_XPCOL
+#define SALF_BWD_XPCOL 0  // 1: component-major warp reduction (A/B: 4.61 vs 4.59 ms, kept off)
+#endif
+
+constexpr int kXpRows = SALF_BWD_XPCOL ? 27 : 32, kXpCols = SALF_BWD_XPCOL ? 36 : 28;
+constexpr size_t kXpBytes = sizeof(float) * 4 * kXpRows * kXpCols;  // 4 warps
+
 // per-entry field constants, each duplicated (p, p) so a packed op reads it as
 // one 64-bit shared-memory operand: w_s 0..3, w_c 4..12, w_sh 13..24, a 25,
 // 1/b 26, a/2 27, (a/2)(1/b) 28
@@ -1886,7 +1923,9 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
   __shared__ EntryF sm[kChunkB];
   __shared__ __align__(16) float2 spp[kChunkB][kPP];
   __shared__ float red[kChunkB][kW][kGradStride];
-  __shared__ __align__(16) float xp[kW][32][28];
+  // warp-reduction scratch in dynamic shared memory (static + this exceed the 48 KB static limit)
+  extern __shared__ __align__(16) float xp_dyn[];
+  float(*xp)[kXpRows][kXpCols] = reinterpret_cast<float(*)[kXpRows][kXpCols]>(xp_dyn);
   __shared__ double s_iv[256 * 3];  // per pixel slot: fp64 1/d (bwd_pair64)
   __shared__ int s_max;
   const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
@@ -1899,9 +1938,21 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
   BwdPix bp[2];
   bool in[2];
   if (threadIdx.x == 0) s_max = 0;
+  // pixel slots of this thread's two pixels: 16 x 16 tiles with SALF_BWD_BLOCK give each warp an
+  // 8 x 8 block (lane -> column, two vertically adjacent rows), so a warp's pixels see nearly the
+  // same entries (more entries skipped by the whole warp, fewer idle lanes in the packed pass)
+  int slot[2];
+  const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5;
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    const int li = threadIdx.x + k * 128;
+    if (SALF_BWD_BLOCK && c.tile == 16)
+      slot[k] = ((wid0 >> 1) * 8 + (lane0 >> 3) * 2 + k) * 16 + (wid0 & 1) * 8 + (lane0 & 7);
+    else
+      slot[k] = threadIdx.x + k * 128;
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int li = slot[k];
     const int px = tx * c.tile + li % c.tile, py = ty * c.tile + li / c.tile;
     in[k] = li < npix && px < c.width && py < c.height;
     bp[k].n_stop = 0;
@@ -1966,8 +2017,8 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     prefetch_prev(sc, entries, base - kChunkB, beg, kChunkB);
     const int jb = (int)(base - beg);
     uint32_t wb0 = 0u, wb1 = 0u;  // hit words of this chunk
-    if (in[0] && jb < bp[0].n_stop) wb0 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + threadIdx.x);
-    if (in[1] && jb < bp[1].n_stop) wb1 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + threadIdx.x + 128);
+    if (in[0] && jb < bp[0].n_stop) wb0 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + slot[0]);
+    if (in[1] && jb < bp[1].n_stop) wb1 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + slot[1]);
     for (int j = cn - 1; j >= 0; --j) {
       const bool h0 = (wb0 >> j) & 1u, h1 = (wb1 >> j) & 1u;
       if (!__any_sync(0xffffffffu, h0 || h1)) {  // no pixel of this warp includes entry j
@@ -1980,15 +2031,37 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
       hh.delta = hh.dq = f2(0.f);
       if (kRot) hh.gm[0] = hh.gm[1] = hh.gm[2] = hh.gm[3] = f2(0.f);
       bool act = false;
-      if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + threadIdx.x * 3, hh, 0);
-      if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + (threadIdx.x + 128) * 3, hh, 1);
+      if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + slot[0] * 3, hh, 0);
+      if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + slot[1] * 3, hh, 1);
       float tot = 0.0f;
       if (__any_sync(0xffffffffu, act)) {
         float g[32];
 #pragma unroll
         for (int k = 0; k < 32; ++k) g[k] = 0.f;
         bwd_segment2<kRot, sdf, kDepth>(spp[j], q, hh, g);
-        // warp reduction: transpose through shared memory, lane k sums component k
+        // warp reduction through shared memory, lane k sums component k over the 32 lanes
+#if SALF_BWD_XPCOL
+        // component-major: lane r stores its 27 values down column r (conflict-free STS), lane k
+        // reads its component's 32 values as 8 LDS.128 (row pitch 36 floats: the 8 lanes of a
+        // 128-bit phase hit distinct banks) and sums them with packed adds
+        float *xc = &xp[warp][0][0];
+#pragma unroll
+        for (int m = 0; m < kGradStride; ++m) xc[m * 36 + lane] = g[m];
+        __syncwarp();
+        if (lane < kGradStride) {
+          const float4 *rowk = reinterpret_cast<const float4 *>(xc + lane * 36);
+          float2 a0 = f2(0.f), a1 = f2(0.f);
+#pragma unroll
+          for (int m = 0; m < 8; m += 2) {
+            const float4 u = rowk[m], v = rowk[m + 1];
+            a0 = add2(a0, add2(make_float2(u.x, u.y), make_float2(v.x, v.y)));
+            a1 = add2(a1, add2(make_float2(u.z, u.w), make_float2(v.z, v.w)));
+          }
+          const float2 a = add2(a0, a1);
+          tot = a.x + a.y;
+        }
+        __syncwarp();
+#else
         float4 *row = reinterpret_cast<float4 *>(&xp[warp][lane][0]);
 #pragma unroll
         for (int m = 0; m < 7; ++m) row[m] = make_float4(g[4 * m], g[4 * m + 1], g[4 * m + 2], g[4 * m + 3]);
@@ -2005,6 +2078,7 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
           tot = (t0 + t1) + (t2 + t3);
         }
         __syncwarp();
+#endif
       }
       if (lane < kGradStride) red[j][warp][lane] = tot;
     }
@@ -2212,10 +2286,16 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
     const bool depth = d_depth != nullptr;  // no depth seeds (colour-only loss): the depth term is dropped
 #define SALF_LAUNCH_BWD(ROT, SDF, DEPTH)                                                                    \
   do {                                                                                                      \
-    if (hitbits)                                                                                            \
-      k_backward_hits<ROT, SDF, DEPTH><<<n_tiles, 128, 0, st>>>(                                             \
+    if (hitbits) {                                                                                          \
+      static bool attr = false;                                                                             \
+      if (!attr) {                                                                                          \
+        cudaFuncSetAttribute(k_backward_hits<ROT, SDF, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)kXpBytes);                                                                \
+        attr = true;                                                                                        \
+      }                                                                                                     \
+      k_backward_hits<ROT, SDF, DEPTH><<<n_tiles, 128, kXpBytes, st>>>(                                      \
           *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, hitbits); \
-    else                                                                                                    \
+    } else                                                                                                  \
       k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH><<<n_tiles, threads_np, 0, st>>>(                        \
           *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order);    \
   } while (0)

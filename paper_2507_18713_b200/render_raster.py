@@ -112,7 +112,7 @@ def _project(ds: DeviceScene, cam: CameraModel, near: float, tile: int, want_rec
         span_ref=torch.empty((m, 4), dtype=torch.int32, device=dev),
         span_fit=torch.empty((m, 4), dtype=torch.int32, device=dev),
         zkey=torch.empty(m, dtype=torch.int64, device=dev),
-        vrange=torch.empty(m, dtype=torch.int32, device=dev),
+        vrange=torch.empty((m, 2), dtype=torch.int32, device=dev),  # footprint rows, columns
     )
     if want_rect:
         out["rect"] = torch.empty((m, 4), dtype=torch.float64, device=dev)
