@@ -21,9 +21,10 @@ and on rank 0 at N = 1: the C1 frame (configs[0]) on the GPU next to the
 reference algorithm over the whole frame on the host cores (not
 extrapolated), the C3 sweep on the host cores (whole sweep), the C2 CPU
 baseline (sampled tiles, extrapolated, labelled), the surface regime and
-C4.  `--impl reference` times the reference's CPU algorithm (the oracle port,
-oracle/salf_oracle.py -- the reference is pure Python and cannot travel to
-the GPU box) on the same C2 workload.
+C4.  `--impl reference` times the reference on the host cores on the same C2
+workload: the UNMODIFIED reference package installed in baseline/_ref
+(tools/install_reference.sh; it travels to the GPU box), kind "reference"; if
+it is missing, the oracle port (oracle/salf_oracle.py), kind "port".
 """
 
 from __future__ import annotations
@@ -66,6 +67,138 @@ def config_dict(regime: str, world: int, extra: dict | None = None) -> dict:
 # work (projection, pixel rays, octree) is done once per worker at start-up.
 
 _W = {}
+REF_PKG = ROOT / "baseline" / "_ref"  # the UNMODIFIED reference (tools/install_reference.sh); travels to the box
+
+
+def ref_available() -> bool:
+    return (REF_PKG / "salf" / "render_raster.py").is_file()
+
+
+def _ref_scene(sc):
+    """The reference's Scene over this package's scene arrays (no copies)."""
+    import salf.scene as RS
+    b = RS.SceneBounds(sc.bounds.aabb_min, sc.bounds.aabb_max, sc.bounds.base_edge, sc.bounds.max_levels)
+    v = RS.SparseVoxelSet(b, budget=max(sc.static.n + 10, 10))
+    src = sc.static
+    v.level, v.ijk, v.w_s, v.w_c, v.w_sh = src.level, src.ijk, src.w_s, src.w_c, src.w_sh
+    v.log_a, v.log_b, v.rotation = src.log_a, src.log_b, src.rotation
+    return RS.Scene(bounds=b, static=v, density_mode=sc.density_mode)
+
+
+def _ref_cam(c):
+    import salf.sensors as RS
+    return RS.CameraModel(kind=c.kind, width=c.width, height=c.height, fx=c.fx, fy=c.fy, cx=c.cx, cy=c.cy,
+                          position=c.position, quaternion=c.quaternion)
+
+
+def _cpu_init_ref(kind, regime):
+    """Worker state for the REFERENCE package's own functions (kind "reference")."""
+    sys.path.insert(0, str(REF_PKG))
+    import salf.render_raster as RR
+    import salf.render_ray as RY
+    from paper_2507_18713_b200 import configs
+    from paper_2507_18713_b200.scenes import get_scene
+    name = {"c1": "S20k", "c2": "S1M", "c3": "S1M"}[kind]
+    sc = _ref_scene(get_scene(name, regime if kind != "c1" else "init"))
+    _W.update(ref=True, scene=sc)
+    if kind in ("c1", "c2"):
+        _W["cam"] = _ref_cam(configs.c1_camera() if kind == "c1" else configs.c2_camera())
+        _W["flat"] = RR.flatten_scene(sc)
+        if kind == "c2":  # tile membership once per worker (render_raster.py:97-176 on the whole frame)
+            rmin, rmax, _, culled = RR.project_voxels(_W["flat"], _W["cam"])
+            with np.errstate(invalid="ignore"):
+                u0 = np.maximum(np.ceil(rmin[:, 0] - 0.5), 0.0)
+                u1 = np.minimum(np.floor(rmax[:, 0] - 0.5), _W["cam"].width - 1)
+                v0 = np.maximum(np.ceil(rmin[:, 1] - 0.5), 0.0)
+                v1 = np.minimum(np.floor(rmax[:, 1] - 0.5), _W["cam"].height - 1)
+            ok = ~culled & (u0 <= u1) & (v0 <= v1)
+            _W["span"] = (np.where(ok, u0 // 16, 1), np.where(ok, v0 // 16, 1), np.where(ok, u1 // 16, 0),
+                          np.where(ok, v1 // 16, 0))
+    else:
+        _W["oct"] = RY.build_scene_octrees(sc)
+        lid = configs.c3_lidar()
+        import salf.sensors as RSn
+        b = RSn.gen_lidar_rays(RSn.LidarModel(beam_elevations=lid.beam_elevations, azimuth_start=lid.azimuth_start,
+                                              azimuth_end=lid.azimuth_end, steps=lid.steps,
+                                              scan_period=lid.scan_period, position=lid.position,
+                                              quaternion=lid.quaternion, linear_velocity=lid.linear_velocity,
+                                              angular_velocity=lid.angular_velocity))
+        _W["o"], _W["d"], _W["t"] = b.origins, b.dirs, b.t_stamps
+
+
+def _ref_c2_tiles(tiles):
+    """The reference on one 16x16 C2 tile, forward AND backward: `rasterize`
+    (render_raster.py:201-301) of the tile (camera principal point shifted, the
+    voxels whose span covers the tile), then the raster gradient as SURVEY §8c
+    defines it -- the tile's hit pairs from the reference's `_pair_fields`
+    and field evaluators, `_composite` (render_ray.py:86-114) and
+    `backward_records` (backward.py:35-101).  Returns seconds."""
+    import dataclasses
+    from types import SimpleNamespace
+    import salf.backward as RB
+    import salf.render_raster as RR
+    import salf.render_ray as RY
+    import salf.scene as RS
+    flat, cam = _W["flat"], _W["cam"]
+    total = 0.0
+    for t in tiles:
+        tx, ty = t % 120, t // 120
+        sx0, sy0, sx1, sy1 = _W["span"]
+        sel = np.flatnonzero((sx0 <= tx) & (tx <= sx1) & (sy0 <= ty) & (ty <= sy1))
+        sub = RR.FlatVoxels(centers=flat.centers[sel], edges=flat.edges[sel], rotations=flat.rotations[sel],
+                            w_s=flat.w_s[sel], w_c=flat.w_c[sel], w_sh=flat.w_sh[sel], log_a=flat.log_a[sel],
+                            log_b=flat.log_b[sel], density_mode=flat.density_mode)
+        tcam = dataclasses.replace(cam, width=16, height=16, cx=cam.cx - 16 * tx, cy=cam.cy - 16 * ty)
+        t0 = time.perf_counter()
+        RR.rasterize(sub, tcam)
+        bins = RR.cull_and_bin(sub, tcam)
+        ent = bins.entries[bins.offsets[0]:bins.offsets[1]]
+        dirs = RR.gen_camera_rays(tcam).dirs
+        t_near = RR.NEAR_PLANE / (dirs @ tcam.rotation_matrix())[:, 2]
+        pp, vv = np.repeat(np.arange(256), ent.size), np.tile(ent, 256)
+        with np.errstate(over="ignore", invalid="ignore"):
+            o, d, t_in, t_out = RR._pair_fields(sub, np.broadcast_to(tcam.position, (pp.size, 3)), dirs[pp], vv)
+            t0p = np.maximum(np.maximum(t_in, t_near[pp]), 0.0)
+            hit = t_out > t0p + 1e-12
+            pp, vv, o, d, t0p, t1p = pp[hit], vv[hit], o[hit], d[hit], t0p[hit], t_out[hit]
+            tm = 0.5 * (t0p + t1p)
+            x = (o + tm[:, None] * d) / (0.5 * sub.edges[vv])[:, None]
+            s_f = RS.eval_sdf(x, sub.w_s[vv])
+            sig = RS.sdf_to_density(s_f, np.exp(sub.log_a[vv]), np.exp(sub.log_b[vv]))
+            alpha = RS.segment_opacity(sig, t1p - t0p)
+            color = RS.eval_color(x, d, sub.w_c[vv], sub.w_sh[vv])
+        bg = np.zeros(3)
+        (tb, inc, _w, oc, op, dep, ws, tf, gs) = RY._composite(pp, alpha, color, tm, 256, bg, RR.STOP_THRESHOLD)
+        rec = RY.RenderRecords(n_rays=256, ray=pp, owner=np.full(pp.size, -1, np.int32), vid=vv, t0=t0p, t1=t1p,
+                               x=x, omega=d, s_field=s_f, sigma=sig, alpha=alpha, color=color, t_before=tb,
+                               included=inc, out_color=oc, opacity=op, depth=dep, weight_sum=ws, t_final=tf,
+                               background=bg, density_mode=sub.density_mode, group_start=gs)
+        static = SimpleNamespace(w_s=sub.w_s, w_c=sub.w_c, w_sh=sub.w_sh, log_a=sub.log_a, log_b=sub.log_b)
+        RB.backward_records(rec, SimpleNamespace(static=static, actors=[], density_mode=sub.density_mode),
+                            np.full((256, 3), 1e-6), np.zeros(256))
+        total += time.perf_counter() - t0
+    return total
+
+
+def _ref_c1_band(rows):
+    """The reference's rasterize of tile rows [r0, r1) of the C1 frame (a band camera)."""
+    import dataclasses
+    import salf.render_raster as RR
+    cam = _W["cam"]
+    r0, r1 = rows
+    band = dataclasses.replace(cam, height=16 * (r1 - r0), cy=cam.cy - 16 * r0)
+    t0 = time.perf_counter()
+    fb = RR.rasterize(_W["flat"], band)
+    return time.perf_counter() - t0, fb.color
+
+
+def _ref_c3_block(lohi):
+    """The reference's integrate_rays depth (render_lidar_ranges' body, render_ray.py:297-306) of a ray block."""
+    import salf.render_ray as RY
+    lo, hi = lohi
+    t0 = time.perf_counter()
+    rec = RY.integrate_rays(_W["scene"], _W["oct"], _W["o"][lo:hi], _W["d"][lo:hi], _W["t"][lo:hi])
+    return time.perf_counter() - t0, rec.depth
 
 
 def _pin_threads():
@@ -142,8 +275,11 @@ class CpuPool:
         self.workers = workers or min(len(os.sched_getaffinity(0)), 64)
         get_scene({"c1": "S20k", "c2": "S1M", "c3": "S1M"}[kind], regime if kind != "c1" else "init")
         _pin_threads()  # inherited by the spawned workers before they import numpy
+        # the reference package itself when it is installed (baseline/_ref), else the oracle port
+        self.kind = "reference" if ref_available() else "port"
         t0 = time.perf_counter()
-        self.pool = ProcessPoolExecutor(self.workers, mp_context=mp.get_context("spawn"), initializer=_cpu_init,
+        self.pool = ProcessPoolExecutor(self.workers, mp_context=mp.get_context("spawn"),
+                                        initializer=_cpu_init_ref if self.kind == "reference" else _cpu_init,
                                         initargs=(kind, regime))
         list(self.pool.map(_cpu_ready, range(self.workers)))
         self.init_s = time.perf_counter() - t0
@@ -164,7 +300,7 @@ def c2_cpu_step(pool: CpuPool, seed: int):
     Extrapolated frame time on these cores = (8160 / k) x sum(tile times) / workers."""
     tiles = c2_tiles_sample(seed, pool.workers)
     t0 = time.perf_counter()
-    secs = list(pool.pool.map(_c2_tiles, [[t] for t in tiles]))
+    secs = list(pool.pool.map(_ref_c2_tiles if pool.kind == "reference" else _c2_tiles, [[t] for t in tiles]))
     wall = time.perf_counter() - t0
     frame_s = 8160 / len(tiles) * float(np.sum(secs)) / pool.workers
     return 1.0 / frame_s, wall, float(np.mean(secs))
@@ -174,7 +310,7 @@ def c1_cpu_frame(pool: CpuPool):
     """The whole C1 frame (256 x 256, 16 tile rows) in row bands over the workers."""
     bands = [(r, r + 1) for r in range(16)]
     t0 = time.perf_counter()
-    out = list(pool.pool.map(_c1_band, bands))
+    out = list(pool.pool.map(_ref_c1_band if pool.kind == "reference" else _c1_band, bands))
     wall = time.perf_counter() - t0
     img = np.concatenate([c for _, c in out], axis=0)
     return wall, img
@@ -184,7 +320,7 @@ def c3_cpu_sweep(pool: CpuPool, n_rays=230400):
     """The whole C3 sweep in ray blocks over the workers."""
     cuts = np.linspace(0, n_rays, 4 * pool.workers + 1).round().astype(int)
     t0 = time.perf_counter()
-    out = list(pool.pool.map(_c3_block, list(zip(cuts[:-1], cuts[1:]))))
+    out = list(pool.pool.map(_ref_c3_block if pool.kind == "reference" else _c3_block, list(zip(cuts[:-1], cuts[1:]))))
     wall = time.perf_counter() - t0
     return wall, np.concatenate([d for _, d in out])
 
@@ -214,7 +350,7 @@ def run_reference(args, rank):
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference pipeline scene S1M, bytes pinned by sha256)",
         "config": config_dict(args.regime, args.gpus),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.workers, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.workers, "kind": pool.kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "ms_per_step is the wall time of one sample step (a fraction frames_per_step of a frame); "
                 "value is the extrapolated whole-frame rate on these cores",
@@ -752,7 +888,7 @@ def cpu_baselines(args, ds, dev, lidar_ms, value):
     pool.close()
     v = float(np.mean(vals))
     out["cpu_baseline"] = {
-        "value": v, "unit": UNIT, "cores": pool.workers, "kind": "port",
+        "value": v, "unit": UNIT, "cores": pool.workers, "kind": pool.kind,
         "sample": f"2 x {pool.workers} random 16x16 tiles of the 8160 (one per worker, stratified over tile rows), "
                   f"fwd + bwd, projection once per worker, {float(np.sum(walls)):.1f} s wall; frame time = "
                   f"8160/k x sum(tile s) / {pool.workers} workers (EXTRAPOLATED)",
@@ -769,7 +905,7 @@ def cpu_baselines(args, ds, dev, lidar_ms, value):
     gimg = RR.rasterize(ds20, c1cam).color.double().cpu().numpy()
     out["c1"] = {"workload": "C1: S20k (19,992 voxels), 256x256 pinhole raster forward (BASELINE configs[0])",
                  "gpu_fps": 1e3 / gpu_ms, "cpu_fps": 1.0 / wall, "cpu_cores": pool.workers,
-                 "cpu_kind": "port", "cpu_s_per_frame": wall, "gpu_over_cpu": (1e3 / gpu_ms) * wall,
+                 "cpu_kind": pool.kind, "cpu_s_per_frame": wall, "gpu_over_cpu": (1e3 / gpu_ms) * wall,
                  "max_abs_diff_gpu_vs_cpu": float(np.abs(gimg - img).max()),
                  "note": "whole frame on both sides, not extrapolated (16 tile-row bands over the workers)"}
     del ds20
@@ -779,7 +915,7 @@ def cpu_baselines(args, ds, dev, lidar_ms, value):
     pool.close()
     out["cpu_baseline_lidar"] = {
         "workload": "C3: 128 x 1800 LiDAR sweep on S1M (BASELINE configs[2])",
-        "value": 230400 / wall, "unit": "rays/s", "cores": pool.workers, "kind": "port",
+        "value": 230400 / wall, "unit": "rays/s", "cores": pool.workers, "kind": pool.kind,
         "sample": "the whole sweep (230,400 rays) in ray blocks over the workers, not extrapolated",
         "gpu_rays_per_s": 230400 / (lidar_ms * 1e-3), "gpu_over_cpu": (230400 / (lidar_ms * 1e-3)) / (230400 / wall),
         "returns": int(np.isfinite(dep).sum())}
