@@ -866,7 +866,8 @@ def extras(ds, oc, args):
                      "c3_lidar_sweeps_per_s": 1e3 / ms_a, "c3_lidar_ms": ms_a,
                      "c2_raster_forward_fps_incl_flatten_upload": 1e3 / ms_r,
                      "note": "S1M init + 2 moving cars; LiDAR via the merge path (no early stop with live "
-                             "actors, render_ray.py:175); raster flattens + uploads the posed scene per frame"}
+                             "actors, render_ray.py:175); raster: static set resident, the posed actor voxels "
+                             "(host NumPy poses, render_raster.py:70-82) uploaded per frame"}
     return out
 
 
