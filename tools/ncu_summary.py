@@ -63,7 +63,8 @@ def main(rep, out_md, traffic_json=None):
         rd, wr = avg["dram__bytes_read.sum"], avg["dram__bytes_write.sum"]
         key = {"k_composite": "raster_composite", "k_composite_fast": "raster_composite",
                "k_composite_redo": "raster_composite_redo", "k_backward": "raster_backward",
-               "k_backward_fast": "raster_backward", "k_ray_forward": "ray_forward",
+               "k_backward_fast": "raster_backward", "k_backward_hits": "raster_backward",
+               "k_ray_forward": "ray_forward",
                "k_ray_forward_fast": "ray_forward", "k_ray_backward": "ray_backward"}.get(
             name.split("<")[0].replace("salf::", ""), name)
         traffic[key] = rd + wr
