@@ -672,13 +672,14 @@ def run_ours(args, world, rank, local):
     oc = RY.build_scene_octrees(scene)
     lid = configs.c3_lidar()
     lb = gen_lidar_rays(lid, device=dev)
+    # the sweep as render_lidar_ranges renders it (render_ray.py:297-306: inference, no backward state)
     for _ in range(max(args.warmup, 3)):
-        RY.render_lidar(ds, oc, lb)
+        RY.render_lidar(ds, oc, lb, need_state=False)
     barrier()
     la, lb_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     la.record()
     for _ in range(args.steps):
-        RY.render_lidar(ds, oc, lb)
+        RY.render_lidar(ds, oc, lb, need_state=False)
     lb_ev.record()
     barrier()
     t_l = torch.tensor([la.elapsed_time(lb_ev) / args.steps], dtype=torch.float64, device=dev)
@@ -687,7 +688,8 @@ def run_ours(args, world, rank, local):
     lidar_ms = float(t_l.item())
     lidar = {"metric": "LiDAR rays/s (128 beams x 1800 steps, S1M init)", "rays_per_s": world * lb.n / (lidar_ms * 1e-3),
              "sweeps_per_s": world * 1e3 / lidar_ms, "ms_per_sweep": lidar_ms, "n_gpus": world,
-             "scaling": "weak", "sharding": "one LiDAR sweep per rank, no exchange"}
+             "scaling": "weak", "sharding": "one LiDAR sweep per rank, no exchange",
+             "what": "render_lidar_ranges (inference; the training path with backward state is inside c5)"}
 
     # ---- C5: the rig training step sharded over the ranks (strong scaling) ----
     c5 = c5_step(args, world, rank, dev, scene, ds, oc, barrier)
@@ -809,7 +811,7 @@ def extras(ds, oc, args):
     head = rng.uniform(-0.5, 0.5, (2, 13)).astype(np.float32)
     ms = _timeit(lambda: RY.render_lidar(ds, oc, lb, features=feat, head=head))
     out["c3_lidar_intensity_raydrop"] = {"sweeps_per_s": 1e3 / ms, "rays_per_s": lb.n / (ms * 1e-3), "ms": ms}
-    ms = _timeit(lambda: RY.render_lidar(ds, oc, gen_lidar_rays(lidar)))
+    ms = _timeit(lambda: RY.render_lidar(ds, oc, gen_lidar_rays(lidar), need_state=False))
     out["c3_lidar_with_raygen"] = {"sweeps_per_s": 1e3 / ms, "ms": ms}
     del feat
 
@@ -824,7 +826,7 @@ def extras(ds, oc, args):
             fb, st = RR.rasterize(dss, cam, return_state=True)
             RR.rasterize_backward(st, dcs, None, as_dict=False)
 
-        ms_l = _timeit(lambda: RY.render_lidar(dss, ocs, lb))
+        ms_l = _timeit(lambda: RY.render_lidar(dss, ocs, lb, need_state=False))
         return {"voxels": dss.n, "c2_forward_fps": 1e3 / _timeit(lambda: RR.rasterize(dss, cam)),
                 "c2_fwd_bwd_fps": 1e3 / _timeit(fb_step, n=5),
                 "c3_lidar_sweeps_per_s": 1e3 / ms_l, "c3_lidar_rays_per_s": lb.n / (ms_l * 1e-3),
@@ -843,7 +845,8 @@ def extras(ds, oc, args):
 
     def c4_frame():
         b = camera_rays(c4)
-        return RY.integrate_rays(ds2, oc2, b.origins, b.dirs, valid=b.valid, check_unit=False, check=False)
+        return RY.integrate_rays(ds2, oc2, b.origins, b.dirs, valid=b.valid, check_unit=False, check=False,
+                                 need_state=False)  # render_rays_image semantics (no backward)
 
     out["c4_fisheye_rs_fps_S2M"] = 1e3 / _timeit(c4_frame, n=5)
     del ds2, oc2

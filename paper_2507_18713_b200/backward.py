@@ -33,6 +33,8 @@ def backward_grad_buffer(records: RenderRecords, d_color, d_depth,
     dd = _lib.as_f64(d_depth, dev).reshape(n)
     if grad is None:
         grad = torch.zeros((max(ds.n, 1), _lib.GRAD_STRIDE), dtype=torch.float64, device=dev)
+    if records.saved is None:
+        raise ValueError("these records were rendered with need_state=False (inference): no backward")
     if n and records.ex_rec is not None:
         raise ValueError("records with actor segments: use backward_records")
     if n and deterministic:

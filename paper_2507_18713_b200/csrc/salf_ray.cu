@@ -11,6 +11,8 @@
 // warp-aggregated atomics.
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "salf_common.cuh"
 #include "salf_internal.h"
 
@@ -548,7 +550,7 @@ __global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, sa
 #ifndef SALF_RAYF_MINB_CAM
 #define SALF_RAYF_MINB_CAM 6  // camera rays (colour): measured best (C4 10.9 -> 9.7 ms)
 #endif
-template <bool kLidar, bool kSdf, bool kFeat = false>
+template <bool kLidar, bool kSdf, bool kFeat = false, bool kTot64 = true>
 __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_CAM) k_ray_forward_fast(
     OctDev t, salf_scene_t sc, int64_t n, const double *__restrict__ orig, const double *__restrict__ dirs,
     const uint8_t *__restrict__ valid, salf_raster_opts_t opt, float *__restrict__ out_rgb,
@@ -562,11 +564,13 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   if (i >= n) return;
   const double y_stop_d = -log(1.0 - opt.stop_threshold);
   const float y_stop = (float)y_stop_d, y_stop_err = (float)fabs(y_stop_d - (double)y_stop);
-  // fp64 totals of the exact fp32 products w c, w, w t_mid: the mixed backward
-  // rebuilds its suffix sums from them (seg_grad_f32); T = exp(-Y) exactly as
-  // the backward recomputes it (also for the first segment)
+  // kTot64 (a backward follows): fp64 totals of the exact fp32 products w c, w,
+  // w t_mid -- the mixed backward rebuilds its suffix sums from them
+  // (seg_grad_f32); without saved state (inference) plain fp32 sums.  T = exp(-Y)
+  // exactly as the backward recomputes it (also for the first segment)
+  using Acc = typename std::conditional<kTot64, double, float>::type;
   float T = fast_exp(-0.f), EY = 0.f, Yh = 0.f, Yc = 0.f;
-  double acc_c[3] = {0.0, 0.0, 0.0}, acc_w = 0.0, acc_wt = 0.0;
+  Acc acc_c[3] = {0, 0, 0}, acc_w = 0, acc_wt = 0;
   double last_t0 = -INFINITY;
   int64_t n_seg = 0, n_inc = 0;
   int32_t st = 0;
@@ -614,7 +618,10 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
                               (float)(kShC1 * m.d[0])};
         eval_color32g(p, x, gam, col);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) acc_c[k] = fma(wd, (double)col[k], acc_c[k]);
+        for (int k = 0; k < 3; ++k) {
+          if constexpr (kTot64) acc_c[k] = fma(wd, (double)col[k], acc_c[k]);
+          else acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
+        }
       }
       if (feat) {  // intensity / ray-drop extension: blended 8-channel feature
         const float4 f0 = __ldg(reinterpret_cast<const float4 *>(lf.feat) + 2 * vid);
@@ -623,8 +630,13 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc_f[k] = fma(wd, (double)fv[k], acc_f[k]);
       }
-      acc_w = __dadd_rn(acc_w, wd);
-      acc_wt = fma(wd, tm, acc_wt);
+      if constexpr (kTot64) {
+        acc_w = __dadd_rn(acc_w, wd);
+        acc_wt = fma(wd, tm, acc_wt);
+      } else {
+        acc_w += w;
+        acc_wt = __fmaf_rn(w, (float)tm, acc_wt);
+      }
       EY += y * (rel + 2.f * kU);
       neumaier_add(Yh, Yc, y);
       T = fast_exp(-(Yh + Yc));
@@ -643,9 +655,9 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   if (ok) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-      if (out_rgb) out_rgb[3 * i + k] = (float)fma((double)T, opt.background[k], acc_c[k]);
+      if (out_rgb) out_rgb[3 * i + k] = (float)fma((double)T, opt.background[k], (double)acc_c[k]);
     out_op[i] = (float)(-expm1(-Y));  // 1 - T without cancellation near T = 1
-    out_depth[i] = vdepth ? (float)__ddiv_rn(acc_wt, acc_w) : NAN;
+    out_depth[i] = vdepth ? (float)__ddiv_rn((double)acc_wt, (double)acc_w) : NAN;
   } else {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -661,7 +673,7 @@ __global__ void __launch_bounds__(128, kLidar ? SALF_RAY_MINB : SALF_RAYF_MINB_C
   }
   if (feat) {
     // linear head on [blended feature, expected depth (0 if none), view dir] + sigmoid (as k_ray_forward)
-    const float dep = vdepth ? (float)__ddiv_rn(acc_wt, acc_w) : 0.0f;
+    const float dep = vdepth ? (float)__ddiv_rn((double)acc_wt, (double)acc_w) : 0.0f;
     const float dv[3] = {(float)dirs[3 * i], (float)dirs[3 * i + 1], (float)dirs[3 * i + 2]};
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -1130,12 +1142,21 @@ extern "C" int salf_ray_forward(const salf_octree_t *tree, const salf_scene_t *s
       // certified mixed precision, then fp64 recomputation of the flagged rays
       if (!status) return set_error(SALF_EINVAL, "the mixed-precision ray forward needs a status buffer");
       cudaStream_t st = (cudaStream_t)stream;
-      if (scene->density_mode == SALF_DENSITY_SDF)
+      const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
+      if (!saved) {  // inference (no backward follows): fp32 totals
+        if (sdf)
+          k_ray_forward_fast<false, true, false, false><<<grid, 128, 0, st>>>(
+              t, *scene, n, origins, dirs, valid, *opts, out_rgb, out_opacity, out_depth, nullptr, status, lf);
+        else
+          k_ray_forward_fast<false, false, false, false><<<grid, 128, 0, st>>>(
+              t, *scene, n, origins, dirs, valid, *opts, out_rgb, out_opacity, out_depth, nullptr, status, lf);
+      } else if (sdf) {
         k_ray_forward_fast<false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
                                                               out_opacity, out_depth, saved, status, lf);
-      else
+      } else {
         k_ray_forward_fast<false, false><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
                                                                out_opacity, out_depth, saved, status, lf);
+      }
       static const bool no_redo = getenv("SALF_NO_REDO") && getenv("SALF_NO_REDO")[0] == '1';  // diagnostics
       if (!no_redo)
         k_ray_forward<false, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, valid, *opts, out_rgb,
@@ -1168,6 +1189,13 @@ extern "C" int salf_lidar_forward(const salf_octree_t *tree, const salf_scene_t 
         else
           k_ray_forward_fast<true, false, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts,
                                                                       nullptr, out_opacity, out_depth, saved, status, lf);
+      } else if (!saved) {  // inference (no backward follows): fp32 totals
+        if (sdf)
+          k_ray_forward_fast<true, true, false, false><<<grid, 128, 0, st>>>(
+              t, *scene, n, origins, dirs, nullptr, *opts, nullptr, out_opacity, out_depth, nullptr, status, lf);
+        else
+          k_ray_forward_fast<true, false, false, false><<<grid, 128, 0, st>>>(
+              t, *scene, n, origins, dirs, nullptr, *opts, nullptr, out_opacity, out_depth, nullptr, status, lf);
       } else if (sdf) {
         k_ray_forward_fast<true, true><<<grid, 128, 0, st>>>(t, *scene, n, origins, dirs, nullptr, *opts, nullptr,
                                                              out_opacity, out_depth, saved, status, lf);

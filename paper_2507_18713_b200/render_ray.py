@@ -174,7 +174,7 @@ def _actor_segments(scene: Scene, octrees: SceneOctrees, o: torch.Tensor, d: tor
 def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf,
                    background=(0.0, 0.0, 0.0), stop_threshold: float = STOP_THRESHOLD,
                    valid=None, exact_color: bool = False, check_unit: bool = True,
-                   check: bool = True) -> RenderRecords:
+                   check: bool = True, need_state: bool = True) -> RenderRecords:
     """Render a ray batch against the composed scene (render_ray.py:161-239).
 
     Static scenes use one fused march/shade/composite launch with the
@@ -187,7 +187,10 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
     raises like the reference for rays the marcher cannot finish
     (RuntimeError "octree marching failed to terminate", octree.py:251-252;
     ValueError for a query outside the root, octree.py:144-145); `check=False`
-    leaves them as status bits on the records (no host synchronisation)."""
+    leaves them as status bits on the records (no host synchronisation).
+    `need_state=False` (inference: no backward on these records) skips the
+    per-ray replay state, and the kernel keeps plain fp32 totals instead of the
+    fp64 totals the mixed backward rebuilds its suffix sums from."""
     if np.any(np.isfinite(np.asarray(t_max, np.float64))):
         raise NotImplementedError("finite t_max is only supported by march_batch")
     lib = _lib.load()
@@ -209,7 +212,8 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
     rgb = torch.empty((n, 3), dtype=torch.float32, device=dev)
     op = torch.empty(n, dtype=torch.float32, device=dev)
     depth = torch.empty(n, dtype=torch.float32, device=dev)
-    saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev)
+    live_or_state = need_state or (isinstance(scene, Scene) and any(a.voxels.n for a in scene.actors))
+    saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev) if live_or_state else None
     status = torch.zeros(n, dtype=torch.int32, device=dev)
     opts = _opts(background, stop_threshold, exact_color)
     sc, t = ds.c_struct(), tree.c_struct()
@@ -227,7 +231,7 @@ def integrate_rays(scene, octrees, origins, dirs, t_stamps=None, *, t_max=np.inf
         return rec
     _lib.check(lib.salf_ray_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
                                     _lib.ptr(vmask), _lib.ref(opts), rgb.data_ptr(), op.data_ptr(),
-                                    depth.data_ptr(), saved.data_ptr(), status.data_ptr(),
+                                    depth.data_ptr(), _lib.ptr(saved), status.data_ptr(),
                                     _lib.stream_ptr()), "integrate_rays")
     rec = RenderRecords(n, rgb, op, depth, saved, status, o, d, vmask, ds, tree, opts,
                         np.asarray(background, np.float64))
@@ -266,7 +270,8 @@ def render_rays_image(scene, octrees, batch, *, background=(0.0, 0.0, 0.0), chun
     h, w = batch.shape
     rec = integrate_rays(scene, octrees, batch.origins, batch.dirs, batch.t_stamps,
                          background=background, stop_threshold=stop_threshold, valid=batch.valid,
-                         exact_color=exact_color, check_unit=not getattr(batch, "generated", False))
+                         exact_color=exact_color, check_unit=not getattr(batch, "generated", False),
+                         need_state=False)
     return rec.out_color.reshape(h, w, 3), rec.opacity.reshape(h, w), rec.depth.reshape(h, w)
 
 
@@ -290,7 +295,8 @@ class LidarReturn:
 
 
 def render_lidar(scene, octrees, batch, *, features=None, head=None,
-                 stop_threshold: float = STOP_THRESHOLD, want_feature: bool = False) -> LidarReturn:
+                 stop_threshold: float = STOP_THRESHOLD, want_feature: bool = False,
+                 need_state: bool = True) -> LidarReturn:
     """LiDAR sweep: expected range (render_lidar_ranges, render_ray.py:297-306)
     plus the optional intensity / ray-drop extension (not in
     the reference -- SPEC.md:8): per-voxel 8-channel `features` (M, 8) are
@@ -310,7 +316,9 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
         raise ValueError("ray directions must be unit norm")
     depth = torch.empty(n, dtype=torch.float32, device=dev)
     op = torch.empty(n, dtype=torch.float32, device=dev)
-    saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev)
+    # need_state=False: inference only (no lidar_backward on the result): fp32 totals, no replay state
+    saved = torch.empty((n, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev) \
+        if (need_state or features is not None) else None
     status = torch.zeros(n, dtype=torch.int32, device=dev)
     f = h = of = oh = fa = None
     if features is not None:
@@ -328,7 +336,7 @@ def render_lidar(scene, octrees, batch, *, features=None, head=None,
     _lib.check(lib.salf_lidar_forward(_lib.ref(t), _lib.ref(sc), n, o.data_ptr(), d.data_ptr(),
                                       _lib.ref(opts), _lib.ptr(f), _lib.ptr(h), depth.data_ptr(),
                                       op.data_ptr(), _lib.ptr(of), _lib.ptr(oh), _lib.ptr(fa),
-                                      saved.data_ptr(), status.data_ptr(), _lib.stream_ptr()), "render_lidar")
+                                      _lib.ptr(saved), status.data_ptr(), _lib.stream_ptr()), "render_lidar")
     shp = batch.shape
     return LidarReturn(depth.reshape(shp), op.reshape(shp),
                        None if oh is None else oh[:, 0].reshape(shp),
@@ -348,6 +356,8 @@ def lidar_backward(ret: LidarReturn, d_depth=None, *, features=None, head=None, 
     background) and through the expected depth."""
     lib = _lib.load()
     ds, dev = ret.scene, ret.scene.device
+    if ret.saved is None:
+        raise ValueError("lidar_backward needs render_lidar(..., need_state=True)")
     n = ret.saved.shape[0]
     dd = torch.zeros(n, dtype=torch.float64, device=dev) if d_depth is None else \
         _lib.as_f64(d_depth, dev).reshape(n).clone()
@@ -389,7 +399,7 @@ def render_lidar_ranges(scene, octrees, batch, *, chunk: int = 65536) -> torch.T
     One fused launch without colour (the reference evaluates colour for every
     segment and discards it here)."""
     del chunk
-    ret = render_lidar(scene, octrees, batch)
+    ret = render_lidar(scene, octrees, batch, need_state=False)
     raise_for_status(ret.status)
     return ret.depth
 
