@@ -151,7 +151,7 @@ class Backend:
             flat = FlatVoxels(ours.centers(), ours.edges(), ours.rotation, ours.w_s, ours.w_c, ours.w_sh,
                               ours.log_a, ours.log_b, density_mode)
             e = _SetEntry((v.level, v.ijk, v.rotation), DeviceScene(flat, self.device))
-            if len(self._sets) >= 4:  # oldest first: densification retires whole sets
+            if len(self._sets) >= 8:  # oldest first: densification retires whole sets
                 self._sets.pop(next(iter(self._sets)))
             self._sets[key] = e
         else:
