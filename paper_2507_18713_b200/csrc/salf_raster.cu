@@ -1333,6 +1333,26 @@ __device__ __forceinline__ void prefetch_prev(const salf_scene_t &sc, const int3
 #endif
 constexpr float kU24 = 5.9604645e-8f;  // 2^-24
 
+// The reference's pair test in fp64 and in its own order (ray_box_range,
+// octree.py:184-194, on o = camera - centre; t0 = max(t_in, t_near, 0); hit iff
+// t1 > t0 + 1e-12, render_raster.py:239-241) for a pixel ray without zero
+// components: what the certified forward falls back to for a chord its fp32
+// bound cannot place on either side of zero.
+__device__ __forceinline__ bool pair_hit_ref64(const RayF &r, const EntryF &e, double &t0, double &t1) {
+  double ti = 0.0, to = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double inv = 1.0 / r.d[k];
+    const double ta = __dmul_rn(__dsub_rn(-e.half, e.o[k]), inv), tb = __dmul_rn(__dsub_rn(e.half, e.o[k]), inv);
+    const double nk = npmin(ta, tb), fk = npmax(ta, tb);
+    ti = k ? npmax(ti, nk) : nk;
+    to = k ? npmin(to, fk) : fk;
+  }
+  t0 = npmax(ti, r.tn0);  // max(max(t_in, t_near), 0) with r.tn0 = max(t_near, 0)
+  t1 = to;
+  return t1 > __dadd_rn(t0, 1e-12);
+}
+
 #ifndef SALF_FWDF_MINB
 #define SALF_FWDF_MINB 3
 #endif
@@ -1431,10 +1451,16 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           }
           continue;
         }
-        // a chord within its fp32 error of zero may be an fp64 miss: fp64 redo decides
-        if ((SALF_FLAGMASK & 1) && u1 - u0 <= 2.f * dd &&
-            u1 - u0 <= chord_err(ray->inv, e.hf, qv, ray->tn0f - ts, u0, u1, fabsf(ts) + ray->tn0f))
-          flag = true;
+        float delta = u1 - u0, um = 0.5f * (u0 + u1);
+        // a chord within its fp32 error of zero may be an fp64 miss: this pair is decided in fp64
+        // in the reference's order (render_raster.py:239-241) -- rare, so no pixel-wide redo
+        if ((SALF_FLAGMASK & 1) && u1 - u0 <= 2.f * dd && ray->fast &&
+            u1 - u0 <= chord_err(ray->inv, e.hf, qv, ray->tn0f - ts, u0, u1, fabsf(ts) + ray->tn0f)) {
+          double t0d, t1d;
+          if (!pair_hit_ref64(*ray, e, t0d, t1d)) continue;
+          delta = (float)(t1d - t0d);
+          um = (float)(0.5 * (t0d + t1d) - (double)ts);
+        }
         // inclusion of this hit: Y_before < y_stop (certified outside the band)
         const float Ys = Yh + Yc;
         const float gap = y_stop - Ys;
@@ -1446,8 +1472,6 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           break;
         }
         hbm |= 1ull << j;
-        const float delta = u1 - u0;
-        const float um = 0.5f * (u0 + u1);
         float x[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
