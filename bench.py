@@ -372,10 +372,15 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
+            return
+        # NVML start-up takes ~0.1-0.3 s: wait for the first sample so the timed region is covered
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 3.0 and not Path(self.f.name).read_text().strip():
+            time.sleep(0.01)
 
     def stop(self):
         if self.p is None:
@@ -562,6 +567,7 @@ def run_ours(args, world, rank, local):
         times.append((a, b))
         kev.append(ev)
     barrier()
+    torch.cuda.synchronize()
     clk = clocks.stop()
     ms = [a.elapsed_time(b) for a, b in times]
     kms = {}
