@@ -42,7 +42,7 @@ for c in cams:
     dc = torch.sign(torch.randn(c.height, c.width, 3, dtype=torch.float64, device=ds.device)) / 1e6
     dd = torch.zeros((c.height, c.width), dtype=torch.float64, device=ds.device)
     f = timeit(lambda: RR.rasterize(ds, c, return_state=True))
-    b = timeit(lambda: RR.rasterize_backward(st, dc, dd, grad, as_dict=False))
+    b = timeit(lambda: RR.rasterize_backward(st, dc, None, grad, as_dict=False))  # colour-only, as rig_step
     out["cams"].append({"fwd_ms": f, "bwd_ms": b, "instances": int(st.n_instances) if hasattr(st, "n_instances") else None})
 out["lidars"] = []
 for l in lidars:
