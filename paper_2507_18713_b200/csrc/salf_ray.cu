@@ -422,7 +422,7 @@ struct LidarFeat {
 };
 
 #ifndef SALF_RAY_MINB
-#define SALF_RAY_MINB 4
+#define SALF_RAY_MINB 5
 #endif
 // kLidar: depth-only rays (render_lidar_ranges never reads colour), plus the
 // optional intensity / ray-drop extension.

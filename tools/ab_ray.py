@@ -36,7 +36,8 @@ ds = DeviceScene.from_scene(sc)
 oc = RY.build_scene_octrees(sc)
 lb = gen_lidar_rays(configs.c3_lidar())
 out = {"tag": tag}
-out["c3_lidar_ms"] = timeit(lambda: RY.render_lidar(ds, oc, lb))
+out["c3_lidar_ms"] = timeit(lambda: RY.render_lidar(ds, oc, lb, need_state=False))
+out["c3_lidar_state_ms"] = timeit(lambda: RY.render_lidar(ds, oc, lb))
 out["c3_fwd_ms"] = timeit(lambda: RY.integrate_rays(ds, oc, lb.origins, lb.dirs))
 rec = RY.integrate_rays(ds, oc, lb.origins, lb.dirs)
 dd = torch.sign(torch.randn(lb.n, device="cuda", dtype=torch.float64)) / lb.n
@@ -50,7 +51,7 @@ s2 = get_scene("S2M", "init")
 ds2 = DeviceScene.from_scene(s2)
 oc2 = RY.build_scene_octrees(s2)
 cb = camera_rays(configs.c4_camera())
-out["c4_ms"] = timeit(lambda: RY.integrate_rays(ds2, oc2, cb.origins, cb.dirs, valid=cb.valid), n=5)
+out["c4_ms"] = timeit(lambda: RY.integrate_rays(ds2, oc2, cb.origins, cb.dirs, valid=cb.valid, need_state=False), n=5)
 r2 = RY.integrate_rays(ds2, oc2, cb.origins, cb.dirs, valid=cb.valid)
 out["c4_digest"] = [float(r2.saved[:, 6].sum()), float(torch.nan_to_num(r2.depth.double()).sum())]
 print(json.dumps(out))
