@@ -422,12 +422,15 @@ struct LidarFeat {
 };
 
 #ifndef SALF_RAY_MINB
-#define SALF_RAY_MINB 5
+#define SALF_RAY_MINB 5  // LiDAR fast forward (measured: 5 beats 4 for the training instantiation)
+#endif
+#ifndef SALF_RAYX_MINB
+#define SALF_RAYX_MINB 4  // fp64 ray forward (parity mode and the redo): 128 registers, no spills
 #endif
 // kLidar: depth-only rays (render_lidar_ranges never reads colour), plus the
 // optional intensity / ray-drop extension.
 template <bool kExactColor, bool kLidar, bool kRedo = false>
-__global__ void __launch_bounds__(128, SALF_RAY_MINB) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
+__global__ void __launch_bounds__(128, SALF_RAYX_MINB) k_ray_forward(OctDev t, salf_scene_t sc, int64_t n,
                                                      const double *__restrict__ orig, const double *__restrict__ dirs,
                                                      const uint8_t *__restrict__ valid, salf_raster_opts_t opt,
                                                      float *__restrict__ out_rgb, float *__restrict__ out_op,
