@@ -183,3 +183,23 @@ def as_f64(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=torch.float64).contiguous()
     return torch.as_tensor(np.array(x, dtype=np.float64, order="C"), device=device)
+
+
+# NVTX ranges around the phases of a frame (SALF_NVTX=1; e.g. `ncu --nvtx
+# --nvtx-include "raster_backward/"`): a no-op context otherwise.
+NVTX = os.environ.get("SALF_NVTX", "0") == "1"
+
+
+class _NoRange:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_RANGE = _NoRange()
+
+
+def nvtx(name: str):
+    return torch.cuda.nvtx.range(name) if NVTX else _NO_RANGE

@@ -249,21 +249,24 @@ def rasterize(flat, cam: CameraModel, *, background=(0.0, 0.0, 0.0), tile: int =
     depth = torch.empty((h, w), dtype=torch.float32, device=dev)
     saved = torch.empty((h * w, _lib.SAVED_STRIDE), dtype=torch.float64, device=dev) \
         if return_state else None
-    p = _project(ds, cam, near, tile)
+    with _lib.nvtx("raster_project"):
+        p = _project(ds, cam, near, tile)
     opts = _opts(background, near, stop_threshold, tile, exact_color)
     sc, cs = ds.c_struct(), cam.c_struct(rolling=False)
     for attempt in range(2):
-        offsets, entries, counts, cap, _ = _bin(ds, cam, near, tile, p, mode=1)
+        with _lib.nvtx("raster_bin"):
+            offsets, entries, counts, cap, _ = _bin(ds, cam, near, tile, p, mode=1)
         # hit words for the backward (default mode): which list entries each pixel includes
         hitbits = torch.empty(lib.salf_raster_hitbits_words(cap, offsets.numel() - 1), dtype=torch.int32,
                               device=dev) if (return_state and not exact_color) else None
         ev = _timed(events, "raster_composite")
-        _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
-                                             offsets.data_ptr(), entries.data_ptr(),
-                                             rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
-                                             _lib.ptr(saved), p["vrange"].data_ptr(), None, _lib.ptr(hitbits),
-                                             _lib.stream_ptr()),
-                   "rasterize")
+        with _lib.nvtx("raster_composite"):
+            _lib.check(lib.salf_raster_composite(_lib.ref(sc), _lib.ref(cs), _lib.ref(opts),
+                                                 offsets.data_ptr(), entries.data_ptr(),
+                                                 rgb.data_ptr(), op.data_ptr(), depth.data_ptr(),
+                                                 _lib.ptr(saved), p["vrange"].data_ptr(), None, _lib.ptr(hitbits),
+                                                 _lib.stream_ptr()),
+                       "rasterize")
         if ev is not None:
             ev[2].record()
         # capacity check after the composite is enqueued: the host waits for the
@@ -328,6 +331,8 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
                                                   tws.data_ptr(), tws.numel(), _lib.stream_ptr()),
                        "rasterize_backward")
         ev = _timed(events, "raster_backward")
+        rng = _lib.nvtx("raster_backward")
+        rng.__enter__()
         if deterministic:
             wsb = lib.salf_raster_backward_det_workspace_bytes(state.n_instances, max(ds.n, 1))
             ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
@@ -342,6 +347,7 @@ def rasterize_backward(state: RasterState, d_color, d_depth, grad: torch.Tensor 
                                                 state.saved.data_ptr(), dc.data_ptr(), _lib.ptr(dd),
                                                 grad.data_ptr(), _lib.ptr(state.vrange), _lib.ptr(state.tile_order),
                                                 _lib.ptr(state.hitbits), _lib.stream_ptr()), "rasterize_backward")
+        rng.__exit__(None, None, None)
         if ev is not None:
             ev[2].record()
     if as_dict:

@@ -19,6 +19,7 @@ import torch
 
 from . import render_raster as RR
 from . import render_ray as RY
+from ._lib import nvtx
 from .backward import l1_color_seed
 from .parallel import allreduce_, allreduce_grad_, band_camera
 from .render_ray import raise_for_status
@@ -98,9 +99,13 @@ def rig_backward(fs: ForwardState, grad: torch.Tensor, global_counts: torch.Tens
 def rig_step(ds, octree, sensors, targets, items, grad: torch.Tensor, depth_weight: float = 10.0):
     """One rank's share of a training step; all-reduces the counts, the
     gradient buffer and the loss sums.  Returns (loss_sums, global_counts)."""
-    fs = rig_forward(ds, octree, sensors, targets, items)
-    counts = allreduce_(fs.counts.clone())
-    rig_backward(fs, grad, counts, depth_weight)
-    allreduce_grad_(grad)
+    with nvtx("rig_forward"):
+        fs = rig_forward(ds, octree, sensors, targets, items)
+    with nvtx("rig_allreduce_counts"):
+        counts = allreduce_(fs.counts.clone())
+    with nvtx("rig_backward"):
+        rig_backward(fs, grad, counts, depth_weight)
+    with nvtx("rig_allreduce_grad"):
+        allreduce_grad_(grad)
     losses = allreduce_(fs.losses.clone())
     return losses, counts
