@@ -45,3 +45,34 @@ for k in range(0, 9):
     march_segments(t, o, d)
 torch.cuda.synchronize()
 print("jump tables ok")
+# round 2: hand-written sort (multi-CTA, device count), capacity re-bin, hit-word backward on a
+# bigger frame, device actor rays + merge, inference ray / LiDAR paths
+from paper_2507_18713_b200 import _lib
+lib = _lib.load()
+for kb, end in ((4, 13), (8, 64)):
+    n = 50_000
+    keys = torch.randint(0, 1 << 13, (n,), device="cuda", dtype=torch.int32 if kb == 4 else torch.int64)
+    vals = torch.arange(n, device="cuda", dtype=torch.int32)
+    ko, vo = torch.empty_like(keys), torch.empty_like(vals)
+    nd = torch.tensor([n - 123], device="cuda", dtype=torch.int64)
+    wsb = lib.salf_sort_pairs_workspace_bytes(n, kb, 0, end)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.salf_sort_pairs(keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vo.data_ptr(), kb, nd.data_ptr(),
+                                   n, 0, end, ws.data_ptr(), wsb, _lib.stream_ptr()), "sort")
+big = CameraModel(kind="pinhole", width=320, height=256, fx=300.0, fy=300.0, cx=160.0, cy=128.0, position=pos,
+                  quaternion=look_at_quaternion(pos, [4.0, 4.0, 2.0]))
+RR._CAPACITY[("cuda:0", 1)] = 5  # forces the re-bin path
+fb, st = RR.rasterize(flat, big, return_state=True)
+RR.rasterize_backward(st, torch.full((256, 320, 3), 1e-3, device="cuda", dtype=torch.float64), None)
+act = load_golden_scene("actors")
+oca = RY.build_scene_octrees(act)
+rec = RY.integrate_rays(act, oca, o, d, np.linspace(0.0, 0.5, 300))
+RR.rasterize_scene(act, cam, 0.25)
+RY.integrate_rays(sc, oc, o, d, need_state=False)
+from paper_2507_18713_b200.sensors import LidarModel, gen_lidar_rays
+lb = gen_lidar_rays(LidarModel(beam_elevations=np.linspace(-0.4, 0.2, 8), steps=64, position=np.array([4.013, 3.987, 2.5])))
+RY.render_lidar(sc, oc, lb, need_state=False)
+ret = RY.render_lidar(sc, oc, lb)
+RY.lidar_backward(ret, torch.full((lb.n,), 1e-3, device="cuda", dtype=torch.float64))
+torch.cuda.synchronize()
+print("round-2 paths ok")
