@@ -151,6 +151,17 @@ int salf_sort_pairs(const void *keys_in, const int32_t *vals_in, void *keys_out,
                     int32_t key_bytes, const int64_t *n_dev, int64_t n_max, int32_t begin_bit, int32_t end_bit,
                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* Sort (u64 key, int32 value) pairs that are unique as pairs into (key, value)
+ * order -- for input in ascending value order the permutation of the stable
+ * sort above, which is how the binning's depth rank (render_raster.py:177,
+ * z[vox] ties broken by voxel index) uses it.  Splitter bucket sort: five
+ * launches, workspace independent of n; n_max < 2^32.  Device pointers,
+ * stream-ordered, inputs not modified. */
+size_t salf_sort_pairs_unique_workspace_bytes(void);
+int salf_sort_pairs_unique(const uint64_t *keys_in, const int32_t *vals_in, uint64_t *keys_out, int32_t *vals_out,
+                           const int64_t *n_dev, int64_t n_max, void *workspace, size_t workspace_bytes,
+                           void *stream);
+
 /* rasterize (render_raster.py:201-301) over prebuilt render bins.
  * out_rgb (H*W*3), out_opacity, out_depth f32; saved (H*W*8 f64, nullable):
  * acc_rgb[3], acc_w, acc_wt, T_final, n_stop (entries examined), n_included

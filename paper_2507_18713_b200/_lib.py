@@ -78,6 +78,8 @@ SIGNATURES = {
     "salf_sort_pairs_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32, C.c_int32]),
     "salf_sort_pairs": (C.c_int, [vp, vp, vp, vp, C.c_int32, vp, C.c_int64, C.c_int32, C.c_int32, vp,
                                   C.c_size_t, vp]),
+    "salf_sort_pairs_unique_workspace_bytes": (C.c_size_t, []),
+    "salf_sort_pairs_unique": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, vp, C.c_size_t, vp]),
     "salf_raster_composite": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "salf_raster_hitbits_words": (C.c_size_t, [C.c_int64, C.c_int32]),
     "salf_raster_backward": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -2142,6 +2142,10 @@ extern "C" int salf_project_voxels(const salf_scene_t *scene, const salf_camera_
 }
 
 // workspace layout for salf_raster_bin
+#ifndef SALF_DEPTH_BUCKET
+#define SALF_DEPTH_BUCKET 1  // depth rank by splitter bucket sort (0: 8-pass radix sort)
+#endif
+
 struct BinWs {
   int64_t *cnt, *base_r;
   uint64_t *st_sel, *st_scan;  // look-back status of k_select_vis / k_scan_ranked
@@ -2178,7 +2182,7 @@ static BinWs carve(void *ws, int64_t n, int64_t cap, int n_tiles, size_t *total)
   w.keys_a = (uint32_t *)take(sizeof(uint32_t) * cap);
   w.keys_b = (uint32_t *)take(sizeof(uint32_t) * cap);
   w.vals_a = (int32_t *)take(sizeof(int32_t) * cap);
-  w.sort_bytes = std::max(radix_sort_workspace_bytes(n, 8, 0, 64),
+  w.sort_bytes = std::max(std::max(radix_sort_workspace_bytes(n, 8, 0, 64), bucket_sort_workspace_bytes()),
                           radix_sort_workspace_bytes(cap, 4, 0, bits_for((uint64_t)std::max(n_tiles, 1))));
   w.sort_tmp = take(w.sort_bytes);
   *total = off;
@@ -2218,8 +2222,15 @@ extern "C" int salf_raster_bin(const salf_scene_t *scene, const salf_camera_t *c
     k_select_vis<<<gs, sortk::kBlock, 0, st>>>(n, reinterpret_cast<const int4 *>(span), zkey, w.cnt, w.vis_idx,
                                                w.zk_vis, w.st_sel, w.tickets, counts);
     // global depth rank of the visible voxels: stable sort of (zkey, index) -> lexsort's (z, vox) order
+#if SALF_DEPTH_BUCKET
+    // vis_idx is ascending (stable compaction) and unique, so the (z, index)
+    // bucket sort gives the stable radix sort's permutation
+    int rc = bucket_sort_pairs_u64(w.zk_vis, w.vis_idx, w.zk_sorted, w.vis_sorted, counts, n, w.sort_tmp,
+                                   w.sort_bytes, st);
+#else
     int rc = radix_sort_pairs_u64(w.zk_vis, w.vis_idx, w.zk_sorted, w.vis_sorted, counts, n, 0, 64, w.sort_tmp,
                                   w.sort_bytes, st);
+#endif
     if (rc != SALF_OK) return rc;
     // instance slots in rank order
     k_scan_ranked<<<gs, sortk::kBlock, 0, st>>>(counts, w.vis_sorted, w.cnt, w.base_r, w.st_scan, w.tickets + 1);

@@ -15,6 +15,8 @@
 //     tiles (flag + 30-bit count in one 32-bit word);
 //   * scatter: global digit start + look-back prefix + warp prefix + rank.
 // Element counts can be device-resident (n_dev): CTAs past the end exit.
+#include <climits>
+
 #include "salf_internal.h"
 #include "salf_sort.cuh"
 
@@ -276,6 +278,225 @@ int radix_sort_pairs_u64(const uint64_t *keys_in, const int32_t *vals_in, uint64
                                      ws_bytes, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// Splitter bucket sort of (u64 key, int32 value) pairs that are unique as pairs
+// (the binning's depth rank: values are voxel indices), ordered by (key, value)
+// -- the same permutation as the stable LSD radix sort of keys over input in
+// value order.  kBuckets - 1 splitters are taken at evenly spaced input
+// positions and sorted; every element finds its bucket by binary search,
+// buckets are filled through CTA-aggregated slot claims, and one CTA per bucket
+// sorts it in shared memory (bitonic; global memory beyond the capacity).
+// Five launches instead of the radix sort's nine, no per-digit look-back chain.
+namespace sortk {
+
+constexpr int kBuckets = 1024;
+constexpr int kBktTile = 2048;  // elements per CTA of the count / scatter kernels
+constexpr int kBktCap = 2048;   // bucket elements sorted in shared memory
+
+__device__ __forceinline__ bool kv_less(uint64_t ka, int32_t va, uint64_t kb, int32_t vb) {
+  return ka < kb || (ka == kb && va < vb);
+}
+
+// in-place direction-free bitonic network over P = next pow2 >= n elements
+// (pairs past n skipped: the virtual pads are +inf)
+template <typename KeyAt, typename ValAt>
+__device__ __forceinline__ void bitonic_sort(int n, KeyAt key, ValAt val) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const bool mirror = j == (k >> 1);
+      for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+        int a, b;
+        if (mirror) {
+          const int h = k >> 1, blk = i >> (31 - __clz(h)), off = i & (h - 1);
+          a = blk * k + off;
+          b = blk * k + k - 1 - off;
+        } else {
+          a = 2 * i - (i & (j - 1));
+          b = a + j;
+        }
+        if (b >= n) continue;
+        const uint64_t ka = key(a), kb = key(b);
+        const int32_t va = val(a), vb = val(b);
+        if (kv_less(kb, vb, ka, va)) {
+          key(a) = kb; key(b) = ka;
+          val(a) = vb; val(b) = va;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// splitters: kBktOver * kBuckets evenly spaced samples sorted in one CTA, every
+// kBktOver-th kept (oversampling evens out the bucket sizes)
+constexpr int kBktOver = 4;
+__global__ void __launch_bounds__(1024) k_bkt_splitters(const uint64_t *__restrict__ kin,
+                                                        const int32_t *__restrict__ vin,
+                                                        const int64_t *__restrict__ n_dev, int64_t n_max,
+                                                        uint64_t *__restrict__ sk, int32_t *__restrict__ sv) {
+  constexpr int m = kBktOver * kBuckets;
+  __shared__ uint64_t k_s[m];
+  __shared__ int32_t v_s[m];
+  const int64_t n = n_dev ? min(*n_dev, n_max) : n_max;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const int64_t pos = (int64_t)(((double)i + 0.5) * (double)n / m);
+    const bool ok = pos < n;
+    k_s[i] = ok ? kin[pos] : ~0ull;
+    v_s[i] = ok ? vin[pos] : INT_MAX;
+  }
+  __syncthreads();
+  bitonic_sort(m, [&](int i) -> uint64_t & { return k_s[i]; }, [&](int i) -> int32_t & { return v_s[i]; });
+  for (int i = threadIdx.x; i < kBuckets - 1; i += blockDim.x) {
+    sk[i] = k_s[kBktOver * (i + 1)];
+    sv[i] = v_s[kBktOver * (i + 1)];
+  }
+}
+
+// bucket of (key, value): the number of splitters strictly below it
+__device__ __forceinline__ int bkt_of(const uint64_t *sk, const int32_t *sv, uint64_t k, int32_t v) {
+  int lo = 0, hi = kBuckets - 1;  // answer in [0, kBuckets - 1]
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (kv_less(sk[mid], sv[mid], k, v)) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// per-bucket counts (CTA-aggregated in shared memory)
+__global__ void __launch_bounds__(256) k_bkt_count(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
+                                                   const int64_t *__restrict__ n_dev, int64_t n_max,
+                                                   const uint64_t *__restrict__ spk, const int32_t *__restrict__ spv,
+                                                   uint32_t *__restrict__ bcnt) {
+  __shared__ uint64_t sk[kBuckets - 1];
+  __shared__ int32_t sv[kBuckets - 1];
+  __shared__ uint32_t c[kBuckets];
+  const int64_t n = n_dev ? min(*n_dev, n_max) : n_max;
+  const int64_t start = (int64_t)blockIdx.x * kBktTile;
+  if (start >= n) return;
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) {
+    c[i] = 0;
+    if (i < kBuckets - 1) { sk[i] = spk[i]; sv[i] = spv[i]; }
+  }
+  __syncthreads();
+  const int64_t end = min(start + kBktTile, n);
+  for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) atomicAdd(&c[bkt_of(sk, sv, kin[i], vin[i])], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+    if (c[i]) atomicAdd(bcnt + i, c[i]);
+}
+
+// bucket offsets (exclusive scan, one CTA of kBuckets threads); cursors start there
+__global__ void __launch_bounds__(kBuckets) k_bkt_scan(const uint32_t *__restrict__ bcnt, uint32_t *__restrict__ boff,
+                                                       uint32_t *__restrict__ cursor) {
+  __shared__ uint32_t s_w[kBuckets / 32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t v = bcnt[t];
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[w] = x;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int i = 0; i < w; ++i) off += s_w[i];
+  const uint32_t ex = off + x - v;
+  boff[t] = ex;
+  cursor[t] = ex;
+  if (t == kBuckets - 1) boff[kBuckets] = ex + v;
+}
+
+// scatter into the buckets (CTA-aggregated slot claims, any order inside a bucket)
+__global__ void __launch_bounds__(256) k_bkt_scatter(const uint64_t *__restrict__ kin, const int32_t *__restrict__ vin,
+                                                     const int64_t *__restrict__ n_dev, int64_t n_max,
+                                                     const uint64_t *__restrict__ spk, const int32_t *__restrict__ spv,
+                                                     uint32_t *__restrict__ cursor, uint64_t *__restrict__ kout,
+                                                     int32_t *__restrict__ vout) {
+  __shared__ uint64_t sk[kBuckets - 1];
+  __shared__ int32_t sv[kBuckets - 1];
+  __shared__ uint32_t c[kBuckets];
+  __shared__ uint16_t bk[kBktTile];
+  const int64_t n = n_dev ? min(*n_dev, n_max) : n_max;
+  const int64_t start = (int64_t)blockIdx.x * kBktTile;
+  if (start >= n) return;
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x) {
+    c[i] = 0;
+    if (i < kBuckets - 1) { sk[i] = spk[i]; sv[i] = spv[i]; }
+  }
+  __syncthreads();
+  const int64_t end = min(start + kBktTile, n);
+  for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
+    const int b = bkt_of(sk, sv, kin[i], vin[i]);
+    bk[i - start] = (uint16_t)b;
+    atomicAdd(&c[b], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kBuckets; i += blockDim.x)
+    if (c[i]) c[i] = atomicAdd(cursor + i, c[i]);
+  __syncthreads();
+  for (int64_t i = start + threadIdx.x; i < end; i += blockDim.x) {
+    const uint32_t pos = atomicAdd(&c[bk[i - start]], 1u);
+    kout[pos] = kin[i];
+    vout[pos] = vin[i];
+  }
+}
+
+// one CTA per bucket: sort it by (key, value)
+__global__ void __launch_bounds__(256) k_bkt_sort(const uint32_t *__restrict__ boff, uint64_t *__restrict__ kio,
+                                                  int32_t *__restrict__ vio) {
+  __shared__ uint64_t k_s[kBktCap];
+  __shared__ int32_t v_s[kBktCap];
+  const int64_t beg = boff[blockIdx.x];
+  const int n = (int)(boff[blockIdx.x + 1] - beg);
+  if (n <= 1) return;
+  if (n <= kBktCap) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      k_s[i] = kio[beg + i];
+      v_s[i] = vio[beg + i];
+    }
+    __syncthreads();
+    bitonic_sort(n, [&](int i) -> uint64_t & { return k_s[i]; }, [&](int i) -> int32_t & { return v_s[i]; });
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      kio[beg + i] = k_s[i];
+      vio[beg + i] = v_s[i];
+    }
+    return;
+  }
+  bitonic_sort(n, [&](int i) -> uint64_t & { return kio[beg + i]; }, [&](int i) -> int32_t & { return vio[beg + i]; });
+}
+
+}  // namespace sortk
+
+size_t bucket_sort_workspace_bytes() {
+  return 256 * 4 + (sizeof(uint64_t) + sizeof(int32_t)) * sortk::kBuckets + sizeof(uint32_t) * (3 * sortk::kBuckets + 1);
+}
+
+int bucket_sort_pairs_u64(const uint64_t *keys_in, const int32_t *vals_in, uint64_t *keys_out, int32_t *vals_out,
+                          const int64_t *n_dev, int64_t n_max, void *ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace sortk;
+  if (n_max <= 0) return SALF_OK;
+  if (n_max >= (int64_t)UINT32_MAX) return set_error(SALF_EINVAL, "bucket sort: too many keys");
+  if (ws_bytes < bucket_sort_workspace_bytes()) return set_error(SALF_EWORKSPACE, "bucket sort workspace too small");
+  char *p = (char *)ws;
+  uint64_t *spk = (uint64_t *)p;
+  p += sizeof(uint64_t) * kBuckets;
+  int32_t *spv = (int32_t *)p;
+  p += sizeof(int32_t) * kBuckets;
+  uint32_t *bcnt = (uint32_t *)p, *boff = bcnt + kBuckets, *cursor = boff + kBuckets + 1;
+  cudaMemsetAsync(bcnt, 0, sizeof(uint32_t) * kBuckets, st);
+  const unsigned grid = (unsigned)((n_max + kBktTile - 1) / kBktTile);
+  k_bkt_splitters<<<1, 1024, 0, st>>>(keys_in, vals_in, n_dev, n_max, spk, spv);
+  k_bkt_count<<<grid, 256, 0, st>>>(keys_in, vals_in, n_dev, n_max, spk, spv, bcnt);
+  k_bkt_scan<<<1, kBuckets, 0, st>>>(bcnt, boff, cursor);
+  k_bkt_scatter<<<grid, 256, 0, st>>>(keys_in, vals_in, n_dev, n_max, spk, spv, cursor, keys_out, vals_out);
+  k_bkt_sort<<<kBuckets, 256, 0, st>>>(boff, keys_out, vals_out);
+  return check_cuda("bucket_sort_pairs");
+}
+
 }  // namespace salf
 
 extern "C" size_t salf_sort_pairs_workspace_bytes(int64_t n_max, int32_t key_bytes, int32_t begin_bit,
@@ -297,6 +518,18 @@ extern "C" int salf_sort_pairs(const void *keys_in, const int32_t *vals_in, void
       return salf::radix_sort_pairs_u64((const uint64_t *)keys_in, vals_in, (uint64_t *)keys_out, vals_out, n_dev,
                                         n_max, begin_bit, end_bit, workspace, workspace_bytes, st);
     return salf::set_error(SALF_EINVAL, "sort_pairs: key_bytes must be 4 or 8, got %d", key_bytes);
+  }
+  SALF_CATCH
+}
+
+extern "C" size_t salf_sort_pairs_unique_workspace_bytes(void) { return salf::bucket_sort_workspace_bytes(); }
+
+extern "C" int salf_sort_pairs_unique(const uint64_t *keys_in, const int32_t *vals_in, uint64_t *keys_out,
+                                      int32_t *vals_out, const int64_t *n_dev, int64_t n_max, void *workspace,
+                                      size_t workspace_bytes, void *stream) {
+  SALF_TRY {
+    return salf::bucket_sort_pairs_u64(keys_in, vals_in, keys_out, vals_out, n_dev, n_max, workspace,
+                                       workspace_bytes, (cudaStream_t)stream);
   }
   SALF_CATCH
 }

@@ -105,4 +105,11 @@ int radix_sort_pairs_u64(const uint64_t *keys_in, const int32_t *vals_in, uint64
                          const int64_t *n_dev, int64_t n_max, int begin_bit, int end_bit, void *ws, size_t ws_bytes,
                          cudaStream_t st);
 
+// Splitter bucket sort of (u64 key, int32 value) pairs unique as pairs, ordered by
+// (key, value) -- for value-ordered input the same permutation as the stable
+// radix sort of the keys.  Workspace: bucket_sort_workspace_bytes() (independent of n).
+size_t bucket_sort_workspace_bytes();
+int bucket_sort_pairs_u64(const uint64_t *keys_in, const int32_t *vals_in, uint64_t *keys_out, int32_t *vals_out,
+                          const int64_t *n_dev, int64_t n_max, void *ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace salf

@@ -58,6 +58,68 @@ def test_u64_depth_keys_stable(n):
     assert np.array_equal(np.argsort(z, kind="stable"), order)
 
 
+def _sort_unique(keys: np.ndarray, vals: np.ndarray, n_dev=None):
+    from paper_2507_18713_b200 import _lib
+    lib = _lib.load()
+    n = keys.size
+    kin = torch.from_numpy(keys.view(np.int64)).cuda()
+    vin = torch.from_numpy(vals).cuda()
+    kout = torch.full_like(kin, -1)
+    vout = torch.full_like(vin, -1)
+    nd = torch.tensor([n_dev], dtype=torch.int64, device="cuda") if n_dev is not None else None
+    wsb = lib.salf_sort_pairs_unique_workspace_bytes()
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.salf_sort_pairs_unique(kin.data_ptr(), vin.data_ptr(), kout.data_ptr(), vout.data_ptr(),
+                                          _lib.ptr(nd), n, ws.data_ptr(), wsb, _lib.stream_ptr()), "sort_unique")
+    torch.cuda.synchronize()
+    return kout.cpu().numpy().view(np.uint64), vout.cpu().numpy(), kin.cpu().numpy().view(np.uint64)
+
+
+def _depth_keys(z):
+    bits = z.view(np.uint64)
+    return np.where(bits >> 63 == 1, ~bits, bits | (np.uint64(1) << np.uint64(63))).astype(np.uint64)
+
+
+@pytest.mark.parametrize("n,kind", [(1, "rand"), (2, "rand"), (1023, "rand"), (4097, "ties"), (640_000, "ties"),
+                                    (2_000_000, "rand"), (300_000, "const"), (300_000, "sorted"),
+                                    (300_000, "two"), (300_000, "periodic")])
+def test_unique_pair_sort_matches_stable_sort(n, kind):
+    """The depth-rank bucket sort: the stable sort's permutation for value-
+    ordered input, including all-equal keys (every element in one key: the
+    splitters split on the value) and inputs skewed against the samples."""
+    rng = np.random.default_rng(n)
+    if kind == "rand":
+        z = rng.uniform(0.05, 200.0, n)
+    elif kind == "ties":
+        z = rng.uniform(0.05, 200.0, n)
+        z[rng.integers(0, n, n // 3)] = z[0]
+    elif kind == "const":
+        z = np.full(n, 3.25)
+    elif kind == "sorted":
+        z = np.sort(rng.uniform(0.05, 200.0, n))[::-1].copy()
+    elif kind == "two":
+        z = np.where(rng.random(n) < 0.999, 1.0, 2.0)
+    else:
+        z = np.where(np.arange(n) % 4096 == 0, 1.0, 5.0 + rng.random(n))
+    keys = _depth_keys(z)
+    vals = np.arange(n, dtype=np.int32)
+    ko, vo, kin = _sort_unique(keys, vals)
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(vo, order)
+    assert np.array_equal(ko, keys[order])
+    assert np.array_equal(kin, keys), "input keys modified"
+
+
+def test_unique_pair_sort_device_count():
+    rng = np.random.default_rng(5)
+    n_max, n = 50_000, 31_001
+    keys = _depth_keys(rng.uniform(0.05, 200.0, n_max))
+    vals = np.arange(n_max, dtype=np.int32)
+    ko, vo, _ = _sort_unique(keys, vals, n_dev=n)
+    assert np.array_equal(vo[:n], np.argsort(keys[:n], kind="stable"))
+    assert np.all(vo[n:] == -1), "wrote past the device count"
+
+
 def test_device_count_and_bit_range():
     rng = np.random.default_rng(3)
     n_max, n = 50_000, 37_123
