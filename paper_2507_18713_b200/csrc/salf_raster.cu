@@ -1422,12 +1422,26 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
     for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j], vrange);
     __syncthreads();
     prefetch_next(sc, entries, base + kChunk, end, kChunk);
+    // entries whose footprint meets this warp's pixel rows and columns: one test per entry per
+    // warp (lane l tests entries l and l + 32), the loop below visits only those
+    uint64_t wmask;
+    {
+      bool f0 = false, f1 = false;
+      if (lane < cn) {
+        const EntryF &e = sm[lane];
+        f0 = !(e.vhi < wr0 || e.vlo > wr1 || e.uhi < wc0 || e.ulo > wc1);
+      }
+      if (lane + 32 < cn) {
+        const EntryF &e = sm[lane + 32];
+        f1 = !(e.vhi < wr0 || e.vlo > wr1 || e.uhi < wc0 || e.ulo > wc1);
+      }
+      wmask = ((uint64_t)__ballot_sync(0xffffffffu, f1) << 32) | __ballot_sync(0xffffffffu, f0);
+    }
     if (alive) {
       uint64_t hbm = 0ull;  // included hits of this chunk (bit j: list position base - beg + j)
-      for (int j = 0; j < cn; ++j) {
+      for (uint64_t m = wmask; m; m &= m - 1) {
+        const int j = __ffsll((long long)m) - 1;
         const EntryF &e = sm[j];
-        // footprint misses this warp's pixel rows or columns (warp-uniform)
-        if (e.vhi < wr0 || e.vlo > wr1 || e.uhi < wc0 || e.ulo > wc1) continue;
         const RayF *ray = &r;
         RayF rr;
         if (kRot && e.rot) {  // the pixel ray in the voxel's frame (render_raster.py:191-196)
@@ -1951,6 +1965,7 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
   extern __shared__ __align__(16) float xp_dyn[];
   float(*xp)[kXpRows][kXpCols] = reinterpret_cast<float(*)[kXpRows][kXpCols]>(xp_dyn);
   __shared__ double s_iv[256 * 3];  // per pixel slot: fp64 1/d (bwd_pair64)
+  __shared__ uint32_t s_wm[kW];     // per warp: entries of the chunk it includes
   __shared__ int s_max;
   const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
@@ -2043,12 +2058,13 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     uint32_t wb0 = 0u, wb1 = 0u;  // hit words of this chunk
     if (in[0] && jb < bp[0].n_stop) wb0 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + slot[0]);
     if (in[1] && jb < bp[1].n_stop) wb1 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + slot[1]);
-    for (int j = cn - 1; j >= 0; --j) {
+    // entries some pixel of this warp includes, back to front (the block reduction below reads
+    // red[j][w] only where warp w's mask has bit j)
+    const uint32_t wmask = __reduce_or_sync(0xffffffffu, wb0 | wb1);
+    if (lane == 0) s_wm[warp] = wmask;
+    for (uint32_t m = wmask; m; m &= ~(1u << (31 - __clz(m)))) {
+      const int j = 31 - __clz(m);
       const bool h0 = (wb0 >> j) & 1u, h1 = (wb1 >> j) & 1u;
-      if (!__any_sync(0xffffffffu, h0 || h1)) {  // no pixel of this warp includes entry j
-        if (lane < kGradStride) red[j][warp][lane] = 0.f;
-        continue;
-      }
       const EntryF &e = sm[j];
       Hit2 hh;
       hh.x[0] = hh.x[1] = hh.x[2] = f2(0.f);
@@ -2109,7 +2125,9 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     __syncthreads();
     for (int t = threadIdx.x; t < cn * kGradStride; t += 128) {
       const int j = t / kGradStride, k = t - j * kGradStride;
-      const float sum = (red[j][0][k] + red[j][1][k]) + (red[j][2][k] + red[j][3][k]);
+      const float r0 = (s_wm[0] >> j) & 1u ? red[j][0][k] : 0.f, r1 = (s_wm[1] >> j) & 1u ? red[j][1][k] : 0.f;
+      const float r2 = (s_wm[2] >> j) & 1u ? red[j][2][k] : 0.f, r3 = (s_wm[3] >> j) & 1u ? red[j][3][k] : 0.f;
+      const float sum = (r0 + r1) + (r2 + r3);
       if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
       else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
     }
@@ -2276,8 +2294,10 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
       const int64_t npx = (int64_t)c.width * c.height;
       const unsigned rb = (unsigned)((npx + 127) / 128);
       const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
+      // whole warps (the per-chunk footprint masks are warp ballots); slots past tile^2 idle
 #define SALF_LAUNCH_FWD(ROT, SDF)                                                                             \
-  k_composite_fast<ROT, SDF><<<n_tiles, threads, 0, st>>>(*scene, c, *opts, offsets, entries, out_rgb, out_opacity, \
+  k_composite_fast<ROT, SDF><<<n_tiles, (threads + 31) & ~31, 0, st>>>(*scene, c, *opts, offsets, entries,         \
+                                                                      out_rgb, out_opacity,                         \
                                                          out_depth, saved, vrange, tile_order, hitbits)
       if (rot) {
         if (sdf) SALF_LAUNCH_FWD(true, true); else SALF_LAUNCH_FWD(true, false);

@@ -154,7 +154,7 @@ def test_tile_size_scheduling_backward(golden, golden_meta, tile, exact):
     ga = RR.rasterize_backward(sa, dc, dd, as_dict=False)
     gb = RR.rasterize_backward(sb, dc, dd, as_dict=False)
     err = ((ga - gb).abs().max(dim=0).values / ga.abs().max(dim=0).values.clamp_min(1e-30)).max()
-    assert float(err) < 1e-5
+    assert float(err) < 1e-5, float(err)
 
 
 @pytest.mark.parametrize("exact", [True, False], ids=["fp64", "mixed"])
