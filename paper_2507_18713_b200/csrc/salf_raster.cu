@@ -1949,6 +1949,72 @@ __device__ __forceinline__ bool pair64_into(const salf_scene_t &sc, const EntryF
   return true;
 }
 
+#ifndef SALF_BWD_PAIR2
+#define SALF_BWD_PAIR2 1  // both pixels' fp64 chords as one straight-line block (0: one divergent pass per pixel)
+#endif
+
+// bwd_pair64 for BOTH pixels of a thread at once: the two fp64 chord chains
+// are independent, so interleaving them halves the exposed DFMA latency of
+// the per-pixel passes (which the warp runs back to back whenever any lane
+// has each pixel hit -- nearly always).  Rotated voxels and rays with a zero
+// component take bwd_pair per pixel.
+template <bool kRot, bool kDepth>
+__device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF &e, const BwdPix bp[2],
+                                            const double *__restrict__ iv0, const double *__restrict__ iv1, bool h0,
+                                            bool h1, Hit2 &h) {
+  const bool gen0 = h0 && ((kRot && e.rot) || !bp[0].r.fast), gen1 = h1 && ((kRot && e.rot) || !bp[1].r.fast);
+  const bool f0 = h0 && !gen0, f1 = h1 && !gen1;
+  bool act = false;
+  if (f0 || f1) {
+    const double *ivp[2] = {iv0, iv1};
+    double ts[2], u0[2], u1[2];
+    float qf[2][3];
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      const RayF &r = bp[l].r;
+      ts[l] = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
+      u0[l] = r.tn0 - ts[l];
+      u1[l] = INFINITY;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+      for (int l = 0; l < 2; ++l) {
+        const double qk = fma(ts[l], bp[l].r.d[k], e.o[k]);
+        const double ik = ivp[l][k];
+        const double hk = e.half * fabs(ik);
+        u0[l] = fmax(u0[l], fma(-qk, ik, -hk));
+        u1[l] = fmin(u1[l], fma(-qk, ik, hk));
+        qf[l][k] = (float)qk;
+      }
+    }
+    const bool ok0 = f0 && u1[0] > u0[0] + 1e-12, ok1 = f1 && u1[1] > u0[1] + 1e-12;
+    float um[2], dl[2], dq[2];
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      dl[l] = (float)(u1[l] - u0[l]);
+      um[l] = (float)(0.5 * (u0[l] + u1[l]));
+      dq[l] = kDepth ? (float)(ts[l] - bp[l].D) + um[l] : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float x0 = __fmaf_rn(um[0], bp[0].r.df[k], qf[0][k]) * e.inv_hf;
+      const float x1 = __fmaf_rn(um[1], bp[1].r.df[k], qf[1][k]) * e.inv_hf;
+      h.x[k] = make_float2(ok0 ? x0 : 0.f, ok1 ? x1 : 0.f);
+    }
+    h.delta = make_float2(ok0 ? dl[0] : 0.f, ok1 ? dl[1] : 0.f);
+    h.dq = make_float2(ok0 ? dq[0] : 0.f, ok1 ? dq[1] : 0.f);
+    if (kRot) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) h.gm[m] = make_float2(ok0 ? bp[0].r.gam[m] : 0.f, ok1 ? bp[1].r.gam[m] : 0.f);
+    }
+    act = ok0 || ok1;
+  }
+  if (gen0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], iv0, h, 0);
+  if (gen1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], iv1, h, 1);
+  return act;
+}
+
 template <bool kRot, bool sdf, bool kDepth>
 __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
@@ -2071,8 +2137,12 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
       hh.delta = hh.dq = f2(0.f);
       if (kRot) hh.gm[0] = hh.gm[1] = hh.gm[2] = hh.gm[3] = f2(0.f);
       bool act = false;
+#if SALF_BWD_PAIR2
+      act = pair64_both<kRot, kDepth>(sc, e, bp, s_iv + slot[0] * 3, s_iv + slot[1] * 3, h0, h1, hh);
+#else
       if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + slot[0] * 3, hh, 0);
       if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + slot[1] * 3, hh, 1);
+#endif
       float tot = 0.0f;
       if (__any_sync(0xffffffffu, act)) {
         float g[32];
