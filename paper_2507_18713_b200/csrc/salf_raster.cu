@@ -1311,6 +1311,31 @@ __device__ __forceinline__ void prefetch_next(const salf_scene_t &sc, const int3
 #endif
 }
 
+// Split form: the entry index is loaded before the current chunk is staged
+// (its latency hides behind the staging) and the prefetches issued after.
+__device__ __forceinline__ int32_t prefetch_index(const int32_t *__restrict__ entries, int64_t first, int64_t lo,
+                                                  int64_t hi, int chunk) {
+#if SALF_PREFETCH
+  const int64_t j = first + threadIdx.x;
+  return (threadIdx.x < chunk && j >= lo && j < hi) ? __ldg(entries + j) : -1;
+#else
+  (void)entries; (void)first; (void)lo; (void)hi; (void)chunk;
+  return -1;
+#endif
+}
+__device__ __forceinline__ void prefetch_voxel(const salf_scene_t &sc, int32_t v) {
+#if SALF_PREFETCH
+  if (v >= 0) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.geo + 4 * (int64_t)v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.aux + 4 * (int64_t)v));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.prm + (int64_t)v * SALF_PRM_STRIDE));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(sc.prm + (int64_t)v * SALF_PRM_STRIDE + 24));
+  }
+#else
+  (void)sc; (void)v;
+#endif
+}
+
 // Same for the backward's back-to-front walk: the chunk before `prev` + chunk.
 __device__ __forceinline__ void prefetch_prev(const salf_scene_t &sc, const int32_t *__restrict__ entries,
                                               int64_t prev, int64_t beg, int chunk) {
@@ -1418,10 +1443,11 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
   const int64_t hb_base = hit_word_base(beg, tile_id);
   for (int64_t base = beg; base < end; base += kChunk) {
     const int cn = (int)min((int64_t)kChunk, end - base);
+    const int32_t pf = prefetch_index(entries, base + kChunk, beg, end, kChunk);
     __syncthreads();
     for (int j = threadIdx.x; j < cn; j += nthreads) stage_entry_f<kRot>(sc, c, entries[base + j], sm[j], vrange);
     __syncthreads();
-    prefetch_next(sc, entries, base + kChunk, end, kChunk);
+    prefetch_voxel(sc, pf);
     // entries whose footprint meets this warp's pixel rows and columns: one test per entry per
     // warp (lane l tests entries l and l + 32), the loop below visits only those
     uint64_t wmask;
@@ -1438,9 +1464,14 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
       wmask = ((uint64_t)__ballot_sync(0xffffffffu, f1) << 32) | __ballot_sync(0xffffffffu, f0);
     }
     if (alive) {
-      uint64_t hbm = 0ull;  // included hits of this chunk (bit j: list position base - beg + j)
-      for (uint64_t m = wmask; m; m &= m - 1) {
-        const int j = __ffsll((long long)m) - 1;
+      // the chunk's two 32-entry halves (32-bit bit scans and masks), each ending with its hit
+      // word (bit jj: list position base - beg + 32 half + jj is an included hit).  A pixel that
+      // stops in the first half never has its second word read (the backward reads words below
+      // its stop index only).
+      for (int half = 0; half < 2 && alive && (half == 0 || cn > 32); ++half) {
+      uint32_t hb = 0u;
+      for (uint32_t m = half ? (uint32_t)(wmask >> 32) : (uint32_t)wmask; m; m &= m - 1) {
+        const int jj = __ffs(m) - 1, j = jj + 32 * half;
         const EntryF &e = sm[j];
         const RayF *ray = &r;
         RayF rr;
@@ -1485,7 +1516,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
           n_stop = (int)(base - beg) + j;
           break;
         }
-        hbm |= 1ull << j;
+        hb |= 1u << jj;
         float x[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
@@ -1518,10 +1549,7 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
         T = fast_exp(-(Yh + Yc));
         ++n_inc;
       }
-      if (hitbits) {
-        uint32_t *hw = hitbits + hb_base + (int64_t)((base - beg) >> 5) * kHitSlots + pslot;
-        hw[0] = (uint32_t)hbm;
-        if (cn > 32) hw[kHitSlots] = (uint32_t)(hbm >> 32);
+      if (hitbits) hitbits[hb_base + (int64_t)(((base - beg) >> 5) + half) * kHitSlots + pslot] = hb;
       }
     }
     if (!__syncthreads_or(alive)) break;
@@ -2102,6 +2130,7 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
   for (int64_t base = beg + ((lim - beg - 1) / kChunkB) * kChunkB; base >= beg && lim > beg; base -= kChunkB) {
     const int cn = (int)min((int64_t)kChunkB, lim - base);
     __syncthreads();
+    const int32_t pf = prefetch_index(entries, base - kChunkB, beg, lim, kChunkB);
     for (int j = threadIdx.x; j < cn; j += 128) {
       EntryF &e = sm[j];
       stage_entry_f<kRot>(sc, c, entries[base + j], e, vrange);
@@ -2119,7 +2148,7 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
       pp[28] = f2(ha * e.inv_b);
     }
     __syncthreads();
-    prefetch_prev(sc, entries, base - kChunkB, beg, kChunkB);
+    prefetch_voxel(sc, pf);
     const int jb = (int)(base - beg);
     uint32_t wb0 = 0u, wb1 = 0u;  // hit words of this chunk
     if (in[0] && jb < bp[0].n_stop) wb0 = __ldg(hitbits + hb + (int64_t)(jb >> 5) * kHitSlots + slot[0]);
