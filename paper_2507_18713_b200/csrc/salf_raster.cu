@@ -2002,8 +2002,9 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
       const RayF &r = bp[l].r;
       ts[l] = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
       u0[l] = r.tn0 - ts[l];
-      u1[l] = INFINITY;
     }
+    // plain compare-selects: every value here is finite (fast rays), so fmax / fmin's NaN
+    // handling (several extra instructions per call on sm_100) is not needed
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
 #pragma unroll
@@ -2011,8 +2012,9 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
         const double qk = fma(ts[l], bp[l].r.d[k], e.o[k]);
         const double ik = ivp[l][k];
         const double hk = e.half * fabs(ik);
-        u0[l] = fmax(u0[l], fma(-qk, ik, -hk));
-        u1[l] = fmin(u1[l], fma(-qk, ik, hk));
+        const double n = fma(-qk, ik, -hk), f = fma(-qk, ik, hk);
+        u0[l] = n > u0[l] ? n : u0[l];
+        u1[l] = (k == 0 || f < u1[l]) ? f : u1[l];
         qf[l][k] = (float)qk;
       }
     }
@@ -2222,13 +2224,20 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
       if (lane < kGradStride) red[j][warp][lane] = tot;
     }
     __syncthreads();
+#ifdef SALF_AB_NOFINAL
+    if (false)
+#endif
     for (int t = threadIdx.x; t < cn * kGradStride; t += 128) {
       const int j = t / kGradStride, k = t - j * kGradStride;
       const float r0 = (s_wm[0] >> j) & 1u ? red[j][0][k] : 0.f, r1 = (s_wm[1] >> j) & 1u ? red[j][1][k] : 0.f;
       const float r2 = (s_wm[2] >> j) & 1u ? red[j][2][k] : 0.f, r3 = (s_wm[3] >> j) & 1u ? red[j][3][k] : 0.f;
       const float sum = (r0 + r1) + (r2 + r3);
       if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
+#ifndef SALF_AB_NOATOM
       else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
+#else
+      else if (sum == 12345.f) grad[0] = sum;  // A/B only
+#endif
     }
   }
 }
