@@ -332,7 +332,10 @@ __device__ __forceinline__ void bitonic_sort(int n, KeyAt key, ValAt val) {
 
 // splitters: kBktOver * kBuckets evenly spaced samples sorted in one CTA, every
 // kBktOver-th kept (oversampling evens out the bucket sizes)
-constexpr int kBktOver = 4;
+#ifndef SALF_BKT_OVER
+#define SALF_BKT_OVER 2
+#endif
+constexpr int kBktOver = SALF_BKT_OVER;
 __global__ void __launch_bounds__(1024) k_bkt_splitters(const uint64_t *__restrict__ kin,
                                                         const int32_t *__restrict__ vin,
                                                         const int64_t *__restrict__ n_dev, int64_t n_max,

@@ -38,6 +38,18 @@ for mode in (0, 1):
         if i >= 3:
             ts.append(a.elapsed_time(b))
     out[f"mode{mode}_bin_ms"] = float(np.median(ts))
+    # device time alone: a spin kernel ahead of the start event keeps the host enqueue off the clock
+    ts = []
+    for i in range(23):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)
+        a.record()
+        RR._bin(ds, cam, near, tile, proj, mode)
+        b.record()
+        b.synchronize()
+        if i >= 3:
+            ts.append(a.elapsed_time(b))
+    out[f"mode{mode}_bin_device_ms"] = float(np.median(ts))
     ts = []
     for i in range(13):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
