@@ -2045,6 +2045,10 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
   return act;
 }
 
+#ifndef SALF_BWD_WARPATOM
+#define SALF_BWD_WARPATOM 1  // each warp adds its entry totals itself (0: block reduction, then one atomic per component)
+#endif
+
 template <bool kRot, bool sdf, bool kDepth>
 __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
@@ -2221,23 +2225,25 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
         __syncwarp();
 #endif
       }
+#if SALF_BWD_WARPATOM
+      if (!partial) {  // each warp adds its own entry totals (no block reduction, no end-of-chunk barrier)
+        if (lane < kGradStride && tot != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + lane, (double)tot);
+        continue;
+      }
+#endif
       if (lane < kGradStride) red[j][warp][lane] = tot;
     }
-    __syncthreads();
-#ifdef SALF_AB_NOFINAL
-    if (false)
+#if SALF_BWD_WARPATOM
+    if (!partial) continue;
 #endif
+    __syncthreads();
     for (int t = threadIdx.x; t < cn * kGradStride; t += 128) {
       const int j = t / kGradStride, k = t - j * kGradStride;
       const float r0 = (s_wm[0] >> j) & 1u ? red[j][0][k] : 0.f, r1 = (s_wm[1] >> j) & 1u ? red[j][1][k] : 0.f;
       const float r2 = (s_wm[2] >> j) & 1u ? red[j][2][k] : 0.f, r3 = (s_wm[3] >> j) & 1u ? red[j][3][k] : 0.f;
       const float sum = (r0 + r1) + (r2 + r3);
       if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
-#ifndef SALF_AB_NOATOM
       else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
-#else
-      else if (sum == 12345.f) grad[0] = sum;  // A/B only
-#endif
     }
   }
 }

@@ -407,7 +407,11 @@ def test_raster_backward_deterministic_mode(golden, golden_meta, exact, rand300_
     from paper_2507_18713_b200.device import grads_to_dict
     assert_grads(grads_to_dict(runs[0]), want, rand300_mag)
     atomic = RR.rasterize_backward(st, dc, dd, as_dict=False)
-    torch.testing.assert_close(runs[0], atomic, rtol=1e-6, atol=1e-12)
+    # the atomic mode adds each warp's fp32 entry totals in fp64, the deterministic mode rounds
+    # a tile's sum over its warps to one fp32 partial row: they differ by that rounding
+    # (<= 2^-24 of a tile partial), bounded here per parameter column
+    col_max = atomic.abs().amax(dim=0, keepdim=True).clamp_min(1e-300)
+    assert bool(((runs[0] - atomic).abs() <= 1e-6 * atomic.abs() + 1e-6 * col_max).all())
 
 
 @pytest.mark.parametrize("case", ["integ", "fd"])
