@@ -1851,6 +1851,10 @@ __device__ __forceinline__ float2 expm1_neg2(float2 x) {
 constexpr int kXpRows = SALF_BWD_XPCOL ? 27 : 32, kXpCols = SALF_BWD_XPCOL ? 36 : 28;
 constexpr size_t kXpBytes = sizeof(float) * 4 * kXpRows * kXpCols;  // 4 warps
 
+#ifndef SALF_BWD_HALF
+#define SALF_BWD_HALF 1  // atomic mode: two 2-warp CTAs per tile (0: one 4-warp CTA)
+#endif
+
 // per-entry field constants, each duplicated (p, p) so a packed op reads it as
 // one 64-bit shared-memory operand: w_s 0..3, w_c 4..12, w_sh 13..24, a 25,
 // 1/b 26, a/2 27, (a/2)(1/b) 28
@@ -2049,25 +2053,33 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
 #define SALF_BWD_WARPATOM 1  // each warp adds its entry totals itself (0: block reduction, then one atomic per component)
 #endif
 
-template <bool kRot, bool sdf, bool kDepth>
-__global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
+// kW warps per CTA: 4 (a whole 16 x 16 tile; the deterministic mode, whose
+// instance rows need one CTA per tile) or 2 (half a tile: two CTAs per tile,
+// each staging the tile's list for its own 16 x 8 half).  With 2 the warps
+// that meet at each chunk barrier are 2, not 4: less time lost to the
+// slowest warp of the chunk, for twice the staging work.
+template <bool kRot, bool sdf, bool kDepth, int kW>
+__global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_hits(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
     const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial,
     const int32_t *__restrict__ vrange, const int32_t *__restrict__ tile_order,
     const uint32_t *__restrict__ hitbits) {
   static_assert(kChunkB == 32, "hit words: one 32-entry word per staged chunk");
-  constexpr int kW = 4;  // warps
+  static_assert(kW == 2 || kW == 4, "a CTA covers a whole tile or half of one");
+  constexpr int kParts = 4 / kW, kThreads = 32 * kW;
   __shared__ EntryF sm[kChunkB];
   __shared__ __align__(16) float2 spp[kChunkB][kPP];
-  __shared__ float red[kChunkB][kW][kGradStride];
+  // per-warp entry totals for the CTA's fixed-order sum (deterministic mode: kW == 4 only)
+  __shared__ float red[kW == 4 ? kChunkB : 1][kW][kGradStride];
   // warp-reduction scratch in dynamic shared memory (static + this exceed the 48 KB static limit)
   extern __shared__ __align__(16) float xp_dyn[];
   float(*xp)[kXpRows][kXpCols] = reinterpret_cast<float(*)[kXpRows][kXpCols]>(xp_dyn);
-  __shared__ double s_iv[256 * 3];  // per pixel slot: fp64 1/d (bwd_pair64)
+  __shared__ double s_iv[2 * kThreads * 3];  // per pixel slot of this CTA: fp64 1/d (bwd_pair64)
   __shared__ uint32_t s_wm[kW];     // per warp: entries of the chunk it includes
   __shared__ int s_max;
-  const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
+  const int tslot = (int)blockIdx.x / kParts, part = (int)blockIdx.x % kParts;
+  const int tile_id = tile_order ? __ldg(tile_order + tslot) : tslot;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   const int npix = c.tile * c.tile;
   const int64_t beg = offsets[tile_id];
@@ -2081,14 +2093,17 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
   // 8 x 8 block (lane -> column, two vertically adjacent rows), so a warp's pixels see nearly the
   // same entries (more entries skipped by the whole warp, fewer idle lanes in the packed pass)
   int slot[2];
-  const int lane0 = threadIdx.x & 31, wid0 = threadIdx.x >> 5;
+  const int lane0 = threadIdx.x & 31, wid0 = part * kW + (threadIdx.x >> 5);  // warp within the tile
+  const int t0 = part * kThreads + threadIdx.x;                            // thread within the tile
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     if (SALF_BWD_BLOCK && c.tile == 16)
       slot[k] = ((wid0 >> 1) * 8 + (lane0 >> 3) * 2 + k) * 16 + (wid0 & 1) * 8 + (lane0 & 7);
     else
-      slot[k] = threadIdx.x + k * 128;
+      slot[k] = t0 + k * 128;
   }
+  // s_iv row of each pixel: this CTA's pixel k of thread t
+  const int ivrow[2] = {threadIdx.x, kThreads + (int)threadIdx.x};
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int li = slot[k];
@@ -2098,7 +2113,7 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     if (in[k]) {
       bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, bp[k]);
 #pragma unroll
-      for (int a = 0; a < 3; ++a) s_iv[li * 3 + a] = 1.0 / bp[k].r.d[a];
+      for (int a = 0; a < 3; ++a) s_iv[ivrow[k] * 3 + a] = 1.0 / bp[k].r.d[a];
     } else {
       // idle slot (outside the image): finite state, never hit (n_stop 0); its lane of the
       // packed chain must stay finite (0 * NaN would poison the warp sums)
@@ -2137,7 +2152,7 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
     const int cn = (int)min((int64_t)kChunkB, lim - base);
     __syncthreads();
     const int32_t pf = prefetch_index(entries, base - kChunkB, beg, lim, kChunkB);
-    for (int j = threadIdx.x; j < cn; j += 128) {
+    for (int j = threadIdx.x; j < cn; j += kThreads) {
       EntryF &e = sm[j];
       stage_entry_f<kRot>(sc, c, entries[base + j], e, vrange);
       float2 *pp = spp[j];
@@ -2173,10 +2188,10 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
       if (kRot) hh.gm[0] = hh.gm[1] = hh.gm[2] = hh.gm[3] = f2(0.f);
       bool act = false;
 #if SALF_BWD_PAIR2
-      act = pair64_both<kRot, kDepth>(sc, e, bp, s_iv + slot[0] * 3, s_iv + slot[1] * 3, h0, h1, hh);
+      act = pair64_both<kRot, kDepth>(sc, e, bp, s_iv + ivrow[0] * 3, s_iv + ivrow[1] * 3, h0, h1, hh);
 #else
-      if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + slot[0] * 3, hh, 0);
-      if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + slot[1] * 3, hh, 1);
+      if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + ivrow[0] * 3, hh, 0);
+      if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + ivrow[1] * 3, hh, 1);
 #endif
       float tot = 0.0f;
       if (__any_sync(0xffffffffu, act)) {
@@ -2231,17 +2246,21 @@ __global__ void __launch_bounds__(128, SALF_BWDF_MINB) k_backward_hits(
         continue;
       }
 #endif
-      if (lane < kGradStride) red[j][warp][lane] = tot;
+      if constexpr (kW == 4) {
+        if (lane < kGradStride) red[j][warp][lane] = tot;
+      }
     }
 #if SALF_BWD_WARPATOM
     if (!partial) continue;
 #endif
+    if constexpr (kW != 4) continue;  // (the deterministic mode launches whole-tile CTAs)
     __syncthreads();
-    for (int t = threadIdx.x; t < cn * kGradStride; t += 128) {
+    for (int t = threadIdx.x; t < cn * kGradStride; t += kThreads) {
       const int j = t / kGradStride, k = t - j * kGradStride;
-      const float r0 = (s_wm[0] >> j) & 1u ? red[j][0][k] : 0.f, r1 = (s_wm[1] >> j) & 1u ? red[j][1][k] : 0.f;
-      const float r2 = (s_wm[2] >> j) & 1u ? red[j][2][k] : 0.f, r3 = (s_wm[3] >> j) & 1u ? red[j][3][k] : 0.f;
-      const float sum = (r0 + r1) + (r2 + r3);
+      float r[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) r[w] = (w < kW && ((s_wm[w % kW] >> j) & 1u)) ? red[j][w % kW][k] : 0.f;
+      const float sum = (r[0] + r[1]) + (r[2] + r[3]);
       if (partial) partial[(base + j) * kGradStride + k] = sum;  // deterministic mode: one row per instance
       else if (sum != 0.0f) atomicAdd(grad + sm[j].vid * kGradStride + k, (double)sum);
     }
@@ -2458,12 +2477,18 @@ static int raster_backward_launch(const salf_scene_t *scene, const salf_camera_t
     if (hitbits) {                                                                                          \
       static bool attr = false;                                                                             \
       if (!attr) {                                                                                          \
-        cudaFuncSetAttribute(k_backward_hits<ROT, SDF, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+        cudaFuncSetAttribute(k_backward_hits<ROT, SDF, DEPTH, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                              (int)kXpBytes);                                                                \
+        cudaFuncSetAttribute(k_backward_hits<ROT, SDF, DEPTH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)(kXpBytes / 2));                                                          \
         attr = true;                                                                                        \
       }                                                                                                     \
-      k_backward_hits<ROT, SDF, DEPTH><<<n_tiles, 128, kXpBytes, st>>>(                                      \
-          *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, hitbits); \
+      if (partial || !SALF_BWD_HALF)                                                                        \
+        k_backward_hits<ROT, SDF, DEPTH, 4><<<n_tiles, 128, kXpBytes, st>>>(                                 \
+            *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, hitbits); \
+      else                                                                                                  \
+        k_backward_hits<ROT, SDF, DEPTH, 2><<<2 * n_tiles, 64, kXpBytes / 2, st>>>(                          \
+            *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order, hitbits); \
     } else                                                                                                  \
       k_backward_fast<ROT, SALF_BWD_NP, SDF, DEPTH><<<n_tiles, threads_np, 0, st>>>(                        \
           *scene, c, *opts, offsets, entries, saved, d_rgb, d_depth, grad, partial, vrange, tile_order);    \
