@@ -1381,6 +1381,9 @@ __device__ __forceinline__ bool pair_hit_ref64(const RayF &r, const EntryF &e, d
 #ifndef SALF_FWDF_MINB
 #define SALF_FWDF_MINB 3
 #endif
+#ifndef SALF_FWD_HALF
+#define SALF_FWD_HALF 1  // 16 x 16 tiles: two 4-warp CTAs per tile (0: one 8-warp CTA)
+#endif
 template <bool kRot, bool sdf>
 __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
                                                         const int64_t *__restrict__ offsets,
@@ -1389,15 +1392,18 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
                                                         float *__restrict__ out_depth, double *__restrict__ saved,
                                                         const int32_t *__restrict__ vrange,
                                                         const int32_t *__restrict__ tile_order,
-                                                        uint32_t *__restrict__ hitbits) {
+                                                        uint32_t *__restrict__ hitbits, int parts) {
   static_assert(kChunk == 64, "hit words: two 32-entry words per staged chunk");
   __shared__ EntryF sm[kChunk];
   // heaviest tiles first (tile_order: tiles by list length, descending) -> no ragged last wave
-  const int tile_id = tile_order ? __ldg(tile_order + blockIdx.x) : (int)blockIdx.x;
+  // parts == 2 (16 x 16 tiles): two 4-warp CTAs per tile, one per 16 x 8 half (fewer warps meet
+  // at each chunk barrier); parts == 1: one CTA per tile
+  const int tslot = (int)blockIdx.x / parts, part = (int)blockIdx.x % parts;
+  const int tile_id = tile_order ? __ldg(tile_order + tslot) : tslot;
   const int tx = tile_id % c.tiles_x, ty = tile_id / c.tiles_x;
   // 16 x 16 tiles: warp w shades the 8 x 4 pixel block (w & 1, w >> 1) of the tile, so the
   // per-entry footprint test below culls on columns as well as rows; other tile sizes: rows
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wid = part * ((int)blockDim.x >> 5) + (threadIdx.x >> 5);
   const bool blocks = c.tile == 16;
   const int lx = blocks ? (wid & 1) * 8 + (lane & 7) : threadIdx.x % c.tile;
   const int ly = blocks ? (wid >> 1) * 4 + (lane >> 3) : threadIdx.x / c.tile;
@@ -2427,11 +2433,14 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
       const int64_t npx = (int64_t)c.width * c.height;
       const unsigned rb = (unsigned)((npx + 127) / 128);
       const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
-      // whole warps (the per-chunk footprint masks are warp ballots); slots past tile^2 idle
+      // whole warps (the per-chunk footprint masks are warp ballots); slots past tile^2 idle.
+      // 16 x 16 tiles: two 128-thread CTAs per tile (16 x 8 halves)
+      const int fparts = (opts->tile == 16 && SALF_FWD_HALF) ? 2 : 1;
+      const int fthreads = ((threads + 31) & ~31) / fparts;
 #define SALF_LAUNCH_FWD(ROT, SDF)                                                                             \
-  k_composite_fast<ROT, SDF><<<n_tiles, (threads + 31) & ~31, 0, st>>>(*scene, c, *opts, offsets, entries,         \
-                                                                      out_rgb, out_opacity,                         \
-                                                         out_depth, saved, vrange, tile_order, hitbits)
+  k_composite_fast<ROT, SDF><<<n_tiles * fparts, fthreads, 0, st>>>(*scene, c, *opts, offsets, entries,       \
+                                                                    out_rgb, out_opacity, out_depth, saved,  \
+                                                                    vrange, tile_order, hitbits, fparts)
       if (rot) {
         if (sdf) SALF_LAUNCH_FWD(true, true); else SALF_LAUNCH_FWD(true, false);
         if (!no_redo)
