@@ -1381,8 +1381,8 @@ __device__ __forceinline__ bool pair_hit_ref64(const RayF &r, const EntryF &e, d
 #ifndef SALF_FWDF_MINB
 #define SALF_FWDF_MINB 3
 #endif
-#ifndef SALF_FWD_HALF
-#define SALF_FWD_HALF 1  // 16 x 16 tiles: two 4-warp CTAs per tile (0: one 8-warp CTA)
+#ifndef SALF_FWD_PARTS
+#define SALF_FWD_PARTS 2  // 16 x 16 tiles: CTAs per tile (1: one 8-warp CTA, 2: 16 x 8 halves, 4: 16 x 4)
 #endif
 template <bool kRot, bool sdf>
 __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt,
@@ -2109,7 +2109,7 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
       slot[k] = t0 + k * 128;
   }
   // s_iv row of each pixel: this CTA's pixel k of thread t
-  const int ivrow[2] = {threadIdx.x, kThreads + (int)threadIdx.x};
+  const int ivrow[2] = {(int)threadIdx.x, kThreads + (int)threadIdx.x};
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int li = slot[k];
@@ -2434,8 +2434,8 @@ extern "C" int salf_raster_composite(const salf_scene_t *scene, const salf_camer
       const unsigned rb = (unsigned)((npx + 127) / 128);
       const bool sdf = scene->density_mode == SALF_DENSITY_SDF;
       // whole warps (the per-chunk footprint masks are warp ballots); slots past tile^2 idle.
-      // 16 x 16 tiles: two 128-thread CTAs per tile (16 x 8 halves)
-      const int fparts = (opts->tile == 16 && SALF_FWD_HALF) ? 2 : 1;
+      // 16 x 16 tiles: SALF_FWD_PARTS CTAs per tile
+      const int fparts = opts->tile == 16 ? SALF_FWD_PARTS : 1;
       const int fthreads = ((threads + 31) & ~31) / fparts;
 #define SALF_LAUNCH_FWD(ROT, SDF)                                                                             \
   k_composite_fast<ROT, SDF><<<n_tiles * fparts, fthreads, 0, st>>>(*scene, c, *opts, offsets, entries,       \
