@@ -59,6 +59,21 @@ for kb, end in ((4, 13), (8, 64)):
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     _lib.check(lib.salf_sort_pairs(keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vo.data_ptr(), kb, nd.data_ptr(),
                                    n, 0, end, ws.data_ptr(), wsb, _lib.stream_ptr()), "sort")
+# splitter bucket sort (the depth rank): device count, all-equal keys (one key, split on the value)
+for const in (False, True):
+    n = 60_000
+    keys = (torch.zeros(n, device="cuda", dtype=torch.int64) + 7 if const
+            else torch.randint(0, 1 << 40, (n,), device="cuda", dtype=torch.int64))
+    vals = torch.arange(n, device="cuda", dtype=torch.int32)
+    ko, vo = torch.empty_like(keys), torch.empty_like(vals)
+    nd = torch.tensor([n - 999], device="cuda", dtype=torch.int64)
+    wsb = lib.salf_sort_pairs_unique_workspace_bytes()
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.salf_sort_pairs_unique(keys.data_ptr(), vals.data_ptr(), ko.data_ptr(), vo.data_ptr(),
+                                          nd.data_ptr(), n, ws.data_ptr(), wsb, _lib.stream_ptr()), "sort_unique")
+# non-16 tile (one CTA per tile, partial warps rounded up) forward + backward
+fb13, st13 = RR.rasterize(flat, cam, tile=13, return_state=True)
+RR.rasterize_backward(st13, dc, dd)
 big = CameraModel(kind="pinhole", width=320, height=256, fx=300.0, fy=300.0, cx=160.0, cy=128.0, position=pos,
                   quaternion=look_at_quaternion(pos, [4.0, 4.0, 2.0]))
 RR._CAPACITY[("cuda:0", 1)] = 5  # forces the re-bin path
