@@ -188,8 +188,40 @@ __device__ __forceinline__ float expm1_neg(float x) {
   return x > -0.25f ? small : fast_exp(x) - 1.0f;
 }
 
+#ifndef SALF_COLOR_PACK
+#define SALF_COLOR_PACK 1  // red and green channels in fp32x2 (FFMA2 with broadcast x / gam)
+#endif
+
 // fp32 colour with a precomputed per-ray SH basis gam = (C0, C1 y, C1 z, C1 x).
+// With SALF_COLOR_PACK the red and green dot products run as one fp32x2 chain
+// (FMUL2 / FFMA2, the x and gam operands broadcast): each half performs the
+// scalar chain's IEEE operations in the same order, so c is bit-identical.
 __device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3], const float gam[4], float c[3]) {
+#if SALF_COLOR_PACK
+  {
+    float2 z = __fmul2_rn(make_float2(p.wc[0], p.wc[3]), make_float2(x[0], x[0]));
+    z = __ffma2_rn(make_float2(p.wc[1], p.wc[4]), make_float2(x[1], x[1]), z);
+    z = __ffma2_rn(make_float2(p.wc[2], p.wc[5]), make_float2(x[2], x[2]), z);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) z = __ffma2_rn(make_float2(p.wsh[k], p.wsh[4 + k]), make_float2(gam[k], gam[k]), z);
+    const float2 t = __fmul2_rn(make_float2(-z.x, -z.y), make_float2(1.4426950408889634f, 1.4426950408889634f));
+    float2 E;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(E.x) : "f"(t.x));
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(E.y) : "f"(t.y));
+    const float2 d = __fadd2_rn(make_float2(1.0f, 1.0f), E);
+    c[0] = fast_rcp(d.x);
+    c[1] = fast_rcp(d.y);
+  }
+  {
+    float z = __fmaf_rn(p.wc[8], x[2], __fmaf_rn(p.wc[7], x[1], p.wc[6] * x[0]));
+    z = __fmaf_rn(p.wsh[8], gam[0], z);
+    z = __fmaf_rn(p.wsh[9], gam[1], z);
+    z = __fmaf_rn(p.wsh[10], gam[2], z);
+    z = __fmaf_rn(p.wsh[11], gam[3], z);
+    c[2] = fast_rcp(1.0f + fast_exp(-z));
+  }
+  return;
+#endif
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     float z = __fmaf_rn(p.wc[3 * i + 2], x[2], __fmaf_rn(p.wc[3 * i + 1], x[1], p.wc[3 * i] * x[0]));
