@@ -1861,9 +1861,9 @@ constexpr size_t kXpBytes = sizeof(float) * 4 * kXpRows * kXpCols;  // 4 warps
 #define SALF_BWD_HALF 1  // atomic mode: two 2-warp CTAs per tile (0: one 4-warp CTA)
 #endif
 
-// per-entry field constants, each duplicated (p, p) so a packed op reads it as
-// one 64-bit shared-memory operand: w_s 0..3, w_c 4..12, w_sh 13..24, a 25,
-// 1/b 26, a/2 27, (a/2)(1/b) 28
+// per-entry field constants, one float each (the packed ops take them as a
+// broadcast .F32 operand): w_s 0..3, w_c 4..12, w_sh 13..24, a 25, 1/b 26,
+// a/2 27, (a/2)(1/b) 28
 constexpr int kPP = 30;
 
 struct Pix2 {
@@ -1880,18 +1880,18 @@ struct Hit2 {
 };
 
 template <bool kRot, bool sdf, bool kDepth>
-__device__ __forceinline__ void bwd_segment2(const float2 *__restrict__ pp, Pix2 &q, const Hit2 &h, float g[32]) {
+__device__ __forceinline__ void bwd_segment2(const float *__restrict__ pp, Pix2 &q, const Hit2 &h, float g[32]) {
   const float2 X0 = h.x[0], X1 = h.x[1], X2 = h.x[2], dl = h.delta;
   const float2 G0 = f2((float)kShC0);
   const float2 G1 = kRot ? h.gm[1] : q.g1, G2 = kRot ? h.gm[2] : q.g2, G3 = kRot ? h.gm[3] : q.g3;
   // fields (scene.py:229-284)
-  const float2 s = fma2(pp[2], X2, fma2(pp[1], X1, fma2(pp[0], X0, pp[3])));
+  const float2 s = fma2(f2(pp[2]), X2, fma2(f2(pp[1]), X1, fma2(f2(pp[0]), X0, f2(pp[3]))));
   float2 ee = f2(0.f), sigma;
   if (sdf) {
-    const float ib = pp[26].x;
+    const float ib = pp[26];
     ee = exp2v(make_float2(-fabsf(s.x) * ib, -fabsf(s.y) * ib));
-    const float2 he = mul2(pp[27], ee);
-    const float2 ahe = add2(pp[25], neg2(he));
+    const float2 he = mul2(f2(pp[27]), ee);
+    const float2 ahe = add2(f2(pp[25]), neg2(he));
     sigma = make_float2(s.x > 0.f ? ahe.x : he.x, s.y > 0.f ? ahe.y : he.y);
   } else {
     sigma = exp2v(s);
@@ -1920,11 +1920,11 @@ __device__ __forceinline__ void bwd_segment2(const float2 *__restrict__ pp, Pix2
   float2 col[3], omcol[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    float2 z = fma2(pp[4 + 3 * i + 2], X2, fma2(pp[4 + 3 * i + 1], X1, mul2(pp[4 + 3 * i], X0)));
-    z = fma2(pp[13 + 4 * i + 0], G0, z);
-    z = fma2(pp[13 + 4 * i + 1], G1, z);
-    z = fma2(pp[13 + 4 * i + 2], G2, z);
-    z = fma2(pp[13 + 4 * i + 3], G3, z);
+    float2 z = fma2(f2(pp[4 + 3 * i + 2]), X2, fma2(f2(pp[4 + 3 * i + 1]), X1, mul2(f2(pp[4 + 3 * i]), X0)));
+    z = fma2(f2(pp[13 + 4 * i + 0]), G0, z);
+    z = fma2(f2(pp[13 + 4 * i + 1]), G1, z);
+    z = fma2(f2(pp[13 + 4 * i + 2]), G2, z);
+    z = fma2(f2(pp[13 + 4 * i + 3]), G3, z);
     const float2 E = exp2v(neg2(z));
     col[i] = rcp2(add2(f2(1.0f), E));
     omcol[i] = mul2(E, col[i]);
@@ -1938,7 +1938,7 @@ __device__ __forceinline__ void bwd_segment2(const float2 *__restrict__ pp, Pix2
   const float2 gs = mul2(mul2(ga, dl), om);  // :66
   float2 ds, gla, glb;
   if (sdf) {
-    const float2 k2e = mul2(pp[28], ee);
+    const float2 k2e = mul2(f2(pp[28]), ee);
     const float2 d = mul2(gs, k2e);
     ds = make_float2(s.x == 0.f ? 0.f : d.x, s.y == 0.f ? 0.f : d.y);  // :92
     gla = mul2(gs, sigma);                                               // :94
@@ -2075,7 +2075,7 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
   static_assert(kW == 2 || kW == 4, "a CTA covers a whole tile or half of one");
   constexpr int kParts = 4 / kW, kThreads = 32 * kW;
   __shared__ EntryF sm[kChunkB];
-  __shared__ __align__(16) float2 spp[kChunkB][kPP];
+  __shared__ __align__(16) float spp[kChunkB][kPP];  // per-entry constants (broadcast operands of the packed ops)
   // per-warp entry totals for the CTA's fixed-order sum (deterministic mode: kW == 4 only)
   __shared__ float red[kW == 4 ? kChunkB : 1][kW][kGradStride];
   // warp-reduction scratch in dynamic shared memory (static + this exceed the 48 KB static limit)
@@ -2161,18 +2161,18 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
     for (int j = threadIdx.x; j < cn; j += kThreads) {
       EntryF &e = sm[j];
       stage_entry_f<kRot>(sc, c, entries[base + j], e, vrange);
-      float2 *pp = spp[j];
+      float *pp = spp[j];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) pp[m] = f2(e.p.ws[m]);
+      for (int m = 0; m < 4; ++m) pp[m] = e.p.ws[m];
 #pragma unroll
-      for (int m = 0; m < 9; ++m) pp[4 + m] = f2(e.p.wc[m]);
+      for (int m = 0; m < 9; ++m) pp[4 + m] = e.p.wc[m];
 #pragma unroll
-      for (int m = 0; m < 12; ++m) pp[13 + m] = f2(e.p.wsh[m]);
+      for (int m = 0; m < 12; ++m) pp[13 + m] = e.p.wsh[m];
       const float ha = 0.5f * e.a;
-      pp[25] = f2(e.a);
-      pp[26] = f2(e.inv_b);
-      pp[27] = f2(ha);
-      pp[28] = f2(ha * e.inv_b);
+      pp[25] = e.a;
+      pp[26] = e.inv_b;
+      pp[27] = ha;
+      pp[28] = ha * e.inv_b;
     }
     __syncthreads();
     prefetch_voxel(sc, pf);
