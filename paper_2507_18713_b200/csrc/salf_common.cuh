@@ -220,8 +220,7 @@ __device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3],
     z = __fmaf_rn(p.wsh[11], gam[3], z);
     c[2] = fast_rcp(1.0f + fast_exp(-z));
   }
-  return;
-#endif
+#else
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     float z = __fmaf_rn(p.wc[3 * i + 2], x[2], __fmaf_rn(p.wc[3 * i + 1], x[1], p.wc[3 * i] * x[0]));
@@ -231,6 +230,7 @@ __device__ __forceinline__ void eval_color32g(const VoxPrm &p, const float x[3],
     z = __fmaf_rn(p.wsh[4 * i + 3], gam[3], z);
     c[i] = fast_rcp(1.0f + fast_exp(-z));
   }
+#endif
 }
 
 // (N,3) @ (3,3) as NumPy/OpenBLAS computes it on x86: fma(a2, b2, fma(a1, b1, a0*b0)).

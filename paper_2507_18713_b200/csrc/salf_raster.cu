@@ -947,11 +947,31 @@ __device__ __forceinline__ float chord_err(const float inv[3], float hf, const f
 // is fp32 (its error only moves the reference point along the ray).  No fp64
 // and no fp64<->fp32 conversion per pair.  Rays with a zero direction
 // component use the fp64 reference slab test (octree.py:184-194).
+#ifndef SALF_PAIR_PACK
+#define SALF_PAIR_PACK 1  // forward pair test: x and y slabs in fp32x2
+#endif
 __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float q[3], float &u0, float &u1,
                                            float &ts) {
   if (r.fast) {
     ts = -__fmaf_rn(e.oh[2], r.df[2], __fmaf_rn(e.oh[1], r.df[1], e.oh[0] * r.df[0]));
     // slab k: u in [(-s h - q) / d, (s h - q) / d], s = sign(d): h |1/d| -/+ q/d
+#if SALF_PAIR_PACK
+    // axes x and y as fp32x2 (each half the scalar chain's IEEE operations), z scalar
+    const float2 tt = make_float2(ts, ts);
+    const float2 q01 = __fadd2_rn(__ffma2_rn(tt, make_float2(r.df[0], r.df[1]), make_float2(e.oh[0], e.oh[1])),
+                                  __ffma2_rn(tt, make_float2(r.dl[0], r.dl[1]), make_float2(e.ol[0], e.ol[1])));
+    q[0] = q01.x;
+    q[1] = q01.y;
+    q[2] = __fmaf_rn(ts, r.df[2], e.oh[2]) + __fmaf_rn(ts, r.dl[2], e.ol[2]);
+    const float2 nqi01 = __fmul2_rn(q01, make_float2(-r.inv[0], -r.inv[1]));  // -q/d (exact negation)
+    const float2 ai01 = make_float2(fabsf(r.inv[0]), fabsf(r.inv[1]));
+    const float2 n01 = __ffma2_rn(make_float2(-e.hf, -e.hf), ai01, nqi01);
+    const float2 f01 = __ffma2_rn(make_float2(e.hf, e.hf), ai01, nqi01);
+    const float qi2 = q[2] * r.inv[2];
+    const float n2 = __fmaf_rn(-e.hf, fabsf(r.inv[2]), -qi2), f2v = __fmaf_rn(e.hf, fabsf(r.inv[2]), -qi2);
+    const float un = fmaxf(fmaxf(fmaxf(-INFINITY, n01.x), n01.y), n2);
+    const float uf = fminf(fminf(fminf(INFINITY, f01.x), f01.y), f2v);
+#else
     float un = -INFINITY, uf = INFINITY;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -960,6 +980,7 @@ __device__ __forceinline__ bool pair_hit_f(const RayF &r, const EntryF &e, float
       un = fmaxf(un, __fmaf_rn(-e.hf, fabsf(r.inv[k]), -qi));
       uf = fminf(uf, __fmaf_rn(e.hf, fabsf(r.inv[k]), -qi));
     }
+#endif
     u0 = fmaxf(un, r.tn0f - ts);
     u1 = uf;
     return u1 > u0;
@@ -1524,8 +1545,19 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
         }
         hb |= 1u << jj;
         float x[3];
+#if SALF_PAIR_PACK
+        {
+          const float2 x01 = __fmul2_rn(__ffma2_rn(make_float2(um, um), make_float2(ray->df[0], ray->df[1]),
+                                                   make_float2(qv[0], qv[1])),
+                                        make_float2(e.inv_hf, e.inv_hf));
+          x[0] = x01.x;
+          x[1] = x01.y;
+          x[2] = __fmaf_rn(um, ray->df[2], qv[2]) * e.inv_hf;
+        }
+#else
 #pragma unroll
         for (int k = 0; k < 3; ++k) x[k] = __fmaf_rn(um, ray->df[k], qv[k]) * e.inv_hf;
+#endif
         const VoxPrm &p = e.p;
         const float s = __fmaf_rn(p.ws[2], x[2], __fmaf_rn(p.ws[1], x[1], __fmaf_rn(p.ws[0], x[0], p.ws[3])));
         const float ds_abs = e.wn * (__fmaf_rn(pdd0, e.inv_hf, pdd) + 10.f * kU24);
@@ -1544,8 +1576,17 @@ __global__ void __launch_bounds__(256, SALF_FWDF_MINB) k_composite_fast(salf_sce
         float col[3];
         eval_color32g(p, x, ray->gam, col);
         const float w = T * alpha;
+#if SALF_PAIR_PACK
+        {
+          const float2 a01 = __ffma2_rn(make_float2(w, w), make_float2(col[0], col[1]), make_float2(acc_c[0], acc_c[1]));
+          acc_c[0] = a01.x;
+          acc_c[1] = a01.y;
+          acc_c[2] = __fmaf_rn(w, col[2], acc_c[2]);
+        }
+#else
 #pragma unroll
         for (int k = 0; k < 3; ++k) acc_c[k] = __fmaf_rn(w, col[k], acc_c[k]);
+#endif
         acc_w += w;
         acc_wt = __fmaf_rn(w, ts + um, acc_wt);
         EY += __fmaf_rn(y, rel + 2.f * kU24, 2.f * sigma * dd);
