@@ -1724,7 +1724,7 @@ __global__ void __launch_bounds__(128) k_composite_redo(salf_scene_t sc, Pinhole
 #define SALF_BWD_NP 2  // pixels per thread
 #endif
 #ifndef SALF_BWDF_MINB
-#define SALF_BWDF_MINB 4  // resident CTAs per SM the register budget is sized for
+#define SALF_BWDF_MINB 5  // resident 4-warp CTAs per SM the register budget is sized for (2-warp CTAs: twice as many)
 #endif
 
 template <bool kRot, int NP, bool sdf, bool kDepth = true>
@@ -2028,6 +2028,29 @@ __device__ __forceinline__ bool pair64_into(const salf_scene_t &sc, const EntryF
   return true;
 }
 
+// Staged geometry of a hit-word backward entry (the field constants live in spp).
+struct EntryG {
+  double o[3], half;
+  float hf, inv_hf;
+  int vid, rot;
+};
+__device__ __forceinline__ EntryF entry_f(const EntryG &g) {
+  EntryF e;  // the fields bwd_pair reads
+#pragma unroll
+  for (int m = 0; m < 3; ++m) e.o[m] = g.o[m];
+  e.half = g.half;
+  e.hf = g.hf;
+  e.inv_hf = g.inv_hf;
+  e.vid = g.vid;
+  e.rot = g.rot;
+  return e;
+}
+
+#ifndef SALF_BWD_RAYSMEM
+#define SALF_BWD_RAYSMEM 1  // the pixels' fp64 direction and near plane in shared memory (not registers)
+#endif
+constexpr int kIvRow = SALF_BWD_RAYSMEM ? 7 : 3;  // doubles per pixel row of s_iv: 1/d (+ d, t_near0)
+
 #ifndef SALF_BWD_PAIR2
 #define SALF_BWD_PAIR2 1  // both pixels' fp64 chords as one straight-line block (0: one divergent pass per pixel)
 #endif
@@ -2038,7 +2061,7 @@ __device__ __forceinline__ bool pair64_into(const salf_scene_t &sc, const EntryF
 // has each pixel hit -- nearly always).  Rotated voxels and rays with a zero
 // component take bwd_pair per pixel.
 template <bool kRot, bool kDepth>
-__device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF &e, const BwdPix bp[2],
+__device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryG &e, const BwdPix bp[2],
                                             const double *__restrict__ iv0, const double *__restrict__ iv1, bool h0,
                                             bool h1, Hit2 &h) {
   const bool gen0 = h0 && ((kRot && e.rot) || !bp[0].r.fast), gen1 = h1 && ((kRot && e.rot) || !bp[1].r.fast);
@@ -2050,9 +2073,15 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
     float qf[2][3];
 #pragma unroll
     for (int l = 0; l < 2; ++l) {
+#if SALF_BWD_RAYSMEM
+      const double *d = ivp[l] + 3;  // d[0..2], tn0 follow 1/d in the pixel's shared-memory row
+      ts[l] = -fma(e.o[2], d[2], fma(e.o[1], d[1], e.o[0] * d[0]));
+      u0[l] = d[3] - ts[l];
+#else
       const RayF &r = bp[l].r;
       ts[l] = -fma(e.o[2], r.d[2], fma(e.o[1], r.d[1], e.o[0] * r.d[0]));
       u0[l] = r.tn0 - ts[l];
+#endif
     }
     // plain compare-selects: every value here is finite (fast rays), so fmax / fmin's NaN
     // handling (several extra instructions per call on sm_100) is not needed
@@ -2060,7 +2089,11 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
     for (int k = 0; k < 3; ++k) {
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
+#if SALF_BWD_RAYSMEM
+        const double qk = fma(ts[l], ivp[l][3 + k], e.o[k]);
+#else
         const double qk = fma(ts[l], bp[l].r.d[k], e.o[k]);
+#endif
         const double ik = ivp[l][k];
         const double hk = e.half * fabs(ik);
         const double n = fma(-qk, ik, -hk), f = fma(-qk, ik, hk);
@@ -2091,8 +2124,24 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
     }
     act = ok0 || ok1;
   }
-  if (gen0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], iv0, h, 0);
-  if (gen1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], iv1, h, 1);
+#if SALF_BWD_RAYSMEM
+  // the general path reads the fp64 ray from its shared-memory row
+  if (gen0 || gen1) {
+    const double *ivq[2] = {iv0, iv1};
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      if (!(l ? gen1 : gen0)) continue;
+      BwdPix b = bp[l];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) b.r.d[k] = ivq[l][3 + k];
+      b.r.tn0 = ivq[l][6];
+      act |= pair64_into<kRot, kDepth>(sc, entry_f(e), b, ivq[l], h, l);
+    }
+  }
+#else
+  if (gen0) act |= pair64_into<kRot, kDepth>(sc, entry_f(e), bp[0], iv0, h, 0);
+  if (gen1) act |= pair64_into<kRot, kDepth>(sc, entry_f(e), bp[1], iv1, h, 1);
+#endif
   return act;
 }
 
@@ -2106,7 +2155,7 @@ __device__ __forceinline__ bool pair64_both(const salf_scene_t &sc, const EntryF
 // that meet at each chunk barrier are 2, not 4: less time lost to the
 // slowest warp of the chunk, for twice the staging work.
 template <bool kRot, bool sdf, bool kDepth, int kW>
-__global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_hits(
+__global__ void __launch_bounds__(32 * kW, (kRot ? 4 : SALF_BWDF_MINB) * 4 / kW) k_backward_hits(
     salf_scene_t sc, PinholeDev c, salf_raster_opts_t opt, const int64_t *__restrict__ offsets,
     const int32_t *__restrict__ entries, const double *__restrict__ saved, const double *__restrict__ d_rgb,
     const double *__restrict__ d_depth, double *__restrict__ grad, float *__restrict__ partial,
@@ -2115,14 +2164,14 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
   static_assert(kChunkB == 32, "hit words: one 32-entry word per staged chunk");
   static_assert(kW == 2 || kW == 4, "a CTA covers a whole tile or half of one");
   constexpr int kParts = 4 / kW, kThreads = 32 * kW;
-  __shared__ EntryF sm[kChunkB];
+  __shared__ EntryG sm[kChunkB];
   __shared__ __align__(16) float spp[kChunkB][kPP];  // per-entry constants (broadcast operands of the packed ops)
   // per-warp entry totals for the CTA's fixed-order sum (deterministic mode: kW == 4 only)
   __shared__ float red[kW == 4 ? kChunkB : 1][kW][kGradStride];
   // warp-reduction scratch in dynamic shared memory (static + this exceed the 48 KB static limit)
   extern __shared__ __align__(16) float xp_dyn[];
   float(*xp)[kXpRows][kXpCols] = reinterpret_cast<float(*)[kXpRows][kXpCols]>(xp_dyn);
-  __shared__ double s_iv[2 * kThreads * 3];  // per pixel slot of this CTA: fp64 1/d (bwd_pair64)
+  __shared__ double s_iv[2 * kThreads * kIvRow];  // per pixel of this CTA: fp64 1/d (+ d, t_near0)
   __shared__ uint32_t s_wm[kW];     // per warp: entries of the chunk it includes
   __shared__ int s_max;
   const int tslot = (int)blockIdx.x / kParts, part = (int)blockIdx.x % kParts;
@@ -2160,7 +2209,12 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
     if (in[k]) {
       bwd_pixel_init(c, opt, px, py, saved, d_rgb, d_depth, bp[k]);
 #pragma unroll
-      for (int a = 0; a < 3; ++a) s_iv[ivrow[k] * 3 + a] = 1.0 / bp[k].r.d[a];
+      for (int a = 0; a < 3; ++a) s_iv[ivrow[k] * kIvRow + a] = 1.0 / bp[k].r.d[a];
+#if SALF_BWD_RAYSMEM
+#pragma unroll
+      for (int a = 0; a < 3; ++a) s_iv[ivrow[k] * kIvRow + 3 + a] = bp[k].r.d[a];
+      s_iv[ivrow[k] * kIvRow + 6] = bp[k].r.tn0;
+#endif
     } else {
       // idle slot (outside the image): finite state, never hit (n_stop 0); its lane of the
       // packed chain must stay finite (0 * NaN would poison the warp sums)
@@ -2200,8 +2254,16 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
     __syncthreads();
     const int32_t pf = prefetch_index(entries, base - kChunkB, beg, lim, kChunkB);
     for (int j = threadIdx.x; j < cn; j += kThreads) {
-      EntryF &e = sm[j];
-      stage_entry_f<kRot>(sc, c, entries[base + j], e, vrange);
+      EntryF e;
+      stage_entry_f<kRot>(sc, c, entries[base + j], e, nullptr);
+      EntryG &eg = sm[j];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) eg.o[m] = e.o[m];
+      eg.half = e.half;
+      eg.hf = e.hf;
+      eg.inv_hf = e.inv_hf;
+      eg.vid = e.vid;
+      eg.rot = e.rot;
       float *pp = spp[j];
 #pragma unroll
       for (int m = 0; m < 4; ++m) pp[m] = e.p.ws[m];
@@ -2228,17 +2290,17 @@ __global__ void __launch_bounds__(32 * kW, SALF_BWDF_MINB * 4 / kW) k_backward_h
     for (uint32_t m = wmask; m; m &= ~(1u << (31 - __clz(m)))) {
       const int j = 31 - __clz(m);
       const bool h0 = (wb0 >> j) & 1u, h1 = (wb1 >> j) & 1u;
-      const EntryF &e = sm[j];
+      const EntryG &e = sm[j];
       Hit2 hh;
       hh.x[0] = hh.x[1] = hh.x[2] = f2(0.f);
       hh.delta = hh.dq = f2(0.f);
       if (kRot) hh.gm[0] = hh.gm[1] = hh.gm[2] = hh.gm[3] = f2(0.f);
       bool act = false;
 #if SALF_BWD_PAIR2
-      act = pair64_both<kRot, kDepth>(sc, e, bp, s_iv + ivrow[0] * 3, s_iv + ivrow[1] * 3, h0, h1, hh);
+      act = pair64_both<kRot, kDepth>(sc, e, bp, s_iv + ivrow[0] * kIvRow, s_iv + ivrow[1] * kIvRow, h0, h1, hh);
 #else
-      if (h0) act |= pair64_into<kRot, kDepth>(sc, e, bp[0], s_iv + ivrow[0] * 3, hh, 0);
-      if (h1) act |= pair64_into<kRot, kDepth>(sc, e, bp[1], s_iv + ivrow[1] * 3, hh, 1);
+      if (h0) act |= pair64_into<kRot, kDepth>(sc, entry_f(e), bp[0], s_iv + ivrow[0] * kIvRow, hh, 0);
+      if (h1) act |= pair64_into<kRot, kDepth>(sc, entry_f(e), bp[1], s_iv + ivrow[1] * kIvRow, hh, 1);
 #endif
       float tot = 0.0f;
       if (__any_sync(0xffffffffu, act)) {
