@@ -307,10 +307,14 @@ __global__ void k_emit(const int64_t *__restrict__ nums, const int32_t *__restri
     const int nx = s.z - s.x + 1;
     const int cnt = nx * (s.w - s.y + 1);
     const int64_t b = base_r[r];
-    if (b + cnt > cap) continue;
+    // past the capacity: write the part that fits, so every slot below the capacity holds a real
+    // (tile, voxel) instance -- the truncated lists are composited (then re-binned) and must only
+    // name real voxels
+    if (b >= cap) continue;
+    const int lim = (int)min((int64_t)cnt, cap - b);
     int ty = s.y + lane / nx, tx = s.x + lane % nx;
     const int dy = kEmitLanes / nx, dx = kEmitLanes % nx;
-    for (int k = lane; k < cnt; k += kEmitLanes) {
+    for (int k = lane; k < lim; k += kEmitLanes) {
       keys[b + k] = (uint32_t)(ty * tiles_x + tx);
       vals[b + k] = v;
       tx += dx;  // advance by kEmitLanes instances in row-major order

@@ -158,3 +158,38 @@ def test_rasterize_regrows_capacity():
             RR._CAPACITY.pop(key, None)
         else:
             RR._CAPACITY[key] = saved
+
+
+def test_truncated_binning_names_only_real_voxels():
+    """A capacity below the frame's instance count: every slot below the
+    capacity holds a real (tile, voxel) instance, including the slots of the
+    voxel whose range straddles the capacity (those lists are composited
+    before the re-bin; a skipped partial range left stale slots behind)."""
+    from conftest import load_golden_scene
+    from paper_2507_18713_b200 import _lib, render_raster as RR
+    from paper_2507_18713_b200.device import DeviceScene
+    from paper_2507_18713_b200.scene import flatten_scene
+    from paper_2507_18713_b200.sensors import CameraModel, look_at_quaternion
+    lib = _lib.load()
+    ds = DeviceScene.from_scene(load_golden_scene("rand400"))
+    pos = np.array([13.0, 11.0, 7.0])
+    cam = CameraModel(kind="pinhole", width=96, height=80, fx=90.0, fy=90.0, cx=48.0, cy=40.0,
+                      position=pos, quaternion=look_at_quaternion(pos, [4.0, 4.0, 2.0]))
+    p = RR._project(ds, cam, RR.NEAR_PLANE, RR.TILE_SIZE)
+    n_full = RR._bin_sync(ds, cam, RR.NEAR_PLANE, RR.TILE_SIZE, p, 1)[2]
+    n_tiles = (-(-cam.width // 16)) * (-(-cam.height // 16))
+    for cap in (1, 37, n_full // 2 + 3, n_full - 1):
+        offsets = torch.full((n_tiles + 1,), -7, dtype=torch.int64, device="cuda")
+        entries = torch.full((cap,), -123456, dtype=torch.int32, device="cuda")
+        counts = torch.empty(2, dtype=torch.int64, device="cuda")
+        wsb = lib.salf_raster_bin_workspace_bytes(ds.n, cap, n_tiles)
+        ws = torch.full((wsb,), 0xA5, dtype=torch.uint8, device="cuda")  # stale workspace bytes
+        sc, cs = ds.c_struct(), cam.c_struct(rolling=False)
+        _lib.check(lib.salf_raster_bin(_lib.ref(sc), _lib.ref(cs), float(RR.NEAR_PLANE), 16, 1,
+                                       p["zkey"].data_ptr(), p["span_fit"].data_ptr(), None, ws.data_ptr(), wsb, cap,
+                                       offsets.data_ptr(), entries.data_ptr(), counts.data_ptr(),
+                                       _lib.stream_ptr()), "bin")
+        e, off = entries.cpu().numpy(), offsets.cpu().numpy()
+        assert int(counts[1]) == n_full
+        assert off[0] == 0 and off[-1] == cap and np.all(np.diff(off) >= 0)
+        assert e.min() >= 0 and e.max() < ds.n, (cap, e.min(), e.max())
